@@ -1,0 +1,210 @@
+/*
+ * shardweave_b200 — C ABI of the B200-native tensor-parallel transformer step.
+ *
+ * This is the drop-in boundary for the hot path of the reference ("shardweave", the C++
+ * restatement of Redco, arXiv 2310.16355). Every entry point is extern "C", noexcept, takes
+ * plain pointers and sizes, and returns an sw_status; sw_last_error() holds the message.
+ * Each declaration cites the reference interface it replaces (paths under
+ * /root/reference/proj/).
+ *
+ * Conventions
+ *   - Parameter shapes travel as (names[n], ranks[n], dims_flat[sum(ranks)]).
+ *   - Kernels are stored [out_features, in_features] exactly as the reference
+ *     (graph.hpp:353-375); partitions are "replicated" or "split:<dim>" (partition.hpp:11-39).
+ *   - Strings returned as `char**` are malloc'd; release them with sw_free().
+ *   - Token ids / labels are int32 (the reference stores them as float and rounds them with
+ *     llround, kernels.hpp:21-26).
+ *   - `stream` arguments are cudaStream_t passed as void* (NULL = legacy default stream).
+ */
+#ifndef SHARDWEAVE_B200_H_
+#define SHARDWEAVE_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define SW_API __attribute__((visibility("default")))
+#else
+#define SW_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes mirror the reference's exception classes:
+ * ShapeError/NonFiniteError (tensor.hpp:37-45), ConfigError/PartitionError/CheckpointError
+ * (errors.hpp:10-35), AutodiffError (autodiff.hpp:15-18). */
+typedef enum sw_status {
+  SW_OK = 0,
+  SW_ERR_SHAPE = 1,
+  SW_ERR_PARTITION = 2,
+  SW_ERR_CONFIG = 3,
+  SW_ERR_NONFINITE = 4,
+  SW_ERR_CHECKPOINT = 5,
+  SW_ERR_AUTODIFF = 6,
+  SW_ERR_CUDA = 7,
+  SW_ERR_NCCL = 8,
+  SW_ERR_INTERNAL = 9
+} sw_status;
+
+/* Thread-local message of the last failing call on this thread. */
+SW_API const char* sw_last_error(void);
+SW_API const char* sw_version(void);
+SW_API void sw_free(void* p);
+
+/* ============================================================================================
+ * Rule engine (host, bit-exact with the reference)
+ * ========================================================================================== */
+
+typedef struct sw_model_spec sw_model_spec;
+typedef struct sw_plan sw_plan;
+
+/* Replaces parse_model_spec (model_spec.hpp:30-34, model_spec.cpp:44-119). */
+SW_API sw_status sw_model_spec_parse(const char* text, sw_model_spec** out);
+/* out[7] = {vocab_size, n_layers, d_model, n_heads, d_ff, max_seq_len, tie_embeddings} */
+SW_API sw_status sw_model_spec_dims(const sw_model_spec* spec, int64_t out[7]);
+/* Role overrides of the spec as "pattern\trole\n" lines. */
+SW_API sw_status sw_model_spec_overrides(const sw_model_spec* spec, char** text_out);
+SW_API void sw_model_spec_free(sw_model_spec* spec);
+
+/* Replaces transformer_param_shapes (model.hpp:17-43): "name\td0,d1\n" in tree order. */
+SW_API sw_status sw_transformer_param_shapes(const sw_model_spec* spec, char** text_out);
+
+/* Replaces infer_roles (roles.hpp:58-64, roles.cpp:150-189). Output lines
+ * "name\trole\tsequence_index\n"; warnings joined by '\n'. */
+SW_API sw_status sw_infer_roles(const char* const* names, const int32_t* ranks, const int64_t* dims,
+                         size_t n, const char* const* override_patterns,
+                         const char* const* override_roles, size_t n_overrides, char** roles_out,
+                         char** warnings_out);
+
+/* Replaces derive_plan(ParamTree, n_shards, overrides) (plan.hpp:35-47, plan.cpp:39-91),
+ * including role-inference warnings folded in front (plan.hpp:40-47). */
+SW_API sw_status sw_plan_derive(const char* const* names, const int32_t* ranks, const int64_t* dims,
+                         size_t n, const char* const* override_patterns,
+                         const char* const* override_roles, size_t n_overrides, int n_shards,
+                         sw_plan** out);
+/* Replaces parse_plan (plan.cpp:196-239). */
+SW_API sw_status sw_plan_parse(const char* text, int n_shards, sw_plan** out);
+/* Replaces serialize_plan (plan.cpp:181-194). */
+SW_API sw_status sw_plan_serialize(const sw_plan* plan, char** text_out);
+/* Replaces validate_plan (plan.cpp:93-179): violations joined by '\n' (empty = valid). */
+SW_API sw_status sw_plan_validate(const sw_plan* plan, const char* const* names, const int32_t* ranks,
+                           const int64_t* dims, size_t n, char** violations_out);
+SW_API sw_status sw_plan_warnings(const sw_plan* plan, char** text_out);
+SW_API sw_status sw_plan_size(const sw_plan* plan, size_t* n_entries, int* n_shards);
+/* kind: 0 replicated, 1 split (dim valid). */
+SW_API sw_status sw_plan_entry(const sw_plan* plan, size_t i, const char** name, int* kind, int64_t* dim);
+SW_API void sw_plan_free(sw_plan* plan);
+
+/* Shard index map (sharded_tensor.hpp:14-36, :52-74): the local shape of `rank` and the
+ * [begin, end) range it owns along the split dim (0..size for replicated). */
+SW_API sw_status sw_shard_range(const int64_t* global_dims, int32_t rank_of_tensor, int kind,
+                         int64_t dim, int n_shards, int shard_rank, int64_t* local_dims_out,
+                         int64_t* begin_out, int64_t* end_out);
+
+/* expected_state_elements (train_state.hpp:236-245). */
+SW_API sw_status sw_expected_state_elements(const sw_plan* plan, const char* const* names,
+                                     const int32_t* ranks, const int64_t* dims, size_t n,
+                                     int mp_size, int64_t* out);
+
+/* ============================================================================================
+ * Mesh and collectives
+ * ========================================================================================== */
+
+typedef struct sw_mesh sw_mesh;
+
+/* NCCL unique id (128 bytes) for sw_mesh_create; rank 0 creates it and broadcasts it. */
+SW_API sw_status sw_nccl_unique_id(uint8_t out[128]);
+
+/* Replaces build_mesh (mesh.hpp:47-52, mesh.cpp:27-57). device_id = dp_index*mp + mp_index.
+ *   world == 1 : every device of the dp x mp mesh lives in this process on `cuda_device`
+ *                (collectives are device kernels summing in ascending rank order, like
+ *                collectives.hpp:27-52) — the single-GPU emulation of the mesh;
+ *   world == dp*mp : one device per process; `rank` is this process's device id and
+ *                collectives run on NCCL communicators split per mp group / dp group. */
+SW_API sw_status sw_mesh_create(int dp, int mp, int n_hosts, int rank, int world,
+                         const uint8_t* nccl_id, int cuda_device, sw_mesh** out);
+/* CommReport::to_csv (mesh.cpp:128-138) of everything this mesh communicated. */
+SW_API sw_status sw_mesh_comm_report(const sw_mesh* mesh, char** csv_out);
+SW_API sw_status sw_mesh_reset_comm_report(sw_mesh* mesh);
+SW_API void sw_mesh_free(sw_mesh* mesh);
+
+/* ============================================================================================
+ * Model program + train state (spmd_forward_backward / TrainState / adamw_step)
+ * ========================================================================================== */
+
+typedef struct sw_model sw_model;
+
+/* AdamWConfig (train_state.hpp:172-178). */
+typedef struct sw_adamw_cfg {
+  double lr;
+  double beta1;
+  double beta2;
+  double eps;
+  double weight_decay;
+} sw_adamw_cfg;
+
+/* Lowers transformer_loss(spec, batch, seq_len) (model.hpp:144-152) onto the mesh with the
+ * plan: shard materialiser layout (train_state.hpp:50-74), device buffers, kernel schedule.
+ * `batch` is the per-replica batch (rows of each dp slice, spmd.hpp:751-769). */
+SW_API sw_status sw_model_create(const sw_model_spec* spec, const sw_plan* plan, sw_mesh* mesh,
+                          int batch, int seq_len, sw_model** out);
+SW_API void sw_model_free(sw_model* model);
+
+/* init_transformer_params(spec, RngStream(seed, stream_name)) (model.hpp:49-70), generated
+ * on the device from the same counter-based splitmix64 stream (rng.hpp:15-91). */
+SW_API sw_status sw_model_init_params(sw_model* model, uint64_t seed, const char* stream_name);
+/* Materialise one full host tensor (fp32, row-major) onto this process's shards. */
+SW_API sw_status sw_model_set_param(sw_model* model, const char* name, const float* full, int64_t numel);
+/* gather (sharded_tensor.hpp:78-98) of replica 0's shards of a parameter / its gradient /
+ * its AdamW moments (which: 0 param, 1 grad, 2 adam_m, 3 adam_v) into a full host tensor. */
+SW_API sw_status sw_model_get_tensor(sw_model* model, const char* name, int which, float* full_out,
+                              int64_t numel);
+
+/* Copies one global batch (dp*batch rows of seq_len) from host memory to the devices.
+ * weights may be NULL (all ones). */
+SW_API sw_status sw_model_stage_batch(sw_model* model, const int32_t* tokens, const int32_t* targets,
+                               const float* weights);
+/* spmd_forward_backward for every replica (spmd.hpp:782-814) on the staged batch; gradients
+ * are written (accumulate = 0) or added (accumulate = 1) into the grad buffers. */
+SW_API sw_status sw_model_forward_backward(sw_model* model, int accumulate);
+/* scale_grads (train_state.hpp:146-150). */
+SW_API sw_status sw_model_scale_grads(sw_model* model, double factor);
+/* dp_sync_grads (train_state.hpp:155-170). */
+SW_API sw_status sw_model_dp_sync(sw_model* model);
+/* adamw_step (train_state.hpp:183-220); check_finite mirrors its NonFiniteError check. */
+SW_API sw_status sw_model_adamw_step(sw_model* model, const sw_adamw_cfg* cfg, int check_finite);
+/* One optimizer step of Trainer::fit (pipeline.hpp:388-449) with accumulate_grad_batches=1:
+ * forward_backward + dp_sync + adamw. */
+SW_API sw_status sw_model_train_step(sw_model* model, const sw_adamw_cfg* cfg);
+/* Mean over replicas of the last forward's weighted-mean loss (pipeline.hpp:425-426).
+ * Synchronises the device. */
+SW_API sw_status sw_model_last_loss(sw_model* model, double* loss_out);
+/* Logits [dp*batch, seq_len, vocab] of the staged batch (transformer_logits, model.hpp:76-139). */
+SW_API sw_status sw_model_forward_logits(sw_model* model, float* logits_out);
+/* Device stream used by this process's first local device (cudaStream_t as void*). */
+SW_API sw_status sw_model_stream(sw_model* model, void** stream_out);
+/* Number of kernel launches issued by the last forward_backward/adamw/train_step call. */
+SW_API sw_status sw_model_launch_count(sw_model* model, int64_t* out);
+/* Bytes of device memory held by this process's model state and activations. */
+SW_API sw_status sw_model_device_bytes(sw_model* model, int64_t* out);
+
+/* ============================================================================================
+ * Kernel-level entry points (device pointers). Used by the parity tests and the roofline
+ * measurements; each is one launch on `stream`.
+ * ========================================================================================== */
+
+/* C[M,N] = sum_k A[m,k] B[n,k] — bf16 in, fp32 accumulate (tcgen05). a_mn_major / b_mn_major
+ * select the operand layouts; epi: 0 bf16, 1 f32 (+accumulate), 2 bias+gelu (C=pre, C2=act),
+ * 3 residual f32 (C = aux + acc + bias), 4 gelu-backward (C = acc * gelu'(aux)). */
+SW_API sw_status sw_k_gemm_bf16(int M, int N, int K, const void* A, int64_t lda, int a_mn_major,
+                         const void* B, int64_t ldb, int b_mn_major, int epi, void* C, int64_t ldc,
+                         void* C2, int64_t ldc2, const float* bias, const void* aux,
+                         int64_t ld_aux, float alpha, int accumulate, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SHARDWEAVE_B200_H_ */

@@ -1,0 +1,51 @@
+// Host-side interface of the tcgen05 GEMM family.
+//
+// Logical product: C[M, N] = sum_k A[m, k] * B[n, k]   (bf16 operands, fp32 accumulation in TMEM)
+//
+// Each operand is either K-major (row r at ptr + r*ld, k contiguous) or MN-major
+// (k-th row at ptr + k*ld, m/n contiguous). With weights stored [out, in] (graph.hpp:353-375)
+// the three linear-layer products are
+//   forward   y  = x . W^T   : A = x  (K-major),  B = W   (K-major)
+//   dgrad     dx = dy . W    : A = dy (K-major),  B = W   (MN-major)
+//   wgrad     dW = dy^T . x  : A = dy (MN-major), B = x   (MN-major)
+// so no operand is ever transposed in memory.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace sw {
+
+enum class Epi : int {
+  kStoreBf16 = 0,   // C(bf16) = alpha*acc (+ bias)
+  kStoreF32 = 1,    // C(f32)  = alpha*acc (+ bias) (+ C if accumulate)
+  kBiasGelu = 2,    // C(bf16) = acc + bias (pre-activation), C2(bf16) = gelu(acc + bias)
+  kResidF32 = 3,    // C(f32)  = aux(f32) + acc + bias     (residual stream update; C may alias aux)
+  kGeluBwd = 4,     // C(bf16) = acc * gelu'(aux(bf16))    (fc2 dgrad fused with GeLU backward)
+};
+
+struct GemmParams {
+  int M = 0, N = 0, K = 0;
+  const void* A = nullptr;
+  int64_t lda = 0;
+  int a_mn_major = 0;
+  const void* B = nullptr;
+  int64_t ldb = 0;
+  int b_mn_major = 0;
+  Epi epi = Epi::kStoreBf16;
+  void* C = nullptr;
+  int64_t ldc = 0;
+  void* C2 = nullptr;
+  int64_t ldc2 = 0;
+  const float* bias = nullptr;
+  const void* aux = nullptr;
+  int64_t ld_aux = 0;
+  float alpha = 1.0f;
+  int accumulate = 0;
+  int num_sms = 0;  // 0 = all
+};
+
+// Returns cudaSuccess or the launch error. Throws std::runtime_error on invalid shapes.
+cudaError_t gemm_bf16(const GemmParams& p, cudaStream_t stream);
+
+}  // namespace sw

@@ -1,0 +1,323 @@
+// Persistent, warp-specialised tcgen05 GEMM for sm_100a.
+//
+// Roles per CTA (256 threads, one CTA per SM):
+//   warp 0      : TMA producer (one elected lane) — fills a STAGES-deep smem ring
+//   warp 1      : MMA issuer (one lane) — tcgen05.mma 128x256x16 into a TMEM accumulator
+//   warp 2      : TMEM allocator (512 columns = two 128x256 fp32 accumulators)
+//   warps 4..7  : epilogue — tcgen05.ld accumulator rows, fused bias/GeLU/residual, store
+// The two TMEM accumulators let the epilogue of tile i overlap the MMAs of tile i+1.
+//
+// This is the executor for the reference's `kernels::linear` (kernels.hpp:146-161) on both
+// branches of SpmdInterpreter::linear_onto (spmd.hpp:274-340) and for the linear VJP
+// matmuls emitted by autodiff (autodiff.hpp:124-139).
+#include <stdexcept>
+#include <string>
+
+#include "gemm.h"
+#include "sm100.cuh"
+#include "tensormap.h"
+
+namespace sw {
+namespace {
+
+constexpr int BM = 128;
+constexpr int BN = 256;
+constexpr int BK = 64;
+constexpr int STAGES = 4;
+constexpr int A_STAGE = BM * BK * 2;  // 16 KiB
+constexpr int B_STAGE = BN * BK * 2;  // 32 KiB
+constexpr int STAGE_BYTES = A_STAGE + B_STAGE;
+constexpr int TMEM_COLS = 512;
+constexpr int NUM_THREADS = 256;
+constexpr int GROUP_M = 8;
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
+
+__device__ __forceinline__ void tile_coords(int t, int num_m, int num_n, int& mb, int& nb) {
+  const int per_group = GROUP_M * num_n;
+  const int g = t / per_group;
+  const int first_m = g * GROUP_M;
+  const int gsz = min(num_m - first_m, GROUP_M);
+  const int r = t - g * per_group;
+  mb = first_m + r % gsz;
+  nb = r / gsz;
+}
+
+template <Epi EPI>
+__device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int row, int col0, int ncols,
+                                               const uint32_t (&r)[32]) {
+  float v[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]) * p.alpha;
+  if (p.bias != nullptr) {
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      if (i < ncols) v[i] += __ldg(p.bias + col0 + i);
+    }
+  }
+  if constexpr (EPI == Epi::kStoreBf16 || EPI == Epi::kBiasGelu || EPI == Epi::kGeluBwd) {
+    if constexpr (EPI == Epi::kGeluBwd) {
+      const __nv_bfloat16* pre =
+          reinterpret_cast<const __nv_bfloat16*>(p.aux) + static_cast<int64_t>(row) * p.ld_aux + col0;
+#pragma unroll
+      for (int c = 0; c < 32; c += 8) {
+        if (c < ncols) {
+          uint4 raw = *reinterpret_cast<const uint4*>(pre + c);
+          const uint32_t w[4] = {raw.x, raw.y, raw.z, raw.w};
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            float2 x = dev::unpack_bf16x2(w[j]);
+            v[c + 2 * j] *= dev::gelu_tanh_grad(x.x);
+            v[c + 2 * j + 1] *= dev::gelu_tanh_grad(x.y);
+          }
+        }
+      }
+    }
+    __nv_bfloat16* out =
+        reinterpret_cast<__nv_bfloat16*>(p.C) + static_cast<int64_t>(row) * p.ldc + col0;
+#pragma unroll
+    for (int c = 0; c < 32; c += 8) {
+      if (c < ncols) {
+        uint4 w;
+        w.x = dev::pack_bf16x2(v[c + 0], v[c + 1]);
+        w.y = dev::pack_bf16x2(v[c + 2], v[c + 3]);
+        w.z = dev::pack_bf16x2(v[c + 4], v[c + 5]);
+        w.w = dev::pack_bf16x2(v[c + 6], v[c + 7]);
+        *reinterpret_cast<uint4*>(out + c) = w;
+      }
+    }
+    if constexpr (EPI == Epi::kBiasGelu) {
+      __nv_bfloat16* act =
+          reinterpret_cast<__nv_bfloat16*>(p.C2) + static_cast<int64_t>(row) * p.ldc2 + col0;
+#pragma unroll
+      for (int c = 0; c < 32; c += 8) {
+        if (c < ncols) {
+          uint4 w;
+          w.x = dev::pack_bf16x2(dev::gelu_tanh(v[c + 0]), dev::gelu_tanh(v[c + 1]));
+          w.y = dev::pack_bf16x2(dev::gelu_tanh(v[c + 2]), dev::gelu_tanh(v[c + 3]));
+          w.z = dev::pack_bf16x2(dev::gelu_tanh(v[c + 4]), dev::gelu_tanh(v[c + 5]));
+          w.w = dev::pack_bf16x2(dev::gelu_tanh(v[c + 6]), dev::gelu_tanh(v[c + 7]));
+          *reinterpret_cast<uint4*>(act + c) = w;
+        }
+      }
+    }
+  } else {
+    // fp32 outputs
+    float* out = reinterpret_cast<float*>(p.C) + static_cast<int64_t>(row) * p.ldc + col0;
+    const float* add = nullptr;
+    if constexpr (EPI == Epi::kResidF32) {
+      add = reinterpret_cast<const float*>(p.aux) + static_cast<int64_t>(row) * p.ld_aux + col0;
+    } else {
+      if (p.accumulate) add = out;
+    }
+#pragma unroll
+    for (int c = 0; c < 32; c += 4) {
+      if (c < ncols) {
+        float4 w = make_float4(v[c], v[c + 1], v[c + 2], v[c + 3]);
+        if (add != nullptr) {
+          float4 a = *reinterpret_cast<const float4*>(add + c);
+          w.x += a.x;
+          w.y += a.y;
+          w.z += a.z;
+          w.w += a.w;
+        }
+        *reinterpret_cast<float4*>(out + c) = w;
+      }
+    }
+  }
+}
+
+template <Epi EPI>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                     const GemmParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * A_STAGE;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_STAGE);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const uint32_t warp = dev::warp_idx_sync();
+  const uint32_t lane = threadIdx.x & 31;
+
+  const int num_m = (p.M + BM - 1) / BM;
+  const int num_n = (p.N + BN - 1) / BN;
+  const int num_tiles = num_m * num_n;
+  const int num_kb = (p.K + BK - 1) / BK;
+
+  if (warp == 0 && lane == 0) {
+    dev::tma_prefetch_desc(&tmA);
+    dev::tma_prefetch_desc(&tmB);
+    for (int s = 0; s < STAGES; ++s) {
+      dev::mbar_init(&full[s], 1);
+      dev::mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      dev::mbar_init(&tfull[a], 1);
+      dev::mbar_init(&tempty[a], 4);
+    }
+    dev::fence_barrier_init();
+  }
+  if (warp == 2) dev::tmem_alloc<TMEM_COLS>(tmem_slot);
+  dev::tc_fence_before();
+  __syncthreads();
+  dev::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer ----------------
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        int mb, nb;
+        tile_coords(t, num_m, num_n, mb, nb);
+        const int m0 = mb * BM, n0 = nb * BN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          dev::mbar_wait(&empty[stage], phase ^ 1);
+          dev::mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
+          const int k0 = kb * BK;
+          uint8_t* a_dst = sA + stage * A_STAGE;
+          uint8_t* b_dst = sB + stage * B_STAGE;
+          if (!p.a_mn_major) {
+            dev::tma_load_2d(a_dst, &tmA, &full[stage], k0, m0);
+          } else {
+#pragma unroll
+            for (int c = 0; c < BM / 64; ++c)
+              dev::tma_load_2d(a_dst + c * 8192, &tmA, &full[stage], m0 + c * 64, k0);
+          }
+          if (!p.b_mn_major) {
+            dev::tma_load_2d(b_dst, &tmB, &full[stage], k0, n0);
+          } else {
+#pragma unroll
+            for (int c = 0; c < BN / 64; ++c)
+              dev::tma_load_2d(b_dst + c * 8192, &tmB, &full[stage], n0 + c * 64, k0);
+          }
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------- MMA issuer ----------------
+      const uint32_t idesc = dev::make_idesc_bf16(BM, BN, p.a_mn_major, p.b_mn_major);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        dev::mbar_wait(&tempty[acc], acc_phase ^ 1);
+        dev::tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          dev::mbar_wait(&full[stage], phase);
+          dev::tc_fence_after();
+          const uint32_t a_base = dev::smem_u32(sA + stage * A_STAGE);
+          const uint32_t b_base = dev::smem_u32(sB + stage * B_STAGE);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            const uint64_t adesc =
+                p.a_mn_major ? dev::make_sdesc_sw128(a_base + k * 2048, 8192, 1024)
+                             : dev::make_sdesc_sw128(a_base + k * 32, 16, 1024);
+            const uint64_t bdesc =
+                p.b_mn_major ? dev::make_sdesc_sw128(b_base + k * 2048, 8192, 1024)
+                             : dev::make_sdesc_sw128(b_base + k * 32, 16, 1024);
+            dev::umma_f16_ss(d_tmem, adesc, bdesc, idesc, (kb | k) != 0 ? 1u : 0u);
+          }
+          dev::umma_commit(&empty[stage]);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        dev::umma_commit(&tfull[acc]);
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    // ---------------- epilogue ----------------
+    const uint32_t q = warp & 3;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      int mb, nb;
+      tile_coords(t, num_m, num_n, mb, nb);
+      const int row = mb * BM + q * 32 + lane;
+      dev::mbar_wait(&tfull[acc], acc_phase);
+      dev::tc_fence_after();
+      const int n_left = p.N - nb * BN;
+#pragma unroll 1
+      for (int j = 0; j < BN / 32; ++j) {
+        const int ncols = min(32, n_left - j * 32);
+        if (ncols <= 0) break;
+        uint32_t r[32];
+        dev::tmem_ld_32x32b_x32(tmem_base + ((q * 32) << 16) + acc * BN + j * 32, r);
+        dev::tmem_ld_wait();
+        if (row < p.M) epilogue_chunk<EPI>(p, row, nb * BN + j * 32, ncols, r);
+      }
+      dev::tc_fence_before();
+      if (lane == 0) dev::mbar_arrive(&tempty[acc]);
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+  }
+
+  __syncthreads();
+  if (warp == 2) {
+    dev::tc_fence_after();
+    dev::tmem_dealloc<TMEM_COLS>(tmem_base);
+  }
+}
+
+template <Epi EPI>
+cudaError_t launch(const GemmParams& p, cudaStream_t stream) {
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(gemm_bf16_kernel<EPI>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  CUtensorMap ta = p.a_mn_major ? make_tmap_bf16_2d(p.A, p.M, p.K, p.lda, 64, 64)
+                                : make_tmap_bf16_2d(p.A, p.K, p.M, p.lda, 64, BM);
+  CUtensorMap tb = p.b_mn_major ? make_tmap_bf16_2d(p.B, p.N, p.K, p.ldb, 64, 64)
+                                : make_tmap_bf16_2d(p.B, p.K, p.N, p.ldb, 64, BN);
+  const int num_tiles = ((p.M + BM - 1) / BM) * ((p.N + BN - 1) / BN);
+  const int sms = p.num_sms > 0 ? p.num_sms : device_sm_count();
+  const int grid = num_tiles < sms ? num_tiles : sms;
+  gemm_bf16_kernel<EPI><<<grid, NUM_THREADS, SMEM_BYTES, stream>>>(ta, tb, p);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t gemm_bf16(const GemmParams& p, cudaStream_t stream) {
+  if (p.M <= 0 || p.N <= 0 || p.K <= 0) {
+    throw std::runtime_error("gemm_bf16: empty problem M=" + std::to_string(p.M) +
+                             " N=" + std::to_string(p.N) + " K=" + std::to_string(p.K));
+  }
+  if (p.N % 8 != 0) throw std::runtime_error("gemm_bf16: N must be a multiple of 8");
+  if (p.ldc % 8 != 0) throw std::runtime_error("gemm_bf16: ldc must be a multiple of 8");
+  switch (p.epi) {
+    case Epi::kStoreBf16: return launch<Epi::kStoreBf16>(p, stream);
+    case Epi::kStoreF32: return launch<Epi::kStoreF32>(p, stream);
+    case Epi::kBiasGelu: return launch<Epi::kBiasGelu>(p, stream);
+    case Epi::kResidF32: return launch<Epi::kResidF32>(p, stream);
+    case Epi::kGeluBwd: return launch<Epi::kGeluBwd>(p, stream);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace sw

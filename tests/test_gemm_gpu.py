@@ -1,0 +1,114 @@
+"""tcgen05 GEMM family vs a plain PyTorch fp32 reference of the same op (same bf16 inputs).
+
+Covers both operand majors (forward / dgrad / wgrad layouts of a [out, in] weight), ragged M/N/K
+tails, and every fused epilogue."""
+import math
+
+import pytest
+import torch
+
+from paper_2310_16355_b200 import _lib
+
+pytestmark = pytest.mark.gpu
+
+DEV = "cuda"
+
+
+def _gemm(A, a_mn, B, b_mn, M, N, K, epi, C, C2=None, bias=None, aux=None, alpha=1.0, acc=0):
+    L = _lib.lib()
+    lda = A.stride(0)
+    ldb = B.stride(0)
+    _lib.check(L.sw_k_gemm_bf16(
+        M, N, K, A.data_ptr(), lda, a_mn, B.data_ptr(), ldb, b_mn, epi, C.data_ptr(), C.stride(0),
+        C2.data_ptr() if C2 is not None else None, C2.stride(0) if C2 is not None else 0,
+        bias.data_ptr() if bias is not None else None,
+        aux.data_ptr() if aux is not None else None, aux.stride(0) if aux is not None else 0,
+        alpha, acc, None))
+    torch.cuda.synchronize()
+
+
+def _ref_operands(M, N, K, a_mn, b_mn, gen):
+    a = torch.randn(M, K, generator=gen, device=DEV).bfloat16()
+    b = torch.randn(N, K, generator=gen, device=DEV).bfloat16()
+    A = a.t().contiguous() if a_mn else a
+    B = b.t().contiguous() if b_mn else b
+    ref = a.float() @ b.float().t()
+    return A, B, ref
+
+
+def _rel(x, y):
+    return ((x.float() - y.float()).norm() / y.float().norm().clamp_min(1e-30)).item()
+
+
+@pytest.mark.parametrize("a_mn,b_mn", [(0, 0), (0, 1), (1, 1), (1, 0)])
+@pytest.mark.parametrize("M,N,K", [(128, 256, 64), (256, 512, 256), (200, 136, 72),
+                                   (512, 1376, 512), (1000, 776, 1000)])
+def test_gemm_layouts_f32(M, N, K, a_mn, b_mn):
+    gen = torch.Generator(device=DEV).manual_seed(M * 7 + N * 3 + K + a_mn * 2 + b_mn)
+    A, B, ref = _ref_operands(M, N, K, a_mn, b_mn, gen)
+    C = torch.full((M, N), float("nan"), device=DEV)
+    _gemm(A, a_mn, B, b_mn, M, N, K, 1, C)
+    assert _rel(C, ref) < 1e-5
+
+
+@pytest.mark.parametrize("M,N,K", [(384, 768, 512), (4096, 4096, 4096)])
+def test_gemm_bf16_bias(M, N, K):
+    gen = torch.Generator(device=DEV).manual_seed(1)
+    A, B, ref = _ref_operands(M, N, K, 0, 0, gen)
+    bias = torch.randn(N, generator=gen, device=DEV)
+    C = torch.empty(M, N, device=DEV, dtype=torch.bfloat16)
+    _gemm(A, 0, B, 0, M, N, K, 0, C, bias=bias)
+    assert _rel(C, ref + bias) < 1e-2
+
+
+def test_gemm_bias_gelu():
+    M, N, K = 300, 520, 256
+    gen = torch.Generator(device=DEV).manual_seed(2)
+    A, B, ref = _ref_operands(M, N, K, 0, 0, gen)
+    bias = torch.randn(N, generator=gen, device=DEV)
+    pre = torch.empty(M, N, device=DEV, dtype=torch.bfloat16)
+    act = torch.empty(M, N, device=DEV, dtype=torch.bfloat16)
+    _gemm(A, 0, B, 0, M, N, K, 2, pre, C2=act, bias=bias)
+    x = ref + bias
+    g = 0.5 * x * (1 + torch.tanh(0.7978845608028654 * (x + 0.044715 * x ** 3)))
+    assert _rel(pre, x) < 1e-2
+    assert _rel(act, g) < 1e-2
+
+
+def test_gemm_residual_f32():
+    M, N, K = 256, 512, 384
+    gen = torch.Generator(device=DEV).manual_seed(3)
+    A, B, ref = _ref_operands(M, N, K, 0, 0, gen)
+    bias = torch.randn(N, generator=gen, device=DEV)
+    h = torch.randn(M, N, generator=gen, device=DEV)
+    want = h + ref + bias
+    _gemm(A, 0, B, 0, M, N, K, 3, h, bias=bias, aux=h)  # in place on the residual stream
+    assert _rel(h, want) < 1e-5
+
+
+def test_gemm_gelu_bwd_dgrad():
+    # d_pre = (dy . W) * gelu'(pre) with W stored [out, in] -> B operand MN-major
+    M, Nout, Kin = 256, 512, 384  # dy [M, Nout], W [Nout, Kin], result [M, Kin]
+    gen = torch.Generator(device=DEV).manual_seed(4)
+    dy = torch.randn(M, Nout, generator=gen, device=DEV).bfloat16()
+    W = torch.randn(Nout, Kin, generator=gen, device=DEV).bfloat16()
+    pre = torch.randn(M, Kin, generator=gen, device=DEV).bfloat16()
+    out = torch.empty(M, Kin, device=DEV, dtype=torch.bfloat16)
+    _gemm(dy, 0, W, 1, M, Kin, Nout, 4, out, aux=pre)
+    x = pre.float()
+    t = torch.tanh(0.7978845608028654 * (x + 0.044715 * x ** 3))
+    gp = 0.5 * (1 + t) + 0.5 * x * (1 - t * t) * 0.7978845608028654 * (1 + 3 * 0.044715 * x * x)
+    want = (dy.float() @ W.float()) * gp
+    assert _rel(out, want) < 1e-2
+
+
+def test_gemm_wgrad_accumulate():
+    # dW[N, K] += dy^T x, both operands MN-major (token dim is the reduction dim)
+    T, Nout, Kin = 640, 384, 256
+    gen = torch.Generator(device=DEV).manual_seed(5)
+    dy = torch.randn(T, Nout, generator=gen, device=DEV).bfloat16()
+    x = torch.randn(T, Kin, generator=gen, device=DEV).bfloat16()
+    dW = torch.randn(Nout, Kin, generator=gen, device=DEV)
+    want = dW + dy.float().t() @ x.float()
+    _gemm(dy, 1, x, 1, Nout, Kin, T, 1, dW, acc=1)
+    assert _rel(dW, want) < 1e-5
