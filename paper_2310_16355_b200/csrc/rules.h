@@ -1,0 +1,88 @@
+// Host rule engine: parameter-role inference, the two sharding rules, plan validation and the
+// plan text format, plus the model-spec parser and the transformer parameter tree.
+//
+// Contract: for every input, the entries, their order, warnings and error messages are
+// identical to the reference (roles.cpp, plan.cpp, model_spec.cpp, model.hpp:17-43). The
+// golden cases in tests/golden/rules.json are produced by the reference itself.
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <utility>
+#include <vector>
+
+namespace sw {
+
+using Dims = std::vector<int64_t>;
+
+struct NamedShape {
+  std::string name;
+  Dims dims;
+};
+
+enum class Role : uint8_t { kQKV, kOut, kFC, kEmbedding, kNorm, kBias, kOther };
+
+const char* role_name(Role r);
+Role parse_role(const std::string& text);  // throws Error(SW_ERR_CONFIG)
+
+struct RoleOverride {
+  std::string pattern;
+  Role role;
+};
+
+struct RoleOf {
+  std::string name;
+  Role role = Role::kOther;
+  int seq = -1;  // position among fully-connected kernels of the same block
+};
+
+struct RoleResult {
+  std::vector<RoleOf> roles;
+  std::vector<std::string> warnings;
+};
+
+RoleResult infer_roles(const std::vector<NamedShape>& shapes,
+                       const std::vector<RoleOverride>& overrides);
+
+struct Layout {
+  enum Kind : uint8_t { kReplicated = 0, kSplit = 1 };
+  Kind kind = kReplicated;
+  int64_t dim = -1;
+  bool operator==(const Layout& o) const {
+    return kind == o.kind && (kind != kSplit || dim == o.dim);
+  }
+};
+
+struct Plan {
+  int n_shards = 1;
+  std::vector<std::pair<std::string, Layout>> entries;
+  std::vector<std::string> warnings;
+  const Layout* find(const std::string& name) const;
+  const Layout& at(const std::string& name) const;  // throws Error(SW_ERR_CONFIG)
+};
+
+Plan derive_plan(const std::vector<RoleOf>& roles, const std::vector<NamedShape>& shapes,
+                 int n_shards);
+std::vector<std::string> validate_plan(const Plan& plan, const std::vector<NamedShape>& shapes);
+std::string serialize_plan(const Plan& plan);
+Plan parse_plan(const std::string& text, int n_shards);
+int64_t expected_state_elements(const Plan& plan, const std::vector<NamedShape>& shapes,
+                                int mp_size);
+
+std::string dims_str(const Dims& d);  // "[a,b]"
+
+struct ModelSpec {
+  int64_t vocab_size = 0;
+  int n_layers = 0;
+  int64_t d_model = 0;
+  int n_heads = 0;
+  int64_t d_ff = 0;
+  int64_t max_seq_len = 0;
+  bool tie_embeddings = false;
+  std::vector<RoleOverride> overrides;
+};
+
+ModelSpec parse_model_spec(const std::string& text);
+std::vector<NamedShape> transformer_param_shapes(const ModelSpec& spec);
+
+}  // namespace sw
