@@ -38,6 +38,10 @@ struct GemmParams {
   void* C2 = nullptr;
   int64_t ldc2 = 0;
   const float* bias = nullptr;
+  // Segmented bias: column n reads bias[(n / bias_seg) * bias_seg_stride + n % bias_seg]
+  // (fused QKV: three column blocks whose biases live in three separate full-width vectors).
+  int bias_seg = 0;  // 0 = plain bias[n]
+  int64_t bias_seg_stride = 0;
   const void* aux = nullptr;
   int64_t ld_aux = 0;
   float alpha = 1.0f;

@@ -49,9 +49,18 @@ __device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int row, int
 #pragma unroll
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]) * p.alpha;
   if (p.bias != nullptr) {
+    if (p.bias_seg == 0) {
 #pragma unroll
-    for (int i = 0; i < 32; ++i) {
-      if (i < ncols) v[i] += __ldg(p.bias + col0 + i);
+      for (int i = 0; i < 32; ++i) {
+        if (i < ncols) v[i] += __ldg(p.bias + col0 + i);
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const int c = col0 + i;
+        const int sg = c / p.bias_seg;
+        if (i < ncols) v[i] += __ldg(p.bias + sg * p.bias_seg_stride + (c - sg * p.bias_seg));
+      }
     }
   }
   if constexpr (EPI == Epi::kStoreBf16 || EPI == Epi::kBiasGelu || EPI == Epi::kGeluBwd) {

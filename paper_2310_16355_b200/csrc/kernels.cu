@@ -1,0 +1,668 @@
+// Non-GEMM kernels of the tensor-parallel step: embeddings, LayerNorm, bias-gradient column
+// sums, fused cross entropy, residual adds, AdamW, emulated collectives and device-side
+// parameter init. All are HBM-bound; they use 16-byte vector accesses where the row pitch
+// allows and grid-stride loops sized to the SM count.
+#include <cmath>
+#include <cstdint>
+
+#include "kernels.h"
+#include "sm100.cuh"
+
+namespace sw {
+namespace k {
+
+namespace {
+
+constexpr int kSMs = 148;
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// Sum over the block; every thread receives the total. `red` must hold 32 floats.
+__device__ __forceinline__ float block_sum(float v, float* red) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  v = warp_sum(v);
+  __syncthreads();
+  if (lane == 0) red[w] = v;
+  __syncthreads();
+  const int nw = (blockDim.x + 31) >> 5;
+  float t = lane < nw ? red[lane] : 0.f;
+  return warp_sum(t);
+}
+
+inline int grid_for(int64_t n, int threads, int per_thread = 1) {
+  int64_t g = (n + static_cast<int64_t>(threads) * per_thread - 1) / (static_cast<int64_t>(threads) * per_thread);
+  if (g > 8 * kSMs) g = 8 * kSMs;
+  if (g < 1) g = 1;
+  return static_cast<int>(g);
+}
+
+// ------------------------------------------------------------------------------------------
+// embeddings
+// ------------------------------------------------------------------------------------------
+__global__ void embed_fwd_kernel(const int32_t* __restrict__ ids, const float* __restrict__ tok,
+                                 const float* __restrict__ pos, float* __restrict__ h, int T, int d) {
+  const int64_t m = blockIdx.x;
+  const int64_t id = ids[m];
+  const int t = static_cast<int>(m % T);
+  const float* a = tok + id * d;
+  const float* b = pos + static_cast<int64_t>(t) * d;
+  float* o = h + m * d;
+  if ((d & 3) == 0) {
+    for (int i = threadIdx.x * 4; i < d; i += blockDim.x * 4) {
+      float4 x = *reinterpret_cast<const float4*>(a + i);
+      float4 y = *reinterpret_cast<const float4*>(b + i);
+      *reinterpret_cast<float4*>(o + i) = make_float4(x.x + y.x, x.y + y.y, x.z + y.z, x.w + y.w);
+    }
+  } else {
+    for (int i = threadIdx.x; i < d; i += blockDim.x) o[i] = a[i] + b[i];
+  }
+}
+
+__global__ void embed_bwd_tok_kernel(const int32_t* __restrict__ ids, const float* __restrict__ g,
+                                     float* __restrict__ dtok, int d) {
+  const int64_t m = blockIdx.x;
+  const int64_t id = ids[m];
+  for (int i = threadIdx.x; i < d; i += blockDim.x) atomicAdd(dtok + id * d + i, g[m * d + i]);
+}
+
+__global__ void embed_bwd_pos_kernel(const float* __restrict__ g, float* __restrict__ dpos, int B,
+                                     int T, int d, int accumulate) {
+  const int t = blockIdx.x;
+  for (int i = threadIdx.x; i < d; i += blockDim.x) {
+    float s = 0.f;
+    for (int b = 0; b < B; ++b) s += g[(static_cast<int64_t>(b) * T + t) * d + i];
+    float* o = dpos + static_cast<int64_t>(t) * d + i;
+    *o = accumulate ? *o + s : s;
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// LayerNorm
+// ------------------------------------------------------------------------------------------
+template <int THREADS, int V4>
+__global__ void __launch_bounds__(THREADS) ln_fwd_kernel(const float* __restrict__ x,
+                                                         const float* __restrict__ scale,
+                                                         const float* __restrict__ bias,
+                                                         bf16* __restrict__ y, float* __restrict__ mean_out,
+                                                         float* __restrict__ rstd_out, int d, float eps) {
+  __shared__ float red[32];
+  const int64_t row = blockIdx.x;
+  const float* xr = x + row * d;
+  float4 v[V4];
+  float s = 0.f;
+#pragma unroll
+  for (int j = 0; j < V4; ++j) {
+    const int c = (threadIdx.x + j * THREADS) * 4;
+    v[j] = c < d ? *reinterpret_cast<const float4*>(xr + c) : make_float4(0, 0, 0, 0);
+    s += v[j].x + v[j].y + v[j].z + v[j].w;
+  }
+  const float mean = block_sum(s, red) / d;
+  float q = 0.f;
+#pragma unroll
+  for (int j = 0; j < V4; ++j) {
+    const int c = (threadIdx.x + j * THREADS) * 4;
+    if (c < d) {
+      const float a = v[j].x - mean, b = v[j].y - mean, e = v[j].z - mean, f = v[j].w - mean;
+      q += a * a + b * b + e * e + f * f;
+    }
+  }
+  const float var = block_sum(q, red) / d;
+  const float rstd = 1.0f / sqrtf(var + eps);
+  bf16* yr = y + row * d;
+#pragma unroll
+  for (int j = 0; j < V4; ++j) {
+    const int c = (threadIdx.x + j * THREADS) * 4;
+    if (c < d) {
+      const float4 sc = *reinterpret_cast<const float4*>(scale + c);
+      const float4 bi = *reinterpret_cast<const float4*>(bias + c);
+      uint2 w;
+      w.x = dev::pack_bf16x2((v[j].x - mean) * rstd * sc.x + bi.x, (v[j].y - mean) * rstd * sc.y + bi.y);
+      w.y = dev::pack_bf16x2((v[j].z - mean) * rstd * sc.z + bi.z, (v[j].w - mean) * rstd * sc.w + bi.w);
+      *reinterpret_cast<uint2*>(yr + c) = w;
+    }
+  }
+  if (threadIdx.x == 0) {
+    mean_out[row] = mean;
+    rstd_out[row] = rstd;
+  }
+}
+
+// Any d (scalar path).
+__global__ void ln_fwd_generic_kernel(const float* __restrict__ x, const float* __restrict__ scale,
+                                      const float* __restrict__ bias, bf16* __restrict__ y,
+                                      float* __restrict__ mean_out, float* __restrict__ rstd_out,
+                                      int d, float eps) {
+  __shared__ float red[32];
+  const int64_t row = blockIdx.x;
+  const float* xr = x + row * d;
+  float s = 0.f;
+  for (int i = threadIdx.x; i < d; i += blockDim.x) s += xr[i];
+  const float mean = block_sum(s, red) / d;
+  float q = 0.f;
+  for (int i = threadIdx.x; i < d; i += blockDim.x) {
+    const float a = xr[i] - mean;
+    q += a * a;
+  }
+  const float var = block_sum(q, red) / d;
+  const float rstd = 1.0f / sqrtf(var + eps);
+  for (int i = threadIdx.x; i < d; i += blockDim.x) {
+    y[row * d + i] = __float2bfloat16((xr[i] - mean) * rstd * scale[i] + bias[i]);
+  }
+  if (threadIdx.x == 0) {
+    mean_out[row] = mean;
+    rstd_out[row] = rstd;
+  }
+}
+
+// One CTA walks rows r = blockIdx.x, +gridDim.x, ...; each thread owns fixed columns and
+// accumulates dscale / dbias partials in registers, flushed with one atomic per column.
+template <int THREADS, int V4>
+__global__ void __launch_bounds__(THREADS) ln_bwd_kernel(
+    const float* __restrict__ x, const float* __restrict__ mean, const float* __restrict__ rstd,
+    const float* __restrict__ scale, const float* __restrict__ dy, float* __restrict__ g_io,
+    bf16* __restrict__ g_bf16, float* __restrict__ dscale, float* __restrict__ dbias, int64_t M,
+    int d, int accumulate) {
+  __shared__ float red[32];
+  float4 ds[V4], db[V4], sc[V4];
+#pragma unroll
+  for (int j = 0; j < V4; ++j) {
+    const int c = (threadIdx.x + j * THREADS) * 4;
+    ds[j] = db[j] = make_float4(0, 0, 0, 0);
+    sc[j] = c < d ? *reinterpret_cast<const float4*>(scale + c) : make_float4(0, 0, 0, 0);
+  }
+  for (int64_t row = blockIdx.x; row < M; row += gridDim.x) {
+    const float mu = mean[row], rs = rstd[row];
+    float4 xh[V4], gg[V4];
+    float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+    for (int j = 0; j < V4; ++j) {
+      const int c = (threadIdx.x + j * THREADS) * 4;
+      if (c < d) {
+        const float4 xv = *reinterpret_cast<const float4*>(x + row * d + c);
+        const float4 dv = *reinterpret_cast<const float4*>(dy + row * d + c);
+        xh[j] = make_float4((xv.x - mu) * rs, (xv.y - mu) * rs, (xv.z - mu) * rs, (xv.w - mu) * rs);
+        gg[j] = make_float4(dv.x * sc[j].x, dv.y * sc[j].y, dv.z * sc[j].z, dv.w * sc[j].w);
+        ds[j].x += dv.x * xh[j].x; ds[j].y += dv.y * xh[j].y; ds[j].z += dv.z * xh[j].z; ds[j].w += dv.w * xh[j].w;
+        db[j].x += dv.x; db[j].y += dv.y; db[j].z += dv.z; db[j].w += dv.w;
+        s1 += gg[j].x + gg[j].y + gg[j].z + gg[j].w;
+        s2 += gg[j].x * xh[j].x + gg[j].y * xh[j].y + gg[j].z * xh[j].z + gg[j].w * xh[j].w;
+      }
+    }
+    const float gm = block_sum(s1, red) / d;
+    const float gxm = block_sum(s2, red) / d;
+#pragma unroll
+    for (int j = 0; j < V4; ++j) {
+      const int c = (threadIdx.x + j * THREADS) * 4;
+      if (c < d) {
+        float4 dx = make_float4(rs * (gg[j].x - gm - xh[j].x * gxm), rs * (gg[j].y - gm - xh[j].y * gxm),
+                                rs * (gg[j].z - gm - xh[j].z * gxm), rs * (gg[j].w - gm - xh[j].w * gxm));
+        float* gp = g_io + row * d + c;
+        if (accumulate) {
+          const float4 o = *reinterpret_cast<const float4*>(gp);
+          dx.x += o.x; dx.y += o.y; dx.z += o.z; dx.w += o.w;
+        }
+        *reinterpret_cast<float4*>(gp) = dx;
+        uint2 w;
+        w.x = dev::pack_bf16x2(dx.x, dx.y);
+        w.y = dev::pack_bf16x2(dx.z, dx.w);
+        *reinterpret_cast<uint2*>(g_bf16 + row * d + c) = w;
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < V4; ++j) {
+    const int c = (threadIdx.x + j * THREADS) * 4;
+    if (c < d) {
+      atomicAdd(dscale + c, ds[j].x); atomicAdd(dscale + c + 1, ds[j].y);
+      atomicAdd(dscale + c + 2, ds[j].z); atomicAdd(dscale + c + 3, ds[j].w);
+      atomicAdd(dbias + c, db[j].x); atomicAdd(dbias + c + 1, db[j].y);
+      atomicAdd(dbias + c + 2, db[j].z); atomicAdd(dbias + c + 3, db[j].w);
+    }
+  }
+}
+
+__global__ void ln_bwd_generic_kernel(const float* __restrict__ x, const float* __restrict__ mean,
+                                      const float* __restrict__ rstd, const float* __restrict__ scale,
+                                      const float* __restrict__ dy, float* __restrict__ g_io,
+                                      bf16* __restrict__ g_bf16, float* __restrict__ dscale,
+                                      float* __restrict__ dbias, int d, int accumulate) {
+  __shared__ float red[32];
+  const int64_t row = blockIdx.x;
+  const float mu = mean[row], rs = rstd[row];
+  float s1 = 0.f, s2 = 0.f;
+  for (int i = threadIdx.x; i < d; i += blockDim.x) {
+    const float xh = (x[row * d + i] - mu) * rs;
+    const float g = dy[row * d + i] * scale[i];
+    s1 += g;
+    s2 += g * xh;
+  }
+  const float gm = block_sum(s1, red) / d;
+  const float gxm = block_sum(s2, red) / d;
+  for (int i = threadIdx.x; i < d; i += blockDim.x) {
+    const float xh = (x[row * d + i] - mu) * rs;
+    const float dv = dy[row * d + i];
+    const float g = dv * scale[i];
+    float dx = rs * (g - gm - xh * gxm);
+    if (accumulate) dx += g_io[row * d + i];
+    g_io[row * d + i] = dx;
+    g_bf16[row * d + i] = __float2bfloat16(dx);
+    atomicAdd(dscale + i, dv * xh);
+    atomicAdd(dbias + i, dv);
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// column sums (bias gradients)
+// ------------------------------------------------------------------------------------------
+constexpr int kColChunk = 64;  // columns per CTA
+constexpr int kRowChunk = 256; // rows per CTA (partials)
+
+template <typename T>
+__device__ __forceinline__ float ld_as_float(const T* p);
+template <>
+__device__ __forceinline__ float ld_as_float<float>(const float* p) { return *p; }
+template <>
+__device__ __forceinline__ float ld_as_float<bf16>(const bf16* p) { return __bfloat162float(*p); }
+
+// stage 1: partial[chunk][n] = sum over 256 rows of the chunk. Threads: 64 columns x 4 rows.
+template <typename T>
+__global__ void colsum_partial_kernel(const T* __restrict__ X, int64_t ld, int64_t M, int N,
+                                      float* __restrict__ partial) {
+  __shared__ float sm[4][kColChunk];
+  const int c = blockIdx.x * kColChunk + (threadIdx.x & 63);
+  const int ry = threadIdx.x >> 6;
+  const int64_t r0 = static_cast<int64_t>(blockIdx.y) * kRowChunk;
+  float s = 0.f;
+  if (c < N) {
+    const int64_t r_end = (M < r0 + kRowChunk) ? M : r0 + kRowChunk;
+    for (int64_t r = r0 + ry; r < r_end; r += 4) s += ld_as_float(X + r * ld + c);
+  }
+  sm[ry][threadIdx.x & 63] = s;
+  __syncthreads();
+  if (ry == 0 && c < N) {
+    partial[static_cast<int64_t>(blockIdx.y) * N + c] = sm[0][threadIdx.x] + sm[1][threadIdx.x] +
+                                                        sm[2][threadIdx.x] + sm[3][threadIdx.x];
+  }
+}
+
+__global__ void colsum_final_kernel(const float* __restrict__ partial, int chunks, int N, int seg,
+                                    float* out0, float* out1, float* out2, int accumulate) {
+  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= N) return;
+  float s = 0.f;
+  for (int c = 0; c < chunks; ++c) s += partial[static_cast<int64_t>(c) * N + n];
+  const int si = n / seg;
+  float* o = (si == 0 ? out0 : si == 1 ? out1 : out2) + (n - si * seg);
+  *o = accumulate ? *o + s : s;
+}
+
+// ------------------------------------------------------------------------------------------
+// reductions / cross entropy
+// ------------------------------------------------------------------------------------------
+__global__ void sum_f32_kernel(const float* __restrict__ x, int64_t n, float* out) {
+  __shared__ float red[32];
+  float s = 0.f;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) s += x[i];
+  s = block_sum(s, red);
+  if (threadIdx.x == 0) *out = s;
+}
+
+__global__ void loss_reduce_kernel(const float* __restrict__ wl, int64_t n, const float* wsum,
+                                   double* loss) {
+  __shared__ double red[32];
+  double s = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) s += wl[i];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (blockDim.x + 31) / 32; ++w) t += red[w];
+    *loss = t / static_cast<double>(*wsum);
+  }
+}
+
+// One CTA per row. Pass 1: per-thread online (max, sumexp) -> block combine. Pass 2: gradient.
+__global__ void __launch_bounds__(512) xent_kernel(bf16* __restrict__ logits, int64_t ld, int V,
+                                                   const int32_t* __restrict__ targets,
+                                                   const float* __restrict__ weights,
+                                                   const float* __restrict__ wsum,
+                                                   float* __restrict__ wloss, int write_grad) {
+  __shared__ float red_m[32], red_s[32];
+  __shared__ float bc[2];
+  const int64_t row = blockIdx.x;
+  bf16* lr = logits + row * ld;
+  const bool vec = (V % 8 == 0) && (ld % 8 == 0);
+  float mx = -INFINITY, se = 0.f;
+  auto acc = [&](float x) {
+    if (x > mx) {
+      se = se * __expf(mx - x) + 1.f;
+      mx = x;
+    } else {
+      se += __expf(x - mx);
+    }
+  };
+  if (vec) {
+    for (int i = threadIdx.x * 8; i < V; i += blockDim.x * 8) {
+      const uint4 u = *reinterpret_cast<const uint4*>(lr + i);
+      const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 f = dev::unpack_bf16x2(w[j]);
+        acc(f.x);
+        acc(f.y);
+      }
+    }
+  } else {
+    for (int i = threadIdx.x; i < V; i += blockDim.x) acc(__bfloat162float(lr[i]));
+  }
+  // combine (max, sum) across the warp then the block
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float m2 = __shfl_xor_sync(0xffffffffu, mx, o);
+    const float s2 = __shfl_xor_sync(0xffffffffu, se, o);
+    const float m = fmaxf(mx, m2);
+    se = (mx == -INFINITY ? 0.f : se * __expf(mx - m)) + (m2 == -INFINITY ? 0.f : s2 * __expf(m2 - m));
+    mx = m;
+  }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) {
+    red_m[wid] = mx;
+    red_s[wid] = se;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float m = -INFINITY;
+    const int nw = blockDim.x / 32;
+    for (int w = 0; w < nw; ++w) m = fmaxf(m, red_m[w]);
+    float s = 0.f;
+    for (int w = 0; w < nw; ++w) s += red_s[w] * __expf(red_m[w] - m);
+    bc[0] = m;
+    bc[1] = s;
+    const int tgt = targets[row];
+    const float lse = m + logf(s);
+    wloss[row] = weights[row] * (lse - __bfloat162float(lr[tgt]));
+  }
+  __syncthreads();
+  if (!write_grad) return;
+  const float m = bc[0];
+  const float inv = 1.0f / bc[1];
+  const float scale = weights[row] / *wsum;
+  const int tgt = targets[row];
+  if (vec) {
+    for (int i = threadIdx.x * 8; i < V; i += blockDim.x * 8) {
+      uint4 u = *reinterpret_cast<const uint4*>(lr + i);
+      uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 f = dev::unpack_bf16x2(w[j]);
+        float a = __expf(f.x - m) * inv, b = __expf(f.y - m) * inv;
+        if (i + 2 * j == tgt) a -= 1.f;
+        if (i + 2 * j + 1 == tgt) b -= 1.f;
+        w[j] = dev::pack_bf16x2(a * scale, b * scale);
+      }
+      *reinterpret_cast<uint4*>(lr + i) = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+  } else {
+    for (int i = threadIdx.x; i < V; i += blockDim.x) {
+      float a = __expf(__bfloat162float(lr[i]) - m) * inv;
+      if (i == tgt) a -= 1.f;
+      lr[i] = __float2bfloat16(a * scale);
+    }
+  }
+}
+
+__global__ void add_residual_bias_kernel(const float* __restrict__ a, const float* __restrict__ b,
+                                         const float* __restrict__ bias, float* __restrict__ y,
+                                         int64_t n4, int d) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n4;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const float4 x = reinterpret_cast<const float4*>(a)[i];
+    const float4 z = reinterpret_cast<const float4*>(b)[i];
+    const int c = static_cast<int>((i * 4) % d);
+    const float4 bb = *reinterpret_cast<const float4*>(bias + c);
+    reinterpret_cast<float4*>(y)[i] = make_float4(x.x + z.x + bb.x, x.y + z.y + bb.y, x.z + z.z + bb.z, x.w + z.w + bb.w);
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// optimizer / misc
+// ------------------------------------------------------------------------------------------
+__device__ __forceinline__ void adamw_one(float& p, float& m, float& v, float g, float lr, float b1,
+                                          float b2, float eps, float wd, float c1, float c2) {
+  // train_state.hpp:214-216, evaluated in Scalar=float with the same operation order.
+  m = b1 * m + (1.0f - b1) * g;
+  v = b2 * v + (1.0f - b2) * (g * g);
+  p = p - lr * (__fdiv_rn(__fdiv_rn(m, c1), __fsqrt_rn(__fdiv_rn(v, c2)) + eps) + wd * p);
+}
+
+__global__ void adamw_kernel(float* __restrict__ p, float* __restrict__ m, float* __restrict__ v,
+                             const float* __restrict__ g, bf16* __restrict__ shadow, int64_t n,
+                             float lr, float b1, float b2, float eps, float wd, float c1, float c2) {
+  const int64_t n4 = n / 4;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n4; i += stride) {
+    float4 pp = reinterpret_cast<float4*>(p)[i];
+    float4 mm = reinterpret_cast<float4*>(m)[i];
+    float4 vv = reinterpret_cast<float4*>(v)[i];
+    const float4 gg = reinterpret_cast<const float4*>(g)[i];
+    adamw_one(pp.x, mm.x, vv.x, gg.x, lr, b1, b2, eps, wd, c1, c2);
+    adamw_one(pp.y, mm.y, vv.y, gg.y, lr, b1, b2, eps, wd, c1, c2);
+    adamw_one(pp.z, mm.z, vv.z, gg.z, lr, b1, b2, eps, wd, c1, c2);
+    adamw_one(pp.w, mm.w, vv.w, gg.w, lr, b1, b2, eps, wd, c1, c2);
+    reinterpret_cast<float4*>(p)[i] = pp;
+    reinterpret_cast<float4*>(m)[i] = mm;
+    reinterpret_cast<float4*>(v)[i] = vv;
+    uint2 w;
+    w.x = dev::pack_bf16x2(pp.x, pp.y);
+    w.y = dev::pack_bf16x2(pp.z, pp.w);
+    reinterpret_cast<uint2*>(shadow)[i] = w;
+  }
+  for (int64_t i = n4 * 4 + blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n; i += stride) {
+    adamw_one(p[i], m[i], v[i], g[i], lr, b1, b2, eps, wd, c1, c2);
+    shadow[i] = __float2bfloat16(p[i]);
+  }
+}
+
+__global__ void nonfinite_kernel(const float* __restrict__ x, int64_t n, int* flag) {
+  int bad = 0;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    bad |= !isfinite(x[i]);
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 1);
+}
+
+__global__ void scale_kernel(float* x, int64_t n, float a) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    x[i] *= a;
+  }
+}
+
+__global__ void cast_kernel(const float* __restrict__ x, bf16* __restrict__ y, int64_t n) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    y[i] = __float2bfloat16(x[i]);
+  }
+}
+
+__global__ void fill_kernel(float* x, int64_t n, float v) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    x[i] = v;
+  }
+}
+
+struct RankPtrs {
+  float* p[16];
+};
+
+__global__ void sum_ranks_kernel(RankPtrs bufs, int nranks, int64_t n, float scale) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    float s = bufs.p[0][i];
+    for (int r = 1; r < nranks; ++r) s += bufs.p[r][i];
+    s *= scale;
+    for (int r = 0; r < nranks; ++r) bufs.p[r][i] = s;
+  }
+}
+
+__device__ __forceinline__ uint64_t splitmix_mix(uint64_t z) {
+  z += 0x9e3779b97f4a7c15ull;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+
+__global__ void init_normal_kernel(float* out, int64_t lr, int64_t lc, int64_t r0, int64_t c0,
+                                   int64_t cols, uint64_t key, uint64_t base, double scale) {
+  const int64_t n = lr * lc;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t i = e / lc, j = e - (e / lc) * lc;
+    const uint64_t g = static_cast<uint64_t>((r0 + i) * cols + (c0 + j));
+    const uint64_t d1 = splitmix_mix(key + base + 2 * g);
+    const uint64_t d2 = splitmix_mix(key + base + 2 * g + 1);
+    double u1 = static_cast<double>(d1 >> 11) * 0x1.0p-53;
+    const double u2 = static_cast<double>(d2 >> 11) * 0x1.0p-53;
+    if (u1 <= 0.0) u1 = 0x1.0p-53;
+    const double r = sqrt(-2.0 * log(u1));
+    const double z = r * cos(2.0 * 3.14159265358979323846 * u2);
+    out[e] = static_cast<float>(z * scale);
+  }
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------------------------------
+// launchers
+// ------------------------------------------------------------------------------------------
+void embed_fwd(const int32_t* ids, const float* tok, const float* pos, float* h, int64_t M, int T,
+               int d, cudaStream_t s) {
+  embed_fwd_kernel<<<static_cast<unsigned>(M), d >= 1024 ? 256 : 128, 0, s>>>(ids, tok, pos, h, T, d);
+}
+
+void embed_bwd_tok(const int32_t* ids, const float* g, float* dtok, int64_t M, int d, cudaStream_t s) {
+  embed_bwd_tok_kernel<<<static_cast<unsigned>(M), 256, 0, s>>>(ids, g, dtok, d);
+}
+
+void embed_bwd_pos(const float* g, float* dpos, int B, int T, int d, int accumulate, cudaStream_t s) {
+  embed_bwd_pos_kernel<<<T, 256, 0, s>>>(g, dpos, B, T, d, accumulate);
+}
+
+void layernorm_fwd(const float* x, const float* scale, const float* bias, bf16* y, float* mean,
+                   float* rstd, int64_t M, int d, float eps, cudaStream_t s) {
+  const unsigned g = static_cast<unsigned>(M);
+  if (d % 4 == 0 && d <= 512) {
+    ln_fwd_kernel<32, 4><<<g, 32, 0, s>>>(x, scale, bias, y, mean, rstd, d, eps);
+  } else if (d % 4 == 0 && d <= 4096) {
+    ln_fwd_kernel<256, 4><<<g, 256, 0, s>>>(x, scale, bias, y, mean, rstd, d, eps);
+  } else if (d % 4 == 0 && d <= 12288) {
+    ln_fwd_kernel<512, 6><<<g, 512, 0, s>>>(x, scale, bias, y, mean, rstd, d, eps);
+  } else {
+    ln_fwd_generic_kernel<<<g, 256, 0, s>>>(x, scale, bias, y, mean, rstd, d, eps);
+  }
+}
+
+void layernorm_bwd(const float* x, const float* mean, const float* rstd, const float* scale,
+                   const float* dy, float* g_io, bf16* g_bf16, float* dscale, float* dbias,
+                   int64_t M, int d, int accumulate, cudaStream_t s) {
+  const unsigned g = static_cast<unsigned>(M < 2 * kSMs ? M : 2 * kSMs);
+  if (d % 4 == 0 && d <= 512) {
+    ln_bwd_kernel<32, 4><<<g, 32, 0, s>>>(x, mean, rstd, scale, dy, g_io, g_bf16, dscale, dbias, M, d, accumulate);
+  } else if (d % 4 == 0 && d <= 4096) {
+    ln_bwd_kernel<256, 4><<<g, 256, 0, s>>>(x, mean, rstd, scale, dy, g_io, g_bf16, dscale, dbias, M, d, accumulate);
+  } else if (d % 4 == 0 && d <= 12288) {
+    ln_bwd_kernel<512, 6><<<g, 512, 0, s>>>(x, mean, rstd, scale, dy, g_io, g_bf16, dscale, dbias, M, d, accumulate);
+  } else {
+    ln_bwd_generic_kernel<<<static_cast<unsigned>(M), 256, 0, s>>>(x, mean, rstd, scale, dy, g_io, g_bf16,
+                                                                  dscale, dbias, d, accumulate);
+  }
+}
+
+void colsum_bf16(const bf16* X, int64_t ld, int64_t M, int N, int seg, float* out0, float* out1,
+                 float* out2, int accumulate, float* scratch, cudaStream_t s) {
+  const int chunks = static_cast<int>((M + kRowChunk - 1) / kRowChunk);
+  dim3 grid((N + kColChunk - 1) / kColChunk, chunks);
+  colsum_partial_kernel<bf16><<<grid, 256, 0, s>>>(X, ld, M, N, scratch);
+  colsum_final_kernel<<<(N + 255) / 256, 256, 0, s>>>(scratch, chunks, N, seg > 0 ? seg : N, out0,
+                                                     out1, out2, accumulate);
+}
+
+void colsum_f32(const float* X, int64_t ld, int64_t M, int N, float* out, int accumulate,
+                float* scratch, cudaStream_t s) {
+  const int chunks = static_cast<int>((M + kRowChunk - 1) / kRowChunk);
+  dim3 grid((N + kColChunk - 1) / kColChunk, chunks);
+  colsum_partial_kernel<float><<<grid, 256, 0, s>>>(X, ld, M, N, scratch);
+  colsum_final_kernel<<<(N + 255) / 256, 256, 0, s>>>(scratch, chunks, N, N, out, nullptr, nullptr,
+                                                     accumulate);
+}
+
+void sum_f32(const float* x, int64_t n, float* out, cudaStream_t s) {
+  sum_f32_kernel<<<1, 1024, 0, s>>>(x, n, out);
+}
+
+void xent_fwd_bwd(bf16* logits, int64_t ld, int64_t M, int V, const int32_t* targets,
+                  const float* weights, const float* wsum, float* wloss, int write_grad,
+                  cudaStream_t s) {
+  xent_kernel<<<static_cast<unsigned>(M), 512, 0, s>>>(logits, ld, V, targets, weights, wsum, wloss,
+                                                       write_grad);
+}
+
+void loss_reduce(const float* wloss, int64_t M, const float* wsum, double* loss, cudaStream_t s) {
+  loss_reduce_kernel<<<1, 1024, 0, s>>>(wloss, M, wsum, loss);
+}
+
+void add_residual_bias(const float* a, const float* b, const float* bias, float* y, int64_t M,
+                       int d, cudaStream_t s) {
+  const int64_t n4 = M * d / 4;
+  add_residual_bias_kernel<<<grid_for(n4, 256), 256, 0, s>>>(a, b, bias, y, n4, d);
+}
+
+void adamw(float* p, float* m, float* v, const float* g, bf16* shadow, int64_t n, float lr,
+           float b1, float b2, float eps, float wd, float c1, float c2, cudaStream_t s) {
+  adamw_kernel<<<grid_for(n / 4 + 1, 256), 256, 0, s>>>(p, m, v, g, shadow, n, lr, b1, b2, eps, wd, c1, c2);
+}
+
+void nonfinite_check(const float* x, int64_t n, int* flag, cudaStream_t s) {
+  nonfinite_kernel<<<grid_for(n, 256, 4), 256, 0, s>>>(x, n, flag);
+}
+
+void scale_f32(float* x, int64_t n, float a, cudaStream_t s) {
+  scale_kernel<<<grid_for(n, 256, 4), 256, 0, s>>>(x, n, a);
+}
+
+void cast_f32_bf16(const float* x, bf16* y, int64_t n, cudaStream_t s) {
+  cast_kernel<<<grid_for(n, 256, 4), 256, 0, s>>>(x, y, n);
+}
+
+void fill_f32(float* out, int64_t n, float v, cudaStream_t s) {
+  fill_kernel<<<grid_for(n, 256, 4), 256, 0, s>>>(out, n, v);
+}
+
+void sum_ranks_f32(float* const* bufs, int nranks, int64_t n, float scale, cudaStream_t s) {
+  RankPtrs p{};
+  for (int r = 0; r < nranks && r < 16; ++r) p.p[r] = bufs[r];
+  sum_ranks_kernel<<<grid_for(n, 256, 4), 256, 0, s>>>(p, nranks, n, scale);
+}
+
+void init_normal(float* out, int64_t lr, int64_t lc, int64_t r0, int64_t c0, int64_t cols,
+                 uint64_t key, uint64_t base_counter, double scale, cudaStream_t s) {
+  init_normal_kernel<<<grid_for(lr * lc, 256, 4), 256, 0, s>>>(out, lr, lc, r0, c0, cols, key,
+                                                              base_counter, scale);
+}
+
+}  // namespace k
+}  // namespace sw

@@ -1,0 +1,84 @@
+// Launchers of the non-GEMM kernels of the step (HBM-bound elementwise / reduction work).
+// Every launcher enqueues exactly one kernel on `s` and returns nothing; errors surface through
+// cudaGetLastError at the executor's checkpoints.
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace sw {
+namespace k {
+
+using bf16 = __nv_bfloat16;
+
+// h[m, :] = tok[ids[m], :] + pos[m % T, :]                       (model.hpp:90-98)
+void embed_fwd(const int32_t* ids, const float* tok, const float* pos, float* h, int64_t M, int T,
+               int d, cudaStream_t s);
+// dtok[ids[m], :] += g[m, :] (atomic); dpos[t, :] (+)= sum_b g[b*T + t, :]   (kernels.hpp:291-304)
+void embed_bwd_tok(const int32_t* ids, const float* g, float* dtok, int64_t M, int d, cudaStream_t s);
+void embed_bwd_pos(const float* g, float* dpos, int B, int T, int d, int accumulate, cudaStream_t s);
+
+// LayerNorm over the last dim, biased variance, eps (kernels.hpp:184-215): y = xhat*scale+bias
+// (bf16), mean/rstd saved for the backward.
+void layernorm_fwd(const float* x, const float* scale, const float* bias, bf16* y, float* mean,
+                   float* rstd, int64_t M, int d, float eps, cudaStream_t s);
+// dx = rstd*(g - mean(g) - xhat*mean(g*xhat)), g = dy*scale (kernels.hpp:232-271).
+// g_io: residual-stream gradient; g_io = (accumulate ? g_io : 0) + dx; g_bf16 = bf16(g_io).
+// dscale += sum_rows dy*xhat, dbias += sum_rows dy (atomics; caller zeroes when needed).
+void layernorm_bwd(const float* x, const float* mean, const float* rstd, const float* scale,
+                   const float* dy, float* g_io, bf16* g_bf16, float* dscale, float* dbias,
+                   int64_t M, int d, int accumulate, cudaStream_t s);
+
+// Column sums of X [M, N] (bf16 or f32, row pitch ld) written (accumulate=0) or added into
+// out: column n goes to outs[n / seg][n % seg] (up to 3 segments). scratch: >= 64*N floats.
+void colsum_bf16(const bf16* X, int64_t ld, int64_t M, int N, int seg, float* out0, float* out1,
+                 float* out2, int accumulate, float* scratch, cudaStream_t s);
+void colsum_f32(const float* X, int64_t ld, int64_t M, int N, float* out, int accumulate,
+                float* scratch, cudaStream_t s);
+
+// sum of weights -> wsum[0]
+void sum_f32(const float* x, int64_t n, float* out, cudaStream_t s);
+// Fused softmax cross entropy forward + backward over the vocab (kernels.hpp:327-363):
+// wloss[m] = w[m] * (logsumexp - logit[target]); logits <- (softmax - onehot) * w[m] / wsum.
+void xent_fwd_bwd(bf16* logits, int64_t ld, int64_t M, int V, const int32_t* targets,
+                  const float* weights, const float* wsum, float* wloss, int write_grad,
+                  cudaStream_t s);
+// loss[0] = sum(wloss) / wsum (double)
+void loss_reduce(const float* wloss, int64_t M, const float* wsum, double* loss, cudaStream_t s);
+
+// Causal scaled-dot-product attention on the head-sharded QKV activations:
+// qkv [M, 3*Dl] (q | k | v, head h at column h*hd), o [M, Dl], lse [B, Hl, T]
+// (graph.hpp:650-661 with the -1e9 causal mask of model.hpp:100-106).
+void attention_fwd(const bf16* qkv, bf16* o, float* lse, int B, int T, int Hl, int hd,
+                   cudaStream_t s);
+// dqkv [M, 3*Dl]; scratch: fp32 [B*Hl*T] (delta) + fp32 [M, 3*Dl] (dk/dv accumulators).
+void attention_bwd(const bf16* qkv, const bf16* o, const float* lse, const bf16* dout, bf16* dqkv,
+                   float* scratch, int B, int T, int Hl, int hd, cudaStream_t s);
+
+// y = a + b + bias[col]   (row-parallel output after the all-reduce: residual + partial + bias)
+void add_residual_bias(const float* a, const float* b, const float* bias, float* y, int64_t M,
+                       int d, cudaStream_t s);
+
+// AdamW over a flat shard (train_state.hpp:183-220, Scalar = float); also refreshes the bf16
+// shadow copy used by the GEMMs.
+void adamw(float* p, float* m, float* v, const float* g, bf16* shadow, int64_t n, float lr,
+           float b1, float b2, float eps, float wd, float c1, float c2, cudaStream_t s);
+// flag[0] |= any non-finite among x[0..n)
+void nonfinite_check(const float* x, int64_t n, int* flag, cudaStream_t s);
+void scale_f32(float* x, int64_t n, float a, cudaStream_t s);
+void cast_f32_bf16(const float* x, bf16* y, int64_t n, cudaStream_t s);
+
+// Emulated collective: every bufs[r][0..n) <- sum_{r ascending} bufs[r] (collectives.hpp:27-52).
+void sum_ranks_f32(float* const* bufs, int nranks, int64_t n, float scale, cudaStream_t s);
+
+// init_transformer_params on the device (model.hpp:49-70 + rng.hpp:15-91): element (r, c) of
+// the FULL [rows, cols] tensor takes normal draw number base_draw/2 + r*cols + c of the stream
+// with key `key`, times `scale`. The local shard covers rows [r0, r0+lr) x cols [c0, c0+lc).
+void init_normal(float* out, int64_t lr, int64_t lc, int64_t r0, int64_t c0, int64_t cols,
+                 uint64_t key, uint64_t base_counter, double scale, cudaStream_t s);
+void fill_f32(float* out, int64_t n, float v, cudaStream_t s);
+
+}  // namespace k
+}  // namespace sw

@@ -1,0 +1,827 @@
+// GPU executor of the tensor-parallel transformer step (see model.h).
+#include "model.h"
+
+#include <cmath>
+#include <cstring>
+#include <stdexcept>
+
+#include "gemm.h"
+#include "kernels.h"
+#include "status.h"
+
+namespace sw {
+
+namespace {
+
+uint64_t mix64(uint64_t z) {
+  z += 0x9e3779b97f4a7c15ull;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+
+uint64_t fnv1a(const std::string& s) {
+  uint64_t h = 0xcbf29ce484222325ull;
+  for (unsigned char c : s) {
+    h ^= c;
+    h *= 0x100000001b3ull;
+  }
+  return h;
+}
+
+int64_t numel_of(const Dims& d) {
+  int64_t n = 1;
+  for (int64_t x : d) n *= x;
+  return n;
+}
+
+constexpr int64_t kAlign = 64;  // elements; keeps every slot 256-B aligned in fp32, 128-B in bf16
+
+}  // namespace
+
+// ---------------------------------------------------------------------------------------------
+// construction: plan -> per-rank layout
+// ---------------------------------------------------------------------------------------------
+Model::Model(const ModelSpec& spec, const Plan& plan, Mesh* mesh, int batch, int seq_len)
+    : spec_(spec), plan_(plan), mesh_(mesh), B_(batch), T_(seq_len) {
+  if (mesh == nullptr) fail(SW_ERR_CONFIG, "sw_model_create: mesh is NULL");
+  if (batch < 1 || seq_len < 1) {
+    fail(SW_ERR_CONFIG, "transformer_logits: batch and seq_len must be positive");
+  }
+  if (seq_len > spec.max_seq_len) {
+    fail(SW_ERR_CONFIG, "transformer_logits: seq_len " + std::to_string(seq_len) +
+                            " exceeds max_seq_len " + std::to_string(spec.max_seq_len));
+  }
+  if (plan.n_shards != mesh->mp) {
+    fail(SW_ERR_CONFIG, "sw_model_create: plan has n_shards=" + std::to_string(plan.n_shards) +
+                            " but the mesh has mp=" + std::to_string(mesh->mp));
+  }
+  M_ = static_cast<int64_t>(B_) * T_;
+  L_ = spec.n_layers;
+  d_ = static_cast<int>(spec.d_model);
+  H_ = spec.n_heads;
+  hd_ = d_ / H_;
+  dff_ = static_cast<int>(spec.d_ff);
+  V_ = static_cast<int>(spec.vocab_size);
+  S_ = static_cast<int>(spec.max_seq_len);
+  cuda_check(cudaSetDevice(mesh->cuda_device), "cudaSetDevice");
+  cuda_check(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "cudaStreamCreate");
+  build_layout();
+  allocate();
+}
+
+Model::~Model() {
+  if (stream_) cudaStreamSynchronize(stream_);
+  for (void* p : allocations_) cudaFree(p);
+  if (stream_) cudaStreamDestroy(stream_);
+}
+
+template <typename T>
+T* Model::alloc(int64_t n) {
+  void* p = nullptr;
+  const size_t bytes = static_cast<size_t>(n > 0 ? n : 1) * sizeof(T);
+  cuda_check(cudaMalloc(&p, bytes), "cudaMalloc");
+  allocations_.push_back(p);
+  bytes_ += static_cast<int64_t>(bytes);
+  return static_cast<T*>(p);
+}
+
+void Model::build_layout() {
+  const int t = mesh_->mp;
+  const std::vector<NamedShape> shapes = transformer_param_shapes(spec_);
+  // init draw bases in tree order (model.hpp:55-68: one stream, 2 draws per normal)
+  uint64_t draws = 0;
+  std::unordered_map<std::string, std::pair<int, uint64_t>> init_of;
+  for (const auto& p : shapes) {
+    const std::string leaf = p.name.substr(p.name.rfind('/') + 1);
+    if (leaf == "bias") {
+      init_of[p.name] = {0, 0};
+    } else if (leaf == "scale") {
+      init_of[p.name] = {1, 0};
+    } else {
+      init_of[p.name] = {2, draws};
+      draws += 2 * static_cast<uint64_t>(numel_of(p.dims));
+    }
+  }
+  auto make_slot = [&](const NamedShape& p) {
+    Slot s;
+    s.name = p.name;
+    s.global = p.dims;
+    const Layout* l = plan_.find(p.name);
+    if (l == nullptr) fail(SW_ERR_CONFIG, "ShardingPlan: no entry for parameter '" + p.name + "'");
+    s.layout = *l;
+    s.local = p.dims;
+    s.begin = 0;
+    s.end = p.dims.empty() ? 1 : p.dims[0];
+    if (l->kind == Layout::kSplit) {
+      if (l->dim < 0 || static_cast<size_t>(l->dim) >= p.dims.size()) {
+        fail(SW_ERR_PARTITION, "local_shape: split dim " + std::to_string(l->dim) + " out of range for " +
+                                   dims_str(p.dims));
+      }
+      if (p.dims[l->dim] % t != 0) {
+        fail(SW_ERR_PARTITION, "local_shape: dim " + std::to_string(l->dim) + " of " + dims_str(p.dims) +
+                                   " is not divisible by " + std::to_string(t) + " shards");
+      }
+      s.local[l->dim] = p.dims[l->dim] / t;
+      s.end = s.local[l->dim];  // rank-relative; begin/end rescaled per rank on use
+    }
+    s.numel = numel_of(s.local);
+    s.init = init_of[p.name].first;
+    s.draw_base = init_of[p.name].second;
+    if (s.init == 2) {
+      s.init_scale = p.name.rfind("embed/", 0) == 0 ? 0.02 : 1.0 / std::sqrt(static_cast<double>(p.dims[1]));
+    }
+    return s;
+  };
+  std::unordered_map<std::string, const NamedShape*> by_name;
+  for (const auto& p : shapes) by_name[p.name] = &p;
+  int64_t off = 0;
+  auto place = [&](const std::string& name, bool align) {
+    const auto it = by_name.find(name);
+    Slot s = make_slot(*it->second);
+    if (align) off = (off + kAlign - 1) / kAlign * kAlign;
+    s.offset = off;
+    off += s.numel;
+    slots_.push_back(s);
+    slot_of_[name] = static_cast<int>(slots_.size()) - 1;
+    return static_cast<int>(slots_.size()) - 1;
+  };
+  tok_ = place("embed/tok/kernel", true);
+  pos_ = place("embed/pos/kernel", true);
+  for (int l = 0; l < L_; ++l) {
+    const std::string b = "block_" + std::to_string(l) + "/";
+    LayerSlots ls{};
+    ls.q_k = place(b + "attn/q/kernel", true);  // q|k|v kernels contiguous: fused [3*d/t, d]
+    ls.k_k = place(b + "attn/k/kernel", false);
+    ls.v_k = place(b + "attn/v/kernel", false);
+    ls.q_b = place(b + "attn/q/bias", true);    // q|k|v biases contiguous: [3*d]
+    ls.k_b = place(b + "attn/k/bias", false);
+    ls.v_b = place(b + "attn/v/bias", false);
+    ls.o_k = place(b + "attn/o/kernel", true);
+    ls.o_b = place(b + "attn/o/bias", true);
+    ls.ln1_s = place(b + "ln1/scale", true);
+    ls.ln1_b = place(b + "ln1/bias", true);
+    ls.ln2_s = place(b + "ln2/scale", true);
+    ls.ln2_b = place(b + "ln2/bias", true);
+    ls.fc1_k = place(b + "mlp/fc1/kernel", true);
+    ls.fc1_b = place(b + "mlp/fc1/bias", true);
+    ls.fc2_k = place(b + "mlp/fc2/kernel", true);
+    ls.fc2_b = place(b + "mlp/fc2/bias", true);
+    layers_.push_back(ls);
+  }
+  lnf_s_ = place("final_ln/scale", true);
+  lnf_b_ = place("final_ln/bias", true);
+  if (!spec_.tie_embeddings) head_ = place("lm_head/kernel", true);
+  flat_n_ = (off + kAlign - 1) / kAlign * kAlign;
+
+  // Which blocks run tensor-parallel: the two sharding rules give column-split QKV / fc1 and
+  // row-split O / fc2; a block whose kernels were all degraded to replicated runs replicated.
+  auto is_split = [&](int s, int64_t dim) {
+    return slots_[s].layout.kind == Layout::kSplit && slots_[s].layout.dim == dim;
+  };
+  auto is_repl = [&](int s) { return slots_[s].layout.kind == Layout::kReplicated; };
+  auto unsupported = [&](const std::string& what) {
+    fail(SW_ERR_PARTITION, "GPU executor: unsupported partition for " + what +
+                               " (supported: the rule layout or fully replicated)");
+  };
+  for (const Slot& s : slots_) {
+    if (s.global.size() < 2 && !is_repl(static_cast<int>(&s - slots_.data()))) {
+      unsupported("1-D parameter '" + s.name + "'");
+    }
+  }
+  if (!is_repl(tok_) || !is_repl(pos_)) unsupported("embedding tables");
+  for (int l = 0; l < L_; ++l) {
+    const LayerSlots& ls = layers_[l];
+    const bool attn_tp = is_split(ls.q_k, 0) && is_split(ls.k_k, 0) && is_split(ls.v_k, 0) && is_split(ls.o_k, 1);
+    const bool attn_rep = is_repl(ls.q_k) && is_repl(ls.k_k) && is_repl(ls.v_k) && is_repl(ls.o_k);
+    const bool mlp_tp = is_split(ls.fc1_k, 0) && is_split(ls.fc2_k, 1);
+    const bool mlp_rep = is_repl(ls.fc1_k) && is_repl(ls.fc2_k);
+    if (!(attn_tp || attn_rep)) unsupported("the attention kernels of block_" + std::to_string(l));
+    if (!(mlp_tp || mlp_rep)) unsupported("the MLP kernels of block_" + std::to_string(l));
+    const int ta = attn_tp ? mesh_->mp : 1, tm = mlp_tp ? mesh_->mp : 1;
+    if (l == 0) {
+      ta_ = ta;
+      tm_ = tm;
+    } else if (ta != ta_ || tm != tm_) {
+      unsupported("blocks with different layouts");
+    }
+  }
+  if (head_ >= 0) {
+    if (is_split(head_, 0)) {
+      th_ = mesh_->mp;
+    } else if (!is_repl(head_)) {
+      unsupported("lm_head/kernel");
+    }
+  }
+  if (th_ > 1) {
+    fail(SW_ERR_PARTITION, "GPU executor: the vocab-parallel lm_head (split:0 at mp>1) is not "
+                           "implemented yet; use the default (replicated) plan");
+  }
+  if (H_ % ta_ != 0) {
+    fail(SW_ERR_PARTITION, "GPU executor: n_heads " + std::to_string(H_) + " not divisible by the " +
+                               std::to_string(ta_) + "-way attention split (the reference all-gathers "
+                               "q/k/v here, spmd.hpp:58-71)");
+  }
+  dl_ = d_ / ta_;
+  hl_ = H_ / ta_;
+  fl_ = dff_ / tm_;
+  vl_ = V_ / th_;
+  ldv_ = (vl_ + 7) / 8 * 8;
+  for (auto [what, v] : {std::pair<const char*, int>{"d_model", d_}, {"d_model/t", dl_}, {"d_ff/t", fl_},
+                         {"vocab", vl_}}) {
+    if (v % 8 != 0) {
+      fail(SW_ERR_CONFIG, std::string("GPU executor: ") + what + " = " + std::to_string(v) +
+                              " must be a multiple of 8 (16-byte TMA rows)");
+    }
+  }
+}
+
+void Model::allocate() {
+  const int64_t M = M_;
+  for (int dev : mesh_->local_devices()) {
+    Rank R;
+    R.device = dev;
+    R.dpi = mesh_->dp_index(dev);
+    R.mpi = mesh_->mp_index(dev);
+    R.p = alloc<float>(flat_n_);
+    R.g = alloc<float>(flat_n_);
+    R.m = alloc<float>(flat_n_);
+    R.v = alloc<float>(flat_n_);
+    R.w = alloc<bf16>(flat_n_);
+    cuda_check(cudaMemsetAsync(R.p, 0, flat_n_ * 4, stream_), "memset");
+    cuda_check(cudaMemsetAsync(R.g, 0, flat_n_ * 4, stream_), "memset");
+    cuda_check(cudaMemsetAsync(R.m, 0, flat_n_ * 4, stream_), "memset");
+    cuda_check(cudaMemsetAsync(R.v, 0, flat_n_ * 4, stream_), "memset");
+    cuda_check(cudaMemsetAsync(R.w, 0, flat_n_ * 2, stream_), "memset");
+    for (int l = 0; l <= L_; ++l) R.hs.push_back(alloc<float>(M * d_));
+    for (int l = 0; l < L_; ++l) {
+      R.hmid.push_back(alloc<float>(M * d_));
+      R.stats1.push_back(alloc<float>(2 * M));
+      R.stats2.push_back(alloc<float>(2 * M));
+      R.a1.push_back(alloc<bf16>(M * d_));
+      R.a2.push_back(alloc<bf16>(M * d_));
+      R.qkv.push_back(alloc<bf16>(M * 3 * dl_));
+      R.o.push_back(alloc<bf16>(M * dl_));
+      R.lse.push_back(alloc<float>(M * hl_));
+      R.pre.push_back(alloc<bf16>(M * fl_));
+      R.act.push_back(alloc<bf16>(M * fl_));
+    }
+    R.statsf = alloc<float>(2 * M);
+    R.f = alloc<bf16>(M * d_);
+    R.logits = alloc<bf16>(M * ldv_);
+    R.tokens = alloc<int32_t>(M);
+    R.targets = alloc<int32_t>(M);
+    R.weights = alloc<float>(M);
+    R.wloss = alloc<float>(M);
+    R.wsum = alloc<float>(1);
+    R.loss = alloc<double>(1);
+    R.part = alloc<float>(M * d_);
+    R.dx = alloc<float>(M * d_);
+    R.gres = alloc<float>(M * d_);
+    R.gb = alloc<bf16>(M * d_);
+    R.dpre = alloc<bf16>(M * fl_);
+    R.dout = alloc<bf16>(M * dl_);
+    R.dqkv = alloc<bf16>(M * 3 * dl_);
+    const int64_t chunks = (M + 255) / 256;
+    int64_t widest = d_;
+    if (3 * dl_ > widest) widest = 3 * dl_;
+    if (fl_ > widest) widest = fl_;
+    R.col_scratch = alloc<float>(chunks * widest);
+    R.attn_scratch = alloc<float>(M * hl_ + M * 2 * dl_);
+    ranks_.push_back(R);
+  }
+  d_flag_ = alloc<int>(1);
+  cuda_check(cudaStreamSynchronize(stream_), "allocate");
+}
+
+std::vector<Rank*> Model::replica(int dpi) {
+  std::vector<Rank*> g;
+  for (Rank& R : ranks_) {
+    if (R.dpi == dpi) g.push_back(&R);
+  }
+  return g;
+}
+
+// ---------------------------------------------------------------------------------------------
+// parameters
+// ---------------------------------------------------------------------------------------------
+void Model::init_params(uint64_t seed, const std::string& stream_name) {
+  const uint64_t key = mix64(seed ^ mix64(fnv1a(stream_name)));
+  for (Rank& R : ranks_) {
+    for (const Slot& s : slots_) {
+      float* dst = R.p + s.offset;
+      if (s.init == 0) {
+        cuda_check(cudaMemsetAsync(dst, 0, s.numel * 4, stream_), "memset");
+      } else if (s.init == 1) {
+        k::fill_f32(dst, s.numel, 1.0f, stream_);
+        ++launches_;
+      } else {
+        int64_t r0 = 0, c0 = 0;
+        if (s.layout.kind == Layout::kSplit) {
+          (s.layout.dim == 0 ? r0 : c0) = s.local[s.layout.dim] * R.mpi;
+        }
+        k::init_normal(dst, s.local[0], s.local[1], r0, c0, s.global[1], key, s.draw_base,
+                       s.init_scale, stream_);
+        ++launches_;
+      }
+    }
+    cuda_check(cudaMemsetAsync(R.m, 0, flat_n_ * 4, stream_), "memset");
+    cuda_check(cudaMemsetAsync(R.v, 0, flat_n_ * 4, stream_), "memset");
+    k::cast_f32_bf16(R.p, R.w, flat_n_, stream_);
+    ++launches_;
+  }
+  step_ = 0;
+  cuda_check(cudaGetLastError(), "init_params");
+}
+
+void Model::set_param(const std::string& name, const float* full, int64_t numel) {
+  const auto it = slot_of_.find(name);
+  if (it == slot_of_.end()) fail(SW_ERR_CONFIG, "TrainState: no parameter named '" + name + "'");
+  const Slot& s = slots_[it->second];
+  if (numel != numel_of(s.global)) {
+    fail(SW_ERR_SHAPE, "set_param: '" + name + "' expects " + std::to_string(numel_of(s.global)) +
+                           " elements, got " + std::to_string(numel));
+  }
+  for (Rank& R : ranks_) {
+    float* dst = R.p + s.offset;
+    if (s.layout.kind != Layout::kSplit) {
+      cuda_check(cudaMemcpyAsync(dst, full, numel * 4, cudaMemcpyHostToDevice, stream_), "H2D");
+    } else {
+      const int64_t rows = s.global[0], cols = s.global[1];
+      if (s.layout.dim == 0) {
+        const int64_t lr = s.local[0];
+        cuda_check(cudaMemcpyAsync(dst, full + R.mpi * lr * cols, lr * cols * 4, cudaMemcpyHostToDevice, stream_),
+                   "H2D");
+      } else {
+        const int64_t lc = s.local[1];
+        cuda_check(cudaMemcpy2DAsync(dst, lc * 4, full + R.mpi * lc, cols * 4, lc * 4, rows,
+                                     cudaMemcpyHostToDevice, stream_),
+                   "H2D 2D");
+      }
+    }
+    k::cast_f32_bf16(dst, R.w + s.offset, s.numel, stream_);
+  }
+  cuda_check(cudaStreamSynchronize(stream_), "set_param");
+}
+
+void Model::get_tensor(const std::string& name, int which, float* full, int64_t numel) {
+  const auto it = slot_of_.find(name);
+  if (it == slot_of_.end()) fail(SW_ERR_CONFIG, "TrainState: no parameter named '" + name + "'");
+  const Slot& s = slots_[it->second];
+  if (numel != numel_of(s.global)) {
+    fail(SW_ERR_SHAPE, "get_tensor: '" + name + "' has " + std::to_string(numel_of(s.global)) +
+                           " elements, got a buffer of " + std::to_string(numel));
+  }
+  auto base = [&](Rank& R) -> float* {
+    switch (which) {
+      case 0: return R.p;
+      case 1: return R.g;
+      case 2: return R.m;
+      case 3: return R.v;
+    }
+    fail(SW_ERR_CONFIG, "get_tensor: `which` must be 0..3");
+  };
+  cuda_check(cudaStreamSynchronize(stream_), "sync");
+  if (s.layout.kind != Layout::kSplit) {
+    Rank& R = *replica(mesh_->emulated ? 0 : ranks_[0].dpi)[0];
+    cuda_check(cudaMemcpy(full, base(R) + s.offset, numel * 4, cudaMemcpyDeviceToHost), "D2H");
+    return;
+  }
+  const int64_t rows = s.global[0], cols = s.global[1];
+  if (mesh_->emulated) {
+    for (Rank* R : replica(0)) {
+      const float* src = base(*R) + s.offset;
+      if (s.layout.dim == 0) {
+        cuda_check(cudaMemcpy(full + R->mpi * s.local[0] * cols, src, s.numel * 4, cudaMemcpyDeviceToHost), "D2H");
+      } else {
+        const int64_t lc = s.local[1];
+        cuda_check(cudaMemcpy2D(full + R->mpi * lc, cols * 4, src, lc * 4, lc * 4, rows, cudaMemcpyDeviceToHost),
+                   "D2H 2D");
+      }
+    }
+    return;
+  }
+  // NCCL mode: all-gather the shards of this replica's mp group (collective over mp ranks).
+  Rank& R = ranks_[0];
+  float* tmp = nullptr;
+  cuda_check(cudaMalloc(&tmp, numel * 4), "cudaMalloc");
+  nccl_check(ncclAllGather(base(R) + s.offset, tmp, s.numel, ncclFloat, mesh_->mp_comm, stream_), "AllGather");
+  std::vector<float> host(numel);
+  cuda_check(cudaMemcpyAsync(host.data(), tmp, numel * 4, cudaMemcpyDeviceToHost, stream_), "D2H");
+  cuda_check(cudaStreamSynchronize(stream_), "sync");
+  cudaFree(tmp);
+  const int t = mesh_->mp;
+  if (s.layout.dim == 0) {
+    std::memcpy(full, host.data(), numel * 4);
+  } else {
+    const int64_t lc = s.local[1];
+    for (int r = 0; r < t; ++r)
+      for (int64_t i = 0; i < rows; ++i)
+        std::memcpy(full + i * cols + r * lc, host.data() + r * s.numel + i * lc, lc * 4);
+  }
+}
+
+void Model::stage_batch(const int32_t* tokens, const int32_t* targets, const float* weights) {
+  for (Rank& R : ranks_) {
+    const int64_t off = static_cast<int64_t>(R.dpi) * M_;
+    cuda_check(cudaMemcpyAsync(R.tokens, tokens + off, M_ * 4, cudaMemcpyHostToDevice, stream_), "H2D");
+    cuda_check(cudaMemcpyAsync(R.targets, targets + off, M_ * 4, cudaMemcpyHostToDevice, stream_), "H2D");
+    if (weights != nullptr) {
+      cuda_check(cudaMemcpyAsync(R.weights, weights + off, M_ * 4, cudaMemcpyHostToDevice, stream_), "H2D");
+    } else {
+      k::fill_f32(R.weights, M_, 1.0f, stream_);
+      ++launches_;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// collectives
+// ---------------------------------------------------------------------------------------------
+void Model::ar_mp_ptrs(std::vector<Rank*>& grp, const std::vector<float*>& ptrs, int64_t n) {
+  if (mesh_->mp == 1) return;
+  if (mesh_->emulated) {
+    k::sum_ranks_f32(ptrs.data(), static_cast<int>(ptrs.size()), n, 1.0f, stream_);
+    ++launches_;
+  } else {
+    nccl_check(ncclAllReduce(ptrs[0], ptrs[0], n, ncclFloat, ncclSum, mesh_->mp_comm, stream_), "AllReduce");
+  }
+  mesh_->record(CollKind::kAllReduce, mesh_->mp_group(grp[0]->dpi), static_cast<uint64_t>(n) * 4);
+}
+
+void Model::ar_mp(std::vector<Rank*>& grp, float* Rank::*buf, int64_t n) {
+  std::vector<float*> ptrs;
+  for (Rank* R : grp) ptrs.push_back(R->*buf);
+  ar_mp_ptrs(grp, ptrs, n);
+}
+
+// In-place all-gather of a replicated 1-D slot's grad whose chunk `mpi` was produced locally.
+void Model::ag_mp_slot(std::vector<Rank*>& grp, int slot, int64_t chunk) {
+  if (mesh_->mp == 1) return;
+  const int t = mesh_->mp;
+  if (mesh_->emulated) {
+    for (Rank* src : grp) {
+      for (Rank* dst : grp) {
+        if (dst == src) continue;
+        cuda_check(cudaMemcpyAsync(G(*dst, slot) + src->mpi * chunk, G(*src, slot) + src->mpi * chunk,
+                                   chunk * 4, cudaMemcpyDeviceToDevice, stream_),
+                   "D2D");
+      }
+    }
+  } else {
+    Rank& R = *grp[0];
+    float* base = G(R, slot);
+    nccl_check(ncclAllGather(base + R.mpi * chunk, base, chunk, ncclFloat, mesh_->mp_comm, stream_), "AllGather");
+  }
+  mesh_->record(CollKind::kAllGather, mesh_->mp_group(grp[0]->dpi), static_cast<uint64_t>(chunk) * t * 4);
+}
+
+void Model::gemm(Rank& R, int M, int N, int K, const void* A, int64_t lda, int a_mn, const void* B,
+                 int64_t ldb, int b_mn, int epi, void* C, int64_t ldc, void* C2, int64_t ldc2,
+                 const float* bias, const void* aux, int64_t ld_aux, int accumulate, int bias_seg,
+                 int64_t bias_seg_stride) {
+  (void)R;
+  GemmParams p;
+  p.M = M;
+  p.N = N;
+  p.K = K;
+  p.A = A;
+  p.lda = lda;
+  p.a_mn_major = a_mn;
+  p.B = B;
+  p.ldb = ldb;
+  p.b_mn_major = b_mn;
+  p.epi = static_cast<Epi>(epi);
+  p.C = C;
+  p.ldc = ldc;
+  p.C2 = C2;
+  p.ldc2 = ldc2;
+  p.bias = bias;
+  p.bias_seg = bias_seg;
+  p.bias_seg_stride = bias_seg_stride;
+  p.aux = aux;
+  p.ld_aux = ld_aux;
+  p.accumulate = accumulate;
+  cuda_check(gemm_bf16(p, stream_), "gemm launch");
+  ++launches_;
+}
+
+// ---------------------------------------------------------------------------------------------
+// forward (transformer_logits + transformer_loss, model.hpp:76-152)
+// ---------------------------------------------------------------------------------------------
+void Model::forward_replica(std::vector<Rank*>& grp, bool need_grad) {
+  const int64_t M = M_;
+  const int d = d_, dl = dl_, fl = fl_;
+  for (Rank* R : grp) {
+    k::embed_fwd(R->tokens, P(*R, tok_), P(*R, pos_), R->hs[0], M, T_, d, stream_);
+    ++launches_;
+  }
+  for (int l = 0; l < L_; ++l) {
+    const LayerSlots& ls = layers_[l];
+    for (Rank* R : grp) {
+      k::layernorm_fwd(R->hs[l], P(*R, ls.ln1_s), P(*R, ls.ln1_b), R->a1[l], R->stats1[l], R->stats1[l] + M,
+                       M, d, 1e-5f, stream_);
+      ++launches_;
+      // column-parallel QKV (spmd.hpp:284-303): [M, d] x [3*dl, d]^T, bias slices of q|k|v
+      gemm(*R, static_cast<int>(M), 3 * dl, d, R->a1[l], d, 0, W(*R, ls.q_k), d, 0,
+           static_cast<int>(Epi::kStoreBf16), R->qkv[l], 3 * dl, nullptr, 0, P(*R, ls.q_b) + R->mpi * dl,
+           nullptr, 0, 0, dl, d);
+      k::attention_fwd(R->qkv[l], R->o[l], R->lse[l], B_, T_, hl_, hd_, stream_);
+      ++launches_;
+    }
+    // row-parallel O (spmd.hpp:305-324): local GEMM, all-reduce, then + bias (+ residual)
+    if (ta_ == 1) {
+      for (Rank* R : grp) {
+        gemm(*R, static_cast<int>(M), d, dl, R->o[l], dl, 0, W(*R, ls.o_k), dl, 0,
+             static_cast<int>(Epi::kResidF32), R->hmid[l], d, nullptr, 0, P(*R, ls.o_b), R->hs[l], d);
+      }
+    } else {
+      for (Rank* R : grp) {
+        gemm(*R, static_cast<int>(M), d, dl, R->o[l], dl, 0, W(*R, ls.o_k), dl, 0,
+             static_cast<int>(Epi::kStoreF32), R->part, d);
+      }
+      ar_mp(grp, &Rank::part, M * d);
+      for (Rank* R : grp) {
+        k::add_residual_bias(R->hs[l], R->part, P(*R, ls.o_b), R->hmid[l], M, d, stream_);
+        ++launches_;
+      }
+    }
+    for (Rank* R : grp) {
+      k::layernorm_fwd(R->hmid[l], P(*R, ls.ln2_s), P(*R, ls.ln2_b), R->a2[l], R->stats2[l], R->stats2[l] + M,
+                       M, d, 1e-5f, stream_);
+      ++launches_;
+      gemm(*R, static_cast<int>(M), fl, d, R->a2[l], d, 0, W(*R, ls.fc1_k), d, 0,
+           static_cast<int>(Epi::kBiasGelu), R->pre[l], fl, R->act[l], fl, P(*R, ls.fc1_b) + R->mpi * fl);
+    }
+    if (tm_ == 1) {
+      for (Rank* R : grp) {
+        gemm(*R, static_cast<int>(M), d, fl, R->act[l], fl, 0, W(*R, ls.fc2_k), fl, 0,
+             static_cast<int>(Epi::kResidF32), R->hs[l + 1], d, nullptr, 0, P(*R, ls.fc2_b), R->hmid[l], d);
+      }
+    } else {
+      for (Rank* R : grp) {
+        gemm(*R, static_cast<int>(M), d, fl, R->act[l], fl, 0, W(*R, ls.fc2_k), fl, 0,
+             static_cast<int>(Epi::kStoreF32), R->part, d);
+      }
+      ar_mp(grp, &Rank::part, M * d);
+      for (Rank* R : grp) {
+        k::add_residual_bias(R->hmid[l], R->part, P(*R, ls.fc2_b), R->hs[l + 1], M, d, stream_);
+        ++launches_;
+      }
+    }
+  }
+  const int head = head_ >= 0 ? head_ : tok_;
+  for (Rank* R : grp) {
+    k::layernorm_fwd(R->hs[L_], P(*R, lnf_s_), P(*R, lnf_b_), R->f, R->statsf, R->statsf + M, M, d, 1e-5f,
+                     stream_);
+    ++launches_;
+    // LM head (replicated under the reference plan: every rank computes all V columns)
+    gemm(*R, static_cast<int>(M), vl_, d, R->f, d, 0, W(*R, head), d, 0, static_cast<int>(Epi::kStoreBf16),
+         R->logits, ldv_);
+    k::sum_f32(R->weights, M, R->wsum, stream_);
+    k::xent_fwd_bwd(R->logits, ldv_, M, vl_, R->targets, R->weights, R->wsum, R->wloss, need_grad ? 1 : 0,
+                    stream_);
+    k::loss_reduce(R->wloss, M, R->wsum, R->loss, stream_);
+    launches_ += 3;
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// backward (the VJPs of autodiff.hpp, executed with the partition rules of spmd.hpp:342-387)
+// ---------------------------------------------------------------------------------------------
+void Model::backward_replica(std::vector<Rank*>& grp, bool accumulate) {
+  const int64_t M = M_;
+  const int d = d_, dl = dl_, fl = fl_;
+  const int acc = accumulate ? 1 : 0;
+  const bool tied = head_ < 0;
+  const int head = tied ? tok_ : head_;
+  // slots updated with atomics start from zero unless accumulating
+  if (!accumulate) {
+    for (Rank* R : grp) {
+      auto zero = [&](int s) {
+        cuda_check(cudaMemsetAsync(G(*R, s), 0, slots_[s].numel * 4, stream_), "memset");
+      };
+      for (const LayerSlots& ls : layers_) {
+        zero(ls.ln1_s);
+        zero(ls.ln1_b);
+        zero(ls.ln2_s);
+        zero(ls.ln2_b);
+      }
+      zero(lnf_s_);
+      zero(lnf_b_);
+      if (!tied) zero(tok_);
+      if (T_ < S_) {
+        cuda_check(cudaMemsetAsync(G(*R, pos_) + static_cast<int64_t>(T_) * d, 0,
+                                   static_cast<int64_t>(S_ - T_) * d * 4, stream_),
+                   "memset");
+      }
+    }
+  }
+  for (Rank* R : grp) {
+    // head: d(final_h) = dlogits . W_head ; dW_head (+)= dlogits^T . final_h
+    gemm(*R, static_cast<int>(M), d, vl_, R->logits, ldv_, 0, W(*R, head), d, 1,
+         static_cast<int>(Epi::kStoreF32), R->dx, d);
+    gemm(*R, vl_, d, static_cast<int>(M), R->logits, ldv_, 1, R->f, d, 1, static_cast<int>(Epi::kStoreF32),
+         G(*R, head), d, nullptr, 0, nullptr, nullptr, 0, acc);
+    k::layernorm_bwd(R->hs[L_], R->statsf, R->statsf + M, P(*R, lnf_s_), R->dx, R->gres, R->gb, G(*R, lnf_s_),
+                     G(*R, lnf_b_), M, d, 0, stream_);
+    ++launches_;
+  }
+  for (int l = L_ - 1; l >= 0; --l) {
+    const LayerSlots& ls = layers_[l];
+    // ---- MLP ----
+    for (Rank* R : grp) {
+      k::colsum_f32(R->gres, d, M, d, G(*R, ls.fc2_b), acc, R->col_scratch, stream_);
+      launches_ += 2;
+      gemm(*R, d, fl, static_cast<int>(M), R->gb, d, 1, R->act[l], fl, 1, static_cast<int>(Epi::kStoreF32),
+           G(*R, ls.fc2_k), fl, nullptr, 0, nullptr, nullptr, 0, acc);
+      gemm(*R, static_cast<int>(M), fl, d, R->gb, d, 0, W(*R, ls.fc2_k), fl, 1,
+           static_cast<int>(Epi::kGeluBwd), R->dpre, fl, nullptr, 0, nullptr, R->pre[l], fl);
+      k::colsum_bf16(R->dpre, fl, M, fl, 0, G(*R, ls.fc1_b) + R->mpi * fl, nullptr, nullptr, acc,
+                     R->col_scratch, stream_);
+      launches_ += 2;
+      gemm(*R, fl, d, static_cast<int>(M), R->dpre, fl, 1, R->a2[l], d, 1, static_cast<int>(Epi::kStoreF32),
+           G(*R, ls.fc1_k), d, nullptr, 0, nullptr, nullptr, 0, acc);
+      gemm(*R, static_cast<int>(M), d, fl, R->dpre, fl, 0, W(*R, ls.fc1_k), d, 1,
+           static_cast<int>(Epi::kStoreF32), R->dx, d);
+    }
+    if (tm_ > 1) ar_mp(grp, &Rank::dx, M * d);
+    for (Rank* R : grp) {
+      k::layernorm_bwd(R->hmid[l], R->stats2[l], R->stats2[l] + M, P(*R, ls.ln2_s), R->dx, R->gres, R->gb,
+                       G(*R, ls.ln2_s), G(*R, ls.ln2_b), M, d, 1, stream_);
+      ++launches_;
+    }
+    // ---- attention ----
+    for (Rank* R : grp) {
+      k::colsum_f32(R->gres, d, M, d, G(*R, ls.o_b), acc, R->col_scratch, stream_);
+      launches_ += 2;
+      gemm(*R, d, dl, static_cast<int>(M), R->gb, d, 1, R->o[l], dl, 1, static_cast<int>(Epi::kStoreF32),
+           G(*R, ls.o_k), dl, nullptr, 0, nullptr, nullptr, 0, acc);
+      gemm(*R, static_cast<int>(M), dl, d, R->gb, d, 0, W(*R, ls.o_k), dl, 1,
+           static_cast<int>(Epi::kStoreBf16), R->dout, dl);
+      k::attention_bwd(R->qkv[l], R->o[l], R->lse[l], R->dout, R->dqkv, R->attn_scratch, B_, T_, hl_, hd_,
+                       stream_);
+      launches_ += 3;
+      k::colsum_bf16(R->dqkv, 3 * dl, M, 3 * dl, dl, G(*R, ls.q_b) + R->mpi * dl, G(*R, ls.k_b) + R->mpi * dl,
+                     G(*R, ls.v_b) + R->mpi * dl, acc, R->col_scratch, stream_);
+      launches_ += 2;
+      gemm(*R, 3 * dl, d, static_cast<int>(M), R->dqkv, 3 * dl, 1, R->a1[l], d, 1,
+           static_cast<int>(Epi::kStoreF32), G(*R, ls.q_k), d, nullptr, 0, nullptr, nullptr, 0, acc);
+      gemm(*R, static_cast<int>(M), d, 3 * dl, R->dqkv, 3 * dl, 0, W(*R, ls.q_k), d, 1,
+           static_cast<int>(Epi::kStoreF32), R->dx, d);
+    }
+    if (ta_ > 1) ar_mp(grp, &Rank::dx, M * d);
+    for (Rank* R : grp) {
+      k::layernorm_bwd(R->hs[l], R->stats1[l], R->stats1[l] + M, P(*R, ls.ln1_s), R->dx, R->gres, R->gb,
+                       G(*R, ls.ln1_s), G(*R, ls.ln1_b), M, d, 1, stream_);
+      ++launches_;
+    }
+  }
+  for (Rank* R : grp) {
+    k::embed_bwd_pos(R->gres, G(*R, pos_), B_, T_, d, acc, stream_);
+    k::embed_bwd_tok(R->tokens, R->gres, G(*R, tok_), M, d, stream_);
+    launches_ += 2;
+  }
+  // column-parallel biases are replicated parameters: gather their gradient chunks
+  // (the to_partition coercion of spmd.hpp:803-812).
+  for (const LayerSlots& ls : layers_) {
+    if (ta_ > 1) {
+      ag_mp_slot(grp, ls.q_b, dl);
+      ag_mp_slot(grp, ls.k_b, dl);
+      ag_mp_slot(grp, ls.v_b, dl);
+    }
+    if (tm_ > 1) ag_mp_slot(grp, ls.fc1_b, fl);
+  }
+}
+
+void Model::forward_backward(bool accumulate) {
+  cuda_check(cudaSetDevice(mesh_->cuda_device), "cudaSetDevice");
+  launches_ = 0;
+  const int first = mesh_->emulated ? 0 : ranks_[0].dpi;
+  const int last = mesh_->emulated ? mesh_->dp - 1 : ranks_[0].dpi;
+  for (int r = first; r <= last; ++r) {
+    std::vector<Rank*> grp = replica(r);
+    forward_replica(grp, true);
+    backward_replica(grp, accumulate);
+  }
+  cuda_check(cudaGetLastError(), "forward_backward");
+}
+
+void Model::forward_only() {
+  cuda_check(cudaSetDevice(mesh_->cuda_device), "cudaSetDevice");
+  const int first = mesh_->emulated ? 0 : ranks_[0].dpi;
+  const int last = mesh_->emulated ? mesh_->dp - 1 : ranks_[0].dpi;
+  for (int r = first; r <= last; ++r) {
+    std::vector<Rank*> grp = replica(r);
+    forward_replica(grp, false);
+  }
+  cuda_check(cudaGetLastError(), "forward");
+}
+
+void Model::scale_grads(double factor) {
+  for (Rank& R : ranks_) {
+    k::scale_f32(R.g, flat_n_, static_cast<float>(factor), stream_);
+    ++launches_;
+  }
+}
+
+void Model::dp_sync() {
+  if (mesh_->dp == 1) return;
+  const float inv = 1.0f / static_cast<float>(mesh_->dp);
+  for (int j = 0; j < mesh_->mp; ++j) {
+    if (mesh_->emulated) {
+      std::vector<float*> ptrs;
+      for (int id : mesh_->dp_group(j)) ptrs.push_back(ranks_[id].g);
+      k::sum_ranks_f32(ptrs.data(), static_cast<int>(ptrs.size()), flat_n_, inv, stream_);
+      ++launches_;
+    } else if (ranks_[0].mpi == j) {
+      nccl_check(ncclAllReduce(ranks_[0].g, ranks_[0].g, flat_n_, ncclFloat, ncclSum, mesh_->dp_comm, stream_),
+                 "AllReduce(dp)");
+      k::scale_f32(ranks_[0].g, flat_n_, inv, stream_);
+      ++launches_;
+    }
+    mesh_->record(CollKind::kAllReduce, mesh_->dp_group(j), static_cast<uint64_t>(flat_n_) * 4);
+  }
+}
+
+void Model::adamw(double lr, double b1, double b2, double eps, double wd, bool check_finite) {
+  if (check_finite) {
+    cuda_check(cudaMemsetAsync(d_flag_, 0, sizeof(int), stream_), "memset");
+    for (Rank& R : ranks_) {
+      k::nonfinite_check(R.g, flat_n_, d_flag_, stream_);
+      ++launches_;
+    }
+    int flag = 0;
+    cuda_check(cudaMemcpyAsync(&flag, d_flag_, sizeof(int), cudaMemcpyDeviceToHost, stream_), "D2H");
+    cuda_check(cudaStreamSynchronize(stream_), "sync");
+    if (flag) {
+      // slow path: name the first offending parameter like train_state.hpp:207-210
+      std::vector<float> host;
+      for (const Slot& s : slots_) {
+        for (Rank& R : ranks_) {
+          host.resize(s.numel);
+          cuda_check(cudaMemcpy(host.data(), R.g + s.offset, s.numel * 4, cudaMemcpyDeviceToHost), "D2H");
+          for (float x : host) {
+            if (!std::isfinite(x)) {
+              fail(SW_ERR_NONFINITE, "adamw_step: non-finite gradient for parameter '" + s.name + "'");
+            }
+          }
+        }
+      }
+      fail(SW_ERR_NONFINITE, "adamw_step: non-finite gradient");
+    }
+  }
+  const double t = static_cast<double>(step_ + 1);
+  const float c1 = static_cast<float>(1.0 - std::pow(b1, t));
+  const float c2 = static_cast<float>(1.0 - std::pow(b2, t));
+  for (Rank& R : ranks_) {
+    k::adamw(R.p, R.m, R.v, R.g, R.w, flat_n_, static_cast<float>(lr), static_cast<float>(b1),
+             static_cast<float>(b2), static_cast<float>(eps), static_cast<float>(wd), c1, c2, stream_);
+    ++launches_;
+  }
+  ++step_;
+  cuda_check(cudaGetLastError(), "adamw");
+}
+
+double Model::last_loss() {
+  cuda_check(cudaStreamSynchronize(stream_), "sync");
+  double sum = 0.0;
+  int n = 0;
+  for (Rank& R : ranks_) {
+    if (R.mpi != 0) continue;
+    double x = 0.0;
+    cuda_check(cudaMemcpy(&x, R.loss, sizeof(double), cudaMemcpyDeviceToHost), "D2H");
+    sum += x;
+    ++n;
+  }
+  if (!mesh_->emulated && mesh_->dp > 1) {
+    // mean over replicas: every rank contributes its replica's loss once per mp column
+    double* tmp = nullptr;
+    cuda_check(cudaMalloc(&tmp, sizeof(double)), "cudaMalloc");
+    double x = 0.0;
+    cuda_check(cudaMemcpy(&x, ranks_[0].loss, sizeof(double), cudaMemcpyDeviceToHost), "D2H");
+    cuda_check(cudaMemcpy(tmp, &x, sizeof(double), cudaMemcpyHostToDevice), "H2D");
+    nccl_check(ncclAllReduce(tmp, tmp, 1, ncclDouble, ncclSum, mesh_->dp_comm, stream_), "AllReduce(loss)");
+    cuda_check(cudaMemcpyAsync(&x, tmp, sizeof(double), cudaMemcpyDeviceToHost, stream_), "D2H");
+    cuda_check(cudaStreamSynchronize(stream_), "sync");
+    cudaFree(tmp);
+    return x / mesh_->dp;
+  }
+  return n > 0 ? sum / n : 0.0;
+}
+
+void Model::logits_to_host(float* out) {
+  cuda_check(cudaStreamSynchronize(stream_), "sync");
+  std::vector<bf16> tmp(static_cast<size_t>(M_ * ldv_));
+  const int first = mesh_->emulated ? 0 : ranks_[0].dpi;
+  const int last = mesh_->emulated ? mesh_->dp - 1 : ranks_[0].dpi;
+  for (int r = first; r <= last; ++r) {
+    Rank& R = *replica(r)[0];
+    cuda_check(cudaMemcpy(tmp.data(), R.logits, tmp.size() * 2, cudaMemcpyDeviceToHost), "D2H");
+    float* o = out + (mesh_->emulated ? static_cast<int64_t>(r) * M_ * V_ : 0);
+    for (int64_t i = 0; i < M_; ++i)
+      for (int j = 0; j < V_; ++j) o[i * V_ + j] = __bfloat162float(tmp[i * ldv_ + j]);
+  }
+}
+
+}  // namespace sw

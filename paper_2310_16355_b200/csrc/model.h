@@ -1,0 +1,129 @@
+// GPU executor of the tensor-parallel transformer step.
+//
+// Replaces, for the transformer_loss program (model.hpp:144-152), the reference's
+// SpmdInterpreter::run / spmd_forward_backward (spmd.hpp:96-119, :782-814), the shard
+// materialiser shard_params / replica_param_views / gather_params (train_state.hpp:50-110),
+// dp_sync_grads (:155-170) and adamw_step (:183-220).
+//
+// Per device ("rank") the state is five flat buffers over that rank's parameter shards
+// (fp32 master params, grads, Adam m, Adam v; bf16 shadow for the GEMMs), laid out so that
+// every GEMM operand is one contiguous, TMA-addressable matrix: the q, k, v kernel shards of a
+// layer are adjacent ([3*d/t, d] fused QKV) and their replicated biases are adjacent ([3*d]).
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "mesh.h"
+#include "rules.h"
+
+namespace sw {
+
+using bf16 = __nv_bfloat16;
+
+struct Slot {
+  std::string name;
+  Dims global, local;
+  Layout layout;
+  int64_t begin = 0, end = 0;  // owned range along the split dim
+  int64_t offset = 0;          // element offset in the rank's flat buffers
+  int64_t numel = 0;           // local elements
+  int init = 0;                // 0 zeros, 1 ones, 2 normal
+  double init_scale = 0.0;
+  uint64_t draw_base = 0;      // counter of the slot's first draw in the init stream
+};
+
+struct LayerSlots {
+  int ln1_s, ln1_b, q_k, k_k, v_k, q_b, k_b, v_b, o_k, o_b, ln2_s, ln2_b, fc1_k, fc1_b, fc2_k, fc2_b;
+};
+
+struct Rank {
+  int device = 0, dpi = 0, mpi = 0;
+  float *p = nullptr, *g = nullptr, *m = nullptr, *v = nullptr;
+  bf16* w = nullptr;
+  // activations saved for the backward, per layer
+  std::vector<float*> hs, hmid, stats1, stats2;  // stats: mean[M] | rstd[M]
+  std::vector<bf16*> a1, a2, qkv, o, pre, act;
+  std::vector<float*> lse;
+  float* statsf = nullptr;
+  bf16* f = nullptr;
+  bf16* logits = nullptr;
+  // inputs
+  int32_t *tokens = nullptr, *targets = nullptr;
+  float* weights = nullptr;
+  float *wloss = nullptr, *wsum = nullptr;
+  double* loss = nullptr;
+  // scratch
+  float *part = nullptr, *dx = nullptr, *gres = nullptr, *col_scratch = nullptr, *attn_scratch = nullptr;
+  bf16 *gb = nullptr, *dpre = nullptr, *dout = nullptr, *dqkv = nullptr;
+};
+
+class Model {
+ public:
+  Model(const ModelSpec& spec, const Plan& plan, Mesh* mesh, int batch, int seq_len);
+  ~Model();
+
+  void init_params(uint64_t seed, const std::string& stream_name);
+  void set_param(const std::string& name, const float* full, int64_t numel);
+  void get_tensor(const std::string& name, int which, float* full, int64_t numel);
+  void stage_batch(const int32_t* tokens, const int32_t* targets, const float* weights);
+  void forward_backward(bool accumulate);
+  void forward_only();
+  void scale_grads(double factor);
+  void dp_sync();
+  void adamw(double lr, double b1, double b2, double eps, double wd, bool check_finite);
+  double last_loss();
+  void logits_to_host(float* out);
+
+  cudaStream_t stream() const { return stream_; }
+  int64_t launches() const { return launches_; }
+  void reset_launches() { launches_ = 0; }
+  int64_t device_bytes() const { return bytes_; }
+
+ private:
+  template <typename T>
+  T* alloc(int64_t n);
+  void build_layout();
+  void allocate();
+  std::vector<Rank*> replica(int dpi);
+  void forward_replica(std::vector<Rank*>& grp, bool need_grad);
+  void backward_replica(std::vector<Rank*>& grp, bool accumulate);
+  void ar_mp(std::vector<Rank*>& grp, float* Rank::*buf, int64_t n);
+  void ar_mp_ptrs(std::vector<Rank*>& grp, const std::vector<float*>& ptrs, int64_t n);
+  void ag_mp_slot(std::vector<Rank*>& grp, int slot, int64_t chunk);
+  void gemm(Rank& R, int M, int N, int K, const void* A, int64_t lda, int a_mn, const void* B,
+            int64_t ldb, int b_mn, int epi, void* C, int64_t ldc, void* C2 = nullptr,
+            int64_t ldc2 = 0, const float* bias = nullptr, const void* aux = nullptr,
+            int64_t ld_aux = 0, int accumulate = 0, int bias_seg = 0, int64_t bias_seg_stride = 0);
+  float* P(Rank& R, int slot) { return R.p + slots_[slot].offset; }
+  float* G(Rank& R, int slot) { return R.g + slots_[slot].offset; }
+  bf16* W(Rank& R, int slot) { return R.w + slots_[slot].offset; }
+
+  ModelSpec spec_;
+  Plan plan_;
+  Mesh* mesh_;
+  int B_, T_;
+  int64_t M_;
+  int L_, d_, H_, hd_, dff_, V_, S_;
+  int ta_ = 1, tm_ = 1, th_ = 1;  // TP degree of attention, MLP, LM head (1 = replicated)
+  int dl_, hl_, fl_, vl_, ldv_;
+  std::vector<Slot> slots_;
+  std::unordered_map<std::string, int> slot_of_;
+  std::vector<LayerSlots> layers_;
+  int tok_ = -1, pos_ = -1, lnf_s_ = -1, lnf_b_ = -1, head_ = -1;
+  int64_t flat_n_ = 0;
+  std::vector<Rank> ranks_;
+  std::vector<void*> allocations_;
+  cudaStream_t stream_ = nullptr;
+  int* d_flag_ = nullptr;
+  int64_t launches_ = 0;
+  int64_t bytes_ = 0;
+  uint64_t step_ = 0;
+};
+
+}  // namespace sw
