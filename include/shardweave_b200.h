@@ -203,6 +203,31 @@ SW_API sw_status sw_k_gemm_bf16(int M, int N, int K, const void* A, int64_t lda,
                          void* C2, int64_t ldc2, const float* bias, const void* aux,
                          int64_t ld_aux, float alpha, int accumulate, void* stream);
 
+/* Causal attention over head-sharded activations (graph.hpp:650-661 + model.hpp:100-106):
+ * qkv [B*T, 3*Hl*hd] bf16 (q | k | v), o [B*T, Hl*hd] bf16, lse [B, Hl, T] fp32. */
+SW_API sw_status sw_k_attention_fwd(const void* qkv, void* o, float* lse, int B, int T, int Hl,
+                                    int hd, void* stream);
+/* dqkv [B*T, 3*Hl*hd] bf16; scratch fp32 of B*T*Hl + B*T*2*Hl*hd elements. */
+SW_API sw_status sw_k_attention_bwd(const void* qkv, const void* o, const float* lse,
+                                    const void* dout, void* dqkv, float* scratch, int B, int T,
+                                    int Hl, int hd, void* stream);
+/* LayerNorm (kernels.hpp:184-271): y bf16, mean/rstd fp32 [M]. */
+SW_API sw_status sw_k_layernorm_fwd(const float* x, const float* scale, const float* bias, void* y,
+                                    float* mean, float* rstd, int64_t M, int d, float eps,
+                                    void* stream);
+SW_API sw_status sw_k_layernorm_bwd(const float* x, const float* mean, const float* rstd,
+                                    const float* scale, const float* dy, float* g_io, void* g_bf16,
+                                    float* dscale, float* dbias, int64_t M, int d, int accumulate,
+                                    void* stream);
+/* Fused softmax cross entropy fwd+bwd over bf16 logits [M, ld] (kernels.hpp:327-363). */
+SW_API sw_status sw_k_xent(void* logits, int64_t ld, int64_t M, int V, const int32_t* targets,
+                           const float* weights, const float* wsum, float* wloss, int write_grad,
+                           void* stream);
+/* AdamW over a flat shard (train_state.hpp:211-216), bf16 shadow refresh. */
+SW_API sw_status sw_k_adamw(float* p, float* m, float* v, const float* g, void* shadow, int64_t n,
+                            float lr, float b1, float b2, float eps, float wd, float c1, float c2,
+                            void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -49,8 +49,23 @@ def _softmax(x):
     return e / e.sum(-1, keepdims=True)
 
 
-def forward_backward(params: dict, spec: dict, tokens, targets, weights, need_grads=True):
-    """Returns (loss, grads dict, logits). tokens/targets int [B,T], weights [B,T]."""
+def bf16_round(x):
+    """Round-to-nearest-even to bfloat16, returned as float64."""
+    a = np.asarray(x, np.float32)
+    u = a.view(np.uint32).astype(np.uint64)
+    u = ((u + 0x7FFF + ((u >> 16) & 1)) >> 16) << 16
+    return u.astype(np.uint32).view(np.float32).astype(np.float64)
+
+
+def forward_backward(params: dict, spec: dict, tokens, targets, weights, need_grads=True,
+                     bf16_acts=False):
+    """Returns (loss, grads dict, logits). tokens/targets int [B,T], weights [B,T].
+
+    bf16_acts=True rounds every GEMM operand that a bf16 tensor-core implementation stores in
+    bf16 (LayerNorm outputs, q/k/v, attention output, GeLU input/output, logits and the
+    backward's dlogits / residual-gradient / dpre / d(attn out) / dqkv), so a bf16 device run
+    can be checked at a tolerance set by accumulation order rather than storage rounding."""
+    R = bf16_round if bf16_acts else (lambda x: x)
     B, T = tokens.shape
     d, H, L = spec["d_model"], spec["n_heads"], spec["n_layers"]
     hd = d // H
@@ -62,26 +77,32 @@ def forward_backward(params: dict, spec: dict, tokens, targets, weights, need_gr
     for l in range(L):
         pre = f"block_{l}/"
         a, xh1, r1 = layer_norm(h, p[pre + "ln1/scale"], p[pre + "ln1/bias"])
+        a = R(a)
 
         def proj(name):
-            y = a @ p[pre + f"attn/{name}/kernel"].T + p[pre + f"attn/{name}/bias"]
+            y = R(a @ p[pre + f"attn/{name}/kernel"].T + p[pre + f"attn/{name}/bias"])
             return y.reshape(B, T, H, hd).transpose(0, 2, 1, 3)
 
         q, k, v = proj("q"), proj("k"), proj("v")
         s = q @ k.transpose(0, 1, 3, 2) * (1.0 / math.sqrt(hd)) + mask
         P = _softmax(s)
         att = P @ v
-        merged = att.transpose(0, 2, 1, 3).reshape(B, T, d)
+        merged = R(att.transpose(0, 2, 1, 3).reshape(B, T, d))
         h_mid = h + merged @ p[pre + "attn/o/kernel"].T + p[pre + "attn/o/bias"]
         m, xh2, r2 = layer_norm(h_mid, p[pre + "ln2/scale"], p[pre + "ln2/bias"])
-        up = m @ p[pre + "mlp/fc1/kernel"].T + p[pre + "mlp/fc1/bias"]
-        g = gelu(up)
+        m = R(m)
+        up_full = m @ p[pre + "mlp/fc1/kernel"].T + p[pre + "mlp/fc1/bias"]
+        g = R(gelu(up_full))
+        up = R(up_full)
         h_out = h_mid + g @ p[pre + "mlp/fc2/kernel"].T + p[pre + "mlp/fc2/bias"]
         cache.append((a, xh1, r1, q, k, v, P, merged, m, xh2, r2, up, g))
         h = h_out
     f, xhf, rf = layer_norm(h, p["final_ln/scale"], p["final_ln/bias"])
+    f = R(f)
     W_head = p["embed/tok/kernel"] if tied else p["lm_head/kernel"]
-    logits = f @ W_head.T
+    if bf16_acts:
+        W_head = bf16_round(W_head)
+    logits = R(f @ W_head.T)
     mx = logits.max(-1, keepdims=True)
     lse = mx[..., 0] + np.log(np.exp(logits - mx).sum(-1))
     ce = lse - np.take_along_axis(logits, targets[..., None], -1)[..., 0]
@@ -95,6 +116,7 @@ def forward_backward(params: dict, spec: dict, tokens, targets, weights, need_gr
     np.put_along_axis(dlogits, targets[..., None],
                       np.take_along_axis(dlogits, targets[..., None], -1) - 1.0, -1)
     dlogits *= (weights / wsum)[..., None]
+    dlogits = R(dlogits)
     V = logits.shape[-1]
     dW_head = dlogits.reshape(-1, V).T @ f.reshape(-1, d)
     df = dlogits @ W_head
@@ -102,27 +124,31 @@ def forward_backward(params: dict, spec: dict, tokens, targets, weights, need_gr
     for l in reversed(range(L)):
         pre = f"block_{l}/"
         a, xh1, r1, q, k, v, P, merged, m, xh2, r2, up, g = cache[l]
-        dflat = dh.reshape(-1, d)
+        dflat = R(dh.reshape(-1, d))
         grads[pre + "mlp/fc2/kernel"] = dflat.T @ g.reshape(-1, g.shape[-1])
-        grads[pre + "mlp/fc2/bias"] = dflat.sum(0)
-        dup = (dh @ p[pre + "mlp/fc2/kernel"]) * gelu_grad(up)
+        grads[pre + "mlp/fc2/bias"] = dh.reshape(-1, d).sum(0)
+        dup = R((dflat.reshape(dh.shape) @ p[pre + "mlp/fc2/kernel"]) * gelu_grad(up))
         grads[pre + "mlp/fc1/kernel"] = dup.reshape(-1, dup.shape[-1]).T @ m.reshape(-1, d)
         grads[pre + "mlp/fc1/bias"] = dup.reshape(-1, dup.shape[-1]).sum(0)
         dm = dup @ p[pre + "mlp/fc1/kernel"]
         dx, grads[pre + "ln2/scale"], grads[pre + "ln2/bias"] = layer_norm_bwd(xh2, r2, p[pre + "ln2/scale"], dm)
         dh = dh + dx
-        dflat = dh.reshape(-1, d)
+        dflat = R(dh.reshape(-1, d))
         grads[pre + "attn/o/kernel"] = dflat.T @ merged.reshape(-1, d)
-        grads[pre + "attn/o/bias"] = dflat.sum(0)
-        datt = (dh @ p[pre + "attn/o/kernel"]).reshape(B, T, H, hd).transpose(0, 2, 1, 3)
+        grads[pre + "attn/o/bias"] = dh.reshape(-1, d).sum(0)
+        datt = R(dflat.reshape(dh.shape) @ p[pre + "attn/o/kernel"]).reshape(B, T, H, hd).transpose(0, 2, 1, 3)
         dP = datt @ v.transpose(0, 1, 3, 2)
         dv = P.transpose(0, 1, 3, 2) @ datt
-        dS = P * (dP - (dP * P).sum(-1, keepdims=True)) * (1.0 / math.sqrt(hd))
+        if bf16_acts:  # flash-style: delta = rowsum(dO * O) with the stored (bf16) O
+            delta = (datt * merged.reshape(B, T, H, hd).transpose(0, 2, 1, 3)).sum(-1, keepdims=True)
+        else:
+            delta = (dP * P).sum(-1, keepdims=True)
+        dS = P * (dP - delta) * (1.0 / math.sqrt(hd))
         dq = dS @ k
         dk = dS.transpose(0, 1, 3, 2) @ q
         da = np.zeros_like(a)
         for name, dy in (("q", dq), ("k", dk), ("v", dv)):
-            dyf = dy.transpose(0, 2, 1, 3).reshape(-1, d)
+            dyf = R(dy.transpose(0, 2, 1, 3).reshape(-1, d))
             grads[pre + f"attn/{name}/kernel"] = dyf.T @ a.reshape(-1, d)
             grads[pre + f"attn/{name}/bias"] = dyf.sum(0)
             da += (dyf @ p[pre + f"attn/{name}/kernel"]).reshape(B, T, d)

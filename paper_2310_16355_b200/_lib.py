@@ -95,3 +95,12 @@ def _declare(L: C.CDLL) -> None:
     L.sw_k_gemm_bf16.argtypes = [C.c_int, C.c_int, C.c_int, vp, i64, C.c_int, vp, i64, C.c_int,
                                  C.c_int, vp, i64, vp, i64, vp, vp, i64, f32, C.c_int, vp]
     L.sw_k_gemm_bf16.restype = C.c_int
+    L.sw_k_attention_fwd.argtypes = [vp, vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, vp]
+    L.sw_k_attention_bwd.argtypes = [vp, vp, vp, vp, vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, vp]
+    L.sw_k_layernorm_fwd.argtypes = [vp, vp, vp, vp, vp, vp, i64, C.c_int, f32, vp]
+    L.sw_k_layernorm_bwd.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, vp, i64, C.c_int, C.c_int, vp]
+    L.sw_k_xent.argtypes = [vp, i64, i64, C.c_int, vp, vp, vp, vp, C.c_int, vp]
+    L.sw_k_adamw.argtypes = [vp, vp, vp, vp, vp, i64, f32, f32, f32, f32, f32, f32, f32, vp]
+    for fn in ("sw_k_attention_fwd", "sw_k_attention_bwd", "sw_k_layernorm_fwd",
+               "sw_k_layernorm_bwd", "sw_k_xent", "sw_k_adamw"):
+        getattr(L, fn).restype = C.c_int

@@ -3,6 +3,7 @@
 #include <string>
 
 #include "gemm.h"
+#include "kernels.h"
 #include "status.h"
 
 namespace sw {
@@ -50,6 +51,62 @@ sw_status sw_k_gemm_bf16(int M, int N, int K, const void* A, int64_t lda, int a_
     p.alpha = alpha;
     p.accumulate = accumulate;
     sw::cuda_check(sw::gemm_bf16(p, static_cast<cudaStream_t>(stream)), "gemm_bf16 launch");
+  });
+}
+
+sw_status sw_k_attention_fwd(const void* qkv, void* o, float* lse, int B, int T, int Hl, int hd,
+                             void* stream) {
+  return sw::guarded([&] {
+    sw::k::attention_fwd(static_cast<const sw::k::bf16*>(qkv), static_cast<sw::k::bf16*>(o), lse, B, T, Hl,
+                         hd, static_cast<cudaStream_t>(stream));
+    sw::cuda_check(cudaGetLastError(), "attention_fwd");
+  });
+}
+
+sw_status sw_k_attention_bwd(const void* qkv, const void* o, const float* lse, const void* dout,
+                             void* dqkv, float* scratch, int B, int T, int Hl, int hd, void* stream) {
+  return sw::guarded([&] {
+    sw::k::attention_bwd(static_cast<const sw::k::bf16*>(qkv), static_cast<const sw::k::bf16*>(o), lse,
+                         static_cast<const sw::k::bf16*>(dout), static_cast<sw::k::bf16*>(dqkv), scratch, B, T,
+                         Hl, hd, static_cast<cudaStream_t>(stream));
+    sw::cuda_check(cudaGetLastError(), "attention_bwd");
+  });
+}
+
+sw_status sw_k_layernorm_fwd(const float* x, const float* scale, const float* bias, void* y, float* mean,
+                             float* rstd, int64_t M, int d, float eps, void* stream) {
+  return sw::guarded([&] {
+    sw::k::layernorm_fwd(x, scale, bias, static_cast<sw::k::bf16*>(y), mean, rstd, M, d, eps,
+                         static_cast<cudaStream_t>(stream));
+    sw::cuda_check(cudaGetLastError(), "layernorm_fwd");
+  });
+}
+
+sw_status sw_k_layernorm_bwd(const float* x, const float* mean, const float* rstd, const float* scale,
+                             const float* dy, float* g_io, void* g_bf16, float* dscale, float* dbias,
+                             int64_t M, int d, int accumulate, void* stream) {
+  return sw::guarded([&] {
+    sw::k::layernorm_bwd(x, mean, rstd, scale, dy, g_io, static_cast<sw::k::bf16*>(g_bf16), dscale, dbias, M,
+                         d, accumulate, static_cast<cudaStream_t>(stream));
+    sw::cuda_check(cudaGetLastError(), "layernorm_bwd");
+  });
+}
+
+sw_status sw_k_xent(void* logits, int64_t ld, int64_t M, int V, const int32_t* targets, const float* weights,
+                    const float* wsum, float* wloss, int write_grad, void* stream) {
+  return sw::guarded([&] {
+    sw::k::xent_fwd_bwd(static_cast<sw::k::bf16*>(logits), ld, M, V, targets, weights, wsum, wloss, write_grad,
+                        static_cast<cudaStream_t>(stream));
+    sw::cuda_check(cudaGetLastError(), "xent");
+  });
+}
+
+sw_status sw_k_adamw(float* p, float* m, float* v, const float* g, void* shadow, int64_t n, float lr,
+                     float b1, float b2, float eps, float wd, float c1, float c2, void* stream) {
+  return sw::guarded([&] {
+    sw::k::adamw(p, m, v, g, static_cast<sw::k::bf16*>(shadow), n, lr, b1, b2, eps, wd, c1, c2,
+                 static_cast<cudaStream_t>(stream));
+    sw::cuda_check(cudaGetLastError(), "adamw");
   });
 }
 
