@@ -187,6 +187,13 @@ SW_API sw_status sw_model_forward_logits(sw_model* model, float* logits_out);
 SW_API sw_status sw_model_stream(sw_model* model, void** stream_out);
 /* Number of kernel launches issued by the last forward_backward/adamw/train_step call. */
 SW_API sw_status sw_model_launch_count(sw_model* model, int64_t* out);
+/* Per-launch device timing with CUDA events on the model stream (categories: 0 GEMM,
+ * 1 attention fwd, 2 attention bwd, 3 LayerNorm, 4 cross entropy, 5 AdamW, 6 collectives,
+ * 7 other). read_profile returns, per category since the last read: device ms, algorithmic
+ * work (FLOPs for 0-2, HBM bytes for 3-5, bus bytes for 6) and launch count. */
+SW_API sw_status sw_model_set_profiling(sw_model* model, int enable);
+SW_API sw_status sw_model_read_profile(sw_model* model, double ms[8], double work[8],
+                                       int64_t count[8]);
 /* Bytes of device memory held by this process's model state and activations. */
 SW_API sw_status sw_model_device_bytes(sw_model* model, int64_t* out);
 

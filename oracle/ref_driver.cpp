@@ -13,6 +13,10 @@
 //                                                    audit-style trajectory dump (cli.cpp:179-240)
 //   bench <spec> <mp> <batch> <seq> <steps> <threads>   CPU timing of spmd_forward_backward+AdamW
 #include <chrono>
+#include <cstdlib>
+#include <mutex>
+#include <new>
+#include <unordered_map>
 #include <cstdio>
 #include <cstring>
 #include <fstream>
@@ -30,6 +34,56 @@
 #include "shardweave/train_state.hpp"
 
 using namespace shardweave;
+
+// The reference allocates a fresh std::vector for every op result (tensor.hpp value semantics);
+// at full model width that is hundreds of MB per op, and glibc returns every such block to the
+// OS (mmap/munmap + page faults dominated the CPU time). Real deployments would sit on a
+// caching allocator, so this driver provides one: large blocks are kept in per-size free
+// lists and reused. Arithmetic is untouched.
+namespace {
+constexpr std::size_t kCacheMin = 1 << 20;
+struct BlockCache {
+  std::mutex mu;
+  std::unordered_map<std::size_t, std::vector<void*>> free_;
+};
+BlockCache& block_cache() {
+  static BlockCache* c = new BlockCache();
+  return *c;
+}
+}  // namespace
+
+void* operator new(std::size_t n) {
+  const std::size_t total = n + 64;
+  if (n >= kCacheMin) {
+    BlockCache& c = block_cache();
+    std::lock_guard<std::mutex> lock(c.mu);
+    auto it = c.free_.find(total);
+    if (it != c.free_.end() && !it->second.empty()) {
+      void* p = it->second.back();
+      it->second.pop_back();
+      return static_cast<char*>(p) + 64;
+    }
+  }
+  void* p = std::malloc(total);
+  if (p == nullptr) throw std::bad_alloc();
+  *static_cast<std::size_t*>(p) = total;
+  return static_cast<char*>(p) + 64;
+}
+
+void operator delete(void* q) noexcept {
+  if (q == nullptr) return;
+  void* p = static_cast<char*>(q) - 64;
+  const std::size_t total = *static_cast<std::size_t*>(p);
+  if (total - 64 >= kCacheMin) {
+    BlockCache& c = block_cache();
+    std::lock_guard<std::mutex> lock(c.mu);
+    c.free_[total].push_back(p);
+    return;
+  }
+  std::free(p);
+}
+
+void operator delete(void* q, std::size_t) noexcept { operator delete(q); }
 
 namespace {
 

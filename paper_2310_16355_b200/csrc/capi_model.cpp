@@ -202,6 +202,20 @@ sw_status sw_model_launch_count(sw_model* model, int64_t* out) {
   });
 }
 
+sw_status sw_model_set_profiling(sw_model* model, int enable) {
+  return sw::guarded([&] {
+    require(model, "model");
+    model->model->set_profiling(enable != 0);
+  });
+}
+
+sw_status sw_model_read_profile(sw_model* model, double ms[8], double work[8], int64_t count[8]) {
+  return sw::guarded([&] {
+    require(model, "model");
+    model->model->read_profile(ms, work, count);
+  });
+}
+
 sw_status sw_model_device_bytes(sw_model* model, int64_t* out) {
   return sw::guarded([&] {
     require(model, "model");

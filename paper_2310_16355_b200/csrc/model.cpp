@@ -72,6 +72,7 @@ Model::Model(const ModelSpec& spec, const Plan& plan, Mesh* mesh, int batch, int
 
 Model::~Model() {
   if (stream_) cudaStreamSynchronize(stream_);
+  for (cudaEvent_t e : events_) cudaEventDestroy(e);
   for (void* p : allocations_) cudaFree(p);
   if (stream_) cudaStreamDestroy(stream_);
 }
@@ -440,12 +441,15 @@ void Model::stage_batch(const int32_t* tokens, const int32_t* targets, const flo
 // ---------------------------------------------------------------------------------------------
 void Model::ar_mp_ptrs(std::vector<Rank*>& grp, const std::vector<float*>& ptrs, int64_t n) {
   if (mesh_->mp == 1) return;
+  const double t = mesh_->mp;
+  tic();
   if (mesh_->emulated) {
     k::sum_ranks_f32(ptrs.data(), static_cast<int>(ptrs.size()), n, 1.0f, stream_);
     ++launches_;
   } else {
     nccl_check(ncclAllReduce(ptrs[0], ptrs[0], n, ncclFloat, ncclSum, mesh_->mp_comm, stream_), "AllReduce");
   }
+  toc(kProfComm, 2.0 * (t - 1) / t * 4.0 * n);  // NCCL bus bytes
   mesh_->record(CollKind::kAllReduce, mesh_->mp_group(grp[0]->dpi), static_cast<uint64_t>(n) * 4);
 }
 
@@ -502,7 +506,9 @@ void Model::gemm(Rank& R, int M, int N, int K, const void* A, int64_t lda, int a
   p.aux = aux;
   p.ld_aux = ld_aux;
   p.accumulate = accumulate;
+  tic();
   cuda_check(gemm_bf16(p, stream_), "gemm launch");
+  toc(kProfGemm, 2.0 * M * N * static_cast<double>(K));
   ++launches_;
 }
 
@@ -519,14 +525,18 @@ void Model::forward_replica(std::vector<Rank*>& grp, bool need_grad) {
   for (int l = 0; l < L_; ++l) {
     const LayerSlots& ls = layers_[l];
     for (Rank* R : grp) {
+      tic();
       k::layernorm_fwd(R->hs[l], P(*R, ls.ln1_s), P(*R, ls.ln1_b), R->a1[l], R->stats1[l], R->stats1[l] + M,
                        M, d, 1e-5f, stream_);
+      toc(kProfNorm, 6.0 * M * d);
       ++launches_;
       // column-parallel QKV (spmd.hpp:284-303): [M, d] x [3*dl, d]^T, bias slices of q|k|v
       gemm(*R, static_cast<int>(M), 3 * dl, d, R->a1[l], d, 0, W(*R, ls.q_k), d, 0,
            static_cast<int>(Epi::kStoreBf16), R->qkv[l], 3 * dl, nullptr, 0, P(*R, ls.q_b) + R->mpi * dl,
            nullptr, 0, 0, dl, d);
+      tic();
       k::attention_fwd(R->qkv[l], R->o[l], R->lse[l], B_, T_, hl_, hd_, stream_);
+      toc(kProfAttnFwd, 2.0 * B_ * hl_ * static_cast<double>(T_) * T_ * hd_);
       ++launches_;
     }
     // row-parallel O (spmd.hpp:305-324): local GEMM, all-reduce, then + bias (+ residual)
@@ -547,8 +557,10 @@ void Model::forward_replica(std::vector<Rank*>& grp, bool need_grad) {
       }
     }
     for (Rank* R : grp) {
+      tic();
       k::layernorm_fwd(R->hmid[l], P(*R, ls.ln2_s), P(*R, ls.ln2_b), R->a2[l], R->stats2[l], R->stats2[l] + M,
                        M, d, 1e-5f, stream_);
+      toc(kProfNorm, 6.0 * M * d);
       ++launches_;
       gemm(*R, static_cast<int>(M), fl, d, R->a2[l], d, 0, W(*R, ls.fc1_k), d, 0,
            static_cast<int>(Epi::kBiasGelu), R->pre[l], fl, R->act[l], fl, P(*R, ls.fc1_b) + R->mpi * fl);
@@ -572,15 +584,19 @@ void Model::forward_replica(std::vector<Rank*>& grp, bool need_grad) {
   }
   const int head = head_ >= 0 ? head_ : tok_;
   for (Rank* R : grp) {
+    tic();
     k::layernorm_fwd(R->hs[L_], P(*R, lnf_s_), P(*R, lnf_b_), R->f, R->statsf, R->statsf + M, M, d, 1e-5f,
                      stream_);
+    toc(kProfNorm, 6.0 * M * d);
     ++launches_;
     // LM head (replicated under the reference plan: every rank computes all V columns)
     gemm(*R, static_cast<int>(M), vl_, d, R->f, d, 0, W(*R, head), d, 0, static_cast<int>(Epi::kStoreBf16),
          R->logits, ldv_);
     k::sum_f32(R->weights, M, R->wsum, stream_);
+    tic();
     k::xent_fwd_bwd(R->logits, ldv_, M, vl_, R->targets, R->weights, R->wsum, R->wloss, need_grad ? 1 : 0,
                     stream_);
+    toc(kProfXent, (need_grad ? 4.0 : 2.0) * M * vl_);
     k::loss_reduce(R->wloss, M, R->wsum, R->loss, stream_);
     launches_ += 3;
   }
@@ -623,8 +639,10 @@ void Model::backward_replica(std::vector<Rank*>& grp, bool accumulate) {
          static_cast<int>(Epi::kStoreF32), R->dx, d);
     gemm(*R, vl_, d, static_cast<int>(M), R->logits, ldv_, 1, R->f, d, 1, static_cast<int>(Epi::kStoreF32),
          G(*R, head), d, nullptr, 0, nullptr, nullptr, 0, acc);
+    tic();
     k::layernorm_bwd(R->hs[L_], R->statsf, R->statsf + M, P(*R, lnf_s_), R->dx, R->gres, R->gb, G(*R, lnf_s_),
                      G(*R, lnf_b_), M, d, 0, stream_);
+    toc(kProfNorm, 18.0 * M * d);
     ++launches_;
   }
   for (int l = L_ - 1; l >= 0; --l) {
@@ -647,8 +665,10 @@ void Model::backward_replica(std::vector<Rank*>& grp, bool accumulate) {
     }
     if (tm_ > 1) ar_mp(grp, &Rank::dx, M * d);
     for (Rank* R : grp) {
+      tic();
       k::layernorm_bwd(R->hmid[l], R->stats2[l], R->stats2[l] + M, P(*R, ls.ln2_s), R->dx, R->gres, R->gb,
                        G(*R, ls.ln2_s), G(*R, ls.ln2_b), M, d, 1, stream_);
+      toc(kProfNorm, 18.0 * M * d);
       ++launches_;
     }
     // ---- attention ----
@@ -659,8 +679,10 @@ void Model::backward_replica(std::vector<Rank*>& grp, bool accumulate) {
            G(*R, ls.o_k), dl, nullptr, 0, nullptr, nullptr, 0, acc);
       gemm(*R, static_cast<int>(M), dl, d, R->gb, d, 0, W(*R, ls.o_k), dl, 1,
            static_cast<int>(Epi::kStoreBf16), R->dout, dl);
+      tic();
       k::attention_bwd(R->qkv[l], R->o[l], R->lse[l], R->dout, R->dqkv, R->attn_scratch, B_, T_, hl_, hd_,
                        stream_);
+      toc(kProfAttnBwd, 4.0 * B_ * hl_ * static_cast<double>(T_) * T_ * hd_);
       launches_ += 3;
       k::colsum_bf16(R->dqkv, 3 * dl, M, 3 * dl, dl, G(*R, ls.q_b) + R->mpi * dl, G(*R, ls.k_b) + R->mpi * dl,
                      G(*R, ls.v_b) + R->mpi * dl, acc, R->col_scratch, stream_);
@@ -672,8 +694,10 @@ void Model::backward_replica(std::vector<Rank*>& grp, bool accumulate) {
     }
     if (ta_ > 1) ar_mp(grp, &Rank::dx, M * d);
     for (Rank* R : grp) {
+      tic();
       k::layernorm_bwd(R->hs[l], R->stats1[l], R->stats1[l] + M, P(*R, ls.ln1_s), R->dx, R->gres, R->gb,
                        G(*R, ls.ln1_s), G(*R, ls.ln1_b), M, d, 1, stream_);
+      toc(kProfNorm, 18.0 * M * d);
       ++launches_;
     }
   }
@@ -775,8 +799,10 @@ void Model::adamw(double lr, double b1, double b2, double eps, double wd, bool c
   const float c1 = static_cast<float>(1.0 - std::pow(b1, t));
   const float c2 = static_cast<float>(1.0 - std::pow(b2, t));
   for (Rank& R : ranks_) {
+    tic();
     k::adamw(R.p, R.m, R.v, R.g, R.w, flat_n_, static_cast<float>(lr), static_cast<float>(b1),
              static_cast<float>(b2), static_cast<float>(eps), static_cast<float>(wd), c1, c2, stream_);
+    toc(kProfAdamw, 30.0 * flat_n_);
     ++launches_;
   }
   ++step_;
@@ -822,6 +848,53 @@ void Model::logits_to_host(float* out) {
     for (int64_t i = 0; i < M_; ++i)
       for (int j = 0; j < V_; ++j) o[i * V_ + j] = __bfloat162float(tmp[i * ldv_ + j]);
   }
+}
+
+// ---------------------------------------------------------------------------------------------
+// profiling
+// ---------------------------------------------------------------------------------------------
+void Model::set_profiling(bool on) {
+  prof_ = on;
+  ev_next_ = 0;
+  prof_rec_.clear();
+}
+
+void Model::tic() {
+  if (!prof_) return;
+  if (ev_next_ + 2 > events_.size()) {
+    for (int i = 0; i < 256; ++i) {
+      cudaEvent_t e;
+      cuda_check(cudaEventCreate(&e), "cudaEventCreate");
+      events_.push_back(e);
+    }
+  }
+  cuda_check(cudaEventRecord(events_[ev_next_], stream_), "cudaEventRecord");
+}
+
+void Model::toc(int cat, double work) {
+  if (!prof_) return;
+  cuda_check(cudaEventRecord(events_[ev_next_ + 1], stream_), "cudaEventRecord");
+  ev_next_ += 2;
+  prof_rec_.emplace_back(cat, work);
+}
+
+void Model::read_profile(double* ms, double* work, int64_t* count) {
+  for (int c = 0; c < kProfCats; ++c) {
+    ms[c] = 0.0;
+    work[c] = 0.0;
+    count[c] = 0;
+  }
+  cuda_check(cudaStreamSynchronize(stream_), "sync");
+  for (size_t i = 0; i < prof_rec_.size(); ++i) {
+    float t = 0.f;
+    cuda_check(cudaEventElapsedTime(&t, events_[2 * i], events_[2 * i + 1]), "cudaEventElapsedTime");
+    const int c = prof_rec_[i].first;
+    ms[c] += t;
+    work[c] += prof_rec_[i].second;
+    count[c] += 1;
+  }
+  ev_next_ = 0;
+  prof_rec_.clear();
 }
 
 }  // namespace sw

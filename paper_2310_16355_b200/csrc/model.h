@@ -63,6 +63,21 @@ struct Rank {
   bf16 *gb = nullptr, *dpre = nullptr, *dout = nullptr, *dqkv = nullptr;
 };
 
+// Kernel categories of the per-launch profile (CUDA events around each launch, read back
+// after a synchronize). `work` is algorithmic FLOPs for GEMM/attention and algorithmic HBM
+// bytes for the memory-bound kernels.
+enum ProfCat : int {
+  kProfGemm = 0,
+  kProfAttnFwd = 1,
+  kProfAttnBwd = 2,
+  kProfNorm = 3,
+  kProfXent = 4,
+  kProfAdamw = 5,
+  kProfComm = 6,
+  kProfOther = 7,
+  kProfCats = 8
+};
+
 class Model {
  public:
   Model(const ModelSpec& spec, const Plan& plan, Mesh* mesh, int batch, int seq_len);
@@ -83,6 +98,9 @@ class Model {
   cudaStream_t stream() const { return stream_; }
   int64_t launches() const { return launches_; }
   void reset_launches() { launches_ = 0; }
+  void set_profiling(bool on);
+  // Per category: summed device milliseconds, summed work, launch count (since the last read).
+  void read_profile(double* ms, double* work, int64_t* count);
   int64_t device_bytes() const { return bytes_; }
 
  private:
@@ -122,6 +140,13 @@ class Model {
   cudaStream_t stream_ = nullptr;
   int* d_flag_ = nullptr;
   int64_t launches_ = 0;
+  // profiling
+  void tic();
+  void toc(int cat, double work);
+  bool prof_ = false;
+  std::vector<cudaEvent_t> events_;
+  size_t ev_next_ = 0;
+  std::vector<std::pair<int, double>> prof_rec_;
   int64_t bytes_ = 0;
   uint64_t step_ = 0;
 };

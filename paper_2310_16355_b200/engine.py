@@ -49,13 +49,16 @@ def _declare():
     L.sw_model_stream.argtypes = [vp, C.POINTER(vp)]
     L.sw_model_launch_count.argtypes = [vp, C.POINTER(C.c_int64)]
     L.sw_model_device_bytes.argtypes = [vp, C.POINTER(C.c_int64)]
+    L.sw_model_set_profiling.argtypes = [vp, C.c_int]
+    L.sw_model_read_profile.argtypes = [vp, C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                        C.POINTER(C.c_int64)]
     for fn in ("sw_nccl_unique_id", "sw_mesh_create", "sw_mesh_comm_report",
                "sw_mesh_reset_comm_report", "sw_model_create", "sw_model_init_params",
                "sw_model_set_param", "sw_model_get_tensor", "sw_model_stage_batch",
                "sw_model_forward_backward", "sw_model_scale_grads", "sw_model_dp_sync",
                "sw_model_adamw_step", "sw_model_train_step", "sw_model_last_loss",
                "sw_model_forward_logits", "sw_model_stream", "sw_model_launch_count",
-               "sw_model_device_bytes"):
+               "sw_model_device_bytes", "sw_model_set_profiling", "sw_model_read_profile"):
         getattr(L, fn).restype = C.c_int
     L._engine_declared = True
     return L
@@ -214,6 +217,19 @@ class Model:
         x = C.c_int64()
         _lib.check(_declare().sw_model_launch_count(self._h, C.byref(x)))
         return x.value
+
+    PROFILE_CATEGORIES = ("gemm", "attn_fwd", "attn_bwd", "layernorm", "xent", "adamw", "comm", "other")
+
+    def set_profiling(self, on: bool):
+        _lib.check(_declare().sw_model_set_profiling(self._h, int(on)))
+
+    def read_profile(self) -> dict:
+        ms = (C.c_double * 8)()
+        work = (C.c_double * 8)()
+        cnt = (C.c_int64 * 8)()
+        _lib.check(_declare().sw_model_read_profile(self._h, ms, work, cnt))
+        return {c: {"ms": ms[i], "work": work[i], "launches": cnt[i]}
+                for i, c in enumerate(self.PROFILE_CATEGORIES)}
 
     def device_bytes(self) -> int:
         x = C.c_int64()
