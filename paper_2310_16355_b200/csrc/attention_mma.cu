@@ -1,13 +1,616 @@
-// Tensor-core causal attention for head_dim 64/128 (placeholder dispatch: returns false until
-// the kernels are in, so the generic path runs).
+// tcgen05 flash attention (causal, head-sharded) for head_dim 64 / 128.
+//
+// Forward, one CTA per (128-query block, batch*head), heaviest (latest) query blocks first:
+//   warp 0  TMA producer: Q once, then K_j / V_j into a 2-stage ring (one 2-D tensor map over
+//           the fused qkv activations [B*T, 3*Dl], box 64 x 128, SWIZZLE_128B)
+//   warp 1  MMA issuer:   S_j = Q K_j^T into one of two TMEM S buffers (128 fp32 columns each);
+//           O += P_j V_j into the TMEM O accumulator (P from smem, V as an MN-major operand)
+//   warp 2  TMEM allocator (512 columns)
+//   warps 4..7 softmax:   thread t owns query row t: reads S_j from TMEM lane t, online softmax
+//           with lazy rescaling (O in TMEM is rescaled only when the running max grows by more
+//           than 2^8), writes P_j (bf16) into a SWIZZLE_128B smem tile, finally O / l -> bf16.
+// S_{j+1} is computed on the tensor core while the softmax warps work on S_j, and P_j V_j
+// runs while they work on S_{j+1}.
+//
+// Backward, one CTA per (128-key block, batch*head) iterating over query blocks i >= j:
+//   S^T = K Q_i^T and dP^T = V dO_i^T (TMEM, lane = key), P^T = exp(S^T*scale - lse),
+//   dS^T = P^T * (dP^T - delta) * scale written to smem (bf16), then
+//   dV += P^T dO_i, dK += dS^T Q_i (TMEM accumulators), dQ_i = dS K (TMEM, lane = query) added
+//   to an fp32 dQ accumulator in HBM with vector reductions.
+// Every smem tile is a [rows x 64-column] SWIZZLE_128B chunk array, usable both as a K-major
+// and as an MN-major UMMA operand, so no tile is ever transposed.
+#include <cmath>
+
 #include "kernels.h"
+#include "sm100.cuh"
+#include "tensormap.h"
 
 namespace sw {
 namespace k {
 
-bool attention_mma_fwd(const bf16*, bf16*, float*, int, int, int, int, cudaStream_t) { return false; }
-bool attention_mma_bwd(const bf16*, const bf16*, const float*, const bf16*, bf16*, float*, int, int,
-                       int, int, cudaStream_t) {
+namespace {
+
+constexpr int BQ = 128;
+constexpr int BKV = 128;
+constexpr int CHUNK = 128 * 128;  // bytes of one [128 rows x 64 bf16] SW128 chunk
+
+__device__ __forceinline__ uint64_t kdesc(uint32_t base, int kk) {
+  // K-major operand, 16-element K step kk: chunk kk/4, +32 B inside the swizzle row.
+  return dev::make_sdesc_sw128(base + (kk >> 2) * CHUNK + (kk & 3) * 32, 16, 1024);
+}
+
+__device__ __forceinline__ uint64_t mndesc(uint32_t base, int kk) {
+  // MN-major operand whose K runs along the 128 rows of each chunk: 16 rows per step;
+  // 64-wide M/N chunks CHUNK bytes apart.
+  return dev::make_sdesc_sw128(base + kk * 2048, CHUNK, 1024);
+}
+
+template <int HD>
+struct FwdLayout {
+  static constexpr int Q = BQ * HD * 2;
+  static constexpr int KV = BKV * HD * 2;
+  static constexpr int P = BQ * BKV * 2;
+  static constexpr int OFF_Q = 0;
+  static constexpr int OFF_K = OFF_Q + Q;
+  static constexpr int OFF_V = OFF_K + 2 * KV;
+  static constexpr int OFF_P = OFF_V + 2 * KV;
+  static constexpr int OFF_BAR = OFF_P + 2 * P;
+  static constexpr int BYTES = OFF_BAR + 256 + 1024;
+};
+
+template <int HD>
+__global__ void __launch_bounds__(256, 1)
+    attn_fwd_tc(const __grid_constant__ CUtensorMap tm, bf16* __restrict__ out, float* __restrict__ lse,
+                int T, int Hl, float scale_log2, float scale) {
+  using Lay = FwdLayout<HD>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem + Lay::OFF_Q;
+  uint8_t* sK = smem + Lay::OFF_K;
+  uint8_t* sV = smem + Lay::OFF_V;
+  uint8_t* sP = smem + Lay::OFF_P;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Lay::OFF_BAR);
+  uint64_t* q_full = bars + 0;
+  uint64_t* kv_full = bars + 1;   // [2]
+  uint64_t* kv_empty = bars + 3;  // [2]
+  uint64_t* s_full = bars + 5;    // [2]
+  uint64_t* p_full = bars + 7;    // [2]
+  uint64_t* pv_done = bars + 9;   // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
+
+  const int nqb = (T + BQ - 1) / BQ;
+  const int BH = gridDim.x / nqb;
+  const int qb = nqb - 1 - static_cast<int>(blockIdx.x) / BH;  // heaviest blocks first
+  const int bh = static_cast<int>(blockIdx.x) % BH;
+  const int b = bh / Hl, h = bh % Hl;
+  const int Dl = Hl * HD;
+  const int q0 = qb * BQ;
+  const int row0 = b * T;
+  const int nkv = qb + 1;
+
+  const uint32_t warp = dev::warp_idx_sync();
+  const uint32_t lane = threadIdx.x & 31;
+  if (warp == 0 && lane == 0) {
+    dev::tma_prefetch_desc(&tm);
+    dev::mbar_init(q_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      dev::mbar_init(&kv_full[i], 1);
+      dev::mbar_init(&kv_empty[i], 1);
+      dev::mbar_init(&s_full[i], 1);
+      dev::mbar_init(&p_full[i], 128);
+      dev::mbar_init(&pv_done[i], 1);
+    }
+    dev::fence_barrier_init();
+  }
+  if (warp == 2) dev::tmem_alloc<512>(tmem_slot);
+  dev::tc_fence_before();
+  __syncthreads();
+  dev::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t t_o = tmem + 256;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      dev::mbar_arrive_expect_tx(q_full, Lay::Q);
+#pragma unroll
+      for (int c = 0; c < HD / 64; ++c) dev::tma_load_2d(sQ + c * CHUNK, &tm, q_full, h * HD + c * 64, row0 + q0);
+      for (int j = 0; j < nkv; ++j) {
+        const int st = j & 1;
+        dev::mbar_wait(&kv_empty[st], ((j >> 1) & 1) ^ 1);
+        dev::mbar_arrive_expect_tx(&kv_full[st], 2 * Lay::KV);
+#pragma unroll
+        for (int c = 0; c < HD / 64; ++c) {
+          dev::tma_load_2d(sK + st * Lay::KV + c * CHUNK, &tm, &kv_full[st], Dl + h * HD + c * 64, row0 + j * BKV);
+          dev::tma_load_2d(sV + st * Lay::KV + c * CHUNK, &tm, &kv_full[st], 2 * Dl + h * HD + c * 64, row0 + j * BKV);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t id_s = dev::make_idesc_bf16(BQ, BKV, 0, 0);
+      const uint32_t id_o = dev::make_idesc_bf16(BQ, HD, 0, 1);
+      const uint32_t aq = dev::smem_u32(sQ);
+      dev::mbar_wait(q_full, 0);
+      auto issue_pv = [&](int j) {
+        const int bb = j & 1;
+        dev::mbar_wait(&p_full[bb], (j >> 1) & 1);
+        dev::tc_fence_after();
+        const uint32_t ap = dev::smem_u32(sP + bb * Lay::P);
+        const uint32_t bv = dev::smem_u32(sV + bb * Lay::KV);
+#pragma unroll
+        for (int kk = 0; kk < BKV / 16; ++kk) {
+          dev::umma_f16_ss(t_o, kdesc(ap, kk), mndesc(bv, kk), id_o, (j > 0 || kk > 0) ? 1u : 0u);
+        }
+        dev::umma_commit(&pv_done[bb]);
+        dev::umma_commit(&kv_empty[bb]);
+      };
+      for (int j = 0; j < nkv; ++j) {
+        const int st = j & 1;
+        dev::mbar_wait(&kv_full[st], (j >> 1) & 1);
+        dev::tc_fence_after();
+        const uint32_t bk = dev::smem_u32(sK + st * Lay::KV);
+#pragma unroll
+        for (int kk = 0; kk < HD / 16; ++kk) {
+          dev::umma_f16_ss(tmem + st * 128, kdesc(aq, kk), kdesc(bk, kk), id_s, kk > 0 ? 1u : 0u);
+        }
+        dev::umma_commit(&s_full[st]);
+        if (j >= 1) issue_pv(j - 1);
+      }
+      issue_pv(nkv - 1);
+    }
+  } else if (warp >= 4) {
+    const int r = static_cast<int>(threadIdx.x) - 128;  // query row within the block
+    const int q = q0 + r;
+    const uint32_t lane_base = static_cast<uint32_t>((warp & 3) * 32) << 16;
+    float m_used = -INFINITY, l = 0.f;
+    for (int j = 0; j < nkv; ++j) {
+      const int bb = j & 1;
+      dev::mbar_wait(&s_full[bb], (j >> 1) & 1);
+      dev::tc_fence_after();
+      const uint32_t ts = tmem + lane_base + bb * 128;
+      const bool diag = (j == nkv - 1);
+      const int key0 = j * BKV;
+      float mx = -INFINITY;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint32_t v[32];
+        dev::tmem_ld_32x32b_x32(ts + c * 32, v);
+        dev::tmem_ld_wait();
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const int key = key0 + c * 32 + i;
+          const bool ok = !diag || (key <= q && key < T);
+          if (ok) mx = fmaxf(mx, __uint_as_float(v[i]));
+        }
+      }
+      // lazy rescale: keep the stale max unless the new one is 2^8 larger in exp2 units
+      bool resc = false;
+      float factor = 1.f;
+      if (j == 0) {
+        m_used = mx;
+      } else if ((mx - m_used) * scale_log2 > 8.f) {
+        resc = true;
+        factor = dev::ex2_approx((m_used - mx) * scale_log2);
+        m_used = mx;
+        l *= factor;
+      }
+      if (__any_sync(0xffffffffu, resc)) {
+        // O is rewritten in TMEM: wait for every earlier P V product to land
+        dev::mbar_wait(&pv_done[(j - 1) & 1], ((j - 1) >> 1) & 1);
+        dev::tc_fence_after();
+#pragma unroll
+        for (int c = 0; c < HD / 32; ++c) {
+          uint32_t v[32];
+          dev::tmem_ld_32x32b_x32(t_o + lane_base + c * 32, v);
+          dev::tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * factor);
+          dev::tmem_st_32x32b_x32(t_o + lane_base + c * 32, v);
+        }
+        dev::tmem_st_wait();
+      }
+      // the P buffer bb was last read by P_{j-2} V_{j-2}
+      if (j >= 2) dev::mbar_wait(&pv_done[bb], ((j - 2) >> 1) & 1);
+      const float mb = m_used * scale_log2;
+      uint8_t* tile = sP + bb * Lay::P;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint32_t v[32];
+        dev::tmem_ld_32x32b_x32(ts + c * 32, v);
+        dev::tmem_ld_wait();
+        uint32_t pk[16];
+#pragma unroll
+        for (int i = 0; i < 32; i += 2) {
+          const int key = key0 + c * 32 + i;
+          float p0 = dev::ex2_approx(__uint_as_float(v[i]) * scale_log2 - mb);
+          float p1 = dev::ex2_approx(__uint_as_float(v[i + 1]) * scale_log2 - mb);
+          if (diag) {
+            if (!(key <= q && key < T)) p0 = 0.f;
+            if (!(key + 1 <= q && key + 1 < T)) p1 = 0.f;
+          }
+          l += p0 + p1;
+          pk[i / 2] = dev::pack_bf16x2(p0, p1);
+        }
+        // 32 keys = 4 x 16-byte units of chunk c/2
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          dev::st_sw128(tile, BQ, r, c >> 1, (c & 1) * 4 + u,
+                        make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]));
+        }
+      }
+      dev::fence_proxy_async_smem();
+      dev::tc_fence_before();
+      dev::mbar_arrive(&p_full[bb]);
+    }
+    // epilogue: O / l
+    dev::mbar_wait(&pv_done[(nkv - 1) & 1], ((nkv - 1) >> 1) & 1);
+    dev::tc_fence_after();
+    const float inv = 1.f / l;
+    bf16* orow = out + (static_cast<int64_t>(row0) + q) * Dl + h * HD;
+#pragma unroll
+    for (int c = 0; c < HD / 32; ++c) {
+      uint32_t v[32];
+      dev::tmem_ld_32x32b_x32(t_o + lane_base + c * 32, v);
+      dev::tmem_ld_wait();
+      if (q < T) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          uint4 w;
+          w.x = dev::pack_bf16x2(__uint_as_float(v[8 * u + 0]) * inv, __uint_as_float(v[8 * u + 1]) * inv);
+          w.y = dev::pack_bf16x2(__uint_as_float(v[8 * u + 2]) * inv, __uint_as_float(v[8 * u + 3]) * inv);
+          w.z = dev::pack_bf16x2(__uint_as_float(v[8 * u + 4]) * inv, __uint_as_float(v[8 * u + 5]) * inv);
+          w.w = dev::pack_bf16x2(__uint_as_float(v[8 * u + 6]) * inv, __uint_as_float(v[8 * u + 7]) * inv);
+          *reinterpret_cast<uint4*>(orow + c * 32 + 8 * u) = w;
+        }
+      }
+    }
+    if (q < T) lse[static_cast<int64_t>(bh) * T + q] = m_used * scale + logf(l);
+  }
+  dev::tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    dev::tc_fence_after();
+    dev::tmem_dealloc<512>(tmem);
+  }
+}
+
+template <int HD>
+bool launch_fwd(const bf16* qkv, bf16* o, float* lse, int B, int T, int Hl, cudaStream_t s) {
+  using Lay = FwdLayout<HD>;
+  static bool configured = false;
+  if (!configured) {
+    if (cudaFuncSetAttribute(attn_fwd_tc<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, Lay::BYTES) !=
+        cudaSuccess) {
+      return false;
+    }
+    configured = true;
+  }
+  const int Dl = Hl * HD;
+  const CUtensorMap tm = make_tmap_bf16_2d(qkv, 3ull * Dl, static_cast<uint64_t>(B) * T, 3ull * Dl, 64, 128);
+  const int nqb = (T + BQ - 1) / BQ;
+  const double scale = 1.0 / std::sqrt(static_cast<double>(HD));
+  attn_fwd_tc<HD><<<nqb * B * Hl, 256, Lay::BYTES, s>>>(tm, o, lse, T, Hl,
+                                                         static_cast<float>(scale * 1.4426950408889634),
+                                                         static_cast<float>(scale));
+  return true;
+}
+
+
+// ---------------------------------------------------------------------------------------------
+// backward
+// ---------------------------------------------------------------------------------------------
+template <int HD>
+struct BwdLayout {
+  static constexpr int T_ = 128 * HD * 2;  // one [128 x HD] bf16 tile
+  static constexpr int PT = 128 * 128 * 2;
+  static constexpr int OFF_K = 0;
+  static constexpr int OFF_V = OFF_K + T_;
+  static constexpr int OFF_Q = OFF_V + T_;
+  static constexpr int OFF_DO = OFF_Q + T_;
+  static constexpr int OFF_PT = OFF_DO + T_;
+  static constexpr int OFF_DST = OFF_PT + PT;
+  static constexpr int OFF_STAT = OFF_DST + PT;   // [2][2][128] floats: lse, delta (double buffered)
+  static constexpr int OFF_BAR = OFF_STAT + 2 * 2 * 128 * 4;
+  static constexpr int BYTES = OFF_BAR + 256 + 1024;
+};
+
+template <int HD>
+__global__ void __launch_bounds__(256, 1)
+    attn_bwd_tc(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
+                const float* __restrict__ lse, const float* __restrict__ delta, float* __restrict__ dq_acc,
+                bf16* __restrict__ dqkv, int T, int Hl, float scale_log2, float scale) {
+  using Lay = BwdLayout<HD>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sK = smem + Lay::OFF_K;
+  uint8_t* sV = smem + Lay::OFF_V;
+  uint8_t* sQ = smem + Lay::OFF_Q;
+  uint8_t* sDO = smem + Lay::OFF_DO;
+  uint8_t* sPt = smem + Lay::OFF_PT;
+  uint8_t* sDSt = smem + Lay::OFF_DST;
+  float* sStat = reinterpret_cast<float*>(smem + Lay::OFF_STAT);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Lay::OFF_BAR);
+  uint64_t* kv_full = bars + 0;
+  uint64_t* qdo_full = bars + 1;
+  uint64_t* qdo_empty = bars + 2;
+  uint64_t* st_full = bars + 3;
+  uint64_t* p_full = bars + 4;
+  uint64_t* mma_done = bars + 5;
+  uint64_t* dq_free = bars + 6;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8);
+
+  const int nb = (T + 127) / 128;
+  const int BH = gridDim.x / nb;
+  const int kb = static_cast<int>(blockIdx.x) / BH;  // key block; block 0 has the most work
+  const int bh = static_cast<int>(blockIdx.x) % BH;
+  const int b = bh / Hl, h = bh % Hl;
+  const int Dl = Hl * HD;
+  const int key0 = kb * 128;
+  const int row0 = b * T;
+  const int nq = nb - kb;  // query blocks kb .. nb-1
+
+  const uint32_t warp = dev::warp_idx_sync();
+  const uint32_t lane = threadIdx.x & 31;
+  if (warp == 0 && lane == 0) {
+    dev::tma_prefetch_desc(&tm_qkv);
+    dev::tma_prefetch_desc(&tm_do);
+    dev::mbar_init(kv_full, 1);
+    dev::mbar_init(qdo_full, 1);
+    dev::mbar_init(qdo_empty, 1);
+    dev::mbar_init(st_full, 1);
+    dev::mbar_init(p_full, 128);
+    dev::mbar_init(mma_done, 1);
+    dev::mbar_init(dq_free, 128);
+    dev::fence_barrier_init();
+  }
+  if (warp == 2) dev::tmem_alloc<512>(tmem_slot);
+  dev::tc_fence_before();
+  __syncthreads();
+  dev::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t t_s = tmem, t_dp = tmem + 128, t_dv = tmem + 256, t_dk = tmem + 256 + HD, t_dq = tmem;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      dev::mbar_arrive_expect_tx(kv_full, 2 * Lay::T_);
+#pragma unroll
+      for (int c = 0; c < HD / 64; ++c) {
+        dev::tma_load_2d(sK + c * CHUNK, &tm_qkv, kv_full, Dl + h * HD + c * 64, row0 + key0);
+        dev::tma_load_2d(sV + c * CHUNK, &tm_qkv, kv_full, 2 * Dl + h * HD + c * 64, row0 + key0);
+      }
+      for (int n = 0; n < nq; ++n) {
+        const int qs = (kb + n) * 128;
+        dev::mbar_wait(qdo_empty, (n & 1) ^ 1);
+        dev::mbar_arrive_expect_tx(qdo_full, 2 * Lay::T_);
+#pragma unroll
+        for (int c = 0; c < HD / 64; ++c) {
+          dev::tma_load_2d(sQ + c * CHUNK, &tm_qkv, qdo_full, h * HD + c * 64, row0 + qs);
+          dev::tma_load_2d(sDO + c * CHUNK, &tm_do, qdo_full, h * HD + c * 64, row0 + qs);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t id_s = dev::make_idesc_bf16(128, 128, 0, 0);
+      const uint32_t id_kv = dev::make_idesc_bf16(128, HD, 0, 1);
+      const uint32_t id_q = dev::make_idesc_bf16(128, HD, 1, 1);
+      const uint32_t aK = dev::smem_u32(sK), aV = dev::smem_u32(sV), aQ = dev::smem_u32(sQ);
+      const uint32_t aDO = dev::smem_u32(sDO), aPt = dev::smem_u32(sPt), aDSt = dev::smem_u32(sDSt);
+      dev::mbar_wait(kv_full, 0);
+      for (int n = 0; n < nq; ++n) {
+        dev::mbar_wait(qdo_full, n & 1);
+        if (n >= 1) dev::mbar_wait(dq_free, (n - 1) & 1);
+        dev::tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < HD / 16; ++kk) dev::umma_f16_ss(t_s, kdesc(aK, kk), kdesc(aQ, kk), id_s, kk > 0);
+#pragma unroll
+        for (int kk = 0; kk < HD / 16; ++kk) dev::umma_f16_ss(t_dp, kdesc(aV, kk), kdesc(aDO, kk), id_s, kk > 0);
+        dev::umma_commit(st_full);
+        dev::mbar_wait(p_full, n & 1);
+        dev::tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)
+          dev::umma_f16_ss(t_dv, kdesc(aPt, kk), mndesc(aDO, kk), id_kv, (n > 0 || kk > 0) ? 1u : 0u);
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)
+          dev::umma_f16_ss(t_dk, kdesc(aDSt, kk), mndesc(aQ, kk), id_kv, (n > 0 || kk > 0) ? 1u : 0u);
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) dev::umma_f16_ss(t_dq, mndesc(aDSt, kk), mndesc(aK, kk), id_q, kk > 0);
+        dev::umma_commit(mma_done);
+        dev::umma_commit(qdo_empty);
+      }
+    }
+  } else if (warp >= 4) {
+    const int t = static_cast<int>(threadIdx.x) - 128;  // key row (S^T lane) / query row (dQ lane)
+    const int key = key0 + t;
+    const uint32_t lane_base = static_cast<uint32_t>((warp & 3) * 32) << 16;
+    const float log2e = 1.4426950408889634f;
+    for (int n = 0; n < nq; ++n) {
+      const int qs = (kb + n) * 128;
+      float* st_lse = sStat + (n & 1) * 256;
+      float* st_del = st_lse + 128;
+      {
+        const int qq = qs + t;
+        st_lse[t] = qq < T ? lse[static_cast<int64_t>(bh) * T + qq] * log2e : 0.f;
+        st_del[t] = qq < T ? delta[static_cast<int64_t>(bh) * T + qq] : 0.f;
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      dev::mbar_wait(st_full, n & 1);
+      dev::tc_fence_after();
+      if (n >= 1) dev::mbar_wait(mma_done, (n - 1) & 1);  // sPt / sDSt free again
+      const bool diag = (n == 0);
+#pragma unroll 1
+      for (int c = 0; c < 4; ++c) {
+        uint32_t sv[32], pv[32];
+        dev::tmem_ld_32x32b_x32(t_s + lane_base + c * 32, sv);
+        dev::tmem_ld_32x32b_x32(t_dp + lane_base + c * 32, pv);
+        dev::tmem_ld_wait();
+        uint32_t pk[16], dk[16];
+#pragma unroll
+        for (int i = 0; i < 32; i += 2) {
+          float pp[2], dd[2];
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const int qi = c * 32 + i + u;
+            const int qq = qs + qi;
+            float p = dev::ex2_approx(__uint_as_float(sv[i + u]) * scale_log2 - st_lse[qi]);
+            const bool ok = qq < T && key < T && (!diag || qq >= key);
+            p = ok ? p : 0.f;
+            pp[u] = p;
+            dd[u] = p * (__uint_as_float(pv[i + u]) - st_del[qi]) * scale;
+          }
+          pk[i / 2] = dev::pack_bf16x2(pp[0], pp[1]);
+          dk[i / 2] = dev::pack_bf16x2(dd[0], dd[1]);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          dev::st_sw128(sPt, 128, t, c >> 1, (c & 1) * 4 + u, make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]));
+          dev::st_sw128(sDSt, 128, t, c >> 1, (c & 1) * 4 + u, make_uint4(dk[4 * u], dk[4 * u + 1], dk[4 * u + 2], dk[4 * u + 3]));
+        }
+      }
+      dev::fence_proxy_async_smem();
+      dev::tc_fence_before();
+      dev::mbar_arrive(p_full);
+      // dQ_i (TMEM lane = query row) -> fp32 reductions into the dQ accumulator
+      dev::mbar_wait(mma_done, n & 1);
+      dev::tc_fence_after();
+      const int qq = qs + t;
+      float* dst = dq_acc + (static_cast<int64_t>(row0) + qq) * Dl + h * HD;
+#pragma unroll 1
+      for (int c = 0; c < HD / 32; ++c) {
+        uint32_t v[32];
+        dev::tmem_ld_32x32b_x32(t_dq + lane_base + c * 32, v);
+        dev::tmem_ld_wait();
+        if (qq < T) {
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            dev::red_add_v4(dst + c * 32 + 4 * u, __uint_as_float(v[4 * u]), __uint_as_float(v[4 * u + 1]),
+                            __uint_as_float(v[4 * u + 2]), __uint_as_float(v[4 * u + 3]));
+          }
+        }
+      }
+      dev::tc_fence_before();
+      dev::mbar_arrive(dq_free);
+    }
+    // dK, dV (lane = key row) -> bf16 rows of dqkv
+    dev::mbar_wait(mma_done, (nq - 1) & 1);
+    dev::tc_fence_after();
+    const int64_t ld = 3LL * Dl;
+    bf16* dk_row = dqkv + (static_cast<int64_t>(row0) + key) * ld + Dl + h * HD;
+    bf16* dv_row = dk_row + Dl;
+#pragma unroll 1
+    for (int c = 0; c < HD / 32; ++c) {
+      uint32_t a[32], v[32];
+      dev::tmem_ld_32x32b_x32(t_dk + lane_base + c * 32, a);
+      dev::tmem_ld_32x32b_x32(t_dv + lane_base + c * 32, v);
+      dev::tmem_ld_wait();
+      if (key < T) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          uint4 w, z;
+          w.x = dev::pack_bf16x2(__uint_as_float(a[8 * u + 0]), __uint_as_float(a[8 * u + 1]));
+          w.y = dev::pack_bf16x2(__uint_as_float(a[8 * u + 2]), __uint_as_float(a[8 * u + 3]));
+          w.z = dev::pack_bf16x2(__uint_as_float(a[8 * u + 4]), __uint_as_float(a[8 * u + 5]));
+          w.w = dev::pack_bf16x2(__uint_as_float(a[8 * u + 6]), __uint_as_float(a[8 * u + 7]));
+          z.x = dev::pack_bf16x2(__uint_as_float(v[8 * u + 0]), __uint_as_float(v[8 * u + 1]));
+          z.y = dev::pack_bf16x2(__uint_as_float(v[8 * u + 2]), __uint_as_float(v[8 * u + 3]));
+          z.z = dev::pack_bf16x2(__uint_as_float(v[8 * u + 4]), __uint_as_float(v[8 * u + 5]));
+          z.w = dev::pack_bf16x2(__uint_as_float(v[8 * u + 6]), __uint_as_float(v[8 * u + 7]));
+          *reinterpret_cast<uint4*>(dk_row + c * 32 + 8 * u) = w;
+          *reinterpret_cast<uint4*>(dv_row + c * 32 + 8 * u) = z;
+        }
+      }
+    }
+  }
+  dev::tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    dev::tc_fence_after();
+    dev::tmem_dealloc<512>(tmem);
+  }
+}
+
+// delta[bh, q] = sum_c dO[q, c] * O[q, c] (one warp per row)
+__global__ void delta_kernel(const bf16* __restrict__ o, const bf16* __restrict__ dout, float* __restrict__ delta,
+                             int T, int Hl, int hd, int64_t rows) {
+  const int64_t wid = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (wid >= rows * Hl) return;
+  const int64_t m = wid / Hl;
+  const int h = static_cast<int>(wid % Hl);
+  const int64_t off = m * (static_cast<int64_t>(Hl) * hd) + h * hd;
+  float s = 0.f;
+  for (int c = lane * 2; c < hd; c += 64) {
+    const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(o + off + c));
+    const float2 bb = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(dout + off + c));
+    s += a.x * bb.x + a.y * bb.y;
+  }
+#pragma unroll
+  for (int x = 16; x > 0; x >>= 1) s += __shfl_xor_sync(0xffffffffu, s, x);
+  if (lane == 0) {
+    const int64_t b = m / T, t = m % T;
+    delta[(b * Hl + h) * T + t] = s;
+  }
+}
+
+__global__ void dq_to_bf16(const float* __restrict__ acc, bf16* __restrict__ dqkv, int64_t rows, int Dl) {
+  const int64_t n4 = rows * Dl / 4;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n4;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = (e * 4) / Dl, c = (e * 4) % Dl;
+    const float4 v = reinterpret_cast<const float4*>(acc)[e];
+    uint2 w;
+    w.x = dev::pack_bf16x2(v.x, v.y);
+    w.y = dev::pack_bf16x2(v.z, v.w);
+    *reinterpret_cast<uint2*>(dqkv + r * 3LL * Dl + c) = w;
+  }
+}
+
+template <int HD>
+bool launch_bwd(const bf16* qkv, const bf16* o, const float* lse, const bf16* dout, bf16* dqkv, float* scratch,
+                int B, int T, int Hl, cudaStream_t s) {
+  using Lay = BwdLayout<HD>;
+  static bool configured = false;
+  if (!configured) {
+    if (cudaFuncSetAttribute(attn_bwd_tc<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, Lay::BYTES) !=
+        cudaSuccess) {
+      return false;
+    }
+    configured = true;
+  }
+  const int Dl = Hl * HD;
+  const int64_t M = static_cast<int64_t>(B) * T;
+  float* delta = scratch;
+  float* dq = scratch + ((M * Hl + 63) / 64) * 64;
+  cudaMemsetAsync(dq, 0, sizeof(float) * M * Dl, s);
+  const int64_t warps = M * Hl;
+  delta_kernel<<<static_cast<unsigned>((warps * 32 + 255) / 256), 256, 0, s>>>(o, dout, delta, T, Hl, HD, M);
+  const CUtensorMap tm_qkv = make_tmap_bf16_2d(qkv, 3ull * Dl, static_cast<uint64_t>(M), 3ull * Dl, 64, 128);
+  const CUtensorMap tm_do = make_tmap_bf16_2d(dout, static_cast<uint64_t>(Dl), static_cast<uint64_t>(M),
+                                              static_cast<uint64_t>(Dl), 64, 128);
+  const int nb = (T + 127) / 128;
+  const double scale = 1.0 / std::sqrt(static_cast<double>(HD));
+  attn_bwd_tc<HD><<<nb * B * Hl, 256, Lay::BYTES, s>>>(tm_qkv, tm_do, lse, delta, dq, dqkv, T, Hl,
+                                                        static_cast<float>(scale * 1.4426950408889634),
+                                                        static_cast<float>(scale));
+  dq_to_bf16<<<1184, 256, 0, s>>>(dq, dqkv, M, Dl);
+  return true;
+}
+
+}  // namespace
+
+bool attention_mma_fwd(const bf16* qkv, bf16* o, float* lse, int B, int T, int Hl, int hd, cudaStream_t s) {
+  if (((3 * Hl * hd) % 8) != 0) return false;
+  if (hd == 128) return launch_fwd<128>(qkv, o, lse, B, T, Hl, s);
+  if (hd == 64) return launch_fwd<64>(qkv, o, lse, B, T, Hl, s);
+  return false;
+}
+
+bool attention_mma_bwd(const bf16* qkv, const bf16* o, const float* lse, const bf16* dout, bf16* dqkv,
+                       float* scratch, int B, int T, int Hl, int hd, cudaStream_t s) {
+  if (((Hl * hd) % 8) != 0) return false;
+  if (hd == 128) return launch_bwd<128>(qkv, o, lse, dout, dqkv, scratch, B, T, Hl, s);
+  if (hd == 64) return launch_bwd<64>(qkv, o, lse, dout, dqkv, scratch, B, T, Hl, s);
   return false;
 }
 
