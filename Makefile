@@ -18,7 +18,7 @@ OBJS      := $(patsubst $(SRC_DIR)/%.cu,$(BUILD_DIR)/%.cu.o,$(CU_SRCS)) \
              $(patsubst $(SRC_DIR)/%.cpp,$(BUILD_DIR)/%.cpp.o,$(CPP_SRCS))
 HDRS      := $(wildcard $(SRC_DIR)/*.h $(SRC_DIR)/*.cuh) include/shardweave_b200.h
 
-all: $(LIB)
+all: $(LIB) examples/cpp_train_step
 
 $(BUILD_DIR)/%.cu.o: $(SRC_DIR)/%.cu $(HDRS)
 	@mkdir -p $(BUILD_DIR)
@@ -36,3 +36,10 @@ clean:
 	rm -rf $(BUILD_DIR) $(LIB)
 
 .PHONY: all clean
+
+examples/cpp_train_step: examples/cpp_train_step.cpp include/shardweave_b200.hpp $(LIB)
+	$(CXX) -std=c++17 -O2 -Iinclude $< -o $@ -Lpaper_2310_16355_b200 -lshardweave_b200 \
+	    -Wl,-rpath,'$$ORIGIN/../paper_2310_16355_b200'
+
+examples: examples/cpp_train_step
+.PHONY: examples
