@@ -79,9 +79,9 @@ __global__ void __launch_bounds__(256, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
 
   const int nqb = (T + BQ - 1) / BQ;
-  const int BH = gridDim.x / nqb;
-  const int qb = nqb - 1 - static_cast<int>(blockIdx.x) / BH;  // heaviest blocks first
-  const int bh = static_cast<int>(blockIdx.x) % BH;
+  // consecutive CTAs share (batch, head) so its K/V stays L2-resident; heaviest block first
+  const int qb = nqb - 1 - static_cast<int>(blockIdx.x) % nqb;
+  const int bh = static_cast<int>(blockIdx.x) / nqb;
   const int b = bh / Hl, h = bh % Hl;
   const int Dl = Hl * HD;
   const int q0 = qb * BQ;
@@ -170,19 +170,23 @@ __global__ void __launch_bounds__(256, 1)
       const uint32_t ts = tmem + lane_base + bb * 128;
       const bool diag = (j == nkv - 1);
       const int key0 = j * BKV;
-      float mx = -INFINITY;
+      // one pass over the 128 scores of this row: all four TMEM loads in flight, one wait
+      uint32_t v[128];
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
-        uint32_t v[32];
-        dev::tmem_ld_32x32b_x32(ts + c * 32, v);
-        dev::tmem_ld_wait();
+        dev::tmem_ld_32x32b_x32(ts + c * 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32 * c));
+      }
+      dev::tmem_ld_wait();
+      if (diag) {
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          const int key = key0 + c * 32 + i;
-          const bool ok = !diag || (key <= q && key < T);
-          if (ok) mx = fmaxf(mx, __uint_as_float(v[i]));
+        for (int i = 0; i < 128; ++i) {
+          const int key = key0 + i;
+          if (!(key <= q && key < T)) v[i] = __float_as_uint(-INFINITY);
         }
       }
+      float mx = __uint_as_float(v[0]);
+#pragma unroll
+      for (int i = 1; i < 128; ++i) mx = fmaxf(mx, __uint_as_float(v[i]));
       // lazy rescale: keep the stale max unless the new one is 2^8 larger in exp2 units
       bool resc = false;
       float factor = 1.f;
@@ -198,14 +202,14 @@ __global__ void __launch_bounds__(256, 1)
         // O is rewritten in TMEM: wait for every earlier P V product to land
         dev::mbar_wait(&pv_done[(j - 1) & 1], ((j - 1) >> 1) & 1);
         dev::tc_fence_after();
-#pragma unroll
+#pragma unroll 1
         for (int c = 0; c < HD / 32; ++c) {
-          uint32_t v[32];
-          dev::tmem_ld_32x32b_x32(t_o + lane_base + c * 32, v);
+          uint32_t o[32];
+          dev::tmem_ld_32x32b_x32(t_o + lane_base + c * 32, o);
           dev::tmem_ld_wait();
 #pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * factor);
-          dev::tmem_st_32x32b_x32(t_o + lane_base + c * 32, v);
+          for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * factor);
+          dev::tmem_st_32x32b_x32(t_o + lane_base + c * 32, o);
         }
         dev::tmem_st_wait();
       }
@@ -213,31 +217,20 @@ __global__ void __launch_bounds__(256, 1)
       if (j >= 2) dev::mbar_wait(&pv_done[bb], ((j - 2) >> 1) & 1);
       const float mb = m_used * scale_log2;
       uint8_t* tile = sP + bb * Lay::P;
+      float ls = 0.f;
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint32_t v[32];
-        dev::tmem_ld_32x32b_x32(ts + c * 32, v);
-        dev::tmem_ld_wait();
-        uint32_t pk[16];
+      for (int c = 0; c < 16; ++c) {  // 16 units of 8 keys
+        uint32_t pk[4];
 #pragma unroll
-        for (int i = 0; i < 32; i += 2) {
-          const int key = key0 + c * 32 + i;
-          float p0 = dev::ex2_approx(__uint_as_float(v[i]) * scale_log2 - mb);
-          float p1 = dev::ex2_approx(__uint_as_float(v[i + 1]) * scale_log2 - mb);
-          if (diag) {
-            if (!(key <= q && key < T)) p0 = 0.f;
-            if (!(key + 1 <= q && key + 1 < T)) p1 = 0.f;
-          }
-          l += p0 + p1;
-          pk[i / 2] = dev::pack_bf16x2(p0, p1);
+        for (int e = 0; e < 4; ++e) {
+          const float p0 = dev::ex2_approx(fmaf(__uint_as_float(v[8 * c + 2 * e]), scale_log2, -mb));
+          const float p1 = dev::ex2_approx(fmaf(__uint_as_float(v[8 * c + 2 * e + 1]), scale_log2, -mb));
+          ls += p0 + p1;
+          pk[e] = dev::pack_bf16x2(p0, p1);
         }
-        // 32 keys = 4 x 16-byte units of chunk c/2
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          dev::st_sw128(tile, BQ, r, c >> 1, (c & 1) * 4 + u,
-                        make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]));
-        }
+        dev::st_sw128(tile, BQ, r, c >> 3, c & 7, make_uint4(pk[0], pk[1], pk[2], pk[3]));
       }
+      l += ls;
       dev::fence_proxy_async_smem();
       dev::tc_fence_before();
       dev::mbar_arrive(&p_full[bb]);
@@ -340,9 +333,9 @@ __global__ void __launch_bounds__(256, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8);
 
   const int nb = (T + 127) / 128;
-  const int BH = gridDim.x / nb;
-  const int kb = static_cast<int>(blockIdx.x) / BH;  // key block; block 0 has the most work
-  const int bh = static_cast<int>(blockIdx.x) % BH;
+  // consecutive CTAs share (batch, head) (Q/dO stay L2-resident); key block 0 has the most work
+  const int kb = static_cast<int>(blockIdx.x) % nb;
+  const int bh = static_cast<int>(blockIdx.x) / nb;
   const int b = bh / Hl, h = bh % Hl;
   const int Dl = Hl * HD;
   const int key0 = kb * 128;
@@ -440,32 +433,36 @@ __global__ void __launch_bounds__(256, 1)
       if (n >= 1) dev::mbar_wait(mma_done, (n - 1) & 1);  // sPt / sDSt free again
       const bool diag = (n == 0);
 #pragma unroll 1
-      for (int c = 0; c < 4; ++c) {
-        uint32_t sv[32], pv[32];
-        dev::tmem_ld_32x32b_x32(t_s + lane_base + c * 32, sv);
-        dev::tmem_ld_32x32b_x32(t_dp + lane_base + c * 32, pv);
+      for (int half = 0; half < 2; ++half) {
+        // 64 query columns of S^T and dP^T: four TMEM loads in flight, one wait
+        uint32_t sv[64], pv[64];
+        dev::tmem_ld_32x32b_x32(t_s + lane_base + half * 64, *reinterpret_cast<uint32_t(*)[32]>(sv));
+        dev::tmem_ld_32x32b_x32(t_s + lane_base + half * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(sv + 32));
+        dev::tmem_ld_32x32b_x32(t_dp + lane_base + half * 64, *reinterpret_cast<uint32_t(*)[32]>(pv));
+        dev::tmem_ld_32x32b_x32(t_dp + lane_base + half * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(pv + 32));
         dev::tmem_ld_wait();
-        uint32_t pk[16], dk[16];
 #pragma unroll
-        for (int i = 0; i < 32; i += 2) {
-          float pp[2], dd[2];
+        for (int u = 0; u < 8; ++u) {  // 8 units of 8 query columns
+          uint32_t pk[4], dk[4];
 #pragma unroll
-          for (int u = 0; u < 2; ++u) {
-            const int qi = c * 32 + i + u;
-            const int qq = qs + qi;
-            float p = dev::ex2_approx(__uint_as_float(sv[i + u]) * scale_log2 - st_lse[qi]);
-            const bool ok = qq < T && key < T && (!diag || qq >= key);
-            p = ok ? p : 0.f;
-            pp[u] = p;
-            dd[u] = p * (__uint_as_float(pv[i + u]) - st_del[qi]) * scale;
+          for (int e = 0; e < 4; ++e) {
+            float pp[2], dd[2];
+#pragma unroll
+            for (int w2 = 0; w2 < 2; ++w2) {
+              const int ci = 8 * u + 2 * e + w2;  // column within the half
+              const int qi = half * 64 + ci;
+              const int qq = qs + qi;
+              float p = dev::ex2_approx(fmaf(__uint_as_float(sv[ci]), scale_log2, -st_lse[qi]));
+              const bool ok = qq < T && key < T && (!diag || qq >= key);
+              p = ok ? p : 0.f;
+              pp[w2] = p;
+              dd[w2] = p * (__uint_as_float(pv[ci]) - st_del[qi]) * scale;
+            }
+            pk[e] = dev::pack_bf16x2(pp[0], pp[1]);
+            dk[e] = dev::pack_bf16x2(dd[0], dd[1]);
           }
-          pk[i / 2] = dev::pack_bf16x2(pp[0], pp[1]);
-          dk[i / 2] = dev::pack_bf16x2(dd[0], dd[1]);
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          dev::st_sw128(sPt, 128, t, c >> 1, (c & 1) * 4 + u, make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]));
-          dev::st_sw128(sDSt, 128, t, c >> 1, (c & 1) * 4 + u, make_uint4(dk[4 * u], dk[4 * u + 1], dk[4 * u + 2], dk[4 * u + 3]));
+          dev::st_sw128(sPt, 128, t, half, u, make_uint4(pk[0], pk[1], pk[2], pk[3]));
+          dev::st_sw128(sDSt, 128, t, half, u, make_uint4(dk[0], dk[1], dk[2], dk[3]));
         }
       }
       dev::fence_proxy_async_smem();
