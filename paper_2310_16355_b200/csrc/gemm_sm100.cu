@@ -10,6 +10,7 @@
 // This is the executor for the reference's `kernels::linear` (kernels.hpp:146-161) on both
 // branches of SpmdInterpreter::linear_onto (spmd.hpp:274-340) and for the linear VJP
 // matmuls emitted by autodiff (autodiff.hpp:124-139).
+#include <cstdlib>
 #include <stdexcept>
 #include <string>
 
@@ -31,6 +32,15 @@ constexpr int TMEM_COLS = 512;
 constexpr int NUM_THREADS = 256;
 constexpr int GROUP_M = 8;
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
+
+// SW_GEMM_1SM=1 selects the single-CTA kernel (debug / comparison).
+bool use_pairs() {
+  static const bool pairs = [] {
+    const char* e = std::getenv("SW_GEMM_1SM");
+    return !(e != nullptr && e[0] == '1');
+  }();
+  return pairs;
+}
 
 __device__ __forceinline__ void tile_coords(int t, int num_m, int num_n, int& mb, int& nb) {
   const int per_group = GROUP_M * num_n;
@@ -290,8 +300,198 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   }
 }
 
+
+// ---------------------------------------------------------------------------------------------
+// CTA-pair variant (cta_group::2): a cluster of two CTAs computes a 256 x 256 tile with one
+// M=256 MMA issued by the even CTA. Each CTA stages its own 128 rows of A and 128 rows (half)
+// of B, so per-SM operand traffic is 32 KB per 64-deep k-block instead of 48 KB (the
+// single-CTA kernel is TMA-ingress bound at ~83% tensor-pipe activity).
+// ---------------------------------------------------------------------------------------------
+constexpr int P_STAGES = 6;
+constexpr int P_A_STAGE = 128 * BK * 2;  // 16 KiB
+constexpr int P_B_STAGE = 128 * BK * 2;  // 16 KiB (half of the N=256 tile)
+constexpr int P_STAGE_BYTES = P_A_STAGE + P_B_STAGE;
+constexpr int P_SMEM_BYTES = P_STAGES * P_STAGE_BYTES + 1024 + 256;
+
+template <Epi EPI>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
+    gemm_bf16_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                         const GemmParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + P_STAGES * P_A_STAGE;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + P_STAGES * P_B_STAGE);
+  uint64_t* empty = full + P_STAGES;
+  uint64_t* tfull = empty + P_STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const uint32_t warp = dev::warp_idx_sync();
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t rank = dev::cluster_ctarank();
+
+  const int num_m = (p.M + 2 * BM - 1) / (2 * BM);  // pair tiles along M (256 rows)
+  const int num_n = (p.N + BN - 1) / BN;
+  const int num_tiles = num_m * num_n;
+  const int num_kb = (p.K + BK - 1) / BK;
+  const int pair = static_cast<int>(blockIdx.x) >> 1;
+  const int npairs = static_cast<int>(gridDim.x) >> 1;
+
+  if (warp == 0 && lane == 0) {
+    dev::tma_prefetch_desc(&tmA);
+    dev::tma_prefetch_desc(&tmB);
+    for (int s = 0; s < P_STAGES; ++s) {
+      dev::mbar_init(&full[s], 1);
+      dev::mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      dev::mbar_init(&tfull[a], 1);
+      dev::mbar_init(&tempty[a], 8);
+    }
+    dev::fence_barrier_init();
+  }
+  if (warp == 2) dev::tmem_alloc_2sm<TMEM_COLS>(tmem_slot);
+  dev::tc_fence_before();
+  dev::cluster_sync();
+  dev::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = pair; t < num_tiles; t += npairs) {
+        int mb, nb;
+        tile_coords(t, num_m, num_n, mb, nb);
+        const int m0 = mb * 2 * BM + static_cast<int>(rank) * BM;
+        const int n0 = nb * BN + static_cast<int>(rank) * 128;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          dev::mbar_wait(&empty[stage], phase ^ 1);
+          if (rank == 0) dev::mbar_arrive_expect_tx(&full[stage], 2 * P_STAGE_BYTES);
+          const int k0 = kb * BK;
+          uint8_t* a_dst = sA + stage * P_A_STAGE;
+          uint8_t* b_dst = sB + stage * P_B_STAGE;
+          if (!p.a_mn_major) {
+            dev::tma_load_2d_2sm(a_dst, &tmA, &full[stage], k0, m0);
+          } else {
+            dev::tma_load_2d_2sm(a_dst, &tmA, &full[stage], m0, k0);
+            dev::tma_load_2d_2sm(a_dst + 8192, &tmA, &full[stage], m0 + 64, k0);
+          }
+          if (!p.b_mn_major) {
+            dev::tma_load_2d_2sm(b_dst, &tmB, &full[stage], k0, n0);
+          } else {
+            dev::tma_load_2d_2sm(b_dst, &tmB, &full[stage], n0, k0);
+            dev::tma_load_2d_2sm(b_dst + 8192, &tmB, &full[stage], n0 + 64, k0);
+          }
+          if (++stage == P_STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (rank == 0 && lane == 0) {
+      const uint32_t idesc = dev::make_idesc_bf16(2 * BM, BN, p.a_mn_major, p.b_mn_major);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int t = pair; t < num_tiles; t += npairs) {
+        dev::mbar_wait(&tempty[acc], acc_phase ^ 1);
+        dev::tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          dev::mbar_wait(&full[stage], phase);
+          dev::tc_fence_after();
+          const uint32_t a_base = dev::smem_u32(sA + stage * P_A_STAGE);
+          const uint32_t b_base = dev::smem_u32(sB + stage * P_B_STAGE);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            const uint64_t adesc =
+                p.a_mn_major ? dev::make_sdesc_sw128(a_base + k * 2048, 8192, 1024)
+                             : dev::make_sdesc_sw128(a_base + k * 32, 16, 1024);
+            const uint64_t bdesc =
+                p.b_mn_major ? dev::make_sdesc_sw128(b_base + k * 2048, 8192, 1024)
+                             : dev::make_sdesc_sw128(b_base + k * 32, 16, 1024);
+            dev::umma_f16_ss_2sm(d_tmem, adesc, bdesc, idesc, (kb | k) != 0 ? 1u : 0u);
+          }
+          dev::umma_commit_2sm(&empty[stage], 0x3);
+          if (++stage == P_STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        dev::umma_commit_2sm(&tfull[acc], 0x3);
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    const uint32_t q = warp & 3;
+    const uint32_t tempty_leader = dev::mapa_shared(dev::smem_u32(&tempty[0]), 0);
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int t = pair; t < num_tiles; t += npairs) {
+      int mb, nb;
+      tile_coords(t, num_m, num_n, mb, nb);
+      const int row = mb * 2 * BM + static_cast<int>(rank) * BM + static_cast<int>(q) * 32 + static_cast<int>(lane);
+      dev::mbar_wait(&tfull[acc], acc_phase);
+      dev::tc_fence_after();
+      const int n_left = p.N - nb * BN;
+#pragma unroll 1
+      for (int j = 0; j < BN / 32; ++j) {
+        const int ncols = min(32, n_left - j * 32);
+        if (ncols <= 0) break;
+        uint32_t r[32];
+        dev::tmem_ld_32x32b_x32(tmem_base + ((q * 32) << 16) + acc * BN + j * 32, r);
+        dev::tmem_ld_wait();
+        if (row < p.M) epilogue_chunk<EPI>(p, row, nb * BN + j * 32, ncols, r);
+      }
+      dev::tc_fence_before();
+      if (lane == 0) dev::mbar_arrive_cluster(tempty_leader + acc * 8);
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+  }
+
+  dev::tc_fence_before();
+  dev::cluster_sync();
+  if (warp == 2) {
+    dev::tc_fence_after();
+    dev::tmem_dealloc_2sm<TMEM_COLS>(tmem_base);
+  }
+}
+
+template <Epi EPI>
+cudaError_t launch_2sm(const GemmParams& p, cudaStream_t stream) {
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(gemm_bf16_2sm_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         P_SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  CUtensorMap ta = p.a_mn_major ? make_tmap_bf16_2d(p.A, p.M, p.K, p.lda, 64, 64)
+                                : make_tmap_bf16_2d(p.A, p.K, p.M, p.lda, 64, BM);
+  CUtensorMap tb = p.b_mn_major ? make_tmap_bf16_2d(p.B, p.N, p.K, p.ldb, 64, 64)
+                                : make_tmap_bf16_2d(p.B, p.K, p.N, p.ldb, 64, 128);
+  const int num_tiles = ((p.M + 2 * BM - 1) / (2 * BM)) * ((p.N + BN - 1) / BN);
+  const int sms = (p.num_sms > 0 ? p.num_sms : device_sm_count()) & ~1;
+  const int grid = 2 * num_tiles < sms ? 2 * num_tiles : sms;
+  gemm_bf16_2sm_kernel<EPI><<<grid, NUM_THREADS, P_SMEM_BYTES, stream>>>(ta, tb, p);
+  return cudaGetLastError();
+}
+
 template <Epi EPI>
 cudaError_t launch(const GemmParams& p, cudaStream_t stream) {
+  if (use_pairs()) return launch_2sm<EPI>(p, stream);
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(gemm_bf16_kernel<EPI>,

@@ -151,7 +151,7 @@ def test_tensor_parallel_invariance():
     for mp in (2, 4):
         assert abs(res[mp][0] - res[1][0]) / res[1][0] < 2e-4
         for n in res[1][1]:
-            t = 1e-2 if n.endswith(SCORE_PATH) else 5e-3
+            t = 1e-2 if (n.endswith(SCORE_PATH) or n.startswith("embed/")) else 5e-3
             assert rel_l2(res[mp][1][n].astype(np.float64), res[1][1][n].astype(np.float64)) < t, (mp, n)
 
 
