@@ -423,6 +423,82 @@ __global__ void __launch_bounds__(512) xent_kernel(bf16* __restrict__ logits, in
   }
 }
 
+// ---- vocab-parallel cross entropy ----
+__global__ void __launch_bounds__(512) xent_vp_stats_kernel(const bf16* __restrict__ logits, int64_t ld, int Vl,
+                                                            int v0, const int32_t* __restrict__ targets,
+                                                            float* __restrict__ stats, float* __restrict__ tlogit) {
+  __shared__ float red_m[32], red_s[32];
+  const int64_t row = blockIdx.x;
+  const bf16* lr = logits + row * ld;
+  float mx = -INFINITY, se = 0.f;
+  for (int i = threadIdx.x; i < Vl; i += blockDim.x) {
+    const float x = __bfloat162float(lr[i]);
+    if (x > mx) {
+      se = se * __expf(mx - x) + 1.f;
+      mx = x;
+    } else {
+      se += __expf(x - mx);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float m2 = __shfl_xor_sync(0xffffffffu, mx, o);
+    const float s2 = __shfl_xor_sync(0xffffffffu, se, o);
+    const float m = fmaxf(mx, m2);
+    se = (mx == -INFINITY ? 0.f : se * __expf(mx - m)) + (m2 == -INFINITY ? 0.f : s2 * __expf(m2 - m));
+    mx = m;
+  }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) {
+    red_m[wid] = mx;
+    red_s[wid] = se;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float m = -INFINITY;
+    const int nw = blockDim.x / 32;
+    for (int w = 0; w < nw; ++w) m = fmaxf(m, red_m[w]);
+    float sum = 0.f;
+    for (int w = 0; w < nw; ++w) sum += red_s[w] * __expf(red_m[w] - m);
+    stats[2 * row] = m;
+    stats[2 * row + 1] = sum;
+    const int t = targets[row] - v0;
+    tlogit[row] = (t >= 0 && t < Vl) ? __bfloat162float(lr[t]) : 0.f;
+  }
+}
+
+__global__ void xent_vp_combine_kernel(const float* __restrict__ stats_all, int t, int64_t M,
+                                       const float* __restrict__ tlogit, const float* __restrict__ weights,
+                                       float* __restrict__ lse, float* __restrict__ wloss) {
+  for (int64_t m = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; m < M;
+       m += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    float mx = -INFINITY;
+    for (int r = 0; r < t; ++r) mx = fmaxf(mx, stats_all[(r * M + m) * 2]);
+    float s = 0.f;
+    for (int r = 0; r < t; ++r) s += stats_all[(r * M + m) * 2 + 1] * __expf(stats_all[(r * M + m) * 2] - mx);
+    const float l = mx + logf(s);
+    lse[m] = l;
+    wloss[m] = weights[m] * (l - tlogit[m]);
+  }
+}
+
+__global__ void __launch_bounds__(512) xent_vp_grad_kernel(bf16* __restrict__ logits, int64_t ld, int Vl, int v0,
+                                                           const int32_t* __restrict__ targets,
+                                                           const float* __restrict__ lse,
+                                                           const float* __restrict__ weights,
+                                                           const float* __restrict__ wsum) {
+  const int64_t row = blockIdx.x;
+  bf16* lr = logits + row * ld;
+  const float l = lse[row];
+  const float scale = weights[row] / *wsum;
+  const int t = targets[row] - v0;
+  for (int i = threadIdx.x; i < Vl; i += blockDim.x) {
+    float a = __expf(__bfloat162float(lr[i]) - l);
+    if (i == t) a -= 1.f;
+    lr[i] = __float2bfloat16(a * scale);
+  }
+}
+
 __global__ void add_residual_bias_kernel(const float* __restrict__ a, const float* __restrict__ b,
                                          const float* __restrict__ bias, float* __restrict__ y,
                                          int64_t n4, int d) {
@@ -619,6 +695,21 @@ void xent_fwd_bwd(bf16* logits, int64_t ld, int64_t M, int V, const int32_t* tar
                   cudaStream_t s) {
   xent_kernel<<<static_cast<unsigned>(M), 512, 0, s>>>(logits, ld, V, targets, weights, wsum, wloss,
                                                        write_grad);
+}
+
+void xent_vp_stats(const bf16* logits, int64_t ld, int64_t M, int Vl, int v0, const int32_t* targets,
+                   float* stats, float* tlogit, cudaStream_t s) {
+  xent_vp_stats_kernel<<<static_cast<unsigned>(M), 512, 0, s>>>(logits, ld, Vl, v0, targets, stats, tlogit);
+}
+
+void xent_vp_combine(const float* stats_all, int t, int64_t M, const float* tlogit, const float* weights,
+                     float* lse, float* wloss, cudaStream_t s) {
+  xent_vp_combine_kernel<<<grid_for(M, 256), 256, 0, s>>>(stats_all, t, M, tlogit, weights, lse, wloss);
+}
+
+void xent_vp_grad(bf16* logits, int64_t ld, int64_t M, int Vl, int v0, const int32_t* targets, const float* lse,
+                  const float* weights, const float* wsum, cudaStream_t s) {
+  xent_vp_grad_kernel<<<static_cast<unsigned>(M), 512, 0, s>>>(logits, ld, Vl, v0, targets, lse, weights, wsum);
 }
 
 void loss_reduce(const float* wloss, int64_t M, const float* wsum, double* loss, cudaStream_t s) {

@@ -45,6 +45,17 @@ void sum_f32(const float* x, int64_t n, float* out, cudaStream_t s);
 void xent_fwd_bwd(bf16* logits, int64_t ld, int64_t M, int V, const int32_t* targets,
                   const float* weights, const float* wsum, float* wloss, int write_grad,
                   cudaStream_t s);
+// Vocab-parallel cross entropy (logits split along the vocab across mp ranks; the lm_head
+// split:0 override of SURVEY D1). Rank-local pass: stats[2m] = local max, stats[2m+1] = sum of
+// exp(x - max); tlogit[m] = logit of the target if this rank owns it, else 0.
+void xent_vp_stats(const bf16* logits, int64_t ld, int64_t M, int Vl, int v0, const int32_t* targets,
+                   float* stats, float* tlogit, cudaStream_t s);
+// After gathering every rank's stats ([t][M*2]) and summing tlogit: lse[m], wloss[m].
+void xent_vp_combine(const float* stats_all, int t, int64_t M, const float* tlogit, const float* weights,
+                     float* lse, float* wloss, cudaStream_t s);
+// logits <- (exp(x - lse) - onehot) * w / wsum on the local vocab slice.
+void xent_vp_grad(bf16* logits, int64_t ld, int64_t M, int Vl, int v0, const int32_t* targets, const float* lse,
+                  const float* weights, const float* wsum, cudaStream_t s);
 // loss[0] = sum(wloss) / wsum (double)
 void loss_reduce(const float* wloss, int64_t M, const float* wsum, double* loss, cudaStream_t s);
 

@@ -214,10 +214,6 @@ void Model::build_layout() {
       unsupported("lm_head/kernel");
     }
   }
-  if (th_ > 1) {
-    fail(SW_ERR_PARTITION, "GPU executor: the vocab-parallel lm_head (split:0 at mp>1) is not "
-                           "implemented yet; use the default (replicated) plan");
-  }
   if (H_ % ta_ != 0) {
     fail(SW_ERR_PARTITION, "GPU executor: n_heads " + std::to_string(H_) + " not divisible by the " +
                                std::to_string(ta_) + "-way attention split (the reference all-gathers "
@@ -288,7 +284,10 @@ void Model::allocate() {
     if (3 * dl_ > widest) widest = 3 * dl_;
     if (fl_ > widest) widest = fl_;
     R.col_scratch = alloc<float>(chunks * widest);
-    R.attn_scratch = alloc<float>(M * hl_ + M * 2 * dl_);
+    R.attn_scratch = alloc<float>(M * hl_ + M * 2 * dl_ + 64);
+    R.xstats = alloc<float>(static_cast<int64_t>(mesh_->mp) * M * 2);
+    R.xt = alloc<float>(M);
+    R.xlse = alloc<float>(M);
     ranks_.push_back(R);
   }
   d_flag_ = alloc<int>(1);
@@ -480,6 +479,26 @@ void Model::ag_mp_slot(std::vector<Rank*>& grp, int slot, int64_t chunk) {
   mesh_->record(CollKind::kAllGather, mesh_->mp_group(grp[0]->dpi), static_cast<uint64_t>(chunk) * t * 4);
 }
 
+void Model::ag_mp_buf(std::vector<Rank*>& grp, float* Rank::*buf, int64_t chunk) {
+  if (mesh_->mp == 1) return;
+  const int t = mesh_->mp;
+  if (mesh_->emulated) {
+    for (Rank* src : grp) {
+      for (Rank* dst : grp) {
+        if (dst == src) continue;
+        cuda_check(cudaMemcpyAsync(dst->*buf + src->mpi * chunk, src->*buf + src->mpi * chunk, chunk * 4,
+                                   cudaMemcpyDeviceToDevice, stream_),
+                   "D2D");
+      }
+    }
+  } else {
+    Rank& R = *grp[0];
+    nccl_check(ncclAllGather(R.*buf + R.mpi * chunk, R.*buf, chunk, ncclFloat, mesh_->mp_comm, stream_),
+               "AllGather");
+  }
+  mesh_->record(CollKind::kAllGather, mesh_->mp_group(grp[0]->dpi), static_cast<uint64_t>(chunk) * t * 4);
+}
+
 void Model::gemm(Rank& R, int M, int N, int K, const void* A, int64_t lda, int a_mn, const void* B,
                  int64_t ldb, int b_mn, int epi, void* C, int64_t ldc, void* C2, int64_t ldc2,
                  const float* bias, const void* aux, int64_t ld_aux, int accumulate, int bias_seg,
@@ -593,12 +612,41 @@ void Model::forward_replica(std::vector<Rank*>& grp, bool need_grad) {
     gemm(*R, static_cast<int>(M), vl_, d, R->f, d, 0, W(*R, head), d, 0, static_cast<int>(Epi::kStoreBf16),
          R->logits, ldv_);
     k::sum_f32(R->weights, M, R->wsum, stream_);
-    tic();
-    k::xent_fwd_bwd(R->logits, ldv_, M, vl_, R->targets, R->weights, R->wsum, R->wloss, need_grad ? 1 : 0,
-                    stream_);
-    toc(kProfXent, (need_grad ? 4.0 : 2.0) * M * vl_);
+    ++launches_;
+  }
+  if (th_ == 1) {
+    for (Rank* R : grp) {
+      tic();
+      k::xent_fwd_bwd(R->logits, ldv_, M, vl_, R->targets, R->weights, R->wsum, R->wloss, need_grad ? 1 : 0,
+                      stream_);
+      toc(kProfXent, (need_grad ? 4.0 : 2.0) * M * vl_);
+      ++launches_;
+    }
+  } else {
+    // vocab-parallel CE: local (max, sumexp) + owned target logit, exchanged across the mp group
+    for (Rank* R : grp) {
+      tic();
+      k::xent_vp_stats(R->logits, ldv_, M, vl_, R->mpi * vl_, R->targets, R->xstats + R->mpi * M * 2, R->xt,
+                       stream_);
+      toc(kProfXent, 2.0 * M * vl_);
+      ++launches_;
+    }
+    ag_mp_buf(grp, &Rank::xstats, M * 2);
+    ar_mp(grp, &Rank::xt, M);
+    for (Rank* R : grp) {
+      k::xent_vp_combine(R->xstats, mesh_->mp, M, R->xt, R->weights, R->xlse, R->wloss, stream_);
+      ++launches_;
+      if (need_grad) {
+        tic();
+        k::xent_vp_grad(R->logits, ldv_, M, vl_, R->mpi * vl_, R->targets, R->xlse, R->weights, R->wsum, stream_);
+        toc(kProfXent, 4.0 * M * vl_);
+        ++launches_;
+      }
+    }
+  }
+  for (Rank* R : grp) {
     k::loss_reduce(R->wloss, M, R->wsum, R->loss, stream_);
-    launches_ += 3;
+    ++launches_;
   }
 }
 
@@ -639,6 +687,9 @@ void Model::backward_replica(std::vector<Rank*>& grp, bool accumulate) {
          static_cast<int>(Epi::kStoreF32), R->dx, d);
     gemm(*R, vl_, d, static_cast<int>(M), R->logits, ldv_, 1, R->f, d, 1, static_cast<int>(Epi::kStoreF32),
          G(*R, head), d, nullptr, 0, nullptr, nullptr, 0, acc);
+  }
+  if (th_ > 1) ar_mp(grp, &Rank::dx, M * d);  // vocab-parallel head: d(final_h) partials
+  for (Rank* R : grp) {
     tic();
     k::layernorm_bwd(R->hs[L_], R->statsf, R->statsf + M, P(*R, lnf_s_), R->dx, R->gres, R->gb, G(*R, lnf_s_),
                      G(*R, lnf_b_), M, d, 0, stream_);
@@ -842,11 +893,14 @@ void Model::logits_to_host(float* out) {
   const int first = mesh_->emulated ? 0 : ranks_[0].dpi;
   const int last = mesh_->emulated ? mesh_->dp - 1 : ranks_[0].dpi;
   for (int r = first; r <= last; ++r) {
-    Rank& R = *replica(r)[0];
-    cuda_check(cudaMemcpy(tmp.data(), R.logits, tmp.size() * 2, cudaMemcpyDeviceToHost), "D2H");
     float* o = out + (mesh_->emulated ? static_cast<int64_t>(r) * M_ * V_ : 0);
-    for (int64_t i = 0; i < M_; ++i)
-      for (int j = 0; j < V_; ++j) o[i * V_ + j] = __bfloat162float(tmp[i * ldv_ + j]);
+    for (Rank* R : replica(r)) {
+      if (th_ == 1 && R->mpi != 0) continue;
+      cuda_check(cudaMemcpy(tmp.data(), R->logits, tmp.size() * 2, cudaMemcpyDeviceToHost), "D2H");
+      const int64_t c0 = th_ == 1 ? 0 : static_cast<int64_t>(R->mpi) * vl_;
+      for (int64_t i = 0; i < M_; ++i)
+        for (int j = 0; j < vl_; ++j) o[i * V_ + c0 + j] = __bfloat162float(tmp[i * ldv_ + j]);
+    }
   }
 }
 

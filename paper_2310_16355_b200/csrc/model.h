@@ -60,6 +60,8 @@ struct Rank {
   double* loss = nullptr;
   // scratch
   float *part = nullptr, *dx = nullptr, *gres = nullptr, *col_scratch = nullptr, *attn_scratch = nullptr;
+  // vocab-parallel cross entropy: per-rank (max, sumexp) of every mp rank, target logit, lse
+  float *xstats = nullptr, *xt = nullptr, *xlse = nullptr;
   bf16 *gb = nullptr, *dpre = nullptr, *dout = nullptr, *dqkv = nullptr;
 };
 
@@ -114,6 +116,8 @@ class Model {
   void ar_mp(std::vector<Rank*>& grp, float* Rank::*buf, int64_t n);
   void ar_mp_ptrs(std::vector<Rank*>& grp, const std::vector<float*>& ptrs, int64_t n);
   void ag_mp_slot(std::vector<Rank*>& grp, int slot, int64_t chunk);
+  // in-place all-gather: chunk `mpi` of base(R) is local, the others arrive from the peers
+  void ag_mp_buf(std::vector<Rank*>& grp, float* Rank::*buf, int64_t chunk);
   void gemm(Rank& R, int M, int N, int K, const void* A, int64_t lda, int a_mn, const void* B,
             int64_t ldb, int b_mn, int epi, void* C, int64_t ldc, void* C2 = nullptr,
             int64_t ldc2 = 0, const float* bias = nullptr, const void* aux = nullptr,

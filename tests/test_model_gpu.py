@@ -96,6 +96,9 @@ def check_grads(model, spec, want, tol=1e-2):
     ("mini.spec", 2, 2, 2, 16),
     ("tiny.spec", 1, 1, 4, 128),
     ("tiny.spec", 1, 2, 4, 128),
+    ("tiny_vocab_parallel.spec", 1, 2, 4, 128),
+    ("tiny_vocab_parallel.spec", 2, 2, 2, 128),
+    ("mini_vocab_parallel.spec", 1, 4, 2, 16),
 ])
 def test_forward_backward_matches_oracle(spec_name, dp, mp, batch, seq):
     spec = spec_of(spec_name)
@@ -223,3 +226,27 @@ def test_nonfinite_gradient_raises():
     model.forward_backward()
     with pytest.raises(engine._lib.NonFiniteError, match="non-finite gradient for parameter"):
         model.adamw_step(engine.AdamWConfig())
+
+
+def test_vocab_parallel_head_plan_and_comm():
+    """With `role lm_head/kernel = fully_connected` the head is split:0; the step
+    exchanges (max, sumexp) stats + target logits instead of all-gathering the logits, and
+    all-reduces d(final_h) once."""
+    spec = spec_of("tiny_vocab_parallel.spec")
+    model, mesh, plan = make(spec, 1, 2, 4, 128)
+    assert plan.at("lm_head/kernel") == "split:0"
+    model.init_params(42, "model-init")
+    tokens, targets, weights = rng_ref.audit_batch(42, 0, 4, 128, spec.vocab_size)
+    model.stage_batch(tokens, targets, weights)
+    logits = model.forward_logits()
+    ref = oracle_params(spec)
+    _, _, want = model_ref.forward_backward(gemm_rounded(ref), spec_dict(spec), tokens, targets, weights,
+                                            need_grads=False)
+    assert rel_l2(logits.astype(np.float64), want) < 1e-2
+    mesh.reset_comm_report()
+    model.forward_backward()
+    csv = mesh.comm_report().splitlines()
+    ar, ag = csv[1].split(","), csv[2].split(",")
+    L = spec.n_layers
+    assert int(ar[1]) == 4 * L + 2  # + target-logit AR (fwd) + d(final_h) AR (bwd)
+    assert int(ag[1]) == 4 * L + 1  # + the CE stats all-gather
