@@ -38,7 +38,9 @@ def parse_args():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--spec", default=os.path.join(ROOT, "oracle", "specs", "llama7b.spec"))
+    ap.add_argument("--spec", default=os.path.join(ROOT, "oracle", "specs", "llama7b_vocab_parallel.spec"),
+                    help="model spec; the default carries `role lm_head/kernel = fully_connected` "
+                         "(vocab-parallel head, SURVEY D1) - identical to llama7b.spec at TP=1")
     ap.add_argument("--batch", type=int, default=4, help="sequences per replica per step")
     ap.add_argument("--seq", type=int, default=2048)
     ap.add_argument("--profile-steps", type=int, default=2)
@@ -205,25 +207,18 @@ def run_ours(args):
     import torch
 
     from paper_2310_16355_b200 import _lib, engine, rules
+    from paper_2310_16355_b200 import dist as D
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    info = D.rank_info()
+    world, rank, local = info.world, info.rank, info.local_rank
     torch.cuda.set_device(local)
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("gloo", rank=rank, world_size=world)
+    dist = D.init_host_group(info)
     tp, dp = world, 1
 
     spec = rules.read_model_spec(args.spec)
     shapes = rules.transformer_param_shapes(spec)
     plan = rules.derive_plan(shapes, tp, spec.overrides)
-    nccl_id = None
-    if world > 1:
-        obj = [engine.nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        nccl_id = obj[0]
+    nccl_id = D.share_nccl_id(dist, rank)
     mesh = engine.Mesh(dp, tp, 1, rank if world > 1 else 0, world, nccl_id, local)
     B, T = args.batch, args.seq
     model = engine.Model(spec, plan, mesh, B, T)
@@ -244,11 +239,7 @@ def run_ours(args):
             dist.barrier()
 
     def max_over_ranks(x):
-        if dist is None:
-            return x
-        t = torch.tensor([x], dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t[0])
+        return D.max_over_ranks(dist, x)
 
     # ---- device-resident inputs: value ----
     model.stage_batch(*batches[0], ones)
@@ -327,7 +318,8 @@ def run_ours(args):
                                f"train step: fwd+bwd+AdamW, seq {T}",
                    "spec": os.path.relpath(args.spec, ROOT), "global_batch": rows, "seq_len": T,
                    "parallelism": f"tp{tp}" if dp == 1 else f"dp{dp}xtp{tp}",
-                   "plan": "reference rules (derive_plan), lm_head replicated",
+                   "plan": "reference rules (derive_plan) + spec overrides: lm_head/kernel "
+                           + plan.at("lm_head/kernel") + (" (vocab-parallel)" if tp > 1 and plan.at("lm_head/kernel") == "split:0" else ""),
                    "l2": "inputs larger than L2 (activations/weights >> 126 MB); no flush"},
         "mfu": {"tflops_per_gpu": round(step_tflops_per_gpu, 1),
                 "frac_of_measured_bf16_sustained": round(step_tflops_per_gpu / peak_t, 3),
