@@ -54,17 +54,18 @@ struct FwdLayout {
   static constexpr int OFF_K = OFF_Q + Q;
   static constexpr int OFF_V = OFF_K + 2 * KV;
   static constexpr int OFF_P = OFF_V + 2 * KV;
-  static constexpr int OFF_BAR = OFF_P + 2 * P;
-  static constexpr int BYTES = OFF_BAR + 256 + 1024;
+  static constexpr int OFF_X = OFF_P + 2 * P;  // row max / row sum exchange, [2][2][128] floats
+  static constexpr int OFF_BAR = OFF_X + 4 * 128 * 4;
+  static constexpr int BYTES = OFF_BAR + 128;  // the dynamic smem base is 1024-aligned (declared)
 };
 
 template <int HD>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(384, 1)
     attn_fwd_tc(const __grid_constant__ CUtensorMap tm, bf16* __restrict__ out, float* __restrict__ lse,
                 int T, int Hl, float scale_log2, float scale) {
   using Lay = FwdLayout<HD>;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw;
   uint8_t* sQ = smem + Lay::OFF_Q;
   uint8_t* sK = smem + Lay::OFF_K;
   uint8_t* sV = smem + Lay::OFF_V;
@@ -97,7 +98,7 @@ __global__ void __launch_bounds__(256, 1)
       dev::mbar_init(&kv_full[i], 1);
       dev::mbar_init(&kv_empty[i], 1);
       dev::mbar_init(&s_full[i], 1);
-      dev::mbar_init(&p_full[i], 128);
+      dev::mbar_init(&p_full[i], 256);
       dev::mbar_init(&pv_done[i], 1);
     }
     dev::fence_barrier_init();
@@ -159,34 +160,38 @@ __global__ void __launch_bounds__(256, 1)
       issue_pv(nkv - 1);
     }
   } else if (warp >= 4) {
-    const int r = static_cast<int>(threadIdx.x) - 128;  // query row within the block
+    // Two softmax warpgroups: warps 4-7 own keys [0, 64) of every query row, warps 8-11 keys
+    // [64, 128); the row max and the final row sum are exchanged through shared memory.
+    const int wg = (static_cast<int>(warp) - 4) >> 2;
+    const int r = static_cast<int>(threadIdx.x) - 128 - wg * 128;  // query row within the block
     const int q = q0 + r;
     const uint32_t lane_base = static_cast<uint32_t>((warp & 3) * 32) << 16;
+    float* xm = reinterpret_cast<float*>(smem + Lay::OFF_X);  // [parity][wg][128]
     float m_used = -INFINITY, l = 0.f;
     for (int j = 0; j < nkv; ++j) {
       const int bb = j & 1;
       dev::mbar_wait(&s_full[bb], (j >> 1) & 1);
       dev::tc_fence_after();
-      const uint32_t ts = tmem + lane_base + bb * 128;
+      const uint32_t ts = tmem + lane_base + bb * 128 + wg * 64;
       const bool diag = (j == nkv - 1);
-      const int key0 = j * BKV;
-      // one pass over the 128 scores of this row: all four TMEM loads in flight, one wait
-      uint32_t v[128];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        dev::tmem_ld_32x32b_x32(ts + c * 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32 * c));
-      }
+      const int key0 = j * BKV + wg * 64;
+      uint32_t v[64];
+      dev::tmem_ld_32x32b_x32(ts, *reinterpret_cast<uint32_t(*)[32]>(v));
+      dev::tmem_ld_32x32b_x32(ts + 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
       dev::tmem_ld_wait();
       if (diag) {
 #pragma unroll
-        for (int i = 0; i < 128; ++i) {
+        for (int i = 0; i < 64; ++i) {
           const int key = key0 + i;
           if (!(key <= q && key < T)) v[i] = __float_as_uint(-INFINITY);
         }
       }
-      float mx = __uint_as_float(v[0]);
+      float mloc = __uint_as_float(v[0]);
 #pragma unroll
-      for (int i = 1; i < 128; ++i) mx = fmaxf(mx, __uint_as_float(v[i]));
+      for (int i = 1; i < 64; ++i) mloc = fmaxf(mloc, __uint_as_float(v[i]));
+      xm[(bb * 2 + wg) * 128 + r] = mloc;
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+      const float mx = fmaxf(mloc, xm[(bb * 2 + (wg ^ 1)) * 128 + r]);
       // lazy rescale: keep the stale max unless the new one is 2^8 larger in exp2 units
       bool resc = false;
       float factor = 1.f;
@@ -203,7 +208,7 @@ __global__ void __launch_bounds__(256, 1)
         dev::mbar_wait(&pv_done[(j - 1) & 1], ((j - 1) >> 1) & 1);
         dev::tc_fence_after();
 #pragma unroll 1
-        for (int c = 0; c < HD / 32; ++c) {
+        for (int c = wg * (HD / 64); c < (wg + 1) * (HD / 64); ++c) {
           uint32_t o[32];
           dev::tmem_ld_32x32b_x32(t_o + lane_base + c * 32, o);
           dev::tmem_ld_wait();
@@ -219,7 +224,7 @@ __global__ void __launch_bounds__(256, 1)
       uint8_t* tile = sP + bb * Lay::P;
       float ls = 0.f;
 #pragma unroll
-      for (int c = 0; c < 16; ++c) {  // 16 units of 8 keys
+      for (int c = 0; c < 8; ++c) {  // 8 units of 8 keys
         uint32_t pk[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
@@ -228,20 +233,25 @@ __global__ void __launch_bounds__(256, 1)
           ls += p0 + p1;
           pk[e] = dev::pack_bf16x2(p0, p1);
         }
-        dev::st_sw128(tile, BQ, r, c >> 3, c & 7, make_uint4(pk[0], pk[1], pk[2], pk[3]));
+        dev::st_sw128(tile, BQ, r, wg, c, make_uint4(pk[0], pk[1], pk[2], pk[3]));
       }
       l += ls;
       dev::fence_proxy_async_smem();
       dev::tc_fence_before();
       dev::mbar_arrive(&p_full[bb]);
     }
-    // epilogue: O / l
+    // epilogue: O / l with l summed over both halves (the other parity's exchange slots were
+    // last read before the final block's barrier)
+    const int xp = ((nkv - 1) & 1) ^ 1;
+    xm[(xp * 2 + wg) * 128 + r] = l;
+    asm volatile("bar.sync 1, 256;" ::: "memory");
+    l += xm[(xp * 2 + (wg ^ 1)) * 128 + r];
     dev::mbar_wait(&pv_done[(nkv - 1) & 1], ((nkv - 1) >> 1) & 1);
     dev::tc_fence_after();
     const float inv = 1.f / l;
     bf16* orow = out + (static_cast<int64_t>(row0) + q) * Dl + h * HD;
 #pragma unroll
-    for (int c = 0; c < HD / 32; ++c) {
+    for (int c = wg * (HD / 64); c < (wg + 1) * (HD / 64); ++c) {
       uint32_t v[32];
       dev::tmem_ld_32x32b_x32(t_o + lane_base + c * 32, v);
       dev::tmem_ld_wait();
@@ -257,7 +267,7 @@ __global__ void __launch_bounds__(256, 1)
         }
       }
     }
-    if (q < T) lse[static_cast<int64_t>(bh) * T + q] = m_used * scale + logf(l);
+    if (wg == 0 && q < T) lse[static_cast<int64_t>(bh) * T + q] = m_used * scale + logf(l);
   }
   dev::tc_fence_before();
   __syncthreads();
@@ -282,7 +292,7 @@ bool launch_fwd(const bf16* qkv, bf16* o, float* lse, int B, int T, int Hl, cuda
   const CUtensorMap tm = make_tmap_bf16_2d(qkv, 3ull * Dl, static_cast<uint64_t>(B) * T, 3ull * Dl, 64, 128);
   const int nqb = (T + BQ - 1) / BQ;
   const double scale = 1.0 / std::sqrt(static_cast<double>(HD));
-  attn_fwd_tc<HD><<<nqb * B * Hl, 256, Lay::BYTES, s>>>(tm, o, lse, T, Hl,
+  attn_fwd_tc<HD><<<nqb * B * Hl, 384, Lay::BYTES, s>>>(tm, o, lse, T, Hl,
                                                          static_cast<float>(scale * 1.4426950408889634),
                                                          static_cast<float>(scale));
   return true;
@@ -308,8 +318,9 @@ struct BwdLayout {
 };
 
 template <int HD>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(384, 1)
     attn_bwd_tc(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
+                const __grid_constant__ CUtensorMap tm_dq,
                 const float* __restrict__ lse, const float* __restrict__ delta, float* __restrict__ dq_acc,
                 bf16* __restrict__ dqkv, int T, int Hl, float scale_log2, float scale) {
   using Lay = BwdLayout<HD>;
@@ -347,13 +358,14 @@ __global__ void __launch_bounds__(256, 1)
   if (warp == 0 && lane == 0) {
     dev::tma_prefetch_desc(&tm_qkv);
     dev::tma_prefetch_desc(&tm_do);
+    dev::tma_prefetch_desc(&tm_dq);
     dev::mbar_init(kv_full, 1);
     dev::mbar_init(qdo_full, 1);
     dev::mbar_init(qdo_empty, 1);
     dev::mbar_init(st_full, 1);
-    dev::mbar_init(p_full, 128);
+    dev::mbar_init(p_full, 256);
     dev::mbar_init(mma_done, 1);
-    dev::mbar_init(dq_free, 128);
+    dev::mbar_init(dq_free, 256);
     dev::fence_barrier_init();
   }
   if (warp == 2) dev::tmem_alloc<512>(tmem_slot);
@@ -414,26 +426,34 @@ __global__ void __launch_bounds__(256, 1)
       }
     }
   } else if (warp >= 4) {
-    const int t = static_cast<int>(threadIdx.x) - 128;  // key row (S^T lane) / query row (dQ lane)
+    // Two softmax warpgroups: warps 4-7 take query columns [0, 64) of every key row, warps 8-11
+    // columns [64, 128) (TMEM lane quarter = warp % 4 for both).
+    const int wg = (static_cast<int>(warp) - 4) >> 2;                     // 0 or 1
+    const int t = static_cast<int>(threadIdx.x) - 128 - wg * 128;        // key row (S^T lane) / query row (dQ lane)
+    const int tid = static_cast<int>(threadIdx.x) - 128;                 // 0..255
     const int key = key0 + t;
     const uint32_t lane_base = static_cast<uint32_t>((warp & 3) * 32) << 16;
     const float log2e = 1.4426950408889634f;
+    uint8_t* stage = wg == 0 ? sPt : sDSt;  // dQ staging tile of this warpgroup (free after mma_done)
     for (int n = 0; n < nq; ++n) {
       const int qs = (kb + n) * 128;
       float* st_lse = sStat + (n & 1) * 256;
       float* st_del = st_lse + 128;
-      {
-        const int qq = qs + t;
-        st_lse[t] = qq < T ? lse[static_cast<int64_t>(bh) * T + qq] * log2e : 0.f;
-        st_del[t] = qq < T ? delta[static_cast<int64_t>(bh) * T + qq] : 0.f;
+      if (tid < 128) {
+        const int qq = qs + tid;
+        st_lse[tid] = qq < T ? lse[static_cast<int64_t>(bh) * T + qq] * log2e : 0.f;
+      } else {
+        const int qq = qs + tid - 128;
+        st_del[tid - 128] = qq < T ? delta[static_cast<int64_t>(bh) * T + qq] : 0.f;
       }
-      asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (t == 0) dev::bulk_wait_read();  // sPt / sDSt double as the dQ staging tiles
+      asm volatile("bar.sync 1, 256;" ::: "memory");
       dev::mbar_wait(st_full, n & 1);
       dev::tc_fence_after();
       if (n >= 1) dev::mbar_wait(mma_done, (n - 1) & 1);  // sPt / sDSt free again
       const bool diag = (n == 0);
-#pragma unroll 1
-      for (int half = 0; half < 2; ++half) {
+      {
+        const int half = wg;
         // 64 query columns of S^T and dP^T: four TMEM loads in flight, one wait
         uint32_t sv[64], pv[64];
         dev::tmem_ld_32x32b_x32(t_s + lane_base + half * 64, *reinterpret_cast<uint32_t(*)[32]>(sv));
@@ -468,35 +488,50 @@ __global__ void __launch_bounds__(256, 1)
       dev::fence_proxy_async_smem();
       dev::tc_fence_before();
       dev::mbar_arrive(p_full);
-      // dQ_i (TMEM lane = query row) -> fp32 reductions into the dQ accumulator
+      // dQ_i rows (TMEM lane = query row): each warpgroup stages HD/2 fp32 columns in SW128
+      // tiles (32 columns each) and TMA reduce-adds them into the fp32 dQ accumulator
+      // (rows past T carry zeros: dS is masked there).
       dev::mbar_wait(mma_done, n & 1);
       dev::tc_fence_after();
-      const int qq = qs + t;
-      float* dst = dq_acc + (static_cast<int64_t>(row0) + qq) * Dl + h * HD;
-#pragma unroll 1
-      for (int c = 0; c < HD / 32; ++c) {
-        uint32_t v[32];
-        dev::tmem_ld_32x32b_x32(t_dq + lane_base + c * 32, v);
-        dev::tmem_ld_wait();
-        if (qq < T) {
+      constexpr int HALF = HD / 2;
+      uint32_t v[HALF];
 #pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            dev::red_add_v4(dst + c * 32 + 4 * u, __uint_as_float(v[4 * u]), __uint_as_float(v[4 * u + 1]),
-                            __uint_as_float(v[4 * u + 2]), __uint_as_float(v[4 * u + 3]));
-          }
+      for (int c = 0; c < HALF / 32; ++c)
+        dev::tmem_ld_32x32b_x32(t_dq + lane_base + wg * HALF + c * 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32 * c));
+      dev::tmem_ld_wait();
+      dev::tc_fence_before();
+      dev::mbar_arrive(dq_free);  // TMEM read: the next S^T may overwrite it
+#pragma unroll
+      for (int bx = 0; bx < HALF / 32; ++bx) {
+        uint8_t* tile = stage + bx * 16384;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int c = bx * 32 + u * 4;
+          *reinterpret_cast<uint4*>(tile + t * 128 + ((u ^ (t & 7)) << 4)) = make_uint4(v[c], v[c + 1], v[c + 2], v[c + 3]);
         }
       }
-      dev::tc_fence_before();
-      dev::mbar_arrive(dq_free);
+      dev::fence_proxy_async_smem();
+      if (wg == 0) {
+        asm volatile("bar.sync 2, 128;" ::: "memory");
+      } else {
+        asm volatile("bar.sync 3, 128;" ::: "memory");
+      }
+      if (t == 0) {
+#pragma unroll
+        for (int bx = 0; bx < HALF / 32; ++bx)
+          dev::tma_reduce_add_2d(&tm_dq, stage + bx * 16384, h * HD + wg * HALF + bx * 32, row0 + qs);
+        dev::bulk_commit();
+      }
     }
-    // dK, dV (lane = key row) -> bf16 rows of dqkv
+    if (t == 0) dev::bulk_wait_all();
+    // dK, dV (lane = key row) -> bf16 rows of dqkv; each warpgroup writes HD/2 columns
     dev::mbar_wait(mma_done, (nq - 1) & 1);
     dev::tc_fence_after();
     const int64_t ld = 3LL * Dl;
     bf16* dk_row = dqkv + (static_cast<int64_t>(row0) + key) * ld + Dl + h * HD;
     bf16* dv_row = dk_row + Dl;
 #pragma unroll 1
-    for (int c = 0; c < HD / 32; ++c) {
+    for (int c = wg * (HD / 64); c < (wg + 1) * (HD / 64); ++c) {
       uint32_t a[32], v[32];
       dev::tmem_ld_32x32b_x32(t_dk + lane_base + c * 32, a);
       dev::tmem_ld_32x32b_x32(t_dv + lane_base + c * 32, v);
@@ -585,9 +620,11 @@ bool launch_bwd(const bf16* qkv, const bf16* o, const float* lse, const bf16* do
   const CUtensorMap tm_qkv = make_tmap_bf16_2d(qkv, 3ull * Dl, static_cast<uint64_t>(M), 3ull * Dl, 64, 128);
   const CUtensorMap tm_do = make_tmap_bf16_2d(dout, static_cast<uint64_t>(Dl), static_cast<uint64_t>(M),
                                               static_cast<uint64_t>(Dl), 64, 128);
+  const CUtensorMap tm_dq = make_tmap_f32_2d(dq, static_cast<uint64_t>(Dl), static_cast<uint64_t>(M),
+                                             static_cast<uint64_t>(Dl), 32, 128);
   const int nb = (T + 127) / 128;
   const double scale = 1.0 / std::sqrt(static_cast<double>(HD));
-  attn_bwd_tc<HD><<<nb * B * Hl, 256, Lay::BYTES, s>>>(tm_qkv, tm_do, lse, delta, dq, dqkv, T, Hl,
+  attn_bwd_tc<HD><<<nb * B * Hl, 384, Lay::BYTES, s>>>(tm_qkv, tm_do, tm_dq, lse, delta, dq, dqkv, T, Hl,
                                                         static_cast<float>(scale * 1.4426950408889634),
                                                         static_cast<float>(scale));
   dq_to_bf16<<<1184, 256, 0, s>>>(dq, dqkv, M, Dl);
