@@ -2,6 +2,7 @@
 #include "model.h"
 
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <stdexcept>
 
@@ -66,13 +67,31 @@ Model::Model(const ModelSpec& spec, const Plan& plan, Mesh* mesh, int batch, int
   S_ = static_cast<int>(spec.max_seq_len);
   cuda_check(cudaSetDevice(mesh->cuda_device), "cudaSetDevice");
   cuda_check(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "cudaStreamCreate");
+  cuda_check(cudaStreamCreateWithFlags(&comm_stream_, cudaStreamNonBlocking), "cudaStreamCreate");
   build_layout();
   allocate();
+  // all-reduce pipelining depth (SW_AR_CHUNKS overrides): 4 row chunks when they stay 128-aligned
+  ar_chunks_ = (mesh_->mp > 1 && M_ % (4 * 128) == 0) ? 4 : 1;
+  if (const char* e = std::getenv("SW_AR_CHUNKS")) {
+    const int c = std::atoi(e);
+    if (c >= 1 && M_ % c == 0) ar_chunks_ = c;
+  }
+  for (int i = 0; i < ar_chunks_; ++i) {
+    cudaEvent_t a, b;
+    cuda_check(cudaEventCreateWithFlags(&a, cudaEventDisableTiming), "cudaEventCreate");
+    cuda_check(cudaEventCreateWithFlags(&b, cudaEventDisableTiming), "cudaEventCreate");
+    ev_prod_.push_back(a);
+    ev_ar_.push_back(b);
+  }
 }
 
 Model::~Model() {
   if (stream_) cudaStreamSynchronize(stream_);
+  if (comm_stream_) cudaStreamSynchronize(comm_stream_);
   for (cudaEvent_t e : events_) cudaEventDestroy(e);
+  for (cudaEvent_t e : ev_prod_) cudaEventDestroy(e);
+  for (cudaEvent_t e : ev_ar_) cudaEventDestroy(e);
+  if (comm_stream_) cudaStreamDestroy(comm_stream_);
   for (void* p : allocations_) cudaFree(p);
   if (stream_) cudaStreamDestroy(stream_);
 }
@@ -438,18 +457,38 @@ void Model::stage_batch(const int32_t* tokens, const int32_t* targets, const flo
 // ---------------------------------------------------------------------------------------------
 // collectives
 // ---------------------------------------------------------------------------------------------
-void Model::ar_mp_ptrs(std::vector<Rank*>& grp, const std::vector<float*>& ptrs, int64_t n) {
+void Model::ar_mp_ptrs(std::vector<Rank*>& grp, const std::vector<float*>& ptrs, int64_t n, cudaStream_t s) {
   if (mesh_->mp == 1) return;
+  if (s == nullptr) s = stream_;
   const double t = mesh_->mp;
-  tic();
+  tic(s);
   if (mesh_->emulated) {
-    k::sum_ranks_f32(ptrs.data(), static_cast<int>(ptrs.size()), n, 1.0f, stream_);
+    k::sum_ranks_f32(ptrs.data(), static_cast<int>(ptrs.size()), n, 1.0f, s);
     ++launches_;
   } else {
-    nccl_check(ncclAllReduce(ptrs[0], ptrs[0], n, ncclFloat, ncclSum, mesh_->mp_comm, stream_), "AllReduce");
+    nccl_check(ncclAllReduce(ptrs[0], ptrs[0], n, ncclFloat, ncclSum, mesh_->mp_comm, s), "AllReduce");
   }
-  toc(kProfComm, 2.0 * (t - 1) / t * 4.0 * n);  // NCCL bus bytes
+  toc(kProfComm, 2.0 * (t - 1) / t * 4.0 * n, s);  // NCCL bus bytes
   mesh_->record(CollKind::kAllReduce, mesh_->mp_group(grp[0]->dpi), static_cast<uint64_t>(n) * 4);
+}
+
+void Model::row_parallel_ar(std::vector<Rank*>& grp, float* Rank::*buf, int width, const RowFn& produce,
+                            const RowFn& consume) {
+  const int C = ar_chunks_;
+  const int64_t rows = M_ / C;
+  for (int c = 0; c < C; ++c) {
+    for (Rank* R : grp) produce(*R, c * rows, rows);
+    cuda_check(cudaEventRecord(ev_prod_[c], stream_), "cudaEventRecord");
+    cuda_check(cudaStreamWaitEvent(comm_stream_, ev_prod_[c], 0), "cudaStreamWaitEvent");
+    std::vector<float*> ptrs;
+    for (Rank* R : grp) ptrs.push_back(R->*buf + c * rows * width);
+    ar_mp_ptrs(grp, ptrs, rows * width, comm_stream_);
+    cuda_check(cudaEventRecord(ev_ar_[c], comm_stream_), "cudaEventRecord");
+  }
+  for (int c = 0; c < C; ++c) {
+    cuda_check(cudaStreamWaitEvent(stream_, ev_ar_[c], 0), "cudaStreamWaitEvent");
+    for (Rank* R : grp) consume(*R, c * rows, rows);
+  }
 }
 
 void Model::ar_mp(std::vector<Rank*>& grp, float* Rank::*buf, int64_t n) {
@@ -565,15 +604,17 @@ void Model::forward_replica(std::vector<Rank*>& grp, bool need_grad) {
              static_cast<int>(Epi::kResidF32), R->hmid[l], d, nullptr, 0, P(*R, ls.o_b), R->hs[l], d);
       }
     } else {
-      for (Rank* R : grp) {
-        gemm(*R, static_cast<int>(M), d, dl, R->o[l], dl, 0, W(*R, ls.o_k), dl, 0,
-             static_cast<int>(Epi::kStoreF32), R->part, d);
-      }
-      ar_mp(grp, &Rank::part, M * d);
-      for (Rank* R : grp) {
-        k::add_residual_bias(R->hs[l], R->part, P(*R, ls.o_b), R->hmid[l], M, d, stream_);
-        ++launches_;
-      }
+      row_parallel_ar(
+          grp, &Rank::part, d,
+          [&](Rank& R, int64_t r0, int64_t rows) {
+            gemm(R, static_cast<int>(rows), d, dl, R.o[l] + r0 * dl, dl, 0, W(R, ls.o_k), dl, 0,
+                 static_cast<int>(Epi::kStoreF32), R.part + r0 * d, d);
+          },
+          [&](Rank& R, int64_t r0, int64_t rows) {
+            k::add_residual_bias(R.hs[l] + r0 * d, R.part + r0 * d, P(R, ls.o_b), R.hmid[l] + r0 * d, rows, d,
+                                 stream_);
+            ++launches_;
+          });
     }
     for (Rank* R : grp) {
       tic();
@@ -590,15 +631,17 @@ void Model::forward_replica(std::vector<Rank*>& grp, bool need_grad) {
              static_cast<int>(Epi::kResidF32), R->hs[l + 1], d, nullptr, 0, P(*R, ls.fc2_b), R->hmid[l], d);
       }
     } else {
-      for (Rank* R : grp) {
-        gemm(*R, static_cast<int>(M), d, fl, R->act[l], fl, 0, W(*R, ls.fc2_k), fl, 0,
-             static_cast<int>(Epi::kStoreF32), R->part, d);
-      }
-      ar_mp(grp, &Rank::part, M * d);
-      for (Rank* R : grp) {
-        k::add_residual_bias(R->hmid[l], R->part, P(*R, ls.fc2_b), R->hs[l + 1], M, d, stream_);
-        ++launches_;
-      }
+      row_parallel_ar(
+          grp, &Rank::part, d,
+          [&](Rank& R, int64_t r0, int64_t rows) {
+            gemm(R, static_cast<int>(rows), d, fl, R.act[l] + r0 * fl, fl, 0, W(R, ls.fc2_k), fl, 0,
+                 static_cast<int>(Epi::kStoreF32), R.part + r0 * d, d);
+          },
+          [&](Rank& R, int64_t r0, int64_t rows) {
+            k::add_residual_bias(R.hmid[l] + r0 * d, R.part + r0 * d, P(R, ls.fc2_b), R.hs[l + 1] + r0 * d, rows,
+                                 d, stream_);
+            ++launches_;
+          });
     }
   }
   const int head = head_ >= 0 ? head_ : tok_;
@@ -682,19 +725,29 @@ void Model::backward_replica(std::vector<Rank*>& grp, bool accumulate) {
     }
   }
   for (Rank* R : grp) {
-    // head: d(final_h) = dlogits . W_head ; dW_head (+)= dlogits^T . final_h
-    gemm(*R, static_cast<int>(M), d, vl_, R->logits, ldv_, 0, W(*R, head), d, 1,
-         static_cast<int>(Epi::kStoreF32), R->dx, d);
+    // dW_head (+)= dlogits^T . final_h
     gemm(*R, vl_, d, static_cast<int>(M), R->logits, ldv_, 1, R->f, d, 1, static_cast<int>(Epi::kStoreF32),
          G(*R, head), d, nullptr, 0, nullptr, nullptr, 0, acc);
   }
-  if (th_ > 1) ar_mp(grp, &Rank::dx, M * d);  // vocab-parallel head: d(final_h) partials
-  for (Rank* R : grp) {
-    tic();
-    k::layernorm_bwd(R->hs[L_], R->statsf, R->statsf + M, P(*R, lnf_s_), R->dx, R->gres, R->gb, G(*R, lnf_s_),
-                     G(*R, lnf_b_), M, d, 0, stream_);
-    toc(kProfNorm, 18.0 * M * d);
-    ++launches_;
+  {
+    // d(final_h) = dlogits . W_head (partial over the vocab shards when the head is split)
+    auto prod = [&](Rank& R, int64_t r0, int64_t rows) {
+      gemm(R, static_cast<int>(rows), d, vl_, R.logits + r0 * ldv_, ldv_, 0, W(R, head), d, 1,
+           static_cast<int>(Epi::kStoreF32), R.dx + r0 * d, d);
+    };
+    auto cons = [&](Rank& R, int64_t r0, int64_t rows) {
+      tic();
+      k::layernorm_bwd(R.hs[L_] + r0 * d, R.statsf + r0, R.statsf + M + r0, P(R, lnf_s_), R.dx + r0 * d,
+                       R.gres + r0 * d, R.gb + r0 * d, G(R, lnf_s_), G(R, lnf_b_), rows, d, 0, stream_);
+      toc(kProfNorm, 18.0 * rows * d);
+      ++launches_;
+    };
+    if (th_ > 1) {
+      row_parallel_ar(grp, &Rank::dx, d, prod, cons);
+    } else {
+      for (Rank* R : grp) prod(*R, 0, M);
+      for (Rank* R : grp) cons(*R, 0, M);
+    }
   }
   for (int l = L_ - 1; l >= 0; --l) {
     const LayerSlots& ls = layers_[l];
@@ -711,16 +764,25 @@ void Model::backward_replica(std::vector<Rank*>& grp, bool accumulate) {
       launches_ += 2;
       gemm(*R, fl, d, static_cast<int>(M), R->dpre, fl, 1, R->a2[l], d, 1, static_cast<int>(Epi::kStoreF32),
            G(*R, ls.fc1_k), d, nullptr, 0, nullptr, nullptr, 0, acc);
-      gemm(*R, static_cast<int>(M), d, fl, R->dpre, fl, 0, W(*R, ls.fc1_k), d, 1,
-           static_cast<int>(Epi::kStoreF32), R->dx, d);
     }
-    if (tm_ > 1) ar_mp(grp, &Rank::dx, M * d);
-    for (Rank* R : grp) {
-      tic();
-      k::layernorm_bwd(R->hmid[l], R->stats2[l], R->stats2[l] + M, P(*R, ls.ln2_s), R->dx, R->gres, R->gb,
-                       G(*R, ls.ln2_s), G(*R, ls.ln2_b), M, d, 1, stream_);
-      toc(kProfNorm, 18.0 * M * d);
-      ++launches_;
+    {
+      auto prod = [&](Rank& R, int64_t r0, int64_t rows) {
+        gemm(R, static_cast<int>(rows), d, fl, R.dpre + r0 * fl, fl, 0, W(R, ls.fc1_k), d, 1,
+             static_cast<int>(Epi::kStoreF32), R.dx + r0 * d, d);
+      };
+      auto cons = [&](Rank& R, int64_t r0, int64_t rows) {
+        tic();
+        k::layernorm_bwd(R.hmid[l] + r0 * d, R.stats2[l] + r0, R.stats2[l] + M + r0, P(R, ls.ln2_s), R.dx + r0 * d,
+                         R.gres + r0 * d, R.gb + r0 * d, G(R, ls.ln2_s), G(R, ls.ln2_b), rows, d, 1, stream_);
+        toc(kProfNorm, 18.0 * rows * d);
+        ++launches_;
+      };
+      if (tm_ > 1) {
+        row_parallel_ar(grp, &Rank::dx, d, prod, cons);
+      } else {
+        for (Rank* R : grp) prod(*R, 0, M);
+        for (Rank* R : grp) cons(*R, 0, M);
+      }
     }
     // ---- attention ----
     for (Rank* R : grp) {
@@ -740,16 +802,25 @@ void Model::backward_replica(std::vector<Rank*>& grp, bool accumulate) {
       launches_ += 2;
       gemm(*R, 3 * dl, d, static_cast<int>(M), R->dqkv, 3 * dl, 1, R->a1[l], d, 1,
            static_cast<int>(Epi::kStoreF32), G(*R, ls.q_k), d, nullptr, 0, nullptr, nullptr, 0, acc);
-      gemm(*R, static_cast<int>(M), d, 3 * dl, R->dqkv, 3 * dl, 0, W(*R, ls.q_k), d, 1,
-           static_cast<int>(Epi::kStoreF32), R->dx, d);
     }
-    if (ta_ > 1) ar_mp(grp, &Rank::dx, M * d);
-    for (Rank* R : grp) {
-      tic();
-      k::layernorm_bwd(R->hs[l], R->stats1[l], R->stats1[l] + M, P(*R, ls.ln1_s), R->dx, R->gres, R->gb,
-                       G(*R, ls.ln1_s), G(*R, ls.ln1_b), M, d, 1, stream_);
-      toc(kProfNorm, 18.0 * M * d);
-      ++launches_;
+    {
+      auto prod = [&](Rank& R, int64_t r0, int64_t rows) {
+        gemm(R, static_cast<int>(rows), d, 3 * dl, R.dqkv + r0 * 3 * dl, 3 * dl, 0, W(R, ls.q_k), d, 1,
+             static_cast<int>(Epi::kStoreF32), R.dx + r0 * d, d);
+      };
+      auto cons = [&](Rank& R, int64_t r0, int64_t rows) {
+        tic();
+        k::layernorm_bwd(R.hs[l] + r0 * d, R.stats1[l] + r0, R.stats1[l] + M + r0, P(R, ls.ln1_s), R.dx + r0 * d,
+                         R.gres + r0 * d, R.gb + r0 * d, G(R, ls.ln1_s), G(R, ls.ln1_b), rows, d, 1, stream_);
+        toc(kProfNorm, 18.0 * rows * d);
+        ++launches_;
+      };
+      if (ta_ > 1) {
+        row_parallel_ar(grp, &Rank::dx, d, prod, cons);
+      } else {
+        for (Rank* R : grp) prod(*R, 0, M);
+        for (Rank* R : grp) cons(*R, 0, M);
+      }
     }
   }
   for (Rank* R : grp) {
@@ -913,8 +984,9 @@ void Model::set_profiling(bool on) {
   prof_rec_.clear();
 }
 
-void Model::tic() {
+void Model::tic(cudaStream_t s) {
   if (!prof_) return;
+  if (s == nullptr) s = stream_;
   if (ev_next_ + 2 > events_.size()) {
     for (int i = 0; i < 256; ++i) {
       cudaEvent_t e;
@@ -922,12 +994,13 @@ void Model::tic() {
       events_.push_back(e);
     }
   }
-  cuda_check(cudaEventRecord(events_[ev_next_], stream_), "cudaEventRecord");
+  cuda_check(cudaEventRecord(events_[ev_next_], s), "cudaEventRecord");
 }
 
-void Model::toc(int cat, double work) {
+void Model::toc(int cat, double work, cudaStream_t s) {
   if (!prof_) return;
-  cuda_check(cudaEventRecord(events_[ev_next_ + 1], stream_), "cudaEventRecord");
+  if (s == nullptr) s = stream_;
+  cuda_check(cudaEventRecord(events_[ev_next_ + 1], s), "cudaEventRecord");
   ev_next_ += 2;
   prof_rec_.emplace_back(cat, work);
 }
@@ -939,6 +1012,7 @@ void Model::read_profile(double* ms, double* work, int64_t* count) {
     count[c] = 0;
   }
   cuda_check(cudaStreamSynchronize(stream_), "sync");
+  cuda_check(cudaStreamSynchronize(comm_stream_), "sync");
   for (size_t i = 0; i < prof_rec_.size(); ++i) {
     float t = 0.f;
     cuda_check(cudaEventElapsedTime(&t, events_[2 * i], events_[2 * i + 1]), "cudaEventElapsedTime");

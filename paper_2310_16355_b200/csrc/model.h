@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <functional>
 #include <string>
 #include <unordered_map>
 #include <vector>
@@ -114,7 +115,12 @@ class Model {
   void forward_replica(std::vector<Rank*>& grp, bool need_grad);
   void backward_replica(std::vector<Rank*>& grp, bool accumulate);
   void ar_mp(std::vector<Rank*>& grp, float* Rank::*buf, int64_t n);
-  void ar_mp_ptrs(std::vector<Rank*>& grp, const std::vector<float*>& ptrs, int64_t n);
+  void ar_mp_ptrs(std::vector<Rank*>& grp, const std::vector<float*>& ptrs, int64_t n, cudaStream_t s = nullptr);
+  // Row-parallel product + all-reduce + consumer, pipelined over row chunks: the producer of
+  // chunk c+1 runs on the compute stream while chunk c is all-reduced on the comm stream.
+  using RowFn = std::function<void(Rank&, int64_t r0, int64_t rows)>;
+  void row_parallel_ar(std::vector<Rank*>& grp, float* Rank::*buf, int width, const RowFn& produce,
+                       const RowFn& consume);
   void ag_mp_slot(std::vector<Rank*>& grp, int slot, int64_t chunk);
   // in-place all-gather: chunk `mpi` of base(R) is local, the others arrive from the peers
   void ag_mp_buf(std::vector<Rank*>& grp, float* Rank::*buf, int64_t chunk);
@@ -142,11 +148,14 @@ class Model {
   std::vector<Rank> ranks_;
   std::vector<void*> allocations_;
   cudaStream_t stream_ = nullptr;
+  cudaStream_t comm_stream_ = nullptr;
+  std::vector<cudaEvent_t> ev_prod_, ev_ar_;
+  int ar_chunks_ = 1;
   int* d_flag_ = nullptr;
   int64_t launches_ = 0;
   // profiling
-  void tic();
-  void toc(int cat, double work);
+  void tic(cudaStream_t s = nullptr);
+  void toc(int cat, double work, cudaStream_t s = nullptr);
   bool prof_ = false;
   std::vector<cudaEvent_t> events_;
   size_t ev_next_ = 0;
