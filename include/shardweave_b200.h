@@ -108,6 +108,11 @@ SW_API sw_status sw_expected_state_elements(const sw_plan* plan, const char* con
                                      const int32_t* ranks, const int64_t* dims, size_t n,
                                      int mp_size, int64_t* out);
 
+/* RngStream(seed, stream_name)[.child(child_index) when >= 0].permutation(n) (rng.hpp:49-65):
+ * the Trainer's per-epoch shuffle (pipeline.hpp:383-385). */
+SW_API sw_status sw_rng_permutation(uint64_t seed, const char* stream_name, int64_t child_index,
+                                    uint64_t n, uint64_t* out);
+
 /* ============================================================================================
  * Mesh and collectives
  * ========================================================================================== */

@@ -12,6 +12,8 @@
 //   golden <spec> <f32|f64> <seed> <dp> <mp> <global_batch> <seq> <steps> <lr> <wd> <out>
 //                                                    audit-style trajectory dump (cli.cpp:179-240)
 //   bench <spec> <mp> <batch> <seq> <steps> <threads>   CPU timing of spmd_forward_backward+AdamW
+//   trainer <spec> <seed> <dp> <mp> <pdb> <accum> <epochs> <n_ex> <seq> <lr> <wd> <warmup> <dir>
+//                                                    Trainer::fit step losses / lrs / run.log
 #include <chrono>
 #include <cstdlib>
 #include <mutex>
@@ -28,6 +30,7 @@
 #include "shardweave/audit.hpp"
 #include "shardweave/model.hpp"
 #include "shardweave/model_spec.hpp"
+#include "shardweave/pipeline.hpp"
 #include "shardweave/plan.hpp"
 #include "shardweave/roles.hpp"
 #include "shardweave/spmd.hpp"
@@ -257,6 +260,64 @@ int bench(const ModelSpec& spec, int mp, std::int64_t batch, std::int64_t seq, i
   return 0;
 }
 
+// Trainer::fit (pipeline.hpp:351-454) on the transformer: examples are token windows drawn from
+// RngStream(seed, "examples") (seq+1 ids each, one stream in order); collate gives tokens /
+// targets (shifted) / weights = 1; loss_fn traces transformer_loss at the collated batch size.
+template <typename Scalar>
+int trainer_golden(const ModelSpec& spec, std::uint64_t seed, int dp, int mp, std::int64_t pdb, int accum,
+                   int epochs, int n_examples, std::int64_t seq, double lr, double wd, double warmup,
+                   const std::string& workdir) {
+  using Example = std::vector<int>;
+  DeployerConfig dc;
+  dc.n_hosts = 1;
+  dc.devices_per_host = dp * mp;
+  dc.n_model_shards = mp;
+  dc.seed = seed;
+  dc.workdir = workdir;
+  Deployer<Scalar> dep(dc);
+  RngStream ex_rng(seed, "examples");
+  std::vector<Example> examples(static_cast<std::size_t>(n_examples));
+  for (auto& e : examples) {
+    e.resize(static_cast<std::size_t>(seq + 1));
+    for (auto& t : e) t = static_cast<int>(ex_rng.next_below(static_cast<std::uint64_t>(spec.vocab_size)));
+  }
+  PipelineSpec<Scalar, Example> ps;
+  ps.collate_fn = [seq](const std::vector<Example>& batch) {
+    const auto rows = static_cast<std::int64_t>(batch.size());
+    Tensor<Scalar> tokens = Tensor<Scalar>::zeros({rows, seq});
+    Tensor<Scalar> targets = Tensor<Scalar>::zeros({rows, seq});
+    for (std::int64_t r = 0; r < rows; ++r) {
+      for (std::int64_t t = 0; t < seq; ++t) {
+        tokens[r * seq + t] = static_cast<Scalar>(batch[static_cast<std::size_t>(r)][static_cast<std::size_t>(t)]);
+        targets[r * seq + t] = static_cast<Scalar>(batch[static_cast<std::size_t>(r)][static_cast<std::size_t>(t + 1)]);
+      }
+    }
+    InputMap<Scalar> in;
+    in.emplace("tokens", std::move(tokens));
+    in.emplace("targets", std::move(targets));
+    in.emplace("weights", Tensor<Scalar>::full({rows, seq}, Scalar(1)));
+    return in;
+  };
+  ps.loss_fn = [&spec, seq](GraphBuilder<Scalar>& b, const ShapeMap& shapes) {
+    return transformer_loss(b, spec, shapes[0].second[0], seq);
+  };
+  RunConfig rc;
+  rc.n_epochs = epochs;
+  rc.per_device_batch_size = pdb;
+  rc.accumulate_grad_batches = accum;
+  rc.optimizer.lr = lr;
+  rc.optimizer.weight_decay = wd;
+  rc.warmup_rate = warmup;
+  const ParamTree<Scalar> init = init_transformer_params<Scalar>(spec, RngStream(seed, "model-init"));
+  Trainer<Scalar, Example> tr(dep, ps, rc, init, spec.overrides);
+  const TrainResult res = tr.fit(examples, {});
+  for (std::size_t i = 0; i < res.step_losses.size(); ++i) {
+    std::printf("STEP\t%zu\t%.17g\t%.17g\n", i, res.step_losses[i], res.step_lrs[i]);
+  }
+  std::printf("LOG\n%s", slurp(res.log_path).c_str());
+  return 0;
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
@@ -343,6 +404,15 @@ int main(int argc, char** argv) {
       const double lr = std::atof(argv[10]), wd = std::atof(argv[11]);
       if (dtype == "f64") return golden<double>(spec, seed, dp, mp, gb, seq, steps, lr, wd, argv[12]);
       return golden<float>(spec, seed, dp, mp, gb, seq, steps, lr, wd, argv[12]);
+    }
+    if (cmd == "trainer" && argc == 15) {
+      // trainer <spec> <seed> <dp> <mp> <per_device_batch> <accumulate> <epochs> <n_examples> <seq>
+      //         <lr> <weight_decay> <warmup_rate> <workdir>
+      const ModelSpec spec = parse_model_spec(slurp(argv[2]));
+      return trainer_golden<float>(spec, std::stoull(argv[3]), std::atoi(argv[4]), std::atoi(argv[5]),
+                                   std::atoll(argv[6]), std::atoi(argv[7]), std::atoi(argv[8]), std::atoi(argv[9]),
+                                   std::atoll(argv[10]), std::atof(argv[11]), std::atof(argv[12]),
+                                   std::atof(argv[13]), argv[14]);
     }
     if (cmd == "bench" && argc == 8) {
       const ModelSpec spec = parse_model_spec(slurp(argv[2]));

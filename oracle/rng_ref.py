@@ -68,6 +68,14 @@ class RngStream:
     def below(self, n: int, bound: int) -> np.ndarray:
         return (self.draws(n) % np.uint64(bound)).astype(np.int64)
 
+    def permutation(self, n: int) -> np.ndarray:
+        """Fisher-Yates (rng.hpp:57-65)."""
+        perm = list(range(n))
+        for i in range(n, 1, -1):
+            j = int(self.draws(1)[0] % np.uint64(i))
+            perm[i - 1], perm[j] = perm[j], perm[i - 1]
+        return np.array(perm)
+
     def child(self, index_or_name) -> "RngStream":
         seed = mix_int(self.seed ^ self.stream_id)
         if isinstance(index_or_name, str):

@@ -166,36 +166,37 @@ __global__ void ln_fwd_generic_kernel(const float* __restrict__ x, const float* 
 
 // One CTA walks rows r = blockIdx.x, +gridDim.x, ...; each thread owns fixed columns and
 // accumulates dscale / dbias partials in registers, flushed with one atomic per column.
+// Two passes per row: pass 1 reduces sum(g) and sum(g*xhat) while accumulating the parameter
+// partials; pass 2 re-reads x / dy (L1/L2 hits) to emit dx. Keeping nothing row-sized in
+// registers lets four CTAs share an SM, which is what the HBM stream needs.
 template <int THREADS, int V4>
-__global__ void __launch_bounds__(THREADS) ln_bwd_kernel(
+__global__ void __launch_bounds__(THREADS, (THREADS <= 256 ? 4 : 2)) ln_bwd_kernel(
     const float* __restrict__ x, const float* __restrict__ mean, const float* __restrict__ rstd,
     const float* __restrict__ scale, const float* __restrict__ dy, float* __restrict__ g_io,
     bf16* __restrict__ g_bf16, float* __restrict__ dscale, float* __restrict__ dbias, int64_t M,
     int d, int accumulate) {
   __shared__ float red[32];
-  float4 ds[V4], db[V4], sc[V4];
+  float4 ds[V4], db[V4];
 #pragma unroll
-  for (int j = 0; j < V4; ++j) {
-    const int c = (threadIdx.x + j * THREADS) * 4;
-    ds[j] = db[j] = make_float4(0, 0, 0, 0);
-    sc[j] = c < d ? *reinterpret_cast<const float4*>(scale + c) : make_float4(0, 0, 0, 0);
-  }
+  for (int j = 0; j < V4; ++j) ds[j] = db[j] = make_float4(0, 0, 0, 0);
   for (int64_t row = blockIdx.x; row < M; row += gridDim.x) {
     const float mu = mean[row], rs = rstd[row];
-    float4 xh[V4], gg[V4];
+    const float* xr = x + row * d;
+    const float* dr = dy + row * d;
     float s1 = 0.f, s2 = 0.f;
 #pragma unroll
     for (int j = 0; j < V4; ++j) {
       const int c = (threadIdx.x + j * THREADS) * 4;
       if (c < d) {
-        const float4 xv = *reinterpret_cast<const float4*>(x + row * d + c);
-        const float4 dv = *reinterpret_cast<const float4*>(dy + row * d + c);
-        xh[j] = make_float4((xv.x - mu) * rs, (xv.y - mu) * rs, (xv.z - mu) * rs, (xv.w - mu) * rs);
-        gg[j] = make_float4(dv.x * sc[j].x, dv.y * sc[j].y, dv.z * sc[j].z, dv.w * sc[j].w);
-        ds[j].x += dv.x * xh[j].x; ds[j].y += dv.y * xh[j].y; ds[j].z += dv.z * xh[j].z; ds[j].w += dv.w * xh[j].w;
+        const float4 xv = __ldg(reinterpret_cast<const float4*>(xr + c));
+        const float4 dv = __ldg(reinterpret_cast<const float4*>(dr + c));
+        const float4 sc = __ldg(reinterpret_cast<const float4*>(scale + c));
+        const float4 xh = make_float4((xv.x - mu) * rs, (xv.y - mu) * rs, (xv.z - mu) * rs, (xv.w - mu) * rs);
+        ds[j].x += dv.x * xh.x; ds[j].y += dv.y * xh.y; ds[j].z += dv.z * xh.z; ds[j].w += dv.w * xh.w;
         db[j].x += dv.x; db[j].y += dv.y; db[j].z += dv.z; db[j].w += dv.w;
-        s1 += gg[j].x + gg[j].y + gg[j].z + gg[j].w;
-        s2 += gg[j].x * xh[j].x + gg[j].y * xh[j].y + gg[j].z * xh[j].z + gg[j].w * xh[j].w;
+        const float gx = dv.x * sc.x, gy = dv.y * sc.y, gz = dv.z * sc.z, gw = dv.w * sc.w;
+        s1 += gx + gy + gz + gw;
+        s2 += gx * xh.x + gy * xh.y + gz * xh.z + gw * xh.w;
       }
     }
     const float gm = block_sum(s1, red) / d;
@@ -204,8 +205,14 @@ __global__ void __launch_bounds__(THREADS) ln_bwd_kernel(
     for (int j = 0; j < V4; ++j) {
       const int c = (threadIdx.x + j * THREADS) * 4;
       if (c < d) {
-        float4 dx = make_float4(rs * (gg[j].x - gm - xh[j].x * gxm), rs * (gg[j].y - gm - xh[j].y * gxm),
-                                rs * (gg[j].z - gm - xh[j].z * gxm), rs * (gg[j].w - gm - xh[j].w * gxm));
+        const float4 xv = __ldg(reinterpret_cast<const float4*>(xr + c));
+        const float4 dv = __ldg(reinterpret_cast<const float4*>(dr + c));
+        const float4 sc = __ldg(reinterpret_cast<const float4*>(scale + c));
+        float4 dx;
+        dx.x = rs * (dv.x * sc.x - gm - (xv.x - mu) * rs * gxm);
+        dx.y = rs * (dv.y * sc.y - gm - (xv.y - mu) * rs * gxm);
+        dx.z = rs * (dv.z * sc.z - gm - (xv.z - mu) * rs * gxm);
+        dx.w = rs * (dv.w * sc.w - gm - (xv.w - mu) * rs * gxm);
         float* gp = g_io + row * d + c;
         if (accumulate) {
           const float4 o = *reinterpret_cast<const float4*>(gp);
@@ -274,24 +281,59 @@ __device__ __forceinline__ float ld_as_float<float>(const float* p) { return *p;
 template <>
 __device__ __forceinline__ float ld_as_float<bf16>(const bf16* p) { return __bfloat162float(*p); }
 
-// stage 1: partial[chunk][n] = sum over 256 rows of the chunk. Threads: 64 columns x 4 rows.
+// stage 1: partial[chunk][n] = sum over the chunk's 256 rows. A CTA covers 256 columns:
+// 32 column groups of 8 (one 16-byte bf16 load / two float4 loads each) x 8 row lanes.
 template <typename T>
-__global__ void colsum_partial_kernel(const T* __restrict__ X, int64_t ld, int64_t M, int N,
-                                      float* __restrict__ partial) {
-  __shared__ float sm[4][kColChunk];
-  const int c = blockIdx.x * kColChunk + (threadIdx.x & 63);
-  const int ry = threadIdx.x >> 6;
-  const int64_t r0 = static_cast<int64_t>(blockIdx.y) * kRowChunk;
-  float s = 0.f;
-  if (c < N) {
-    const int64_t r_end = (M < r0 + kRowChunk) ? M : r0 + kRowChunk;
-    for (int64_t r = r0 + ry; r < r_end; r += 4) s += ld_as_float(X + r * ld + c);
+__device__ __forceinline__ void load8(const T* p, float (&v)[8]);
+template <>
+__device__ __forceinline__ void load8<bf16>(const bf16* p, float (&v)[8]) {
+  const uint4 u = __ldg(reinterpret_cast<const uint4*>(p));
+  const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 f = dev::unpack_bf16x2(w[i]);
+    v[2 * i] = f.x;
+    v[2 * i + 1] = f.y;
   }
-  sm[ry][threadIdx.x & 63] = s;
+}
+template <>
+__device__ __forceinline__ void load8<float>(const float* p, float (&v)[8]) {
+  const float4 a = __ldg(reinterpret_cast<const float4*>(p));
+  const float4 b = __ldg(reinterpret_cast<const float4*>(p + 4));
+  v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+  v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) colsum_partial_kernel(const T* __restrict__ X, int64_t ld, int64_t M, int N,
+                                                             float* __restrict__ partial) {
+  __shared__ float sm[8][257];
+  const int cg = threadIdx.x & 31;  // column group
+  const int rl = threadIdx.x >> 5;  // row lane
+  const int c0 = blockIdx.x * 256 + cg * 8;
+  const int64_t r0 = static_cast<int64_t>(blockIdx.y) * kRowChunk;
+  const int64_t r_end = (M < r0 + kRowChunk) ? M : r0 + kRowChunk;
+  float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  if (c0 + 8 <= N) {
+    for (int64_t r = r0 + rl; r < r_end; r += 8) {
+      float v[8];
+      load8<T>(X + r * ld + c0, v);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc[i] += v[i];
+    }
+  } else {
+    for (int64_t r = r0 + rl; r < r_end; r += 8)
+      for (int i = 0; i < 8 && c0 + i < N; ++i) acc[i] += ld_as_float(X + r * ld + c0 + i);
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) sm[rl][cg * 8 + i] = acc[i];
   __syncthreads();
-  if (ry == 0 && c < N) {
-    partial[static_cast<int64_t>(blockIdx.y) * N + c] = sm[0][threadIdx.x] + sm[1][threadIdx.x] +
-                                                        sm[2][threadIdx.x] + sm[3][threadIdx.x];
+  const int c = blockIdx.x * 256 + threadIdx.x;
+  if (c < N) {
+    float t = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) t += sm[k][threadIdx.x];
+    partial[static_cast<int64_t>(blockIdx.y) * N + c] = t;
   }
 }
 
@@ -655,7 +697,7 @@ void layernorm_fwd(const float* x, const float* scale, const float* bias, bf16* 
 void layernorm_bwd(const float* x, const float* mean, const float* rstd, const float* scale,
                    const float* dy, float* g_io, bf16* g_bf16, float* dscale, float* dbias,
                    int64_t M, int d, int accumulate, cudaStream_t s) {
-  const unsigned g = static_cast<unsigned>(M < 2 * kSMs ? M : 2 * kSMs);
+  const unsigned g = static_cast<unsigned>(M < 4 * kSMs ? M : 4 * kSMs);
   if (d % 4 == 0 && d <= 512) {
     ln_bwd_kernel<32, 4><<<g, 32, 0, s>>>(x, mean, rstd, scale, dy, g_io, g_bf16, dscale, dbias, M, d, accumulate);
   } else if (d % 4 == 0 && d <= 4096) {
@@ -671,7 +713,7 @@ void layernorm_bwd(const float* x, const float* mean, const float* rstd, const f
 void colsum_bf16(const bf16* X, int64_t ld, int64_t M, int N, int seg, float* out0, float* out1,
                  float* out2, int accumulate, float* scratch, cudaStream_t s) {
   const int chunks = static_cast<int>((M + kRowChunk - 1) / kRowChunk);
-  dim3 grid((N + kColChunk - 1) / kColChunk, chunks);
+  dim3 grid((N + 255) / 256, chunks);
   colsum_partial_kernel<bf16><<<grid, 256, 0, s>>>(X, ld, M, N, scratch);
   colsum_final_kernel<<<(N + 255) / 256, 256, 0, s>>>(scratch, chunks, N, seg > 0 ? seg : N, out0,
                                                      out1, out2, accumulate);
@@ -680,7 +722,7 @@ void colsum_bf16(const bf16* X, int64_t ld, int64_t M, int N, int seg, float* ou
 void colsum_f32(const float* X, int64_t ld, int64_t M, int N, float* out, int accumulate,
                 float* scratch, cudaStream_t s) {
   const int chunks = static_cast<int>((M + kRowChunk - 1) / kRowChunk);
-  dim3 grid((N + kColChunk - 1) / kColChunk, chunks);
+  dim3 grid((N + 255) / 256, chunks);
   colsum_partial_kernel<float><<<grid, 256, 0, s>>>(X, ld, M, N, scratch);
   colsum_final_kernel<<<(N + 255) / 256, 256, 0, s>>>(scratch, chunks, N, N, out, nullptr, nullptr,
                                                      accumulate);

@@ -269,10 +269,37 @@ def gen_numeric(tmp, tag, spec, dtype, dp, mp, gb, seq, steps, lr, wd, full):
     print(tag, os.path.getsize(path), "bytes")
 
 
+TRAINER_CASES = [
+    # name, spec, seed, dp, mp, per_device_batch, accumulate, epochs, n_examples, seq, lr, wd, warmup
+    ("trainer_mini_dp2_mp2_acc2", "mini.spec", 42, 2, 2, 2, 2, 2, 24, 16, 0.01, 0.01, 0.25),
+    ("trainer_tiny_dp1_mp2", "tiny.spec", 42, 1, 2, 2, 1, 1, 8, 128, 1e-3, 0.01, 0.1),
+]
+
+
+def gen_trainer(tmp):
+    out = {}
+    for name, spec, seed, dp, mp, pdb, acc, ep, n, seq, lr, wd, wu in TRAINER_CASES:
+        d = tempfile.mkdtemp(dir=tmp)
+        r = subprocess.run([DRIVER, "trainer", os.path.join(SPECS, spec), str(seed), str(dp), str(mp), str(pdb),
+                            str(acc), str(ep), str(n), str(seq), str(lr), str(wd), str(wu), d],
+                           capture_output=True, text=True, check=True).stdout
+        steps = [ln.split("\t") for ln in r.splitlines() if ln.startswith("STEP")]
+        log = r.split("LOG\n", 1)[1]
+        out[name] = dict(spec=spec, seed=seed, dp=dp, mp=mp, per_device_batch_size=pdb, accumulate=acc, epochs=ep,
+                         n_examples=n, seq=seq, lr=lr, weight_decay=wd, warmup_rate=wu,
+                         examples="RngStream(seed, 'examples'): n x (seq+1) next_below(vocab) in order; "
+                                  "tokens = ex[:-1], targets = ex[1:], weights = 1",
+                         losses=[float(x[2]) for x in steps], lrs=[float(x[3]) for x in steps], log=log)
+    with open(os.path.join(HERE, "trainer.json"), "w") as f:
+        json.dump(out, f, indent=1)
+    print("trainer.json:", {k: len(v["losses"]) for k, v in out.items()})
+
+
 def main():
     build()
     with tempfile.TemporaryDirectory() as tmp:
         gen_rules(tmp)
+        gen_trainer(tmp)
         gen_numeric(tmp, "mini_f64_dp1_mp2", "mini.spec", "f64", 1, 2, 2, 16, 3, 1e-2, 0.01, True)
         gen_numeric(tmp, "mini_f64_dp2_mp2", "mini.spec", "f64", 2, 2, 4, 16, 2, 1e-2, 0.01, False)
         gen_numeric(tmp, "mini_f32_dp1_mp4", "mini.spec", "f32", 1, 4, 2, 16, 2, 1e-2, 0.01, False)
