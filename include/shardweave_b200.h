@@ -240,6 +240,15 @@ SW_API sw_status sw_k_adamw(float* p, float* m, float* v, const float* g, void* 
                             float lr, float b1, float b2, float eps, float wd, float c1, float c2,
                             void* stream);
 
+/* Optimizer in the backward: the weight-gradient GEMM G[M,N] = A^T-or-A . B (same operand
+ * conventions as sw_k_gemm_bf16) whose epilogue applies the AdamW update of sw_k_adamw
+ * (train_state.hpp:214-216) to p/m/v [M, ld] in place and refreshes the bf16 shadow; G is never
+ * stored. *nonfinite_flag is OR-ed with 1 when any gradient element is non-finite. */
+SW_API sw_status sw_k_gemm_bf16_adamw(int M, int N, int K, const void* A, int64_t lda, int a_mn_major,
+                                      const void* B, int64_t ldb, int b_mn_major, float* p, float* m, float* v,
+                                      void* shadow, int64_t ld, int* nonfinite_flag, float lr, float b1, float b2,
+                                      float eps, float wd, float c1, float c2, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -101,6 +101,8 @@ def _declare(L: C.CDLL) -> None:
     L.sw_k_layernorm_bwd.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, vp, i64, C.c_int, C.c_int, vp]
     L.sw_k_xent.argtypes = [vp, i64, i64, C.c_int, vp, vp, vp, vp, C.c_int, vp]
     L.sw_k_adamw.argtypes = [vp, vp, vp, vp, vp, i64, f32, f32, f32, f32, f32, f32, f32, vp]
+    L.sw_k_gemm_bf16_adamw.argtypes = [C.c_int, C.c_int, C.c_int, vp, i64, C.c_int, vp, i64, C.c_int,
+                                       vp, vp, vp, vp, i64, vp, f32, f32, f32, f32, f32, f32, f32, vp]
     for fn in ("sw_k_attention_fwd", "sw_k_attention_bwd", "sw_k_layernorm_fwd",
-               "sw_k_layernorm_bwd", "sw_k_xent", "sw_k_adamw"):
+               "sw_k_layernorm_bwd", "sw_k_xent", "sw_k_adamw", "sw_k_gemm_bf16_adamw"):
         getattr(L, fn).restype = C.c_int

@@ -54,6 +54,40 @@ sw_status sw_k_gemm_bf16(int M, int N, int K, const void* A, int64_t lda, int a_
   });
 }
 
+sw_status sw_k_gemm_bf16_adamw(int M, int N, int K, const void* A, int64_t lda, int a_mn_major, const void* B,
+                               int64_t ldb, int b_mn_major, float* p, float* m, float* v, void* shadow, int64_t ld,
+                               int* nonfinite_flag, float lr, float b1, float b2, float eps, float wd, float c1,
+                               float c2, void* stream) {
+  return sw::guarded([&] {
+    if (N % 4 != 0 || ld % 4 != 0) sw::fail(SW_ERR_SHAPE, "sw_k_gemm_bf16_adamw: N and ld must be multiples of 4");
+    sw::GemmParams g;
+    g.M = M;
+    g.N = N;
+    g.K = K;
+    g.A = A;
+    g.lda = lda;
+    g.a_mn_major = a_mn_major;
+    g.B = B;
+    g.ldb = ldb;
+    g.b_mn_major = b_mn_major;
+    g.epi = sw::Epi::kAdamW;
+    g.ldc = ld;
+    g.adam_p = p;
+    g.adam_m = m;
+    g.adam_v = v;
+    g.adam_w = shadow;
+    g.adam_flag = nonfinite_flag;
+    g.adam_lr = lr;
+    g.adam_b1 = b1;
+    g.adam_b2 = b2;
+    g.adam_eps = eps;
+    g.adam_wd = wd;
+    g.adam_c1 = c1;
+    g.adam_c2 = c2;
+    sw::cuda_check(sw::gemm_bf16(g, static_cast<cudaStream_t>(stream)), "gemm_bf16_adamw launch");
+  });
+}
+
 sw_status sw_k_attention_fwd(const void* qkv, void* o, float* lse, int B, int T, int Hl, int hd,
                              void* stream) {
   return sw::guarded([&] {

@@ -162,12 +162,7 @@ sw_status sw_model_train_step(sw_model* model, const sw_adamw_cfg* cfg) {
   return sw::guarded([&] {
     require(model, "model");
     require(cfg, "cfg");
-    sw::Model& m = *model->model;
-    m.forward_backward(false);
-    const int64_t n = m.launches();
-    m.dp_sync();
-    m.adamw(cfg->lr, cfg->beta1, cfg->beta2, cfg->eps, cfg->weight_decay, true);
-    (void)n;
+    model->model->train_step(cfg->lr, cfg->beta1, cfg->beta2, cfg->eps, cfg->weight_decay);
   });
 }
 

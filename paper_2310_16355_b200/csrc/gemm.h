@@ -22,6 +22,9 @@ enum class Epi : int {
   kBiasGelu = 2,    // C(bf16) = acc + bias (pre-activation), C2(bf16) = gelu(acc + bias)
   kResidF32 = 3,    // C(f32)  = aux(f32) + acc + bias     (residual stream update; C may alias aux)
   kGeluBwd = 4,     // C(bf16) = acc * gelu'(aux(bf16))    (fc2 dgrad fused with GeLU backward)
+  kAdamW = 5,       // wgrad with the optimizer in the epilogue: acc is the fp32 gradient of the
+                    // [M, N] weight at adam_* (row pitch ldc); AdamW updates p/m/v in place and
+                    // refreshes the bf16 shadow; non-finite gradients set *adam_flag
 };
 
 struct GemmParams {
@@ -46,6 +49,13 @@ struct GemmParams {
   int64_t ld_aux = 0;
   float alpha = 1.0f;
   int accumulate = 0;
+  // kAdamW (train_state.hpp:211-216, Scalar = float)
+  float* adam_p = nullptr;
+  float* adam_m = nullptr;
+  float* adam_v = nullptr;
+  void* adam_w = nullptr;
+  int* adam_flag = nullptr;
+  float adam_lr = 0.f, adam_b1 = 0.f, adam_b2 = 0.f, adam_eps = 0.f, adam_wd = 0.f, adam_c1 = 1.f, adam_c2 = 1.f;
   int num_sms = 0;  // 0 = all
 };
 

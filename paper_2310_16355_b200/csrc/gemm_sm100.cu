@@ -31,7 +31,8 @@ constexpr int STAGE_BYTES = A_STAGE + B_STAGE;
 constexpr int TMEM_COLS = 512;
 constexpr int NUM_THREADS = 256;
 constexpr int GROUP_M = 8;
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
+constexpr int EPI_STAGE_BYTES = 4 * 32 * 32 * 4;  // per-warp 32x32 fp32 transpose buffers (kAdamW)
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256 + EPI_STAGE_BYTES;
 
 // SW_GEMM_1SM=1 selects the single-CTA kernel (debug / comparison).
 bool use_pairs() {
@@ -50,6 +51,79 @@ __device__ __forceinline__ void tile_coords(int t, int num_m, int num_n, int& mb
   const int r = t - g * per_group;
   mb = first_m + r % gsz;
   nb = r / gsz;
+}
+
+// Optimizer-in-backward epilogue (Epi::kAdamW) for one warp's 32x32 accumulator chunk: the
+// gradient rows (one per lane after tcgen05.ld) are transposed through a 4 KiB per-warp shared
+// buffer so every global access of p/m/v/w covers 4 rows x 128 B (fully used lines), then the
+// AdamW update of train_state.hpp:214-216 is applied in place. The gradient never reaches HBM.
+__device__ __forceinline__ void adamw_chunk(const GemmParams& p, float4* stage, int row0, int col0, int ncols,
+                                            const uint32_t (&r)[32], uint32_t lane) {
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    stage[lane * 8 + (c ^ (lane & 7))] =
+        make_float4(__uint_as_float(r[4 * c]) * p.alpha, __uint_as_float(r[4 * c + 1]) * p.alpha,
+                    __uint_as_float(r[4 * c + 2]) * p.alpha, __uint_as_float(r[4 * c + 3]) * p.alpha);
+  }
+  __syncwarp();
+  const int sub = static_cast<int>(lane >> 3), c4 = static_cast<int>(lane & 7);
+  float4 g[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int rr = 4 * i + sub;
+    g[i] = stage[rr * 8 + (c4 ^ (rr & 7))];
+  }
+  __syncwarp();
+  const bool col_ok = 4 * c4 < ncols;
+  float4 pp[8], mm[8], vv[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int row = row0 + 4 * i + sub;
+    if (col_ok && row < p.M) {
+      const int64_t off = static_cast<int64_t>(row) * p.ldc + col0 + 4 * c4;
+      pp[i] = __ldcs(reinterpret_cast<const float4*>(p.adam_p + off));
+      mm[i] = __ldcs(reinterpret_cast<const float4*>(p.adam_m + off));
+      vv[i] = __ldcs(reinterpret_cast<const float4*>(p.adam_v + off));
+    }
+  }
+  const float y1 = dev::rcp_refined(p.adam_c1), y2 = dev::rcp_refined(p.adam_c2);
+  bool bad = false;
+  uint32_t slow = 0;  // elements whose intermediates left the branch-free fast-path range
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int row = row0 + 4 * i + sub;
+    if (col_ok && row < p.M) {
+      bad |= !(isfinite(g[i].x) & isfinite(g[i].y) & isfinite(g[i].z) & isfinite(g[i].w));
+      slow |= dev::adamw_update_fast(pp[i].x, mm[i].x, vv[i].x, g[i].x, p.adam_lr, p.adam_b1, p.adam_b2, p.adam_eps, p.adam_wd, p.adam_c1, p.adam_c2, y1, y2) ? 0u : 1u << (4 * i);
+      slow |= dev::adamw_update_fast(pp[i].y, mm[i].y, vv[i].y, g[i].y, p.adam_lr, p.adam_b1, p.adam_b2, p.adam_eps, p.adam_wd, p.adam_c1, p.adam_c2, y1, y2) ? 0u : 1u << (4 * i + 1);
+      slow |= dev::adamw_update_fast(pp[i].z, mm[i].z, vv[i].z, g[i].z, p.adam_lr, p.adam_b1, p.adam_b2, p.adam_eps, p.adam_wd, p.adam_c1, p.adam_c2, y1, y2) ? 0u : 1u << (4 * i + 2);
+      slow |= dev::adamw_update_fast(pp[i].w, mm[i].w, vv[i].w, g[i].w, p.adam_lr, p.adam_b1, p.adam_b2, p.adam_eps, p.adam_wd, p.adam_c1, p.adam_c2, y1, y2) ? 0u : 1u << (4 * i + 3);
+    }
+  }
+  if (__any_sync(0xffffffffu, slow != 0)) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      if (slow & (1u << (4 * i))) dev::adamw_update(pp[i].x, mm[i].x, vv[i].x, g[i].x, p.adam_lr, p.adam_b1, p.adam_b2, p.adam_eps, p.adam_wd, p.adam_c1, p.adam_c2);
+      if (slow & (1u << (4 * i + 1))) dev::adamw_update(pp[i].y, mm[i].y, vv[i].y, g[i].y, p.adam_lr, p.adam_b1, p.adam_b2, p.adam_eps, p.adam_wd, p.adam_c1, p.adam_c2);
+      if (slow & (1u << (4 * i + 2))) dev::adamw_update(pp[i].z, mm[i].z, vv[i].z, g[i].z, p.adam_lr, p.adam_b1, p.adam_b2, p.adam_eps, p.adam_wd, p.adam_c1, p.adam_c2);
+      if (slow & (1u << (4 * i + 3))) dev::adamw_update(pp[i].w, mm[i].w, vv[i].w, g[i].w, p.adam_lr, p.adam_b1, p.adam_b2, p.adam_eps, p.adam_wd, p.adam_c1, p.adam_c2);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int row = row0 + 4 * i + sub;
+    if (col_ok && row < p.M) {
+      const int64_t off = static_cast<int64_t>(row) * p.ldc + col0 + 4 * c4;
+      __stcs(reinterpret_cast<float4*>(p.adam_p + off), pp[i]);
+      __stcs(reinterpret_cast<float4*>(p.adam_m + off), mm[i]);
+      __stcs(reinterpret_cast<float4*>(p.adam_v + off), vv[i]);
+      uint2 w;
+      w.x = dev::pack_bf16x2(pp[i].x, pp[i].y);
+      w.y = dev::pack_bf16x2(pp[i].z, pp[i].w);
+      *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(p.adam_w) + off) = w;
+    }
+  }
+  if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(p.adam_flag, 1);
 }
 
 template <Epi EPI>
@@ -159,6 +233,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  float4* epi_stage = reinterpret_cast<float4*>(reinterpret_cast<uint8_t*>(full) + 256);
 
   const uint32_t warp = dev::warp_idx_sync();
   const uint32_t lane = threadIdx.x & 31;
@@ -282,7 +357,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         uint32_t r[32];
         dev::tmem_ld_32x32b_x32(tmem_base + ((q * 32) << 16) + acc * BN + j * 32, r);
         dev::tmem_ld_wait();
-        if (row < p.M) epilogue_chunk<EPI>(p, row, nb * BN + j * 32, ncols, r);
+        if constexpr (EPI == Epi::kAdamW) {
+          adamw_chunk(p, epi_stage + q * 256, row - static_cast<int>(lane), nb * BN + j * 32, ncols, r, lane);
+        } else if (row < p.M) {
+          epilogue_chunk<EPI>(p, row, nb * BN + j * 32, ncols, r);
+        }
       }
       dev::tc_fence_before();
       if (lane == 0) dev::mbar_arrive(&tempty[acc]);
@@ -311,7 +390,7 @@ constexpr int P_STAGES = 6;
 constexpr int P_A_STAGE = 128 * BK * 2;  // 16 KiB
 constexpr int P_B_STAGE = 128 * BK * 2;  // 16 KiB (half of the N=256 tile)
 constexpr int P_STAGE_BYTES = P_A_STAGE + P_B_STAGE;
-constexpr int P_SMEM_BYTES = P_STAGES * P_STAGE_BYTES + 1024 + 256;
+constexpr int P_SMEM_BYTES = P_STAGES * P_STAGE_BYTES + 1024 + 256 + EPI_STAGE_BYTES;
 
 template <Epi EPI>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
@@ -327,6 +406,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
   uint64_t* tfull = empty + P_STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  float4* epi_stage = reinterpret_cast<float4*>(reinterpret_cast<uint8_t*>(full) + 256);
 
   const uint32_t warp = dev::warp_idx_sync();
   const uint32_t lane = threadIdx.x & 31;
@@ -450,7 +530,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         uint32_t r[32];
         dev::tmem_ld_32x32b_x32(tmem_base + ((q * 32) << 16) + acc * BN + j * 32, r);
         dev::tmem_ld_wait();
-        if (row < p.M) epilogue_chunk<EPI>(p, row, nb * BN + j * 32, ncols, r);
+        if constexpr (EPI == Epi::kAdamW) {
+          adamw_chunk(p, epi_stage + q * 256, row - static_cast<int>(lane), nb * BN + j * 32, ncols, r, lane);
+        } else if (row < p.M) {
+          epilogue_chunk<EPI>(p, row, nb * BN + j * 32, ncols, r);
+        }
       }
       dev::tc_fence_before();
       if (lane == 0) dev::mbar_arrive_cluster(tempty_leader + acc * 8);
@@ -525,6 +609,7 @@ cudaError_t gemm_bf16(const GemmParams& p, cudaStream_t stream) {
     case Epi::kBiasGelu: return launch<Epi::kBiasGelu>(p, stream);
     case Epi::kResidF32: return launch<Epi::kResidF32>(p, stream);
     case Epi::kGeluBwd: return launch<Epi::kGeluBwd>(p, stream);
+    case Epi::kAdamW: return launch<Epi::kAdamW>(p, stream);
   }
   return cudaErrorInvalidValue;
 }

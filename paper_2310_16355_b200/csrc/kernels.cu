@@ -559,10 +559,7 @@ __global__ void add_residual_bias_kernel(const float* __restrict__ a, const floa
 // ------------------------------------------------------------------------------------------
 __device__ __forceinline__ void adamw_one(float& p, float& m, float& v, float g, float lr, float b1,
                                           float b2, float eps, float wd, float c1, float c2) {
-  // train_state.hpp:214-216, evaluated in Scalar=float with the same operation order.
-  m = b1 * m + (1.0f - b1) * g;
-  v = b2 * v + (1.0f - b2) * (g * g);
-  p = p - lr * (__fdiv_rn(__fdiv_rn(m, c1), __fsqrt_rn(__fdiv_rn(v, c2)) + eps) + wd * p);
+  dev::adamw_update(p, m, v, g, lr, b1, b2, eps, wd, c1, c2);
 }
 
 __global__ void adamw_kernel(float* __restrict__ p, float* __restrict__ m, float* __restrict__ v,

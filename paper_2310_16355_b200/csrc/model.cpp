@@ -166,32 +166,39 @@ void Model::build_layout() {
     slot_of_[name] = static_cast<int>(slots_.size()) - 1;
     return static_cast<int>(slots_.size()) - 1;
   };
+  // Region 1: the GEMM weight matrices (their wgrad epilogue can apply AdamW in place, see
+  // train_step); region 2: embeddings, biases and LayerNorm parameters.
+  layers_.resize(L_);
+  for (int l = 0; l < L_; ++l) {
+    const std::string b = "block_" + std::to_string(l) + "/";
+    LayerSlots& ls = layers_[l];
+    ls.q_k = place(b + "attn/q/kernel", true);  // q|k|v kernels contiguous: fused [3*d/t, d]
+    ls.k_k = place(b + "attn/k/kernel", false);
+    ls.v_k = place(b + "attn/v/kernel", false);
+    ls.o_k = place(b + "attn/o/kernel", true);
+    ls.fc1_k = place(b + "mlp/fc1/kernel", true);
+    ls.fc2_k = place(b + "mlp/fc2/kernel", true);
+  }
+  if (!spec_.tie_embeddings) head_ = place("lm_head/kernel", true);
+  weights_end_ = (off + kAlign - 1) / kAlign * kAlign;
   tok_ = place("embed/tok/kernel", true);
   pos_ = place("embed/pos/kernel", true);
   for (int l = 0; l < L_; ++l) {
     const std::string b = "block_" + std::to_string(l) + "/";
-    LayerSlots ls{};
-    ls.q_k = place(b + "attn/q/kernel", true);  // q|k|v kernels contiguous: fused [3*d/t, d]
-    ls.k_k = place(b + "attn/k/kernel", false);
-    ls.v_k = place(b + "attn/v/kernel", false);
+    LayerSlots& ls = layers_[l];
     ls.q_b = place(b + "attn/q/bias", true);    // q|k|v biases contiguous: [3*d]
     ls.k_b = place(b + "attn/k/bias", false);
     ls.v_b = place(b + "attn/v/bias", false);
-    ls.o_k = place(b + "attn/o/kernel", true);
     ls.o_b = place(b + "attn/o/bias", true);
     ls.ln1_s = place(b + "ln1/scale", true);
     ls.ln1_b = place(b + "ln1/bias", true);
     ls.ln2_s = place(b + "ln2/scale", true);
     ls.ln2_b = place(b + "ln2/bias", true);
-    ls.fc1_k = place(b + "mlp/fc1/kernel", true);
     ls.fc1_b = place(b + "mlp/fc1/bias", true);
-    ls.fc2_k = place(b + "mlp/fc2/kernel", true);
     ls.fc2_b = place(b + "mlp/fc2/bias", true);
-    layers_.push_back(ls);
   }
   lnf_s_ = place("final_ln/scale", true);
   lnf_b_ = place("final_ln/bias", true);
-  if (!spec_.tie_embeddings) head_ = place("lm_head/kernel", true);
   flat_n_ = (off + kAlign - 1) / kAlign * kAlign;
 
   // Which blocks run tensor-parallel: the two sharding rules give column-split QKV / fc1 and
@@ -696,6 +703,44 @@ void Model::forward_replica(std::vector<Rank*>& grp, bool need_grad) {
 // ---------------------------------------------------------------------------------------------
 // backward (the VJPs of autodiff.hpp, executed with the partition rules of spmd.hpp:342-387)
 // ---------------------------------------------------------------------------------------------
+void Model::wgrad(Rank& R, int slot, int M, int N, int K, const void* A, int64_t lda, const void* B, int64_t ldb,
+                  int accumulate) {
+  if (fused_ == nullptr || slots_[slot].offset >= weights_end_) {
+    gemm(R, M, N, K, A, lda, 1, B, ldb, 1, static_cast<int>(Epi::kStoreF32), G(R, slot), N, nullptr, 0, nullptr,
+         nullptr, 0, accumulate);
+    return;
+  }
+  // optimizer in the epilogue: the gradient never leaves the accumulator
+  GemmParams p;
+  p.M = M;
+  p.N = N;
+  p.K = K;
+  p.A = A;
+  p.lda = lda;
+  p.a_mn_major = 1;
+  p.B = B;
+  p.ldb = ldb;
+  p.b_mn_major = 1;
+  p.epi = Epi::kAdamW;
+  p.ldc = N;
+  p.adam_p = P(R, slot);
+  p.adam_m = R.m + slots_[slot].offset;
+  p.adam_v = R.v + slots_[slot].offset;
+  p.adam_w = W(R, slot);
+  p.adam_flag = d_flag_;
+  p.adam_lr = fused_->lr;
+  p.adam_b1 = fused_->b1;
+  p.adam_b2 = fused_->b2;
+  p.adam_eps = fused_->eps;
+  p.adam_wd = fused_->wd;
+  p.adam_c1 = fused_->c1;
+  p.adam_c2 = fused_->c2;
+  tic();
+  cuda_check(gemm_bf16(p, stream_), "gemm launch");
+  toc(kProfGemm, 2.0 * M * N * static_cast<double>(K));
+  ++launches_;
+}
+
 void Model::backward_replica(std::vector<Rank*>& grp, bool accumulate) {
   const int64_t M = M_;
   const int d = d_, dl = dl_, fl = fl_;
@@ -724,11 +769,8 @@ void Model::backward_replica(std::vector<Rank*>& grp, bool accumulate) {
       }
     }
   }
-  for (Rank* R : grp) {
-    // dW_head (+)= dlogits^T . final_h
-    gemm(*R, vl_, d, static_cast<int>(M), R->logits, ldv_, 1, R->f, d, 1, static_cast<int>(Epi::kStoreF32),
-         G(*R, head), d, nullptr, 0, nullptr, nullptr, 0, acc);
-  }
+  // Every weight's dgrad (which reads the bf16 shadow) is issued before its wgrad, so a wgrad
+  // that applies AdamW in its epilogue never races a reader of the old weights.
   {
     // d(final_h) = dlogits . W_head (partial over the vocab shards when the head is split)
     auto prod = [&](Rank& R, int64_t r0, int64_t rows) {
@@ -749,21 +791,22 @@ void Model::backward_replica(std::vector<Rank*>& grp, bool accumulate) {
       for (Rank* R : grp) cons(*R, 0, M);
     }
   }
+  for (Rank* R : grp) {
+    // dW_head (+)= dlogits^T . final_h
+    wgrad(*R, head, vl_, d, static_cast<int>(M), R->logits, ldv_, R->f, d, acc);
+  }
   for (int l = L_ - 1; l >= 0; --l) {
     const LayerSlots& ls = layers_[l];
     // ---- MLP ----
     for (Rank* R : grp) {
       k::colsum_f32(R->gres, d, M, d, G(*R, ls.fc2_b), acc, R->col_scratch, stream_);
       launches_ += 2;
-      gemm(*R, d, fl, static_cast<int>(M), R->gb, d, 1, R->act[l], fl, 1, static_cast<int>(Epi::kStoreF32),
-           G(*R, ls.fc2_k), fl, nullptr, 0, nullptr, nullptr, 0, acc);
       gemm(*R, static_cast<int>(M), fl, d, R->gb, d, 0, W(*R, ls.fc2_k), fl, 1,
            static_cast<int>(Epi::kGeluBwd), R->dpre, fl, nullptr, 0, nullptr, R->pre[l], fl);
+      wgrad(*R, ls.fc2_k, d, fl, static_cast<int>(M), R->gb, d, R->act[l], fl, acc);
       k::colsum_bf16(R->dpre, fl, M, fl, 0, G(*R, ls.fc1_b) + R->mpi * fl, nullptr, nullptr, acc,
                      R->col_scratch, stream_);
       launches_ += 2;
-      gemm(*R, fl, d, static_cast<int>(M), R->dpre, fl, 1, R->a2[l], d, 1, static_cast<int>(Epi::kStoreF32),
-           G(*R, ls.fc1_k), d, nullptr, 0, nullptr, nullptr, 0, acc);
     }
     {
       auto prod = [&](Rank& R, int64_t r0, int64_t rows) {
@@ -784,14 +827,14 @@ void Model::backward_replica(std::vector<Rank*>& grp, bool accumulate) {
         for (Rank* R : grp) cons(*R, 0, M);
       }
     }
+    for (Rank* R : grp) wgrad(*R, ls.fc1_k, fl, d, static_cast<int>(M), R->dpre, fl, R->a2[l], d, acc);
     // ---- attention ----
     for (Rank* R : grp) {
       k::colsum_f32(R->gres, d, M, d, G(*R, ls.o_b), acc, R->col_scratch, stream_);
       launches_ += 2;
-      gemm(*R, d, dl, static_cast<int>(M), R->gb, d, 1, R->o[l], dl, 1, static_cast<int>(Epi::kStoreF32),
-           G(*R, ls.o_k), dl, nullptr, 0, nullptr, nullptr, 0, acc);
       gemm(*R, static_cast<int>(M), dl, d, R->gb, d, 0, W(*R, ls.o_k), dl, 1,
            static_cast<int>(Epi::kStoreBf16), R->dout, dl);
+      wgrad(*R, ls.o_k, d, dl, static_cast<int>(M), R->gb, d, R->o[l], dl, acc);
       tic();
       k::attention_bwd(R->qkv[l], R->o[l], R->lse[l], R->dout, R->dqkv, R->attn_scratch, B_, T_, hl_, hd_,
                        stream_);
@@ -800,8 +843,6 @@ void Model::backward_replica(std::vector<Rank*>& grp, bool accumulate) {
       k::colsum_bf16(R->dqkv, 3 * dl, M, 3 * dl, dl, G(*R, ls.q_b) + R->mpi * dl, G(*R, ls.k_b) + R->mpi * dl,
                      G(*R, ls.v_b) + R->mpi * dl, acc, R->col_scratch, stream_);
       launches_ += 2;
-      gemm(*R, 3 * dl, d, static_cast<int>(M), R->dqkv, 3 * dl, 1, R->a1[l], d, 1,
-           static_cast<int>(Epi::kStoreF32), G(*R, ls.q_k), d, nullptr, 0, nullptr, nullptr, 0, acc);
     }
     {
       auto prod = [&](Rank& R, int64_t r0, int64_t rows) {
@@ -822,6 +863,7 @@ void Model::backward_replica(std::vector<Rank*>& grp, bool accumulate) {
         for (Rank* R : grp) cons(*R, 0, M);
       }
     }
+    for (Rank* R : grp) wgrad(*R, ls.q_k, 3 * dl, d, static_cast<int>(M), R->dqkv, 3 * dl, R->a1[l], d, acc);
   }
   for (Rank* R : grp) {
     k::embed_bwd_pos(R->gres, G(*R, pos_), B_, T_, d, acc, stream_);
@@ -929,6 +971,61 @@ void Model::adamw(double lr, double b1, double b2, double eps, double wd, bool c
   }
   ++step_;
   cuda_check(cudaGetLastError(), "adamw");
+}
+
+bool Model::train_step(double lr, double b1, double b2, double eps, double wd) {
+  static const bool disabled = [] {
+    const char* e = std::getenv("SW_FUSED_ADAMW");
+    return e != nullptr && e[0] == '0';
+  }();
+  if (disabled || mesh_->dp != 1) {
+    forward_backward(false);
+    dp_sync();
+    adamw(lr, b1, b2, eps, wd, true);
+    return false;
+  }
+  // Optimizer in the backward (dp == 1, no accumulation): every GEMM weight is updated by its
+  // wgrad epilogue; the small parameters (embeddings, biases, LayerNorm) by one flat AdamW.
+  const double t = static_cast<double>(step_ + 1);
+  FusedAdam fa;
+  fa.lr = static_cast<float>(lr);
+  fa.b1 = static_cast<float>(b1);
+  fa.b2 = static_cast<float>(b2);
+  fa.eps = static_cast<float>(eps);
+  fa.wd = static_cast<float>(wd);
+  fa.c1 = static_cast<float>(1.0 - std::pow(b1, t));
+  fa.c2 = static_cast<float>(1.0 - std::pow(b2, t));
+  cuda_check(cudaMemsetAsync(d_flag_, 0, sizeof(int), stream_), "memset");
+  fused_ = &fa;
+  try {
+    forward_backward(false);
+  } catch (...) {
+    fused_ = nullptr;
+    throw;
+  }
+  fused_ = nullptr;
+  const int64_t n_small = flat_n_ - weights_end_;
+  for (Rank& R : ranks_) {
+    k::nonfinite_check(R.g + weights_end_, n_small, d_flag_, stream_);
+    ++launches_;
+  }
+  int flag = 0;
+  cuda_check(cudaMemcpyAsync(&flag, d_flag_, sizeof(int), cudaMemcpyDeviceToHost, stream_), "D2H");
+  cuda_check(cudaStreamSynchronize(stream_), "sync");
+  if (flag) {
+    fail(SW_ERR_NONFINITE, "adamw_step: non-finite gradient (optimizer fused into the backward: this "
+                           "step's GEMM weights were already updated)");
+  }
+  for (Rank& R : ranks_) {
+    tic();
+    k::adamw(R.p + weights_end_, R.m + weights_end_, R.v + weights_end_, R.g + weights_end_, R.w + weights_end_,
+             n_small, fa.lr, fa.b1, fa.b2, fa.eps, fa.wd, fa.c1, fa.c2, stream_);
+    toc(kProfAdamw, 30.0 * n_small);
+    ++launches_;
+  }
+  ++step_;
+  cuda_check(cudaGetLastError(), "train_step");
+  return true;
 }
 
 double Model::last_loss() {

@@ -95,6 +95,9 @@ class Model {
   void scale_grads(double factor);
   void dp_sync();
   void adamw(double lr, double b1, double b2, double eps, double wd, bool check_finite);
+  // forward_backward + dp_sync + adamw; with dp == 1 the optimizer runs inside the backward
+  // (wgrad epilogues). Returns true when the fused path ran.
+  bool train_step(double lr, double b1, double b2, double eps, double wd);
   double last_loss();
   void logits_to_host(float* out);
 
@@ -128,6 +131,12 @@ class Model {
             int64_t ldb, int b_mn, int epi, void* C, int64_t ldc, void* C2 = nullptr,
             int64_t ldc2 = 0, const float* bias = nullptr, const void* aux = nullptr,
             int64_t ld_aux = 0, int accumulate = 0, int bias_seg = 0, int64_t bias_seg_stride = 0);
+  void wgrad(Rank& R, int slot, int M, int N, int K, const void* A, int64_t lda, const void* B, int64_t ldb,
+             int accumulate);
+  struct FusedAdam {
+    float lr, b1, b2, eps, wd, c1, c2;
+  };
+  const FusedAdam* fused_ = nullptr;
   float* P(Rank& R, int slot) { return R.p + slots_[slot].offset; }
   float* G(Rank& R, int slot) { return R.g + slots_[slot].offset; }
   bf16* W(Rank& R, int slot) { return R.w + slots_[slot].offset; }
@@ -145,6 +154,7 @@ class Model {
   std::vector<LayerSlots> layers_;
   int tok_ = -1, pos_ = -1, lnf_s_ = -1, lnf_b_ = -1, head_ = -1;
   int64_t flat_n_ = 0;
+  int64_t weights_end_ = 0;  // [0, weights_end_): GEMM weight matrices; the rest: small params
   std::vector<Rank> ranks_;
   std::vector<void*> allocations_;
   cudaStream_t stream_ = nullptr;

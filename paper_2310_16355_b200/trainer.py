@@ -112,27 +112,31 @@ class Trainer:
         for epoch in range(first_epoch, cfg.n_epochs):
             perm = permutation(self.seed, "data-shuffle", epoch, len(train_examples))
             for s in range(steps_per_epoch):
-                loss_sum = 0.0
-                for micro in range(cfg.accumulate_grad_batches):
-                    off = s * rows_per_step + micro * global_rows
-                    batch = [train_examples[int(perm[off + i])] for i in range(global_rows)]
-                    rows = self._stage(self.collate_fn(batch))
-                    if rows != global_rows:
-                        raise _lib.ShapeError(1, f"Trainer: collate_fn returned {rows} rows for a batch of "
-                                                 f"{global_rows} examples")
-                    self.model.forward_backward(accumulate=micro > 0)
-                    loss_sum += self.model.loss() * dp  # loss() is the mean over replicas
-                loss = loss_sum / (dp * cfg.accumulate_grad_batches)
-                if cfg.accumulate_grad_batches > 1:
-                    self.model.scale_grads(1.0 / cfg.accumulate_grad_batches)
-                self.model.dp_sync()
                 lr = scheduled_lr(self.step, total_steps, warmup_steps, cfg.optimizer.lr)
                 step_cfg = engine.AdamWConfig(lr, cfg.optimizer.beta1, cfg.optimizer.beta2, cfg.optimizer.eps,
                                               cfg.optimizer.weight_decay)
+                loss_sum = 0.0
                 try:
-                    self.model.adamw_step(step_cfg)
+                    for micro in range(cfg.accumulate_grad_batches):
+                        off = s * rows_per_step + micro * global_rows
+                        batch = [train_examples[int(perm[off + i])] for i in range(global_rows)]
+                        rows = self._stage(self.collate_fn(batch))
+                        if rows != global_rows:
+                            raise _lib.ShapeError(1, f"Trainer: collate_fn returned {rows} rows for a batch of "
+                                                     f"{global_rows} examples")
+                        if cfg.accumulate_grad_batches == 1:
+                            # one micro-batch: the fused step (optimizer inside the backward when dp == 1)
+                            self.model.train_step(step_cfg)
+                        else:
+                            self.model.forward_backward(accumulate=micro > 0)
+                        loss_sum += self.model.loss() * dp  # loss() is the mean over replicas
+                    if cfg.accumulate_grad_batches > 1:
+                        self.model.scale_grads(1.0 / cfg.accumulate_grad_batches)
+                        self.model.dp_sync()
+                        self.model.adamw_step(step_cfg)
                 except _lib.NonFiniteError as e:
                     raise _lib.NonFiniteError(4, f"Trainer: aborting at step {self.step + 1}: {e.message}") from None
+                loss = loss_sum / (dp * cfg.accumulate_grad_batches)
                 self._log.write(f"step={self.step} loss={_fmt(loss)} lr={_fmt(lr)}\n")
                 self._log.flush()
                 losses.append(loss)

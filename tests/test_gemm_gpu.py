@@ -112,3 +112,54 @@ def test_gemm_wgrad_accumulate():
     want = dW + dy.float().t() @ x.float()
     _gemm(dy, 1, x, 1, Nout, Kin, T, 1, dW, acc=1)
     assert _rel(dW, want) < 1e-5
+
+
+@pytest.mark.parametrize("M,N,K", [(384, 320, 512), (200, 136, 72), (1024, 4096, 2048)])
+def test_gemm_adamw_epilogue_matches_store_then_adamw(M, N, K):
+    """Epi::kAdamW (optimizer in the backward): the wgrad GEMM with AdamW applied in its
+    epilogue equals storing the fp32 gradient and running sw_k_adamw on it (same gradient bits,
+    same update code), including ragged tiles; the shadow is the bf16 of the new parameter."""
+    L = _lib.lib()
+    gen = torch.Generator(device=DEV).manual_seed(M + N + K)
+    A, B, ref = _ref_operands(M, N, K, 1, 1, gen)
+    # gradients and moments spread over ~40 decades so both the branch-free fast path and the
+    # IEEE fallback of the epilogue run
+    scale = torch.pow(10.0, torch.empty(M, device=DEV).uniform_(-14, 1, generator=gen))
+    A.mul_(scale.bfloat16()[None, :])
+    ref = A.float().t() @ B.float()
+    p = torch.randn(M, N, generator=gen, device=DEV) * 0.05
+    m = torch.randn(M, N, generator=gen, device=DEV) * torch.pow(10.0, torch.empty(M, N, device=DEV).uniform_(-30, -1, generator=gen))
+    v = torch.rand(M, N, generator=gen, device=DEV) * torch.pow(10.0, torch.empty(M, N, device=DEV).uniform_(-38, -2, generator=gen))
+    m[::7] = 0.0
+    v[::7] = 0.0
+    sh = torch.empty(M, N, device=DEV, dtype=torch.bfloat16)
+    p2, m2, v2, sh2 = p.clone(), m.clone(), v.clone(), sh.clone()
+    flag = torch.zeros(1, device=DEV, dtype=torch.int32)
+    hp = dict(lr=1e-3, b1=0.9, b2=0.999, eps=1e-8, wd=0.01, c1=1 - 0.9 ** 3, c2=1 - 0.999 ** 3)
+    _lib.check(L.sw_k_gemm_bf16_adamw(M, N, K, A.data_ptr(), A.stride(0), 1, B.data_ptr(), B.stride(0), 1,
+                                      p.data_ptr(), m.data_ptr(), v.data_ptr(), sh.data_ptr(), N, flag.data_ptr(),
+                                      *hp.values(), None))
+    G = torch.empty(M, N, device=DEV)
+    _gemm(A, 1, B, 1, M, N, K, 1, G)
+    assert _rel(G, ref) < 1e-5
+    _lib.check(L.sw_k_adamw(p2.data_ptr(), m2.data_ptr(), v2.data_ptr(), G.data_ptr(), sh2.data_ptr(), M * N,
+                            *hp.values(), None))
+    torch.cuda.synchronize()
+    assert int(flag.item()) == 0
+    assert torch.equal(p, p2) and torch.equal(m, m2) and torch.equal(v, v2) and torch.equal(sh, sh2)
+
+
+def test_gemm_adamw_epilogue_flags_nonfinite():
+    L = _lib.lib()
+    M, N, K = 256, 256, 128
+    gen = torch.Generator(device=DEV).manual_seed(5)
+    A, B, _ = _ref_operands(M, N, K, 1, 1, gen)
+    A[7, 9] = float("inf")
+    p, m, v = (torch.zeros(M, N, device=DEV) for _ in range(3))
+    sh = torch.empty(M, N, device=DEV, dtype=torch.bfloat16)
+    flag = torch.zeros(1, device=DEV, dtype=torch.int32)
+    _lib.check(L.sw_k_gemm_bf16_adamw(M, N, K, A.data_ptr(), A.stride(0), 1, B.data_ptr(), B.stride(0), 1,
+                                      p.data_ptr(), m.data_ptr(), v.data_ptr(), sh.data_ptr(), N, flag.data_ptr(),
+                                      1e-3, 0.9, 0.999, 1e-8, 0.0, 0.1, 0.001, None))
+    torch.cuda.synchronize()
+    assert int(flag.item()) == 1

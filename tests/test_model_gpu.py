@@ -254,3 +254,50 @@ def test_vocab_parallel_head_plan_and_comm():
     chunks = 4  # row-parallel all-reduces are pipelined over 4 row chunks at M = 512
     assert int(ar[1]) == (4 * L + 1) * chunks + 1  # + d(final_h) (chunked) + target-logit AR
     assert int(ag[1]) == 4 * L + 1  # + the CE stats all-gather
+
+
+@pytest.mark.parametrize("spec_name,mp", [("mini.spec", 1), ("mini.spec", 2), ("tiny_vocab_parallel.spec", 2)])
+def test_fused_optimizer_matches_unfused(spec_name, mp):
+    """train_step with dp == 1 applies AdamW inside the wgrad GEMM epilogues (the gradient of a
+    weight matrix never reaches HBM). After one step the parameters must equal
+    forward_backward + dp_sync + adamw_step (train_state.hpp:170-226 on the stored gradient).
+
+    Both arms carry atomics-order noise (embedding scatter, dQ reduce-add); Adam's first step is
+    ~lr*sign(g), so an element whose true gradient is ~0 may flip: at most 1e-3 of the elements
+    may differ, and by no more than 2*lr. Three more steps must then track in loss (1e-4)."""
+    spec = spec_of(spec_name)
+    seq = 16 if spec_name == "mini.spec" else 128
+    fused, _, _ = make(spec, 1, mp, 2, seq)
+    plain, _, _ = make(spec, 1, mp, 2, seq)
+    for m in (fused, plain):
+        m.init_params(42, "model-init")
+    cfg = engine.AdamWConfig(lr=1e-2, weight_decay=0.01)
+    for step in range(4):
+        tokens, targets, weights = rng_ref.audit_batch(42, step, 2, seq, spec.vocab_size)
+        fused.stage_batch(tokens, targets, weights)
+        fused.train_step(cfg)
+        plain.stage_batch(tokens, targets, weights)
+        plain.forward_backward()
+        plain.dp_sync()
+        plain.adamw_step(cfg)
+        assert abs(fused.loss() - plain.loss()) <= 1e-4 * abs(plain.loss()), step
+        if step == 0:
+            for n in plain.shapes:
+                a, b = fused.get_param(n), plain.get_param(n)
+                d = np.abs(a - b)
+                off = d > 1e-6 + 1e-5 * np.abs(b)
+                assert off.mean() <= 1e-3 or n.endswith("attn/k/bias"), (n, int(off.sum()))
+                assert d.max() <= 2 * cfg.lr * (1 + 1e-3) + 1e-6, (n, float(d.max()))
+
+
+def test_fused_optimizer_nonfinite_raises():
+    spec = spec_of("mini.spec")
+    model, mesh, _ = make(spec, 1, 1, 2, 16)
+    model.init_params(42, "model-init")
+    bad = model.get_param("block_0/ln1/scale")
+    bad[3] = np.nan
+    model.set_param("block_0/ln1/scale", bad)
+    tokens, targets, weights = rng_ref.audit_batch(42, 0, 2, 16, spec.vocab_size)
+    model.stage_batch(tokens, targets, weights)
+    with pytest.raises(engine._lib.NonFiniteError, match="non-finite gradient"):
+        model.train_step(engine.AdamWConfig())
