@@ -56,6 +56,7 @@ struct GemmParams {
   void* adam_w = nullptr;
   int* adam_flag = nullptr;
   float adam_lr = 0.f, adam_b1 = 0.f, adam_b2 = 0.f, adam_eps = 0.f, adam_wd = 0.f, adam_c1 = 1.f, adam_c2 = 1.f;
+  int adam_fast = 0;  // set by gemm_bf16: bias corrections in [2^-14, 1] admit the branch-free path
   int num_sms = 0;  // 0 = all
 };
 

@@ -86,7 +86,15 @@ __device__ __forceinline__ void adamw_chunk(const GemmParams& p, float4* stage, 
       vv[i] = __ldcs(reinterpret_cast<const float4*>(p.adam_v + off));
     }
   }
+  // pull the next chunk's optimizer state toward L2 while this one is updated (lane = row)
+  if (ncols == 32 && col0 + 32 < p.N && row0 + static_cast<int>(lane) < p.M) {
+    const int64_t nxt = static_cast<int64_t>(row0 + static_cast<int>(lane)) * p.ldc + col0 + 32;
+    dev::prefetch_l2(p.adam_p + nxt);
+    dev::prefetch_l2(p.adam_m + nxt);
+    dev::prefetch_l2(p.adam_v + nxt);
+  }
   const float y1 = dev::rcp_refined(p.adam_c1), y2 = dev::rcp_refined(p.adam_c2);
+  const bool fast = p.adam_fast != 0;
   bool bad = false;
   uint32_t slow = 0;  // elements whose intermediates left the branch-free fast-path range
 #pragma unroll
@@ -94,10 +102,10 @@ __device__ __forceinline__ void adamw_chunk(const GemmParams& p, float4* stage, 
     const int row = row0 + 4 * i + sub;
     if (col_ok && row < p.M) {
       bad |= !(isfinite(g[i].x) & isfinite(g[i].y) & isfinite(g[i].z) & isfinite(g[i].w));
-      slow |= dev::adamw_update_fast(pp[i].x, mm[i].x, vv[i].x, g[i].x, p.adam_lr, p.adam_b1, p.adam_b2, p.adam_eps, p.adam_wd, p.adam_c1, p.adam_c2, y1, y2) ? 0u : 1u << (4 * i);
-      slow |= dev::adamw_update_fast(pp[i].y, mm[i].y, vv[i].y, g[i].y, p.adam_lr, p.adam_b1, p.adam_b2, p.adam_eps, p.adam_wd, p.adam_c1, p.adam_c2, y1, y2) ? 0u : 1u << (4 * i + 1);
-      slow |= dev::adamw_update_fast(pp[i].z, mm[i].z, vv[i].z, g[i].z, p.adam_lr, p.adam_b1, p.adam_b2, p.adam_eps, p.adam_wd, p.adam_c1, p.adam_c2, y1, y2) ? 0u : 1u << (4 * i + 2);
-      slow |= dev::adamw_update_fast(pp[i].w, mm[i].w, vv[i].w, g[i].w, p.adam_lr, p.adam_b1, p.adam_b2, p.adam_eps, p.adam_wd, p.adam_c1, p.adam_c2, y1, y2) ? 0u : 1u << (4 * i + 3);
+      slow |= fast && dev::adamw_update_fast(pp[i].x, mm[i].x, vv[i].x, g[i].x, p.adam_lr, p.adam_b1, p.adam_b2, p.adam_eps, p.adam_wd, p.adam_c1, p.adam_c2, y1, y2) ? 0u : 1u << (4 * i);
+      slow |= fast && dev::adamw_update_fast(pp[i].y, mm[i].y, vv[i].y, g[i].y, p.adam_lr, p.adam_b1, p.adam_b2, p.adam_eps, p.adam_wd, p.adam_c1, p.adam_c2, y1, y2) ? 0u : 1u << (4 * i + 1);
+      slow |= fast && dev::adamw_update_fast(pp[i].z, mm[i].z, vv[i].z, g[i].z, p.adam_lr, p.adam_b1, p.adam_b2, p.adam_eps, p.adam_wd, p.adam_c1, p.adam_c2, y1, y2) ? 0u : 1u << (4 * i + 2);
+      slow |= fast && dev::adamw_update_fast(pp[i].w, mm[i].w, vv[i].w, g[i].w, p.adam_lr, p.adam_b1, p.adam_b2, p.adam_eps, p.adam_wd, p.adam_c1, p.adam_c2, y1, y2) ? 0u : 1u << (4 * i + 3);
     }
   }
   if (__any_sync(0xffffffffu, slow != 0)) {
@@ -386,27 +394,131 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 // of B, so per-SM operand traffic is 32 KB per 64-deep k-block instead of 48 KB (the
 // single-CTA kernel is TMA-ingress bound at ~83% tensor-pipe activity).
 // ---------------------------------------------------------------------------------------------
-constexpr int P_STAGES = 6;
 constexpr int P_A_STAGE = 128 * BK * 2;  // 16 KiB
 constexpr int P_B_STAGE = 128 * BK * 2;  // 16 KiB (half of the N=256 tile)
 constexpr int P_STAGE_BYTES = P_A_STAGE + P_B_STAGE;
-constexpr int P_SMEM_BYTES = P_STAGES * P_STAGE_BYTES + 1024 + 256 + EPI_STAGE_BYTES;
+// Optimizer-in-backward (Epi::kAdamW): p/m/v of the CTA's 128 rows x 32 columns are staged
+// by TMA one chunk ahead of the epilogue (double-buffered), updated in shared memory and written
+// back by TMA stores; the operand ring shrinks to 4 stages to make room.
+#ifndef SW_OPT_COLS
+#define SW_OPT_COLS 16
+#endif
+#ifndef SW_OPT_NBUF
+#define SW_OPT_NBUF 2
+#endif
+constexpr int OC = SW_OPT_COLS;           // columns per optimizer-state chunk (16 or 32)
+constexpr int OPT_NBUF = SW_OPT_NBUF;     // chunk buffers in flight
+constexpr int OPT_ARR = 128 * OC * 4;     // one array (p, m or v) of one chunk, 128 rows
+constexpr int OPT_BUF = 3 * OPT_ARR;      // p | m | v
+constexpr int OPT_WBOX = 32 * OC * 4;     // one warp's 32-row box of one array
+template <Epi EPI>
+constexpr int p_stages() {
+  return EPI == Epi::kAdamW ? (227 * 1024 - 1024 - 256 - OPT_NBUF * OPT_BUF) / P_STAGE_BYTES < 6
+                                  ? (227 * 1024 - 1024 - 256 - OPT_NBUF * OPT_BUF) / P_STAGE_BYTES
+                                  : 6
+                            : 6;
+}
+template <Epi EPI>
+constexpr int p_smem_bytes() {
+  return p_stages<EPI>() * P_STAGE_BYTES + (EPI == Epi::kAdamW ? OPT_NBUF * OPT_BUF : 0) + 1024 + 256;
+}
+
+// fp32 tensor maps over p, m, v ([M, ldc], box OC columns x 32 rows, swizzle span = one row).
+struct OptMaps {
+  CUtensorMap p, m, v;
+};
+
+// AdamW on one warp's 32 rows x OC columns with p/m/v resident in shared memory (TMA swizzled
+// rows: 16-byte chunk c of row r sits at chunk c ^ (r & 7) for 128-byte rows, c ^ ((r >> 1) & 3)
+// for 64-byte rows). Lane = row, so the gradient row comes straight from the tcgen05.ld
+// registers; rows/columns outside the matrix were zero-filled by TMA and are clipped by the TMA
+// store, so only the bf16 shadow store is masked.
+__device__ __forceinline__ int opt_pos(int r, int c) {
+  return OC == 32 ? (r * 8 + (c ^ (r & 7))) : (r * 4 + (c ^ ((r >> 1) & 3)));
+}
+
+__device__ __forceinline__ void adamw_chunk_smem(const GemmParams& p, float* sbox, int row, int col0, int ncols,
+                                                 const uint32_t* r, uint32_t lane) {
+  float4* sp = reinterpret_cast<float4*>(sbox);
+  float4* sm = reinterpret_cast<float4*>(sbox + OPT_ARR / 4);
+  float4* sv = reinterpret_cast<float4*>(sbox + OPT_ARR / 2);
+  const float y1 = dev::rcp_refined(p.adam_c1), y2 = dev::rcp_refined(p.adam_c2);
+  const bool fast = p.adam_fast != 0;
+  const int L = static_cast<int>(lane);
+  bool bad = false;
+  uint32_t slow = 0;
+  float4 pv[OC / 4];
+#pragma unroll
+  for (int c = 0; c < OC / 4; ++c) {
+    const int at = opt_pos(L, c);
+    float4 P = sp[at], M = sm[at], V = sv[at];
+    const float g0 = __uint_as_float(r[4 * c]) * p.alpha, g1 = __uint_as_float(r[4 * c + 1]) * p.alpha;
+    const float g2 = __uint_as_float(r[4 * c + 2]) * p.alpha, g3 = __uint_as_float(r[4 * c + 3]) * p.alpha;
+    bad |= !(isfinite(g0) & isfinite(g1) & isfinite(g2) & isfinite(g3));
+    slow |= fast && dev::adamw_update_fast(P.x, M.x, V.x, g0, p.adam_lr, p.adam_b1, p.adam_b2, p.adam_eps, p.adam_wd, p.adam_c1, p.adam_c2, y1, y2) ? 0u : 1u << (4 * c);
+    slow |= fast && dev::adamw_update_fast(P.y, M.y, V.y, g1, p.adam_lr, p.adam_b1, p.adam_b2, p.adam_eps, p.adam_wd, p.adam_c1, p.adam_c2, y1, y2) ? 0u : 1u << (4 * c + 1);
+    slow |= fast && dev::adamw_update_fast(P.z, M.z, V.z, g2, p.adam_lr, p.adam_b1, p.adam_b2, p.adam_eps, p.adam_wd, p.adam_c1, p.adam_c2, y1, y2) ? 0u : 1u << (4 * c + 2);
+    slow |= fast && dev::adamw_update_fast(P.w, M.w, V.w, g3, p.adam_lr, p.adam_b1, p.adam_b2, p.adam_eps, p.adam_wd, p.adam_c1, p.adam_c2, y1, y2) ? 0u : 1u << (4 * c + 3);
+    sp[at] = P;
+    sm[at] = M;
+    sv[at] = V;
+    pv[c] = P;
+  }
+  if (__any_sync(0xffffffffu, slow != 0)) {
+    // IEEE fallback for the elements whose intermediates left the fast-path range (their p/m/v
+    // in shared memory are still the old values)
+#pragma unroll
+    for (int c = 0; c < OC / 4; ++c) {
+      if ((slow >> (4 * c)) & 0xfu) {
+        const int at = opt_pos(L, c);
+        float4 P = sp[at], M = sm[at], V = sv[at];
+        if (slow & (1u << (4 * c))) dev::adamw_update(P.x, M.x, V.x, __uint_as_float(r[4 * c]) * p.alpha, p.adam_lr, p.adam_b1, p.adam_b2, p.adam_eps, p.adam_wd, p.adam_c1, p.adam_c2);
+        if (slow & (1u << (4 * c + 1))) dev::adamw_update(P.y, M.y, V.y, __uint_as_float(r[4 * c + 1]) * p.alpha, p.adam_lr, p.adam_b1, p.adam_b2, p.adam_eps, p.adam_wd, p.adam_c1, p.adam_c2);
+        if (slow & (1u << (4 * c + 2))) dev::adamw_update(P.z, M.z, V.z, __uint_as_float(r[4 * c + 2]) * p.alpha, p.adam_lr, p.adam_b1, p.adam_b2, p.adam_eps, p.adam_wd, p.adam_c1, p.adam_c2);
+        if (slow & (1u << (4 * c + 3))) dev::adamw_update(P.w, M.w, V.w, __uint_as_float(r[4 * c + 3]) * p.alpha, p.adam_lr, p.adam_b1, p.adam_b2, p.adam_eps, p.adam_wd, p.adam_c1, p.adam_c2);
+        sp[at] = P;
+        sm[at] = M;
+        sv[at] = V;
+        pv[c] = P;
+      }
+    }
+  }
+  if (row < p.M) {
+    __nv_bfloat16* w = reinterpret_cast<__nv_bfloat16*>(p.adam_w) + static_cast<int64_t>(row) * p.ldc + col0;
+#pragma unroll
+    for (int c = 0; c < OC / 4; c += 2) {
+      if (4 * c < ncols) {
+        uint4 o;
+        o.x = dev::pack_bf16x2(pv[c].x, pv[c].y);
+        o.y = dev::pack_bf16x2(pv[c].z, pv[c].w);
+        o.z = dev::pack_bf16x2(pv[c + 1].x, pv[c + 1].y);
+        o.w = dev::pack_bf16x2(pv[c + 1].z, pv[c + 1].w);
+        *reinterpret_cast<uint4*>(w + 4 * c) = o;
+      }
+    }
+  }
+  if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(p.adam_flag, 1);
+}
 
 template <Epi EPI>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     gemm_bf16_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                         const GemmParams p) {
+                         const __grid_constant__ OptMaps om, const GemmParams p) {
+  constexpr int P_STAGES = p_stages<EPI>();
+  constexpr bool kOpt = EPI == Epi::kAdamW;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + P_STAGES * P_A_STAGE;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + P_STAGES * P_B_STAGE);
+  uint8_t* sOpt = sB + P_STAGES * P_B_STAGE;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sOpt + (kOpt ? 2 * OPT_BUF : 0));
   uint64_t* empty = full + P_STAGES;
   uint64_t* tfull = empty + P_STAGES;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  float4* epi_stage = reinterpret_cast<float4*>(reinterpret_cast<uint8_t*>(full) + 256);
+  uint64_t* ofull = tempty + 2;
+  uint64_t* oempty = ofull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(oempty + 2);
 
   const uint32_t warp = dev::warp_idx_sync();
   const uint32_t lane = threadIdx.x & 31;
@@ -429,6 +541,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     for (int a = 0; a < 2; ++a) {
       dev::mbar_init(&tfull[a], 1);
       dev::mbar_init(&tempty[a], 8);
+      if (a < OPT_NBUF) {
+        dev::mbar_init(&ofull[a], 1);
+        dev::mbar_init(&oempty[a], 4);
+      }
     }
     dev::fence_barrier_init();
   }
@@ -511,11 +627,46 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         }
       }
     }
+  } else if (warp == 3) {
+    if constexpr (kOpt) {
+      if (lane == 0) {
+        // ---------------- optimizer-state producer (TMA, one chunk ahead) ----------------
+        dev::tma_prefetch_desc(&om.p);
+        dev::tma_prefetch_desc(&om.m);
+        dev::tma_prefetch_desc(&om.v);
+        int buf = 0;
+        uint32_t ph = 0;
+        for (int t = pair; t < num_tiles; t += npairs) {
+          int mb, nb;
+          tile_coords(t, num_m, num_n, mb, nb);
+          const int r0 = mb * 2 * BM + static_cast<int>(rank) * BM;
+          const int n_left = p.N - nb * BN;
+          for (int j = 0; j < BN / OC && j * OC < n_left; ++j) {
+            dev::mbar_wait(&oempty[buf], ph ^ 1);
+            dev::mbar_arrive_expect_tx(&ofull[buf], OPT_BUF);
+            uint8_t* dst = sOpt + buf * OPT_BUF;
+            const int c0 = nb * BN + j * OC;
+#pragma unroll
+            for (int w = 0; w < 4; ++w) {
+              dev::tma_load_2d(dst + w * OPT_WBOX, &om.p, &ofull[buf], c0, r0 + 32 * w);
+              dev::tma_load_2d(dst + OPT_ARR + w * OPT_WBOX, &om.m, &ofull[buf], c0, r0 + 32 * w);
+              dev::tma_load_2d(dst + 2 * OPT_ARR + w * OPT_WBOX, &om.v, &ofull[buf], c0, r0 + 32 * w);
+            }
+            if (++buf == OPT_NBUF) {
+              buf = 0;
+              ph ^= 1;
+            }
+          }
+        }
+      }
+    }
   } else if (warp >= 4) {
     const uint32_t q = warp & 3;
     const uint32_t tempty_leader = dev::mapa_shared(dev::smem_u32(&tempty[0]), 0);
     int acc = 0;
     uint32_t acc_phase = 0;
+    int obuf = 0;
+    uint32_t oph = 0;
     for (int t = pair; t < num_tiles; t += npairs) {
       int mb, nb;
       tile_coords(t, num_m, num_n, mb, nb);
@@ -530,8 +681,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         uint32_t r[32];
         dev::tmem_ld_32x32b_x32(tmem_base + ((q * 32) << 16) + acc * BN + j * 32, r);
         dev::tmem_ld_wait();
-        if constexpr (EPI == Epi::kAdamW) {
-          adamw_chunk(p, epi_stage + q * 256, row - static_cast<int>(lane), nb * BN + j * 32, ncols, r, lane);
+        if constexpr (kOpt) {
+#pragma unroll
+          for (int h = 0; h < 32 / OC; ++h) {
+            const int col0 = nb * BN + j * 32 + h * OC;
+            if (col0 >= p.N) break;
+            dev::mbar_wait(&ofull[obuf], oph);
+            float* sbox = reinterpret_cast<float*>(sOpt + obuf * OPT_BUF) + q * (OPT_WBOX / 4);
+            adamw_chunk_smem(p, sbox, row, col0, min(OC, p.N - col0), r + h * OC, lane);
+            dev::fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              const int rw = row - static_cast<int>(lane);
+              dev::tma_store_2d(&om.p, sbox, col0, rw);
+              dev::tma_store_2d(&om.m, sbox + OPT_ARR / 4, col0, rw);
+              dev::tma_store_2d(&om.v, sbox + OPT_ARR / 2, col0, rw);
+              dev::bulk_commit();
+              dev::bulk_wait_read();  // the stores have left shared memory: hand the buffer back
+              dev::mbar_arrive(&oempty[obuf]);
+            }
+            if (++obuf == OPT_NBUF) {
+              obuf = 0;
+              oph ^= 1;
+            }
+          }
         } else if (row < p.M) {
           epilogue_chunk<EPI>(p, row, nb * BN + j * 32, ncols, r);
         }
@@ -545,6 +718,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     }
   }
 
+  if constexpr (kOpt) {
+    if (warp >= 4 && lane == 0) dev::bulk_wait_all();
+  }
   dev::tc_fence_before();
   dev::cluster_sync();
   if (warp == 2) {
@@ -558,7 +734,7 @@ cudaError_t launch_2sm(const GemmParams& p, cudaStream_t stream) {
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(gemm_bf16_2sm_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         P_SMEM_BYTES);
+                                         p_smem_bytes<EPI>());
     if (e != cudaSuccess) return e;
     configured = true;
   }
@@ -569,7 +745,13 @@ cudaError_t launch_2sm(const GemmParams& p, cudaStream_t stream) {
   const int num_tiles = ((p.M + 2 * BM - 1) / (2 * BM)) * ((p.N + BN - 1) / BN);
   const int sms = (p.num_sms > 0 ? p.num_sms : device_sm_count()) & ~1;
   const int grid = 2 * num_tiles < sms ? 2 * num_tiles : sms;
-  gemm_bf16_2sm_kernel<EPI><<<grid, NUM_THREADS, P_SMEM_BYTES, stream>>>(ta, tb, p);
+  OptMaps om{};
+  if constexpr (EPI == Epi::kAdamW) {
+    om.p = make_tmap_f32_2d(p.adam_p, p.N, p.M, p.ldc, OC, 32);
+    om.m = make_tmap_f32_2d(p.adam_m, p.N, p.M, p.ldc, OC, 32);
+    om.v = make_tmap_f32_2d(p.adam_v, p.N, p.M, p.ldc, OC, 32);
+  }
+  gemm_bf16_2sm_kernel<EPI><<<grid, NUM_THREADS, p_smem_bytes<EPI>(), stream>>>(ta, tb, om, p);
   return cudaGetLastError();
 }
 
@@ -609,7 +791,12 @@ cudaError_t gemm_bf16(const GemmParams& p, cudaStream_t stream) {
     case Epi::kBiasGelu: return launch<Epi::kBiasGelu>(p, stream);
     case Epi::kResidF32: return launch<Epi::kResidF32>(p, stream);
     case Epi::kGeluBwd: return launch<Epi::kGeluBwd>(p, stream);
-    case Epi::kAdamW: return launch<Epi::kAdamW>(p, stream);
+    case Epi::kAdamW: {
+      GemmParams q = p;
+      const float lo = 1.0f / 16384.0f;
+      q.adam_fast = (p.adam_c1 >= lo && p.adam_c1 <= 1.0f && p.adam_c2 >= lo && p.adam_c2 <= 1.0f) ? 1 : 0;
+      return launch<Epi::kAdamW>(q, stream);
+    }
   }
   return cudaErrorInvalidValue;
 }

@@ -17,8 +17,8 @@ CUtensorMap make_tmap_bf16_3d(const void* ptr, uint64_t inner, uint64_t mid, uin
                               uint64_t ld_mid, uint64_t ld_outer, uint32_t box_inner,
                               uint32_t box_mid, uint32_t box_outer, bool swizzle128);
 
-// 2-D fp32 tensor map (row pitch `ld` elements), SWIZZLE_128B, box {box_inner, box_outer}
-// (box_inner * 4 <= 128 bytes).
+// 2-D fp32 tensor map (row pitch `ld` elements), box {box_inner, box_outer}; the swizzle span
+// equals the box row (box_inner * 4 = 128, 64 or 32 bytes -> SWIZZLE_128B / 64B / 32B).
 CUtensorMap make_tmap_f32_2d(const void* ptr, uint64_t inner, uint64_t outer, uint64_t ld, uint32_t box_inner,
                              uint32_t box_outer);
 

@@ -37,12 +37,18 @@ __global__ void div_random(uint64_t base, int mode) {
   if (mode == 1) ub = (ub & 0x807fffffu) | ((96u + (ub >> 24) % 64u) << 23);        // b near 1 (like c1, c2)
   if (mode == 2) ua = (ua & 0x807fffffu) | ((20u + (ua >> 24) % 140u) << 23);       // small a (m, v)
   if (mode == 3) ub = (ub & 0x807fffffu) | ((90u + (ub >> 24) % 50u) << 23);        // b ~ sqrt(v)+eps
-  if (mode == 4) {                                                                   // a/c, c in (0.001, 1]
-    ub = 0x3f800000u - (ub % 0x05000000u);
+  if (mode == 4) {                                                                   // a/c, c in (2^-14, 1]
+    ub = 0x3f800000u - (ub % 0x07000000u);
   }
   const float a = __uint_as_float(ua), b = __uint_as_float(ub);
   bool ok = true;
-  const float f = sw::dev::div_rn_fast(a, b, ok);
+  float f;
+  if (mode == 4) {
+    ok = b >= 1.0f / 16384.0f;
+    f = sw::dev::div_rn_fast_c(a, b, sw::dev::rcp_refined(b), ok);
+  } else {
+    f = sw::dev::div_rn_fast(a, b, ok);
+  }
   const float e = __fdiv_rn(a, b);
   if (ok) {
     atomicAdd(&g_ok_div, 1ull);
