@@ -30,7 +30,10 @@ constexpr int B_STAGE = BN * BK * 2;  // 32 KiB
 constexpr int STAGE_BYTES = A_STAGE + B_STAGE;
 constexpr int TMEM_COLS = 512;
 constexpr int NUM_THREADS = 256;
-constexpr int GROUP_M = 8;
+#ifndef SW_GROUP_M
+#define SW_GROUP_M 8
+#endif
+constexpr int GROUP_M = SW_GROUP_M;  // tile rows per raster group (operand reuse in L2)
 constexpr int EPI_STAGE_BYTES = 4 * 32 * 32 * 4;  // per-warp 32x32 fp32 transpose buffers (kAdamW)
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256 + EPI_STAGE_BYTES;
 
