@@ -20,6 +20,7 @@
 // Every smem tile is a [rows x 64-column] SWIZZLE_128B chunk array, usable both as a K-major
 // and as an MN-major UMMA operand, so no tile is ever transposed.
 #include <cmath>
+#include <cstdlib>
 
 #include "kernels.h"
 #include "sm100.cuh"
@@ -562,6 +563,307 @@ __global__ void __launch_bounds__(384, 1)
   }
 }
 
+// ---------------------------------------------------------------------------------------------
+// backward, pipelined (head_dim 128): one CTA per (128-key block, batch*head) iterating over
+// 64-query blocks. Query-block n+1's S^T / dP^T MMAs run on the tensor core while the softmax
+// warpgroups turn block n's S^T / dP^T into P^T / dS^T, and block n's dQ leaves TMEM through a
+// separate warpgroup, so the per-block chain no longer serialises the tensor pipe.
+//   warp 0      TMA: K, V once; Q_n / dO_n into a 3-deep ring (64-row boxes)
+//   warp 1      MMA: S^T_n = K Q_n^T, dP^T_n = V dO_n^T (TMEM, double-buffered, lane = key);
+//               then dV += P^T dO_n, dK += dS^T Q_n (TMEM accumulators) and
+//               dQ^T_n = K^T dS^T_n (into S^T_n's TMEM columns, lane = head dim)
+//   warp 2      TMEM allocator (512 columns: S^T x2 | dP^T x2 | dV | dK)
+//   warps 4-11  two softmax warpgroups, 32 query columns each (lane = key row)
+//   warps 12-15 dQ warpgroup: dQ^T_n (lane = head dim) -> SW128 fp32 staging -> TMA reduce-add
+//               into the fp32 dQ accumulator
+// ---------------------------------------------------------------------------------------------
+constexpr int BQ2 = 64;
+constexpr int CHUNK64 = 64 * 128;  // bytes of one [64 rows x 64 bf16] SW128 chunk
+
+__device__ __forceinline__ uint64_t kdesc64(uint32_t base, int kk) {
+  return dev::make_sdesc_sw128(base + (kk >> 2) * CHUNK64 + (kk & 3) * 32, 16, 1024);
+}
+
+__device__ __forceinline__ uint64_t mndesc64(uint32_t base, int kk) {
+  return dev::make_sdesc_sw128(base + kk * 2048, CHUNK64, 1024);
+}
+
+constexpr int QST = 3;  // Q / dO ring depth
+
+struct Bwd2Layout {
+  static constexpr int HD = 128;
+  static constexpr int KV = 128 * HD * 2;     // 32 KiB
+  static constexpr int QT = BQ2 * HD * 2;     // 16 KiB
+  static constexpr int PT = 128 * BQ2 * 2;    // 16 KiB: [128 keys x 64 queries] bf16
+  static constexpr int OFF_K = 0;
+  static constexpr int OFF_V = OFF_K + KV;
+  static constexpr int OFF_Q = OFF_V + KV;         // [QST]
+  static constexpr int OFF_DO = OFF_Q + QST * QT;  // [QST]
+  static constexpr int OFF_PT = OFF_DO + QST * QT;
+  static constexpr int DQS = BQ2 * HD * 4;    // 32 KiB: dQ staging, 4 boxes of [64 rows x 32 fp32]
+  static constexpr int OFF_DST = OFF_PT + PT;
+  static constexpr int OFF_DQS = OFF_DST + PT;
+  static constexpr int OFF_STAT = OFF_DQS + DQS;  // [2][2][64] floats: lse, delta
+  static constexpr int OFF_BAR = OFF_STAT + 2 * 2 * BQ2 * 4;
+  static constexpr int BYTES = OFF_BAR + 256;  // dynamic smem base declared 1024-aligned
+};
+
+__global__ void __launch_bounds__(512, 1)
+    attn_bwd_tc2(const __grid_constant__ CUtensorMap tm_qkv64, const __grid_constant__ CUtensorMap tm_qkv128,
+                 const __grid_constant__ CUtensorMap tm_do64, const __grid_constant__ CUtensorMap tm_dq,
+                 const float* __restrict__ lse, const float* __restrict__ delta, bf16* __restrict__ dqkv, int T,
+                 int Hl, float scale_log2, float scale) {
+  using Lay = Bwd2Layout;
+  constexpr int HD = Lay::HD;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t* sK = smem + Lay::OFF_K;
+  uint8_t* sV = smem + Lay::OFF_V;
+  uint8_t* sQ = smem + Lay::OFF_Q;
+  uint8_t* sDO = smem + Lay::OFF_DO;
+  uint8_t* sPt = smem + Lay::OFF_PT;
+  uint8_t* sDSt = smem + Lay::OFF_DST;
+  uint8_t* sDQ = smem + Lay::OFF_DQS;
+  float* sStat = reinterpret_cast<float*>(smem + Lay::OFF_STAT);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Lay::OFF_BAR);
+  uint64_t* kv_full = bars + 0;
+  uint64_t* qdo_full = bars + 1;   // [QST]
+  uint64_t* qdo_empty = bars + 4;  // [QST]
+  uint64_t* s_full = bars + 7;     // [2]
+  uint64_t* s_free = bars + 9;     // [2]  dQ^T of the block two back has left TMEM
+  uint64_t* p_full = bars + 11;
+  uint64_t* mma_done = bars + 12;
+  uint64_t* dq_full = bars + 13;   // [2]  dQ^T_n is in S^T buffer n & 1
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
+
+  const int nb = (T + 127) / 128;
+  const int kb = static_cast<int>(blockIdx.x) % nb;
+  const int bh = static_cast<int>(blockIdx.x) / nb;
+  const int b = bh / Hl, h = bh % Hl;
+  const int Dl = Hl * HD;
+  const int key0 = kb * 128;
+  const int row0 = b * T;
+  const int nq = (T - key0 + BQ2 - 1) / BQ2;  // 64-query blocks starting at the diagonal
+
+  const uint32_t warp = dev::warp_idx_sync();
+  const uint32_t lane = threadIdx.x & 31;
+  if (warp == 0 && lane == 0) {
+    dev::tma_prefetch_desc(&tm_qkv64);
+    dev::tma_prefetch_desc(&tm_qkv128);
+    dev::tma_prefetch_desc(&tm_do64);
+    dev::tma_prefetch_desc(&tm_dq);
+    dev::mbar_init(kv_full, 1);
+    for (int i = 0; i < QST; ++i) {
+      dev::mbar_init(&qdo_full[i], 1);
+      dev::mbar_init(&qdo_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      dev::mbar_init(&s_full[i], 1);
+      dev::mbar_init(&s_free[i], 128);
+      dev::mbar_init(&dq_full[i], 1);
+    }
+    dev::mbar_init(p_full, 256);
+    dev::mbar_init(mma_done, 1);
+    dev::fence_barrier_init();
+  }
+  if (warp == 2) dev::tmem_alloc<512>(tmem_slot);
+  dev::tc_fence_before();
+  __syncthreads();
+  dev::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t t_s = tmem, t_dp = tmem + 128, t_dv = tmem + 256, t_dk = tmem + 384;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      dev::mbar_arrive_expect_tx(kv_full, 2 * Lay::KV);
+#pragma unroll
+      for (int c = 0; c < HD / 64; ++c) {
+        dev::tma_load_2d(sK + c * CHUNK, &tm_qkv128, kv_full, Dl + h * HD + c * 64, row0 + key0);
+        dev::tma_load_2d(sV + c * CHUNK, &tm_qkv128, kv_full, 2 * Dl + h * HD + c * 64, row0 + key0);
+      }
+      for (int n = 0; n < nq; ++n) {
+        const int st = n % QST;
+        const int qs = key0 + n * BQ2;
+        dev::mbar_wait(&qdo_empty[st], ((n / QST) & 1) ^ 1);
+        dev::mbar_arrive_expect_tx(&qdo_full[st], 2 * Lay::QT);
+#pragma unroll
+        for (int c = 0; c < HD / 64; ++c) {
+          dev::tma_load_2d(sQ + st * Lay::QT + c * CHUNK64, &tm_qkv64, &qdo_full[st], h * HD + c * 64, row0 + qs);
+          dev::tma_load_2d(sDO + st * Lay::QT + c * CHUNK64, &tm_do64, &qdo_full[st], h * HD + c * 64, row0 + qs);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t id_s = dev::make_idesc_bf16(128, BQ2, 0, 0);
+      const uint32_t id_kv = dev::make_idesc_bf16(128, HD, 0, 1);
+      const uint32_t id_dq = dev::make_idesc_bf16(HD, BQ2, 1, 1);
+      const uint32_t aK = dev::smem_u32(sK), aV = dev::smem_u32(sV);
+      const uint32_t aPt = dev::smem_u32(sPt), aDSt = dev::smem_u32(sDSt);
+      dev::mbar_wait(kv_full, 0);
+      auto issue_s = [&](int n) {
+        const int st = n & 1, qst = n % QST;
+        dev::mbar_wait(&qdo_full[qst], (n / QST) & 1);
+        if (n >= 2) dev::mbar_wait(&s_free[st], ((n - 2) >> 1) & 1);
+        dev::tc_fence_after();
+        const uint32_t aQ = dev::smem_u32(sQ + qst * Lay::QT), aDO = dev::smem_u32(sDO + qst * Lay::QT);
+#pragma unroll
+        for (int kk = 0; kk < HD / 16; ++kk)
+          dev::umma_f16_ss(t_s + st * BQ2, kdesc(aK, kk), kdesc64(aQ, kk), id_s, kk > 0 ? 1u : 0u);
+#pragma unroll
+        for (int kk = 0; kk < HD / 16; ++kk)
+          dev::umma_f16_ss(t_dp + st * BQ2, kdesc(aV, kk), kdesc64(aDO, kk), id_s, kk > 0 ? 1u : 0u);
+        dev::umma_commit(&s_full[st]);
+      };
+      issue_s(0);
+      for (int n = 0; n < nq; ++n) {
+        const int st = n & 1, qst = n % QST;
+        if (n + 1 < nq) issue_s(n + 1);
+        dev::mbar_wait(p_full, n & 1);
+        dev::tc_fence_after();
+        const uint32_t aQ = dev::smem_u32(sQ + qst * Lay::QT), aDO = dev::smem_u32(sDO + qst * Lay::QT);
+#pragma unroll
+        for (int kk = 0; kk < BQ2 / 16; ++kk)
+          dev::umma_f16_ss(t_dv, kdesc(aPt, kk), mndesc64(aDO, kk), id_kv, (n > 0 || kk > 0) ? 1u : 0u);
+#pragma unroll
+        for (int kk = 0; kk < BQ2 / 16; ++kk)
+          dev::umma_f16_ss(t_dk, kdesc(aDSt, kk), mndesc64(aQ, kk), id_kv, (n > 0 || kk > 0) ? 1u : 0u);
+#pragma unroll
+        for (int kk = 0; kk < 128 / 16; ++kk)
+          dev::umma_f16_ss(t_s + st * BQ2, mndesc(aK, kk), mndesc(aDSt, kk), id_dq, kk > 0 ? 1u : 0u);
+        dev::umma_commit(mma_done);
+        dev::umma_commit(&dq_full[st]);
+        dev::umma_commit(&qdo_empty[qst]);
+      }
+    }
+  } else if (warp >= 4 && warp < 12) {
+    const int wg = (static_cast<int>(warp) - 4) >> 2;             // query columns [32*wg, 32*wg+32)
+    const int t = static_cast<int>(warp & 3) * 32 + static_cast<int>(lane);  // key row
+    const int tid = static_cast<int>(threadIdx.x) - 128;         // 0..255
+    const int key = key0 + t;
+    const uint32_t lane_base = static_cast<uint32_t>((warp & 3) * 32) << 16;
+    const float log2e = 1.4426950408889634f;
+    for (int n = 0; n < nq; ++n) {
+      const int st = n & 1;
+      const int qs = key0 + n * BQ2;
+      float* st_lse = sStat + st * 2 * BQ2;
+      float* st_del = st_lse + BQ2;
+      if (tid < BQ2) {
+        const int qq = qs + tid;
+        st_lse[tid] = qq < T ? lse[static_cast<int64_t>(bh) * T + qq] * log2e : 0.f;
+      } else if (tid < 2 * BQ2) {
+        const int qq = qs + tid - BQ2;
+        st_del[tid - BQ2] = qq < T ? delta[static_cast<int64_t>(bh) * T + qq] : 0.f;
+      }
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+      dev::mbar_wait(&s_full[st], (n >> 1) & 1);
+      dev::tc_fence_after();
+      uint32_t sv[32], pv[32];
+      dev::tmem_ld_32x32b_x32(t_s + lane_base + st * BQ2 + wg * 32, sv);
+      dev::tmem_ld_32x32b_x32(t_dp + lane_base + st * BQ2 + wg * 32, pv);
+      dev::tmem_ld_wait();
+      const bool diag = qs < key0 + 128;
+      uint32_t pk[16], dk[16];
+#pragma unroll
+      for (int e = 0; e < 16; ++e) {
+        float pp[2], dd[2];
+#pragma unroll
+        for (int w2 = 0; w2 < 2; ++w2) {
+          const int qi = wg * 32 + 2 * e + w2;
+          const int qq = qs + qi;
+          float p = dev::ex2_approx(fmaf(__uint_as_float(sv[2 * e + w2]), scale_log2, -st_lse[qi]));
+          const bool ok = qq < T && key < T && (!diag || qq >= key);
+          p = ok ? p : 0.f;
+          pp[w2] = p;
+          dd[w2] = p * (__uint_as_float(pv[2 * e + w2]) - st_del[qi]) * scale;
+        }
+        pk[e] = dev::pack_bf16x2(pp[0], pp[1]);
+        dk[e] = dev::pack_bf16x2(dd[0], dd[1]);
+      }
+      // sPt / sDSt were last read by block n-1's dV / dK / dQ MMAs
+      if (n >= 1) dev::mbar_wait(mma_done, (n - 1) & 1);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        dev::st_sw128(sPt, 128, t, 0, wg * 4 + u, make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]));
+        dev::st_sw128(sDSt, 128, t, 0, wg * 4 + u, make_uint4(dk[4 * u], dk[4 * u + 1], dk[4 * u + 2], dk[4 * u + 3]));
+      }
+      dev::fence_proxy_async_smem();
+      dev::tc_fence_before();
+      dev::mbar_arrive(p_full);
+    }
+    // dK, dV (lane = key row) -> bf16 rows of dqkv; each warpgroup writes HD/2 columns
+    dev::mbar_wait(mma_done, (nq - 1) & 1);
+    dev::tc_fence_after();
+    const int64_t ld = 3LL * Dl;
+    bf16* dk_row = dqkv + (static_cast<int64_t>(row0) + key) * ld + Dl + h * HD;
+    bf16* dv_row = dk_row + Dl;
+#pragma unroll 1
+    for (int c = wg * (HD / 64); c < (wg + 1) * (HD / 64); ++c) {
+      uint32_t a[32], v[32];
+      dev::tmem_ld_32x32b_x32(t_dk + lane_base + c * 32, a);
+      dev::tmem_ld_32x32b_x32(t_dv + lane_base + c * 32, v);
+      dev::tmem_ld_wait();
+      if (key < T) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          uint4 w, z;
+          w.x = dev::pack_bf16x2(__uint_as_float(a[8 * u + 0]), __uint_as_float(a[8 * u + 1]));
+          w.y = dev::pack_bf16x2(__uint_as_float(a[8 * u + 2]), __uint_as_float(a[8 * u + 3]));
+          w.z = dev::pack_bf16x2(__uint_as_float(a[8 * u + 4]), __uint_as_float(a[8 * u + 5]));
+          w.w = dev::pack_bf16x2(__uint_as_float(a[8 * u + 6]), __uint_as_float(a[8 * u + 7]));
+          z.x = dev::pack_bf16x2(__uint_as_float(v[8 * u + 0]), __uint_as_float(v[8 * u + 1]));
+          z.y = dev::pack_bf16x2(__uint_as_float(v[8 * u + 2]), __uint_as_float(v[8 * u + 3]));
+          z.z = dev::pack_bf16x2(__uint_as_float(v[8 * u + 4]), __uint_as_float(v[8 * u + 5]));
+          z.w = dev::pack_bf16x2(__uint_as_float(v[8 * u + 6]), __uint_as_float(v[8 * u + 7]));
+          *reinterpret_cast<uint4*>(dk_row + c * 32 + 8 * u) = w;
+          *reinterpret_cast<uint4*>(dv_row + c * 32 + 8 * u) = z;
+        }
+      }
+    }
+  } else if (warp >= 12) {
+    // dQ^T_n: lane = head dim d, 64 query columns -> SW128 staging [4 boxes][64 rows][32 fp32]
+    // (a warp writes one 128-byte row per query: conflict-free) -> TMA reduce-add
+    const int d = static_cast<int>(warp & 3) * 32 + static_cast<int>(lane);
+    const uint32_t lane_base = static_cast<uint32_t>((warp & 3) * 32) << 16;
+    const int wd = d & 31;
+    uint8_t* bx = sDQ + (d >> 5) * (BQ2 * 128);
+    const bool leader = (warp == 12 && lane == 0);
+    for (int n = 0; n < nq; ++n) {
+      const int st = n & 1;
+      const int qs = key0 + n * BQ2;
+      dev::mbar_wait(&dq_full[st], (n >> 1) & 1);
+      dev::tc_fence_after();
+      uint32_t v[64];
+      dev::tmem_ld_32x32b_x32(t_s + lane_base + st * BQ2, *reinterpret_cast<uint32_t(*)[32]>(v));
+      dev::tmem_ld_32x32b_x32(t_s + lane_base + st * BQ2 + 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
+      dev::tmem_ld_wait();
+      dev::tc_fence_before();
+      dev::mbar_arrive(&s_free[st]);
+      // the previous block's reduce-adds must have read the staging tile
+      if (leader) dev::bulk_wait_read();
+      asm volatile("bar.sync 2, 128;" ::: "memory");
+#pragma unroll
+      for (int q = 0; q < BQ2; ++q) {
+        *reinterpret_cast<uint32_t*>(bx + q * 128 + (((wd >> 2) ^ (q & 7)) << 4) + (wd & 3) * 4) = v[q];
+      }
+      dev::fence_proxy_async_smem();
+      asm volatile("bar.sync 2, 128;" ::: "memory");
+      if (leader) {
+#pragma unroll
+        for (int bb = 0; bb < HD / 32; ++bb)
+          dev::tma_reduce_add_2d(&tm_dq, sDQ + bb * (BQ2 * 128), h * HD + bb * 32, row0 + qs);
+        dev::bulk_commit();
+      }
+    }
+    if (leader) dev::bulk_wait_all();
+  }
+  dev::tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    dev::tc_fence_after();
+    dev::tmem_dealloc<512>(tmem);
+  }
+}
+
 // delta[bh, q] = sum_c dO[q, c] * O[q, c] (one warp per row)
 __global__ void delta_kernel(const bf16* __restrict__ o, const bf16* __restrict__ dout, float* __restrict__ delta,
                              int T, int Hl, int hd, int64_t rows) {
@@ -598,9 +900,51 @@ __global__ void dq_to_bf16(const float* __restrict__ acc, bf16* __restrict__ dqk
   }
 }
 
+bool bwd2_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("SW_ATTN_BWD_V1");
+    return !(e != nullptr && e[0] == '1');
+  }();
+  return on;
+}
+
+bool launch_bwd2(const bf16* qkv, const bf16* o, const float* lse, const bf16* dout, bf16* dqkv, float* scratch,
+                 int B, int T, int Hl, cudaStream_t s) {
+  constexpr int HD = 128;
+  static bool configured = false;
+  if (!configured) {
+    if (cudaFuncSetAttribute(attn_bwd_tc2, cudaFuncAttributeMaxDynamicSharedMemorySize, Bwd2Layout::BYTES) !=
+        cudaSuccess) {
+      return false;
+    }
+    configured = true;
+  }
+  const int Dl = Hl * HD;
+  const int64_t M = static_cast<int64_t>(B) * T;
+  float* delta = scratch;
+  float* dq = scratch + ((M * Hl + 63) / 64) * 64;
+  cudaMemsetAsync(dq, 0, sizeof(float) * M * Dl, s);
+  const int64_t warps = M * Hl;
+  delta_kernel<<<static_cast<unsigned>((warps * 32 + 255) / 256), 256, 0, s>>>(o, dout, delta, T, Hl, HD, M);
+  const CUtensorMap tm_qkv64 = make_tmap_bf16_2d(qkv, 3ull * Dl, static_cast<uint64_t>(M), 3ull * Dl, 64, BQ2);
+  const CUtensorMap tm_qkv128 = make_tmap_bf16_2d(qkv, 3ull * Dl, static_cast<uint64_t>(M), 3ull * Dl, 64, 128);
+  const CUtensorMap tm_do64 = make_tmap_bf16_2d(dout, static_cast<uint64_t>(Dl), static_cast<uint64_t>(M),
+                                                static_cast<uint64_t>(Dl), 64, BQ2);
+  const CUtensorMap tm_dq = make_tmap_f32_2d(dq, static_cast<uint64_t>(Dl), static_cast<uint64_t>(M),
+                                             static_cast<uint64_t>(Dl), 32, BQ2);
+  const int nb = (T + 127) / 128;
+  const double scale = 1.0 / std::sqrt(static_cast<double>(HD));
+  attn_bwd_tc2<<<nb * B * Hl, 512, Bwd2Layout::BYTES, s>>>(tm_qkv64, tm_qkv128, tm_do64, tm_dq, lse, delta, dqkv,
+                                                          T, Hl, static_cast<float>(scale * 1.4426950408889634),
+                                                          static_cast<float>(scale));
+  dq_to_bf16<<<1184, 256, 0, s>>>(dq, dqkv, M, Dl);
+  return true;
+}
+
 template <int HD>
 bool launch_bwd(const bf16* qkv, const bf16* o, const float* lse, const bf16* dout, bf16* dqkv, float* scratch,
                 int B, int T, int Hl, cudaStream_t s) {
+  if (HD == 128 && bwd2_enabled()) return launch_bwd2(qkv, o, lse, dout, dqkv, scratch, B, T, Hl, s);
   using Lay = BwdLayout<HD>;
   static bool configured = false;
   if (!configured) {
