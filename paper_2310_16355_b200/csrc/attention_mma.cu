@@ -693,26 +693,44 @@ __global__ void __launch_bounds__(512, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    // the whole warp runs the issue loop (converged, uniform state); one elected lane issues
+    {
       const uint32_t id_s = dev::make_idesc_bf16(128, BQ2, 0, 0);
       const uint32_t id_kv = dev::make_idesc_bf16(128, HD, 0, 1);
       const uint32_t id_dq = dev::make_idesc_bf16(HD, BQ2, 1, 1);
-      const uint32_t aK = dev::smem_u32(sK), aV = dev::smem_u32(sV);
-      const uint32_t aPt = dev::smem_u32(sPt), aDSt = dev::smem_u32(sDSt);
+      // Descriptor bases built once; a K step only moves the 16-byte address field, so each MMA
+      // costs one add instead of a descriptor rebuild (the issue rate matters at N = 64).
+      const uint64_t dK_k = dev::make_sdesc_sw128(dev::smem_u32(sK), 16, 1024);
+      const uint64_t dK_mn = dev::make_sdesc_sw128(dev::smem_u32(sK), CHUNK, 1024);
+      const uint64_t dV_k = dev::make_sdesc_sw128(dev::smem_u32(sV), 16, 1024);
+      const uint64_t dQ_k = dev::make_sdesc_sw128(dev::smem_u32(sQ), 16, 1024);
+      const uint64_t dQ_mn = dev::make_sdesc_sw128(dev::smem_u32(sQ), CHUNK64, 1024);
+      const uint64_t dDO_k = dev::make_sdesc_sw128(dev::smem_u32(sDO), 16, 1024);
+      const uint64_t dDO_mn = dev::make_sdesc_sw128(dev::smem_u32(sDO), CHUNK64, 1024);
+      const uint64_t dPt_k = dev::make_sdesc_sw128(dev::smem_u32(sPt), 16, 1024);
+      const uint64_t dDSt_k = dev::make_sdesc_sw128(dev::smem_u32(sDSt), 16, 1024);
+      const uint64_t dDSt_mn = dev::make_sdesc_sw128(dev::smem_u32(sDSt), CHUNK, 1024);
+      constexpr uint32_t QT16 = Lay::QT >> 4;
+      auto k128 = [](int kk) { return static_cast<uint64_t>((kk >> 2) * (CHUNK >> 4) + (kk & 3) * 2); };
+      auto k64 = [](int kk) { return static_cast<uint64_t>((kk >> 2) * (CHUNK64 >> 4) + (kk & 3) * 2); };
+      auto mn = [](int kk) { return static_cast<uint64_t>(kk * 128); };
       dev::mbar_wait(kv_full, 0);
       auto issue_s = [&](int n) {
         const int st = n & 1, qst = n % QST;
         dev::mbar_wait(&qdo_full[qst], (n / QST) & 1);
         if (n >= 2) dev::mbar_wait(&s_free[st], ((n - 2) >> 1) & 1);
         dev::tc_fence_after();
-        const uint32_t aQ = dev::smem_u32(sQ + qst * Lay::QT), aDO = dev::smem_u32(sDO + qst * Lay::QT);
+        const uint64_t q_k = dQ_k + qst * QT16, do_k = dDO_k + qst * QT16;
+        if (dev::elect_one_sync()) {
 #pragma unroll
-        for (int kk = 0; kk < HD / 16; ++kk)
-          dev::umma_f16_ss(t_s + st * BQ2, kdesc(aK, kk), kdesc64(aQ, kk), id_s, kk > 0 ? 1u : 0u);
+          for (int kk = 0; kk < HD / 16; ++kk)
+            dev::umma_f16_ss(t_s + st * BQ2, dK_k + k128(kk), q_k + k64(kk), id_s, kk > 0 ? 1u : 0u);
 #pragma unroll
-        for (int kk = 0; kk < HD / 16; ++kk)
-          dev::umma_f16_ss(t_dp + st * BQ2, kdesc(aV, kk), kdesc64(aDO, kk), id_s, kk > 0 ? 1u : 0u);
-        dev::umma_commit(&s_full[st]);
+          for (int kk = 0; kk < HD / 16; ++kk)
+            dev::umma_f16_ss(t_dp + st * BQ2, dV_k + k128(kk), do_k + k64(kk), id_s, kk > 0 ? 1u : 0u);
+          dev::umma_commit(&s_full[st]);
+        }
+        __syncwarp();
       };
       issue_s(0);
       for (int n = 0; n < nq; ++n) {
@@ -720,19 +738,22 @@ __global__ void __launch_bounds__(512, 1)
         if (n + 1 < nq) issue_s(n + 1);
         dev::mbar_wait(p_full, n & 1);
         dev::tc_fence_after();
-        const uint32_t aQ = dev::smem_u32(sQ + qst * Lay::QT), aDO = dev::smem_u32(sDO + qst * Lay::QT);
+        const uint64_t q_mn = dQ_mn + qst * QT16, do_mn = dDO_mn + qst * QT16;
+        if (dev::elect_one_sync()) {
 #pragma unroll
-        for (int kk = 0; kk < BQ2 / 16; ++kk)
-          dev::umma_f16_ss(t_dv, kdesc(aPt, kk), mndesc64(aDO, kk), id_kv, (n > 0 || kk > 0) ? 1u : 0u);
+          for (int kk = 0; kk < BQ2 / 16; ++kk)
+            dev::umma_f16_ss(t_dv, dPt_k + k128(kk), do_mn + mn(kk), id_kv, (n > 0 || kk > 0) ? 1u : 0u);
 #pragma unroll
-        for (int kk = 0; kk < BQ2 / 16; ++kk)
-          dev::umma_f16_ss(t_dk, kdesc(aDSt, kk), mndesc64(aQ, kk), id_kv, (n > 0 || kk > 0) ? 1u : 0u);
+          for (int kk = 0; kk < BQ2 / 16; ++kk)
+            dev::umma_f16_ss(t_dk, dDSt_k + k128(kk), q_mn + mn(kk), id_kv, (n > 0 || kk > 0) ? 1u : 0u);
 #pragma unroll
-        for (int kk = 0; kk < 128 / 16; ++kk)
-          dev::umma_f16_ss(t_s + st * BQ2, mndesc(aK, kk), mndesc(aDSt, kk), id_dq, kk > 0 ? 1u : 0u);
-        dev::umma_commit(mma_done);
-        dev::umma_commit(&dq_full[st]);
-        dev::umma_commit(&qdo_empty[qst]);
+          for (int kk = 0; kk < 128 / 16; ++kk)
+            dev::umma_f16_ss(t_s + st * BQ2, dK_mn + mn(kk), dDSt_mn + mn(kk), id_dq, kk > 0 ? 1u : 0u);
+          dev::umma_commit(mma_done);
+          dev::umma_commit(&dq_full[st]);
+          dev::umma_commit(&qdo_empty[qst]);
+        }
+        __syncwarp();
       }
     }
   } else if (warp >= 4 && warp < 12) {
