@@ -128,34 +128,44 @@ __global__ void __launch_bounds__(384, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    // the whole warp runs the issue loop (uniform descriptors); one elected lane issues
+    {
       const uint32_t id_s = dev::make_idesc_bf16(BQ, BKV, 0, 0);
       const uint32_t id_o = dev::make_idesc_bf16(BQ, HD, 0, 1);
-      const uint32_t aq = dev::smem_u32(sQ);
+      const uint64_t dq = dev::make_sdesc_sw128(dev::smem_u32(sQ), 16, 1024);
+      const uint64_t dk = dev::make_sdesc_sw128(dev::smem_u32(sK), 16, 1024);
+      const uint64_t dp = dev::make_sdesc_sw128(dev::smem_u32(sP), 16, 1024);
+      const uint64_t dv = dev::make_sdesc_sw128(dev::smem_u32(sV), CHUNK, 1024);
+      auto kstep = [](int kk) { return static_cast<uint64_t>((kk >> 2) * (CHUNK >> 4) + (kk & 3) * 2); };
       dev::mbar_wait(q_full, 0);
       auto issue_pv = [&](int j) {
         const int bb = j & 1;
         dev::mbar_wait(&p_full[bb], (j >> 1) & 1);
         dev::tc_fence_after();
-        const uint32_t ap = dev::smem_u32(sP + bb * Lay::P);
-        const uint32_t bv = dev::smem_u32(sV + bb * Lay::KV);
+        const uint64_t ap = dp + static_cast<uint64_t>(bb * (Lay::P >> 4));
+        const uint64_t bv = dv + static_cast<uint64_t>(bb * (Lay::KV >> 4));
+        if (dev::elect_one_sync()) {
 #pragma unroll
-        for (int kk = 0; kk < BKV / 16; ++kk) {
-          dev::umma_f16_ss(t_o, kdesc(ap, kk), mndesc(bv, kk), id_o, (j > 0 || kk > 0) ? 1u : 0u);
+          for (int kk = 0; kk < BKV / 16; ++kk)
+            dev::umma_f16_ss(t_o, ap + kstep(kk), bv + static_cast<uint64_t>(kk * 128), id_o,
+                             (j > 0 || kk > 0) ? 1u : 0u);
+          dev::umma_commit(&pv_done[bb]);
+          dev::umma_commit(&kv_empty[bb]);
         }
-        dev::umma_commit(&pv_done[bb]);
-        dev::umma_commit(&kv_empty[bb]);
+        __syncwarp();
       };
       for (int j = 0; j < nkv; ++j) {
         const int st = j & 1;
         dev::mbar_wait(&kv_full[st], (j >> 1) & 1);
         dev::tc_fence_after();
-        const uint32_t bk = dev::smem_u32(sK + st * Lay::KV);
+        const uint64_t bk = dk + static_cast<uint64_t>(st * (Lay::KV >> 4));
+        if (dev::elect_one_sync()) {
 #pragma unroll
-        for (int kk = 0; kk < HD / 16; ++kk) {
-          dev::umma_f16_ss(tmem + st * 128, kdesc(aq, kk), kdesc(bk, kk), id_s, kk > 0 ? 1u : 0u);
+          for (int kk = 0; kk < HD / 16; ++kk)
+            dev::umma_f16_ss(tmem + st * 128, dq + kstep(kk), bk + kstep(kk), id_s, kk > 0 ? 1u : 0u);
+          dev::umma_commit(&s_full[st]);
         }
-        dev::umma_commit(&s_full[st]);
+        __syncwarp();
         if (j >= 1) issue_pv(j - 1);
       }
       issue_pv(nkv - 1);

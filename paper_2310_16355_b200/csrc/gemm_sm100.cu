@@ -592,8 +592,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    if (rank == 0 && lane == 0) {
+    if (rank == 0) {
+      // the whole warp runs the issue loop (converged: descriptors stay in uniform registers);
+      // one elected lane issues the MMAs and commits
       const uint32_t idesc = dev::make_idesc_bf16(2 * BM, BN, p.a_mn_major, p.b_mn_major);
+      const uint64_t a0 = p.a_mn_major ? dev::make_sdesc_sw128(dev::smem_u32(sA), 8192, 1024)
+                                       : dev::make_sdesc_sw128(dev::smem_u32(sA), 16, 1024);
+      const uint64_t b0 = p.b_mn_major ? dev::make_sdesc_sw128(dev::smem_u32(sB), 8192, 1024)
+                                       : dev::make_sdesc_sw128(dev::smem_u32(sB), 16, 1024);
+      const uint64_t a_step = p.a_mn_major ? (2048 >> 4) : (32 >> 4);  // per 16-deep k step
+      const uint64_t b_step = p.b_mn_major ? (2048 >> 4) : (32 >> 4);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
@@ -605,25 +613,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         for (int kb = 0; kb < num_kb; ++kb) {
           dev::mbar_wait(&full[stage], phase);
           dev::tc_fence_after();
-          const uint32_t a_base = dev::smem_u32(sA + stage * P_A_STAGE);
-          const uint32_t b_base = dev::smem_u32(sB + stage * P_B_STAGE);
+          const uint64_t as = a0 + static_cast<uint64_t>(stage * (P_A_STAGE >> 4));
+          const uint64_t bs = b0 + static_cast<uint64_t>(stage * (P_B_STAGE >> 4));
+          if (dev::elect_one_sync()) {
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k) {
-            const uint64_t adesc =
-                p.a_mn_major ? dev::make_sdesc_sw128(a_base + k * 2048, 8192, 1024)
-                             : dev::make_sdesc_sw128(a_base + k * 32, 16, 1024);
-            const uint64_t bdesc =
-                p.b_mn_major ? dev::make_sdesc_sw128(b_base + k * 2048, 8192, 1024)
-                             : dev::make_sdesc_sw128(b_base + k * 32, 16, 1024);
-            dev::umma_f16_ss_2sm(d_tmem, adesc, bdesc, idesc, (kb | k) != 0 ? 1u : 0u);
+            for (int k = 0; k < BK / 16; ++k)
+              dev::umma_f16_ss_2sm(d_tmem, as + k * a_step, bs + k * b_step, idesc, (kb | k) != 0 ? 1u : 0u);
+            dev::umma_commit_2sm(&empty[stage], 0x3);
           }
-          dev::umma_commit_2sm(&empty[stage], 0x3);
+          __syncwarp();
           if (++stage == P_STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        dev::umma_commit_2sm(&tfull[acc], 0x3);
+        if (dev::elect_one_sync()) dev::umma_commit_2sm(&tfull[acc], 0x3);
+        __syncwarp();
         if (++acc == 2) {
           acc = 0;
           acc_phase ^= 1;
