@@ -778,12 +778,13 @@ __global__ void __launch_bounds__(512, 1)
       const int qs = key0 + n * BQ2;
       float* st_lse = sStat + st * 2 * BQ2;
       float* st_del = st_lse + BQ2;
+      // stats in the form the packed math wants: -lse (log2 units) and -scale * delta
       if (tid < BQ2) {
         const int qq = qs + tid;
-        st_lse[tid] = qq < T ? lse[static_cast<int64_t>(bh) * T + qq] * log2e : 0.f;
+        st_lse[tid] = qq < T ? -lse[static_cast<int64_t>(bh) * T + qq] * log2e : 0.f;
       } else if (tid < 2 * BQ2) {
         const int qq = qs + tid - BQ2;
-        st_del[tid - BQ2] = qq < T ? delta[static_cast<int64_t>(bh) * T + qq] : 0.f;
+        st_del[tid - BQ2] = qq < T ? -scale * delta[static_cast<int64_t>(bh) * T + qq] : 0.f;
       }
       asm volatile("bar.sync 1, 256;" ::: "memory");
       dev::mbar_wait(&s_full[st], (n >> 1) & 1);
@@ -792,23 +793,32 @@ __global__ void __launch_bounds__(512, 1)
       dev::tmem_ld_32x32b_x32(t_s + lane_base + st * BQ2 + wg * 32, sv);
       dev::tmem_ld_32x32b_x32(t_dp + lane_base + st * BQ2 + wg * 32, pv);
       dev::tmem_ld_wait();
-      const bool diag = qs < key0 + 128;
+      // masks only where the block touches the diagonal or the sequence end (block-uniform)
+      const bool masked = qs < key0 + 128 || qs + BQ2 > T || key0 + 128 > T;
+      const float4* nl4 = reinterpret_cast<const float4*>(st_lse + wg * 32);
+      const float4* nd4 = reinterpret_cast<const float4*>(st_del + wg * 32);
+      const float2 sl2 = make_float2(scale_log2, scale_log2), sc2 = make_float2(scale, scale);
       uint32_t pk[16], dk[16];
 #pragma unroll
-      for (int e = 0; e < 16; ++e) {
-        float pp[2], dd[2];
+      for (int g4 = 0; g4 < 8; ++g4) {  // 4 query columns per step: P = 2^(s*sl - lse), dS = P*(dP*sc - sc*delta)
+        const float4 nl = nl4[g4], nd = nd4[g4];
 #pragma unroll
-        for (int w2 = 0; w2 < 2; ++w2) {
-          const int qi = wg * 32 + 2 * e + w2;
-          const int qq = qs + qi;
-          float p = dev::ex2_approx(fmaf(__uint_as_float(sv[2 * e + w2]), scale_log2, -st_lse[qi]));
-          const bool ok = qq < T && key < T && (!diag || qq >= key);
-          p = ok ? p : 0.f;
-          pp[w2] = p;
-          dd[w2] = p * (__uint_as_float(pv[2 * e + w2]) - st_del[qi]) * scale;
+        for (int hh = 0; hh < 2; ++hh) {
+          const int e = 2 * g4 + hh;
+          const float2 a = dev::ffma2(make_float2(__uint_as_float(sv[2 * e]), __uint_as_float(sv[2 * e + 1])), sl2,
+                                      hh ? make_float2(nl.z, nl.w) : make_float2(nl.x, nl.y));
+          float p0 = dev::ex2_approx(a.x), p1 = dev::ex2_approx(a.y);
+          if (masked) {
+            const int qq = qs + wg * 32 + 2 * e;
+            p0 = (qq < T && key < T && qq >= key) ? p0 : 0.f;
+            p1 = (qq + 1 < T && key < T && qq + 1 >= key) ? p1 : 0.f;
+          }
+          const float2 t = dev::ffma2(make_float2(__uint_as_float(pv[2 * e]), __uint_as_float(pv[2 * e + 1])), sc2,
+                                      hh ? make_float2(nd.z, nd.w) : make_float2(nd.x, nd.y));
+          const float2 d = dev::fmul2(make_float2(p0, p1), t);
+          pk[e] = dev::pack_bf16x2(p0, p1);
+          dk[e] = dev::pack_bf16x2(d.x, d.y);
         }
-        pk[e] = dev::pack_bf16x2(pp[0], pp[1]);
-        dk[e] = dev::pack_bf16x2(dd[0], dd[1]);
       }
       // sPt / sDSt were last read by block n-1's dV / dK / dQ MMAs
       if (n >= 1) dev::mbar_wait(mma_done, (n - 1) & 1);
