@@ -1,3 +1,4 @@
+#include <cstdlib>
 // Non-GEMM kernels of the tensor-parallel step: embeddings, LayerNorm, bias-gradient column
 // sums, fused cross entropy, residual adds, AdamW, emulated collectives and device-side
 // parameter init. All are HBM-bound; they use 16-byte vector accesses where the row pitch
@@ -223,6 +224,140 @@ __global__ void __launch_bounds__(THREADS, (THREADS <= 256 ? 4 : 2)) ln_bwd_kern
         w.x = dev::pack_bf16x2(dx.x, dx.y);
         w.y = dev::pack_bf16x2(dx.z, dx.w);
         *reinterpret_cast<uint2*>(g_bf16 + row * d + c) = w;
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < V4; ++j) {
+    const int c = (threadIdx.x + j * THREADS) * 4;
+    if (c < d) {
+      atomicAdd(dscale + c, ds[j].x); atomicAdd(dscale + c + 1, ds[j].y);
+      atomicAdd(dscale + c + 2, ds[j].z); atomicAdd(dscale + c + 3, ds[j].w);
+      atomicAdd(dbias + c, db[j].x); atomicAdd(dbias + c + 1, db[j].y);
+      atomicAdd(dbias + c + 2, db[j].z); atomicAdd(dbias + c + 3, db[j].w);
+    }
+  }
+}
+
+// Block-wide sum of four values with one shared-memory round (red >= 4 * warps floats).
+__device__ __forceinline__ float4 block_sum4(float4 v, float* red) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  v.x = warp_sum(v.x);
+  v.y = warp_sum(v.y);
+  v.z = warp_sum(v.z);
+  v.w = warp_sum(v.w);
+  __syncthreads();
+  if (lane == 0) reinterpret_cast<float4*>(red)[w] = v;
+  __syncthreads();
+  const int nw = (blockDim.x + 31) >> 5;
+  float4 t = lane < nw ? reinterpret_cast<const float4*>(red)[lane] : make_float4(0.f, 0.f, 0.f, 0.f);
+  t.x = warp_sum(t.x);
+  t.y = warp_sum(t.y);
+  t.z = warp_sum(t.z);
+  t.w = warp_sum(t.w);
+  return t;
+}
+
+// LayerNorm backward, two rows per step (d <= 1024 * V4, d % 4 == 0): both rows' x / dy loads
+// are in flight together, their four row sums share one block reduction, and the residual
+// gradient of both rows is prefetched into L1 before that reduction so its latency hides behind
+// it. x / dy are kept in registers between the passes (no re-read).
+template <int THREADS, int V4>
+__global__ void __launch_bounds__(THREADS, 2) ln_bwd2_kernel(
+    const float* __restrict__ x, const float* __restrict__ mean, const float* __restrict__ rstd,
+    const float* __restrict__ scale, const float* __restrict__ dy, float* __restrict__ g_io,
+    bf16* __restrict__ g_bf16, float* __restrict__ dscale, float* __restrict__ dbias, int64_t M,
+    int d, int accumulate) {
+  __shared__ __align__(16) float red[4 * (THREADS / 32)];
+  float4 ds[V4], db[V4];
+#pragma unroll
+  for (int j = 0; j < V4; ++j) ds[j] = db[j] = make_float4(0, 0, 0, 0);
+  const int64_t pairs = (M + 1) / 2;
+  for (int64_t pr = blockIdx.x; pr < pairs; pr += gridDim.x) {
+    const int64_t r0 = 2 * pr;
+    const bool two = r0 + 1 < M;
+    const int64_t r1 = two ? r0 + 1 : r0;
+    const float mu0 = mean[r0], rs0 = rstd[r0], mu1 = mean[r1], rs1 = rstd[r1];
+    float4 xa[V4], da[V4], xb[V4], dbv[V4];
+#pragma unroll
+    for (int j = 0; j < V4; ++j) {
+      const int c = (threadIdx.x + j * THREADS) * 4;
+      if (c < d) {
+        xa[j] = __ldg(reinterpret_cast<const float4*>(x + r0 * d + c));
+        da[j] = __ldg(reinterpret_cast<const float4*>(dy + r0 * d + c));
+        xb[j] = __ldg(reinterpret_cast<const float4*>(x + r1 * d + c));
+        dbv[j] = __ldg(reinterpret_cast<const float4*>(dy + r1 * d + c));
+      }
+    }
+    if (accumulate && (threadIdx.x & 7) == 0) {  // one L1 prefetch per 128-byte line
+#pragma unroll
+      for (int j = 0; j < V4; ++j) {
+        const int c = (threadIdx.x + j * THREADS) * 4;
+        if (c < d) {
+          asm volatile("prefetch.global.L1 [%0];" ::"l"(g_io + r0 * d + c));
+          asm volatile("prefetch.global.L1 [%0];" ::"l"(g_io + r1 * d + c));
+        }
+      }
+    }
+    float4 sums = make_float4(0.f, 0.f, 0.f, 0.f);  // s1(row0), s2(row0), s1(row1), s2(row1)
+#pragma unroll
+    for (int j = 0; j < V4; ++j) {
+      const int c = (threadIdx.x + j * THREADS) * 4;
+      if (c < d) {
+        const float4 sc = __ldg(reinterpret_cast<const float4*>(scale + c));
+        const float4 ha = make_float4((xa[j].x - mu0) * rs0, (xa[j].y - mu0) * rs0, (xa[j].z - mu0) * rs0,
+                                      (xa[j].w - mu0) * rs0);
+        const float4 hb = make_float4((xb[j].x - mu1) * rs1, (xb[j].y - mu1) * rs1, (xb[j].z - mu1) * rs1,
+                                      (xb[j].w - mu1) * rs1);
+        ds[j].x += da[j].x * ha.x; ds[j].y += da[j].y * ha.y; ds[j].z += da[j].z * ha.z; ds[j].w += da[j].w * ha.w;
+        db[j].x += da[j].x; db[j].y += da[j].y; db[j].z += da[j].z; db[j].w += da[j].w;
+        if (two) {
+          ds[j].x += dbv[j].x * hb.x; ds[j].y += dbv[j].y * hb.y; ds[j].z += dbv[j].z * hb.z; ds[j].w += dbv[j].w * hb.w;
+          db[j].x += dbv[j].x; db[j].y += dbv[j].y; db[j].z += dbv[j].z; db[j].w += dbv[j].w;
+        }
+        const float gx = da[j].x * sc.x, gy = da[j].y * sc.y, gz = da[j].z * sc.z, gw = da[j].w * sc.w;
+        sums.x += gx + gy + gz + gw;
+        sums.y += gx * ha.x + gy * ha.y + gz * ha.z + gw * ha.w;
+        const float hx = dbv[j].x * sc.x, hy = dbv[j].y * sc.y, hz = dbv[j].z * sc.z, hw = dbv[j].w * sc.w;
+        sums.z += hx + hy + hz + hw;
+        sums.w += hx * hb.x + hy * hb.y + hz * hb.z + hw * hb.w;
+      }
+    }
+    const float4 t = block_sum4(sums, red);
+    const float gm0 = t.x / d, gxm0 = t.y / d, gm1 = t.z / d, gxm1 = t.w / d;
+#pragma unroll
+    for (int j = 0; j < V4; ++j) {
+      const int c = (threadIdx.x + j * THREADS) * 4;
+      if (c < d) {
+        const float4 sc = __ldg(reinterpret_cast<const float4*>(scale + c));
+        float4 o;
+        o.x = rs0 * (da[j].x * sc.x - gm0 - (xa[j].x - mu0) * rs0 * gxm0);
+        o.y = rs0 * (da[j].y * sc.y - gm0 - (xa[j].y - mu0) * rs0 * gxm0);
+        o.z = rs0 * (da[j].z * sc.z - gm0 - (xa[j].z - mu0) * rs0 * gxm0);
+        o.w = rs0 * (da[j].w * sc.w - gm0 - (xa[j].w - mu0) * rs0 * gxm0);
+        if (accumulate) {
+          const float4 g = *reinterpret_cast<const float4*>(g_io + r0 * d + c);
+          o.x += g.x; o.y += g.y; o.z += g.z; o.w += g.w;
+        }
+        *reinterpret_cast<float4*>(g_io + r0 * d + c) = o;
+        uint2 w;
+        w.x = dev::pack_bf16x2(o.x, o.y);
+        w.y = dev::pack_bf16x2(o.z, o.w);
+        *reinterpret_cast<uint2*>(g_bf16 + r0 * d + c) = w;
+        if (two) {
+          o.x = rs1 * (dbv[j].x * sc.x - gm1 - (xb[j].x - mu1) * rs1 * gxm1);
+          o.y = rs1 * (dbv[j].y * sc.y - gm1 - (xb[j].y - mu1) * rs1 * gxm1);
+          o.z = rs1 * (dbv[j].z * sc.z - gm1 - (xb[j].z - mu1) * rs1 * gxm1);
+          o.w = rs1 * (dbv[j].w * sc.w - gm1 - (xb[j].w - mu1) * rs1 * gxm1);
+          if (accumulate) {
+            const float4 g = *reinterpret_cast<const float4*>(g_io + r1 * d + c);
+            o.x += g.x; o.y += g.y; o.z += g.z; o.w += g.w;
+          }
+          *reinterpret_cast<float4*>(g_io + r1 * d + c) = o;
+          w.x = dev::pack_bf16x2(o.x, o.y);
+          w.y = dev::pack_bf16x2(o.z, o.w);
+          *reinterpret_cast<uint2*>(g_bf16 + r1 * d + c) = w;
+        }
       }
     }
   }
@@ -691,14 +826,27 @@ void layernorm_fwd(const float* x, const float* scale, const float* bias, bf16* 
   }
 }
 
+// SW_LN_BWD_V1=1 selects the one-row-per-step kernel (A/B comparisons).
+static bool ln_bwd_v1() {
+  static const bool v1 = [] {
+    const char* e = std::getenv("SW_LN_BWD_V1");
+    return e != nullptr && e[0] == '1';
+  }();
+  return v1;
+}
+
 void layernorm_bwd(const float* x, const float* mean, const float* rstd, const float* scale,
                    const float* dy, float* g_io, bf16* g_bf16, float* dscale, float* dbias,
                    int64_t M, int d, int accumulate, cudaStream_t s) {
   const unsigned g = static_cast<unsigned>(M < 4 * kSMs ? M : 4 * kSMs);
   if (d % 4 == 0 && d <= 512) {
     ln_bwd_kernel<32, 4><<<g, 32, 0, s>>>(x, mean, rstd, scale, dy, g_io, g_bf16, dscale, dbias, M, d, accumulate);
-  } else if (d % 4 == 0 && d <= 4096) {
+  } else if (d % 4 == 0 && d <= 4096 && ln_bwd_v1()) {
     ln_bwd_kernel<256, 4><<<g, 256, 0, s>>>(x, mean, rstd, scale, dy, g_io, g_bf16, dscale, dbias, M, d, accumulate);
+  } else if (d % 4 == 0 && d <= 4096) {
+    const unsigned g2 = static_cast<unsigned>((M + 1) / 2 < 2 * kSMs ? (M + 1) / 2 : 2 * kSMs);
+    ln_bwd2_kernel<256, 4><<<g2, 256, 0, s>>>(x, mean, rstd, scale, dy, g_io, g_bf16, dscale, dbias, M, d,
+                                              accumulate);
   } else if (d % 4 == 0 && d <= 12288) {
     ln_bwd_kernel<512, 6><<<g, 512, 0, s>>>(x, mean, rstd, scale, dy, g_io, g_bf16, dscale, dbias, M, d, accumulate);
   } else {
