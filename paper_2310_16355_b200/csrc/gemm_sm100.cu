@@ -520,8 +520,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
   uint64_t* tfull = empty + P_STAGES;
   uint64_t* tempty = tfull + 2;
   uint64_t* ofull = tempty + 2;
-  uint64_t* oempty = ofull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(oempty + 2);
+  uint64_t* oempty = ofull + 3;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(oempty + 3);
 
   const uint32_t warp = dev::warp_idx_sync();
   const uint32_t lane = threadIdx.x & 31;
@@ -544,10 +544,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     for (int a = 0; a < 2; ++a) {
       dev::mbar_init(&tfull[a], 1);
       dev::mbar_init(&tempty[a], 8);
-      if (a < OPT_NBUF) {
-        dev::mbar_init(&ofull[a], 1);
-        dev::mbar_init(&oempty[a], 4);
-      }
+    }
+    for (int a = 0; a < OPT_NBUF; ++a) {
+      dev::mbar_init(&ofull[a], 1);
+      dev::mbar_init(&oempty[a], 4);
     }
     dev::fence_barrier_init();
   }
@@ -675,6 +675,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     uint32_t acc_phase = 0;
     int obuf = 0;
     uint32_t oph = 0;
+    int pending = -1;  // buffer whose TMA stores may still be reading shared memory (OPT_NBUF >= 3)
     for (int t = pair; t < num_tiles; t += npairs) {
       int mb, nb;
       tile_coords(t, num_m, num_n, mb, nb);
@@ -705,9 +706,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
               dev::tma_store_2d(&om.m, sbox + OPT_ARR / 4, col0, rw);
               dev::tma_store_2d(&om.v, sbox + OPT_ARR / 2, col0, rw);
               dev::bulk_commit();
-              dev::bulk_wait_read();  // the stores have left shared memory: hand the buffer back
-              dev::mbar_arrive(&oempty[obuf]);
+              if (OPT_NBUF >= 3) {
+                // hand back the previous chunk's buffer once its stores have read it; this
+                // chunk's stores stay in flight while the next chunk is computed
+                if (pending >= 0) {
+                  dev::bulk_wait_read_1();
+                  dev::mbar_arrive(&oempty[pending]);
+                }
+              } else {
+                dev::bulk_wait_read();  // the stores have left shared memory: hand the buffer back
+                dev::mbar_arrive(&oempty[obuf]);
+              }
             }
+            pending = obuf;
             if (++obuf == OPT_NBUF) {
               obuf = 0;
               oph ^= 1;
