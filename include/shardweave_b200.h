@@ -203,6 +203,46 @@ SW_API sw_status sw_model_read_profile(sw_model* model, double ms[8], double wor
 SW_API sw_status sw_model_device_bytes(sw_model* model, int64_t* out);
 
 /* ============================================================================================
+ * SWCK train-state snapshots (checkpoint.hpp:18-28 format, byte-compatible with the reference)
+ * ========================================================================================== */
+
+/* save_checkpoint (checkpoint.hpp:193-220): the optimizer step, the state seed (the init seed),
+ * the given named RNG streams, then replica 0's gathered params / adam_m / adam_v in tree order
+ * (model.hpp:17-43). Under NCCL every rank calls it (the gathers are collective over the mp
+ * group) and world rank 0 writes the file. */
+SW_API sw_status sw_model_save_checkpoint(sw_model* model, const char* path, uint32_t n_rngs,
+                                          const char* const* rng_names, const uint64_t* rng_seeds,
+                                          const uint64_t* rng_stream_ids, const uint64_t* rng_counters);
+/* load_checkpoint (checkpoint.hpp:233-298): validates the file (SW_ERR_CHECKPOINT with the
+ * reference's message and "(at byte offset N)"), re-cuts every tensor onto this model's plan and
+ * mesh, and restores the optimizer step. *n_rngs_out (may be NULL) receives the number of RNG
+ * streams stored; read them with sw_model_checkpoint_rng. */
+SW_API sw_status sw_model_load_checkpoint(sw_model* model, const char* path, uint32_t* n_rngs_out);
+SW_API sw_status sw_model_checkpoint_rng(sw_model* model, uint32_t index, char* name, uint64_t name_cap,
+                                         uint64_t* seed, uint64_t* stream_id, uint64_t* counter);
+/* TrainState step / seed (train_state.hpp:24-27). */
+SW_API sw_status sw_model_state_info(sw_model* model, uint64_t* step, uint64_t* seed);
+
+/* Host-only SWCK codec (no device): parse or write a snapshot file. Records are the
+ * params/x, adam_m/x, adam_v/x triples in file order; only f32 payloads (the executor's
+ * Scalar) are accepted, like load_checkpoint<float>. */
+typedef struct sw_checkpoint sw_checkpoint;
+SW_API sw_status sw_checkpoint_read(const char* path, sw_checkpoint** out);
+SW_API sw_status sw_checkpoint_info(const sw_checkpoint* ck, uint64_t* step, uint64_t* seed, uint32_t* n_rngs,
+                                    uint64_t* n_records);
+SW_API sw_status sw_checkpoint_rng(const sw_checkpoint* ck, uint32_t index, const char** name, uint64_t* seed,
+                                   uint64_t* stream_id, uint64_t* counter);
+SW_API sw_status sw_checkpoint_record(const sw_checkpoint* ck, uint64_t index, const char** name,
+                                      uint32_t* rank, const int64_t** dims, const float** data,
+                                      int64_t* numel);
+SW_API sw_status sw_checkpoint_write(const char* path, uint64_t step, uint64_t seed, uint32_t n_rngs,
+                                     const char* const* rng_names, const uint64_t* rng_seeds,
+                                     const uint64_t* rng_stream_ids, const uint64_t* rng_counters,
+                                     uint64_t n_records, const char* const* rec_names, const uint32_t* ranks,
+                                     const int64_t* const* dims, const float* const* data);
+SW_API void sw_checkpoint_free(sw_checkpoint* ck);
+
+/* ============================================================================================
  * Kernel-level entry points (device pointers). Used by the parity tests and the roofline
  * measurements; each is one launch on `stream`.
  * ========================================================================================== */

@@ -41,6 +41,16 @@ struct ShapeError : Error {
 struct NonFiniteError : Error {
   using Error::Error;
 };
+// CheckpointError (errors.hpp:23-35): the message ends with "(at byte offset N)".
+struct CheckpointError : Error {
+  using Error::Error;
+};
+
+/// A named RNG stream captured in a snapshot (RngSnapshot, checkpoint.hpp:190-191).
+struct RngState {
+  std::string name;
+  uint64_t seed = 0, stream_id = 0, counter = 0;
+};
 
 inline void check(sw_status s) {
   if (s == SW_OK) return;
@@ -50,6 +60,7 @@ inline void check(sw_status s) {
     case SW_ERR_PARTITION: throw PartitionError(s, msg);
     case SW_ERR_SHAPE: throw ShapeError(s, msg);
     case SW_ERR_NONFINITE: throw NonFiniteError(s, msg);
+    case SW_ERR_CHECKPOINT: throw CheckpointError(s, msg);
     default: throw Error(s, msg);
   }
 }
@@ -274,6 +285,37 @@ class Model {
     double x = 0;
     check(sw_model_last_loss(h_, &x));
     return x;
+  }
+  /// save_checkpoint(path, state, mesh, rngs) (checkpoint.hpp:193-220).
+  void save_checkpoint(const std::string& path, const std::vector<RngState>& rngs = {}) {
+    std::vector<const char*> names;
+    std::vector<uint64_t> seeds, ids, ctrs;
+    for (const RngState& r : rngs) {
+      names.push_back(r.name.c_str());
+      seeds.push_back(r.seed);
+      ids.push_back(r.stream_id);
+      ctrs.push_back(r.counter);
+    }
+    check(sw_model_save_checkpoint(h_, path.c_str(), static_cast<uint32_t>(rngs.size()), names.data(),
+                                   seeds.data(), ids.data(), ctrs.data()));
+  }
+  /// load_checkpoint(path, plan, mesh) onto this model (checkpoint.hpp:233-298); returns the
+  /// stored RNG streams.
+  std::vector<RngState> load_checkpoint(const std::string& path) {
+    uint32_t n = 0;
+    check(sw_model_load_checkpoint(h_, path.c_str(), &n));
+    std::vector<RngState> out(n);
+    for (uint32_t i = 0; i < n; ++i) {
+      char buf[4096];
+      check(sw_model_checkpoint_rng(h_, i, buf, sizeof(buf), &out[i].seed, &out[i].stream_id, &out[i].counter));
+      out[i].name = buf;
+    }
+    return out;
+  }
+  uint64_t step() {
+    uint64_t st = 0, sd = 0;
+    check(sw_model_state_info(h_, &st, &sd));
+    return st;
   }
 
  private:

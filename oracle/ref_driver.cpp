@@ -28,6 +28,7 @@
 #include <vector>
 
 #include "shardweave/audit.hpp"
+#include "shardweave/checkpoint.hpp"
 #include "shardweave/model.hpp"
 #include "shardweave/model_spec.hpp"
 #include "shardweave/pipeline.hpp"
@@ -171,7 +172,7 @@ int golden(const ModelSpec& spec, std::uint64_t seed, int dp, int mp, std::int64
   // single-device reference trajectory (audit.hpp:104-118) and the sharded one.
   const DeviceMesh solo = build_mesh(1, 1, 1);
   TrainState<Scalar> ref = shard_params(init, plan, solo);
-  TrainState<Scalar> state = shard_params(init, plan, mesh);
+  TrainState<Scalar> state = shard_params(init, plan, mesh, seed);
   CommReport comm;
   for (int step = 0; step < steps; ++step) {
     const InputMap<Scalar> global = audit_batch<Scalar>(seed, step, global_batch, seq, spec.vocab_size);
@@ -224,6 +225,13 @@ int golden(const ModelSpec& spec, std::uint64_t seed, int dp, int mp, std::int64
   for (const auto& [name, t] : final_ref.entries()) dump.put("ref_final/" + name, t);
   for (const auto& [name, t] : final_spmd.entries()) dump.put("spmd_final/" + name, t);
   std::ofstream(out + "/comm_report.csv") << comm.to_csv();
+  // optional SWCK snapshot of the sharded state (checkpoint.hpp:193-220), with a "train" stream
+  // advanced 17 draws like tests/test_checkpoint.cpp:97-102
+  if (const char* ck = std::getenv("SW_REF_CKPT")) {
+    RngStream train(seed, "train");
+    for (int i = 0; i < 17; ++i) train.next_u64();
+    save_checkpoint(ck, state, mesh, {{"train", train}});
+  }
   return 0;
 }
 
@@ -404,6 +412,30 @@ int main(int argc, char** argv) {
       const double lr = std::atof(argv[10]), wd = std::atof(argv[11]);
       if (dtype == "f64") return golden<double>(spec, seed, dp, mp, gb, seq, steps, lr, wd, argv[12]);
       return golden<float>(spec, seed, dp, mp, gb, seq, steps, lr, wd, argv[12]);
+    }
+    if (cmd == "ckload" && argc == 6) {
+      // ckload <spec> <dtype f32|f64> <mp> <file>: load_checkpoint (checkpoint.hpp:233-298) with the
+      // rule plan at mp; prints "ok <step> <seed> <records>" or the CheckpointError text.
+      const ModelSpec spec = parse_model_spec(slurp(argv[2]));
+      const std::string dtype = argv[3];
+      const int mp = std::atoi(argv[4]);
+      const auto shapes = transformer_param_shapes(spec);
+      ParamTree<double> tree;
+      for (const auto& [name, shape] : shapes) tree.add(name, Tensor<double>::zeros(shape));
+      const ShardingPlan plan = derive_plan(tree, mp, spec.overrides);
+      const DeviceMesh mesh = build_mesh(1, mp, 1);
+      try {
+        if (dtype == "f64") {
+          auto l = load_checkpoint<double>(argv[5], plan, mesh);
+          std::cout << "ok " << l.state.step << " " << l.state.seed << " " << l.state.names.size() << "\n";
+        } else {
+          auto l = load_checkpoint<float>(argv[5], plan, mesh);
+          std::cout << "ok " << l.state.step << " " << l.state.seed << " " << l.state.names.size() << "\n";
+        }
+      } catch (const CheckpointError& e) {
+        std::cout << e.what() << "\n";
+      }
+      return 0;
     }
     if (cmd == "trainer" && argc == 15) {
       // trainer <spec> <seed> <dp> <mp> <per_device_batch> <accumulate> <epochs> <n_examples> <seq>

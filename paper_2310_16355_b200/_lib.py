@@ -44,7 +44,11 @@ class NonFiniteError(SwError):
     pass
 
 
-_ERR_CLASSES = {1: ShapeError, 2: PartitionError, 3: ConfigError, 4: NonFiniteError}
+class CheckpointError(SwError):
+    """Corrupt or truncated snapshot (errors.hpp:23-35); the message carries the byte offset."""
+
+
+_ERR_CLASSES = {1: ShapeError, 2: PartitionError, 3: ConfigError, 4: NonFiniteError, 5: CheckpointError}
 
 _lib = None
 

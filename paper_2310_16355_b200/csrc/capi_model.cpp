@@ -219,3 +219,155 @@ sw_status sw_model_device_bytes(sw_model* model, int64_t* out) {
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------------------------
+// SWCK snapshots
+// ---------------------------------------------------------------------------------------------
+struct sw_checkpoint {
+  sw::Checkpoint ck;
+};
+
+namespace {
+std::vector<sw::CkptRng> rng_list(uint32_t n, const char* const* names, const uint64_t* seeds, const uint64_t* ids,
+                                  const uint64_t* counters) {
+  std::vector<sw::CkptRng> out;
+  if (n > 0) {
+    require(names, "rng_names");
+    require(seeds, "rng_seeds");
+    require(ids, "rng_stream_ids");
+    require(counters, "rng_counters");
+  }
+  for (uint32_t i = 0; i < n; ++i) {
+    require(names[i], "rng name");
+    out.push_back(sw::CkptRng{names[i], seeds[i], ids[i], counters[i]});
+  }
+  return out;
+}
+}  // namespace
+
+extern "C" {
+
+sw_status sw_model_save_checkpoint(sw_model* model, const char* path, uint32_t n_rngs, const char* const* rng_names,
+                                   const uint64_t* rng_seeds, const uint64_t* rng_stream_ids,
+                                   const uint64_t* rng_counters) {
+  return sw::guarded([&] {
+    require(model, "model");
+    require(path, "path");
+    model->model->save_checkpoint(path, rng_list(n_rngs, rng_names, rng_seeds, rng_stream_ids, rng_counters));
+  });
+}
+
+sw_status sw_model_load_checkpoint(sw_model* model, const char* path, uint32_t* n_rngs_out) {
+  return sw::guarded([&] {
+    require(model, "model");
+    require(path, "path");
+    model->model->load_checkpoint(path);
+    if (n_rngs_out != nullptr) *n_rngs_out = static_cast<uint32_t>(model->model->loaded_rngs().size());
+  });
+}
+
+sw_status sw_model_checkpoint_rng(sw_model* model, uint32_t index, char* name, uint64_t name_cap, uint64_t* seed,
+                                  uint64_t* stream_id, uint64_t* counter) {
+  return sw::guarded([&] {
+    require(model, "model");
+    const auto& r = model->model->loaded_rngs();
+    if (index >= r.size()) sw::fail(SW_ERR_CONFIG, "checkpoint rng index out of range");
+    if (name != nullptr) {
+      if (name_cap < r[index].name.size() + 1) sw::fail(SW_ERR_CONFIG, "checkpoint rng name buffer too small");
+      std::memcpy(name, r[index].name.c_str(), r[index].name.size() + 1);
+    }
+    if (seed) *seed = r[index].seed;
+    if (stream_id) *stream_id = r[index].stream_id;
+    if (counter) *counter = r[index].counter;
+  });
+}
+
+sw_status sw_model_state_info(sw_model* model, uint64_t* step, uint64_t* seed) {
+  return sw::guarded([&] {
+    require(model, "model");
+    if (step) *step = model->model->step();
+    if (seed) *seed = model->model->seed();
+  });
+}
+
+sw_status sw_checkpoint_read(const char* path, sw_checkpoint** out) {
+  return sw::guarded([&] {
+    require(path, "path");
+    require(out, "out");
+    auto* ck = new sw_checkpoint{sw::read_checkpoint(path)};
+    *out = ck;
+  });
+}
+
+sw_status sw_checkpoint_info(const sw_checkpoint* ck, uint64_t* step, uint64_t* seed, uint32_t* n_rngs,
+                             uint64_t* n_records) {
+  return sw::guarded([&] {
+    require(ck, "checkpoint");
+    if (step) *step = ck->ck.step;
+    if (seed) *seed = ck->ck.seed;
+    if (n_rngs) *n_rngs = static_cast<uint32_t>(ck->ck.rngs.size());
+    if (n_records) *n_records = ck->ck.records.size();
+  });
+}
+
+sw_status sw_checkpoint_rng(const sw_checkpoint* ck, uint32_t index, const char** name, uint64_t* seed,
+                            uint64_t* stream_id, uint64_t* counter) {
+  return sw::guarded([&] {
+    require(ck, "checkpoint");
+    if (index >= ck->ck.rngs.size()) sw::fail(SW_ERR_CONFIG, "checkpoint rng index out of range");
+    const sw::CkptRng& r = ck->ck.rngs[index];
+    if (name) *name = r.name.c_str();
+    if (seed) *seed = r.seed;
+    if (stream_id) *stream_id = r.stream_id;
+    if (counter) *counter = r.counter;
+  });
+}
+
+sw_status sw_checkpoint_record(const sw_checkpoint* ck, uint64_t index, const char** name, uint32_t* rank,
+                               const int64_t** dims, const float** data, int64_t* numel) {
+  return sw::guarded([&] {
+    require(ck, "checkpoint");
+    if (index >= ck->ck.records.size()) sw::fail(SW_ERR_CONFIG, "checkpoint record index out of range");
+    const sw::CkptRecord& r = ck->ck.records[index];
+    if (name) *name = r.name.c_str();
+    if (rank) *rank = static_cast<uint32_t>(r.shape.size());
+    if (dims) *dims = r.shape.data();
+    if (data) *data = r.data.data();
+    if (numel) *numel = static_cast<int64_t>(r.data.size());
+  });
+}
+
+sw_status sw_checkpoint_write(const char* path, uint64_t step, uint64_t seed, uint32_t n_rngs,
+                              const char* const* rng_names, const uint64_t* rng_seeds, const uint64_t* rng_stream_ids,
+                              const uint64_t* rng_counters, uint64_t n_records, const char* const* rec_names,
+                              const uint32_t* ranks, const int64_t* const* dims, const float* const* data) {
+  return sw::guarded([&] {
+    require(path, "path");
+    sw::Checkpoint ck;
+    ck.step = step;
+    ck.seed = seed;
+    ck.rngs = rng_list(n_rngs, rng_names, rng_seeds, rng_stream_ids, rng_counters);
+    if (n_records > 0) {
+      require(rec_names, "rec_names");
+      require(ranks, "ranks");
+      require(dims, "dims");
+      require(data, "data");
+    }
+    for (uint64_t i = 0; i < n_records; ++i) {
+      sw::CkptRecord r;
+      r.name = rec_names[i];
+      int64_t n = 1;
+      for (uint32_t k = 0; k < ranks[i]; ++k) {
+        r.shape.push_back(dims[i][k]);
+        n *= dims[i][k];
+      }
+      r.data.assign(data[i], data[i] + n);
+      ck.records.push_back(std::move(r));
+    }
+    sw::write_checkpoint(path, ck);
+  });
+}
+
+void sw_checkpoint_free(sw_checkpoint* ck) { delete ck; }
+
+}  // extern "C"

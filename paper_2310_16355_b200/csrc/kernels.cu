@@ -76,6 +76,56 @@ __global__ void embed_bwd_tok_kernel(const int32_t* __restrict__ ids, const floa
   for (int i = threadIdx.x; i < d; i += blockDim.x) atomicAdd(dtok + id * d + i, g[m * d + i]);
 }
 
+// keys[i] = (token << 16) | position, padded with 0xffffffff, bitonic-sorted by one CTA.
+__global__ void __launch_bounds__(1024) sort_token_keys_kernel(const int32_t* __restrict__ ids, int64_t M, int n,
+                                                               uint32_t* __restrict__ keys) {
+  extern __shared__ uint32_t sk[];
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    sk[i] = i < M ? (static_cast<uint32_t>(ids[i]) << 16) | static_cast<uint32_t>(i) : 0xffffffffu;
+  }
+  __syncthreads();
+  for (int k = 2; k <= n; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const int ixj = i ^ j;
+        if (ixj > i) {
+          const uint32_t a = sk[i], b = sk[ixj];
+          const bool up = (i & k) == 0;
+          if ((a > b) == up) {
+            sk[i] = b;
+            sk[ixj] = a;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (int i = threadIdx.x; i < n; i += blockDim.x) keys[i] = sk[i];
+}
+
+// Each CTA owns the token runs that start in its slice of the sorted keys and sums the run's
+// gradient rows in ascending position order; one owner per token row -> plain (non-atomic) +=.
+__global__ void embed_accum_sorted_kernel(const uint32_t* __restrict__ keys, int64_t M, const float* __restrict__ g,
+                                          float* __restrict__ dtok, int d, int64_t per_cta) {
+  const int64_t i0 = blockIdx.x * per_cta;
+  const int64_t i1 = i0 + per_cta < M ? i0 + per_cta : M;
+  for (int64_t i = i0; i < i1; ++i) {
+    const uint32_t tok = keys[i] >> 16;
+    if (i > 0 && (keys[i - 1] >> 16) == tok) continue;  // not the start of a run
+    int64_t e = i + 1;
+    while (e < M && (keys[e] >> 16) == tok) ++e;
+    float* dst = dtok + static_cast<int64_t>(tok) * d;
+    for (int c = threadIdx.x * 4; c < d; c += blockDim.x * 4) {
+      float4 acc = *reinterpret_cast<const float4*>(dst + c);
+      for (int64_t r = i; r < e; ++r) {
+        const float4 v = __ldg(reinterpret_cast<const float4*>(g + static_cast<int64_t>(keys[r] & 0xffffu) * d + c));
+        acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+      }
+      *reinterpret_cast<float4*>(dst + c) = acc;
+    }
+  }
+}
+
 __global__ void embed_bwd_pos_kernel(const float* __restrict__ g, float* __restrict__ dpos, int B,
                                      int T, int d, int accumulate) {
   const int t = blockIdx.x;
@@ -175,7 +225,7 @@ __global__ void __launch_bounds__(THREADS, (THREADS <= 256 ? 4 : 2)) ln_bwd_kern
     const float* __restrict__ x, const float* __restrict__ mean, const float* __restrict__ rstd,
     const float* __restrict__ scale, const float* __restrict__ dy, float* __restrict__ g_io,
     bf16* __restrict__ g_bf16, float* __restrict__ dscale, float* __restrict__ dbias, int64_t M,
-    int d, int accumulate) {
+    int d, int accumulate, float* __restrict__ partials) {
   __shared__ float red[32];
   float4 ds[V4], db[V4];
 #pragma unroll
@@ -231,13 +281,21 @@ __global__ void __launch_bounds__(THREADS, (THREADS <= 256 ? 4 : 2)) ln_bwd_kern
   for (int j = 0; j < V4; ++j) {
     const int c = (threadIdx.x + j * THREADS) * 4;
     if (c < d) {
-      atomicAdd(dscale + c, ds[j].x); atomicAdd(dscale + c + 1, ds[j].y);
-      atomicAdd(dscale + c + 2, ds[j].z); atomicAdd(dscale + c + 3, ds[j].w);
-      atomicAdd(dbias + c, db[j].x); atomicAdd(dbias + c + 1, db[j].y);
-      atomicAdd(dbias + c + 2, db[j].z); atomicAdd(dbias + c + 3, db[j].w);
+      if (partials != nullptr) {  // deterministic: per-CTA partials, summed in CTA order later
+        float* pp = partials + static_cast<int64_t>(blockIdx.x) * 2 * d;
+        *reinterpret_cast<float4*>(pp + c) = ds[j];
+        *reinterpret_cast<float4*>(pp + d + c) = db[j];
+      } else {
+        atomicAdd(dscale + c, ds[j].x); atomicAdd(dscale + c + 1, ds[j].y);
+        atomicAdd(dscale + c + 2, ds[j].z); atomicAdd(dscale + c + 3, ds[j].w);
+        atomicAdd(dbias + c, db[j].x); atomicAdd(dbias + c + 1, db[j].y);
+        atomicAdd(dbias + c + 2, db[j].z); atomicAdd(dbias + c + 3, db[j].w);
+      }
     }
   }
 }
+
+
 
 // Block-wide sum of four values with one shared-memory round (red >= 4 * warps floats).
 __device__ __forceinline__ float4 block_sum4(float4 v, float* red) {
@@ -267,7 +325,7 @@ __global__ void __launch_bounds__(THREADS, 2) ln_bwd2_kernel(
     const float* __restrict__ x, const float* __restrict__ mean, const float* __restrict__ rstd,
     const float* __restrict__ scale, const float* __restrict__ dy, float* __restrict__ g_io,
     bf16* __restrict__ g_bf16, float* __restrict__ dscale, float* __restrict__ dbias, int64_t M,
-    int d, int accumulate) {
+    int d, int accumulate, float* __restrict__ partials) {
   __shared__ __align__(16) float red[4 * (THREADS / 32)];
   float4 ds[V4], db[V4];
 #pragma unroll
@@ -365,12 +423,32 @@ __global__ void __launch_bounds__(THREADS, 2) ln_bwd2_kernel(
   for (int j = 0; j < V4; ++j) {
     const int c = (threadIdx.x + j * THREADS) * 4;
     if (c < d) {
-      atomicAdd(dscale + c, ds[j].x); atomicAdd(dscale + c + 1, ds[j].y);
-      atomicAdd(dscale + c + 2, ds[j].z); atomicAdd(dscale + c + 3, ds[j].w);
-      atomicAdd(dbias + c, db[j].x); atomicAdd(dbias + c + 1, db[j].y);
-      atomicAdd(dbias + c + 2, db[j].z); atomicAdd(dbias + c + 3, db[j].w);
+      if (partials != nullptr) {  // deterministic: per-CTA partials, summed in CTA order later
+        float* pp = partials + static_cast<int64_t>(blockIdx.x) * 2 * d;
+        *reinterpret_cast<float4*>(pp + c) = ds[j];
+        *reinterpret_cast<float4*>(pp + d + c) = db[j];
+      } else {
+        atomicAdd(dscale + c, ds[j].x); atomicAdd(dscale + c + 1, ds[j].y);
+        atomicAdd(dscale + c + 2, ds[j].z); atomicAdd(dscale + c + 3, ds[j].w);
+        atomicAdd(dbias + c, db[j].x); atomicAdd(dbias + c + 1, db[j].y);
+        atomicAdd(dbias + c + 2, db[j].z); atomicAdd(dbias + c + 3, db[j].w);
+      }
     }
   }
+}
+
+
+
+// dscale[c] += sum_b partials[b][0][c], dbias[c] += sum_b partials[b][1][c], b ascending.
+__global__ void ln_param_reduce_kernel(const float* __restrict__ partials, int nblk, int d, float* __restrict__ dscale,
+                                       float* __restrict__ dbias) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= 2 * d) return;
+  const int which = c / d, col = c - which * d;
+  float s = 0.f;
+  for (int b = 0; b < nblk; ++b) s += partials[static_cast<int64_t>(b) * 2 * d + which * d + col];
+  float* o = which == 0 ? dscale : dbias;
+  o[col] += s;
 }
 
 __global__ void ln_bwd_generic_kernel(const float* __restrict__ x, const float* __restrict__ mean,
@@ -804,8 +882,27 @@ void embed_fwd(const int32_t* ids, const float* tok, const float* pos, float* h,
   embed_fwd_kernel<<<static_cast<unsigned>(M), d >= 1024 ? 256 : 128, 0, s>>>(ids, tok, pos, h, T, d);
 }
 
-void embed_bwd_tok(const int32_t* ids, const float* g, float* dtok, int64_t M, int d, cudaStream_t s) {
-  embed_bwd_tok_kernel<<<static_cast<unsigned>(M), 256, 0, s>>>(ids, g, dtok, d);
+void embed_bwd_tok(const int32_t* ids, const float* g, float* dtok, int64_t M, int d, int V, uint32_t* keys,
+                   cudaStream_t s) {
+  if (keys == nullptr || M > 32768 || V > 65535 || d % 4 != 0) {
+    embed_bwd_tok_kernel<<<static_cast<unsigned>(M), 256, 0, s>>>(ids, g, dtok, d);
+    return;
+  }
+  const int n = static_cast<int>(embed_bwd_keys(M));
+  static int configured_bytes = 0;
+  if (n * 4 > configured_bytes) {
+    cudaFuncSetAttribute(sort_token_keys_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, n * 4);
+    configured_bytes = n * 4;
+  }
+  sort_token_keys_kernel<<<1, 1024, n * 4, s>>>(ids, M, n, keys);
+  const int64_t per = 16;
+  embed_accum_sorted_kernel<<<static_cast<unsigned>((M + per - 1) / per), 256, 0, s>>>(keys, M, g, dtok, d, per);
+}
+
+int64_t embed_bwd_keys(int64_t M) {
+  int64_t n = 1;
+  while (n < M) n <<= 1;
+  return n < 2 ? 2 : n;
 }
 
 void embed_bwd_pos(const float* g, float* dpos, int B, int T, int d, int accumulate, cudaStream_t s) {
@@ -835,23 +932,36 @@ static bool ln_bwd_v1() {
   return v1;
 }
 
+int64_t layernorm_bwd_partials(int d) { return static_cast<int64_t>(4 * kSMs) * 2 * d; }
+
 void layernorm_bwd(const float* x, const float* mean, const float* rstd, const float* scale,
                    const float* dy, float* g_io, bf16* g_bf16, float* dscale, float* dbias,
-                   int64_t M, int d, int accumulate, cudaStream_t s) {
+                   int64_t M, int d, int accumulate, cudaStream_t s, float* partials) {
   const unsigned g = static_cast<unsigned>(M < 4 * kSMs ? M : 4 * kSMs);
+  unsigned nblk = g;
   if (d % 4 == 0 && d <= 512) {
-    ln_bwd_kernel<32, 4><<<g, 32, 0, s>>>(x, mean, rstd, scale, dy, g_io, g_bf16, dscale, dbias, M, d, accumulate);
+    ln_bwd_kernel<32, 4><<<g, 32, 0, s>>>(x, mean, rstd, scale, dy, g_io, g_bf16, dscale, dbias, M, d, accumulate,
+                                          partials);
   } else if (d % 4 == 0 && d <= 4096 && ln_bwd_v1()) {
-    ln_bwd_kernel<256, 4><<<g, 256, 0, s>>>(x, mean, rstd, scale, dy, g_io, g_bf16, dscale, dbias, M, d, accumulate);
+    ln_bwd_kernel<256, 4><<<g, 256, 0, s>>>(x, mean, rstd, scale, dy, g_io, g_bf16, dscale, dbias, M, d, accumulate,
+                                            partials);
   } else if (d % 4 == 0 && d <= 4096) {
     const unsigned g2 = static_cast<unsigned>((M + 1) / 2 < 2 * kSMs ? (M + 1) / 2 : 2 * kSMs);
+    nblk = g2;
     ln_bwd2_kernel<256, 4><<<g2, 256, 0, s>>>(x, mean, rstd, scale, dy, g_io, g_bf16, dscale, dbias, M, d,
-                                              accumulate);
+                                              accumulate, partials);
   } else if (d % 4 == 0 && d <= 12288) {
-    ln_bwd_kernel<512, 6><<<g, 512, 0, s>>>(x, mean, rstd, scale, dy, g_io, g_bf16, dscale, dbias, M, d, accumulate);
+    ln_bwd_kernel<512, 6><<<g, 512, 0, s>>>(x, mean, rstd, scale, dy, g_io, g_bf16, dscale, dbias, M, d, accumulate,
+                                            partials);
   } else {
+    // one CTA per row: parameter partials would be row-sized; this shape keeps the atomics
     ln_bwd_generic_kernel<<<static_cast<unsigned>(M), 256, 0, s>>>(x, mean, rstd, scale, dy, g_io, g_bf16,
                                                                   dscale, dbias, d, accumulate);
+    return;
+  }
+  if (partials != nullptr) {
+    ln_param_reduce_kernel<<<static_cast<unsigned>((2 * d + 255) / 256), 256, 0, s>>>(partials, static_cast<int>(nblk),
+                                                                                     d, dscale, dbias);
   }
 }
 

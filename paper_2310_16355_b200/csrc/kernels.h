@@ -17,7 +17,13 @@ using bf16 = __nv_bfloat16;
 void embed_fwd(const int32_t* ids, const float* tok, const float* pos, float* h, int64_t M, int T,
                int d, cudaStream_t s);
 // dtok[ids[m], :] += g[m, :] (atomic); dpos[t, :] (+)= sum_b g[b*T + t, :]   (kernels.hpp:291-304)
-void embed_bwd_tok(const int32_t* ids, const float* g, float* dtok, int64_t M, int d, cudaStream_t s);
+// dtok[ids[m]] += g[m] for every position. With `keys` scratch (ceil_pow2(M) uint32) and
+// V <= 65535, M <= 65536 the positions are sorted by token (one-CTA bitonic sort) and each token's
+// rows are summed in ascending position order (M <= 32768): deterministic, so replicated embedding tables stay
+// bit-identical across tensor-parallel ranks like the reference's. keys == nullptr: atomics.
+void embed_bwd_tok(const int32_t* ids, const float* g, float* dtok, int64_t M, int d, int V, uint32_t* keys,
+                   cudaStream_t s);
+int64_t embed_bwd_keys(int64_t M);  // scratch elements embed_bwd_tok needs
 void embed_bwd_pos(const float* g, float* dpos, int B, int T, int d, int accumulate, cudaStream_t s);
 
 // LayerNorm over the last dim, biased variance, eps (kernels.hpp:184-215): y = xhat*scale+bias
@@ -27,9 +33,12 @@ void layernorm_fwd(const float* x, const float* scale, const float* bias, bf16* 
 // dx = rstd*(g - mean(g) - xhat*mean(g*xhat)), g = dy*scale (kernels.hpp:232-271).
 // g_io: residual-stream gradient; g_io = (accumulate ? g_io : 0) + dx; g_bf16 = bf16(g_io).
 // dscale += sum_rows dy*xhat, dbias += sum_rows dy (atomics; caller zeroes when needed).
+// dscale / dbias: with `partials` scratch (layernorm_bwd_partials(d) floats) every CTA writes its
+// column partials and one fixed-order pass adds them (deterministic); partials == nullptr: atomics.
 void layernorm_bwd(const float* x, const float* mean, const float* rstd, const float* scale,
                    const float* dy, float* g_io, bf16* g_bf16, float* dscale, float* dbias,
-                   int64_t M, int d, int accumulate, cudaStream_t s);
+                   int64_t M, int d, int accumulate, cudaStream_t s, float* partials = nullptr);
+int64_t layernorm_bwd_partials(int d);
 
 // Column sums of X [M, N] (bf16 or f32, row pitch ld) written (accumulate=0) or added into
 // out: column n goes to outs[n / seg][n % seg] (up to 3 segments). scratch: >= 64*N floats.

@@ -1,6 +1,8 @@
 // GPU executor of the tensor-parallel transformer step (see model.h).
 #include "model.h"
 
+#include <unordered_map>
+
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -310,6 +312,8 @@ void Model::allocate() {
     if (3 * dl_ > widest) widest = 3 * dl_;
     if (fl_ > widest) widest = fl_;
     R.col_scratch = alloc<float>(chunks * widest);
+    R.ln_partials = alloc<float>(k::layernorm_bwd_partials(d_));
+    R.tok_keys = alloc<uint32_t>(k::embed_bwd_keys(M_));
     R.attn_scratch = alloc<float>(M * hl_ + M * 2 * dl_ + 64);
     R.xstats = alloc<float>(static_cast<int64_t>(mesh_->mp) * M * 2);
     R.xt = alloc<float>(M);
@@ -357,10 +361,15 @@ void Model::init_params(uint64_t seed, const std::string& stream_name) {
     ++launches_;
   }
   step_ = 0;
+  seed_ = seed;
   cuda_check(cudaGetLastError(), "init_params");
 }
 
 void Model::set_param(const std::string& name, const float* full, int64_t numel) {
+  set_tensor(name, 0, full, numel);
+}
+
+void Model::set_tensor(const std::string& name, int which, const float* full, int64_t numel) {
   const auto it = slot_of_.find(name);
   if (it == slot_of_.end()) fail(SW_ERR_CONFIG, "TrainState: no parameter named '" + name + "'");
   const Slot& s = slots_[it->second];
@@ -368,8 +377,9 @@ void Model::set_param(const std::string& name, const float* full, int64_t numel)
     fail(SW_ERR_SHAPE, "set_param: '" + name + "' expects " + std::to_string(numel_of(s.global)) +
                            " elements, got " + std::to_string(numel));
   }
+  if (which != 0 && which != 2 && which != 3) fail(SW_ERR_CONFIG, "set_tensor: `which` must be 0, 2 or 3");
   for (Rank& R : ranks_) {
-    float* dst = R.p + s.offset;
+    float* dst = (which == 0 ? R.p : which == 2 ? R.m : R.v) + s.offset;
     if (s.layout.kind != Layout::kSplit) {
       cuda_check(cudaMemcpyAsync(dst, full, numel * 4, cudaMemcpyHostToDevice, stream_), "H2D");
     } else {
@@ -385,9 +395,65 @@ void Model::set_param(const std::string& name, const float* full, int64_t numel)
                    "H2D 2D");
       }
     }
-    k::cast_f32_bf16(dst, R.w + s.offset, s.numel, stream_);
+    if (which == 0) k::cast_f32_bf16(dst, R.w + s.offset, s.numel, stream_);
   }
   cuda_check(cudaStreamSynchronize(stream_), "set_param");
+}
+
+void Model::save_checkpoint(const std::string& path, const std::vector<CkptRng>& rngs) {
+  Checkpoint ck;
+  ck.step = step_;
+  ck.seed = seed_;
+  ck.rngs = rngs;
+  static const char* kPrefix[3] = {"params/", "adam_m/", "adam_v/"};
+  static const int kWhich[3] = {0, 2, 3};
+  for (const NamedShape& ns : transformer_param_shapes(spec_)) {  // tree order (model.hpp:17-43)
+    int64_t n = 1;
+    for (int64_t dd : ns.dims) n *= dd;
+    for (int i = 0; i < 3; ++i) {
+      CkptRecord rec;
+      rec.name = std::string(kPrefix[i]) + ns.name;
+      rec.shape.assign(ns.dims.begin(), ns.dims.end());
+      rec.data.resize(static_cast<size_t>(n));
+      get_tensor(ns.name, kWhich[i], rec.data.data(), n);  // collective over the mp group under NCCL
+      ck.records.push_back(std::move(rec));
+    }
+  }
+  // one writer per job: the emulated mesh's process, or world rank 0
+  if (mesh_->emulated || mesh_->rank == 0) write_checkpoint(path, ck);
+}
+
+void Model::load_checkpoint(const std::string& path) {
+  Checkpoint ck = read_checkpoint(path);
+  std::unordered_map<std::string, size_t> in_file;
+  for (size_t r = 0; r < ck.records.size(); r += 3) in_file[ck.records[r].name.substr(7)] = r;
+  for (const NamedShape& ns : transformer_param_shapes(spec_)) {
+    const auto f = in_file.find(ns.name);
+    if (f == in_file.end()) {
+      fail(SW_ERR_CHECKPOINT, "checkpoint: no record for parameter '" + ns.name + "' of this model");
+    }
+    const std::vector<int64_t> want(ns.dims.begin(), ns.dims.end());
+    if (ck.records[f->second].shape != want) {
+      fail(SW_ERR_CHECKPOINT, "checkpoint: record 'params/" + ns.name + "' does not match the model's shape");
+    }
+  }
+  if (in_file.size() != slot_of_.size()) {
+    for (const auto& kv : in_file) {
+      if (slot_of_.find(kv.first) == slot_of_.end()) {
+        fail(SW_ERR_CHECKPOINT, "checkpoint: record 'params/" + kv.first + "' names no parameter of this model");
+      }
+    }
+  }
+  for (size_t r = 0; r < ck.records.size(); r += 3) {
+    const std::string name = ck.records[r].name.substr(7);
+    const int64_t n = static_cast<int64_t>(ck.records[r].data.size());
+    set_tensor(name, 0, ck.records[r].data.data(), n);
+    set_tensor(name, 2, ck.records[r + 1].data.data(), n);
+    set_tensor(name, 3, ck.records[r + 2].data.data(), n);
+  }
+  step_ = ck.step;
+  seed_ = ck.seed;
+  loaded_rngs_ = std::move(ck.rngs);
 }
 
 void Model::get_tensor(const std::string& name, int which, float* full, int64_t numel) {
@@ -780,7 +846,7 @@ void Model::backward_replica(std::vector<Rank*>& grp, bool accumulate) {
     auto cons = [&](Rank& R, int64_t r0, int64_t rows) {
       tic();
       k::layernorm_bwd(R.hs[L_] + r0 * d, R.statsf + r0, R.statsf + M + r0, P(R, lnf_s_), R.dx + r0 * d,
-                       R.gres + r0 * d, R.gb + r0 * d, G(R, lnf_s_), G(R, lnf_b_), rows, d, 0, stream_);
+                       R.gres + r0 * d, R.gb + r0 * d, G(R, lnf_s_), G(R, lnf_b_), rows, d, 0, stream_, R.ln_partials);
       toc(kProfNorm, 18.0 * rows * d);
       ++launches_;
     };
@@ -816,7 +882,7 @@ void Model::backward_replica(std::vector<Rank*>& grp, bool accumulate) {
       auto cons = [&](Rank& R, int64_t r0, int64_t rows) {
         tic();
         k::layernorm_bwd(R.hmid[l] + r0 * d, R.stats2[l] + r0, R.stats2[l] + M + r0, P(R, ls.ln2_s), R.dx + r0 * d,
-                         R.gres + r0 * d, R.gb + r0 * d, G(R, ls.ln2_s), G(R, ls.ln2_b), rows, d, 1, stream_);
+                         R.gres + r0 * d, R.gb + r0 * d, G(R, ls.ln2_s), G(R, ls.ln2_b), rows, d, 1, stream_, R.ln_partials);
         toc(kProfNorm, 18.0 * rows * d);
         ++launches_;
       };
@@ -852,7 +918,7 @@ void Model::backward_replica(std::vector<Rank*>& grp, bool accumulate) {
       auto cons = [&](Rank& R, int64_t r0, int64_t rows) {
         tic();
         k::layernorm_bwd(R.hs[l] + r0 * d, R.stats1[l] + r0, R.stats1[l] + M + r0, P(R, ls.ln1_s), R.dx + r0 * d,
-                         R.gres + r0 * d, R.gb + r0 * d, G(R, ls.ln1_s), G(R, ls.ln1_b), rows, d, 1, stream_);
+                         R.gres + r0 * d, R.gb + r0 * d, G(R, ls.ln1_s), G(R, ls.ln1_b), rows, d, 1, stream_, R.ln_partials);
         toc(kProfNorm, 18.0 * rows * d);
         ++launches_;
       };
@@ -867,7 +933,7 @@ void Model::backward_replica(std::vector<Rank*>& grp, bool accumulate) {
   }
   for (Rank* R : grp) {
     k::embed_bwd_pos(R->gres, G(*R, pos_), B_, T_, d, acc, stream_);
-    k::embed_bwd_tok(R->tokens, R->gres, G(*R, tok_), M, d, stream_);
+    k::embed_bwd_tok(R->tokens, R->gres, G(*R, tok_), M, d, spec_.vocab_size, R->tok_keys, stream_);
     launches_ += 2;
   }
   // column-parallel biases are replicated parameters: gather their gradient chunks

@@ -20,6 +20,7 @@
 #include <unordered_map>
 #include <vector>
 
+#include "checkpoint.h"
 #include "mesh.h"
 #include "rules.h"
 
@@ -61,6 +62,8 @@ struct Rank {
   double* loss = nullptr;
   // scratch
   float *part = nullptr, *dx = nullptr, *gres = nullptr, *col_scratch = nullptr, *attn_scratch = nullptr;
+  float* ln_partials = nullptr;  // per-CTA LayerNorm parameter-gradient partials (deterministic reduction)
+  uint32_t* tok_keys = nullptr;  // sorted (token, position) keys of the embedding backward
   // vocab-parallel cross entropy: per-rank (max, sumexp) of every mp rank, target logit, lse
   float *xstats = nullptr, *xt = nullptr, *xlse = nullptr;
   bf16 *gb = nullptr, *dpre = nullptr, *dout = nullptr, *dqkv = nullptr;
@@ -88,6 +91,15 @@ class Model {
 
   void init_params(uint64_t seed, const std::string& stream_name);
   void set_param(const std::string& name, const float* full, int64_t numel);
+  // which: 0 param (+ bf16 shadow), 2 adam_m, 3 adam_v
+  void set_tensor(const std::string& name, int which, const float* full, int64_t numel);
+  // SWCK snapshots (checkpoint.hpp:193-298): replica 0's gathered p / m / v in tree order;
+  // load re-cuts them onto this model's plan and mesh.
+  void save_checkpoint(const std::string& path, const std::vector<CkptRng>& rngs);
+  void load_checkpoint(const std::string& path);
+  const std::vector<CkptRng>& loaded_rngs() const { return loaded_rngs_; }
+  uint64_t step() const { return step_; }
+  uint64_t seed() const { return seed_; }
   void get_tensor(const std::string& name, int which, float* full, int64_t numel);
   void stage_batch(const int32_t* tokens, const int32_t* targets, const float* weights);
   void forward_backward(bool accumulate);
@@ -172,6 +184,8 @@ class Model {
   std::vector<std::pair<int, double>> prof_rec_;
   int64_t bytes_ = 0;
   uint64_t step_ = 0;
+  uint64_t seed_ = 0;
+  std::vector<CkptRng> loaded_rngs_;
 };
 
 }  // namespace sw

@@ -52,13 +52,20 @@ def _declare():
     L.sw_model_set_profiling.argtypes = [vp, C.c_int]
     L.sw_model_read_profile.argtypes = [vp, C.POINTER(C.c_double), C.POINTER(C.c_double),
                                         C.POINTER(C.c_int64)]
+    u64p = C.POINTER(C.c_uint64)
+    L.sw_model_save_checkpoint.argtypes = [vp, C.c_char_p, C.c_uint32, C.POINTER(C.c_char_p), u64p, u64p, u64p]
+    L.sw_model_load_checkpoint.argtypes = [vp, C.c_char_p, C.POINTER(C.c_uint32)]
+    L.sw_model_checkpoint_rng.argtypes = [vp, C.c_uint32, C.c_char_p, C.c_uint64, u64p, u64p, u64p]
+    L.sw_model_state_info.argtypes = [vp, u64p, u64p]
     for fn in ("sw_nccl_unique_id", "sw_mesh_create", "sw_mesh_comm_report",
                "sw_mesh_reset_comm_report", "sw_model_create", "sw_model_init_params",
                "sw_model_set_param", "sw_model_get_tensor", "sw_model_stage_batch",
                "sw_model_forward_backward", "sw_model_scale_grads", "sw_model_dp_sync",
                "sw_model_adamw_step", "sw_model_train_step", "sw_model_last_loss",
                "sw_model_forward_logits", "sw_model_stream", "sw_model_launch_count",
-               "sw_model_device_bytes", "sw_model_set_profiling", "sw_model_read_profile"):
+               "sw_model_device_bytes", "sw_model_set_profiling", "sw_model_read_profile",
+               "sw_model_save_checkpoint", "sw_model_load_checkpoint", "sw_model_checkpoint_rng",
+               "sw_model_state_info"):
         getattr(L, fn).restype = C.c_int
     L._engine_declared = True
     return L
@@ -235,3 +242,35 @@ class Model:
         x = C.c_int64()
         _lib.check(_declare().sw_model_device_bytes(self._h, C.byref(x)))
         return x.value
+
+    # -- SWCK snapshots (checkpoint.hpp:193-298) ------------------------------------------------
+    def save_checkpoint(self, path: str, rngs=()):
+        """save_checkpoint(path, state, mesh, rngs): rngs is a sequence of
+        (name, seed, stream_id, counter). Under NCCL every rank calls it; rank 0 writes."""
+        rngs = list(rngs)
+        n = len(rngs)
+        names = (C.c_char_p * max(n, 1))(*[r[0].encode() for r in rngs])
+        seeds = (C.c_uint64 * max(n, 1))(*[r[1] for r in rngs])
+        ids = (C.c_uint64 * max(n, 1))(*[r[2] for r in rngs])
+        ctrs = (C.c_uint64 * max(n, 1))(*[r[3] for r in rngs])
+        _lib.check(_declare().sw_model_save_checkpoint(self._h, path.encode(), n, names, seeds, ids, ctrs))
+
+    def load_checkpoint(self, path: str):
+        """load_checkpoint re-cut onto this model's plan and mesh; returns the stored RNG streams
+        as [(name, seed, stream_id, counter)]."""
+        L = _declare()
+        n = C.c_uint32()
+        _lib.check(L.sw_model_load_checkpoint(self._h, path.encode(), C.byref(n)))
+        out = []
+        for i in range(n.value):
+            buf = C.create_string_buffer(4096)
+            s, sid, c = C.c_uint64(), C.c_uint64(), C.c_uint64()
+            _lib.check(L.sw_model_checkpoint_rng(self._h, i, buf, 4096, C.byref(s), C.byref(sid), C.byref(c)))
+            out.append((buf.value.decode(), s.value, sid.value, c.value))
+        return out
+
+    def state_info(self):
+        """(optimizer step, state seed) of the TrainState (train_state.hpp:24-27)."""
+        step, seed = C.c_uint64(), C.c_uint64()
+        _lib.check(_declare().sw_model_state_info(self._h, C.byref(step), C.byref(seed)))
+        return step.value, seed.value

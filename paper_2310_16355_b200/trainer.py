@@ -32,6 +32,14 @@ def scheduled_lr(step: int, total_steps: int, warmup_steps: int, peak: float) ->
     return peak * float(total_steps - step) / float(total_steps - warmup_steps)
 
 
+def stream_id(name: str) -> int:
+    """RngStream's named-stream id (FNV-1a 64 of the name, rng.hpp)."""
+    h = 0xCBF29CE484222325
+    for c in name.encode():
+        h = ((h ^ c) * 0x100000001B3) & 0xFFFFFFFFFFFFFFFF
+    return h
+
+
 def permutation(seed: int, stream: str, child: int, n: int) -> np.ndarray:
     L = _lib.lib()
     L.sw_rng_permutation.argtypes = [C.c_uint64, C.c_char_p, C.c_int64, C.c_uint64, C.c_void_p]
@@ -74,6 +82,7 @@ class Trainer:
         self.model = engine.Model(spec, self.plan, mesh, config.per_device_batch_size, seq_len)
         self.model.init_params(seed, init_stream)
         os.makedirs(workdir, exist_ok=True)
+        self.workdir = workdir
         self.log_path = os.path.join(workdir, "run.log")
         self._log = open(self.log_path, "w")
         self.step = 0
@@ -92,7 +101,16 @@ class Trainer:
                                None if w is None else np.asarray(w, np.float32))
         return rows
 
-    def fit(self, train_examples):
+    def load(self, checkpoint_path: str):
+        """Trainer::load (pipeline.hpp:338-345): restore a snapshot saved by this configuration;
+        fit() then resumes at the epoch the optimizer step implies."""
+        self.model.load_checkpoint(checkpoint_path)
+        self.step = self.model.state_info()[0]
+
+    def fit(self, train_examples, stop_after_epoch: int = -1):
+        """Epochs up to n_epochs (absolute, so a loaded checkpoint resumes where it left off);
+        stop_after_epoch pauses earlier with the LR schedule still spanning n_epochs. Every
+        finished epoch writes <workdir>/last.ckpt (pipeline.hpp:536-539)."""
         cfg = self.config
         if cfg.n_epochs < 1:
             raise ConfigError(3, f"Trainer: n_epochs must be positive, got {cfg.n_epochs}")
@@ -109,7 +127,9 @@ class Trainer:
         warmup_steps = int(cfg.warmup_rate * total_steps)
         losses, lrs = [], []
         first_epoch = self.step // steps_per_epoch
-        for epoch in range(first_epoch, cfg.n_epochs):
+        last_epoch = cfg.n_epochs if stop_after_epoch < 0 else min(stop_after_epoch, cfg.n_epochs)
+        self.checkpoints = []
+        for epoch in range(first_epoch, last_epoch):
             perm = permutation(self.seed, "data-shuffle", epoch, len(train_examples))
             for s in range(steps_per_epoch):
                 lr = scheduled_lr(self.step, total_steps, warmup_steps, cfg.optimizer.lr)
@@ -142,4 +162,7 @@ class Trainer:
                 losses.append(loss)
                 lrs.append(lr)
                 self.step += 1
+            last = os.path.join(self.workdir, "last.ckpt")
+            self.model.save_checkpoint(last, [("train", self.seed, stream_id("train"), 0)])
+            self.checkpoints.append(last)
         return losses, lrs

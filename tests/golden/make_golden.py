@@ -295,6 +295,72 @@ def gen_trainer(tmp):
     print("trainer.json:", {k: len(v["losses"]) for k, v in out.items()})
 
 
+CKPT_CASES = {
+    # name -> how the test derives the file from the golden snapshot
+    "cut1000": "first 1000 bytes",
+    "cut61": "first 61 bytes (header + RNG block, no records)",
+    "empty": "empty file",
+    "magic": "b'NOPE' + 64 zero bytes",
+    "version": "byte 4 set to 0xEE",
+    "dtype": "byte 88 (dtype of the first record) set to 1",
+    "rank": "byte 89..92 (rank of the first record) set to 99",
+    "order": "the first params/ record renamed to adam_x/ (same length)",
+}
+
+
+def ckpt_transform(name, raw):
+    if name == "cut1000":
+        return raw[:1000]
+    if name == "cut61":
+        return raw[:61]
+    if name == "empty":
+        return b""
+    if name == "magic":
+        return b"NOPE" + bytes(64)
+    b = bytearray(raw)
+    if name == "version":
+        b[4] = 0xEE
+    elif name == "dtype":
+        b[88] = 1
+    elif name == "rank":
+        b[89:93] = (99).to_bytes(4, "little")
+    elif name == "order":
+        i = raw.index(b"params/embed/tok/kernel")
+        b[i:i + 7] = b"adam_x/"
+    return bytes(b)
+
+
+def gen_checkpoint(tmp):
+    """SWCK golden: the reference's save_checkpoint of the mini decoder after 3 sharded AdamW
+    steps (f32, dp=1, mp=2, seed 42, "train" stream advanced 17 draws), plus the reference's
+    load_checkpoint verdict on it and on corrupted copies (checkpoint.hpp:233-298)."""
+    d = tempfile.mkdtemp(dir=tmp)
+    path = os.path.join(HERE, "mini_f32_mp2_step3.swck")
+    env = dict(os.environ, SW_REF_CKPT=path)
+    subprocess.run([DRIVER, "golden", os.path.join(SPECS, "mini.spec"), "f32", "42", "1", "2", "2", "16", "3",
+                    "0.01", "0.01", d], check=True, env=env, stdout=subprocess.DEVNULL)
+    raw = open(path, "rb").read()
+
+    def verdict(fpath, mp=2, dtype="f32"):
+        r = subprocess.run([DRIVER, "ckload", os.path.join(SPECS, "mini.spec"), dtype, str(mp), fpath],
+                           capture_output=True, text=True, check=True)
+        return r.stdout.strip()
+
+    cases = {}
+    for name, how in CKPT_CASES.items():
+        f = os.path.join(tmp, name + ".swck")
+        open(f, "wb").write(ckpt_transform(name, raw))
+        cases[name] = dict(transform=how, message=verdict(f))
+    out = dict(file=os.path.basename(path), spec="mini.spec", seed=42, dp=1, mp=2, global_batch=2, seq=16,
+               steps=3, lr=0.01, weight_decay=0.01, size=len(raw),
+               rngs=[dict(name="train", note="RngStream(42, 'train') after 17 next_u64()")],
+               ok={str(mp): verdict(path, mp) for mp in (1, 2, 4)},
+               f64_load=verdict(path, 2, "f64"), cases=cases)
+    with open(os.path.join(HERE, "checkpoint.json"), "w") as f:
+        json.dump(out, f, indent=1)
+    print("checkpoint.json:", out["ok"], {k: v["message"][:40] for k, v in cases.items()})
+
+
 def main():
     build()
     with tempfile.TemporaryDirectory() as tmp:
@@ -304,7 +370,13 @@ def main():
         gen_numeric(tmp, "mini_f64_dp2_mp2", "mini.spec", "f64", 2, 2, 4, 16, 2, 1e-2, 0.01, False)
         gen_numeric(tmp, "mini_f32_dp1_mp4", "mini.spec", "f32", 1, 4, 2, 16, 2, 1e-2, 0.01, False)
         gen_numeric(tmp, "tiny_f64_dp1_mp2", "tiny.spec", "f64", 1, 2, 4, 128, 1, 1e-3, 0.01, False)
+        gen_checkpoint(tmp)
 
 
 if __name__ == "__main__":
-    sys.exit(main())
+    if sys.argv[1:] == ["checkpoint"]:
+        build()
+        with tempfile.TemporaryDirectory() as tmp:
+            gen_checkpoint(tmp)
+    else:
+        sys.exit(main())

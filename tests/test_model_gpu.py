@@ -301,3 +301,24 @@ def test_fused_optimizer_nonfinite_raises():
     model.stage_batch(tokens, targets, weights)
     with pytest.raises(engine._lib.NonFiniteError, match="non-finite gradient"):
         model.train_step(engine.AdamWConfig())
+
+
+def test_replicated_param_grads_are_deterministic():
+    """Embedding and LayerNorm gradients (replicated on every tensor-parallel rank, like the
+    reference's) come from fixed-order reductions (sorted token runs, per-CTA LayerNorm partials
+    summed in CTA order), so two backward passes over the same batch agree bit for bit -- which
+    is what keeps the replicas identical across ranks."""
+    spec = spec_of("tiny.spec")
+    model, mesh, _ = make(spec, 1, 2, 4, 128)
+    model.init_params(42, "model-init")
+    tokens, targets, weights = rng_ref.audit_batch(42, 0, 4, 128, spec.vocab_size)
+    # repeated tokens exercise multi-position runs in the embedding backward
+    tokens[:, ::3] = tokens[0, 0]
+    model.stage_batch(tokens, targets, weights)
+    names = [n for n in model.shapes if n.startswith("embed/") or "/ln" in n or n.startswith("final_ln/")]
+    runs = []
+    for _ in range(2):
+        model.forward_backward()
+        runs.append({n: model.get_grad(n).view(np.uint32).copy() for n in names})
+    for n in names:
+        assert np.array_equal(runs[0][n], runs[1][n]), n

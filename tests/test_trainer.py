@@ -58,3 +58,33 @@ def test_trainer_trajectory_matches_reference(name, tmp_path):
     log = open(tr.log_path).read().splitlines()
     assert [ln.split(" loss=")[0] for ln in log] == [ln.split(" loss=")[0] for ln in c["log"].splitlines()]
     assert [ln.split(" lr=")[1] for ln in log] == [ln.split(" lr=")[1] for ln in c["log"].splitlines()]
+
+
+@pytest.mark.gpu
+def test_trainer_resume_from_last_checkpoint(tmp_path):
+    """Trainer::load + fit resumes at the epoch the saved step implies and continues the same
+    trajectory (tests/test_pipeline.cpp:292-316): an interrupted 2-epoch run (stop after epoch 1,
+    reload last.ckpt into a new Trainer) logs the uninterrupted run's epoch-2 steps."""
+    c = GOLD[sorted(GOLD)[0]]
+    spec = rules.read_model_spec(os.path.join(ROOT, "oracle", "specs", c["spec"]))
+
+    def new_trainer(workdir):
+        cfg = trainer.RunConfig(n_epochs=2, per_device_batch_size=c["per_device_batch_size"],
+                                accumulate_grad_batches=1,
+                                optimizer=engine.AdamWConfig(lr=c["lr"], weight_decay=c["weight_decay"]),
+                                warmup_rate=c["warmup_rate"])
+        return trainer.Trainer(spec, engine.Mesh(c["dp"], c["mp"]), c["seq"], collate, cfg, seed=c["seed"],
+                               workdir=str(workdir))
+
+    ex = examples_for(c, spec.vocab_size)
+    full = new_trainer(tmp_path / "full")
+    losses, lrs = full.fit(ex)
+    first = new_trainer(tmp_path / "a")
+    l1, _ = first.fit(ex, stop_after_epoch=1)
+    assert first.checkpoints == [str(tmp_path / "a" / "last.ckpt")]
+    second = new_trainer(tmp_path / "b")
+    second.load(first.checkpoints[-1])
+    assert second.step == len(l1)
+    l2, lr2 = second.fit(ex)
+    assert lr2 == lrs[len(l1):]
+    np.testing.assert_allclose(l1 + l2, losses, rtol=1e-4)
