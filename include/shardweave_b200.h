@@ -66,6 +66,9 @@ SW_API sw_status sw_model_spec_parse(const char* text, sw_model_spec** out);
 SW_API sw_status sw_model_spec_dims(const sw_model_spec* spec, int64_t out[7]);
 /* Role overrides of the spec as "pattern\trole\n" lines. */
 SW_API sw_status sw_model_spec_overrides(const sw_model_spec* spec, char** text_out);
+/* Extension keys (not in the reference's spec language): mlp = gelu|swiglu,
+ * norm = layernorm|rmsnorm. */
+SW_API sw_status sw_model_spec_variant(const sw_model_spec* spec, int* swiglu, int* rmsnorm);
 SW_API void sw_model_spec_free(sw_model_spec* spec);
 
 /* Replaces transformer_param_shapes (model.hpp:17-43): "name\td0,d1\n" in tree order. */

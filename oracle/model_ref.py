@@ -9,6 +9,9 @@
             cross entropy :230-238, embedding scatter-add kernels.hpp:291-304)
   optimizer adamw_step train_state.hpp:183-220 (c1, c2 in double; decay on every parameter)
   audit     audit_equivalence's single-device trajectory audit.hpp:78-159
+  extension mlp = swiglu / norm = rmsnorm: RMSNorm and SiLU written as the
+            reference-op identities slice(layer_norm(concat(x,-x)))*g and x*softmax([x,0])[0];
+            tests/test_oracle.py checks the closed forms here against those compositions.
 """
 from __future__ import annotations
 
@@ -43,6 +46,30 @@ def layer_norm_bwd(xhat, rstd, s, dy):
     return dx, (dy * xhat).reshape(-1, dy.shape[-1]).sum(0), dy.reshape(-1, dy.shape[-1]).sum(0)
 
 
+def rms_norm(x, s, eps=EPS_LN):
+    """Extension: slice(layer_norm(concat(x, -x)), d) * s: the concatenation has
+    zero mean and variance mean(x^2), so xhat = x / sqrt(mean(x^2) + eps)."""
+    r = 1.0 / np.sqrt((x * x).mean(-1, keepdims=True) + eps)
+    xhat = x * r
+    return xhat * s, xhat, r
+
+
+def rms_norm_bwd(xhat, rstd, s, dy):
+    g = dy * s
+    dx = rstd * (g - xhat * (g * xhat).mean(-1, keepdims=True))
+    return dx, (dy * xhat).reshape(-1, dy.shape[-1]).sum(0)
+
+
+def silu(x):
+    """Extension: x * softmax([x, 0])[0] = x * sigmoid(x)."""
+    return x / (1.0 + np.exp(-x))
+
+
+def silu_grad(x):
+    sg = 1.0 / (1.0 + np.exp(-x))
+    return sg * (1.0 + x * (1.0 - sg))
+
+
 def _softmax(x):
     m = x.max(-1, keepdims=True)
     e = np.exp(x - m)
@@ -66,6 +93,22 @@ def forward_backward(params: dict, spec: dict, tokens, targets, weights, need_gr
     backward's dlogits / residual-gradient / dpre / d(attn out) / dqkv), so a bf16 device run
     can be checked at a tolerance set by accumulation order rather than storage rounding."""
     R = bf16_round if bf16_acts else (lambda x: x)
+    swiglu = spec.get("mlp", "gelu") == "swiglu"
+    rms = spec.get("norm", "layernorm") == "rmsnorm"
+
+    def norm(x, prefix):
+        if rms:
+            y, xh, r = rms_norm(x, p[prefix + "/scale"])
+            return y, xh, r
+        return layer_norm(x, p[prefix + "/scale"], p[prefix + "/bias"])
+
+    def norm_bwd(xh, r, prefix, dy, grads):
+        if rms:
+            dx, grads[prefix + "/scale"] = rms_norm_bwd(xh, r, p[prefix + "/scale"], dy)
+        else:
+            dx, grads[prefix + "/scale"], grads[prefix + "/bias"] = layer_norm_bwd(xh, r, p[prefix + "/scale"], dy)
+        return dx
+
     B, T = tokens.shape
     d, H, L = spec["d_model"], spec["n_heads"], spec["n_layers"]
     hd = d // H
@@ -76,7 +119,7 @@ def forward_backward(params: dict, spec: dict, tokens, targets, weights, need_gr
     cache = []
     for l in range(L):
         pre = f"block_{l}/"
-        a, xh1, r1 = layer_norm(h, p[pre + "ln1/scale"], p[pre + "ln1/bias"])
+        a, xh1, r1 = norm(h, pre + "ln1")
         a = R(a)
 
         def proj(name):
@@ -89,15 +132,22 @@ def forward_backward(params: dict, spec: dict, tokens, targets, weights, need_gr
         att = P @ v
         merged = R(att.transpose(0, 2, 1, 3).reshape(B, T, d))
         h_mid = h + merged @ p[pre + "attn/o/kernel"].T + p[pre + "attn/o/bias"]
-        m, xh2, r2 = layer_norm(h_mid, p[pre + "ln2/scale"], p[pre + "ln2/bias"])
+        m, xh2, r2 = norm(h_mid, pre + "ln2")
         m = R(m)
-        up_full = m @ p[pre + "mlp/fc1/kernel"].T + p[pre + "mlp/fc1/bias"]
-        g = R(gelu(up_full))
-        up = R(up_full)
-        h_out = h_mid + g @ p[pre + "mlp/fc2/kernel"].T + p[pre + "mlp/fc2/bias"]
+        if swiglu:
+            gate = m @ p[pre + "mlp/fc1/gate/kernel"].T
+            upv = m @ p[pre + "mlp/fc1/kernel"].T
+            g = R(silu(gate) * upv)           # h = silu(gate x) * (up x)
+            up = (R(gate), R(upv))
+            h_out = h_mid + g @ p[pre + "mlp/fc2/kernel"].T
+        else:
+            up_full = m @ p[pre + "mlp/fc1/kernel"].T + p[pre + "mlp/fc1/bias"]
+            g = R(gelu(up_full))
+            up = R(up_full)
+            h_out = h_mid + g @ p[pre + "mlp/fc2/kernel"].T + p[pre + "mlp/fc2/bias"]
         cache.append((a, xh1, r1, q, k, v, P, merged, m, xh2, r2, up, g))
         h = h_out
-    f, xhf, rf = layer_norm(h, p["final_ln/scale"], p["final_ln/bias"])
+    f, xhf, rf = norm(h, "final_ln")
     f = R(f)
     W_head = p["embed/tok/kernel"] if tied else p["lm_head/kernel"]
     if bf16_acts:
@@ -120,18 +170,27 @@ def forward_backward(params: dict, spec: dict, tokens, targets, weights, need_gr
     V = logits.shape[-1]
     dW_head = dlogits.reshape(-1, V).T @ f.reshape(-1, d)
     df = dlogits @ W_head
-    dh, grads["final_ln/scale"], grads["final_ln/bias"] = layer_norm_bwd(xhf, rf, p["final_ln/scale"], df)
+    dh = norm_bwd(xhf, rf, "final_ln", df, grads)
     for l in reversed(range(L)):
         pre = f"block_{l}/"
         a, xh1, r1, q, k, v, P, merged, m, xh2, r2, up, g = cache[l]
         dflat = R(dh.reshape(-1, d))
         grads[pre + "mlp/fc2/kernel"] = dflat.T @ g.reshape(-1, g.shape[-1])
-        grads[pre + "mlp/fc2/bias"] = dh.reshape(-1, d).sum(0)
-        dup = R((dflat.reshape(dh.shape) @ p[pre + "mlp/fc2/kernel"]) * gelu_grad(up))
-        grads[pre + "mlp/fc1/kernel"] = dup.reshape(-1, dup.shape[-1]).T @ m.reshape(-1, d)
-        grads[pre + "mlp/fc1/bias"] = dup.reshape(-1, dup.shape[-1]).sum(0)
-        dm = dup @ p[pre + "mlp/fc1/kernel"]
-        dx, grads[pre + "ln2/scale"], grads[pre + "ln2/bias"] = layer_norm_bwd(xh2, r2, p[pre + "ln2/scale"], dm)
+        dhid = dflat.reshape(dh.shape) @ p[pre + "mlp/fc2/kernel"]
+        if swiglu:
+            gate, upv = up
+            dgate = R(dhid * upv * silu_grad(gate))
+            dupv = R(dhid * silu(gate))
+            grads[pre + "mlp/fc1/gate/kernel"] = dgate.reshape(-1, dgate.shape[-1]).T @ m.reshape(-1, d)
+            grads[pre + "mlp/fc1/kernel"] = dupv.reshape(-1, dupv.shape[-1]).T @ m.reshape(-1, d)
+            dm = dgate @ p[pre + "mlp/fc1/gate/kernel"] + dupv @ p[pre + "mlp/fc1/kernel"]
+        else:
+            grads[pre + "mlp/fc2/bias"] = dh.reshape(-1, d).sum(0)
+            dup = R(dhid * gelu_grad(up))
+            grads[pre + "mlp/fc1/kernel"] = dup.reshape(-1, dup.shape[-1]).T @ m.reshape(-1, d)
+            grads[pre + "mlp/fc1/bias"] = dup.reshape(-1, dup.shape[-1]).sum(0)
+            dm = dup @ p[pre + "mlp/fc1/kernel"]
+        dx = norm_bwd(xh2, r2, pre + "ln2", dm, grads)
         dh = dh + dx
         dflat = R(dh.reshape(-1, d))
         grads[pre + "attn/o/kernel"] = dflat.T @ merged.reshape(-1, d)
@@ -152,7 +211,7 @@ def forward_backward(params: dict, spec: dict, tokens, targets, weights, need_gr
             grads[pre + f"attn/{name}/kernel"] = dyf.T @ a.reshape(-1, d)
             grads[pre + f"attn/{name}/bias"] = dyf.sum(0)
             da += (dyf @ p[pre + f"attn/{name}/kernel"]).reshape(B, T, d)
-        dx, grads[pre + "ln1/scale"], grads[pre + "ln1/bias"] = layer_norm_bwd(xh1, r1, p[pre + "ln1/scale"], da)
+        dx = norm_bwd(xh1, r1, pre + "ln1", da, grads)
         dh = dh + dx
     dtok = np.zeros_like(p["embed/tok/kernel"])
     np.add.at(dtok, tokens.reshape(-1), dh.reshape(-1, d))

@@ -94,18 +94,28 @@ def normals_exact(rng: RngStream, n: int) -> np.ndarray:
 
 
 def transformer_param_shapes(spec: dict):
-    """model.hpp:17-43 (tree order)."""
+    """model.hpp:17-43 (tree order); mlp = swiglu / norm = rmsnorm extension leaves."""
     d, V = spec["d_model"], spec["vocab_size"]
+    rms = spec.get("norm", "layernorm") == "rmsnorm"
+    swiglu = spec.get("mlp", "gelu") == "swiglu"
+
+    def norm(p):
+        return [(p + "/scale", (d,))] + ([] if rms else [(p + "/bias", (d,))])
+
     out = [("embed/tok/kernel", (V, d)), ("embed/pos/kernel", (spec["max_seq_len"], d))]
     for l in range(spec["n_layers"]):
         b = f"block_{l}/"
-        out += [(b + "ln1/scale", (d,)), (b + "ln1/bias", (d,))]
+        out += norm(b + "ln1")
         for p in "qkvo":
             out += [(b + f"attn/{p}/kernel", (d, d)), (b + f"attn/{p}/bias", (d,))]
-        out += [(b + "ln2/scale", (d,)), (b + "ln2/bias", (d,)),
-                (b + "mlp/fc1/kernel", (spec["d_ff"], d)), (b + "mlp/fc1/bias", (spec["d_ff"],)),
-                (b + "mlp/fc2/kernel", (d, spec["d_ff"])), (b + "mlp/fc2/bias", (d,))]
-    out += [("final_ln/scale", (d,)), ("final_ln/bias", (d,))]
+        out += norm(b + "ln2")
+        if swiglu:
+            out += [(b + "mlp/fc1/gate/kernel", (spec["d_ff"], d)), (b + "mlp/fc1/kernel", (spec["d_ff"], d)),
+                    (b + "mlp/fc2/kernel", (d, spec["d_ff"]))]
+        else:
+            out += [(b + "mlp/fc1/kernel", (spec["d_ff"], d)), (b + "mlp/fc1/bias", (spec["d_ff"],)),
+                    (b + "mlp/fc2/kernel", (d, spec["d_ff"])), (b + "mlp/fc2/bias", (d,))]
+    out += norm("final_ln")
     if not spec.get("tie_embeddings", False):
         out.append(("lm_head/kernel", (V, d)))
     return out

@@ -80,6 +80,14 @@ sw_status sw_model_spec_dims(const sw_model_spec* spec, int64_t out[7]) {
   });
 }
 
+sw_status sw_model_spec_variant(const sw_model_spec* spec, int* swiglu, int* rmsnorm) {
+  return sw::guarded([&] {
+    require(spec, "spec");
+    if (swiglu) *swiglu = spec->spec.swiglu ? 1 : 0;
+    if (rmsnorm) *rmsnorm = spec->spec.rmsnorm ? 1 : 0;
+  });
+}
+
 sw_status sw_model_spec_overrides(const sw_model_spec* spec, char** text_out) {
   return sw::guarded([&] {
     require(spec, "spec");

@@ -451,6 +451,22 @@ ModelSpec parse_model_spec(const std::string& text) {
       } else {
         fail(SW_ERR_CONFIG, where + quote(key) + " needs true or false, got " + quote(value));
       }
+    } else if (key == "mlp") {  // extension key
+      if (value == "gelu") {
+        spec.swiglu = false;
+      } else if (value == "swiglu") {
+        spec.swiglu = true;
+      } else {
+        fail(SW_ERR_CONFIG, where + quote(key) + " needs gelu or swiglu, got " + quote(value));
+      }
+    } else if (key == "norm") {  // extension key
+      if (value == "layernorm") {
+        spec.rmsnorm = false;
+      } else if (value == "rmsnorm") {
+        spec.rmsnorm = true;
+      } else {
+        fail(SW_ERR_CONFIG, where + quote(key) + " needs layernorm or rmsnorm, got " + quote(value));
+      }
     } else {
       fail(SW_ERR_CONFIG, where + "unknown key " + quote(key));
     }
@@ -472,27 +488,35 @@ ModelSpec parse_model_spec(const std::string& text) {
 }
 
 std::vector<NamedShape> transformer_param_shapes(const ModelSpec& spec) {
+  // model.hpp:17-43 tree order; the mlp/norm extension keys swap in the SwiGLU / RMSNorm leaves
   const int64_t d = spec.d_model;
   std::vector<NamedShape> out;
+  auto norm = [&](const std::string& p) {
+    out.push_back({p + "/scale", {d}});
+    if (!spec.rmsnorm) out.push_back({p + "/bias", {d}});
+  };
   out.push_back({"embed/tok/kernel", {spec.vocab_size, d}});
   out.push_back({"embed/pos/kernel", {spec.max_seq_len, d}});
   for (int l = 0; l < spec.n_layers; ++l) {
     const std::string b = "block_" + std::to_string(l) + "/";
-    out.push_back({b + "ln1/scale", {d}});
-    out.push_back({b + "ln1/bias", {d}});
+    norm(b + "ln1");
     for (const char* proj : {"q", "k", "v", "o"}) {
       out.push_back({b + "attn/" + proj + "/kernel", {d, d}});
       out.push_back({b + "attn/" + proj + "/bias", {d}});
     }
-    out.push_back({b + "ln2/scale", {d}});
-    out.push_back({b + "ln2/bias", {d}});
-    out.push_back({b + "mlp/fc1/kernel", {spec.d_ff, d}});
-    out.push_back({b + "mlp/fc1/bias", {spec.d_ff}});
-    out.push_back({b + "mlp/fc2/kernel", {d, spec.d_ff}});
-    out.push_back({b + "mlp/fc2/bias", {d}});
+    norm(b + "ln2");
+    if (spec.swiglu) {
+      out.push_back({b + "mlp/fc1/gate/kernel", {spec.d_ff, d}});
+      out.push_back({b + "mlp/fc1/kernel", {spec.d_ff, d}});
+      out.push_back({b + "mlp/fc2/kernel", {d, spec.d_ff}});
+    } else {
+      out.push_back({b + "mlp/fc1/kernel", {spec.d_ff, d}});
+      out.push_back({b + "mlp/fc1/bias", {spec.d_ff}});
+      out.push_back({b + "mlp/fc2/kernel", {d, spec.d_ff}});
+      out.push_back({b + "mlp/fc2/bias", {d}});
+    }
   }
-  out.push_back({"final_ln/scale", {d}});
-  out.push_back({"final_ln/bias", {d}});
+  norm("final_ln");
   if (!spec.tie_embeddings) out.push_back({"lm_head/kernel", {spec.vocab_size, d}});
   return out;
 }

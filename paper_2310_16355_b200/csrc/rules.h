@@ -79,6 +79,12 @@ struct ModelSpec {
   int64_t d_ff = 0;
   int64_t max_seq_len = 0;
   bool tie_embeddings = false;
+  // Extension (not in the reference's spec language): `mlp = swiglu` gives the
+  // LLaMA MLP down(silu(gate x) * up x) with gate named block_i/mlp/fc1/gate/kernel (gate:0,
+  // up:0, down:1 under the reference rules, no MLP biases); `norm = rmsnorm` makes every
+  // LayerNorm an RMSNorm (scale only).
+  bool swiglu = false;
+  bool rmsnorm = false;
   std::vector<RoleOverride> overrides;
 };
 

@@ -29,6 +29,8 @@ def _declare():
     L.sw_model_spec_parse.argtypes = [cp, C.POINTER(vp)]
     L.sw_model_spec_dims.argtypes = [vp, C.POINTER(C.c_int64)]
     L.sw_model_spec_overrides.argtypes = [vp, out_str]
+    L.sw_model_spec_variant.argtypes = [vp, C.POINTER(C.c_int), C.POINTER(C.c_int)]
+    L.sw_model_spec_variant.restype = C.c_int
     L.sw_model_spec_free.argtypes = [vp]
     L.sw_model_spec_free.restype = None
     L.sw_transformer_param_shapes.argtypes = [vp, out_str]
@@ -87,6 +89,8 @@ class ModelSpec:
     max_seq_len: int
     tie_embeddings: bool = False
     overrides: list = field(default_factory=list)  # [(pattern, role_name)]
+    mlp: str = "gelu"          # extension key: gelu | swiglu
+    norm: str = "layernorm"    # extension key: layernorm | rmsnorm
     _handle: object = field(default=None, repr=False, compare=False)
 
     def __del__(self):
@@ -103,6 +107,10 @@ class ModelSpec:
                  f"d_model = {self.d_model}", f"n_heads = {self.n_heads}", f"d_ff = {self.d_ff}",
                  f"max_seq_len = {self.max_seq_len}",
                  f"tie_embeddings = {'true' if self.tie_embeddings else 'false'}"]
+        if self.mlp != "gelu":
+            lines.append(f"mlp = {self.mlp}")
+        if self.norm != "layernorm":
+            lines.append(f"norm = {self.norm}")
         lines += [f"role {p} = {r}" for p, r in self.overrides]
         return "\n".join(lines) + "\n"
 
@@ -116,8 +124,11 @@ def parse_model_spec(text: str) -> ModelSpec:
     s = C.c_void_p()
     _lib.check(L.sw_model_spec_overrides(h, C.byref(s)))
     ovr = [tuple(ln.split("\t")) for ln in _take(s).splitlines() if ln]
+    sg, rn = C.c_int(), C.c_int()
+    _lib.check(L.sw_model_spec_variant(h, C.byref(sg), C.byref(rn)))
     return ModelSpec(int(dims[0]), int(dims[1]), int(dims[2]), int(dims[3]), int(dims[4]),
-                     int(dims[5]), bool(dims[6]), ovr, h)
+                     int(dims[5]), bool(dims[6]), ovr, "swiglu" if sg.value else "gelu",
+                     "rmsnorm" if rn.value else "layernorm", h)
 
 
 def read_model_spec(path: str) -> ModelSpec:

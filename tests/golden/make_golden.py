@@ -295,6 +295,35 @@ def gen_trainer(tmp):
     print("trainer.json:", {k: len(v["losses"]) for k, v in out.items()})
 
 
+def gen_ext_plans(tmp):
+    """Plans the REFERENCE derives (plan-shapes) for the SwiGLU / RMSNorm extension trees
+    (SURVEY D2/D3): the rule engine itself is the reference's, so the gate / up / down splits of
+    the extension are pinned exactly like the reference family's."""
+    sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
+    from oracle import rng_ref  # noqa: E402
+    cases = []
+    for spec_name, n_list in (("mini_swiglu.spec", (1, 2, 4)), ("llama7b_swiglu.spec", (1, 2, 4, 8))):
+        kv, ovr = {}, []
+        for ln in open(os.path.join(SPECS, spec_name)):
+            ln = ln.split("#")[0].strip()
+            if not ln:
+                continue
+            k, v = (x.strip() for x in ln.split("=", 1))
+            if k.startswith("role "):
+                ovr.append((k[5:].strip(), v))
+            else:
+                kv[k] = v if k in ("mlp", "norm") else int(v)
+        shapes = [(n, list(sh)) for n, sh in rng_ref.transformer_param_shapes(kv)]
+        sp = write(tmp, "shapes.tsv", shapes_tsv(shapes))
+        args_o = [write(tmp, "ovr.tsv", "".join(f"{p}\t{r}\n" for p, r in ovr))] if ovr else []
+        for n in n_list:
+            cases.append({"name": spec_name, "shapes": shapes, "overrides": ovr, "n_shards": n,
+                          "expected": run(["plan-shapes", sp, str(n)] + args_o, tmp)})
+    with open(os.path.join(HERE, "ext_plans.json"), "w") as f:
+        json.dump({"plan_cases": cases}, f)
+    print("ext_plans.json:", len(cases))
+
+
 CKPT_CASES = {
     # name -> how the test derives the file from the golden snapshot
     "cut1000": "first 1000 bytes",
@@ -371,6 +400,7 @@ def main():
         gen_numeric(tmp, "mini_f32_dp1_mp4", "mini.spec", "f32", 1, 4, 2, 16, 2, 1e-2, 0.01, False)
         gen_numeric(tmp, "tiny_f64_dp1_mp2", "tiny.spec", "f64", 1, 2, 4, 128, 1, 1e-3, 0.01, False)
         gen_checkpoint(tmp)
+        gen_ext_plans(tmp)
 
 
 if __name__ == "__main__":
@@ -378,5 +408,9 @@ if __name__ == "__main__":
         build()
         with tempfile.TemporaryDirectory() as tmp:
             gen_checkpoint(tmp)
+    elif sys.argv[1:] == ["ext_plans"]:
+        build()
+        with tempfile.TemporaryDirectory() as tmp:
+            gen_ext_plans(tmp)
     else:
         sys.exit(main())

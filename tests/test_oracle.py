@@ -110,3 +110,49 @@ def test_comm_report_matches_analytic():
     L, B, T, d, dff = 2, 4, 128, 256, 1024
     assert int(ar[1]) == 12 and int(ag[1]) == 8
     assert int(ar[2]) + int(ag[2]) == 6 * L * B * T * d * 8 + L * (3 * d + dff) * 8
+
+
+def test_extension_ops_equal_reference_op_compositions():
+    """RMSNorm and SiLU are exact compositions of reference ops, so the closed forms
+    the oracle uses are pinned to the reference's layer_norm / softmax: RMSNorm(x)*g ==
+    slice(layer_norm(concat(x, -x)), d)*g and SiLU(x) == x * softmax([x, 0])[0]."""
+    rng = np.random.default_rng(3)
+    x = rng.standard_normal((5, 7, 48)) * 2.0
+    g = rng.standard_normal(48)
+    y, _, _ = model_ref.rms_norm(x, g)
+    cat = np.concatenate([x, -x], -1)
+    ln, _, _ = model_ref.layer_norm(cat, np.ones(96), np.zeros(96))
+    assert np.max(np.abs(y - ln[..., :48] * g)) < 1e-12
+    z = rng.standard_normal(1000) * 6.0
+    two = np.stack([z, np.zeros_like(z)], -1)
+    sm = model_ref._softmax(two)[..., 0]
+    assert np.max(np.abs(model_ref.silu(z) - z * sm)) < 1e-12
+
+
+def test_extension_model_gradients_finite_difference():
+    """f64 central differences through the SwiGLU / RMSNorm decoder (loss of the oracle step)."""
+    spec = dict(vocab_size=16, n_layers=1, d_model=8, n_heads=2, d_ff=12, max_seq_len=4, mlp="swiglu",
+                norm="rmsnorm")
+    params = rng_ref.init_transformer_params(spec, seed=5)
+    rng = np.random.default_rng(1)
+    for k in params:  # non-trivial scales so every term of the RMSNorm backward is exercised
+        if k.endswith("/scale"):
+            params[k] = params[k] + 0.3 * rng.standard_normal(params[k].shape)
+    tokens = rng.integers(0, 16, (2, 4))
+    targets = rng.integers(0, 16, (2, 4))
+    weights = np.ones((2, 4))
+    _, grads, _ = model_ref.forward_backward(params, spec, tokens, targets, weights)
+    assert set(grads) == {n for n, _ in rng_ref.transformer_param_shapes(spec)}
+    for name in ("block_0/mlp/fc1/gate/kernel", "block_0/mlp/fc1/kernel", "block_0/mlp/fc2/kernel",
+                 "block_0/ln2/scale", "block_0/ln1/scale", "final_ln/scale", "embed/tok/kernel"):
+        flat = params[name].reshape(-1)
+        for i in rng.choice(flat.size, size=min(6, flat.size), replace=False):
+            old = flat[i]
+            flat[i] = old + 1e-6
+            lp, _, _ = model_ref.forward_backward(params, spec, tokens, targets, weights, need_grads=False)
+            flat[i] = old - 1e-6
+            lm, _, _ = model_ref.forward_backward(params, spec, tokens, targets, weights, need_grads=False)
+            flat[i] = old
+            fd = (lp - lm) / 2e-6
+            an = grads[name].reshape(-1)[i]
+            assert abs(fd - an) <= 1e-6 * max(1.0, abs(an)) + 1e-8, (name, i, fd, an)
