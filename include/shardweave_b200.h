@@ -275,6 +275,14 @@ SW_API sw_status sw_k_layernorm_bwd(const float* x, const float* mean, const flo
                                     float* dscale, float* dbias, int64_t M, int d, int accumulate,
                                     void* stream);
 /* Fused softmax cross entropy fwd+bwd over bf16 logits [M, ld] (kernels.hpp:327-363). */
+/* RMSNorm (extension): y = x / sqrt(mean(x^2) + eps) * scale (bf16 out), rstd saved;
+ * backward dx = rstd*(g - xhat*mean(g*xhat)), g = dy*scale, with g_io / g_bf16 / dscale as in
+ * sw_k_layernorm_bwd (dscale accumulated). */
+SW_API sw_status sw_k_rmsnorm_fwd(const float* x, const float* scale, void* y, float* rstd, int64_t M, int d,
+                                  float eps, void* stream);
+SW_API sw_status sw_k_rmsnorm_bwd(const float* x, const float* rstd, const float* scale, const float* dy,
+                                  float* g_io, void* g_bf16, float* dscale, int64_t M, int d, int accumulate,
+                                  void* stream);
 SW_API sw_status sw_k_xent(void* logits, int64_t ld, int64_t M, int V, const int32_t* targets,
                            const float* weights, const float* wsum, float* wloss, int write_grad,
                            void* stream);
@@ -282,6 +290,16 @@ SW_API sw_status sw_k_xent(void* logits, int64_t ld, int64_t M, int V, const int
 SW_API sw_status sw_k_adamw(float* p, float* m, float* v, const float* g, void* shadow, int64_t n,
                             float lr, float b1, float b2, float eps, float wd, float c1, float c2,
                             void* stream);
+
+/* SwiGLU MLP (extension): with W_gu = [gate; up] [2N, K] (K-major), h[M,N] =
+ * silu(A W_gate^T) * (A W_up^T) and pre[M, 2N] = bf16(A W_gate^T) | bf16(A W_up^T), one GEMM.
+ * The backward fuses the SwiGLU derivative into the down-projection dgrad: acc = dY . W_down
+ * [M, N]; dpre[M, 2N] = acc*u*silu'(g) | acc*silu(g) from pre. All bf16. */
+SW_API sw_status sw_k_gemm_bf16_swiglu(int M, int N, int K, const void* A, int64_t lda, const void* W_gu, int64_t ldw,
+                                       void* h, int64_t ldh, void* pre, int64_t ldpre, void* stream);
+SW_API sw_status sw_k_gemm_bf16_swiglu_bwd(int M, int N, int K, const void* A, int64_t lda, int a_mn_major,
+                                           const void* B, int64_t ldb, int b_mn_major, const void* pre,
+                                           int64_t ldpre, void* dpre, int64_t lddpre, void* stream);
 
 /* Optimizer in the backward: the weight-gradient GEMM G[M,N] = A^T-or-A . B (same operand
  * conventions as sw_k_gemm_bf16) whose epilogue applies the AdamW update of sw_k_adamw

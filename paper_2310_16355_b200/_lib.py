@@ -103,10 +103,16 @@ def _declare(L: C.CDLL) -> None:
     L.sw_k_attention_bwd.argtypes = [vp, vp, vp, vp, vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, vp]
     L.sw_k_layernorm_fwd.argtypes = [vp, vp, vp, vp, vp, vp, i64, C.c_int, f32, vp]
     L.sw_k_layernorm_bwd.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, vp, i64, C.c_int, C.c_int, vp]
+    L.sw_k_gemm_bf16_swiglu.argtypes = [C.c_int, C.c_int, C.c_int, vp, i64, vp, i64, vp, i64, vp, i64, vp]
+    L.sw_k_gemm_bf16_swiglu_bwd.argtypes = [C.c_int, C.c_int, C.c_int, vp, i64, C.c_int, vp, i64, C.c_int, vp,
+                                            i64, vp, i64, vp]
+    L.sw_k_rmsnorm_fwd.argtypes = [vp, vp, vp, vp, i64, C.c_int, f32, vp]
+    L.sw_k_rmsnorm_bwd.argtypes = [vp, vp, vp, vp, vp, vp, vp, i64, C.c_int, C.c_int, vp]
     L.sw_k_xent.argtypes = [vp, i64, i64, C.c_int, vp, vp, vp, vp, C.c_int, vp]
     L.sw_k_adamw.argtypes = [vp, vp, vp, vp, vp, i64, f32, f32, f32, f32, f32, f32, f32, vp]
     L.sw_k_gemm_bf16_adamw.argtypes = [C.c_int, C.c_int, C.c_int, vp, i64, C.c_int, vp, i64, C.c_int,
                                        vp, vp, vp, vp, i64, vp, f32, f32, f32, f32, f32, f32, f32, vp]
     for fn in ("sw_k_attention_fwd", "sw_k_attention_bwd", "sw_k_layernorm_fwd",
-               "sw_k_layernorm_bwd", "sw_k_xent", "sw_k_adamw", "sw_k_gemm_bf16_adamw"):
+               "sw_k_layernorm_bwd", "sw_k_xent", "sw_k_adamw", "sw_k_gemm_bf16_adamw",
+               "sw_k_rmsnorm_fwd", "sw_k_rmsnorm_bwd", "sw_k_gemm_bf16_swiglu", "sw_k_gemm_bf16_swiglu_bwd"):
         getattr(L, fn).restype = C.c_int

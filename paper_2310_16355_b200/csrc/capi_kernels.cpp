@@ -54,6 +54,51 @@ sw_status sw_k_gemm_bf16(int M, int N, int K, const void* A, int64_t lda, int a_
   });
 }
 
+sw_status sw_k_gemm_bf16_swiglu(int M, int N, int K, const void* A, int64_t lda, const void* W_gu, int64_t ldw,
+                                void* h, int64_t ldh, void* pre, int64_t ldpre, void* stream) {
+  return sw::guarded([&] {
+    sw::GemmParams g;
+    g.M = M;
+    g.N = N;
+    g.K = K;
+    g.A = A;
+    g.lda = lda;
+    g.B = W_gu;
+    g.ldb = ldw;
+    g.epi = sw::Epi::kSwiGLU;
+    g.C = h;
+    g.ldc = ldh;
+    g.C2 = pre;
+    g.ldc2 = ldpre;
+    g.swiglu_half = N;
+    sw::cuda_check(sw::gemm_bf16(g, static_cast<cudaStream_t>(stream)), "gemm_bf16_swiglu launch");
+  });
+}
+
+sw_status sw_k_gemm_bf16_swiglu_bwd(int M, int N, int K, const void* A, int64_t lda, int a_mn_major, const void* B,
+                                    int64_t ldb, int b_mn_major, const void* pre, int64_t ldpre, void* dpre,
+                                    int64_t lddpre, void* stream) {
+  return sw::guarded([&] {
+    sw::GemmParams g;
+    g.M = M;
+    g.N = N;
+    g.K = K;
+    g.A = A;
+    g.lda = lda;
+    g.a_mn_major = a_mn_major;
+    g.B = B;
+    g.ldb = ldb;
+    g.b_mn_major = b_mn_major;
+    g.epi = sw::Epi::kSwiGLUBwd;
+    g.C = dpre;
+    g.ldc = lddpre;
+    g.aux = pre;
+    g.ld_aux = ldpre;
+    g.swiglu_half = N;
+    sw::cuda_check(sw::gemm_bf16(g, static_cast<cudaStream_t>(stream)), "gemm_bf16_swiglu_bwd launch");
+  });
+}
+
 sw_status sw_k_gemm_bf16_adamw(int M, int N, int K, const void* A, int64_t lda, int a_mn_major, const void* B,
                                int64_t ldb, int b_mn_major, float* p, float* m, float* v, void* shadow, int64_t ld,
                                int* nonfinite_flag, float lr, float b1, float b2, float eps, float wd, float c1,
@@ -123,6 +168,24 @@ sw_status sw_k_layernorm_bwd(const float* x, const float* mean, const float* rst
     sw::k::layernorm_bwd(x, mean, rstd, scale, dy, g_io, static_cast<sw::k::bf16*>(g_bf16), dscale, dbias, M,
                          d, accumulate, static_cast<cudaStream_t>(stream));
     sw::cuda_check(cudaGetLastError(), "layernorm_bwd");
+  });
+}
+
+sw_status sw_k_rmsnorm_fwd(const float* x, const float* scale, void* y, float* rstd, int64_t M, int d, float eps,
+                           void* stream) {
+  return sw::guarded([&] {
+    sw::k::layernorm_fwd(x, scale, nullptr, static_cast<sw::k::bf16*>(y), nullptr, rstd, M, d, eps,
+                         static_cast<cudaStream_t>(stream), 1);
+    sw::cuda_check(cudaGetLastError(), "rmsnorm_fwd");
+  });
+}
+
+sw_status sw_k_rmsnorm_bwd(const float* x, const float* rstd, const float* scale, const float* dy, float* g_io,
+                           void* g_bf16, float* dscale, int64_t M, int d, int accumulate, void* stream) {
+  return sw::guarded([&] {
+    sw::k::layernorm_bwd(x, nullptr, rstd, scale, dy, g_io, static_cast<sw::k::bf16*>(g_bf16), dscale, nullptr, M,
+                         d, accumulate, static_cast<cudaStream_t>(stream), nullptr, 1);
+    sw::cuda_check(cudaGetLastError(), "rmsnorm_bwd");
   });
 }
 

@@ -25,6 +25,12 @@ enum class Epi : int {
   kAdamW = 5,       // wgrad with the optimizer in the epilogue: acc is the fp32 gradient of the
                     // [M, N] weight at adam_* (row pitch ldc); AdamW updates p/m/v in place and
                     // refreshes the bf16 shadow; non-finite gradients set *adam_flag
+  // SwiGLU extension. kSwiGLU: B = fused [gate; up] weight [2*N, K] (up rows start at
+  // swiglu_half = N); each 256-wide tile multiplies 128 gate rows and the matching 128 up rows,
+  // the epilogue writes h = silu(g) * u to C [M, N] and the pre-activations g | u to C2 [M, 2N].
+  // kSwiGLUBwd: acc = dh [M, N]; aux = g | u [M, 2N]; C [M, 2N] = dh*u*silu'(g) | dh*silu(g).
+  kSwiGLU = 6,
+  kSwiGLUBwd = 7,
 };
 
 struct GemmParams {
@@ -47,6 +53,7 @@ struct GemmParams {
   int64_t bias_seg_stride = 0;
   const void* aux = nullptr;
   int64_t ld_aux = 0;
+  int swiglu_half = 0;  // kSwiGLU / kSwiGLUBwd: N of the h activations (row offset of up in B)
   float alpha = 1.0f;
   int accumulate = 0;
   // kAdamW (train_state.hpp:211-216, Scalar = float)

@@ -204,6 +204,28 @@ __device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int row, int
         }
       }
     }
+  } else if constexpr (EPI == Epi::kSwiGLUBwd) {
+    const __nv_bfloat16* pre = reinterpret_cast<const __nv_bfloat16*>(p.aux) + static_cast<int64_t>(row) * p.ld_aux;
+    __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(p.C) + static_cast<int64_t>(row) * p.ldc;
+    const int half = p.swiglu_half;
+#pragma unroll
+    for (int c = 0; c < 32; c += 8) {
+      if (c < ncols) {
+        const uint4 rg = *reinterpret_cast<const uint4*>(pre + col0 + c);
+        const uint4 ru = *reinterpret_cast<const uint4*>(pre + half + col0 + c);
+        const uint32_t wg[4] = {rg.x, rg.y, rg.z, rg.w}, wu[4] = {ru.x, ru.y, ru.z, ru.w};
+        uint32_t og[4], ou[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float2 g = dev::unpack_bf16x2(wg[e]), u = dev::unpack_bf16x2(wu[e]);
+          const float d0 = v[c + 2 * e], d1 = v[c + 2 * e + 1];
+          og[e] = dev::pack_bf16x2(d0 * u.x * dev::silu_grad(g.x), d1 * u.y * dev::silu_grad(g.y));
+          ou[e] = dev::pack_bf16x2(d0 * dev::silu(g.x), d1 * dev::silu(g.y));
+        }
+        *reinterpret_cast<uint4*>(out + col0 + c) = make_uint4(og[0], og[1], og[2], og[3]);
+        *reinterpret_cast<uint4*>(out + half + col0 + c) = make_uint4(ou[0], ou[1], ou[2], ou[3]);
+      }
+    }
   } else {
     // fp32 outputs
     float* out = reinterpret_cast<float*>(p.C) + static_cast<int64_t>(row) * p.ldc + col0;
@@ -528,7 +550,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
   const uint32_t rank = dev::cluster_ctarank();
 
   const int num_m = (p.M + 2 * BM - 1) / (2 * BM);  // pair tiles along M (256 rows)
-  const int num_n = (p.N + BN - 1) / BN;
+  constexpr bool kGlu = EPI == Epi::kSwiGLU;
+  const int num_n = kGlu ? (p.N + 127) / 128 : (p.N + BN - 1) / BN;  // SwiGLU: 128 h columns per tile
   const int num_tiles = num_m * num_n;
   const int num_kb = (p.K + BK - 1) / BK;
   const int pair = static_cast<int>(blockIdx.x) >> 1;
@@ -565,7 +588,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         int mb, nb;
         tile_coords(t, num_m, num_n, mb, nb);
         const int m0 = mb * 2 * BM + static_cast<int>(rank) * BM;
-        const int n0 = nb * BN + static_cast<int>(rank) * 128;
+        // SwiGLU: CTA 0 stages the tile's 128 gate rows, CTA 1 the matching 128 up rows
+        const int n0 = kGlu ? (rank == 0 ? nb * 128 : p.swiglu_half + nb * 128)
+                            : nb * BN + static_cast<int>(rank) * 128;
         for (int kb = 0; kb < num_kb; ++kb) {
           dev::mbar_wait(&empty[stage], phase ^ 1);
           if (rank == 0) dev::mbar_arrive_expect_tx(&full[stage], 2 * P_STAGE_BYTES);
@@ -683,8 +708,46 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       dev::mbar_wait(&tfull[acc], acc_phase);
       dev::tc_fence_after();
       const int n_left = p.N - nb * BN;
+      if constexpr (kGlu) {
+        // accumulator columns [0,128) = gate, [128,256) = up for h columns nb*128 + [0,128)
+        const int h_left = p.N - nb * 128;
 #pragma unroll 1
-      for (int j = 0; j < BN / 32; ++j) {
+        for (int j = 0; j < 4; ++j) {
+          const int ncols = min(32, h_left - j * 32);
+          if (ncols <= 0) break;
+          uint32_t rg[32], ru[32];
+          dev::tmem_ld_32x32b_x32(tmem_base + ((q * 32) << 16) + acc * BN + j * 32, rg);
+          dev::tmem_ld_32x32b_x32(tmem_base + ((q * 32) << 16) + acc * BN + 128 + j * 32, ru);
+          dev::tmem_ld_wait();
+          if (row < p.M) {
+            const int c0 = nb * 128 + j * 32;
+            __nv_bfloat16* hrow = reinterpret_cast<__nv_bfloat16*>(p.C) + static_cast<int64_t>(row) * p.ldc + c0;
+            __nv_bfloat16* prow = reinterpret_cast<__nv_bfloat16*>(p.C2) + static_cast<int64_t>(row) * p.ldc2 + c0;
+#pragma unroll
+            for (int c = 0; c < 32; c += 8) {
+              if (c < ncols) {
+                uint32_t hw[4], gw[4], uw[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                  // the stored bf16 pre-activations are what the backward differentiates
+                  const float2 g = dev::unpack_bf16x2(
+                      dev::pack_bf16x2(__uint_as_float(rg[c + 2 * e]), __uint_as_float(rg[c + 2 * e + 1])));
+                  const float2 u = dev::unpack_bf16x2(
+                      dev::pack_bf16x2(__uint_as_float(ru[c + 2 * e]), __uint_as_float(ru[c + 2 * e + 1])));
+                  gw[e] = dev::pack_bf16x2(g.x, g.y);
+                  uw[e] = dev::pack_bf16x2(u.x, u.y);
+                  hw[e] = dev::pack_bf16x2(dev::silu(g.x) * u.x, dev::silu(g.y) * u.y);
+                }
+                *reinterpret_cast<uint4*>(hrow + c) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+                *reinterpret_cast<uint4*>(prow + c) = make_uint4(gw[0], gw[1], gw[2], gw[3]);
+                *reinterpret_cast<uint4*>(prow + p.swiglu_half + c) = make_uint4(uw[0], uw[1], uw[2], uw[3]);
+              }
+            }
+          }
+        }
+      }
+#pragma unroll 1
+      for (int j = 0; j < (kGlu ? 0 : BN / 32); ++j) {
         const int ncols = min(32, n_left - j * 32);
         if (ncols <= 0) break;
         uint32_t r[32];
@@ -759,9 +822,11 @@ cudaError_t launch_2sm(const GemmParams& p, cudaStream_t stream) {
   }
   CUtensorMap ta = p.a_mn_major ? make_tmap_bf16_2d(p.A, p.M, p.K, p.lda, 64, 64)
                                 : make_tmap_bf16_2d(p.A, p.K, p.M, p.lda, 64, BM);
+  const uint64_t b_rows = EPI == Epi::kSwiGLU ? 2ull * p.swiglu_half : static_cast<uint64_t>(p.N);
   CUtensorMap tb = p.b_mn_major ? make_tmap_bf16_2d(p.B, p.N, p.K, p.ldb, 64, 64)
-                                : make_tmap_bf16_2d(p.B, p.K, p.N, p.ldb, 64, 128);
-  const int num_tiles = ((p.M + 2 * BM - 1) / (2 * BM)) * ((p.N + BN - 1) / BN);
+                                : make_tmap_bf16_2d(p.B, p.K, b_rows, p.ldb, 64, 128);
+  const int num_n = EPI == Epi::kSwiGLU ? (p.N + 127) / 128 : (p.N + BN - 1) / BN;
+  const int num_tiles = ((p.M + 2 * BM - 1) / (2 * BM)) * num_n;
   const int sms = (p.num_sms > 0 ? p.num_sms : device_sm_count()) & ~1;
   const int grid = 2 * num_tiles < sms ? 2 * num_tiles : sms;
   OptMaps om{};
@@ -777,6 +842,9 @@ cudaError_t launch_2sm(const GemmParams& p, cudaStream_t stream) {
 template <Epi EPI>
 cudaError_t launch(const GemmParams& p, cudaStream_t stream) {
   if (use_pairs()) return launch_2sm<EPI>(p, stream);
+  if constexpr (EPI == Epi::kSwiGLU) {
+    throw std::runtime_error("gemm_bf16: the SwiGLU epilogue needs the CTA-pair kernel (unset SW_GEMM_1SM)");
+  }
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(gemm_bf16_kernel<EPI>,
@@ -810,6 +878,16 @@ cudaError_t gemm_bf16(const GemmParams& p, cudaStream_t stream) {
     case Epi::kBiasGelu: return launch<Epi::kBiasGelu>(p, stream);
     case Epi::kResidF32: return launch<Epi::kResidF32>(p, stream);
     case Epi::kGeluBwd: return launch<Epi::kGeluBwd>(p, stream);
+    case Epi::kSwiGLU:
+      if (p.swiglu_half != p.N || p.b_mn_major) {
+        throw std::runtime_error("gemm_bf16: SwiGLU needs swiglu_half == N and a K-major fused weight");
+      }
+      return launch<Epi::kSwiGLU>(p, stream);
+    case Epi::kSwiGLUBwd:
+      if (p.swiglu_half != p.N || p.aux == nullptr) {
+        throw std::runtime_error("gemm_bf16: SwiGLU backward needs swiglu_half == N and the pre-activations");
+      }
+      return launch<Epi::kSwiGLUBwd>(p, stream);
     case Epi::kAdamW: {
       GemmParams q = p;
       const float lo = 1.0f / 16384.0f;

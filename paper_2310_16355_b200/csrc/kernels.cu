@@ -145,7 +145,8 @@ __global__ void __launch_bounds__(THREADS) ln_fwd_kernel(const float* __restrict
                                                          const float* __restrict__ scale,
                                                          const float* __restrict__ bias,
                                                          bf16* __restrict__ y, float* __restrict__ mean_out,
-                                                         float* __restrict__ rstd_out, int d, float eps) {
+                                                         float* __restrict__ rstd_out, int d, float eps,
+                                                         int rms) {
   __shared__ float red[32];
   const int64_t row = blockIdx.x;
   const float* xr = x + row * d;
@@ -157,7 +158,8 @@ __global__ void __launch_bounds__(THREADS) ln_fwd_kernel(const float* __restrict
     v[j] = c < d ? *reinterpret_cast<const float4*>(xr + c) : make_float4(0, 0, 0, 0);
     s += v[j].x + v[j].y + v[j].z + v[j].w;
   }
-  const float mean = block_sum(s, red) / d;
+  // RMSNorm (extension): no centring, no bias -- xhat = x / sqrt(mean(x^2) + eps)
+  const float mean = rms ? 0.f : block_sum(s, red) / d;
   float q = 0.f;
 #pragma unroll
   for (int j = 0; j < V4; ++j) {
@@ -175,7 +177,7 @@ __global__ void __launch_bounds__(THREADS) ln_fwd_kernel(const float* __restrict
     const int c = (threadIdx.x + j * THREADS) * 4;
     if (c < d) {
       const float4 sc = *reinterpret_cast<const float4*>(scale + c);
-      const float4 bi = *reinterpret_cast<const float4*>(bias + c);
+      const float4 bi = rms ? make_float4(0.f, 0.f, 0.f, 0.f) : *reinterpret_cast<const float4*>(bias + c);
       uint2 w;
       w.x = dev::pack_bf16x2((v[j].x - mean) * rstd * sc.x + bi.x, (v[j].y - mean) * rstd * sc.y + bi.y);
       w.y = dev::pack_bf16x2((v[j].z - mean) * rstd * sc.z + bi.z, (v[j].w - mean) * rstd * sc.w + bi.w);
@@ -183,7 +185,7 @@ __global__ void __launch_bounds__(THREADS) ln_fwd_kernel(const float* __restrict
     }
   }
   if (threadIdx.x == 0) {
-    mean_out[row] = mean;
+    if (mean_out != nullptr) mean_out[row] = mean;
     rstd_out[row] = rstd;
   }
 }
@@ -192,13 +194,13 @@ __global__ void __launch_bounds__(THREADS) ln_fwd_kernel(const float* __restrict
 __global__ void ln_fwd_generic_kernel(const float* __restrict__ x, const float* __restrict__ scale,
                                       const float* __restrict__ bias, bf16* __restrict__ y,
                                       float* __restrict__ mean_out, float* __restrict__ rstd_out,
-                                      int d, float eps) {
+                                      int d, float eps, int rms) {
   __shared__ float red[32];
   const int64_t row = blockIdx.x;
   const float* xr = x + row * d;
   float s = 0.f;
   for (int i = threadIdx.x; i < d; i += blockDim.x) s += xr[i];
-  const float mean = block_sum(s, red) / d;
+  const float mean = rms ? 0.f : block_sum(s, red) / d;
   float q = 0.f;
   for (int i = threadIdx.x; i < d; i += blockDim.x) {
     const float a = xr[i] - mean;
@@ -207,10 +209,10 @@ __global__ void ln_fwd_generic_kernel(const float* __restrict__ x, const float* 
   const float var = block_sum(q, red) / d;
   const float rstd = 1.0f / sqrtf(var + eps);
   for (int i = threadIdx.x; i < d; i += blockDim.x) {
-    y[row * d + i] = __float2bfloat16((xr[i] - mean) * rstd * scale[i] + bias[i]);
+    y[row * d + i] = __float2bfloat16((xr[i] - mean) * rstd * scale[i] + (rms ? 0.f : bias[i]));
   }
   if (threadIdx.x == 0) {
-    mean_out[row] = mean;
+    if (mean_out != nullptr) mean_out[row] = mean;
     rstd_out[row] = rstd;
   }
 }
@@ -225,13 +227,13 @@ __global__ void __launch_bounds__(THREADS, (THREADS <= 256 ? 4 : 2)) ln_bwd_kern
     const float* __restrict__ x, const float* __restrict__ mean, const float* __restrict__ rstd,
     const float* __restrict__ scale, const float* __restrict__ dy, float* __restrict__ g_io,
     bf16* __restrict__ g_bf16, float* __restrict__ dscale, float* __restrict__ dbias, int64_t M,
-    int d, int accumulate, float* __restrict__ partials) {
+    int d, int accumulate, float* __restrict__ partials, int rms) {
   __shared__ float red[32];
   float4 ds[V4], db[V4];
 #pragma unroll
   for (int j = 0; j < V4; ++j) ds[j] = db[j] = make_float4(0, 0, 0, 0);
   for (int64_t row = blockIdx.x; row < M; row += gridDim.x) {
-    const float mu = mean[row], rs = rstd[row];
+    const float mu = mean ? mean[row] : 0.f, rs = rstd[row];
     const float* xr = x + row * d;
     const float* dr = dy + row * d;
     float s1 = 0.f, s2 = 0.f;
@@ -250,7 +252,7 @@ __global__ void __launch_bounds__(THREADS, (THREADS <= 256 ? 4 : 2)) ln_bwd_kern
         s2 += gx * xh.x + gy * xh.y + gz * xh.z + gw * xh.w;
       }
     }
-    const float gm = block_sum(s1, red) / d;
+    const float gm = rms ? 0.f : block_sum(s1, red) / d;  // RMSNorm: no mean term
     const float gxm = block_sum(s2, red) / d;
 #pragma unroll
     for (int j = 0; j < V4; ++j) {
@@ -288,8 +290,10 @@ __global__ void __launch_bounds__(THREADS, (THREADS <= 256 ? 4 : 2)) ln_bwd_kern
       } else {
         atomicAdd(dscale + c, ds[j].x); atomicAdd(dscale + c + 1, ds[j].y);
         atomicAdd(dscale + c + 2, ds[j].z); atomicAdd(dscale + c + 3, ds[j].w);
-        atomicAdd(dbias + c, db[j].x); atomicAdd(dbias + c + 1, db[j].y);
-        atomicAdd(dbias + c + 2, db[j].z); atomicAdd(dbias + c + 3, db[j].w);
+        if (dbias != nullptr) {
+          atomicAdd(dbias + c, db[j].x); atomicAdd(dbias + c + 1, db[j].y);
+          atomicAdd(dbias + c + 2, db[j].z); atomicAdd(dbias + c + 3, db[j].w);
+        }
       }
     }
   }
@@ -325,7 +329,7 @@ __global__ void __launch_bounds__(THREADS, 2) ln_bwd2_kernel(
     const float* __restrict__ x, const float* __restrict__ mean, const float* __restrict__ rstd,
     const float* __restrict__ scale, const float* __restrict__ dy, float* __restrict__ g_io,
     bf16* __restrict__ g_bf16, float* __restrict__ dscale, float* __restrict__ dbias, int64_t M,
-    int d, int accumulate, float* __restrict__ partials) {
+    int d, int accumulate, float* __restrict__ partials, int rms) {
   __shared__ __align__(16) float red[4 * (THREADS / 32)];
   float4 ds[V4], db[V4];
 #pragma unroll
@@ -335,7 +339,7 @@ __global__ void __launch_bounds__(THREADS, 2) ln_bwd2_kernel(
     const int64_t r0 = 2 * pr;
     const bool two = r0 + 1 < M;
     const int64_t r1 = two ? r0 + 1 : r0;
-    const float mu0 = mean[r0], rs0 = rstd[r0], mu1 = mean[r1], rs1 = rstd[r1];
+    const float mu0 = mean ? mean[r0] : 0.f, rs0 = rstd[r0], mu1 = mean ? mean[r1] : 0.f, rs1 = rstd[r1];
     float4 xa[V4], da[V4], xb[V4], dbv[V4];
 #pragma unroll
     for (int j = 0; j < V4; ++j) {
@@ -382,7 +386,7 @@ __global__ void __launch_bounds__(THREADS, 2) ln_bwd2_kernel(
       }
     }
     const float4 t = block_sum4(sums, red);
-    const float gm0 = t.x / d, gxm0 = t.y / d, gm1 = t.z / d, gxm1 = t.w / d;
+    const float gm0 = rms ? 0.f : t.x / d, gxm0 = t.y / d, gm1 = rms ? 0.f : t.z / d, gxm1 = t.w / d;
 #pragma unroll
     for (int j = 0; j < V4; ++j) {
       const int c = (threadIdx.x + j * THREADS) * 4;
@@ -430,8 +434,10 @@ __global__ void __launch_bounds__(THREADS, 2) ln_bwd2_kernel(
       } else {
         atomicAdd(dscale + c, ds[j].x); atomicAdd(dscale + c + 1, ds[j].y);
         atomicAdd(dscale + c + 2, ds[j].z); atomicAdd(dscale + c + 3, ds[j].w);
-        atomicAdd(dbias + c, db[j].x); atomicAdd(dbias + c + 1, db[j].y);
-        atomicAdd(dbias + c + 2, db[j].z); atomicAdd(dbias + c + 3, db[j].w);
+        if (dbias != nullptr) {
+          atomicAdd(dbias + c, db[j].x); atomicAdd(dbias + c + 1, db[j].y);
+          atomicAdd(dbias + c + 2, db[j].z); atomicAdd(dbias + c + 3, db[j].w);
+        }
       }
     }
   }
@@ -448,17 +454,17 @@ __global__ void ln_param_reduce_kernel(const float* __restrict__ partials, int n
   float s = 0.f;
   for (int b = 0; b < nblk; ++b) s += partials[static_cast<int64_t>(b) * 2 * d + which * d + col];
   float* o = which == 0 ? dscale : dbias;
-  o[col] += s;
+  if (o != nullptr) o[col] += s;
 }
 
 __global__ void ln_bwd_generic_kernel(const float* __restrict__ x, const float* __restrict__ mean,
                                       const float* __restrict__ rstd, const float* __restrict__ scale,
                                       const float* __restrict__ dy, float* __restrict__ g_io,
                                       bf16* __restrict__ g_bf16, float* __restrict__ dscale,
-                                      float* __restrict__ dbias, int d, int accumulate) {
+                                      float* __restrict__ dbias, int d, int accumulate, int rms) {
   __shared__ float red[32];
   const int64_t row = blockIdx.x;
-  const float mu = mean[row], rs = rstd[row];
+  const float mu = mean ? mean[row] : 0.f, rs = rstd[row];
   float s1 = 0.f, s2 = 0.f;
   for (int i = threadIdx.x; i < d; i += blockDim.x) {
     const float xh = (x[row * d + i] - mu) * rs;
@@ -466,7 +472,7 @@ __global__ void ln_bwd_generic_kernel(const float* __restrict__ x, const float* 
     s1 += g;
     s2 += g * xh;
   }
-  const float gm = block_sum(s1, red) / d;
+  const float gm = rms ? 0.f : block_sum(s1, red) / d;
   const float gxm = block_sum(s2, red) / d;
   for (int i = threadIdx.x; i < d; i += blockDim.x) {
     const float xh = (x[row * d + i] - mu) * rs;
@@ -477,7 +483,7 @@ __global__ void ln_bwd_generic_kernel(const float* __restrict__ x, const float* 
     g_io[row * d + i] = dx;
     g_bf16[row * d + i] = __float2bfloat16(dx);
     atomicAdd(dscale + i, dv * xh);
-    atomicAdd(dbias + i, dv);
+    if (dbias != nullptr) atomicAdd(dbias + i, dv);
   }
 }
 
@@ -910,16 +916,16 @@ void embed_bwd_pos(const float* g, float* dpos, int B, int T, int d, int accumul
 }
 
 void layernorm_fwd(const float* x, const float* scale, const float* bias, bf16* y, float* mean,
-                   float* rstd, int64_t M, int d, float eps, cudaStream_t s) {
+                   float* rstd, int64_t M, int d, float eps, cudaStream_t s, int rms) {
   const unsigned g = static_cast<unsigned>(M);
   if (d % 4 == 0 && d <= 512) {
-    ln_fwd_kernel<32, 4><<<g, 32, 0, s>>>(x, scale, bias, y, mean, rstd, d, eps);
+    ln_fwd_kernel<32, 4><<<g, 32, 0, s>>>(x, scale, bias, y, mean, rstd, d, eps, rms);
   } else if (d % 4 == 0 && d <= 4096) {
-    ln_fwd_kernel<256, 4><<<g, 256, 0, s>>>(x, scale, bias, y, mean, rstd, d, eps);
+    ln_fwd_kernel<256, 4><<<g, 256, 0, s>>>(x, scale, bias, y, mean, rstd, d, eps, rms);
   } else if (d % 4 == 0 && d <= 12288) {
-    ln_fwd_kernel<512, 6><<<g, 512, 0, s>>>(x, scale, bias, y, mean, rstd, d, eps);
+    ln_fwd_kernel<512, 6><<<g, 512, 0, s>>>(x, scale, bias, y, mean, rstd, d, eps, rms);
   } else {
-    ln_fwd_generic_kernel<<<g, 256, 0, s>>>(x, scale, bias, y, mean, rstd, d, eps);
+    ln_fwd_generic_kernel<<<g, 256, 0, s>>>(x, scale, bias, y, mean, rstd, d, eps, rms);
   }
 }
 
@@ -936,27 +942,27 @@ int64_t layernorm_bwd_partials(int d) { return static_cast<int64_t>(4 * kSMs) * 
 
 void layernorm_bwd(const float* x, const float* mean, const float* rstd, const float* scale,
                    const float* dy, float* g_io, bf16* g_bf16, float* dscale, float* dbias,
-                   int64_t M, int d, int accumulate, cudaStream_t s, float* partials) {
+                   int64_t M, int d, int accumulate, cudaStream_t s, float* partials, int rms) {
   const unsigned g = static_cast<unsigned>(M < 4 * kSMs ? M : 4 * kSMs);
   unsigned nblk = g;
   if (d % 4 == 0 && d <= 512) {
     ln_bwd_kernel<32, 4><<<g, 32, 0, s>>>(x, mean, rstd, scale, dy, g_io, g_bf16, dscale, dbias, M, d, accumulate,
-                                          partials);
+                                          partials, rms);
   } else if (d % 4 == 0 && d <= 4096 && ln_bwd_v1()) {
     ln_bwd_kernel<256, 4><<<g, 256, 0, s>>>(x, mean, rstd, scale, dy, g_io, g_bf16, dscale, dbias, M, d, accumulate,
-                                            partials);
+                                            partials, rms);
   } else if (d % 4 == 0 && d <= 4096) {
     const unsigned g2 = static_cast<unsigned>((M + 1) / 2 < 2 * kSMs ? (M + 1) / 2 : 2 * kSMs);
     nblk = g2;
     ln_bwd2_kernel<256, 4><<<g2, 256, 0, s>>>(x, mean, rstd, scale, dy, g_io, g_bf16, dscale, dbias, M, d,
-                                              accumulate, partials);
+                                              accumulate, partials, rms);
   } else if (d % 4 == 0 && d <= 12288) {
     ln_bwd_kernel<512, 6><<<g, 512, 0, s>>>(x, mean, rstd, scale, dy, g_io, g_bf16, dscale, dbias, M, d, accumulate,
-                                            partials);
+                                            partials, rms);
   } else {
     // one CTA per row: parameter partials would be row-sized; this shape keeps the atomics
     ln_bwd_generic_kernel<<<static_cast<unsigned>(M), 256, 0, s>>>(x, mean, rstd, scale, dy, g_io, g_bf16,
-                                                                  dscale, dbias, d, accumulate);
+                                                                  dscale, dbias, d, accumulate, rms);
     return;
   }
   if (partials != nullptr) {

@@ -28,8 +28,9 @@ void embed_bwd_pos(const float* g, float* dpos, int B, int T, int d, int accumul
 
 // LayerNorm over the last dim, biased variance, eps (kernels.hpp:184-215): y = xhat*scale+bias
 // (bf16), mean/rstd saved for the backward.
+// rms = 1: RMSNorm (extension): no centring, no bias (bias may be null), mean = 0.
 void layernorm_fwd(const float* x, const float* scale, const float* bias, bf16* y, float* mean,
-                   float* rstd, int64_t M, int d, float eps, cudaStream_t s);
+                   float* rstd, int64_t M, int d, float eps, cudaStream_t s, int rms = 0);
 // dx = rstd*(g - mean(g) - xhat*mean(g*xhat)), g = dy*scale (kernels.hpp:232-271).
 // g_io: residual-stream gradient; g_io = (accumulate ? g_io : 0) + dx; g_bf16 = bf16(g_io).
 // dscale += sum_rows dy*xhat, dbias += sum_rows dy (atomics; caller zeroes when needed).
@@ -37,7 +38,7 @@ void layernorm_fwd(const float* x, const float* scale, const float* bias, bf16* 
 // column partials and one fixed-order pass adds them (deterministic); partials == nullptr: atomics.
 void layernorm_bwd(const float* x, const float* mean, const float* rstd, const float* scale,
                    const float* dy, float* g_io, bf16* g_bf16, float* dscale, float* dbias,
-                   int64_t M, int d, int accumulate, cudaStream_t s, float* partials = nullptr);
+                   int64_t M, int d, int accumulate, cudaStream_t s, float* partials = nullptr, int rms = 0);
 int64_t layernorm_bwd_partials(int d);
 
 // Column sums of X [M, N] (bf16 or f32, row pitch ld) written (accumulate=0) or added into

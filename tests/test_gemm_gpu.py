@@ -163,3 +163,38 @@ def test_gemm_adamw_epilogue_flags_nonfinite():
                                       1e-3, 0.9, 0.999, 1e-8, 0.0, 0.1, 0.001, None))
     torch.cuda.synchronize()
     assert int(flag.item()) == 1
+
+
+@pytest.mark.parametrize("M,N,K", [(256, 128, 64), (300, 200, 136), (1000, 1376, 512), (512, 688, 4096)])
+def test_gemm_swiglu_fwd_bwd(M, N, K):
+    """SwiGLU extension vs torch fp32 on the same bf16 operands: the fused [gate; up]
+    GEMM writes h = silu(g)*u and the bf16 pre-activations; the down-projection dgrad epilogue
+    writes d(gate) | d(up) from them."""
+    L = _lib.lib()
+    gen = torch.Generator(device=DEV).manual_seed(M + 7 * N + K)
+    x = torch.randn(M, K, generator=gen, device=DEV).bfloat16()
+    w = (torch.randn(2 * N, K, generator=gen, device=DEV) / math.sqrt(K)).bfloat16()
+    h = torch.full((M, N), float("nan"), device=DEV).bfloat16()
+    pre = torch.full((M, 2 * N), float("nan"), device=DEV).bfloat16()
+    _lib.check(L.sw_k_gemm_bf16_swiglu(M, N, K, x.data_ptr(), K, w.data_ptr(), K, h.data_ptr(), N, pre.data_ptr(),
+                                       2 * N, None))
+    torch.cuda.synchronize()
+    acc = x.float() @ w.float().t()
+    g_ref, u_ref = acc[:, :N], acc[:, N:]
+    assert _rel(pre[:, :N], g_ref) < 1e-2 and _rel(pre[:, N:], u_ref) < 1e-2
+    gb, ub = pre[:, :N].float(), pre[:, N:].float()
+    assert _rel(h, torch.nn.functional.silu(gb) * ub) < 1e-2
+
+    # backward: dh = dY . W_down (dY [M, D], W_down [D, N] used MN-major like the executor)
+    D = 96
+    dy = torch.randn(M, D, generator=gen, device=DEV).bfloat16()
+    wd = (torch.randn(D, N, generator=gen, device=DEV) / math.sqrt(N)).bfloat16()
+    dpre = torch.full((M, 2 * N), float("nan"), device=DEV).bfloat16()
+    _lib.check(L.sw_k_gemm_bf16_swiglu_bwd(M, N, D, dy.data_ptr(), D, 0, wd.data_ptr(), N, 1, pre.data_ptr(), 2 * N,
+                                           dpre.data_ptr(), 2 * N, None))
+    torch.cuda.synchronize()
+    dh = dy.float() @ wd.float()
+    sg = torch.sigmoid(gb)
+    want_g = dh * ub * sg * (1 + gb * (1 - sg))
+    want_u = dh * torch.nn.functional.silu(gb)
+    assert _rel(dpre[:, :N], want_g) < 1e-2 and _rel(dpre[:, N:], want_u) < 1e-2

@@ -149,3 +149,33 @@ def test_adamw_kernel():
     assert torch.allclose(mm, torch.full_like(mm, 0.1))
     assert torch.allclose(vm, torch.full_like(vm, 0.001))
     assert torch.allclose(pm, torch.full_like(pm, 1 - 0.1 / (1 + 1e-8)))
+
+
+@pytest.mark.parametrize("M,d", [(64, 32), (300, 256), (257, 4096), (33, 9216), (10, 100)])
+def test_rmsnorm_fwd_bwd(M, d):
+    """RMSNorm extension vs torch fp32: y = x * rsqrt(mean(x^2) + eps) * g."""
+    L = _lib.lib()
+    g = torch.Generator(device=DEV).manual_seed(M * 3 + d)
+    x = torch.randn(M, d, generator=g, device=DEV) * 3 + 1
+    s = torch.randn(d, generator=g, device=DEV)
+    y = torch.empty(M, d, device=DEV, dtype=torch.bfloat16)
+    rstd = torch.empty(M, device=DEV)
+    _lib.check(L.sw_k_rmsnorm_fwd(x.data_ptr(), s.data_ptr(), y.data_ptr(), rstd.data_ptr(), M, d, 1e-5, None))
+    xr = x.clone().requires_grad_(True)
+    sr = s.clone().requires_grad_(True)
+    ref = xr * torch.rsqrt((xr * xr).mean(-1, keepdim=True) + 1e-5) * sr
+    torch.cuda.synchronize()
+    assert rel(y, ref) < 1e-2
+    assert torch.allclose(rstd, torch.rsqrt((x * x).mean(-1) + 1e-5), rtol=1e-5)
+    dy = torch.randn(M, d, generator=g, device=DEV)
+    gio = torch.randn(M, d, generator=g, device=DEV)
+    g0 = gio.clone()
+    gb = torch.empty(M, d, device=DEV, dtype=torch.bfloat16)
+    ds = torch.zeros(d, device=DEV)
+    _lib.check(L.sw_k_rmsnorm_bwd(x.data_ptr(), rstd.data_ptr(), s.data_ptr(), dy.data_ptr(), gio.data_ptr(),
+                                  gb.data_ptr(), ds.data_ptr(), M, d, 1, None))
+    (ref * dy).sum().backward()
+    torch.cuda.synchronize()
+    assert rel(gio - g0, xr.grad) < 1e-5
+    assert rel(ds, sr.grad) < 1e-5
+    assert rel(gb, gio) < 1e-2
