@@ -62,19 +62,24 @@ def read_spec(path):
         ln = ln.split("#")[0].strip()
         if "=" in ln and not ln.startswith("role"):
             k, v = (x.strip() for x in ln.split("="))
-            out[k] = (v in ("true", "yes", "1")) if k == "tie_embeddings" else int(v)
+            if k in ("mlp", "norm"):
+                out[k] = v
+            else:
+                out[k] = (v in ("true", "yes", "1")) if k == "tie_embeddings" else int(v)
     return out
 
 
 def matmul_params(s, layers=None):
     L = s["n_layers"] if layers is None else layers
     d, ff, V = s["d_model"], s["d_ff"], s["vocab_size"]
-    return L * (4 * d * d + 2 * d * ff) + V * d
+    n_mlp = 3 if s.get("mlp") == "swiglu" else 2  # SwiGLU: gate, up, down (6.607 G)
+    return L * (4 * d * d + n_mlp * d * ff) + V * d
 
 
 def train_flops_per_token(s, T, layers=None):
     """Algorithmic fwd+bwd FLOPs/token: 6*N_matmul + 6*L*d*T (causal attention counted once),
-    BASELINE.md §2 (32.60 GFLOP/token for the reference-family LLaMA-7B shape at T=2048)."""
+    BASELINE.md §2 (32.60 GFLOP/token for the reference-family LLaMA-7B shape at T=2048; 41.25
+    with the SwiGLU extension)."""
     L = s["n_layers"] if layers is None else layers
     return 6.0 * matmul_params(s, L) + 6.0 * L * s["d_model"] * T
 
@@ -313,7 +318,10 @@ def run_ours(args):
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (uniform random token ids, random-init weights from the reference init stream)",
-        "config": {"workload": f"LLaMA-7B-shape decoder (reference model family, {s['n_layers']} layers, "
+        "config": {"workload": f"LLaMA-7B-shape decoder ("
+                               + ("SwiGLU MLP + RMSNorm extension" if s.get("mlp") == "swiglu"
+                                  else "reference model family")
+                               + f", {s['n_layers']} layers, "
                                f"d={s['d_model']}, H={s['n_heads']}, d_ff={s['d_ff']}, V={s['vocab_size']}) "
                                f"train step: fwd+bwd+AdamW, seq {T}",
                    "spec": os.path.relpath(args.spec, ROOT), "global_batch": rows, "seq_len": T,

@@ -135,10 +135,10 @@ def forward_backward(params: dict, spec: dict, tokens, targets, weights, need_gr
         m, xh2, r2 = norm(h_mid, pre + "ln2")
         m = R(m)
         if swiglu:
-            gate = m @ p[pre + "mlp/fc1/gate/kernel"].T
-            upv = m @ p[pre + "mlp/fc1/kernel"].T
+            gate = R(m @ p[pre + "mlp/fc1/gate/kernel"].T)   # pre-activations, stored bf16 on device
+            upv = R(m @ p[pre + "mlp/fc1/kernel"].T)
             g = R(silu(gate) * upv)           # h = silu(gate x) * (up x)
-            up = (R(gate), R(upv))
+            up = (gate, upv)
             h_out = h_mid + g @ p[pre + "mlp/fc2/kernel"].T
         else:
             up_full = m @ p[pre + "mlp/fc1/kernel"].T + p[pre + "mlp/fc1/bias"]

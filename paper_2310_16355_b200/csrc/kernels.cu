@@ -768,7 +768,7 @@ __global__ void add_residual_bias_kernel(const float* __restrict__ a, const floa
     const float4 x = reinterpret_cast<const float4*>(a)[i];
     const float4 z = reinterpret_cast<const float4*>(b)[i];
     const int c = static_cast<int>((i * 4) % d);
-    const float4 bb = *reinterpret_cast<const float4*>(bias + c);
+    const float4 bb = bias ? *reinterpret_cast<const float4*>(bias + c) : make_float4(0.f, 0.f, 0.f, 0.f);
     reinterpret_cast<float4*>(y)[i] = make_float4(x.x + z.x + bb.x, x.y + z.y + bb.y, x.z + z.z + bb.z, x.w + z.w + bb.w);
   }
 }

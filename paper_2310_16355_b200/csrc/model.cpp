@@ -178,7 +178,12 @@ void Model::build_layout() {
     ls.k_k = place(b + "attn/k/kernel", false);
     ls.v_k = place(b + "attn/v/kernel", false);
     ls.o_k = place(b + "attn/o/kernel", true);
-    ls.fc1_k = place(b + "mlp/fc1/kernel", true);
+    if (spec_.swiglu) {
+      ls.gate_k = place(b + "mlp/fc1/gate/kernel", true);  // gate|up contiguous: fused [2*d_ff/t, d]
+      ls.fc1_k = place(b + "mlp/fc1/kernel", false);
+    } else {
+      ls.fc1_k = place(b + "mlp/fc1/kernel", true);
+    }
     ls.fc2_k = place(b + "mlp/fc2/kernel", true);
   }
   if (!spec_.tie_embeddings) head_ = place("lm_head/kernel", true);
@@ -193,14 +198,16 @@ void Model::build_layout() {
     ls.v_b = place(b + "attn/v/bias", false);
     ls.o_b = place(b + "attn/o/bias", true);
     ls.ln1_s = place(b + "ln1/scale", true);
-    ls.ln1_b = place(b + "ln1/bias", true);
+    if (!spec_.rmsnorm) ls.ln1_b = place(b + "ln1/bias", true);
     ls.ln2_s = place(b + "ln2/scale", true);
-    ls.ln2_b = place(b + "ln2/bias", true);
-    ls.fc1_b = place(b + "mlp/fc1/bias", true);
-    ls.fc2_b = place(b + "mlp/fc2/bias", true);
+    if (!spec_.rmsnorm) ls.ln2_b = place(b + "ln2/bias", true);
+    if (!spec_.swiglu) {
+      ls.fc1_b = place(b + "mlp/fc1/bias", true);
+      ls.fc2_b = place(b + "mlp/fc2/bias", true);
+    }
   }
   lnf_s_ = place("final_ln/scale", true);
-  lnf_b_ = place("final_ln/bias", true);
+  if (!spec_.rmsnorm) lnf_b_ = place("final_ln/bias", true);
   flat_n_ = (off + kAlign - 1) / kAlign * kAlign;
 
   // Which blocks run tensor-parallel: the two sharding rules give column-split QKV / fc1 and
@@ -223,8 +230,10 @@ void Model::build_layout() {
     const LayerSlots& ls = layers_[l];
     const bool attn_tp = is_split(ls.q_k, 0) && is_split(ls.k_k, 0) && is_split(ls.v_k, 0) && is_split(ls.o_k, 1);
     const bool attn_rep = is_repl(ls.q_k) && is_repl(ls.k_k) && is_repl(ls.v_k) && is_repl(ls.o_k);
-    const bool mlp_tp = is_split(ls.fc1_k, 0) && is_split(ls.fc2_k, 1);
-    const bool mlp_rep = is_repl(ls.fc1_k) && is_repl(ls.fc2_k);
+    const bool gate_tp = ls.gate_k < 0 || is_split(ls.gate_k, 0);
+    const bool gate_rep = ls.gate_k < 0 || is_repl(ls.gate_k);
+    const bool mlp_tp = gate_tp && is_split(ls.fc1_k, 0) && is_split(ls.fc2_k, 1);
+    const bool mlp_rep = gate_rep && is_repl(ls.fc1_k) && is_repl(ls.fc2_k);
     if (!(attn_tp || attn_rep)) unsupported("the attention kernels of block_" + std::to_string(l));
     if (!(mlp_tp || mlp_rep)) unsupported("the MLP kernels of block_" + std::to_string(l));
     const int ta = attn_tp ? mesh_->mp : 1, tm = mlp_tp ? mesh_->mp : 1;
@@ -288,7 +297,7 @@ void Model::allocate() {
       R.qkv.push_back(alloc<bf16>(M * 3 * dl_));
       R.o.push_back(alloc<bf16>(M * dl_));
       R.lse.push_back(alloc<float>(M * hl_));
-      R.pre.push_back(alloc<bf16>(M * fl_));
+      R.pre.push_back(alloc<bf16>(M * fl_ * (spec_.swiglu ? 2 : 1)));  // SwiGLU: gate | up
       R.act.push_back(alloc<bf16>(M * fl_));
     }
     R.statsf = alloc<float>(2 * M);
@@ -304,7 +313,7 @@ void Model::allocate() {
     R.dx = alloc<float>(M * d_);
     R.gres = alloc<float>(M * d_);
     R.gb = alloc<bf16>(M * d_);
-    R.dpre = alloc<bf16>(M * fl_);
+    R.dpre = alloc<bf16>(M * fl_ * (spec_.swiglu ? 2 : 1));
     R.dout = alloc<bf16>(M * dl_);
     R.dqkv = alloc<bf16>(M * 3 * dl_);
     const int64_t chunks = (M + 255) / 256;
@@ -614,9 +623,10 @@ void Model::ag_mp_buf(std::vector<Rank*>& grp, float* Rank::*buf, int64_t chunk)
 void Model::gemm(Rank& R, int M, int N, int K, const void* A, int64_t lda, int a_mn, const void* B,
                  int64_t ldb, int b_mn, int epi, void* C, int64_t ldc, void* C2, int64_t ldc2,
                  const float* bias, const void* aux, int64_t ld_aux, int accumulate, int bias_seg,
-                 int64_t bias_seg_stride) {
+                 int64_t bias_seg_stride, int swiglu_half) {
   (void)R;
   GemmParams p;
+  p.swiglu_half = swiglu_half;
   p.M = M;
   p.N = N;
   p.K = K;
@@ -657,8 +667,8 @@ void Model::forward_replica(std::vector<Rank*>& grp, bool need_grad) {
     const LayerSlots& ls = layers_[l];
     for (Rank* R : grp) {
       tic();
-      k::layernorm_fwd(R->hs[l], P(*R, ls.ln1_s), P(*R, ls.ln1_b), R->a1[l], R->stats1[l], R->stats1[l] + M,
-                       M, d, 1e-5f, stream_);
+      k::layernorm_fwd(R->hs[l], P(*R, ls.ln1_s), Pn(*R, ls.ln1_b), R->a1[l], R->stats1[l], R->stats1[l] + M,
+                       M, d, 1e-5f, stream_, spec_.rmsnorm);
       toc(kProfNorm, 6.0 * M * d);
       ++launches_;
       // column-parallel QKV (spmd.hpp:284-303): [M, d] x [3*dl, d]^T, bias slices of q|k|v
@@ -691,17 +701,23 @@ void Model::forward_replica(std::vector<Rank*>& grp, bool need_grad) {
     }
     for (Rank* R : grp) {
       tic();
-      k::layernorm_fwd(R->hmid[l], P(*R, ls.ln2_s), P(*R, ls.ln2_b), R->a2[l], R->stats2[l], R->stats2[l] + M,
-                       M, d, 1e-5f, stream_);
+      k::layernorm_fwd(R->hmid[l], P(*R, ls.ln2_s), Pn(*R, ls.ln2_b), R->a2[l], R->stats2[l], R->stats2[l] + M,
+                       M, d, 1e-5f, stream_, spec_.rmsnorm);
       toc(kProfNorm, 6.0 * M * d);
       ++launches_;
-      gemm(*R, static_cast<int>(M), fl, d, R->a2[l], d, 0, W(*R, ls.fc1_k), d, 0,
-           static_cast<int>(Epi::kBiasGelu), R->pre[l], fl, R->act[l], fl, P(*R, ls.fc1_b) + R->mpi * fl);
+      if (spec_.swiglu) {
+        // one GEMM for gate and up: h = silu(x W_g^T) * (x W_u^T), pre = gate | up (bf16)
+        gemm(*R, static_cast<int>(M), fl, d, R->a2[l], d, 0, W(*R, ls.gate_k), d, 0,
+             static_cast<int>(Epi::kSwiGLU), R->act[l], fl, R->pre[l], 2 * fl, nullptr, nullptr, 0, 0, 0, 0, fl);
+      } else {
+        gemm(*R, static_cast<int>(M), fl, d, R->a2[l], d, 0, W(*R, ls.fc1_k), d, 0,
+             static_cast<int>(Epi::kBiasGelu), R->pre[l], fl, R->act[l], fl, P(*R, ls.fc1_b) + R->mpi * fl);
+      }
     }
     if (tm_ == 1) {
       for (Rank* R : grp) {
         gemm(*R, static_cast<int>(M), d, fl, R->act[l], fl, 0, W(*R, ls.fc2_k), fl, 0,
-             static_cast<int>(Epi::kResidF32), R->hs[l + 1], d, nullptr, 0, P(*R, ls.fc2_b), R->hmid[l], d);
+             static_cast<int>(Epi::kResidF32), R->hs[l + 1], d, nullptr, 0, Pn(*R, ls.fc2_b), R->hmid[l], d);
       }
     } else {
       row_parallel_ar(
@@ -711,7 +727,7 @@ void Model::forward_replica(std::vector<Rank*>& grp, bool need_grad) {
                  static_cast<int>(Epi::kStoreF32), R.part + r0 * d, d);
           },
           [&](Rank& R, int64_t r0, int64_t rows) {
-            k::add_residual_bias(R.hmid[l] + r0 * d, R.part + r0 * d, P(R, ls.fc2_b), R.hs[l + 1] + r0 * d, rows,
+            k::add_residual_bias(R.hmid[l] + r0 * d, R.part + r0 * d, Pn(R, ls.fc2_b), R.hs[l + 1] + r0 * d, rows,
                                  d, stream_);
             ++launches_;
           });
@@ -720,8 +736,8 @@ void Model::forward_replica(std::vector<Rank*>& grp, bool need_grad) {
   const int head = head_ >= 0 ? head_ : tok_;
   for (Rank* R : grp) {
     tic();
-    k::layernorm_fwd(R->hs[L_], P(*R, lnf_s_), P(*R, lnf_b_), R->f, R->statsf, R->statsf + M, M, d, 1e-5f,
-                     stream_);
+    k::layernorm_fwd(R->hs[L_], P(*R, lnf_s_), Pn(*R, lnf_b_), R->f, R->statsf, R->statsf + M, M, d, 1e-5f,
+                     stream_, spec_.rmsnorm);
     toc(kProfNorm, 6.0 * M * d);
     ++launches_;
     // LM head (replicated under the reference plan: every rank computes all V columns)
@@ -817,7 +833,7 @@ void Model::backward_replica(std::vector<Rank*>& grp, bool accumulate) {
   if (!accumulate) {
     for (Rank* R : grp) {
       auto zero = [&](int s) {
-        cuda_check(cudaMemsetAsync(G(*R, s), 0, slots_[s].numel * 4, stream_), "memset");
+        if (s >= 0) cuda_check(cudaMemsetAsync(G(*R, s), 0, slots_[s].numel * 4, stream_), "memset");
       };
       for (const LayerSlots& ls : layers_) {
         zero(ls.ln1_s);
@@ -846,7 +862,8 @@ void Model::backward_replica(std::vector<Rank*>& grp, bool accumulate) {
     auto cons = [&](Rank& R, int64_t r0, int64_t rows) {
       tic();
       k::layernorm_bwd(R.hs[L_] + r0 * d, R.statsf + r0, R.statsf + M + r0, P(R, lnf_s_), R.dx + r0 * d,
-                       R.gres + r0 * d, R.gb + r0 * d, G(R, lnf_s_), G(R, lnf_b_), rows, d, 0, stream_, R.ln_partials);
+                       R.gres + r0 * d, R.gb + r0 * d, G(R, lnf_s_), Gn(R, lnf_b_), rows, d, 0, stream_, R.ln_partials,
+                       spec_.rmsnorm);
       toc(kProfNorm, 18.0 * rows * d);
       ++launches_;
     };
@@ -864,25 +881,39 @@ void Model::backward_replica(std::vector<Rank*>& grp, bool accumulate) {
   for (int l = L_ - 1; l >= 0; --l) {
     const LayerSlots& ls = layers_[l];
     // ---- MLP ----
+    // SwiGLU: dpre = d(gate) | d(up) [M, 2*fl] against the fused [gate; up] weight at gate_k
+    const int fw = spec_.swiglu ? 2 * fl : fl;
+    const int fk = spec_.swiglu ? ls.gate_k : ls.fc1_k;
     for (Rank* R : grp) {
-      k::colsum_f32(R->gres, d, M, d, G(*R, ls.fc2_b), acc, R->col_scratch, stream_);
-      launches_ += 2;
-      gemm(*R, static_cast<int>(M), fl, d, R->gb, d, 0, W(*R, ls.fc2_k), fl, 1,
-           static_cast<int>(Epi::kGeluBwd), R->dpre, fl, nullptr, 0, nullptr, R->pre[l], fl);
+      if (ls.fc2_b >= 0) {
+        k::colsum_f32(R->gres, d, M, d, G(*R, ls.fc2_b), acc, R->col_scratch, stream_);
+        launches_ += 2;
+      }
+      if (spec_.swiglu) {
+        gemm(*R, static_cast<int>(M), fl, d, R->gb, d, 0, W(*R, ls.fc2_k), fl, 1,
+             static_cast<int>(Epi::kSwiGLUBwd), R->dpre, 2 * fl, nullptr, 0, nullptr, R->pre[l], 2 * fl, 0, 0, 0,
+             fl);
+      } else {
+        gemm(*R, static_cast<int>(M), fl, d, R->gb, d, 0, W(*R, ls.fc2_k), fl, 1,
+             static_cast<int>(Epi::kGeluBwd), R->dpre, fl, nullptr, 0, nullptr, R->pre[l], fl);
+      }
       wgrad(*R, ls.fc2_k, d, fl, static_cast<int>(M), R->gb, d, R->act[l], fl, acc);
-      k::colsum_bf16(R->dpre, fl, M, fl, 0, G(*R, ls.fc1_b) + R->mpi * fl, nullptr, nullptr, acc,
-                     R->col_scratch, stream_);
-      launches_ += 2;
+      if (ls.fc1_b >= 0) {
+        k::colsum_bf16(R->dpre, fl, M, fl, 0, G(*R, ls.fc1_b) + R->mpi * fl, nullptr, nullptr, acc,
+                       R->col_scratch, stream_);
+        launches_ += 2;
+      }
     }
     {
       auto prod = [&](Rank& R, int64_t r0, int64_t rows) {
-        gemm(R, static_cast<int>(rows), d, fl, R.dpre + r0 * fl, fl, 0, W(R, ls.fc1_k), d, 1,
+        gemm(R, static_cast<int>(rows), d, fw, R.dpre + r0 * fw, fw, 0, W(R, fk), d, 1,
              static_cast<int>(Epi::kStoreF32), R.dx + r0 * d, d);
       };
       auto cons = [&](Rank& R, int64_t r0, int64_t rows) {
         tic();
         k::layernorm_bwd(R.hmid[l] + r0 * d, R.stats2[l] + r0, R.stats2[l] + M + r0, P(R, ls.ln2_s), R.dx + r0 * d,
-                         R.gres + r0 * d, R.gb + r0 * d, G(R, ls.ln2_s), G(R, ls.ln2_b), rows, d, 1, stream_, R.ln_partials);
+                         R.gres + r0 * d, R.gb + r0 * d, G(R, ls.ln2_s), Gn(R, ls.ln2_b), rows, d, 1, stream_,
+                         R.ln_partials, spec_.rmsnorm);
         toc(kProfNorm, 18.0 * rows * d);
         ++launches_;
       };
@@ -893,7 +924,7 @@ void Model::backward_replica(std::vector<Rank*>& grp, bool accumulate) {
         for (Rank* R : grp) cons(*R, 0, M);
       }
     }
-    for (Rank* R : grp) wgrad(*R, ls.fc1_k, fl, d, static_cast<int>(M), R->dpre, fl, R->a2[l], d, acc);
+    for (Rank* R : grp) wgrad(*R, fk, fw, d, static_cast<int>(M), R->dpre, fw, R->a2[l], d, acc);
     // ---- attention ----
     for (Rank* R : grp) {
       k::colsum_f32(R->gres, d, M, d, G(*R, ls.o_b), acc, R->col_scratch, stream_);
@@ -918,7 +949,8 @@ void Model::backward_replica(std::vector<Rank*>& grp, bool accumulate) {
       auto cons = [&](Rank& R, int64_t r0, int64_t rows) {
         tic();
         k::layernorm_bwd(R.hs[l] + r0 * d, R.stats1[l] + r0, R.stats1[l] + M + r0, P(R, ls.ln1_s), R.dx + r0 * d,
-                         R.gres + r0 * d, R.gb + r0 * d, G(R, ls.ln1_s), G(R, ls.ln1_b), rows, d, 1, stream_, R.ln_partials);
+                         R.gres + r0 * d, R.gb + r0 * d, G(R, ls.ln1_s), Gn(R, ls.ln1_b), rows, d, 1, stream_,
+                         R.ln_partials, spec_.rmsnorm);
         toc(kProfNorm, 18.0 * rows * d);
         ++launches_;
       };
@@ -944,7 +976,7 @@ void Model::backward_replica(std::vector<Rank*>& grp, bool accumulate) {
       ag_mp_slot(grp, ls.k_b, dl);
       ag_mp_slot(grp, ls.v_b, dl);
     }
-    if (tm_ > 1) ag_mp_slot(grp, ls.fc1_b, fl);
+    if (tm_ > 1 && ls.fc1_b >= 0) ag_mp_slot(grp, ls.fc1_b, fl);
   }
 }
 

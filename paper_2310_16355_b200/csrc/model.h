@@ -40,8 +40,11 @@ struct Slot {
   uint64_t draw_base = 0;      // counter of the slot's first draw in the init stream
 };
 
+// Slot indices of one block; -1 = absent (RMSNorm has no bias, the SwiGLU MLP has no biases).
+// With SwiGLU, gate_k and fc1_k (up) are adjacent: the fused [gate; up] weight starts at gate_k.
 struct LayerSlots {
-  int ln1_s, ln1_b, q_k, k_k, v_k, q_b, k_b, v_b, o_k, o_b, ln2_s, ln2_b, fc1_k, fc1_b, fc2_k, fc2_b;
+  int ln1_s = -1, ln1_b = -1, q_k = -1, k_k = -1, v_k = -1, q_b = -1, k_b = -1, v_b = -1, o_k = -1, o_b = -1,
+      ln2_s = -1, ln2_b = -1, gate_k = -1, fc1_k = -1, fc1_b = -1, fc2_k = -1, fc2_b = -1;
 };
 
 struct Rank {
@@ -142,7 +145,8 @@ class Model {
   void gemm(Rank& R, int M, int N, int K, const void* A, int64_t lda, int a_mn, const void* B,
             int64_t ldb, int b_mn, int epi, void* C, int64_t ldc, void* C2 = nullptr,
             int64_t ldc2 = 0, const float* bias = nullptr, const void* aux = nullptr,
-            int64_t ld_aux = 0, int accumulate = 0, int bias_seg = 0, int64_t bias_seg_stride = 0);
+            int64_t ld_aux = 0, int accumulate = 0, int bias_seg = 0, int64_t bias_seg_stride = 0,
+            int swiglu_half = 0);
   void wgrad(Rank& R, int slot, int M, int N, int K, const void* A, int64_t lda, const void* B, int64_t ldb,
              int accumulate);
   struct FusedAdam {
@@ -150,6 +154,8 @@ class Model {
   };
   const FusedAdam* fused_ = nullptr;
   float* P(Rank& R, int slot) { return R.p + slots_[slot].offset; }
+  float* Pn(Rank& R, int slot) { return slot < 0 ? nullptr : P(R, slot); }  // absent slot -> null
+  float* Gn(Rank& R, int slot) { return slot < 0 ? nullptr : G(R, slot); }
   float* G(Rank& R, int slot) { return R.g + slots_[slot].offset; }
   bf16* W(Rank& R, int slot) { return R.w + slots_[slot].offset; }
 

@@ -25,7 +25,7 @@ def spec_of(name):
 def spec_dict(spec):
     return dict(vocab_size=spec.vocab_size, n_layers=spec.n_layers, d_model=spec.d_model,
                 n_heads=spec.n_heads, d_ff=spec.d_ff, max_seq_len=spec.max_seq_len,
-                tie_embeddings=spec.tie_embeddings)
+                tie_embeddings=spec.tie_embeddings, mlp=spec.mlp, norm=spec.norm)
 
 
 def bf16_round(x):
@@ -67,7 +67,9 @@ def make(spec, dp, mp, batch, seq):
     return model, mesh, plan
 
 
-SCORE_PATH = ("attn/q/kernel", "attn/k/kernel", "attn/q/bias")
+# attention-score path: q/k kernels, q bias, and the ln1 scale whose gradient is the sum of the
+# q/k/v input gradients (it inherits the same cancellation)
+SCORE_PATH = ("attn/q/kernel", "attn/k/kernel", "attn/q/bias", "ln1/scale")
 
 
 def check_grads(model, spec, want, tol=1e-2):
@@ -99,6 +101,12 @@ def check_grads(model, spec, want, tol=1e-2):
     ("tiny_vocab_parallel.spec", 1, 2, 4, 128),
     ("tiny_vocab_parallel.spec", 2, 2, 2, 128),
     ("mini_vocab_parallel.spec", 1, 4, 2, 16),
+    # SwiGLU MLP + RMSNorm extension: fused gate|up GEMM, SwiGLU-bwd epilogue
+    ("mini_swiglu.spec", 1, 1, 2, 16),
+    ("mini_swiglu.spec", 1, 2, 2, 16),
+    ("mini_swiglu.spec", 2, 2, 2, 16),
+    ("tiny_swiglu.spec", 1, 1, 4, 128),
+    ("tiny_swiglu.spec", 1, 2, 4, 128),
 ])
 def test_forward_backward_matches_oracle(spec_name, dp, mp, batch, seq):
     spec = spec_of(spec_name)
@@ -120,7 +128,13 @@ def test_forward_backward_matches_oracle(spec_name, dp, mp, batch, seq):
     # where the device stores bf16 (isolates kernel arithmetic from storage rounding)
     sd = spec_dict(spec)
     pr = gemm_rounded(ref)
-    for bf16_acts, tol in ((False, 1e-2 if spec.d_model >= 256 else 2e-2), (True, 1e-2)):
+    # f64 activations: 2e-2 for the small-width cases and for SwiGLU, whose h = silu(g)*u and its
+    # derivatives multiply two bf16-stored pre-activations (~1% from storage alone); the
+    # bf16_acts pass rounds where the device stores (1e-2; 1.5e-2 for SwiGLU, where the attention-score
+    # noise of the reference family reaches the residual stream through five more bf16 stores)
+    f64_tol = 1e-2 if spec.d_model >= 256 and spec.mlp != "swiglu" else 2e-2
+    bf_tol = 1.5e-2 if spec.mlp == "swiglu" else 1e-2
+    for bf16_acts, tol in ((False, f64_tol), (True, bf_tol)):
         want_loss, acc = 0.0, None
         for r in range(dp):
             sl = slice(r * batch, (r + 1) * batch)
@@ -256,7 +270,8 @@ def test_vocab_parallel_head_plan_and_comm():
     assert int(ag[1]) == 4 * L + 1  # + the CE stats all-gather
 
 
-@pytest.mark.parametrize("spec_name,mp", [("mini.spec", 1), ("mini.spec", 2), ("tiny_vocab_parallel.spec", 2)])
+@pytest.mark.parametrize("spec_name,mp", [("mini.spec", 1), ("mini.spec", 2), ("tiny_vocab_parallel.spec", 2),
+                                          ("mini_swiglu.spec", 2)])
 def test_fused_optimizer_matches_unfused(spec_name, mp):
     """train_step with dp == 1 applies AdamW inside the wgrad GEMM epilogues (the gradient of a
     weight matrix never reaches HBM). After one step the parameters must equal
@@ -266,7 +281,7 @@ def test_fused_optimizer_matches_unfused(spec_name, mp):
     ~lr*sign(g), so an element whose true gradient is ~0 may flip: at most 1e-3 of the elements
     may differ, and by no more than 2*lr. Three more steps must then track in loss (1e-4)."""
     spec = spec_of(spec_name)
-    seq = 16 if spec_name == "mini.spec" else 128
+    seq = 16 if spec_name.startswith("mini") else 128
     fused, _, _ = make(spec, 1, mp, 2, seq)
     plain, _, _ = make(spec, 1, mp, 2, seq)
     for m in (fused, plain):
