@@ -425,17 +425,17 @@ constexpr int P_STAGE_BYTES = P_A_STAGE + P_B_STAGE;
 // Optimizer-in-backward (Epi::kAdamW): p/m/v of the CTA's 128 rows x 32 columns are staged
 // by TMA one chunk ahead of the epilogue (double-buffered), updated in shared memory and written
 // back by TMA stores; the operand ring shrinks to 4 stages to make room.
-#ifndef SW_OPT_COLS
-#define SW_OPT_COLS 16
-#endif
-#ifndef SW_OPT_NBUF
-#define SW_OPT_NBUF 2
-#endif
-constexpr int OC = SW_OPT_COLS;           // columns per optimizer-state chunk (16 or 32)
-constexpr int OPT_NBUF = SW_OPT_NBUF;     // chunk buffers in flight
+// Optimizer-state chunks: 16 columns, one buffer per epilogue warpgroup (see the AdamW epilogue).
+constexpr int OC = 16;
+constexpr int OPT_NBUF = 2;
 constexpr int OPT_ARR = 128 * OC * 4;     // one array (p, m or v) of one chunk, 128 rows
 constexpr int OPT_BUF = 3 * OPT_ARR;      // p | m | v
 constexpr int OPT_WBOX = 32 * OC * 4;     // one warp's 32-row box of one array
+// The AdamW epilogue runs two epilogue warpgroups (warps 4-7 and 8-11) on alternate chunks.
+template <Epi EPI>
+constexpr int p_threads() {
+  return EPI == Epi::kAdamW ? 384 : NUM_THREADS;
+}
 template <Epi EPI>
 constexpr int p_stages() {
   return EPI == Epi::kAdamW ? (227 * 1024 - 1024 - 256 - OPT_NBUF * OPT_BUF) / P_STAGE_BYTES < 6
@@ -526,7 +526,7 @@ __device__ __forceinline__ void adamw_chunk_smem(const GemmParams& p, float* sbo
 }
 
 template <Epi EPI>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(p_threads<EPI>(), 1)
     gemm_bf16_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                          const __grid_constant__ OptMaps om, const GemmParams p) {
   constexpr int P_STAGES = p_stages<EPI>();
@@ -566,7 +566,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     }
     for (int a = 0; a < 2; ++a) {
       dev::mbar_init(&tfull[a], 1);
-      dev::mbar_init(&tempty[a], 8);
+      dev::mbar_init(&tempty[a], kOpt ? 16 : 8);  // epilogue warps of both CTAs
     }
     for (int a = 0; a < OPT_NBUF; ++a) {
       dev::mbar_init(&ofull[a], 1);
@@ -667,30 +667,75 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         dev::tma_prefetch_desc(&om.p);
         dev::tma_prefetch_desc(&om.m);
         dev::tma_prefetch_desc(&om.v);
-        int buf = 0;
-        uint32_t ph = 0;
+        uint32_t uses[OPT_NBUF] = {0, 0};
         for (int t = pair; t < num_tiles; t += npairs) {
           int mb, nb;
           tile_coords(t, num_m, num_n, mb, nb);
           const int r0 = mb * 2 * BM + static_cast<int>(rank) * BM;
           const int n_left = p.N - nb * BN;
-          for (int j = 0; j < BN / OC && j * OC < n_left; ++j) {
-            dev::mbar_wait(&oempty[buf], ph ^ 1);
+          // chunk c of the tile goes to buffer c & 1, i.e. to epilogue warpgroup c & 1
+          for (int c = 0; c < BN / OC && c * OC < n_left; ++c) {
+            const int buf = c & 1;
+            dev::mbar_wait(&oempty[buf], (uses[buf] & 1) ^ 1);
+            ++uses[buf];
             dev::mbar_arrive_expect_tx(&ofull[buf], OPT_BUF);
             uint8_t* dst = sOpt + buf * OPT_BUF;
-            const int c0 = nb * BN + j * OC;
+            const int c0 = nb * BN + c * OC;
 #pragma unroll
             for (int w = 0; w < 4; ++w) {
               dev::tma_load_2d(dst + w * OPT_WBOX, &om.p, &ofull[buf], c0, r0 + 32 * w);
               dev::tma_load_2d(dst + OPT_ARR + w * OPT_WBOX, &om.m, &ofull[buf], c0, r0 + 32 * w);
               dev::tma_load_2d(dst + 2 * OPT_ARR + w * OPT_WBOX, &om.v, &ofull[buf], c0, r0 + 32 * w);
             }
-            if (++buf == OPT_NBUF) {
-              buf = 0;
-              ph ^= 1;
-            }
           }
         }
+      }
+    }
+  } else if (kOpt && warp >= 4) {
+    // ---------------- AdamW epilogue: two warpgroups on alternate 16-column chunks ----------------
+    // Warpgroup wg (warps 4-7 / 8-11, the same TMEM lane quarters) owns chunks c = 2j + wg and
+    // the state buffer wg: one chunk per warpgroup in flight, so the latency-bound update of
+    // one overlaps the other's loads, math and TMA stores.
+    const uint32_t q = warp & 3;
+    const int wg = (static_cast<int>(warp) - 4) >> 2;
+    const uint32_t tempty_leader = dev::mapa_shared(dev::smem_u32(&tempty[0]), 0);
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    uint32_t uses = 0;
+    for (int t = pair; t < num_tiles; t += npairs) {
+      int mb, nb;
+      tile_coords(t, num_m, num_n, mb, nb);
+      const int row = mb * 2 * BM + static_cast<int>(rank) * BM + static_cast<int>(q) * 32 + static_cast<int>(lane);
+      dev::mbar_wait(&tfull[acc], acc_phase);
+      dev::tc_fence_after();
+#pragma unroll 1
+      for (int j = 0; j < BN / (2 * OC); ++j) {
+        const int col0 = nb * BN + (2 * j + wg) * OC;
+        if (col0 >= p.N) break;
+        uint32_t r[OC];
+        dev::tmem_ld_32x32b_x16(tmem_base + ((q * 32) << 16) + acc * BN + (2 * j + wg) * OC, r);
+        dev::tmem_ld_wait();
+        dev::mbar_wait(&ofull[wg], uses & 1);
+        ++uses;
+        float* sbox = reinterpret_cast<float*>(sOpt + wg * OPT_BUF) + q * (OPT_WBOX / 4);
+        adamw_chunk_smem(p, sbox, row, col0, min(OC, p.N - col0), r, lane);
+        dev::fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          const int rw = row - static_cast<int>(lane);
+          dev::tma_store_2d(&om.p, sbox, col0, rw);
+          dev::tma_store_2d(&om.m, sbox + OPT_ARR / 4, col0, rw);
+          dev::tma_store_2d(&om.v, sbox + OPT_ARR / 2, col0, rw);
+          dev::bulk_commit();
+          dev::bulk_wait_read();  // the stores have left shared memory: hand the buffer back
+          dev::mbar_arrive(&oempty[wg]);
+        }
+      }
+      dev::tc_fence_before();
+      if (lane == 0) dev::mbar_arrive_cluster(tempty_leader + acc * 8);
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
       }
     }
   } else if (warp >= 4) {
@@ -698,9 +743,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     const uint32_t tempty_leader = dev::mapa_shared(dev::smem_u32(&tempty[0]), 0);
     int acc = 0;
     uint32_t acc_phase = 0;
-    int obuf = 0;
-    uint32_t oph = 0;
-    int pending = -1;  // buffer whose TMA stores may still be reading shared memory (OPT_NBUF >= 3)
     for (int t = pair; t < num_tiles; t += npairs) {
       int mb, nb;
       tile_coords(t, num_m, num_n, mb, nb);
@@ -753,41 +795,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         uint32_t r[32];
         dev::tmem_ld_32x32b_x32(tmem_base + ((q * 32) << 16) + acc * BN + j * 32, r);
         dev::tmem_ld_wait();
-        if constexpr (kOpt) {
-#pragma unroll
-          for (int h = 0; h < 32 / OC; ++h) {
-            const int col0 = nb * BN + j * 32 + h * OC;
-            if (col0 >= p.N) break;
-            dev::mbar_wait(&ofull[obuf], oph);
-            float* sbox = reinterpret_cast<float*>(sOpt + obuf * OPT_BUF) + q * (OPT_WBOX / 4);
-            adamw_chunk_smem(p, sbox, row, col0, min(OC, p.N - col0), r + h * OC, lane);
-            dev::fence_proxy_async_smem();
-            __syncwarp();
-            if (lane == 0) {
-              const int rw = row - static_cast<int>(lane);
-              dev::tma_store_2d(&om.p, sbox, col0, rw);
-              dev::tma_store_2d(&om.m, sbox + OPT_ARR / 4, col0, rw);
-              dev::tma_store_2d(&om.v, sbox + OPT_ARR / 2, col0, rw);
-              dev::bulk_commit();
-              if (OPT_NBUF >= 3) {
-                // hand back the previous chunk's buffer once its stores have read it; this
-                // chunk's stores stay in flight while the next chunk is computed
-                if (pending >= 0) {
-                  dev::bulk_wait_read_1();
-                  dev::mbar_arrive(&oempty[pending]);
-                }
-              } else {
-                dev::bulk_wait_read();  // the stores have left shared memory: hand the buffer back
-                dev::mbar_arrive(&oempty[obuf]);
-              }
-            }
-            pending = obuf;
-            if (++obuf == OPT_NBUF) {
-              obuf = 0;
-              oph ^= 1;
-            }
-          }
-        } else if (row < p.M) {
+        if (row < p.M) {
           epilogue_chunk<EPI>(p, row, nb * BN + j * 32, ncols, r);
         }
       }
@@ -835,7 +843,7 @@ cudaError_t launch_2sm(const GemmParams& p, cudaStream_t stream) {
     om.m = make_tmap_f32_2d(p.adam_m, p.N, p.M, p.ldc, OC, 32);
     om.v = make_tmap_f32_2d(p.adam_v, p.N, p.M, p.ldc, OC, 32);
   }
-  gemm_bf16_2sm_kernel<EPI><<<grid, NUM_THREADS, p_smem_bytes<EPI>(), stream>>>(ta, tb, om, p);
+  gemm_bf16_2sm_kernel<EPI><<<grid, p_threads<EPI>(), p_smem_bytes<EPI>(), stream>>>(ta, tb, om, p);
   return cudaGetLastError();
 }
 
