@@ -205,6 +205,13 @@ SW_API sw_status sw_model_read_profile(sw_model* model, double ms[8], double wor
 /* Bytes of device memory held by this process's model state and activations. */
 SW_API sw_status sw_model_device_bytes(sw_model* model, int64_t* out);
 
+/* Greedy next-token generation: the Predictor loop of cli.cpp:425-447 (window of the last
+ * seq_len tokens, argmax at the newest position, kernels.hpp:515-527 first-maximum rule) for
+ * `batch` rows of P prompt tokens each, n_new tokens per row -> out [batch, n_new]. While the
+ * context fits the window each step runs one position through a KV cache; after that the window
+ * slides and is re-run with positions 0..seq_len-1, as the reference does. Replica 0's state. */
+SW_API sw_status sw_model_generate(sw_model* model, const int32_t* prompts, int P, int n_new, int32_t* out);
+
 /* ============================================================================================
  * SWCK train-state snapshots (checkpoint.hpp:18-28 format, byte-compatible with the reference)
  * ========================================================================================== */

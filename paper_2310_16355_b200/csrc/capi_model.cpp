@@ -247,6 +247,15 @@ std::vector<sw::CkptRng> rng_list(uint32_t n, const char* const* names, const ui
 
 extern "C" {
 
+sw_status sw_model_generate(sw_model* model, const int32_t* prompts, int P, int n_new, int32_t* out) {
+  return sw::guarded([&] {
+    require(model, "model");
+    require(prompts, "prompts");
+    require(out, "out");
+    model->model->generate(prompts, P, n_new, out);
+  });
+}
+
 sw_status sw_model_save_checkpoint(sw_model* model, const char* path, uint32_t n_rngs, const char* const* rng_names,
                                    const uint64_t* rng_seeds, const uint64_t* rng_stream_ids,
                                    const uint64_t* rng_counters) {

@@ -1,0 +1,197 @@
+// Greedy-decode kernels (the Predictor's next-token loop, cli.cpp:425-447,
+// with a KV cache instead of re-running the window): one new position per sequence per step.
+// HBM-bound (every step reads the weights and the cached keys/values once).
+#include <cfloat>
+
+#include "kernels.h"
+#include "sm100.cuh"
+
+namespace sw {
+namespace k {
+
+namespace {
+
+// x[b] = tok[ids[b]] + pos[p]   (model.hpp:92 embedding + learned position)
+__global__ void embed_rows_kernel(const int32_t* __restrict__ ids, const float* __restrict__ tok,
+                                  const float* __restrict__ pos, int p, float* __restrict__ x, int d) {
+  const int b = blockIdx.x;
+  const int64_t id = ids[b];
+  for (int c = threadIdx.x; c < d; c += blockDim.x) x[static_cast<int64_t>(b) * d + c] = tok[id * d + c] + pos[static_cast<int64_t>(p) * d + c];
+}
+
+// k | v of the new row b go to cache row b*T + p of the layer's qkv activations
+__global__ void kv_scatter_kernel(const bf16* __restrict__ src, bf16* __restrict__ cache, int T, int p, int dl) {
+  const int b = blockIdx.x;
+  const bf16* s = src + static_cast<int64_t>(b) * 3 * dl + dl;
+  bf16* t = cache + (static_cast<int64_t>(b) * T + p) * 3 * dl + dl;
+  for (int c = threadIdx.x * 8; c < 2 * dl; c += blockDim.x * 8) {
+    *reinterpret_cast<uint4*>(t + c) = *reinterpret_cast<const uint4*>(s + c);
+  }
+}
+
+// One CTA per (sequence, head): the new query against cached keys 0..p (causal), online softmax
+// per warp over a strided subset of keys, warps merged through shared memory. hd <= 256.
+template <int HDV>  // elements of the head dim held per lane (hd / 32)
+__global__ void __launch_bounds__(256) decode_attention_kernel(const bf16* __restrict__ qnew,
+                                                               const bf16* __restrict__ cache,
+                                                               bf16* __restrict__ out, int T, int p, int Hl,
+                                                               int hd, float scale_log2) {
+  constexpr int WARPS = 8;
+  __shared__ float sm_m[WARPS], sm_l[WARPS];
+  __shared__ float sm_o[WARPS][32 * HDV];
+  const int b = blockIdx.x / Hl, h = blockIdx.x % Hl;
+  const int dl = Hl * hd;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float q[HDV];
+  const bf16* qr = qnew + static_cast<int64_t>(b) * 3 * dl + h * hd;
+#pragma unroll
+  for (int i = 0; i < HDV; ++i) {
+    const int c = lane + 32 * i;
+    q[i] = c < hd ? __bfloat162float(qr[c]) * scale_log2 : 0.f;
+  }
+  float m = -INFINITY, l = 0.f, o[HDV];
+#pragma unroll
+  for (int i = 0; i < HDV; ++i) o[i] = 0.f;
+  for (int j = warp; j <= p; j += WARPS) {
+    const bf16* kr = cache + (static_cast<int64_t>(b) * T + j) * 3 * dl + dl + h * hd;
+    float s = 0.f;
+#pragma unroll
+    for (int i = 0; i < HDV; ++i) {
+      const int c = lane + 32 * i;
+      if (c < hd) s += q[i] * __bfloat162float(kr[c]);
+    }
+#pragma unroll
+    for (int x = 16; x > 0; x >>= 1) s += __shfl_xor_sync(0xffffffffu, s, x);
+    const float mn = fmaxf(m, s);
+    const float corr = dev::ex2_approx(m - mn), e = dev::ex2_approx(s - mn);
+    l = l * corr + e;
+    const bf16* vr = kr + dl;
+#pragma unroll
+    for (int i = 0; i < HDV; ++i) {
+      const int c = lane + 32 * i;
+      o[i] = o[i] * corr + (c < hd ? e * __bfloat162float(vr[c]) : 0.f);
+    }
+    m = mn;
+  }
+  if (lane == 0) {
+    sm_m[warp] = m;
+    sm_l[warp] = l;
+  }
+#pragma unroll
+  for (int i = 0; i < HDV; ++i) sm_o[warp][lane + 32 * i] = o[i];
+  __syncthreads();
+  if (warp == 0) {
+    float M = -INFINITY;
+    for (int w = 0; w < WARPS; ++w) M = fmaxf(M, sm_m[w]);
+    float L = 0.f, acc[HDV];
+#pragma unroll
+    for (int i = 0; i < HDV; ++i) acc[i] = 0.f;
+    for (int w = 0; w < WARPS; ++w) {
+      if (sm_m[w] == -INFINITY) continue;
+      const float f = dev::ex2_approx(sm_m[w] - M);
+      L += sm_l[w] * f;
+#pragma unroll
+      for (int i = 0; i < HDV; ++i) acc[i] += sm_o[w][lane + 32 * i] * f;
+    }
+    bf16* orow = out + static_cast<int64_t>(b) * dl + h * hd;
+#pragma unroll
+    for (int i = 0; i < HDV; ++i) {
+      const int c = lane + 32 * i;
+      if (c < hd) orow[c] = __float2bfloat16(acc[i] / L);
+    }
+  }
+}
+
+// First maximum of each row (kernels.hpp:515-527 semantics: strict > keeps the lowest index).
+// Writes (value, global index) as floats so ranks can combine shards.
+__global__ void argmax_rows_kernel(const bf16* __restrict__ x, int64_t row_stride, int n, int index_base,
+                                   float* __restrict__ out) {
+  const int b = blockIdx.x;
+  const bf16* xr = x + static_cast<int64_t>(b) * row_stride;
+  float best = -INFINITY;
+  int bi = 0x7fffffff;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const float v = __bfloat162float(xr[i]);
+    if (v > best || (v == best && i < bi)) {
+      best = v;
+      bi = i;
+    }
+  }
+  __shared__ float sv[32];
+  __shared__ int si[32];
+#pragma unroll
+  for (int x2 = 16; x2 > 0; x2 >>= 1) {
+    const float ov = __shfl_xor_sync(0xffffffffu, best, x2);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, x2);
+    if (ov > best || (ov == best && oi < bi)) {
+      best = ov;
+      bi = oi;
+    }
+  }
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) {
+    sv[w] = best;
+    si[w] = bi;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int k = 1; k < static_cast<int>(blockDim.x >> 5); ++k) {
+      if (sv[k] > best || (sv[k] == best && si[k] < bi)) {
+        best = sv[k];
+        bi = si[k];
+      }
+    }
+    out[2 * b] = best;
+    out[2 * b + 1] = static_cast<float>(index_base + bi);
+  }
+}
+
+// parts[r][b] = (value, index) of shard r; token[b] = index of the first maximum over shards
+// (shards hold ascending vocab ranges, so the lowest rank wins ties like the global argmax).
+__global__ void argmax_combine_kernel(const float* __restrict__ parts, int shards, int B, int32_t* __restrict__ tok) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  float best = -INFINITY;
+  int bi = 0;
+  for (int r = 0; r < shards; ++r) {
+    const float v = parts[(static_cast<int64_t>(r) * B + b) * 2];
+    if (v > best) {
+      best = v;
+      bi = static_cast<int>(parts[(static_cast<int64_t>(r) * B + b) * 2 + 1]);
+    }
+  }
+  tok[b] = bi;
+}
+
+}  // namespace
+
+void embed_rows(const int32_t* ids, const float* tok, const float* pos, int p, float* x, int B, int d, cudaStream_t s) {
+  embed_rows_kernel<<<B, 256, 0, s>>>(ids, tok, pos, p, x, d);
+}
+
+void kv_scatter(const bf16* qkv_new, bf16* cache, int B, int T, int p, int dl, cudaStream_t s) {
+  kv_scatter_kernel<<<B, 128, 0, s>>>(qkv_new, cache, T, p, dl);
+}
+
+void decode_attention(const bf16* qkv_new, const bf16* cache, bf16* out, int B, int T, int p, int Hl, int hd,
+                      cudaStream_t s) {
+  const float scale_log2 = static_cast<float>(1.4426950408889634 / sqrt(static_cast<double>(hd)));
+  if (hd <= 64) {
+    decode_attention_kernel<2><<<B * Hl, 256, 0, s>>>(qkv_new, cache, out, T, p, Hl, hd, scale_log2);
+  } else if (hd <= 128) {
+    decode_attention_kernel<4><<<B * Hl, 256, 0, s>>>(qkv_new, cache, out, T, p, Hl, hd, scale_log2);
+  } else {
+    decode_attention_kernel<8><<<B * Hl, 256, 0, s>>>(qkv_new, cache, out, T, p, Hl, hd, scale_log2);
+  }
+}
+
+void argmax_rows(const bf16* x, int64_t row_stride, int B, int n, int index_base, float* out, cudaStream_t s) {
+  argmax_rows_kernel<<<B, 256, 0, s>>>(x, row_stride, n, index_base, out);
+}
+
+void argmax_combine(const float* parts, int shards, int B, int32_t* tok, cudaStream_t s) {
+  argmax_combine_kernel<<<(B + 127) / 128, 128, 0, s>>>(parts, shards, B, tok);
+}
+
+}  // namespace k
+}  // namespace sw

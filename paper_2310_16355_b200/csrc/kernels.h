@@ -49,6 +49,14 @@ void colsum_f32(const float* X, int64_t ld, int64_t M, int N, float* out, int ac
                 float* scratch, cudaStream_t s);
 
 // sum of weights -> wsum[0]
+// Greedy decode (decode.cu): one new position per sequence.
+void embed_rows(const int32_t* ids, const float* tok, const float* pos, int p, float* x, int B, int d, cudaStream_t s);
+void kv_scatter(const bf16* qkv_new, bf16* cache, int B, int T, int p, int dl, cudaStream_t s);
+void decode_attention(const bf16* qkv_new, const bf16* cache, bf16* out, int B, int T, int p, int Hl, int hd,
+                      cudaStream_t s);
+void argmax_rows(const bf16* x, int64_t row_stride, int B, int n, int index_base, float* out, cudaStream_t s);
+void argmax_combine(const float* parts, int shards, int B, int32_t* tok, cudaStream_t s);
+
 void sum_f32(const float* x, int64_t n, float* out, cudaStream_t s);
 // Fused softmax cross entropy forward + backward over the vocab (kernels.hpp:327-363):
 // wloss[m] = w[m] * (logsumexp - logit[target]); logits <- (softmax - onehot) * w[m] / wsum.

@@ -1126,6 +1126,177 @@ bool Model::train_step(double lr, double b1, double b2, double eps, double wd) {
   return true;
 }
 
+// ---------------------------------------------------------------------------------------------
+// greedy generation
+// ---------------------------------------------------------------------------------------------
+void Model::pick_tokens(std::vector<Rank*>& grp, const std::vector<const bf16*>& rows, int64_t stride) {
+  const int B = B_;
+  for (size_t i = 0; i < grp.size(); ++i) {
+    Rank& R = *grp[i];
+    DecodeBufs& D = dec_[static_cast<size_t>(&R - ranks_.data())];
+    const int shard = th_ > 1 ? R.mpi : 0;
+    if (th_ > 1) cuda_check(cudaMemsetAsync(D.arg, 0, sizeof(float) * 2 * B * th_, stream_), "memset");
+    k::argmax_rows(rows[i], stride, B, vl_, shard * vl_, D.arg + static_cast<int64_t>(shard) * 2 * B, stream_);
+    ++launches_;
+  }
+  if (th_ > 1) {
+    std::vector<float*> ptrs;
+    for (Rank* R : grp) ptrs.push_back(dec_[static_cast<size_t>(R - ranks_.data())].arg);
+    ar_mp_ptrs(grp, ptrs, static_cast<int64_t>(2) * B * th_);  // all-gather by summing disjoint slots
+  }
+  for (Rank* R : grp) {
+    DecodeBufs& D = dec_[static_cast<size_t>(R - ranks_.data())];
+    k::argmax_combine(D.arg, th_, B, D.tok, stream_);
+    ++launches_;
+  }
+}
+
+void Model::window_forward(std::vector<Rank*>& grp, const std::vector<std::vector<int32_t>>& ctx, int take) {
+  // the reference's window (cli.cpp:435-440): the last `take` context tokens at positions
+  // 0..take-1, zeros after; the causal mask keeps the padding out of position take-1
+  std::vector<int32_t> win(static_cast<size_t>(M_), 0);
+  for (int b = 0; b < B_; ++b) {
+    const std::vector<int32_t>& c = ctx[static_cast<size_t>(b)];
+    for (int j = 0; j < take; ++j) win[static_cast<size_t>(b) * T_ + j] = c[c.size() - take + j];
+  }
+  for (Rank* R : grp) {
+    cuda_check(cudaMemcpyAsync(R->tokens, win.data(), M_ * 4, cudaMemcpyHostToDevice, stream_), "H2D");
+    cuda_check(cudaMemsetAsync(R->targets, 0, M_ * 4, stream_), "memset");
+    k::fill_f32(R->weights, M_, 1.0f, stream_);
+    ++launches_;
+  }
+  forward_replica(grp, false);
+  std::vector<const bf16*> rows;
+  for (Rank* R : grp) rows.push_back(R->logits + static_cast<int64_t>(take - 1) * ldv_);
+  pick_tokens(grp, rows, static_cast<int64_t>(T_) * ldv_);
+}
+
+void Model::decode_step(std::vector<Rank*>& grp, int p) {
+  const int B = B_, d = d_, dl = dl_, fl = fl_;
+  for (Rank* R : grp) {
+    DecodeBufs& D = dec_[static_cast<size_t>(R - ranks_.data())];
+    k::embed_rows(D.tok, P(*R, tok_), P(*R, pos_), p, D.x, B, d, stream_);
+    ++launches_;
+  }
+  auto each = [&](auto&& fn) {
+    for (Rank* R : grp) fn(*R, dec_[static_cast<size_t>(R - ranks_.data())]);
+  };
+  auto reduce = [&](float* DecodeBufs::*buf, int64_t n) {
+    std::vector<float*> ptrs;
+    for (Rank* R : grp) ptrs.push_back(dec_[static_cast<size_t>(R - ranks_.data())].*buf);
+    ar_mp_ptrs(grp, ptrs, n);
+  };
+  for (int l = 0; l < L_; ++l) {
+    const LayerSlots& ls = layers_[l];
+    each([&](Rank& R, DecodeBufs& D) {
+      k::layernorm_fwd(D.x, P(R, ls.ln1_s), Pn(R, ls.ln1_b), D.a, D.stats, D.stats + B, B, d, 1e-5f, stream_,
+                       spec_.rmsnorm);
+      ++launches_;
+      gemm(R, B, 3 * dl, d, D.a, d, 0, W(R, ls.q_k), d, 0, static_cast<int>(Epi::kStoreBf16), D.qkv, 3 * dl, nullptr,
+           0, P(R, ls.q_b) + R.mpi * dl, nullptr, 0, 0, dl, d);
+      k::kv_scatter(D.qkv, R.qkv[l], B, T_, p, dl, stream_);
+      k::decode_attention(D.qkv, R.qkv[l], D.o, B, T_, p, hl_, hd_, stream_);
+      launches_ += 2;
+      if (ta_ == 1) {
+        gemm(R, B, d, dl, D.o, dl, 0, W(R, ls.o_k), dl, 0, static_cast<int>(Epi::kResidF32), D.xmid, d, nullptr, 0,
+             P(R, ls.o_b), D.x, d);
+      } else {
+        gemm(R, B, d, dl, D.o, dl, 0, W(R, ls.o_k), dl, 0, static_cast<int>(Epi::kStoreF32), D.part, d);
+      }
+    });
+    if (ta_ > 1) {
+      reduce(&DecodeBufs::part, static_cast<int64_t>(B) * d);
+      each([&](Rank& R, DecodeBufs& D) {
+        k::add_residual_bias(D.x, D.part, P(R, ls.o_b), D.xmid, B, d, stream_);
+        ++launches_;
+      });
+    }
+    each([&](Rank& R, DecodeBufs& D) {
+      k::layernorm_fwd(D.xmid, P(R, ls.ln2_s), Pn(R, ls.ln2_b), D.a, D.stats, D.stats + B, B, d, 1e-5f, stream_,
+                       spec_.rmsnorm);
+      ++launches_;
+      if (spec_.swiglu) {
+        gemm(R, B, fl, d, D.a, d, 0, W(R, ls.gate_k), d, 0, static_cast<int>(Epi::kSwiGLU), D.h, fl, D.pre, 2 * fl,
+             nullptr, nullptr, 0, 0, 0, 0, fl);
+      } else {
+        gemm(R, B, fl, d, D.a, d, 0, W(R, ls.fc1_k), d, 0, static_cast<int>(Epi::kBiasGelu), D.pre, fl, D.h, fl,
+             P(R, ls.fc1_b) + R.mpi * fl);
+      }
+      if (tm_ == 1) {
+        gemm(R, B, d, fl, D.h, fl, 0, W(R, ls.fc2_k), fl, 0, static_cast<int>(Epi::kResidF32), D.x, d, nullptr, 0,
+             Pn(R, ls.fc2_b), D.xmid, d);
+      } else {
+        gemm(R, B, d, fl, D.h, fl, 0, W(R, ls.fc2_k), fl, 0, static_cast<int>(Epi::kStoreF32), D.part, d);
+      }
+    });
+    if (tm_ > 1) {
+      reduce(&DecodeBufs::part, static_cast<int64_t>(B) * d);
+      each([&](Rank& R, DecodeBufs& D) {
+        k::add_residual_bias(D.xmid, D.part, Pn(R, ls.fc2_b), D.x, B, d, stream_);
+        ++launches_;
+      });
+    }
+  }
+  const int head = head_ >= 0 ? head_ : tok_;
+  std::vector<const bf16*> rows;
+  each([&](Rank& R, DecodeBufs& D) {
+    k::layernorm_fwd(D.x, P(R, lnf_s_), Pn(R, lnf_b_), D.f, D.stats, D.stats + B, B, d, 1e-5f, stream_,
+                     spec_.rmsnorm);
+    ++launches_;
+    gemm(R, B, vl_, d, D.f, d, 0, W(R, head), d, 0, static_cast<int>(Epi::kStoreBf16), D.logits, ldv_);
+    rows.push_back(D.logits);
+  });
+  pick_tokens(grp, rows, ldv_);
+}
+
+void Model::generate(const int32_t* prompts, int P, int n_new, int32_t* out) {
+  if (P < 1 || P > T_) {
+    fail(SW_ERR_SHAPE, "generate: prompt length " + std::to_string(P) + " must be in [1, seq_len " +
+                           std::to_string(T_) + "]");
+  }
+  if (n_new < 1) fail(SW_ERR_CONFIG, "generate: n_new must be positive");
+  cuda_check(cudaSetDevice(mesh_->cuda_device), "cudaSetDevice");
+  if (dec_.empty()) {
+    const int64_t B = B_;
+    for (size_t i = 0; i < ranks_.size(); ++i) {
+      DecodeBufs D;
+      D.x = alloc<float>(B * d_);
+      D.xmid = alloc<float>(B * d_);
+      D.part = alloc<float>(B * d_);
+      D.stats = alloc<float>(2 * B);
+      D.arg = alloc<float>(2 * B * th_);
+      D.a = alloc<bf16>(B * d_);
+      D.qkv = alloc<bf16>(B * 3 * dl_);
+      D.o = alloc<bf16>(B * dl_);
+      D.pre = alloc<bf16>(B * 2 * fl_);
+      D.h = alloc<bf16>(B * fl_);
+      D.f = alloc<bf16>(B * d_);
+      D.logits = alloc<bf16>(B * ldv_);
+      D.tok = alloc<int32_t>(B);
+      dec_.push_back(D);
+    }
+  }
+  std::vector<Rank*> grp = replica(mesh_->emulated ? 0 : ranks_[0].dpi);
+  DecodeBufs& D0 = dec_[static_cast<size_t>(grp[0] - ranks_.data())];
+  std::vector<std::vector<int32_t>> ctx(static_cast<size_t>(B_));
+  for (int b = 0; b < B_; ++b) ctx[static_cast<size_t>(b)].assign(prompts + static_cast<int64_t>(b) * P, prompts + static_cast<int64_t>(b + 1) * P);
+  std::vector<int32_t> tok(static_cast<size_t>(B_));
+  for (int i = 0; i < n_new; ++i) {
+    const int len = static_cast<int>(ctx[0].size());  // context before this step's token
+    if (i == 0 || len > T_) {
+      window_forward(grp, ctx, len < T_ ? len : T_);  // prefill, or the sliding window
+    } else {
+      decode_step(grp, len - 1);  // the newest token sits at position len - 1
+    }
+    cuda_check(cudaMemcpyAsync(tok.data(), D0.tok, B_ * 4, cudaMemcpyDeviceToHost, stream_), "D2H");
+    cuda_check(cudaStreamSynchronize(stream_), "generate");
+    for (int b = 0; b < B_; ++b) {
+      out[static_cast<int64_t>(b) * n_new + i] = tok[static_cast<size_t>(b)];
+      ctx[static_cast<size_t>(b)].push_back(tok[static_cast<size_t>(b)]);
+    }
+  }
+}
+
 double Model::last_loss() {
   cuda_check(cudaStreamSynchronize(stream_), "sync");
   double sum = 0.0;

@@ -101,6 +101,12 @@ class Model {
   void save_checkpoint(const std::string& path, const std::vector<CkptRng>& rngs);
   void load_checkpoint(const std::string& path);
   const std::vector<CkptRng>& loaded_rngs() const { return loaded_rngs_; }
+  // Greedy next-token generation (the Predictor loop of cli.cpp:425-447): prompts [batch, P]
+  // (every row P tokens), n_new tokens per row into out [batch, n_new]. While the context fits
+  // the seq_len window the step runs one position through a KV cache (the layer's qkv
+  // activations); once it slides, the window is re-run with positions 0..T-1 exactly as the
+  // reference does.
+  void generate(const int32_t* prompts, int P, int n_new, int32_t* out);
   uint64_t step() const { return step_; }
   uint64_t seed() const { return seed_; }
   void get_tensor(const std::string& name, int which, float* full, int64_t numel);
@@ -191,6 +197,17 @@ class Model {
   int64_t bytes_ = 0;
   uint64_t step_ = 0;
   uint64_t seed_ = 0;
+  struct DecodeBufs {
+    float *x = nullptr, *xmid = nullptr, *part = nullptr, *stats = nullptr, *arg = nullptr;
+    bf16 *a = nullptr, *qkv = nullptr, *o = nullptr, *pre = nullptr, *h = nullptr, *f = nullptr, *logits = nullptr;
+    int32_t* tok = nullptr;
+  };
+  std::vector<DecodeBufs> dec_;  // per local rank, allocated on the first generate()
+  void decode_step(std::vector<Rank*>& grp, int p);
+  void window_forward(std::vector<Rank*>& grp, const std::vector<std::vector<int32_t>>& ctx, int take);
+  // argmax of one logits row per sequence (per-rank base pointer, row stride in elements) into
+  // every rank's dec_[].tok, combining vocab shards when the head is split
+  void pick_tokens(std::vector<Rank*>& grp, const std::vector<const bf16*>& rows, int64_t stride);
   std::vector<CkptRng> loaded_rngs_;
 };
 

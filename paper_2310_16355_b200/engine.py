@@ -57,6 +57,7 @@ def _declare():
     L.sw_model_load_checkpoint.argtypes = [vp, C.c_char_p, C.POINTER(C.c_uint32)]
     L.sw_model_checkpoint_rng.argtypes = [vp, C.c_uint32, C.c_char_p, C.c_uint64, u64p, u64p, u64p]
     L.sw_model_state_info.argtypes = [vp, u64p, u64p]
+    L.sw_model_generate.argtypes = [vp, vp, C.c_int, C.c_int, vp]
     for fn in ("sw_nccl_unique_id", "sw_mesh_create", "sw_mesh_comm_report",
                "sw_mesh_reset_comm_report", "sw_model_create", "sw_model_init_params",
                "sw_model_set_param", "sw_model_get_tensor", "sw_model_stage_batch",
@@ -65,7 +66,7 @@ def _declare():
                "sw_model_forward_logits", "sw_model_stream", "sw_model_launch_count",
                "sw_model_device_bytes", "sw_model_set_profiling", "sw_model_read_profile",
                "sw_model_save_checkpoint", "sw_model_load_checkpoint", "sw_model_checkpoint_rng",
-               "sw_model_state_info"):
+               "sw_model_state_info", "sw_model_generate"):
         getattr(L, fn).restype = C.c_int
     L._engine_declared = True
     return L
@@ -274,3 +275,14 @@ class Model:
         step, seed = C.c_uint64(), C.c_uint64()
         _lib.check(_declare().sw_model_state_info(self._h, C.byref(step), C.byref(seed)))
         return step.value, seed.value
+
+    # -- greedy generation (Predictor loop, cli.cpp:425-447) ------------------------------------
+    def generate(self, prompts, n_new: int) -> np.ndarray:
+        """prompts [batch, P] token ids -> [batch, n_new] greedy continuations (KV-cached while the
+        context fits seq_len, sliding window after, like the reference)."""
+        p = np.ascontiguousarray(prompts, dtype=np.int32)
+        if p.ndim != 2:
+            raise ValueError("prompts must be [batch, P]")
+        out = np.empty((p.shape[0], n_new), np.int32)
+        _lib.check(_declare().sw_model_generate(self._h, p.ctypes.data, p.shape[1], n_new, out.ctypes.data))
+        return out
