@@ -2,6 +2,7 @@
 // with a KV cache instead of re-running the window): one new position per sequence per step.
 // HBM-bound (every step reads the weights and the cached keys/values once).
 #include <cfloat>
+#include <stdexcept>
 
 #include "kernels.h"
 #include "sm100.cuh"
@@ -29,13 +30,94 @@ __global__ void kv_scatter_kernel(const bf16* __restrict__ src, bf16* __restrict
   }
 }
 
-// One CTA per (sequence, head): the new query against cached keys 0..p (causal), online softmax
-// per warp over a strided subset of keys, warps merged through shared memory. hd <= 256.
-template <int HDV>  // elements of the head dim held per lane (hd / 32)
+// One CTA per (sequence, head): the new query against cached keys 0..p (causal). Lanes work in
+// groups of G = hd/8 (8 head-dim elements each, 16-byte loads of k and v); a warp handles 32/G
+// keys per step with an online softmax per group; groups and warps merge through shared memory.
+template <int HD>
 __global__ void __launch_bounds__(256) decode_attention_kernel(const bf16* __restrict__ qnew,
                                                                const bf16* __restrict__ cache,
                                                                bf16* __restrict__ out, int T, int p, int Hl,
-                                                               int hd, float scale_log2) {
+                                                               float scale_log2) {
+  constexpr int G = HD / 8;          // lanes per key
+  constexpr int KPW = 32 / G;        // keys per warp step
+  constexpr int NG = 8 * KPW;        // groups per CTA
+  __shared__ float sm_m[NG], sm_l[NG];
+  __shared__ float sm_o[NG][HD];
+  const int b = blockIdx.x / Hl, h = blockIdx.x % Hl;
+  const int dl = Hl * HD;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int grp = lane / G, gl = lane % G;
+  const int gid = warp * KPW + grp;
+  float q[8];
+  {
+    const uint4 qv = *reinterpret_cast<const uint4*>(qnew + static_cast<int64_t>(b) * 3 * dl + h * HD + gl * 8);
+    const uint32_t qq[4] = {qv.x, qv.y, qv.z, qv.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float2 f = dev::unpack_bf16x2(qq[e]);
+      q[2 * e] = f.x * scale_log2;
+      q[2 * e + 1] = f.y * scale_log2;
+    }
+  }
+  float m = -INFINITY, l = 0.f, o[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) o[i] = 0.f;
+  // warp-uniform trip count (the shuffles need every lane); groups past p contribute nothing
+  for (int jb = warp * KPW; jb <= p; jb += NG) {
+    const int j = jb + grp;
+    const bool valid = j <= p;
+    const bf16* kr = cache + (static_cast<int64_t>(b) * T + (valid ? j : 0)) * 3 * dl + dl + h * HD + gl * 8;
+    const uint4 kv = *reinterpret_cast<const uint4*>(kr);
+    const uint4 vv = *reinterpret_cast<const uint4*>(kr + dl);
+    const uint32_t kk[4] = {kv.x, kv.y, kv.z, kv.w}, vw[4] = {vv.x, vv.y, vv.z, vv.w};
+    float s = 0.f;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float2 f = dev::unpack_bf16x2(kk[e]);
+      s = fmaf(q[2 * e], f.x, fmaf(q[2 * e + 1], f.y, s));
+    }
+#pragma unroll
+    for (int x = G / 2; x > 0; x >>= 1) s += __shfl_xor_sync(0xffffffffu, s, x);
+    if (!valid) continue;
+    const float mn = fmaxf(m, s);
+    const float corr = dev::ex2_approx(m - mn), e1 = dev::ex2_approx(s - mn);
+    l = l * corr + e1;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float2 f = dev::unpack_bf16x2(vw[e]);
+      o[2 * e] = o[2 * e] * corr + e1 * f.x;
+      o[2 * e + 1] = o[2 * e + 1] * corr + e1 * f.y;
+    }
+    m = mn;
+  }
+  if (gl == 0) {
+    sm_m[gid] = m;
+    sm_l[gid] = l;
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) sm_o[gid][gl * 8 + i] = o[i];
+  __syncthreads();
+  if (threadIdx.x < HD) {
+    const int c = threadIdx.x;
+    float M = -INFINITY;
+    for (int g = 0; g < NG; ++g) M = fmaxf(M, sm_m[g]);
+    float L = 0.f, acc = 0.f;
+    for (int g = 0; g < NG; ++g) {
+      if (sm_m[g] == -INFINITY) continue;
+      const float f = dev::ex2_approx(sm_m[g] - M);
+      L += sm_l[g] * f;
+      acc += sm_o[g][c] * f;
+    }
+    out[static_cast<int64_t>(b) * dl + h * HD + c] = __float2bfloat16(acc / L);
+  }
+}
+
+// Any head dim <= 256 (scalar loads): lane i holds head-dim elements i, i+32, ...
+template <int HDV>
+__global__ void __launch_bounds__(256) decode_attention_any_kernel(const bf16* __restrict__ qnew,
+                                                                   const bf16* __restrict__ cache,
+                                                                   bf16* __restrict__ out, int T, int p, int Hl,
+                                                                   int hd, float scale_log2) {
   constexpr int WARPS = 8;
   __shared__ float sm_m[WARPS], sm_l[WARPS];
   __shared__ float sm_o[WARPS][32 * HDV];
@@ -176,12 +258,19 @@ void kv_scatter(const bf16* qkv_new, bf16* cache, int B, int T, int p, int dl, c
 void decode_attention(const bf16* qkv_new, const bf16* cache, bf16* out, int B, int T, int p, int Hl, int hd,
                       cudaStream_t s) {
   const float scale_log2 = static_cast<float>(1.4426950408889634 / sqrt(static_cast<double>(hd)));
-  if (hd <= 64) {
-    decode_attention_kernel<2><<<B * Hl, 256, 0, s>>>(qkv_new, cache, out, T, p, Hl, hd, scale_log2);
-  } else if (hd <= 128) {
-    decode_attention_kernel<4><<<B * Hl, 256, 0, s>>>(qkv_new, cache, out, T, p, Hl, hd, scale_log2);
-  } else {
-    decode_attention_kernel<8><<<B * Hl, 256, 0, s>>>(qkv_new, cache, out, T, p, Hl, hd, scale_log2);
+  switch (hd) {
+    case 64: decode_attention_kernel<64><<<B * Hl, 256, 0, s>>>(qkv_new, cache, out, T, p, Hl, scale_log2); break;
+    case 128: decode_attention_kernel<128><<<B * Hl, 256, 0, s>>>(qkv_new, cache, out, T, p, Hl, scale_log2); break;
+    case 256: decode_attention_kernel<256><<<B * Hl, 256, 0, s>>>(qkv_new, cache, out, T, p, Hl, scale_log2); break;
+    default:
+      if (hd > 256) throw std::runtime_error("decode_attention: head_dim must be <= 256");
+      if (hd <= 64) {
+        decode_attention_any_kernel<2><<<B * Hl, 256, 0, s>>>(qkv_new, cache, out, T, p, Hl, hd, scale_log2);
+      } else if (hd <= 128) {
+        decode_attention_any_kernel<4><<<B * Hl, 256, 0, s>>>(qkv_new, cache, out, T, p, Hl, hd, scale_log2);
+      } else {
+        decode_attention_any_kernel<8><<<B * Hl, 256, 0, s>>>(qkv_new, cache, out, T, p, Hl, hd, scale_log2);
+      }
   }
 }
 

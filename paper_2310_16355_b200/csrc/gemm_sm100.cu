@@ -871,6 +871,112 @@ cudaError_t launch(const GemmParams& p, cudaStream_t stream) {
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------------------------
+// Small-M path (M <= 8, K-major operands): the decode step's GEMMs are weight-streaming GEMVs.
+// One CTA per 16 output columns streams those weight rows once (16-byte streaming loads; each
+// warp keeps two rows in flight) against the M activation rows (L1-resident), then hands the
+// chunk of every row to the same epilogue as the tensor-core kernel. HBM-bound by design.
+// ---------------------------------------------------------------------------------------------
+constexpr int GEMV_MAX_M = 8;
+constexpr int GEMV_COLS = 16;  // output columns per CTA (enough CTAs to cover the SMs at N = d_model)
+
+template <Epi EPI>
+__global__ void __launch_bounds__(256) gemv_bf16_kernel(const GemmParams p) {
+  __shared__ float sout[GEMV_MAX_M][2 * GEMV_COLS];
+  constexpr bool kGlu = EPI == Epi::kSwiGLU;
+  constexpr int ROWS = kGlu ? 2 * GEMV_COLS : GEMV_COLS;  // SwiGLU: the gate rows and the matching up rows
+  constexpr int RPW = ROWS / 8;                           // weight rows per warp, streamed together
+  const int K = p.K, M = p.M;
+  const int c0 = blockIdx.x * GEMV_COLS;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const __nv_bfloat16* w[RPW];
+  bool ok[RPW];
+#pragma unroll
+  for (int j = 0; j < RPW; ++j) {
+    const int rr = warp + 8 * j;
+    const int col = c0 + (rr % GEMV_COLS);
+    ok[j] = col < p.N;
+    const int wrow = kGlu ? (rr < GEMV_COLS ? col : p.swiglu_half + col) : col;
+    w[j] = reinterpret_cast<const __nv_bfloat16*>(p.B) + static_cast<int64_t>(ok[j] ? wrow : 0) * p.ldb;
+  }
+  float acc[RPW][GEMV_MAX_M];
+#pragma unroll
+  for (int j = 0; j < RPW; ++j)
+#pragma unroll
+    for (int m = 0; m < GEMV_MAX_M; ++m) acc[j][m] = 0.f;
+  const __nv_bfloat16* A = reinterpret_cast<const __nv_bfloat16*>(p.A);
+#pragma unroll 2
+  for (int k = lane * 8; k < K; k += 256) {
+    uint4 wv[RPW];
+#pragma unroll
+    for (int j = 0; j < RPW; ++j) wv[j] = __ldcs(reinterpret_cast<const uint4*>(w[j] + k));  // streamed once
+#pragma unroll
+    for (int m = 0; m < GEMV_MAX_M; ++m) {
+      if (m < M) {
+        const uint4 av = __ldg(reinterpret_cast<const uint4*>(A + static_cast<int64_t>(m) * p.lda + k));  // L1-resident
+        const uint32_t aa[4] = {av.x, av.y, av.z, av.w};
+#pragma unroll
+        for (int j = 0; j < RPW; ++j) {
+          const uint32_t ww[4] = {wv[j].x, wv[j].y, wv[j].z, wv[j].w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float2 a2 = dev::unpack_bf16x2(aa[e]), w2 = dev::unpack_bf16x2(ww[e]);
+            acc[j][m] = fmaf(a2.x, w2.x, fmaf(a2.y, w2.y, acc[j][m]));
+          }
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < RPW; ++j) {
+#pragma unroll
+    for (int m = 0; m < GEMV_MAX_M; ++m) {
+#pragma unroll
+      for (int x = 16; x > 0; x >>= 1) acc[j][m] += __shfl_xor_sync(0xffffffffu, acc[j][m], x);
+    }
+    if (lane == 0) {
+      const int rr = warp + 8 * j;
+      for (int m = 0; m < M; ++m) sout[m][rr] = acc[j][m];
+    }
+  }
+  __syncthreads();
+  const int ncols = min(GEMV_COLS, p.N - c0);
+  if (threadIdx.x < M) {
+    const int row = threadIdx.x;
+    if constexpr (kGlu) {
+      __nv_bfloat16* hrow = reinterpret_cast<__nv_bfloat16*>(p.C) + static_cast<int64_t>(row) * p.ldc + c0;
+      __nv_bfloat16* prow = reinterpret_cast<__nv_bfloat16*>(p.C2) + static_cast<int64_t>(row) * p.ldc2 + c0;
+      for (int c = 0; c < ncols; ++c) {
+        const float g = __bfloat162float(__float2bfloat16(sout[row][c]));
+        const float u = __bfloat162float(__float2bfloat16(sout[row][GEMV_COLS + c]));
+        prow[c] = __float2bfloat16(g);
+        prow[p.swiglu_half + c] = __float2bfloat16(u);
+        hrow[c] = __float2bfloat16(dev::silu(g) * u);
+      }
+    } else {
+      uint32_t r[32];
+#pragma unroll
+      for (int c = 0; c < 32; ++c) r[c] = __float_as_uint(c < GEMV_COLS ? sout[row][c] : 0.f);
+      epilogue_chunk<EPI>(p, row, c0, ncols, r);
+    }
+  }
+}
+
+template <Epi EPI>
+cudaError_t launch_gemv(const GemmParams& p, cudaStream_t stream) {
+  gemv_bf16_kernel<EPI><<<(p.N + GEMV_COLS - 1) / GEMV_COLS, 256, 0, stream>>>(p);
+  return cudaGetLastError();
+}
+
+// The small-M path applies to forward-layout GEMMs whose activations fit in shared memory.
+bool gemv_ok(const GemmParams& p) {
+  return p.M <= GEMV_MAX_M && !p.a_mn_major && !p.b_mn_major && p.K % 8 == 0 && p.lda % 8 == 0 &&
+         p.ldb % 8 == 0 &&
+         (p.epi == Epi::kStoreBf16 || p.epi == Epi::kStoreF32 || p.epi == Epi::kBiasGelu ||
+          p.epi == Epi::kResidF32 || p.epi == Epi::kSwiGLU) &&
+         !(p.epi == Epi::kStoreF32 && p.accumulate);
+}
+
 }  // namespace
 
 cudaError_t gemm_bf16(const GemmParams& p, cudaStream_t stream) {
@@ -880,6 +986,16 @@ cudaError_t gemm_bf16(const GemmParams& p, cudaStream_t stream) {
   }
   if (p.N % 8 != 0) throw std::runtime_error("gemm_bf16: N must be a multiple of 8");
   if (p.ldc % 8 != 0) throw std::runtime_error("gemm_bf16: ldc must be a multiple of 8");
+  if (gemv_ok(p)) {
+    switch (p.epi) {
+      case Epi::kStoreBf16: return launch_gemv<Epi::kStoreBf16>(p, stream);
+      case Epi::kStoreF32: return launch_gemv<Epi::kStoreF32>(p, stream);
+      case Epi::kBiasGelu: return launch_gemv<Epi::kBiasGelu>(p, stream);
+      case Epi::kResidF32: return launch_gemv<Epi::kResidF32>(p, stream);
+      case Epi::kSwiGLU: return launch_gemv<Epi::kSwiGLU>(p, stream);
+      default: break;
+    }
+  }
   switch (p.epi) {
     case Epi::kStoreBf16: return launch<Epi::kStoreBf16>(p, stream);
     case Epi::kStoreF32: return launch<Epi::kStoreF32>(p, stream);

@@ -198,3 +198,27 @@ def test_gemm_swiglu_fwd_bwd(M, N, K):
     want_g = dh * ub * sg * (1 + gb * (1 - sg))
     want_u = dh * torch.nn.functional.silu(gb)
     assert _rel(dpre[:, :N], want_g) < 1e-2 and _rel(dpre[:, N:], want_u) < 1e-2
+
+
+@pytest.mark.parametrize("M", [1, 3, 8])
+@pytest.mark.parametrize("epi", [0, 1, 3])
+def test_small_m_gemv_path(M, epi):
+    """M <= 8 forward GEMMs (the decode step) take the weight-streaming path; same epilogues."""
+    N, K = 200, 136
+    gen = torch.Generator(device=DEV).manual_seed(M * 10 + epi)
+    A, B, ref = _ref_operands(M, N, K, 0, 0, gen)
+    bias = torch.randn(N, generator=gen, device=DEV)
+    if epi == 0:
+        C = torch.empty(M, N, device=DEV, dtype=torch.bfloat16)
+        _gemm(A, 0, B, 0, M, N, K, 0, C, bias=bias)
+        want = ref + bias
+    elif epi == 1:
+        C = torch.full((M, N), float("nan"), device=DEV)
+        _gemm(A, 0, B, 0, M, N, K, 1, C)
+        want = ref
+    else:
+        aux = torch.randn(M, N, generator=gen, device=DEV)
+        C = torch.empty(M, N, device=DEV)
+        _gemm(A, 0, B, 0, M, N, K, 3, C, bias=bias, aux=aux)
+        want = aux + ref + bias
+    assert _rel(C, want) < (1e-2 if epi == 0 else 1e-5)

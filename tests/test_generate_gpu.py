@@ -32,32 +32,35 @@ def spec_dict(spec):
                 norm=spec.norm)
 
 
-def oracle_greedy(model, spec, prompts, n_new, seq):
+def oracle_check(model, spec, prompts, got, seq):
+    """Teacher-forced: at every step the f64 oracle runs the reference's window over the device's
+    own context and must pick the device's token unless its top two logits are within a few bf16
+    ulps (relative margin < 2%). Returns the number of decisive steps."""
     params = {n: model.get_param(n).astype(np.float64) for n in model.shapes}
     for n, v in params.items():  # the device's GEMMs read bf16 weights
         if v.ndim == 2 and not n.startswith("embed/"):
             params[n] = model_ref.bf16_round(v)
-    ctx = [list(r) for r in prompts]
-    toks, margins = [], []
-    for _ in range(n_new):
-        take = min(len(ctx[0]), seq)
-        win = np.zeros((len(ctx), seq), np.int64)
-        for b, c in enumerate(ctx):
-            win[b, :take] = c[-take:]
+    ctx = np.asarray(prompts)
+    decisive = 0
+    for i in range(got.shape[1]):
+        take = min(ctx.shape[1], seq)
+        win = np.zeros((ctx.shape[0], seq), np.int64)
+        win[:, :take] = ctx[:, -take:]
         _, _, logits = model_ref.forward_backward(params, spec_dict(spec), win, win, np.ones(win.shape),
                                                   need_grads=False)
         row = logits[:, take - 1]
-        nxt = row.argmax(-1)
         srt = np.sort(row, -1)
-        margins.append(srt[:, -1] - srt[:, -2])
-        toks.append(nxt)
-        for b in range(len(ctx)):
-            ctx[b].append(int(nxt[b]))
-    return np.stack(toks, 1), np.stack(margins, 1)
+        margin = (srt[:, -1] - srt[:, -2]) / np.maximum(np.abs(srt[:, -1]), 1.0)
+        for b in range(ctx.shape[0]):
+            if margin[b] >= 0.02:
+                assert got[b, i] == row[b].argmax(), (i, b, got[b, i], row[b].argmax(), margin[b])
+                decisive += 1
+        ctx = np.concatenate([ctx, got[:, i:i + 1]], 1)
+    return decisive
 
 
 @pytest.mark.parametrize("spec_name,mp", [("mini.spec", 1), ("mini.spec", 2), ("mini_vocab_parallel.spec", 2),
-                                          ("mini_swiglu.spec", 2)])
+                                          ("mini_swiglu.spec", 2), ("mini_hd64.spec", 1)])
 def test_kv_cached_greedy_matches_window_recompute_and_oracle(spec_name, mp):
     batch, seq, P, n_new = 2, 16, 5, 20  # 5 + 20 > 16: the last steps run the sliding window
     model, spec = build(spec_name, mp, batch, seq)
@@ -75,11 +78,8 @@ def test_kv_cached_greedy_matches_window_recompute_and_oracle(spec_name, mp):
     recompute = np.stack(recompute, 1)
     assert np.array_equal(got, recompute), (got, recompute)
 
-    want, margin = oracle_greedy(model, spec, prompts, n_new, seq)
-    # identical wherever the f64 oracle is not at a near-tie (bf16 weights/activations on device)
-    first_tie = np.argmax((margin < 0.05).any(0)) if (margin < 0.05).any() else n_new
-    assert np.array_equal(got[:, :first_tie], want[:, :first_tie]), (got, want, margin)
-    assert first_tie >= n_new // 2, margin
+    decisive = oracle_check(model, spec, prompts, got, seq)
+    assert decisive >= got.size // 2, decisive
 
 
 def test_generate_rejects_bad_prompts():
