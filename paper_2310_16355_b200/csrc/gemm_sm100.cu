@@ -878,14 +878,21 @@ cudaError_t launch(const GemmParams& p, cudaStream_t stream) {
 // chunk of every row to the same epilogue as the tensor-core kernel. HBM-bound by design.
 // ---------------------------------------------------------------------------------------------
 constexpr int GEMV_MAX_M = 8;
-constexpr int GEMV_COLS = 16;  // output columns per CTA (enough CTAs to cover the SMs at N = d_model)
+#ifndef SW_GEMV_COLS
+#define SW_GEMV_COLS 16  // >= 8 (16-byte bf16 stores in the epilogue)
+#endif
+#ifndef SW_GEMV_UNROLL
+#define SW_GEMV_UNROLL 2
+#endif
+constexpr int GEMV_UNROLL = SW_GEMV_UNROLL;
+constexpr int GEMV_COLS = SW_GEMV_COLS;  // output columns per CTA (enough CTAs to cover the SMs at N = d_model)
 
 template <Epi EPI>
 __global__ void __launch_bounds__(256) gemv_bf16_kernel(const GemmParams p) {
   __shared__ float sout[GEMV_MAX_M][2 * GEMV_COLS];
   constexpr bool kGlu = EPI == Epi::kSwiGLU;
   constexpr int ROWS = kGlu ? 2 * GEMV_COLS : GEMV_COLS;  // SwiGLU: the gate rows and the matching up rows
-  constexpr int RPW = ROWS / 8;                           // weight rows per warp, streamed together
+  constexpr int RPW = ROWS / 8 > 0 ? ROWS / 8 : 1;         // weight rows per warp, streamed together
   const int K = p.K, M = p.M;
   const int c0 = blockIdx.x * GEMV_COLS;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -905,7 +912,7 @@ __global__ void __launch_bounds__(256) gemv_bf16_kernel(const GemmParams p) {
 #pragma unroll
     for (int m = 0; m < GEMV_MAX_M; ++m) acc[j][m] = 0.f;
   const __nv_bfloat16* A = reinterpret_cast<const __nv_bfloat16*>(p.A);
-#pragma unroll 2
+#pragma unroll GEMV_UNROLL
   for (int k = lane * 8; k < K; k += 256) {
     uint4 wv[RPW];
 #pragma unroll
