@@ -905,9 +905,39 @@ __global__ void __launch_bounds__(512, 1)
   }
 }
 
-// delta[bh, q] = sum_c dO[q, c] * O[q, c] (one warp per row)
+// delta[bh, q] = sum_c dO[q, c] * O[q, c]: hd/8 lanes per (row, head), 16-byte loads
 __global__ void delta_kernel(const bf16* __restrict__ o, const bf16* __restrict__ dout, float* __restrict__ delta,
                              int T, int Hl, int hd, int64_t rows) {
+  const int lpr = hd / 8;  // lanes per (row, head): 16 at hd = 128
+  const int64_t item = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) / lpr;
+  const int sub = static_cast<int>(threadIdx.x % lpr);
+  const bool active = item < rows * Hl;
+  float s = 0.f;
+  if (active) {
+    const int64_t m = item / Hl;
+    const int h = static_cast<int>(item % Hl);
+    const int64_t off = m * (static_cast<int64_t>(Hl) * hd) + h * hd + sub * 8;
+    const uint4 a = *reinterpret_cast<const uint4*>(o + off);
+    const uint4 b = *reinterpret_cast<const uint4*>(dout + off);
+    const uint32_t aa[4] = {a.x, a.y, a.z, a.w}, bb[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float2 x = dev::unpack_bf16x2(aa[e]), y = dev::unpack_bf16x2(bb[e]);
+      s = fmaf(x.x, y.x, fmaf(x.y, y.y, s));
+    }
+  }
+  for (int x = lpr / 2; x > 0; x >>= 1) s += __shfl_xor_sync(0xffffffffu, s, x);
+  if (active && sub == 0) {
+    const int64_t m = item / Hl;
+    const int h = static_cast<int>(item % Hl);
+    const int64_t b2 = m / T, t = m % T;
+    delta[(b2 * Hl + h) * T + t] = s;
+  }
+}
+
+// scalar fallback for head dims that are not a multiple of 8 lanes' worth (one warp per row)
+__global__ void delta_any_kernel(const bf16* __restrict__ o, const bf16* __restrict__ dout, float* __restrict__ delta,
+                                 int T, int Hl, int hd, int64_t rows) {
   const int64_t wid = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (wid >= rows * Hl) return;
@@ -925,6 +955,16 @@ __global__ void delta_kernel(const bf16* __restrict__ o, const bf16* __restrict_
   if (lane == 0) {
     const int64_t b = m / T, t = m % T;
     delta[(b * Hl + h) * T + t] = s;
+  }
+}
+
+void launch_delta(const bf16* o, const bf16* dout, float* delta, int T, int Hl, int hd, int64_t M, cudaStream_t s) {
+  if (hd % 8 == 0 && hd / 8 <= 32 && (hd / 8 & (hd / 8 - 1)) == 0) {
+    const int64_t threads = M * Hl * (hd / 8);
+    delta_kernel<<<static_cast<unsigned>((threads + 255) / 256), 256, 0, s>>>(o, dout, delta, T, Hl, hd, M);
+  } else {
+    const int64_t warps = M * Hl;
+    delta_any_kernel<<<static_cast<unsigned>((warps * 32 + 255) / 256), 256, 0, s>>>(o, dout, delta, T, Hl, hd, M);
   }
 }
 
@@ -965,8 +1005,7 @@ bool launch_bwd2(const bf16* qkv, const bf16* o, const float* lse, const bf16* d
   float* delta = scratch;
   float* dq = scratch + ((M * Hl + 63) / 64) * 64;
   cudaMemsetAsync(dq, 0, sizeof(float) * M * Dl, s);
-  const int64_t warps = M * Hl;
-  delta_kernel<<<static_cast<unsigned>((warps * 32 + 255) / 256), 256, 0, s>>>(o, dout, delta, T, Hl, HD, M);
+  launch_delta(o, dout, delta, T, Hl, HD, M, s);
   const CUtensorMap tm_qkv64 = make_tmap_bf16_2d(qkv, 3ull * Dl, static_cast<uint64_t>(M), 3ull * Dl, 64, BQ2);
   const CUtensorMap tm_qkv128 = make_tmap_bf16_2d(qkv, 3ull * Dl, static_cast<uint64_t>(M), 3ull * Dl, 64, 128);
   const CUtensorMap tm_do64 = make_tmap_bf16_2d(dout, static_cast<uint64_t>(Dl), static_cast<uint64_t>(M),
@@ -1000,8 +1039,7 @@ bool launch_bwd(const bf16* qkv, const bf16* o, const float* lse, const bf16* do
   float* delta = scratch;
   float* dq = scratch + ((M * Hl + 63) / 64) * 64;
   cudaMemsetAsync(dq, 0, sizeof(float) * M * Dl, s);
-  const int64_t warps = M * Hl;
-  delta_kernel<<<static_cast<unsigned>((warps * 32 + 255) / 256), 256, 0, s>>>(o, dout, delta, T, Hl, HD, M);
+  launch_delta(o, dout, delta, T, Hl, HD, M, s);
   const CUtensorMap tm_qkv = make_tmap_bf16_2d(qkv, 3ull * Dl, static_cast<uint64_t>(M), 3ull * Dl, 64, 128);
   const CUtensorMap tm_do = make_tmap_bf16_2d(dout, static_cast<uint64_t>(Dl), static_cast<uint64_t>(M),
                                               static_cast<uint64_t>(Dl), 64, 128);

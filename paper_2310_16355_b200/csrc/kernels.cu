@@ -445,16 +445,26 @@ __global__ void __launch_bounds__(THREADS, 2) ln_bwd2_kernel(
 
 
 
-// dscale[c] += sum_b partials[b][0][c], dbias[c] += sum_b partials[b][1][c], b ascending.
+// dscale[c] += sum_b partials[b][0][c], dbias[c] += sum_b partials[b][1][c]: four interleaved
+// accumulators (b mod 4) combined in a fixed order -- deterministic, and four loads in flight.
 __global__ void ln_param_reduce_kernel(const float* __restrict__ partials, int nblk, int d, float* __restrict__ dscale,
                                        float* __restrict__ dbias) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= 2 * d) return;
   const int which = c / d, col = c - which * d;
-  float s = 0.f;
-  for (int b = 0; b < nblk; ++b) s += partials[static_cast<int64_t>(b) * 2 * d + which * d + col];
+  const float* src = partials + which * d + col;
+  const int64_t stride = 2LL * d;
+  float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+  int b = 0;
+  for (; b + 3 < nblk; b += 4) {
+    s0 += src[(b + 0) * stride];
+    s1 += src[(b + 1) * stride];
+    s2 += src[(b + 2) * stride];
+    s3 += src[(b + 3) * stride];
+  }
+  for (; b < nblk; ++b) s0 += src[b * stride];
   float* o = which == 0 ? dscale : dbias;
-  if (o != nullptr) o[col] += s;
+  if (o != nullptr) o[col] += (s0 + s1) + (s2 + s3);
 }
 
 __global__ void ln_bwd_generic_kernel(const float* __restrict__ x, const float* __restrict__ mean,
@@ -966,8 +976,8 @@ void layernorm_bwd(const float* x, const float* mean, const float* rstd, const f
     return;
   }
   if (partials != nullptr) {
-    ln_param_reduce_kernel<<<static_cast<unsigned>((2 * d + 255) / 256), 256, 0, s>>>(partials, static_cast<int>(nblk),
-                                                                                     d, dscale, dbias);
+    ln_param_reduce_kernel<<<static_cast<unsigned>((2 * d + 63) / 64), 64, 0, s>>>(partials, static_cast<int>(nblk), d,
+                                                                                  dscale, dbias);
   }
 }
 
