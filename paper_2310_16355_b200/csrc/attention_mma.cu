@@ -311,6 +311,278 @@ bool launch_fwd(const bf16* qkv, bf16* o, float* lse, int B, int T, int Hl, cuda
 
 
 // ---------------------------------------------------------------------------------------------
+// forward, two query tiles per CTA (head_dim 128): each softmax warpgroup owns a whole 128-row
+// query tile (lane = row, all 128 keys of a block: no cross-warpgroup max exchange), and the two
+// tiles ping-pong on the tensor core -- while one warpgroup turns S into P, the MMA warp runs
+// the other tile's S = Q K^T and O += P V. P goes back into the S columns of TMEM as bf16 and
+// feeds the O MMA straight from TMEM (tcgen05.mma with A in tensor memory).
+//   TMEM: S_A | O_A | S_B | O_B (128 columns each)
+//   smem: Q_A, Q_B, and a 2-stage K/V ring shared by both tiles
+// ---------------------------------------------------------------------------------------------
+struct Fwd2Layout {
+  static constexpr int HD = 128;
+  static constexpr int Q = 128 * HD * 2;
+  static constexpr int KV = 128 * HD * 2;
+  static constexpr int OFF_QA = 0;
+  static constexpr int OFF_QB = OFF_QA + Q;
+  static constexpr int OFF_K = OFF_QB + Q;       // [2]
+  static constexpr int OFF_V = OFF_K + 2 * KV;   // [2]
+  static constexpr int OFF_BAR = OFF_V + 2 * KV;
+  static constexpr int BYTES = OFF_BAR + 256;
+};
+
+__global__ void __launch_bounds__(384, 1)
+    attn_fwd_tc2(const __grid_constant__ CUtensorMap tm, bf16* __restrict__ out, float* __restrict__ lse, int T,
+                 int Hl, float scale_log2, float scale) {
+  using Lay = Fwd2Layout;
+  constexpr int HD = Lay::HD;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t* sQ[2] = {smem + Lay::OFF_QA, smem + Lay::OFF_QB};
+  uint8_t* sK = smem + Lay::OFF_K;
+  uint8_t* sV = smem + Lay::OFF_V;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Lay::OFF_BAR);
+  uint64_t* q_full = bars + 0;
+  uint64_t* kv_full = bars + 1;   // [2]
+  uint64_t* kv_empty = bars + 3;  // [2]
+  uint64_t* s_full = bars + 5;    // [tile]
+  uint64_t* p_full = bars + 7;    // [tile]
+  uint64_t* pv_done = bars + 9;   // [tile]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
+
+  const int nqb = (T + 127) / 128;
+  const int npair = (nqb + 1) / 2;
+  const int pi = npair - 1 - static_cast<int>(blockIdx.x) % npair;  // heaviest pair first
+  const int bh = static_cast<int>(blockIdx.x) / npair;
+  const int b = bh / Hl, h = bh % Hl;
+  const int Dl = Hl * HD;
+  const int row0 = b * T;
+  const int qa = 2 * pi;
+  const bool hasB = qa + 1 < nqb;
+  const int nkv_t[2] = {qa + 1, hasB ? qa + 2 : 0};
+  const int nkv = hasB ? qa + 2 : qa + 1;
+
+  const uint32_t warp = dev::warp_idx_sync();
+  const uint32_t lane = threadIdx.x & 31;
+  if (warp == 0 && lane == 0) {
+    dev::tma_prefetch_desc(&tm);
+    dev::mbar_init(q_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      dev::mbar_init(&kv_full[i], 1);
+      dev::mbar_init(&kv_empty[i], 1);
+      dev::mbar_init(&s_full[i], 1);
+      dev::mbar_init(&p_full[i], 128);
+      dev::mbar_init(&pv_done[i], 1);
+    }
+    dev::fence_barrier_init();
+  }
+  if (warp == 2) dev::tmem_alloc<512>(tmem_slot);
+  dev::tc_fence_before();
+  __syncthreads();
+  dev::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      dev::mbar_arrive_expect_tx(q_full, Lay::Q * (hasB ? 2 : 1));
+      for (int t = 0; t < (hasB ? 2 : 1); ++t) {
+#pragma unroll
+        for (int c = 0; c < HD / 64; ++c)
+          dev::tma_load_2d(sQ[t] + c * CHUNK, &tm, q_full, h * HD + c * 64, row0 + (qa + t) * 128);
+      }
+      for (int j = 0; j < nkv; ++j) {
+        const int st = j & 1;
+        dev::mbar_wait(&kv_empty[st], ((j >> 1) & 1) ^ 1);
+        dev::mbar_arrive_expect_tx(&kv_full[st], 2 * Lay::KV);
+#pragma unroll
+        for (int c = 0; c < HD / 64; ++c) {
+          dev::tma_load_2d(sK + st * Lay::KV + c * CHUNK, &tm, &kv_full[st], Dl + h * HD + c * 64, row0 + j * 128);
+          dev::tma_load_2d(sV + st * Lay::KV + c * CHUNK, &tm, &kv_full[st], 2 * Dl + h * HD + c * 64, row0 + j * 128);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // whole warp runs the schedule; one elected lane issues
+    const uint32_t id_s = dev::make_idesc_bf16(128, 128, 0, 0);
+    const uint32_t id_o = dev::make_idesc_bf16(128, HD, 0, 1);
+    const uint64_t dq[2] = {dev::make_sdesc_sw128(dev::smem_u32(sQ[0]), 16, 1024),
+                            dev::make_sdesc_sw128(dev::smem_u32(sQ[1]), 16, 1024)};
+    const uint64_t dk = dev::make_sdesc_sw128(dev::smem_u32(sK), 16, 1024);
+    const uint64_t dv = dev::make_sdesc_sw128(dev::smem_u32(sV), CHUNK, 1024);
+    auto kstep = [](int kk) { return static_cast<uint64_t>((kk >> 2) * (CHUNK >> 4) + (kk & 3) * 2); };
+    auto issue_s = [&](int t, int j) {
+      const uint64_t bk = dk + static_cast<uint64_t>((j & 1) * (Lay::KV >> 4));
+      if (dev::elect_one_sync()) {
+#pragma unroll
+        for (int kk = 0; kk < HD / 16; ++kk)
+          dev::umma_f16_ss(tmem + t * 256, dq[t] + kstep(kk), bk + kstep(kk), id_s, kk > 0 ? 1u : 0u);
+        dev::umma_commit(&s_full[t]);
+      }
+      __syncwarp();
+    };
+    auto issue_pv = [&](int t, int j) {
+      dev::mbar_wait(&p_full[t], j & 1);
+      dev::tc_fence_after();
+      const uint64_t bv = dv + static_cast<uint64_t>((j & 1) * (Lay::KV >> 4));
+      if (dev::elect_one_sync()) {
+#pragma unroll
+        for (int kk = 0; kk < 128 / 16; ++kk)  // P (bf16 pairs) sits in the first 64 columns of S
+          dev::umma_f16_ts(tmem + t * 256 + 128, tmem + t * 256 + kk * 8, bv + static_cast<uint64_t>(kk * 128), id_o,
+                           (j > 0 || kk > 0) ? 1u : 0u);
+        dev::umma_commit(&pv_done[t]);
+      }
+      __syncwarp();
+    };
+    dev::mbar_wait(q_full, 0);
+    dev::mbar_wait(&kv_full[0], 0);
+    dev::tc_fence_after();
+    issue_s(0, 0);
+    if (hasB) issue_s(1, 0);
+    for (int j = 0; j < nkv; ++j) {
+      if (j < nkv_t[0]) issue_pv(0, j);
+      if (j + 1 < nkv) {
+        dev::mbar_wait(&kv_full[(j + 1) & 1], ((j + 1) >> 1) & 1);
+        dev::tc_fence_after();
+      }
+      if (j + 1 < nkv_t[0]) issue_s(0, j + 1);
+      if (j < nkv_t[1]) issue_pv(1, j);
+      if (j + 1 < nkv_t[1]) issue_s(1, j + 1);
+      if (dev::elect_one_sync()) dev::umma_commit(&kv_empty[j & 1]);  // K_j / V_j consumed
+      __syncwarp();
+    }
+  } else if (warp >= 4) {
+    const int t = (static_cast<int>(warp) - 4) >> 2;  // query tile of this warpgroup
+    if (t == 0 || hasB) {
+      const int r = static_cast<int>(warp & 3) * 32 + static_cast<int>(lane);
+      const int q0 = (qa + t) * 128;
+      const int q = q0 + r;
+      const int nk = nkv_t[t];
+      const uint32_t lane_base = static_cast<uint32_t>((warp & 3) * 32) << 16;
+      const uint32_t tS = tmem + lane_base + t * 256, tO = tS + 128;
+      float m_used = -INFINITY, l = 0.f;
+      for (int j = 0; j < nk; ++j) {
+        dev::mbar_wait(&s_full[t], j & 1);
+        dev::tc_fence_after();
+        uint32_t v[128];
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          dev::tmem_ld_32x32b_x32(tS + c * 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32 * c));
+        dev::tmem_ld_wait();
+        if (j == nk - 1 || (j + 1) * 128 > T) {
+#pragma unroll
+          for (int i = 0; i < 128; ++i) {
+            const int key = j * 128 + i;
+            if (!(key <= q && key < T)) v[i] = __float_as_uint(-INFINITY);
+          }
+        }
+        float mx = fmaxf(__uint_as_float(v[0]), __uint_as_float(v[127]));
+#pragma unroll
+        for (int i = 1; i < 127; i += 2) mx = dev::fmax3(mx, __uint_as_float(v[i]), __uint_as_float(v[i + 1]));
+        // lazy rescale: keep the stale max unless the new one is 2^8 larger in exp2 units; the
+        // O rewrite uses warp-collective TMEM loads/stores, so the whole warp takes it together
+        // (factor 1 for the rows that keep their max)
+        bool resc = false;
+        float factor = 1.f;
+        if (j == 0) {
+          m_used = mx;
+        } else if ((mx - m_used) * scale_log2 > 8.f) {
+          resc = true;
+          factor = dev::ex2_approx((m_used - mx) * scale_log2);
+          m_used = mx;
+          l *= factor;
+        }
+        if (__any_sync(0xffffffffu, resc)) {
+          dev::mbar_wait(&pv_done[t], (j - 1) & 1);  // every earlier P V has landed in O
+          dev::tc_fence_after();
+#pragma unroll 1
+          for (int c = 0; c < HD / 32; ++c) {
+            uint32_t o[32];
+            dev::tmem_ld_32x32b_x32(tO + c * 32, o);
+            dev::tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * factor);
+            dev::tmem_st_32x32b_x32(tO + c * 32, o);
+          }
+          dev::tmem_st_wait();
+        }
+        const float mb = m_used * scale_log2;
+        const float2 sl2 = make_float2(scale_log2, scale_log2), nmb2 = make_float2(-mb, -mb);
+        float2 ls2 = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int e = 0; e < 64; ++e) {  // P in place: v[e] = bf16x2(p[2e], p[2e+1])
+          const float2 a = dev::ffma2(make_float2(__uint_as_float(v[2 * e]), __uint_as_float(v[2 * e + 1])), sl2, nmb2);
+          const float2 pp = make_float2(dev::ex2_approx(a.x), dev::ex2_approx(a.y));
+          ls2 = dev::fadd2(ls2, pp);
+          v[e] = dev::pack_bf16x2(pp.x, pp.y);
+        }
+        l += ls2.x + ls2.y;
+        dev::tmem_st_32x32b_x32(tS, *reinterpret_cast<uint32_t(*)[32]>(v));
+        dev::tmem_st_32x32b_x32(tS + 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
+        dev::tmem_st_wait();
+        dev::tc_fence_before();
+        dev::mbar_arrive(&p_full[t]);
+      }
+      dev::mbar_wait(&pv_done[t], (nk - 1) & 1);
+      dev::tc_fence_after();
+      const float inv = 1.f / l;
+      bf16* orow = out + (static_cast<int64_t>(row0) + q) * Dl + h * HD;
+#pragma unroll
+      for (int c = 0; c < HD / 32; ++c) {
+        uint32_t o[32];
+        dev::tmem_ld_32x32b_x32(tO + c * 32, o);
+        dev::tmem_ld_wait();
+        if (q < T) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            uint4 w;
+            w.x = dev::pack_bf16x2(__uint_as_float(o[8 * u + 0]) * inv, __uint_as_float(o[8 * u + 1]) * inv);
+            w.y = dev::pack_bf16x2(__uint_as_float(o[8 * u + 2]) * inv, __uint_as_float(o[8 * u + 3]) * inv);
+            w.z = dev::pack_bf16x2(__uint_as_float(o[8 * u + 4]) * inv, __uint_as_float(o[8 * u + 5]) * inv);
+            w.w = dev::pack_bf16x2(__uint_as_float(o[8 * u + 6]) * inv, __uint_as_float(o[8 * u + 7]) * inv);
+            *reinterpret_cast<uint4*>(orow + c * 32 + 8 * u) = w;
+          }
+        }
+      }
+      if (q < T) lse[static_cast<int64_t>(bh) * T + q] = m_used * scale + logf(l);
+    }
+  }
+  dev::tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    dev::tc_fence_after();
+    dev::tmem_dealloc<512>(tmem);
+  }
+}
+
+bool fwd2_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("SW_ATTN_FWD_V1");
+    return !(e != nullptr && e[0] == '1');
+  }();
+  return on;
+}
+
+bool launch_fwd2(const bf16* qkv, bf16* o, float* lse, int B, int T, int Hl, cudaStream_t s) {
+  static bool configured = false;
+  if (!configured) {
+    if (cudaFuncSetAttribute(attn_fwd_tc2, cudaFuncAttributeMaxDynamicSharedMemorySize, Fwd2Layout::BYTES) !=
+        cudaSuccess) {
+      return false;
+    }
+    configured = true;
+  }
+  constexpr int HD = 128;
+  const int Dl = Hl * HD;
+  const CUtensorMap tm = make_tmap_bf16_2d(qkv, 3ull * Dl, static_cast<uint64_t>(B) * T, 3ull * Dl, 64, 128);
+  const int nqb = (T + 127) / 128;
+  const int npair = (nqb + 1) / 2;
+  const double scale = 1.0 / std::sqrt(static_cast<double>(HD));
+  attn_fwd_tc2<<<npair * B * Hl, 384, Fwd2Layout::BYTES, s>>>(tm, o, lse, T, Hl,
+                                                              static_cast<float>(scale * 1.4426950408889634),
+                                                              static_cast<float>(scale));
+  return true;
+}
+
+// ---------------------------------------------------------------------------------------------
 // backward
 // ---------------------------------------------------------------------------------------------
 template <int HD>
@@ -1058,7 +1330,7 @@ bool launch_bwd(const bf16* qkv, const bf16* o, const float* lse, const bf16* do
 
 bool attention_mma_fwd(const bf16* qkv, bf16* o, float* lse, int B, int T, int Hl, int hd, cudaStream_t s) {
   if (((3 * Hl * hd) % 8) != 0) return false;
-  if (hd == 128) return launch_fwd<128>(qkv, o, lse, B, T, Hl, s);
+  if (hd == 128) return fwd2_enabled() ? launch_fwd2(qkv, o, lse, B, T, Hl, s) : launch_fwd<128>(qkv, o, lse, B, T, Hl, s);
   if (hd == 64) return launch_fwd<64>(qkv, o, lse, B, T, Hl, s);
   return false;
 }

@@ -179,3 +179,27 @@ def test_rmsnorm_fwd_bwd(M, d):
     assert rel(gio - g0, xr.grad) < 1e-5
     assert rel(ds, sr.grad) < 1e-5
     assert rel(gb, gio) < 1e-2
+
+
+@pytest.mark.parametrize("hd", [64, 128])
+def test_attention_lazy_rescale_path(hd):
+    """Scores that grow along the keys force the online-softmax max to jump by more than 2^8
+    between key blocks, so every query row rescales its O accumulator (the warp-collective TMEM
+    rewrite) -- the path random inputs almost never take."""
+    L = _lib.lib()
+    B, T, Hl = 2, 640, 2
+    Dl = Hl * hd
+    g = torch.Generator(device=DEV).manual_seed(11)
+    x = torch.randn(B * T, 3 * Dl, generator=g, device=DEV) * 0.1
+    x = x.view(B, T, 3, Hl, hd)
+    ramp = torch.arange(T, device=DEV, dtype=torch.float32)[None, :, None, None] / 48.0
+    x[:, :, 0] += 0.5                       # q along the ones direction
+    x[:, :, 1] += ramp                      # k grows with the key index
+    qkv = x.reshape(B * T, 3 * Dl).bfloat16()
+    o = torch.empty(B * T, Dl, device=DEV, dtype=torch.bfloat16)
+    lse = torch.empty(B, Hl, T, device=DEV)
+    _lib.check(L.sw_k_attention_fwd(qkv.data_ptr(), o.data_ptr(), lse.data_ptr(), B, T, Hl, hd, None))
+    torch.cuda.synchronize()
+    want_o, want_lse = ref_attention(qkv, B, T, Hl, hd)
+    assert rel(o, want_o) < 1e-2
+    assert ((lse - want_lse).abs() / want_lse.abs().clamp_min(1)).max().item() < 1e-3
