@@ -273,6 +273,9 @@ SW_API sw_status sw_k_attention_fwd(const void* qkv, void* o, float* lse, int B,
 SW_API sw_status sw_k_attention_bwd(const void* qkv, const void* o, const float* lse,
                                     const void* dout, void* dqkv, float* scratch, int B, int T,
                                     int Hl, int hd, void* stream);
+/* Debug/profiling only: 4096 clock64 stamps of the attention-backward CTA named by the
+ * SW_ATTN_TRACE_CTA environment variable (slot map in tools/attn_trace.py). */
+SW_API sw_status sw_k_attention_trace(unsigned long long* out);
 /* LayerNorm (kernels.hpp:184-271): y bf16, mean/rstd fp32 [M]. */
 SW_API sw_status sw_k_layernorm_fwd(const float* x, const float* scale, const float* bias, void* y,
                                     float* mean, float* rstd, int64_t M, int d, float eps,

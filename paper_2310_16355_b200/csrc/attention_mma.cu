@@ -35,6 +35,54 @@ constexpr int BQ = 128;
 constexpr int BKV = 128;
 constexpr int CHUNK = 128 * 128;  // bytes of one [128 rows x 64 bf16] SW128 chunk
 
+// Work order of the causal kernels: (batch*head) in groups of G; inside a group the heaviest
+// unit (most key/query blocks) of every head first, so the block scheduler's last wave holds the
+// lightest units while the G heads of a group still share their K/V or Q/dO reads through L2.
+// G <= 0: head-major order (unit fastest). Returns the unit rank (0 = heaviest) and bh.
+__device__ __forceinline__ void work_item(int idx, int nunits, int nbh, int G, int& unit, int& bh) {
+  if (G <= 0) {
+    unit = idx % nunits;
+    bh = idx / nunits;
+    return;
+  }
+  const int grp = idx / (G * nunits);
+  const int r = idx - grp * G * nunits;
+  const int g = min(G, nbh - grp * G);
+  unit = r / g;
+  bh = grp * G + r % g;
+}
+
+// Phase tracing of one CTA (tools/attn_trace.py): clock64 stamps at the pipeline's waits.
+__device__ unsigned long long g_attn_trace[4096];
+#define ATTN_TR(slot)                                                                \
+  do {                                                                               \
+    if (static_cast<int>(blockIdx.x) == trace_cta) g_attn_trace[(slot)] = clock64(); \
+  } while (0)
+
+int trace_cta() {
+  static const int c = [] {
+    const char* e = std::getenv("SW_ATTN_TRACE_CTA");
+    return e != nullptr ? std::atoi(e) : -1;
+  }();
+  return c;
+}
+
+int bwd_dq_first() {
+  static const int v = [] {
+    const char* e = std::getenv("SW_ATTN_BWD_DQ_FIRST");
+    return e != nullptr ? std::atoi(e) : 1;
+  }();
+  return v;
+}
+
+int work_group() {
+  static const int g = [] {
+    const char* e = std::getenv("SW_ATTN_GROUP");
+    return e != nullptr ? std::atoi(e) : 8;
+  }();
+  return g;
+}
+
 __device__ __forceinline__ uint64_t kdesc(uint32_t base, int kk) {
   // K-major operand, 16-element K step kk: chunk kk/4, +32 B inside the swizzle row.
   return dev::make_sdesc_sw128(base + (kk >> 2) * CHUNK + (kk & 3) * 32, 16, 1024);
@@ -333,7 +381,7 @@ struct Fwd2Layout {
 
 __global__ void __launch_bounds__(384, 1)
     attn_fwd_tc2(const __grid_constant__ CUtensorMap tm, bf16* __restrict__ out, float* __restrict__ lse, int T,
-                 int Hl, float scale_log2, float scale) {
+                 int Hl, float scale_log2, float scale, int nbh, int group) {
   using Lay = Fwd2Layout;
   constexpr int HD = Lay::HD;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -351,8 +399,9 @@ __global__ void __launch_bounds__(384, 1)
 
   const int nqb = (T + 127) / 128;
   const int npair = (nqb + 1) / 2;
-  const int pi = npair - 1 - static_cast<int>(blockIdx.x) % npair;  // heaviest pair first
-  const int bh = static_cast<int>(blockIdx.x) / npair;
+  int rank_, bh;
+  work_item(static_cast<int>(blockIdx.x), npair, nbh, group, rank_, bh);
+  const int pi = npair - 1 - rank_;  // heaviest pair first
   const int b = bh / Hl, h = bh % Hl;
   const int Dl = Hl * HD;
   const int row0 = b * T;
@@ -578,7 +627,7 @@ bool launch_fwd2(const bf16* qkv, bf16* o, float* lse, int B, int T, int Hl, cud
   const double scale = 1.0 / std::sqrt(static_cast<double>(HD));
   attn_fwd_tc2<<<npair * B * Hl, 384, Fwd2Layout::BYTES, s>>>(tm, o, lse, T, Hl,
                                                               static_cast<float>(scale * 1.4426950408889634),
-                                                              static_cast<float>(scale));
+                                                              static_cast<float>(scale), B * Hl, work_group());
   return true;
 }
 
@@ -894,7 +943,7 @@ __global__ void __launch_bounds__(512, 1)
     attn_bwd_tc2(const __grid_constant__ CUtensorMap tm_qkv64, const __grid_constant__ CUtensorMap tm_qkv128,
                  const __grid_constant__ CUtensorMap tm_do64, const __grid_constant__ CUtensorMap tm_dq,
                  const float* __restrict__ lse, const float* __restrict__ delta, bf16* __restrict__ dqkv, int T,
-                 int Hl, float scale_log2, float scale) {
+                 int Hl, float scale_log2, float scale, int nbh, int group, int trace_cta, int dq_first) {
   using Lay = Bwd2Layout;
   constexpr int HD = Lay::HD;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -918,8 +967,8 @@ __global__ void __launch_bounds__(512, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
 
   const int nb = (T + 127) / 128;
-  const int kb = static_cast<int>(blockIdx.x) % nb;
-  const int bh = static_cast<int>(blockIdx.x) / nb;
+  int kb, bh;
+  work_item(static_cast<int>(blockIdx.x), nb, nbh, group, kb, bh);  // kb 0 = most query blocks
   const int b = bh / Hl, h = bh % Hl;
   const int Dl = Hl * HD;
   const int key0 = kb * 128;
@@ -928,6 +977,10 @@ __global__ void __launch_bounds__(512, 1)
 
   const uint32_t warp = dev::warp_idx_sync();
   const uint32_t lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    ATTN_TR(4000);
+    if (static_cast<int>(blockIdx.x) == trace_cta) g_attn_trace[4001] = static_cast<unsigned long long>(nq);
+  }
   if (warp == 0 && lane == 0) {
     dev::tma_prefetch_desc(&tm_qkv64);
     dev::tma_prefetch_desc(&tm_qkv128);
@@ -997,11 +1050,14 @@ __global__ void __launch_bounds__(512, 1)
       auto k64 = [](int kk) { return static_cast<uint64_t>((kk >> 2) * (CHUNK64 >> 4) + (kk & 3) * 2); };
       auto mn = [](int kk) { return static_cast<uint64_t>(kk * 128); };
       dev::mbar_wait(kv_full, 0);
+      if (lane == 0) ATTN_TR(4002);
       auto issue_s = [&](int n) {
         const int st = n & 1, qst = n % QST;
         dev::mbar_wait(&qdo_full[qst], (n / QST) & 1);
+        if (lane == 0 && n < 64) ATTN_TR(n * 16 + 0);
         if (n >= 2) dev::mbar_wait(&s_free[st], ((n - 2) >> 1) & 1);
         dev::tc_fence_after();
+        if (lane == 0 && n < 64) ATTN_TR(n * 16 + 1);
         const uint64_t q_k = dQ_k + qst * QT16, do_k = dDO_k + qst * QT16;
         if (dev::elect_one_sync()) {
 #pragma unroll
@@ -1020,19 +1076,30 @@ __global__ void __launch_bounds__(512, 1)
         if (n + 1 < nq) issue_s(n + 1);
         dev::mbar_wait(p_full, n & 1);
         dev::tc_fence_after();
+        if (lane == 0 && n < 64) ATTN_TR(n * 16 + 2);
         const uint64_t q_mn = dQ_mn + qst * QT16, do_mn = dDO_mn + qst * QT16;
         if (dev::elect_one_sync()) {
+          // dQ^T first (default): its TMEM drain (dQ warpgroup) then overlaps dV / dK, so the S
+          // buffer it occupies is free again by the time S_{n+2} is issued
+          if (dq_first) {
+#pragma unroll
+            for (int kk = 0; kk < 128 / 16; ++kk)
+              dev::umma_f16_ss(t_s + st * BQ2, dK_mn + mn(kk), dDSt_mn + mn(kk), id_dq, kk > 0 ? 1u : 0u);
+            dev::umma_commit(&dq_full[st]);
+          }
 #pragma unroll
           for (int kk = 0; kk < BQ2 / 16; ++kk)
             dev::umma_f16_ss(t_dv, dPt_k + k128(kk), do_mn + mn(kk), id_kv, (n > 0 || kk > 0) ? 1u : 0u);
 #pragma unroll
           for (int kk = 0; kk < BQ2 / 16; ++kk)
             dev::umma_f16_ss(t_dk, dDSt_k + k128(kk), q_mn + mn(kk), id_kv, (n > 0 || kk > 0) ? 1u : 0u);
+          if (!dq_first) {
 #pragma unroll
-          for (int kk = 0; kk < 128 / 16; ++kk)
-            dev::umma_f16_ss(t_s + st * BQ2, dK_mn + mn(kk), dDSt_mn + mn(kk), id_dq, kk > 0 ? 1u : 0u);
+            for (int kk = 0; kk < 128 / 16; ++kk)
+              dev::umma_f16_ss(t_s + st * BQ2, dK_mn + mn(kk), dDSt_mn + mn(kk), id_dq, kk > 0 ? 1u : 0u);
+            dev::umma_commit(&dq_full[st]);
+          }
           dev::umma_commit(mma_done);
-          dev::umma_commit(&dq_full[st]);
           dev::umma_commit(&qdo_empty[qst]);
         }
         __syncwarp();
@@ -1058,9 +1125,11 @@ __global__ void __launch_bounds__(512, 1)
         const int qq = qs + tid - BQ2;
         st_del[tid - BQ2] = qq < T ? -scale * delta[static_cast<int64_t>(bh) * T + qq] : 0.f;
       }
+      if (lane == 0 && (warp == 4 || warp == 8) && n < 64) ATTN_TR(n * 16 + 3 + (warp == 8) * 5);
       asm volatile("bar.sync 1, 256;" ::: "memory");
       dev::mbar_wait(&s_full[st], (n >> 1) & 1);
       dev::tc_fence_after();
+      if (lane == 0 && (warp == 4 || warp == 8) && n < 64) ATTN_TR(n * 16 + 4 + (warp == 8) * 5);
       uint32_t sv[32], pv[32];
       dev::tmem_ld_32x32b_x32(t_s + lane_base + st * BQ2 + wg * 32, sv);
       dev::tmem_ld_32x32b_x32(t_dp + lane_base + st * BQ2 + wg * 32, pv);
@@ -1093,7 +1162,9 @@ __global__ void __launch_bounds__(512, 1)
         }
       }
       // sPt / sDSt were last read by block n-1's dV / dK / dQ MMAs
+      if (lane == 0 && (warp == 4 || warp == 8) && n < 64) ATTN_TR(n * 16 + 5 + (warp == 8) * 5);
       if (n >= 1) dev::mbar_wait(mma_done, (n - 1) & 1);
+      if (lane == 0 && (warp == 4 || warp == 8) && n < 64) ATTN_TR(n * 16 + 6 + (warp == 8) * 5);
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         dev::st_sw128(sPt, 128, t, 0, wg * 4 + u, make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]));
@@ -1102,10 +1173,12 @@ __global__ void __launch_bounds__(512, 1)
       dev::fence_proxy_async_smem();
       dev::tc_fence_before();
       dev::mbar_arrive(p_full);
+      if (lane == 0 && (warp == 4 || warp == 8) && n < 64) ATTN_TR(n * 16 + 7 + (warp == 8) * 5);
     }
     // dK, dV (lane = key row) -> bf16 rows of dqkv; each warpgroup writes HD/2 columns
     dev::mbar_wait(mma_done, (nq - 1) & 1);
     dev::tc_fence_after();
+    if (lane == 0 && warp == 4) ATTN_TR(4003);
     const int64_t ld = 3LL * Dl;
     bf16* dk_row = dqkv + (static_cast<int64_t>(row0) + key) * ld + Dl + h * HD;
     bf16* dv_row = dk_row + Dl;
@@ -1145,12 +1218,14 @@ __global__ void __launch_bounds__(512, 1)
       const int qs = key0 + n * BQ2;
       dev::mbar_wait(&dq_full[st], (n >> 1) & 1);
       dev::tc_fence_after();
+      if (leader && n < 64) ATTN_TR(n * 16 + 13);
       uint32_t v[64];
       dev::tmem_ld_32x32b_x32(t_s + lane_base + st * BQ2, *reinterpret_cast<uint32_t(*)[32]>(v));
       dev::tmem_ld_32x32b_x32(t_s + lane_base + st * BQ2 + 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
       dev::tmem_ld_wait();
       dev::tc_fence_before();
       dev::mbar_arrive(&s_free[st]);
+      if (leader && n < 64) ATTN_TR(n * 16 + 14);
       // the previous block's reduce-adds must have read the staging tile
       if (leader) dev::bulk_wait_read();
       asm volatile("bar.sync 2, 128;" ::: "memory");
@@ -1171,6 +1246,7 @@ __global__ void __launch_bounds__(512, 1)
   }
   dev::tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) ATTN_TR(4004);
   if (warp == 2) {
     dev::tc_fence_after();
     dev::tmem_dealloc<512>(tmem);
@@ -1288,7 +1364,7 @@ bool launch_bwd2(const bf16* qkv, const bf16* o, const float* lse, const bf16* d
   const double scale = 1.0 / std::sqrt(static_cast<double>(HD));
   attn_bwd_tc2<<<nb * B * Hl, 512, Bwd2Layout::BYTES, s>>>(tm_qkv64, tm_qkv128, tm_do64, tm_dq, lse, delta, dqkv,
                                                           T, Hl, static_cast<float>(scale * 1.4426950408889634),
-                                                          static_cast<float>(scale));
+                                                          static_cast<float>(scale), B * Hl, work_group(), trace_cta(), bwd_dq_first());
   dq_to_bf16<<<1184, 256, 0, s>>>(dq, dqkv, M, Dl);
   return true;
 }
@@ -1327,6 +1403,10 @@ bool launch_bwd(const bf16* qkv, const bf16* o, const float* lse, const bf16* do
 }
 
 }  // namespace
+
+void attention_trace_read(unsigned long long* out) {
+  cudaMemcpyFromSymbol(out, g_attn_trace, sizeof(unsigned long long) * 4096);
+}
 
 bool attention_mma_fwd(const bf16* qkv, bf16* o, float* lse, int B, int T, int Hl, int hd, cudaStream_t s) {
   if (((3 * Hl * hd) % 8) != 0) return false;

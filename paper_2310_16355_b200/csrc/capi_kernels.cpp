@@ -152,6 +152,11 @@ sw_status sw_k_attention_bwd(const void* qkv, const void* o, const float* lse, c
   });
 }
 
+// Debug: clock64 stamps of the traced attention-backward CTA (SW_ATTN_TRACE_CTA), 4096 slots.
+sw_status sw_k_attention_trace(unsigned long long* out) {
+  return sw::guarded([&] { sw::k::attention_trace_read(out); });
+}
+
 sw_status sw_k_layernorm_fwd(const float* x, const float* scale, const float* bias, void* y, float* mean,
                              float* rstd, int64_t M, int d, float eps, void* stream) {
   return sw::guarded([&] {

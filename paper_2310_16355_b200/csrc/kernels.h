@@ -80,6 +80,7 @@ void loss_reduce(const float* wloss, int64_t M, const float* wsum, double* loss,
 // Causal scaled-dot-product attention on the head-sharded QKV activations:
 // qkv [M, 3*Dl] (q | k | v, head h at column h*hd), o [M, Dl], lse [B, Hl, T]
 // (graph.hpp:650-661 with the -1e9 causal mask of model.hpp:100-106).
+void attention_trace_read(unsigned long long* out);
 void attention_fwd(const bf16* qkv, bf16* o, float* lse, int B, int T, int Hl, int hd,
                    cudaStream_t s);
 // dqkv [M, 3*Dl]; scratch: fp32 [B*Hl*T] (delta) + fp32 [M, 3*Dl] (dk/dv accumulators).
