@@ -43,3 +43,11 @@ examples/cpp_train_step: examples/cpp_train_step.cpp include/shardweave_b200.hpp
 
 examples: examples/cpp_train_step
 .PHONY: examples
+
+# Experiment builds for same-box A/B timing: make variant NAME=<n> DEFS="-D..." -> variants/libsw_<n>.so
+# (load with SW_LIB_PATH=variants/libsw_<n>.so)
+variant:
+	@mkdir -p build_$(NAME) variants
+	$(MAKE) LIB=variants/libsw_$(NAME).so BUILD_DIR=build_$(NAME) NVCCFLAGS="$(NVCCFLAGS) $(DEFS)" \
+	    variants/libsw_$(NAME).so
+.PHONY: variant

@@ -276,6 +276,9 @@ SW_API sw_status sw_k_attention_bwd(const void* qkv, const void* o, const float*
 /* Debug/profiling only: 4096 clock64 stamps of the attention-backward CTA named by the
  * SW_ATTN_TRACE_CTA environment variable (slot map in tools/attn_trace.py). */
 SW_API sw_status sw_k_attention_trace(unsigned long long* out);
+/* Debug/profiling only: 1024 per-tile phase stamps of the CTA-pair GEMM CTA named by
+ * SW_GEMM_TRACE_CTA (slot map in tools/gemm_trace.py). */
+SW_API sw_status sw_k_gemm_trace(unsigned long long* out);
 /* LayerNorm (kernels.hpp:184-271): y bf16, mean/rstd fp32 [M]. */
 SW_API sw_status sw_k_layernorm_fwd(const float* x, const float* scale, const float* bias, void* y,
                                     float* mean, float* rstd, int64_t M, int d, float eps,

@@ -10,7 +10,8 @@ import os
 import re
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libshardweave_b200.so")
+# SW_LIB_PATH: load an experiment build instead (`make variant`); still no fallback
+LIB_PATH = os.environ.get("SW_LIB_PATH") or os.path.join(_HERE, "libshardweave_b200.so")
 HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "shardweave_b200.h")
 
 STATUS_NAMES = {

@@ -152,6 +152,10 @@ sw_status sw_k_attention_bwd(const void* qkv, const void* o, const float* lse, c
   });
 }
 
+sw_status sw_k_gemm_trace(unsigned long long* out) {
+  return sw::guarded([&] { sw::gemm_trace_read(out); });
+}
+
 // Debug: clock64 stamps of the traced attention-backward CTA (SW_ATTN_TRACE_CTA), 4096 slots.
 sw_status sw_k_attention_trace(unsigned long long* out) {
   return sw::guarded([&] { sw::k::attention_trace_read(out); });

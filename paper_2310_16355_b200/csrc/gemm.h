@@ -65,9 +65,13 @@ struct GemmParams {
   float adam_lr = 0.f, adam_b1 = 0.f, adam_b2 = 0.f, adam_eps = 0.f, adam_wd = 0.f, adam_c1 = 1.f, adam_c2 = 1.f;
   int adam_fast = 0;  // set by gemm_bf16: bias corrections in [2^-14, 1] admit the branch-free path
   int num_sms = 0;  // 0 = all
+  int trace_cta = -1;  // profiling: CTA whose per-tile phases are stamped (SW_GEMM_TRACE_CTA)
 };
 
 // Returns cudaSuccess or the launch error. Throws std::runtime_error on invalid shapes.
 cudaError_t gemm_bf16(const GemmParams& p, cudaStream_t stream);
+
+// Profiling: the 1024 per-tile phase stamps of the CTA named by SW_GEMM_TRACE_CTA.
+void gemm_trace_read(unsigned long long* out);
 
 }  // namespace sw
