@@ -328,7 +328,9 @@ def run_ours(args):
                    "parallelism": f"tp{tp}" if dp == 1 else f"dp{dp}xtp{tp}",
                    "plan": "reference rules (derive_plan) + spec overrides: lm_head/kernel "
                            + plan.at("lm_head/kernel") + (" (vocab-parallel)" if tp > 1 and plan.at("lm_head/kernel") == "split:0" else ""),
-                   "l2": "inputs larger than L2 (activations/weights >> 126 MB); no flush"},
+                   "l2": "inputs larger than L2 (activations/weights >> 126 MB); no flush",
+                   "allreduce": ("bf16" if os.environ.get("SW_AR_BF16") == "1" else "fp32") + " payloads, "
+                                 f"{os.environ.get('SW_AR_CHUNKS', '4')} row chunks on a comm stream"},
         "mfu": {"tflops_per_gpu": round(step_tflops_per_gpu, 1),
                 "frac_of_measured_bf16_sustained": round(step_tflops_per_gpu / peak_t, 3),
                 "frac_of_2.25PF_spec": round(step_tflops_per_gpu / 2250.0, 3),

@@ -525,6 +525,12 @@ __device__ __forceinline__ void adamw_chunk_smem(const GemmParams& p, float* sbo
   if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(p.adam_flag, 1);
 }
 
+// Phase trace of one CTA (tools/gemm_trace.py), per tile i < 64 of that CTA:
+// [8i] MMA passed tempty, [8i+1] MMA issued the last k-block, [8i+2] cycles the MMA warp waited
+// on full[] in the tile, [8i+3] epilogue warp 4 passed tfull, [8i+4] warp 4 released the
+// accumulator, [8i+5] warp 8 released it, [8i+6] cycles warp 4 waited on ofull in the tile.
+__device__ unsigned long long g_gemm_trace[1024];
+
 template <Epi EPI>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(p_threads<EPI>(), 1)
     gemm_bf16_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -631,13 +637,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(p_threads<EPI>(), 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int t = pair; t < num_tiles; t += npairs) {
+      const bool tr = static_cast<int>(blockIdx.x) == p.trace_cta;
+      int ti = 0;
+      for (int t = pair; t < num_tiles; t += npairs, ++ti) {
         dev::mbar_wait(&tempty[acc], acc_phase ^ 1);
         dev::tc_fence_after();
+        if (tr && lane == 0 && ti < 64) g_gemm_trace[8 * ti] = clock64();
+        long long waited = 0;
         const uint32_t d_tmem = tmem_base + acc * BN;
         for (int kb = 0; kb < num_kb; ++kb) {
+          const long long w0 = tr ? clock64() : 0;
           dev::mbar_wait(&full[stage], phase);
           dev::tc_fence_after();
+          if (tr) waited += clock64() - w0;
           const uint64_t as = a0 + static_cast<uint64_t>(stage * (P_A_STAGE >> 4));
           const uint64_t bs = b0 + static_cast<uint64_t>(stage * (P_B_STAGE >> 4));
           if (dev::elect_one_sync()) {
@@ -654,6 +666,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(p_threads<EPI>(), 1)
         }
         if (dev::elect_one_sync()) dev::umma_commit_2sm(&tfull[acc], 0x3);
         __syncwarp();
+        if (tr && lane == 0 && ti < 64) {
+          g_gemm_trace[8 * ti + 1] = clock64();
+          g_gemm_trace[8 * ti + 2] = waited;
+        }
         if (++acc == 2) {
           acc = 0;
           acc_phase ^= 1;
@@ -702,12 +718,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(p_threads<EPI>(), 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     uint32_t uses = 0;
-    for (int t = pair; t < num_tiles; t += npairs) {
+    const bool tr = static_cast<int>(blockIdx.x) == p.trace_cta && lane == 0;
+    int ti = 0;
+    for (int t = pair; t < num_tiles; t += npairs, ++ti) {
       int mb, nb;
       tile_coords(t, num_m, num_n, mb, nb);
       const int row = mb * 2 * BM + static_cast<int>(rank) * BM + static_cast<int>(q) * 32 + static_cast<int>(lane);
       dev::mbar_wait(&tfull[acc], acc_phase);
       dev::tc_fence_after();
+      if (tr && warp == 4 && ti < 64) g_gemm_trace[8 * ti + 3] = clock64();
+      long long owait = 0;
 #pragma unroll 1
       for (int j = 0; j < BN / (2 * OC); ++j) {
         const int col0 = nb * BN + (2 * j + wg) * OC;
@@ -715,7 +735,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(p_threads<EPI>(), 1)
         uint32_t r[OC];
         dev::tmem_ld_32x32b_x16(tmem_base + ((q * 32) << 16) + acc * BN + (2 * j + wg) * OC, r);
         dev::tmem_ld_wait();
+        const long long o0 = tr ? clock64() : 0;
         dev::mbar_wait(&ofull[wg], uses & 1);
+        if (tr) owait += clock64() - o0;
         ++uses;
         float* sbox = reinterpret_cast<float*>(sOpt + wg * OPT_BUF) + q * (OPT_WBOX / 4);
         adamw_chunk_smem(p, sbox, row, col0, min(OC, p.N - col0), r, lane);
@@ -732,6 +754,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(p_threads<EPI>(), 1)
         }
       }
       dev::tc_fence_before();
+      if (tr && (warp == 4 || warp == 8) && ti < 64) {
+        g_gemm_trace[8 * ti + (warp == 4 ? 4 : 5)] = clock64();
+        if (warp == 4) g_gemm_trace[8 * ti + 6] = owait;
+      }
       if (lane == 0) dev::mbar_arrive_cluster(tempty_leader + acc * 8);
       if (++acc == 2) {
         acc = 0;
@@ -843,7 +869,13 @@ cudaError_t launch_2sm(const GemmParams& p, cudaStream_t stream) {
     om.m = make_tmap_f32_2d(p.adam_m, p.N, p.M, p.ldc, OC, 32);
     om.v = make_tmap_f32_2d(p.adam_v, p.N, p.M, p.ldc, OC, 32);
   }
-  gemm_bf16_2sm_kernel<EPI><<<grid, p_threads<EPI>(), p_smem_bytes<EPI>(), stream>>>(ta, tb, om, p);
+  static const int trace_cta = [] {
+    const char* e = std::getenv("SW_GEMM_TRACE_CTA");
+    return e != nullptr ? std::atoi(e) : -1;
+  }();
+  GemmParams q = p;
+  q.trace_cta = trace_cta;
+  gemm_bf16_2sm_kernel<EPI><<<grid, p_threads<EPI>(), p_smem_bytes<EPI>(), stream>>>(ta, tb, om, q);
   return cudaGetLastError();
 }
 
@@ -985,6 +1017,10 @@ bool gemv_ok(const GemmParams& p) {
 }
 
 }  // namespace
+
+void gemm_trace_read(unsigned long long* out) {
+  cudaMemcpyFromSymbol(out, g_gemm_trace, sizeof(unsigned long long) * 1024);
+}
 
 cudaError_t gemm_bf16(const GemmParams& p, cudaStream_t stream) {
   if (p.M <= 0 || p.N <= 0 || p.K <= 0) {

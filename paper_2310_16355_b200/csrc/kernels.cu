@@ -217,15 +217,25 @@ __global__ void ln_fwd_generic_kernel(const float* __restrict__ x, const float* 
   }
 }
 
+// dy loaders: the residual-stream gradient arrives as fp32, or as bf16 after a bf16 all-reduce
+__device__ __forceinline__ float4 ldg4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
+__device__ __forceinline__ float4 ldg4(const bf16* p) {
+  const uint2 u = __ldg(reinterpret_cast<const uint2*>(p));
+  const float2 a = dev::unpack_bf16x2(u.x), b = dev::unpack_bf16x2(u.y);
+  return make_float4(a.x, a.y, b.x, b.y);
+}
+__device__ __forceinline__ float ld1(const float* p) { return *p; }
+__device__ __forceinline__ float ld1(const bf16* p) { return __bfloat162float(*p); }
+
 // One CTA walks rows r = blockIdx.x, +gridDim.x, ...; each thread owns fixed columns and
 // accumulates dscale / dbias partials in registers, flushed with one atomic per column.
 // Two passes per row: pass 1 reduces sum(g) and sum(g*xhat) while accumulating the parameter
 // partials; pass 2 re-reads x / dy (L1/L2 hits) to emit dx. Keeping nothing row-sized in
 // registers lets four CTAs share an SM, which is what the HBM stream needs.
-template <int THREADS, int V4>
+template <int THREADS, int V4, typename DY>
 __global__ void __launch_bounds__(THREADS, (THREADS <= 256 ? 4 : 2)) ln_bwd_kernel(
     const float* __restrict__ x, const float* __restrict__ mean, const float* __restrict__ rstd,
-    const float* __restrict__ scale, const float* __restrict__ dy, float* __restrict__ g_io,
+    const float* __restrict__ scale, const DY* __restrict__ dy, float* __restrict__ g_io,
     bf16* __restrict__ g_bf16, float* __restrict__ dscale, float* __restrict__ dbias, int64_t M,
     int d, int accumulate, float* __restrict__ partials, int rms) {
   __shared__ float red[32];
@@ -235,14 +245,14 @@ __global__ void __launch_bounds__(THREADS, (THREADS <= 256 ? 4 : 2)) ln_bwd_kern
   for (int64_t row = blockIdx.x; row < M; row += gridDim.x) {
     const float mu = mean ? mean[row] : 0.f, rs = rstd[row];
     const float* xr = x + row * d;
-    const float* dr = dy + row * d;
+    const DY* dr = dy + row * d;
     float s1 = 0.f, s2 = 0.f;
 #pragma unroll
     for (int j = 0; j < V4; ++j) {
       const int c = (threadIdx.x + j * THREADS) * 4;
       if (c < d) {
         const float4 xv = __ldg(reinterpret_cast<const float4*>(xr + c));
-        const float4 dv = __ldg(reinterpret_cast<const float4*>(dr + c));
+        const float4 dv = ldg4(dr + c);
         const float4 sc = __ldg(reinterpret_cast<const float4*>(scale + c));
         const float4 xh = make_float4((xv.x - mu) * rs, (xv.y - mu) * rs, (xv.z - mu) * rs, (xv.w - mu) * rs);
         ds[j].x += dv.x * xh.x; ds[j].y += dv.y * xh.y; ds[j].z += dv.z * xh.z; ds[j].w += dv.w * xh.w;
@@ -259,7 +269,7 @@ __global__ void __launch_bounds__(THREADS, (THREADS <= 256 ? 4 : 2)) ln_bwd_kern
       const int c = (threadIdx.x + j * THREADS) * 4;
       if (c < d) {
         const float4 xv = __ldg(reinterpret_cast<const float4*>(xr + c));
-        const float4 dv = __ldg(reinterpret_cast<const float4*>(dr + c));
+        const float4 dv = ldg4(dr + c);
         const float4 sc = __ldg(reinterpret_cast<const float4*>(scale + c));
         float4 dx;
         dx.x = rs * (dv.x * sc.x - gm - (xv.x - mu) * rs * gxm);
@@ -324,10 +334,10 @@ __device__ __forceinline__ float4 block_sum4(float4 v, float* red) {
 // are in flight together, their four row sums share one block reduction, and the residual
 // gradient of both rows is prefetched into L1 before that reduction so its latency hides behind
 // it. x / dy are kept in registers between the passes (no re-read).
-template <int THREADS, int V4>
+template <int THREADS, int V4, typename DY>
 __global__ void __launch_bounds__(THREADS, 2) ln_bwd2_kernel(
     const float* __restrict__ x, const float* __restrict__ mean, const float* __restrict__ rstd,
-    const float* __restrict__ scale, const float* __restrict__ dy, float* __restrict__ g_io,
+    const float* __restrict__ scale, const DY* __restrict__ dy, float* __restrict__ g_io,
     bf16* __restrict__ g_bf16, float* __restrict__ dscale, float* __restrict__ dbias, int64_t M,
     int d, int accumulate, float* __restrict__ partials, int rms) {
   __shared__ __align__(16) float red[4 * (THREADS / 32)];
@@ -346,9 +356,9 @@ __global__ void __launch_bounds__(THREADS, 2) ln_bwd2_kernel(
       const int c = (threadIdx.x + j * THREADS) * 4;
       if (c < d) {
         xa[j] = __ldg(reinterpret_cast<const float4*>(x + r0 * d + c));
-        da[j] = __ldg(reinterpret_cast<const float4*>(dy + r0 * d + c));
+        da[j] = ldg4(dy + r0 * d + c);
         xb[j] = __ldg(reinterpret_cast<const float4*>(x + r1 * d + c));
-        dbv[j] = __ldg(reinterpret_cast<const float4*>(dy + r1 * d + c));
+        dbv[j] = ldg4(dy + r1 * d + c);
       }
     }
     if (accumulate && (threadIdx.x & 7) == 0) {  // one L1 prefetch per 128-byte line
@@ -467,9 +477,10 @@ __global__ void ln_param_reduce_kernel(const float* __restrict__ partials, int n
   if (o != nullptr) o[col] += (s0 + s1) + (s2 + s3);
 }
 
+template <typename DY>
 __global__ void ln_bwd_generic_kernel(const float* __restrict__ x, const float* __restrict__ mean,
                                       const float* __restrict__ rstd, const float* __restrict__ scale,
-                                      const float* __restrict__ dy, float* __restrict__ g_io,
+                                      const DY* __restrict__ dy, float* __restrict__ g_io,
                                       bf16* __restrict__ g_bf16, float* __restrict__ dscale,
                                       float* __restrict__ dbias, int d, int accumulate, int rms) {
   __shared__ float red[32];
@@ -478,7 +489,7 @@ __global__ void ln_bwd_generic_kernel(const float* __restrict__ x, const float* 
   float s1 = 0.f, s2 = 0.f;
   for (int i = threadIdx.x; i < d; i += blockDim.x) {
     const float xh = (x[row * d + i] - mu) * rs;
-    const float g = dy[row * d + i] * scale[i];
+    const float g = ld1(dy + row * d + i) * scale[i];
     s1 += g;
     s2 += g * xh;
   }
@@ -486,7 +497,7 @@ __global__ void ln_bwd_generic_kernel(const float* __restrict__ x, const float* 
   const float gxm = block_sum(s2, red) / d;
   for (int i = threadIdx.x; i < d; i += blockDim.x) {
     const float xh = (x[row * d + i] - mu) * rs;
-    const float dv = dy[row * d + i];
+    const float dv = ld1(dy + row * d + i);
     const float g = dv * scale[i];
     float dx = rs * (g - gm - xh * gxm);
     if (accumulate) dx += g_io[row * d + i];
@@ -783,6 +794,19 @@ __global__ void add_residual_bias_kernel(const float* __restrict__ a, const floa
   }
 }
 
+__global__ void add_residual_bias_bf16_kernel(const float* __restrict__ a, const bf16* __restrict__ b,
+                                              const float* __restrict__ bias, float* __restrict__ y, int64_t n4,
+                                              int d) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n4;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const float4 x = reinterpret_cast<const float4*>(a)[i];
+    const float4 z = ldg4(b + i * 4);
+    const int c = static_cast<int>((i * 4) % d);
+    const float4 bb = bias ? *reinterpret_cast<const float4*>(bias + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+    reinterpret_cast<float4*>(y)[i] = make_float4(x.x + z.x + bb.x, x.y + z.y + bb.y, x.z + z.z + bb.z, x.w + z.w + bb.w);
+  }
+}
+
 // ------------------------------------------------------------------------------------------
 // optimizer / misc
 // ------------------------------------------------------------------------------------------
@@ -860,6 +884,21 @@ __global__ void sum_ranks_kernel(RankPtrs bufs, int nranks, int64_t n, float sca
     for (int r = 1; r < nranks; ++r) s += bufs.p[r][i];
     s *= scale;
     for (int r = 0; r < nranks; ++r) bufs.p[r][i] = s;
+  }
+}
+
+struct RankPtrsBf16 {
+  bf16* p[16];
+};
+
+// bf16 payloads: fp32 sum in ascending rank order, one rounding (NCCL's ring rounds per hop)
+__global__ void sum_ranks_bf16_kernel(RankPtrsBf16 bufs, int nranks, int64_t n, float scale) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    float s = __bfloat162float(bufs.p[0][i]);
+    for (int r = 1; r < nranks; ++r) s += __bfloat162float(bufs.p[r][i]);
+    const bf16 o = __float2bfloat16(s * scale);
+    for (int r = 0; r < nranks; ++r) bufs.p[r][i] = o;
   }
 }
 
@@ -950,28 +989,29 @@ static bool ln_bwd_v1() {
 
 int64_t layernorm_bwd_partials(int d) { return static_cast<int64_t>(4 * kSMs) * 2 * d; }
 
-void layernorm_bwd(const float* x, const float* mean, const float* rstd, const float* scale,
-                   const float* dy, float* g_io, bf16* g_bf16, float* dscale, float* dbias,
-                   int64_t M, int d, int accumulate, cudaStream_t s, float* partials, int rms) {
+template <typename DY>
+static void layernorm_bwd_t(const float* x, const float* mean, const float* rstd, const float* scale, const DY* dy,
+                            float* g_io, bf16* g_bf16, float* dscale, float* dbias, int64_t M, int d, int accumulate,
+                            cudaStream_t s, float* partials, int rms) {
   const unsigned g = static_cast<unsigned>(M < 4 * kSMs ? M : 4 * kSMs);
   unsigned nblk = g;
   if (d % 4 == 0 && d <= 512) {
-    ln_bwd_kernel<32, 4><<<g, 32, 0, s>>>(x, mean, rstd, scale, dy, g_io, g_bf16, dscale, dbias, M, d, accumulate,
+    ln_bwd_kernel<32, 4, DY><<<g, 32, 0, s>>>(x, mean, rstd, scale, dy, g_io, g_bf16, dscale, dbias, M, d, accumulate,
                                           partials, rms);
   } else if (d % 4 == 0 && d <= 4096 && ln_bwd_v1()) {
-    ln_bwd_kernel<256, 4><<<g, 256, 0, s>>>(x, mean, rstd, scale, dy, g_io, g_bf16, dscale, dbias, M, d, accumulate,
+    ln_bwd_kernel<256, 4, DY><<<g, 256, 0, s>>>(x, mean, rstd, scale, dy, g_io, g_bf16, dscale, dbias, M, d, accumulate,
                                             partials, rms);
   } else if (d % 4 == 0 && d <= 4096) {
     const unsigned g2 = static_cast<unsigned>((M + 1) / 2 < 2 * kSMs ? (M + 1) / 2 : 2 * kSMs);
     nblk = g2;
-    ln_bwd2_kernel<256, 4><<<g2, 256, 0, s>>>(x, mean, rstd, scale, dy, g_io, g_bf16, dscale, dbias, M, d,
+    ln_bwd2_kernel<256, 4, DY><<<g2, 256, 0, s>>>(x, mean, rstd, scale, dy, g_io, g_bf16, dscale, dbias, M, d,
                                               accumulate, partials, rms);
   } else if (d % 4 == 0 && d <= 12288) {
-    ln_bwd_kernel<512, 6><<<g, 512, 0, s>>>(x, mean, rstd, scale, dy, g_io, g_bf16, dscale, dbias, M, d, accumulate,
+    ln_bwd_kernel<512, 6, DY><<<g, 512, 0, s>>>(x, mean, rstd, scale, dy, g_io, g_bf16, dscale, dbias, M, d, accumulate,
                                             partials, rms);
   } else {
     // one CTA per row: parameter partials would be row-sized; this shape keeps the atomics
-    ln_bwd_generic_kernel<<<static_cast<unsigned>(M), 256, 0, s>>>(x, mean, rstd, scale, dy, g_io, g_bf16,
+    ln_bwd_generic_kernel<DY><<<static_cast<unsigned>(M), 256, 0, s>>>(x, mean, rstd, scale, dy, g_io, g_bf16,
                                                                   dscale, dbias, d, accumulate, rms);
     return;
   }
@@ -979,6 +1019,18 @@ void layernorm_bwd(const float* x, const float* mean, const float* rstd, const f
     ln_param_reduce_kernel<<<static_cast<unsigned>((2 * d + 63) / 64), 64, 0, s>>>(partials, static_cast<int>(nblk), d,
                                                                                   dscale, dbias);
   }
+}
+
+void layernorm_bwd(const float* x, const float* mean, const float* rstd, const float* scale, const float* dy,
+                   float* g_io, bf16* g_bf16, float* dscale, float* dbias, int64_t M, int d, int accumulate,
+                   cudaStream_t s, float* partials, int rms) {
+  layernorm_bwd_t(x, mean, rstd, scale, dy, g_io, g_bf16, dscale, dbias, M, d, accumulate, s, partials, rms);
+}
+
+void layernorm_bwd(const float* x, const float* mean, const float* rstd, const float* scale, const bf16* dy,
+                   float* g_io, bf16* g_bf16, float* dscale, float* dbias, int64_t M, int d, int accumulate,
+                   cudaStream_t s, float* partials, int rms) {
+  layernorm_bwd_t(x, mean, rstd, scale, dy, g_io, g_bf16, dscale, dbias, M, d, accumulate, s, partials, rms);
 }
 
 void colsum_bf16(const bf16* X, int64_t ld, int64_t M, int N, int seg, float* out0, float* out1,
@@ -1035,6 +1087,12 @@ void add_residual_bias(const float* a, const float* b, const float* bias, float*
   add_residual_bias_kernel<<<grid_for(n4, 256), 256, 0, s>>>(a, b, bias, y, n4, d);
 }
 
+void add_residual_bias(const float* a, const bf16* b, const float* bias, float* y, int64_t M, int d,
+                       cudaStream_t s) {
+  const int64_t n4 = M * d / 4;
+  add_residual_bias_bf16_kernel<<<grid_for(n4, 256), 256, 0, s>>>(a, b, bias, y, n4, d);
+}
+
 void adamw(float* p, float* m, float* v, const float* g, bf16* shadow, int64_t n, float lr,
            float b1, float b2, float eps, float wd, float c1, float c2, cudaStream_t s) {
   adamw_kernel<<<grid_for(n / 4 + 1, 256), 256, 0, s>>>(p, m, v, g, shadow, n, lr, b1, b2, eps, wd, c1, c2);
@@ -1060,6 +1118,12 @@ void sum_ranks_f32(float* const* bufs, int nranks, int64_t n, float scale, cudaS
   RankPtrs p{};
   for (int r = 0; r < nranks && r < 16; ++r) p.p[r] = bufs[r];
   sum_ranks_kernel<<<grid_for(n, 256, 4), 256, 0, s>>>(p, nranks, n, scale);
+}
+
+void sum_ranks_bf16(bf16* const* bufs, int nranks, int64_t n, float scale, cudaStream_t s) {
+  RankPtrsBf16 p{};
+  for (int r = 0; r < nranks && r < 16; ++r) p.p[r] = bufs[r];
+  sum_ranks_bf16_kernel<<<grid_for(n, 256, 4), 256, 0, s>>>(p, nranks, n, scale);
 }
 
 void init_normal(float* out, int64_t lr, int64_t lc, int64_t r0, int64_t c0, int64_t cols,

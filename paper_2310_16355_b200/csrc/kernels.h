@@ -39,6 +39,10 @@ void layernorm_fwd(const float* x, const float* scale, const float* bias, bf16* 
 void layernorm_bwd(const float* x, const float* mean, const float* rstd, const float* scale,
                    const float* dy, float* g_io, bf16* g_bf16, float* dscale, float* dbias,
                    int64_t M, int d, int accumulate, cudaStream_t s, float* partials = nullptr, int rms = 0);
+// Same, with the residual-stream gradient dy in bf16 (after a bf16 all-reduce).
+void layernorm_bwd(const float* x, const float* mean, const float* rstd, const float* scale,
+                   const bf16* dy, float* g_io, bf16* g_bf16, float* dscale, float* dbias,
+                   int64_t M, int d, int accumulate, cudaStream_t s, float* partials = nullptr, int rms = 0);
 int64_t layernorm_bwd_partials(int d);
 
 // Column sums of X [M, N] (bf16 or f32, row pitch ld) written (accumulate=0) or added into
@@ -90,6 +94,8 @@ void attention_bwd(const bf16* qkv, const bf16* o, const float* lse, const bf16*
 // y = a + b + bias[col]   (row-parallel output after the all-reduce: residual + partial + bias)
 void add_residual_bias(const float* a, const float* b, const float* bias, float* y, int64_t M,
                        int d, cudaStream_t s);
+void add_residual_bias(const float* a, const bf16* b, const float* bias, float* y, int64_t M, int d,
+                       cudaStream_t s);
 
 // AdamW over a flat shard (train_state.hpp:183-220, Scalar = float); also refreshes the bf16
 // shadow copy used by the GEMMs.
@@ -102,6 +108,7 @@ void cast_f32_bf16(const float* x, bf16* y, int64_t n, cudaStream_t s);
 
 // Emulated collective: every bufs[r][0..n) <- sum_{r ascending} bufs[r] (collectives.hpp:27-52).
 void sum_ranks_f32(float* const* bufs, int nranks, int64_t n, float scale, cudaStream_t s);
+void sum_ranks_bf16(bf16* const* bufs, int nranks, int64_t n, float scale, cudaStream_t s);
 
 // init_transformer_params on the device (model.hpp:49-70 + rng.hpp:15-91): element (r, c) of
 // the FULL [rows, cols] tensor takes normal draw number base_draw/2 + r*cols + c of the stream

@@ -70,6 +70,10 @@ Model::Model(const ModelSpec& spec, const Plan& plan, Mesh* mesh, int batch, int
   cuda_check(cudaSetDevice(mesh->cuda_device), "cudaSetDevice");
   cuda_check(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "cudaStreamCreate");
   cuda_check(cudaStreamCreateWithFlags(&comm_stream_, cudaStreamNonBlocking), "cudaStreamCreate");
+  {
+    const char* e = std::getenv("SW_AR_BF16");
+    ar_bf16_ = mesh_->mp > 1 && e != nullptr && e[0] == '1';
+  }
   build_layout();
   allocate();
   // all-reduce pipelining depth (SW_AR_CHUNKS overrides): 4 row chunks when they stay 128-aligned
@@ -311,6 +315,7 @@ void Model::allocate() {
     R.loss = alloc<double>(1);
     R.part = alloc<float>(M * d_);
     R.dx = alloc<float>(M * d_);
+    if (ar_bf16_) R.arb = alloc<bf16>(M * d_);
     R.gres = alloc<float>(M * d_);
     R.gb = alloc<bf16>(M * d_);
     R.dpre = alloc<bf16>(M * fl_ * (spec_.swiglu ? 2 : 1));
@@ -554,6 +559,62 @@ void Model::ar_mp_ptrs(std::vector<Rank*>& grp, const std::vector<float*>& ptrs,
   mesh_->record(CollKind::kAllReduce, mesh_->mp_group(grp[0]->dpi), static_cast<uint64_t>(n) * 4);
 }
 
+void Model::ar_mp_ptrs(std::vector<Rank*>& grp, const std::vector<bf16*>& ptrs, int64_t n, cudaStream_t s) {
+  if (mesh_->mp == 1) return;
+  const double t = mesh_->mp;
+  tic(s);
+  if (mesh_->emulated) {
+    k::sum_ranks_bf16(ptrs.data(), static_cast<int>(ptrs.size()), n, 1.0f, s);
+    ++launches_;
+  } else {
+    nccl_check(ncclAllReduce(ptrs[0], ptrs[0], n, ncclBfloat16, ncclSum, mesh_->mp_comm, s), "AllReduce(bf16)");
+  }
+  toc(kProfComm, 2.0 * (t - 1) / t * 2.0 * n, s);  // NCCL bus bytes
+  mesh_->record(CollKind::kAllReduce, mesh_->mp_group(grp[0]->dpi), static_cast<uint64_t>(n) * 2);
+}
+
+void Model::row_parallel_ar(std::vector<Rank*>& grp, bf16* Rank::*buf, int width, const RowFn& produce,
+                            const RowFn& consume) {
+  const int C = ar_chunks_;
+  const int64_t rows = M_ / C;
+  for (int c = 0; c < C; ++c) {
+    for (Rank* R : grp) produce(*R, c * rows, rows);
+    cuda_check(cudaEventRecord(ev_prod_[c], stream_), "cudaEventRecord");
+    cuda_check(cudaStreamWaitEvent(comm_stream_, ev_prod_[c], 0), "cudaStreamWaitEvent");
+    std::vector<bf16*> ptrs;
+    for (Rank* R : grp) ptrs.push_back(R->*buf + c * rows * width);
+    ar_mp_ptrs(grp, ptrs, rows * width, comm_stream_);
+    cuda_check(cudaEventRecord(ev_ar_[c], comm_stream_), "cudaEventRecord");
+  }
+  for (int c = 0; c < C; ++c) {
+    cuda_check(cudaStreamWaitEvent(stream_, ev_ar_[c], 0), "cudaStreamWaitEvent");
+    for (Rank* R : grp) consume(*R, c * rows, rows);
+  }
+}
+
+void Model::row_ar(std::vector<Rank*>& grp, float* Rank::*f32buf, const std::function<const bf16*(Rank&)>& a,
+                   int64_t lda, int K, int w_slot, int b_mn, const ConsFn& consume) {
+  const int d = d_;
+  const int64_t ldb = b_mn ? d : K;
+  if (ar_bf16_) {
+    row_parallel_ar(
+        grp, &Rank::arb, d,
+        [&](Rank& R, int64_t r0, int64_t rows) {
+          gemm(R, static_cast<int>(rows), d, K, a(R) + r0 * lda, lda, 0, W(R, w_slot), ldb, b_mn,
+               static_cast<int>(Epi::kStoreBf16), R.arb + r0 * d, d);
+        },
+        [&](Rank& R, int64_t r0, int64_t rows) { consume(R, r0, rows, nullptr, R.arb + r0 * d); });
+  } else {
+    row_parallel_ar(
+        grp, f32buf, d,
+        [&](Rank& R, int64_t r0, int64_t rows) {
+          gemm(R, static_cast<int>(rows), d, K, a(R) + r0 * lda, lda, 0, W(R, w_slot), ldb, b_mn,
+               static_cast<int>(Epi::kStoreF32), R.*f32buf + r0 * d, d);
+        },
+        [&](Rank& R, int64_t r0, int64_t rows) { consume(R, r0, rows, R.*f32buf + r0 * d, nullptr); });
+  }
+}
+
 void Model::row_parallel_ar(std::vector<Rank*>& grp, float* Rank::*buf, int width, const RowFn& produce,
                             const RowFn& consume) {
   const int C = ar_chunks_;
@@ -687,15 +748,13 @@ void Model::forward_replica(std::vector<Rank*>& grp, bool need_grad) {
              static_cast<int>(Epi::kResidF32), R->hmid[l], d, nullptr, 0, P(*R, ls.o_b), R->hs[l], d);
       }
     } else {
-      row_parallel_ar(
-          grp, &Rank::part, d,
-          [&](Rank& R, int64_t r0, int64_t rows) {
-            gemm(R, static_cast<int>(rows), d, dl, R.o[l] + r0 * dl, dl, 0, W(R, ls.o_k), dl, 0,
-                 static_cast<int>(Epi::kStoreF32), R.part + r0 * d, d);
-          },
-          [&](Rank& R, int64_t r0, int64_t rows) {
-            k::add_residual_bias(R.hs[l] + r0 * d, R.part + r0 * d, P(R, ls.o_b), R.hmid[l] + r0 * d, rows, d,
-                                 stream_);
+      row_ar(
+          grp, &Rank::part, [&](Rank& R) -> const bf16* { return R.o[l]; }, dl, dl, ls.o_k, 0,
+          [&](Rank& R, int64_t r0, int64_t rows, const float* f32, const bf16* b16) {
+            if (b16 != nullptr)
+              k::add_residual_bias(R.hs[l] + r0 * d, b16, P(R, ls.o_b), R.hmid[l] + r0 * d, rows, d, stream_);
+            else
+              k::add_residual_bias(R.hs[l] + r0 * d, f32, P(R, ls.o_b), R.hmid[l] + r0 * d, rows, d, stream_);
             ++launches_;
           });
     }
@@ -720,15 +779,15 @@ void Model::forward_replica(std::vector<Rank*>& grp, bool need_grad) {
              static_cast<int>(Epi::kResidF32), R->hs[l + 1], d, nullptr, 0, Pn(*R, ls.fc2_b), R->hmid[l], d);
       }
     } else {
-      row_parallel_ar(
-          grp, &Rank::part, d,
-          [&](Rank& R, int64_t r0, int64_t rows) {
-            gemm(R, static_cast<int>(rows), d, fl, R.act[l] + r0 * fl, fl, 0, W(R, ls.fc2_k), fl, 0,
-                 static_cast<int>(Epi::kStoreF32), R.part + r0 * d, d);
-          },
-          [&](Rank& R, int64_t r0, int64_t rows) {
-            k::add_residual_bias(R.hmid[l] + r0 * d, R.part + r0 * d, Pn(R, ls.fc2_b), R.hs[l + 1] + r0 * d, rows,
-                                 d, stream_);
+      row_ar(
+          grp, &Rank::part, [&](Rank& R) -> const bf16* { return R.act[l]; }, fl, fl, ls.fc2_k, 0,
+          [&](Rank& R, int64_t r0, int64_t rows, const float* f32, const bf16* b16) {
+            if (b16 != nullptr)
+              k::add_residual_bias(R.hmid[l] + r0 * d, b16, Pn(R, ls.fc2_b), R.hs[l + 1] + r0 * d, rows, d,
+                                   stream_);
+            else
+              k::add_residual_bias(R.hmid[l] + r0 * d, f32, Pn(R, ls.fc2_b), R.hs[l + 1] + r0 * d, rows, d,
+                                   stream_);
             ++launches_;
           });
     }
@@ -868,7 +927,20 @@ void Model::backward_replica(std::vector<Rank*>& grp, bool accumulate) {
       ++launches_;
     };
     if (th_ > 1) {
-      row_parallel_ar(grp, &Rank::dx, d, prod, cons);
+      row_ar(grp, &Rank::dx, [&](Rank& R) -> const bf16* { return R.logits; }, ldv_, vl_, head, 1,
+             [&](Rank& R, int64_t r0, int64_t rows, const float* f32, const bf16* b16) {
+               tic();
+               if (b16 != nullptr)
+                 k::layernorm_bwd(R.hs[L_] + r0 * d, R.statsf + r0, R.statsf + M + r0, P(R, lnf_s_), b16,
+                                  R.gres + r0 * d, R.gb + r0 * d, G(R, lnf_s_), Gn(R, lnf_b_), rows, d, 0, stream_,
+                                  R.ln_partials, spec_.rmsnorm);
+               else
+                 k::layernorm_bwd(R.hs[L_] + r0 * d, R.statsf + r0, R.statsf + M + r0, P(R, lnf_s_), f32,
+                                  R.gres + r0 * d, R.gb + r0 * d, G(R, lnf_s_), Gn(R, lnf_b_), rows, d, 0, stream_,
+                                  R.ln_partials, spec_.rmsnorm);
+               toc(kProfNorm, 18.0 * rows * d);
+               ++launches_;
+             });
     } else {
       for (Rank* R : grp) prod(*R, 0, M);
       for (Rank* R : grp) cons(*R, 0, M);
@@ -918,7 +990,20 @@ void Model::backward_replica(std::vector<Rank*>& grp, bool accumulate) {
         ++launches_;
       };
       if (tm_ > 1) {
-        row_parallel_ar(grp, &Rank::dx, d, prod, cons);
+        row_ar(grp, &Rank::dx, [&](Rank& R) -> const bf16* { return R.dpre; }, fw, fw, fk, 1,
+               [&](Rank& R, int64_t r0, int64_t rows, const float* f32, const bf16* b16) {
+                 tic();
+                 if (b16 != nullptr)
+                   k::layernorm_bwd(R.hmid[l] + r0 * d, R.stats2[l] + r0, R.stats2[l] + M + r0, P(R, ls.ln2_s), b16,
+                                    R.gres + r0 * d, R.gb + r0 * d, G(R, ls.ln2_s), Gn(R, ls.ln2_b), rows, d, 1,
+                                    stream_, R.ln_partials, spec_.rmsnorm);
+                 else
+                   k::layernorm_bwd(R.hmid[l] + r0 * d, R.stats2[l] + r0, R.stats2[l] + M + r0, P(R, ls.ln2_s), f32,
+                                    R.gres + r0 * d, R.gb + r0 * d, G(R, ls.ln2_s), Gn(R, ls.ln2_b), rows, d, 1,
+                                    stream_, R.ln_partials, spec_.rmsnorm);
+                 toc(kProfNorm, 18.0 * rows * d);
+                 ++launches_;
+               });
       } else {
         for (Rank* R : grp) prod(*R, 0, M);
         for (Rank* R : grp) cons(*R, 0, M);
@@ -955,7 +1040,20 @@ void Model::backward_replica(std::vector<Rank*>& grp, bool accumulate) {
         ++launches_;
       };
       if (ta_ > 1) {
-        row_parallel_ar(grp, &Rank::dx, d, prod, cons);
+        row_ar(grp, &Rank::dx, [&](Rank& R) -> const bf16* { return R.dqkv; }, 3 * dl, 3 * dl, ls.q_k, 1,
+               [&](Rank& R, int64_t r0, int64_t rows, const float* f32, const bf16* b16) {
+                 tic();
+                 if (b16 != nullptr)
+                   k::layernorm_bwd(R.hs[l] + r0 * d, R.stats1[l] + r0, R.stats1[l] + M + r0, P(R, ls.ln1_s), b16,
+                                    R.gres + r0 * d, R.gb + r0 * d, G(R, ls.ln1_s), Gn(R, ls.ln1_b), rows, d, 1,
+                                    stream_, R.ln_partials, spec_.rmsnorm);
+                 else
+                   k::layernorm_bwd(R.hs[l] + r0 * d, R.stats1[l] + r0, R.stats1[l] + M + r0, P(R, ls.ln1_s), f32,
+                                    R.gres + r0 * d, R.gb + r0 * d, G(R, ls.ln1_s), Gn(R, ls.ln1_b), rows, d, 1,
+                                    stream_, R.ln_partials, spec_.rmsnorm);
+                 toc(kProfNorm, 18.0 * rows * d);
+                 ++launches_;
+               });
       } else {
         for (Rank* R : grp) prod(*R, 0, M);
         for (Rank* R : grp) cons(*R, 0, M);

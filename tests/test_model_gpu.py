@@ -146,8 +146,11 @@ def test_forward_backward_matches_oracle(spec_name, dp, mp, batch, seq):
         check_grads(model, spec, acc, tol)
 
 
-def test_tensor_parallel_invariance():
-    """The sharded step equals the unsharded one (what audit_equivalence checks, audit.hpp:78)."""
+@pytest.mark.parametrize("ar_bf16", [1, 0])
+def test_tensor_parallel_invariance(ar_bf16, monkeypatch):
+    """The sharded step equals the unsharded one (what audit_equivalence checks, audit.hpp:78),
+    with the row-parallel all-reduce payloads in fp32 (the default) and in bf16 (SW_AR_BF16=1)."""
+    monkeypatch.setenv("SW_AR_BF16", str(ar_bf16))
     spec = spec_of("tiny.spec")
     tokens, targets, weights = rng_ref.audit_batch(42, 0, 4, 128, spec.vocab_size)
     res = {}
@@ -167,7 +170,7 @@ def test_tensor_parallel_invariance():
             # chunks (M = 512 tokens); 4 bias-grad AG/layer
             chunks = 4
             assert int(ar[1]) == 4 * spec.n_layers * chunks and int(ag[1]) == 4 * spec.n_layers
-            assert int(ar[2]) == 4 * spec.n_layers * 512 * spec.d_model * 4
+            assert int(ar[2]) == 4 * spec.n_layers * 512 * spec.d_model * (2 if ar_bf16 else 4)
     for mp in (2, 4):
         assert abs(res[mp][0] - res[1][0]) / res[1][0] < 2e-4
         for n in res[1][1]:
