@@ -69,6 +69,14 @@ SW_API sw_status sw_model_spec_overrides(const sw_model_spec* spec, char** text_
 /* Extension keys (not in the reference's spec language): mlp = gelu|swiglu,
  * norm = layernorm|rmsnorm. */
 SW_API sw_status sw_model_spec_variant(const sw_model_spec* spec, int* swiglu, int* rmsnorm);
+/* Extension: arch = t5 encoder-decoder. out = {is_t5, n_dec_layers, d_kv,
+ * rel_buckets, rel_max_distance}. The reference has no encoder-decoder model; the T5 tree is
+ * named with its attn / cross_attn / mlp scopes so derive_plan (plan.cpp:39-91) plans it. */
+SW_API sw_status sw_model_spec_t5(const sw_model_spec* spec, int64_t out[5]);
+/* T5 relative-position bucket ids [tq, tk] (rp = key - query) for a bidirectional (encoder)
+ * or causal (decoder) stack. */
+SW_API sw_status sw_t5_rel_buckets(int64_t tq, int64_t tk, int bidirectional, int num_buckets,
+                                   int max_distance, int32_t* out);
 SW_API void sw_model_spec_free(sw_model_spec* spec);
 
 /* Replaces transformer_param_shapes (model.hpp:17-43): "name\td0,d1\n" in tree order. */

@@ -93,8 +93,37 @@ def normals_exact(rng: RngStream, n: int) -> np.ndarray:
     return out
 
 
+def t5_param_shapes(spec: dict):
+    """Extension: the T5 encoder-decoder tree, named with the reference's
+    attn / cross_attn / mlp scopes (roles.cpp:36-43) so its rule engine plans it. Per block:
+    ln1, attn q/k/v [H*d_kv, d], o [d, H*d_kv], (block 0 only) attn/rel_bias [buckets, H],
+    decoder ln_x + cross_attn, ln2, mlp fc1 [d_ff, d] / fc2 [d, d_ff]; no biases; RMSNorm scales."""
+    d, V, H = spec["d_model"], spec["vocab_size"], spec["n_heads"]
+    inner = H * spec["d_kv"]
+    out = [("embed/tok/kernel", (V, d))]
+
+    def attn(b, scope):
+        return [(b + f"{scope}/{p}/kernel", (inner, d)) for p in "qkv"] + [(b + f"{scope}/o/kernel", (d, inner))]
+
+    for st, layers, dec in (("enc", spec["n_layers"], False), ("dec", spec["n_dec_layers"], True)):
+        for l in range(layers):
+            b = f"{st}/block_{l}/"
+            out += [(b + "ln1/scale", (d,))] + attn(b, "attn")
+            if l == 0:
+                out.append((b + "attn/rel_bias/kernel", (spec.get("rel_buckets", 32), H)))
+            if dec:
+                out += [(b + "ln_x/scale", (d,))] + attn(b, "cross_attn")
+            out += [(b + "ln2/scale", (d,)), (b + "mlp/fc1/kernel", (spec["d_ff"], d)),
+                    (b + "mlp/fc2/kernel", (d, spec["d_ff"]))]
+        out.append((f"{st}/final_ln/scale", (d,)))
+    out.append(("lm_head/kernel", (V, d)))
+    return out
+
+
 def transformer_param_shapes(spec: dict):
     """model.hpp:17-43 (tree order); mlp = swiglu / norm = rmsnorm extension leaves."""
+    if spec.get("arch", "decoder") == "t5":
+        return t5_param_shapes(spec)
     d, V = spec["d_model"], spec["vocab_size"]
     rms = spec.get("norm", "layernorm") == "rmsnorm"
     swiglu = spec.get("mlp", "gelu") == "swiglu"

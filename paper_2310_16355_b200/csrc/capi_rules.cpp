@@ -88,6 +88,24 @@ sw_status sw_model_spec_variant(const sw_model_spec* spec, int* swiglu, int* rms
   });
 }
 
+sw_status sw_model_spec_t5(const sw_model_spec* spec, int64_t out[5]) {
+  return sw::guarded([&] {
+    require(spec, "spec");
+    const sw::ModelSpec& s = spec->spec;
+    const int64_t v[5] = {s.t5 ? 1 : 0, s.n_dec_layers, s.d_kv, s.rel_buckets, s.rel_max_distance};
+    std::memcpy(out, v, sizeof(v));
+  });
+}
+
+sw_status sw_t5_rel_buckets(int64_t tq, int64_t tk, int bidirectional, int num_buckets, int max_distance,
+                            int32_t* out) {
+  return sw::guarded([&] {
+    require(out, "out");
+    for (int64_t i = 0; i < tq; ++i)
+      for (int64_t j = 0; j < tk; ++j) out[i * tk + j] = sw::t5_rel_bucket(j - i, bidirectional != 0, num_buckets, max_distance);
+  });
+}
+
 sw_status sw_model_spec_overrides(const sw_model_spec* spec, char** text_out) {
   return sw::guarded([&] {
     require(spec, "spec");

@@ -7,6 +7,7 @@
 #include "rules.h"
 
 #include <algorithm>
+#include <cmath>
 #include <array>
 #include <cctype>
 #include <map>
@@ -467,6 +468,22 @@ ModelSpec parse_model_spec(const std::string& text) {
       } else {
         fail(SW_ERR_CONFIG, where + quote(key) + " needs layernorm or rmsnorm, got " + quote(value));
       }
+    } else if (key == "arch") {  // extension key (T5 encoder-decoder, BASELINE cfg4)
+      if (value == "decoder") {
+        spec.t5 = false;
+      } else if (value == "t5") {
+        spec.t5 = true;
+      } else {
+        fail(SW_ERR_CONFIG, where + quote(key) + " needs decoder or t5, got " + quote(value));
+      }
+    } else if (key == "n_dec_layers") {
+      spec.n_dec_layers = static_cast<int>(as_int());
+    } else if (key == "d_kv") {
+      spec.d_kv = as_int();
+    } else if (key == "rel_buckets") {
+      spec.rel_buckets = static_cast<int>(as_int());
+    } else if (key == "rel_max_distance") {
+      spec.rel_max_distance = static_cast<int>(as_int());
     } else {
       fail(SW_ERR_CONFIG, where + "unknown key " + quote(key));
     }
@@ -484,10 +501,78 @@ ModelSpec parse_model_spec(const std::string& text) {
     fail(SW_ERR_CONFIG, "model spec: d_model " + std::to_string(spec.d_model) +
                             " is not divisible by n_heads " + std::to_string(spec.n_heads));
   }
+  const bool t5_keys = std::find(seen.begin(), seen.end(), "n_dec_layers") != seen.end() ||
+                       std::find(seen.begin(), seen.end(), "d_kv") != seen.end() ||
+                       std::find(seen.begin(), seen.end(), "rel_buckets") != seen.end() ||
+                       std::find(seen.begin(), seen.end(), "rel_max_distance") != seen.end();
+  if (spec.t5) {
+    if (spec.n_dec_layers < 1 || spec.d_kv < 1 || spec.rel_buckets < 4 || spec.rel_buckets % 2 != 0 ||
+        spec.rel_max_distance < spec.rel_buckets) {
+      fail(SW_ERR_CONFIG, "model spec: arch = t5 needs n_dec_layers >= 1, d_kv >= 1, an even rel_buckets >= 4 "
+                          "and rel_max_distance >= rel_buckets");
+    }
+    if (spec.tie_embeddings || spec.swiglu) {
+      fail(SW_ERR_CONFIG, "model spec: arch = t5 has its own lm_head and a ReLU MLP "
+                          "(tie_embeddings / mlp = swiglu are not supported)");
+    }
+    spec.rmsnorm = true;  // T5LayerNorm: scale only, no centring
+  } else if (t5_keys) {
+    fail(SW_ERR_CONFIG, "model spec: n_dec_layers / d_kv / rel_buckets / rel_max_distance need arch = t5");
+  }
   return spec;
 }
 
+int t5_rel_bucket(int64_t rp, bool bidirectional, int num_buckets, int max_distance) {
+  int ret = 0;
+  int64_t n = 0;
+  if (bidirectional) {
+    num_buckets /= 2;
+    if (rp > 0) ret += num_buckets;
+    n = rp < 0 ? -rp : rp;
+  } else {
+    n = rp < 0 ? -rp : 0;
+  }
+  const int max_exact = num_buckets / 2;
+  if (n < max_exact) return ret + static_cast<int>(n);
+  const double x = std::log(static_cast<double>(n) / max_exact) / std::log(static_cast<double>(max_distance) / max_exact) *
+                   (num_buckets - max_exact);
+  int large = max_exact + static_cast<int>(std::floor(x + 1e-9));
+  if (large > num_buckets - 1) large = num_buckets - 1;
+  return ret + large;
+}
+
+static std::vector<NamedShape> t5_param_shapes(const ModelSpec& spec) {
+  const int64_t d = spec.d_model, inner = spec.n_heads * spec.d_kv;
+  std::vector<NamedShape> out;
+  out.push_back({"embed/tok/kernel", {spec.vocab_size, d}});
+  auto attn = [&](const std::string& b, const char* scope) {
+    for (const char* proj : {"q", "k", "v"}) out.push_back({b + scope + "/" + proj + "/kernel", {inner, d}});
+    out.push_back({b + scope + "/o/kernel", {d, inner}});
+  };
+  auto stack = [&](const std::string& st, int layers, bool decoder) {
+    for (int l = 0; l < layers; ++l) {
+      const std::string b = st + "/block_" + std::to_string(l) + "/";
+      out.push_back({b + "ln1/scale", {d}});
+      attn(b, "attn");
+      if (l == 0) out.push_back({b + "attn/rel_bias/kernel", {spec.rel_buckets, spec.n_heads}});
+      if (decoder) {
+        out.push_back({b + "ln_x/scale", {d}});
+        attn(b, "cross_attn");
+      }
+      out.push_back({b + "ln2/scale", {d}});
+      out.push_back({b + "mlp/fc1/kernel", {spec.d_ff, d}});
+      out.push_back({b + "mlp/fc2/kernel", {d, spec.d_ff}});
+    }
+    out.push_back({st + "/final_ln/scale", {d}});
+  };
+  stack("enc", spec.n_layers, false);
+  stack("dec", spec.n_dec_layers, true);
+  out.push_back({"lm_head/kernel", {spec.vocab_size, d}});
+  return out;
+}
+
 std::vector<NamedShape> transformer_param_shapes(const ModelSpec& spec) {
+  if (spec.t5) return t5_param_shapes(spec);
   // model.hpp:17-43 tree order; the mlp/norm extension keys swap in the SwiGLU / RMSNorm leaves
   const int64_t d = spec.d_model;
   std::vector<NamedShape> out;

@@ -85,8 +85,25 @@ struct ModelSpec {
   // LayerNorm an RMSNorm (scale only).
   bool swiglu = false;
   bool rmsnorm = false;
+  // Extension (BASELINE cfg4): `arch = t5` selects a T5 encoder-decoder
+  // (T5 v1.0 layer: RMSNorm, unscaled attention with bucketed relative-position bias shared by a
+  // stack's layers, ReLU MLP, no biases, separate lm_head) named with the reference's scopes
+  // (attn / cross_attn / mlp), so the reference rules plan it: n_layers encoder and n_dec_layers
+  // decoder blocks, head dim d_kv (inner width n_heads * d_kv), rel_buckets / rel_max_distance.
+  bool t5 = false;
+  int n_dec_layers = 0;
+  int64_t d_kv = 0;
+  int rel_buckets = 32;
+  int rel_max_distance = 128;
   std::vector<RoleOverride> overrides;
 };
+
+// T5 relative-position bucket (the HF T5 `_relative_position_bucket` rule): rp = key - query;
+// bidirectional (encoder) halves the buckets between rp < 0 and rp > 0; unidirectional
+// (decoder) buckets only rp <= 0. Small |rp| map exactly, larger ones log-spaced up to
+// max_distance. Evaluated in double with a 1e-9 guard before truncation so host and oracle
+// agree at the log-spaced boundaries.
+int t5_rel_bucket(int64_t rp, bool bidirectional, int num_buckets, int max_distance);
 
 ModelSpec parse_model_spec(const std::string& text);
 std::vector<NamedShape> transformer_param_shapes(const ModelSpec& spec);

@@ -31,6 +31,10 @@ def _declare():
     L.sw_model_spec_overrides.argtypes = [vp, out_str]
     L.sw_model_spec_variant.argtypes = [vp, C.POINTER(C.c_int), C.POINTER(C.c_int)]
     L.sw_model_spec_variant.restype = C.c_int
+    L.sw_model_spec_t5.argtypes = [vp, C.POINTER(C.c_int64)]
+    L.sw_model_spec_t5.restype = C.c_int
+    L.sw_t5_rel_buckets.argtypes = [C.c_int64, C.c_int64, C.c_int, C.c_int, C.c_int, vp]
+    L.sw_t5_rel_buckets.restype = C.c_int
     L.sw_model_spec_free.argtypes = [vp]
     L.sw_model_spec_free.restype = None
     L.sw_transformer_param_shapes.argtypes = [vp, out_str]
@@ -91,6 +95,12 @@ class ModelSpec:
     overrides: list = field(default_factory=list)  # [(pattern, role_name)]
     mlp: str = "gelu"          # extension key: gelu | swiglu
     norm: str = "layernorm"    # extension key: layernorm | rmsnorm
+    # extension: arch = t5 encoder-decoder
+    arch: str = "decoder"
+    n_dec_layers: int = 0
+    d_kv: int = 0
+    rel_buckets: int = 32
+    rel_max_distance: int = 128
     _handle: object = field(default=None, repr=False, compare=False)
 
     def __del__(self):
@@ -109,7 +119,10 @@ class ModelSpec:
                  f"tie_embeddings = {'true' if self.tie_embeddings else 'false'}"]
         if self.mlp != "gelu":
             lines.append(f"mlp = {self.mlp}")
-        if self.norm != "layernorm":
+        if self.arch == "t5":
+            lines += ["arch = t5", f"n_dec_layers = {self.n_dec_layers}", f"d_kv = {self.d_kv}",
+                      f"rel_buckets = {self.rel_buckets}", f"rel_max_distance = {self.rel_max_distance}"]
+        elif self.norm != "layernorm":
             lines.append(f"norm = {self.norm}")
         lines += [f"role {p} = {r}" for p, r in self.overrides]
         return "\n".join(lines) + "\n"
@@ -126,9 +139,22 @@ def parse_model_spec(text: str) -> ModelSpec:
     ovr = [tuple(ln.split("\t")) for ln in _take(s).splitlines() if ln]
     sg, rn = C.c_int(), C.c_int()
     _lib.check(L.sw_model_spec_variant(h, C.byref(sg), C.byref(rn)))
+    t5 = (C.c_int64 * 5)()
+    _lib.check(L.sw_model_spec_t5(h, t5))
     return ModelSpec(int(dims[0]), int(dims[1]), int(dims[2]), int(dims[3]), int(dims[4]),
                      int(dims[5]), bool(dims[6]), ovr, "swiglu" if sg.value else "gelu",
-                     "rmsnorm" if rn.value else "layernorm", h)
+                     "rmsnorm" if rn.value else "layernorm", "t5" if t5[0] else "decoder", int(t5[1]), int(t5[2]),
+                     int(t5[3]), int(t5[4]), h)
+
+
+def t5_rel_buckets(tq: int, tk: int, bidirectional: bool, num_buckets: int, max_distance: int):
+    """Bucket ids [tq, tk] of the T5 relative-position bias (host rule engine, rules.h)."""
+    import numpy as np
+
+    out = np.zeros((tq, tk), np.int32)
+    _lib.check(_declare().sw_t5_rel_buckets(tq, tk, int(bidirectional), num_buckets, max_distance,
+                                            out.ctypes.data))
+    return out
 
 
 def read_model_spec(path: str) -> ModelSpec:

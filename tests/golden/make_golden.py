@@ -302,7 +302,8 @@ def gen_ext_plans(tmp):
     sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
     from oracle import rng_ref  # noqa: E402
     cases = []
-    for spec_name, n_list in (("mini_swiglu.spec", (1, 2, 4)), ("llama7b_swiglu.spec", (1, 2, 4, 8))):
+    for spec_name, n_list in (("mini_swiglu.spec", (1, 2, 4)), ("llama7b_swiglu.spec", (1, 2, 4, 8)),
+                              ("mini_t5.spec", (1, 2, 4)), ("t5_11b.spec", (1, 2, 4, 8))):
         kv, ovr = {}, []
         for ln in open(os.path.join(SPECS, spec_name)):
             ln = ln.split("#")[0].strip()
@@ -312,7 +313,7 @@ def gen_ext_plans(tmp):
             if k.startswith("role "):
                 ovr.append((k[5:].strip(), v))
             else:
-                kv[k] = v if k in ("mlp", "norm") else int(v)
+                kv[k] = v if k in ("mlp", "norm", "arch") else int(v)
         shapes = [(n, list(sh)) for n, sh in rng_ref.transformer_param_shapes(kv)]
         sp = write(tmp, "shapes.tsv", shapes_tsv(shapes))
         args_o = [write(tmp, "ovr.tsv", "".join(f"{p}\t{r}\n" for p, r in ovr))] if ovr else []
