@@ -213,6 +213,41 @@ SW_API sw_status sw_model_read_profile(sw_model* model, double ms[8], double wor
 /* Bytes of device memory held by this process's model state and activations. */
 SW_API sw_status sw_model_device_bytes(sw_model* model, int64_t* out);
 
+/* ==========================================================================================
+ * Extension (BASELINE cfg4): T5 encoder-decoder step. The reference has no
+ * encoder-decoder; the program is oracle/t5_ref.py's composition of the reference's ops, run
+ * under the plan derive_plan (plan.cpp:39-91) gives the T5 tree (arch = t5 spec). dp = 1,
+ * tensor parallel over the mesh's mp axis, replicated lm_head.
+ * ========================================================================================== */
+typedef struct sw_t5 sw_t5;
+/* batch rows of enc_len encoder tokens and dec_len decoder tokens (<= max_seq_len). */
+SW_API sw_status sw_t5_create(const sw_model_spec* spec, const sw_plan* plan, sw_mesh* mesh, int batch,
+                              int enc_len, int dec_len, sw_t5** out);
+SW_API void sw_t5_free(sw_t5* model);
+/* init_transformer_params' rules (model.hpp:49-70) over the T5 tree, same device stream. */
+SW_API sw_status sw_t5_init_params(sw_t5* model, uint64_t seed, const char* stream_name);
+/* which: 0 param (+ bf16 shadow), 2 adam_m, 3 adam_v (set); 0..3 incl. 1 grad (get). */
+SW_API sw_status sw_t5_set_tensor(sw_t5* model, const char* name, int which, const float* full,
+                                  int64_t numel);
+SW_API sw_status sw_t5_get_tensor(sw_t5* model, const char* name, int which, float* full_out,
+                                  int64_t numel);
+/* enc_tokens [batch, enc_len]; dec_tokens / targets / weights [batch, dec_len]; weights may be
+ * NULL (all ones). */
+SW_API sw_status sw_t5_stage_batch(sw_t5* model, const int32_t* enc_tokens, const int32_t* dec_tokens,
+                                   const int32_t* targets, const float* weights);
+/* Weighted-mean cross entropy and every parameter gradient (written, not accumulated). */
+SW_API sw_status sw_t5_forward_backward(sw_t5* model);
+/* Decoder logits [batch * dec_len, vocab] of the staged batch. */
+SW_API sw_status sw_t5_forward_logits(sw_t5* model, float* logits_out);
+SW_API sw_status sw_t5_adamw_step(sw_t5* model, const sw_adamw_cfg* cfg);
+SW_API sw_status sw_t5_train_step(sw_t5* model, const sw_adamw_cfg* cfg);
+SW_API sw_status sw_t5_last_loss(sw_t5* model, double* loss_out);
+SW_API sw_status sw_t5_stream(sw_t5* model, void** stream_out);
+SW_API sw_status sw_t5_set_profiling(sw_t5* model, int enable);
+SW_API sw_status sw_t5_read_profile(sw_t5* model, double ms[8], double work[8], int64_t count[8]);
+SW_API sw_status sw_t5_launch_count(sw_t5* model, int64_t* out);
+SW_API sw_status sw_t5_device_bytes(sw_t5* model, int64_t* out);
+
 /* Greedy next-token generation: the Predictor loop of cli.cpp:425-447 (window of the last
  * seq_len tokens, argmax at the newest position, kernels.hpp:515-527 first-maximum rule) for
  * `batch` rows of P prompt tokens each, n_new tokens per row -> out [batch, n_new]. While the

@@ -79,10 +79,13 @@ def attention_fwd(q, k, v, bias=None, causal=False):
     return P @ v, P
 
 
-def attention_bwd(q, k, v, P, dout):
+def attention_bwd(q, k, v, P, dout, o_stored=None):
+    """delta = rowsum(dP * P); with o_stored (bf16_acts) the flash form rowsum(dO * O) over the
+    stored output, as the device computes it (model_ref does the same)."""
     dP = dout @ v.transpose(0, 1, 3, 2)
     dv = P.transpose(0, 1, 3, 2) @ dout
-    dS = P * (dP - (dP * P).sum(-1, keepdims=True))
+    delta = (dP * P).sum(-1, keepdims=True) if o_stored is None else (dout * o_stored).sum(-1, keepdims=True)
+    dS = P * (dP - delta)
     return dS @ k, dS.transpose(0, 1, 3, 2) @ q, dv, dS
 
 
@@ -187,7 +190,7 @@ def forward_backward(params: dict, spec: dict, enc_tokens, dec_tokens, targets, 
         dyf = R(dy.reshape(-1, d))
         grads[pre + f"{scope}/o/kernel"] = dyf.T @ om.reshape(-1, om.shape[-1])
         dom = R(dyf.reshape(dy.shape) @ p[pre + f"{scope}/o/kernel"])
-        dq, dk, dv, dS = attention_bwd(q, k, v, P, _heads(dom, H))
+        dq, dk, dv, dS = attention_bwd(q, k, v, P, _heads(dom, H), _heads(om, H) if bf16_acts else None)
         if ids is not None:
             scatter_bias(st, ids, dS)
         dqf, dkf, dvf = (R(_merge(t)) for t in (dq, dk, dv))

@@ -4,6 +4,7 @@
 
 #include "mesh.h"
 #include "model.h"
+#include "t5.h"
 #include "status.h"
 
 struct sw_model_spec {
@@ -17,6 +18,9 @@ struct sw_mesh {
 };
 struct sw_model {
   sw::Model* model;
+};
+struct sw_t5 {
+  sw::T5Model* model;
 };
 
 namespace {
@@ -378,5 +382,143 @@ sw_status sw_checkpoint_write(const char* path, uint64_t step, uint64_t seed, ui
 }
 
 void sw_checkpoint_free(sw_checkpoint* ck) { delete ck; }
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------------------------
+// T5 encoder-decoder extension
+// ---------------------------------------------------------------------------------------------
+extern "C" {
+
+sw_status sw_t5_create(const sw_model_spec* spec, const sw_plan* plan, sw_mesh* mesh, int batch, int enc_len,
+                       int dec_len, sw_t5** out) {
+  return sw::guarded([&] {
+    require(spec, "spec");
+    require(plan, "plan");
+    require(mesh, "mesh");
+    require(out, "out");
+    *out = new sw_t5{new sw::T5Model(spec->spec, plan->plan, mesh->mesh, batch, enc_len, dec_len)};
+  });
+}
+
+void sw_t5_free(sw_t5* m) {
+  if (m != nullptr) {
+    delete m->model;
+    delete m;
+  }
+}
+
+sw_status sw_t5_init_params(sw_t5* m, uint64_t seed, const char* stream_name) {
+  return sw::guarded([&] {
+    require(m, "model");
+    require(stream_name, "stream_name");
+    m->model->init_params(seed, stream_name);
+  });
+}
+
+sw_status sw_t5_set_tensor(sw_t5* m, const char* name, int which, const float* full, int64_t numel) {
+  return sw::guarded([&] {
+    require(m, "model");
+    require(name, "name");
+    require(full, "full");
+    m->model->set_tensor(name, which, full, numel);
+  });
+}
+
+sw_status sw_t5_get_tensor(sw_t5* m, const char* name, int which, float* full_out, int64_t numel) {
+  return sw::guarded([&] {
+    require(m, "model");
+    require(name, "name");
+    require(full_out, "full_out");
+    m->model->get_tensor(name, which, full_out, numel);
+  });
+}
+
+sw_status sw_t5_stage_batch(sw_t5* m, const int32_t* enc_tokens, const int32_t* dec_tokens, const int32_t* targets,
+                            const float* weights) {
+  return sw::guarded([&] {
+    require(m, "model");
+    require(enc_tokens, "enc_tokens");
+    require(dec_tokens, "dec_tokens");
+    require(targets, "targets");
+    m->model->stage_batch(enc_tokens, dec_tokens, targets, weights);
+  });
+}
+
+sw_status sw_t5_forward_backward(sw_t5* m) {
+  return sw::guarded([&] {
+    require(m, "model");
+    m->model->forward_backward();
+  });
+}
+
+sw_status sw_t5_forward_logits(sw_t5* m, float* logits_out) {
+  return sw::guarded([&] {
+    require(m, "model");
+    require(logits_out, "logits_out");
+    m->model->forward_only();
+    m->model->logits_to_host(logits_out);
+  });
+}
+
+sw_status sw_t5_adamw_step(sw_t5* m, const sw_adamw_cfg* cfg) {
+  return sw::guarded([&] {
+    require(m, "model");
+    require(cfg, "cfg");
+    m->model->adamw(cfg->lr, cfg->beta1, cfg->beta2, cfg->eps, cfg->weight_decay);
+  });
+}
+
+sw_status sw_t5_train_step(sw_t5* m, const sw_adamw_cfg* cfg) {
+  return sw::guarded([&] {
+    require(m, "model");
+    require(cfg, "cfg");
+    m->model->forward_backward();
+    m->model->adamw(cfg->lr, cfg->beta1, cfg->beta2, cfg->eps, cfg->weight_decay);
+  });
+}
+
+sw_status sw_t5_last_loss(sw_t5* m, double* loss_out) {
+  return sw::guarded([&] {
+    require(m, "model");
+    require(loss_out, "loss_out");
+    *loss_out = m->model->last_loss();
+  });
+}
+
+sw_status sw_t5_stream(sw_t5* m, void** stream_out) {
+  return sw::guarded([&] {
+    require(m, "model");
+    *stream_out = m->model->stream();
+  });
+}
+
+sw_status sw_t5_set_profiling(sw_t5* m, int enable) {
+  return sw::guarded([&] {
+    require(m, "model");
+    m->model->set_profiling(enable != 0);
+  });
+}
+
+sw_status sw_t5_read_profile(sw_t5* m, double ms[8], double work[8], int64_t count[8]) {
+  return sw::guarded([&] {
+    require(m, "model");
+    m->model->read_profile(ms, work, count);
+  });
+}
+
+sw_status sw_t5_launch_count(sw_t5* m, int64_t* out) {
+  return sw::guarded([&] {
+    require(m, "model");
+    *out = m->model->launches();
+  });
+}
+
+sw_status sw_t5_device_bytes(sw_t5* m, int64_t* out) {
+  return sw::guarded([&] {
+    require(m, "model");
+    *out = m->model->device_bytes();
+  });
+}
 
 }  // extern "C"

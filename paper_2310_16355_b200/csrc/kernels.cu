@@ -56,16 +56,16 @@ __global__ void embed_fwd_kernel(const int32_t* __restrict__ ids, const float* _
   const int64_t id = ids[m];
   const int t = static_cast<int>(m % T);
   const float* a = tok + id * d;
-  const float* b = pos + static_cast<int64_t>(t) * d;
+  const float* b = pos ? pos + static_cast<int64_t>(t) * d : nullptr;  // T5: no position table
   float* o = h + m * d;
   if ((d & 3) == 0) {
     for (int i = threadIdx.x * 4; i < d; i += blockDim.x * 4) {
       float4 x = *reinterpret_cast<const float4*>(a + i);
-      float4 y = *reinterpret_cast<const float4*>(b + i);
+      float4 y = b ? *reinterpret_cast<const float4*>(b + i) : make_float4(0.f, 0.f, 0.f, 0.f);
       *reinterpret_cast<float4*>(o + i) = make_float4(x.x + y.x, x.y + y.y, x.z + y.z, x.w + y.w);
     }
   } else {
-    for (int i = threadIdx.x; i < d; i += blockDim.x) o[i] = a[i] + b[i];
+    for (int i = threadIdx.x; i < d; i += blockDim.x) o[i] = a[i] + (b ? b[i] : 0.f);
   }
 }
 

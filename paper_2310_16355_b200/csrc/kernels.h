@@ -106,6 +106,38 @@ void nonfinite_check(const float* x, int64_t n, int* flag, cudaStream_t s);
 void scale_f32(float* x, int64_t n, float a, cudaStream_t s);
 void cast_f32_bf16(const float* x, bf16* y, int64_t n, cudaStream_t s);
 
+// ---- T5 encoder-decoder extension (t5_kernels.cu) ----
+// q / k / v / o: bf16 rows of B*T tokens (row pitch ld*), head h at column h*dk; lse [B, Hl, Tq];
+// bias [Hl, Tq, Tk] fp32 or null; scores = scale * q.k (+ bias) (+ causal mask).
+struct T5AttnArgs {
+  const bf16* q = nullptr;
+  int64_t ldq = 0;
+  const bf16* k = nullptr;
+  int64_t ldk = 0;
+  const bf16* v = nullptr;
+  int64_t ldv = 0;
+  bf16* o = nullptr;
+  int64_t ldo = 0;
+  float* lse = nullptr;
+  const float* bias = nullptr;
+  int Tq = 0, Tk = 0, Hl = 0, dk = 0, causal = 0;
+  float scale = 1.f;
+};
+void t5_attention_fwd(const T5AttnArgs& a, int B, cudaStream_t s);
+// dq (bf16, pitch lddq) written; dk / dv (bf16) written from fp32 atomics; dbias (fp32
+// [Hl, Tq, Tk], may be null) accumulated. scratch: t5_attention_scratch floats.
+void t5_attention_bwd(const T5AttnArgs& a, int B, const bf16* dout, int64_t ldd, bf16* dq, int64_t lddq, bf16* dk,
+                      int64_t lddk, bf16* dv, int64_t lddv, float* scratch, float* dbias, cudaStream_t s);
+int64_t t5_attention_scratch(int B, int Hl, int Tq, int Tk, int dk);
+// bias[h, i, j] = table[ids[i, j], h0 + h] for the rank's Hl heads (table [buckets, H])
+void t5_bias_build(const float* table, const int32_t* ids, int H, int h0, int Hl, int64_t TT, float* bias,
+                   cudaStream_t s);
+// table_grad[bucket, h0 + h] += sum over positions with that bucket of dbias[h]
+void t5_bias_grad(const float* dbias, const int32_t* ids, int H, int h0, int Hl, int64_t TT, int nb,
+                  float* table_grad, cudaStream_t s);
+void relu_bf16(bf16* x, int64_t n, cudaStream_t s);
+void relu_bwd_bf16(bf16* g, const bf16* act, int64_t n, cudaStream_t s);  // g *= (act > 0)
+
 // Emulated collective: every bufs[r][0..n) <- sum_{r ascending} bufs[r] (collectives.hpp:27-52).
 void sum_ranks_f32(float* const* bufs, int nranks, int64_t n, float scale, cudaStream_t s);
 void sum_ranks_bf16(bf16* const* bufs, int nranks, int64_t n, float scale, cudaStream_t s);

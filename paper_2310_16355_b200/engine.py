@@ -58,6 +58,28 @@ def _declare():
     L.sw_model_checkpoint_rng.argtypes = [vp, C.c_uint32, C.c_char_p, C.c_uint64, u64p, u64p, u64p]
     L.sw_model_state_info.argtypes = [vp, u64p, u64p]
     L.sw_model_generate.argtypes = [vp, vp, C.c_int, C.c_int, vp]
+    L.sw_t5_create.argtypes = [vp, vp, vp, C.c_int, C.c_int, C.c_int, C.POINTER(vp)]
+    L.sw_t5_free.argtypes = [vp]
+    L.sw_t5_free.restype = None
+    L.sw_t5_init_params.argtypes = [vp, C.c_uint64, C.c_char_p]
+    L.sw_t5_set_tensor.argtypes = [vp, C.c_char_p, C.c_int, vp, C.c_int64]
+    L.sw_t5_get_tensor.argtypes = [vp, C.c_char_p, C.c_int, vp, C.c_int64]
+    L.sw_t5_stage_batch.argtypes = [vp, vp, vp, vp, vp]
+    L.sw_t5_forward_backward.argtypes = [vp]
+    L.sw_t5_forward_logits.argtypes = [vp, vp]
+    L.sw_t5_adamw_step.argtypes = [vp, C.POINTER(AdamWConfigC)]
+    L.sw_t5_train_step.argtypes = [vp, C.POINTER(AdamWConfigC)]
+    L.sw_t5_last_loss.argtypes = [vp, C.POINTER(C.c_double)]
+    L.sw_t5_stream.argtypes = [vp, C.POINTER(vp)]
+    L.sw_t5_set_profiling.argtypes = [vp, C.c_int]
+    L.sw_t5_read_profile.argtypes = [vp, C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_int64)]
+    L.sw_t5_launch_count.argtypes = [vp, C.POINTER(C.c_int64)]
+    L.sw_t5_device_bytes.argtypes = [vp, C.POINTER(C.c_int64)]
+    for fn in ("sw_t5_create", "sw_t5_init_params", "sw_t5_set_tensor", "sw_t5_get_tensor", "sw_t5_stage_batch",
+               "sw_t5_forward_backward", "sw_t5_forward_logits", "sw_t5_adamw_step", "sw_t5_train_step",
+               "sw_t5_last_loss", "sw_t5_stream", "sw_t5_set_profiling", "sw_t5_read_profile",
+               "sw_t5_launch_count", "sw_t5_device_bytes"):
+        getattr(L, fn).restype = C.c_int
     for fn in ("sw_nccl_unique_id", "sw_mesh_create", "sw_mesh_comm_report",
                "sw_mesh_reset_comm_report", "sw_model_create", "sw_model_init_params",
                "sw_model_set_param", "sw_model_get_tensor", "sw_model_stage_batch",
@@ -286,3 +308,101 @@ class Model:
         out = np.empty((p.shape[0], n_new), np.int32)
         _lib.check(_declare().sw_model_generate(self._h, p.ctypes.data, p.shape[1], n_new, out.ctypes.data))
         return out
+
+
+class T5Model:
+    """Extension (BASELINE cfg4): the T5 encoder-decoder step on the mesh with
+    the plan the reference rules give its tree (oracle/t5_ref.py is the math). dp = 1."""
+
+    PROFILE_CATEGORIES = Model.PROFILE_CATEGORIES
+
+    def __init__(self, spec: rules.ModelSpec, plan: rules.Plan, mesh: Mesh, batch: int, enc_len: int, dec_len: int):
+        L = _declare()
+        self.spec, self.plan, self.mesh = spec, plan, mesh
+        self.batch, self.enc_len, self.dec_len = batch, enc_len, dec_len
+        self.shapes = dict(rules.transformer_param_shapes(spec))
+        h = C.c_void_p()
+        _lib.check(L.sw_t5_create(spec.handle, plan.handle, mesh.handle, batch, enc_len, dec_len, C.byref(h)))
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _declare().sw_t5_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
+
+    def init_params(self, seed: int = 42, stream: str = "model-init"):
+        _lib.check(_declare().sw_t5_init_params(self._h, seed, stream.encode()))
+
+    def set_param(self, name: str, value: np.ndarray, which: int = 0):
+        a = np.ascontiguousarray(value, dtype=np.float32)
+        _lib.check(_declare().sw_t5_set_tensor(self._h, name.encode(), which, a.ctypes.data, a.size))
+
+    def _get(self, name: str, which: int) -> np.ndarray:
+        out = np.empty(self.shapes[name], np.float32)
+        _lib.check(_declare().sw_t5_get_tensor(self._h, name.encode(), which, out.ctypes.data, out.size))
+        return out
+
+    def get_param(self, name):
+        return self._get(name, 0)
+
+    def get_grad(self, name):
+        return self._get(name, 1)
+
+    def get_adam(self, name):
+        return self._get(name, 2), self._get(name, 3)
+
+    def stage_batch(self, enc_tokens, dec_tokens, targets, weights=None):
+        e = np.ascontiguousarray(enc_tokens, dtype=np.int32)
+        t = np.ascontiguousarray(dec_tokens, dtype=np.int32)
+        y = np.ascontiguousarray(targets, dtype=np.int32)
+        w = None if weights is None else np.ascontiguousarray(weights, dtype=np.float32)
+        self._staged = (e, t, y, w)
+        _lib.check(_declare().sw_t5_stage_batch(self._h, e.ctypes.data, t.ctypes.data, y.ctypes.data,
+                                                None if w is None else w.ctypes.data))
+
+    def forward_backward(self):
+        _lib.check(_declare().sw_t5_forward_backward(self._h))
+
+    def forward_logits(self) -> np.ndarray:
+        out = np.empty((self.batch, self.dec_len, self.spec.vocab_size), np.float32)
+        _lib.check(_declare().sw_t5_forward_logits(self._h, out.ctypes.data))
+        return out
+
+    def adamw_step(self, cfg: AdamWConfig):
+        c = cfg.c()
+        _lib.check(_declare().sw_t5_adamw_step(self._h, C.byref(c)))
+
+    def train_step(self, cfg: AdamWConfig):
+        c = cfg.c()
+        _lib.check(_declare().sw_t5_train_step(self._h, C.byref(c)))
+
+    def loss(self) -> float:
+        x = C.c_double()
+        _lib.check(_declare().sw_t5_last_loss(self._h, C.byref(x)))
+        return x.value
+
+    def stream(self) -> int:
+        s = C.c_void_p()
+        _lib.check(_declare().sw_t5_stream(self._h, C.byref(s)))
+        return s.value or 0
+
+    def launch_count(self) -> int:
+        x = C.c_int64()
+        _lib.check(_declare().sw_t5_launch_count(self._h, C.byref(x)))
+        return x.value
+
+    def set_profiling(self, on: bool):
+        _lib.check(_declare().sw_t5_set_profiling(self._h, int(on)))
+
+    def read_profile(self) -> dict:
+        ms, work, cnt = (C.c_double * 8)(), (C.c_double * 8)(), (C.c_int64 * 8)()
+        _lib.check(_declare().sw_t5_read_profile(self._h, ms, work, cnt))
+        return {c: {"ms": ms[i], "work": work[i], "launches": cnt[i]} for i, c in enumerate(self.PROFILE_CATEGORIES)}
+
+    def device_bytes(self) -> int:
+        x = C.c_int64()
+        _lib.check(_declare().sw_t5_device_bytes(self._h, C.byref(x)))
+        return x.value
