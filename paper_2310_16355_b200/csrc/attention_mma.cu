@@ -67,6 +67,15 @@ int trace_cta() {
   return c;
 }
 
+// SW_ATTN_BWD_TS=0 selects shared-memory P^T / dS^T operands for dV / dK (A/B comparisons).
+int bwd_ts() {
+  static const int v = [] {
+    const char* e = std::getenv("SW_ATTN_BWD_TS");
+    return e != nullptr ? std::atoi(e) : 1;
+  }();
+  return v;
+}
+
 int bwd_dq_first() {
   static const int v = [] {
     const char* e = std::getenv("SW_ATTN_BWD_DQ_FIRST");
@@ -943,7 +952,7 @@ __global__ void __launch_bounds__(512, 1)
     attn_bwd_tc2(const __grid_constant__ CUtensorMap tm_qkv64, const __grid_constant__ CUtensorMap tm_qkv128,
                  const __grid_constant__ CUtensorMap tm_do64, const __grid_constant__ CUtensorMap tm_dq,
                  const float* __restrict__ lse, const float* __restrict__ delta, bf16* __restrict__ dqkv, int T,
-                 int Hl, float scale_log2, float scale, int nbh, int group, int trace_cta, int dq_first) {
+                 int Hl, float scale_log2, float scale, int nbh, int group, int trace_cta, int dq_first, int ts) {
   using Lay = Bwd2Layout;
   constexpr int HD = Lay::HD;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -1079,6 +1088,21 @@ __global__ void __launch_bounds__(512, 1)
         if (lane == 0 && n < 64) ATTN_TR(n * 16 + 2);
         const uint64_t q_mn = dQ_mn + qst * QT16, do_mn = dDO_mn + qst * QT16;
         if (dev::elect_one_sync()) {
+          if (ts) {
+            // P^T / dS^T were written into the first 32 columns of S^T_n / dP^T_n (bf16 pairs):
+            // dV and dK read A from tensor memory (no shared-memory A traffic); dQ^T then
+            // overwrites S^T_n, after dV has read it (MMAs execute in issue order)
+#pragma unroll
+            for (int kk = 0; kk < BQ2 / 16; ++kk)
+              dev::umma_f16_ts(t_dv, t_s + st * BQ2 + kk * 8, do_mn + mn(kk), id_kv, (n > 0 || kk > 0) ? 1u : 0u);
+#pragma unroll
+            for (int kk = 0; kk < BQ2 / 16; ++kk)
+              dev::umma_f16_ts(t_dk, t_dp + st * BQ2 + kk * 8, q_mn + mn(kk), id_kv, (n > 0 || kk > 0) ? 1u : 0u);
+#pragma unroll
+            for (int kk = 0; kk < 128 / 16; ++kk)
+              dev::umma_f16_ss(t_s + st * BQ2, dK_mn + mn(kk), dDSt_mn + mn(kk), id_dq, kk > 0 ? 1u : 0u);
+            dev::umma_commit(&dq_full[st]);
+          } else {
           // dQ^T first (default): its TMEM drain (dQ warpgroup) then overlaps dV / dK, so the S
           // buffer it occupies is free again by the time S_{n+2} is issued
           if (dq_first) {
@@ -1099,6 +1123,7 @@ __global__ void __launch_bounds__(512, 1)
               dev::umma_f16_ss(t_s + st * BQ2, dK_mn + mn(kk), dDSt_mn + mn(kk), id_dq, kk > 0 ? 1u : 0u);
             dev::umma_commit(&dq_full[st]);
           }
+          }
           dev::umma_commit(mma_done);
           dev::umma_commit(&qdo_empty[qst]);
         }
@@ -1112,19 +1137,23 @@ __global__ void __launch_bounds__(512, 1)
     const int key = key0 + t;
     const uint32_t lane_base = static_cast<uint32_t>((warp & 3) * 32) << 16;
     const float log2e = 1.4426950408889634f;
+    // stats in the form the packed math wants: -lse (log2 units) and -scale * delta. The next
+    // block's raw value is loaded one iteration ahead and only scaled when it is stored, so no
+    // instruction waits on that global load until a whole block later.
+    const float stat_mul = tid < BQ2 ? -log2e : -scale;
+    const float* stat_src = (tid < BQ2 ? lse : delta) + static_cast<int64_t>(bh) * T;
+    auto load_stat = [&](int n) -> float {
+      const int qq = key0 + n * BQ2 + (tid & (BQ2 - 1));
+      return (n < nq && tid < 2 * BQ2 && qq < T) ? __ldg(stat_src + qq) : 0.f;
+    };
+    float stat_next = load_stat(0);
     for (int n = 0; n < nq; ++n) {
       const int st = n & 1;
       const int qs = key0 + n * BQ2;
       float* st_lse = sStat + st * 2 * BQ2;
       float* st_del = st_lse + BQ2;
-      // stats in the form the packed math wants: -lse (log2 units) and -scale * delta
-      if (tid < BQ2) {
-        const int qq = qs + tid;
-        st_lse[tid] = qq < T ? -lse[static_cast<int64_t>(bh) * T + qq] * log2e : 0.f;
-      } else if (tid < 2 * BQ2) {
-        const int qq = qs + tid - BQ2;
-        st_del[tid - BQ2] = qq < T ? -scale * delta[static_cast<int64_t>(bh) * T + qq] : 0.f;
-      }
+      if (tid < 2 * BQ2) st_lse[tid] = stat_next * stat_mul;  // [lse | delta] are contiguous
+      stat_next = load_stat(n + 1);
       if (lane == 0 && (warp == 4 || warp == 8) && n < 64) ATTN_TR(n * 16 + 3 + (warp == 8) * 5);
       asm volatile("bar.sync 1, 256;" ::: "memory");
       dev::mbar_wait(&s_full[st], (n >> 1) & 1);
@@ -1165,10 +1194,22 @@ __global__ void __launch_bounds__(512, 1)
       if (lane == 0 && (warp == 4 || warp == 8) && n < 64) ATTN_TR(n * 16 + 5 + (warp == 8) * 5);
       if (n >= 1) dev::mbar_wait(mma_done, (n - 1) & 1);
       if (lane == 0 && (warp == 4 || warp == 8) && n < 64) ATTN_TR(n * 16 + 6 + (warp == 8) * 5);
+      if (ts) {
+        // S^T_n / dP^T_n are in registers already: their first 32 columns take P^T / dS^T
+        // (bf16 pairs, this warpgroup's 32 queries = 16 columns); dS^T also goes to shared
+        // memory as the B operand of dQ^T
+        dev::tmem_st_32x32b_x16(t_s + lane_base + st * BQ2 + wg * 16, pk);
+        dev::tmem_st_32x32b_x16(t_dp + lane_base + st * BQ2 + wg * 16, dk);
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        dev::st_sw128(sPt, 128, t, 0, wg * 4 + u, make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]));
-        dev::st_sw128(sDSt, 128, t, 0, wg * 4 + u, make_uint4(dk[4 * u], dk[4 * u + 1], dk[4 * u + 2], dk[4 * u + 3]));
+        for (int u = 0; u < 4; ++u)
+          dev::st_sw128(sDSt, 128, t, 0, wg * 4 + u, make_uint4(dk[4 * u], dk[4 * u + 1], dk[4 * u + 2], dk[4 * u + 3]));
+        dev::tmem_st_wait();
+      } else {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          dev::st_sw128(sPt, 128, t, 0, wg * 4 + u, make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]));
+          dev::st_sw128(sDSt, 128, t, 0, wg * 4 + u, make_uint4(dk[4 * u], dk[4 * u + 1], dk[4 * u + 2], dk[4 * u + 3]));
+        }
       }
       dev::fence_proxy_async_smem();
       dev::tc_fence_before();
@@ -1364,7 +1405,7 @@ bool launch_bwd2(const bf16* qkv, const bf16* o, const float* lse, const bf16* d
   const double scale = 1.0 / std::sqrt(static_cast<double>(HD));
   attn_bwd_tc2<<<nb * B * Hl, 512, Bwd2Layout::BYTES, s>>>(tm_qkv64, tm_qkv128, tm_do64, tm_dq, lse, delta, dqkv,
                                                           T, Hl, static_cast<float>(scale * 1.4426950408889634),
-                                                          static_cast<float>(scale), B * Hl, work_group(), trace_cta(), bwd_dq_first());
+                                                          static_cast<float>(scale), B * Hl, work_group(), trace_cta(), bwd_dq_first(), bwd_ts());
   dq_to_bf16<<<1184, 256, 0, s>>>(dq, dqkv, M, Dl);
   return true;
 }
