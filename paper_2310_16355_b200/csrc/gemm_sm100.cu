@@ -30,6 +30,9 @@ constexpr int B_STAGE = BN * BK * 2;  // 32 KiB
 constexpr int STAGE_BYTES = A_STAGE + B_STAGE;
 constexpr int TMEM_COLS = 512;
 constexpr int NUM_THREADS = 256;
+#ifndef SW_EPI_PF
+#define SW_EPI_PF 0  // epilogue: 0 = load-wait-process per chunk (measured best), 2 = next chunk TMEM load in flight
+#endif
 #ifndef SW_GROUP_M
 #define SW_GROUP_M 8
 #endif
@@ -150,11 +153,23 @@ __device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int row, int
         if (i < ncols) v[i] += __ldg(p.bias + col0 + i);
       }
     } else {
+      // one division per 32-column chunk: a chunk never straddles a segment when the segment
+      // width is a multiple of 32 (the fused QKV: d/t), otherwise fall back per column
+      const int sg = col0 / p.bias_seg;
+      const int in_seg = col0 - sg * p.bias_seg;
+      if (in_seg + 32 <= p.bias_seg) {
+        const float* bp = p.bias + sg * p.bias_seg_stride + in_seg;
 #pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        const int c = col0 + i;
-        const int sg = c / p.bias_seg;
-        if (i < ncols) v[i] += __ldg(p.bias + sg * p.bias_seg_stride + (c - sg * p.bias_seg));
+        for (int i = 0; i < 32; ++i) {
+          if (i < ncols) v[i] += __ldg(bp + i);
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const int c = col0 + i;
+          const int s2 = c / p.bias_seg;
+          if (i < ncols) v[i] += __ldg(p.bias + s2 * p.bias_seg_stride + (c - s2 * p.bias_seg));
+        }
       }
     }
   }
@@ -235,19 +250,27 @@ __device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int row, int
     } else {
       if (p.accumulate) add = out;
     }
+    // all addend loads first: `out` may alias `add` (in-place residual update), so a load placed
+    // after a store could not be hoisted and every 16-byte load would cost a full round trip
+    if (add != nullptr) {
+      float4 a[8];
+#pragma unroll
+      for (int c = 0; c < 32; c += 4) {
+        if (c < ncols) a[c / 4] = *reinterpret_cast<const float4*>(add + c);
+      }
+#pragma unroll
+      for (int c = 0; c < 32; c += 4) {
+        if (c < ncols) {
+          v[c] += a[c / 4].x;
+          v[c + 1] += a[c / 4].y;
+          v[c + 2] += a[c / 4].z;
+          v[c + 3] += a[c / 4].w;
+        }
+      }
+    }
 #pragma unroll
     for (int c = 0; c < 32; c += 4) {
-      if (c < ncols) {
-        float4 w = make_float4(v[c], v[c + 1], v[c + 2], v[c + 3]);
-        if (add != nullptr) {
-          float4 a = *reinterpret_cast<const float4*>(add + c);
-          w.x += a.x;
-          w.y += a.y;
-          w.z += a.z;
-          w.w += a.w;
-        }
-        *reinterpret_cast<float4*>(out + c) = w;
-      }
+      if (c < ncols) *reinterpret_cast<float4*>(out + c) = make_float4(v[c], v[c + 1], v[c + 2], v[c + 3]);
     }
   }
 }
@@ -769,12 +792,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(p_threads<EPI>(), 1)
     const uint32_t tempty_leader = dev::mapa_shared(dev::smem_u32(&tempty[0]), 0);
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int t = pair; t < num_tiles; t += npairs) {
+    const bool tr = static_cast<int>(blockIdx.x) == p.trace_cta && lane == 0 && warp == 4;
+    int ti = 0;
+    for (int t = pair; t < num_tiles; t += npairs, ++ti) {
       int mb, nb;
       tile_coords(t, num_m, num_n, mb, nb);
       const int row = mb * 2 * BM + static_cast<int>(rank) * BM + static_cast<int>(q) * 32 + static_cast<int>(lane);
       dev::mbar_wait(&tfull[acc], acc_phase);
       dev::tc_fence_after();
+      if (tr && ti < 64) g_gemm_trace[8 * ti + 3] = clock64();
       const int n_left = p.N - nb * BN;
       if constexpr (kGlu) {
         // accumulator columns [0,128) = gate, [128,256) = up for h columns nb*128 + [0,128)
@@ -815,17 +841,40 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(p_threads<EPI>(), 1)
         }
       }
 #pragma unroll 1
+#if SW_EPI_PF == 0
+#pragma unroll 1
       for (int j = 0; j < (kGlu ? 0 : BN / 32); ++j) {
         const int ncols = min(32, n_left - j * 32);
         if (ncols <= 0) break;
         uint32_t r[32];
         dev::tmem_ld_32x32b_x32(tmem_base + ((q * 32) << 16) + acc * BN + j * 32, r);
         dev::tmem_ld_wait();
-        if (row < p.M) {
-          epilogue_chunk<EPI>(p, row, nb * BN + j * 32, ncols, r);
+        if (row < p.M) epilogue_chunk<EPI>(p, row, nb * BN + j * 32, ncols, r);
+      }
+#else
+      if constexpr (!kGlu) {
+        // the next chunk's tcgen05.ld is in flight while this one is processed
+        const int nch = min(BN / 32, (n_left + 31) / 32);
+        // (two register buffers, the loop unrolled by two only: the GeLU epilogues are long)
+        uint32_t r0[32], r1[32];
+        const uint32_t tbase = tmem_base + ((q * 32) << 16) + acc * BN;
+        dev::tmem_ld_32x32b_x32(tbase, r0);
+        dev::tmem_ld_wait();
+#pragma unroll 1
+        for (int j = 0; j < nch; j += 2) {
+          if (j + 1 < nch) dev::tmem_ld_32x32b_x32(tbase + (j + 1) * 32, r1);
+          if (row < p.M) epilogue_chunk<EPI>(p, row, nb * BN + j * 32, min(32, n_left - j * 32), r0);
+          dev::tmem_ld_wait();
+          if (j + 1 < nch) {
+            if (j + 2 < nch) dev::tmem_ld_32x32b_x32(tbase + (j + 2) * 32, r0);
+            if (row < p.M) epilogue_chunk<EPI>(p, row, nb * BN + (j + 1) * 32, min(32, n_left - (j + 1) * 32), r1);
+            dev::tmem_ld_wait();
+          }
         }
       }
+#endif
       dev::tc_fence_before();
+      if (tr && ti < 64) g_gemm_trace[8 * ti + 4] = clock64();
       if (lane == 0) dev::mbar_arrive_cluster(tempty_leader + acc * 8);
       if (++acc == 2) {
         acc = 0;

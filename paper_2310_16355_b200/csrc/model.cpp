@@ -4,6 +4,7 @@
 #include <unordered_map>
 
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <stdexcept>
@@ -711,6 +712,11 @@ void Model::gemm(Rank& R, int M, int N, int K, const void* A, int64_t lda, int a
   tic();
   cuda_check(gemm_bf16(p, stream_), "gemm launch");
   toc(kProfGemm, 2.0 * M * N * static_cast<double>(K));
+  if (prof_) {
+    prof_tag_.resize(prof_rec_.size());
+    prof_tag_.back() = "gemm," + std::to_string(M) + "," + std::to_string(N) + "," + std::to_string(K) + ",epi" +
+                       std::to_string(epi) + (a_mn ? ",A_mn" : ",A_k") + (b_mn ? ",B_mn" : ",B_k");
+  }
   ++launches_;
 }
 
@@ -879,6 +885,10 @@ void Model::wgrad(Rank& R, int slot, int M, int N, int K, const void* A, int64_t
   tic();
   cuda_check(gemm_bf16(p, stream_), "gemm launch");
   toc(kProfGemm, 2.0 * M * N * static_cast<double>(K));
+  if (prof_) {
+    prof_tag_.resize(prof_rec_.size());
+    prof_tag_.back() = "gemm," + std::to_string(M) + "," + std::to_string(N) + "," + std::to_string(K) + ",adamw,A_mn,B_mn";
+  }
   ++launches_;
 }
 
@@ -1446,6 +1456,7 @@ void Model::set_profiling(bool on) {
   prof_ = on;
   ev_next_ = 0;
   prof_rec_.clear();
+  prof_tag_.clear();
 }
 
 void Model::tic(cudaStream_t s) {
@@ -1477,6 +1488,10 @@ void Model::read_profile(double* ms, double* work, int64_t* count) {
   }
   cuda_check(cudaStreamSynchronize(stream_), "sync");
   cuda_check(cudaStreamSynchronize(comm_stream_), "sync");
+  // SW_PROFILE_LOG=<path>: append one CSV line per timed launch (category, ms, work, tag)
+  const char* log_path = std::getenv("SW_PROFILE_LOG");
+  FILE* log = log_path != nullptr ? std::fopen(log_path, "a") : nullptr;
+  prof_tag_.resize(prof_rec_.size());
   for (size_t i = 0; i < prof_rec_.size(); ++i) {
     float t = 0.f;
     cuda_check(cudaEventElapsedTime(&t, events_[2 * i], events_[2 * i + 1]), "cudaEventElapsedTime");
@@ -1484,9 +1499,12 @@ void Model::read_profile(double* ms, double* work, int64_t* count) {
     ms[c] += t;
     work[c] += prof_rec_[i].second;
     count[c] += 1;
+    if (log != nullptr) std::fprintf(log, "%d,%.6f,%.6g,%s\n", c, t, prof_rec_[i].second, prof_tag_[i].c_str());
   }
+  if (log != nullptr) std::fclose(log);
   ev_next_ = 0;
   prof_rec_.clear();
+  prof_tag_.clear();
 }
 
 }  // namespace sw

@@ -209,6 +209,7 @@ class Model {
   std::vector<cudaEvent_t> events_;
   size_t ev_next_ = 0;
   std::vector<std::pair<int, double>> prof_rec_;
+  std::vector<std::string> prof_tag_;  // per record: GEMM shape / epilogue (SW_PROFILE_LOG dump)
   int64_t bytes_ = 0;
   uint64_t step_ = 0;
   uint64_t seed_ = 0;

@@ -23,8 +23,15 @@ def main(kind, M=12288, N=4096, K=8192):
     flag = torch.zeros(1, device="cuda", dtype=torch.int32)
     s = torch.cuda.current_stream().cuda_stream
     hp = (1e-5, 0.9, 0.999, 1e-8, 0.0, 0.5, 0.5)
+    aux = torch.randn(M, N, device="cuda")
+    outf = torch.empty(M, N, device="cuda")
+    A2 = torch.randn(M, K, device="cuda").bfloat16()
+    B2 = torch.randn(N, K, device="cuda").bfloat16()
     for _ in range(3):
-        if kind == "fused":
+        if kind == "resid":  # forward residual epilogue (kResidF32): K-major operands
+            _lib.check(L.sw_k_gemm_bf16(M, N, K, A2.data_ptr(), K, 0, B2.data_ptr(), K, 0, 3, outf.data_ptr(), N,
+                                        None, 0, None, aux.data_ptr(), N, 1.0, 0, s))
+        elif kind == "fused":
             _lib.check(L.sw_k_gemm_bf16_adamw(M, N, K, A.data_ptr(), M, 1, B.data_ptr(), N, 1, p.data_ptr(),
                                               m.data_ptr(), v.data_ptr(), sh.data_ptr(), N, flag.data_ptr(), *hp, s))
         else:
