@@ -454,6 +454,14 @@ constexpr int OPT_NBUF = 2;
 constexpr int OPT_ARR = 128 * OC * 4;     // one array (p, m or v) of one chunk, 128 rows
 constexpr int OPT_BUF = 3 * OPT_ARR;      // p | m | v
 constexpr int OPT_WBOX = 32 * OC * 4;     // one warp's 32-row box of one array
+// SW_ADAMW_DIRECT=1: the optimizer state moves between HBM and registers directly (coalesced
+// through a 4 KiB per-warp transpose of the gradient) instead of through TMA-staged shared
+// memory -- 8 instead of 48 bytes of shared-memory traffic per parameter, leaving the port to
+// the operand ring (TMA writes + MMA reads already use most of its 128 B/cycle).
+#ifndef SW_ADAMW_DIRECT
+#define SW_ADAMW_DIRECT 0
+#endif
+constexpr int OPT_SMEM = SW_ADAMW_DIRECT ? 8 * 32 * 32 * 4 : OPT_NBUF * OPT_BUF;
 // The AdamW epilogue runs two epilogue warpgroups (warps 4-7 and 8-11) on alternate chunks.
 template <Epi EPI>
 constexpr int p_threads() {
@@ -461,14 +469,14 @@ constexpr int p_threads() {
 }
 template <Epi EPI>
 constexpr int p_stages() {
-  return EPI == Epi::kAdamW ? (227 * 1024 - 1024 - 256 - OPT_NBUF * OPT_BUF) / P_STAGE_BYTES < 6
-                                  ? (227 * 1024 - 1024 - 256 - OPT_NBUF * OPT_BUF) / P_STAGE_BYTES
+  return EPI == Epi::kAdamW ? (227 * 1024 - 1024 - 256 - OPT_SMEM) / P_STAGE_BYTES < 6
+                                  ? (227 * 1024 - 1024 - 256 - OPT_SMEM) / P_STAGE_BYTES
                                   : 6
                             : 6;
 }
 template <Epi EPI>
 constexpr int p_smem_bytes() {
-  return p_stages<EPI>() * P_STAGE_BYTES + (EPI == Epi::kAdamW ? OPT_NBUF * OPT_BUF : 0) + 1024 + 256;
+  return p_stages<EPI>() * P_STAGE_BYTES + (EPI == Epi::kAdamW ? OPT_SMEM : 0) + 1024 + 256;
 }
 
 // fp32 tensor maps over p, m, v ([M, ldc], box OC columns x 32 rows, swizzle span = one row).
@@ -566,7 +574,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(p_threads<EPI>(), 1)
   uint8_t* sA = smem;
   uint8_t* sB = smem + P_STAGES * P_A_STAGE;
   uint8_t* sOpt = sB + P_STAGES * P_B_STAGE;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sOpt + (kOpt ? 2 * OPT_BUF : 0));
+  uint64_t* full = reinterpret_cast<uint64_t*>(sOpt + (kOpt ? OPT_SMEM : 0));
   uint64_t* empty = full + P_STAGES;
   uint64_t* tfull = empty + P_STAGES;
   uint64_t* tempty = tfull + 2;
@@ -700,7 +708,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(p_threads<EPI>(), 1)
       }
     }
   } else if (warp == 3) {
-    if constexpr (kOpt) {
+    if constexpr (kOpt && !SW_ADAMW_DIRECT) {
       if (lane == 0) {
         // ---------------- optimizer-state producer (TMA, one chunk ahead) ----------------
         dev::tma_prefetch_desc(&om.p);
@@ -728,6 +736,36 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(p_threads<EPI>(), 1)
             }
           }
         }
+      }
+    }
+  } else if (kOpt && SW_ADAMW_DIRECT && warp >= 4) {
+    // ---------------- AdamW epilogue, direct: two warpgroups on alternate 32-column chunks ----------------
+    const uint32_t q = warp & 3;
+    const int wg = (static_cast<int>(warp) - 4) >> 2;
+    float4* stage = reinterpret_cast<float4*>(sOpt) + (static_cast<int>(warp) - 4) * 256;
+    const uint32_t tempty_leader = dev::mapa_shared(dev::smem_u32(&tempty[0]), 0);
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int t = pair; t < num_tiles; t += npairs) {
+      int mb, nb;
+      tile_coords(t, num_m, num_n, mb, nb);
+      const int row0 = mb * 2 * BM + static_cast<int>(rank) * BM + static_cast<int>(q) * 32;
+      dev::mbar_wait(&tfull[acc], acc_phase);
+      dev::tc_fence_after();
+#pragma unroll 1
+      for (int j = wg; j < BN / 32; j += 2) {
+        const int col0 = nb * BN + j * 32;
+        if (col0 >= p.N) break;
+        uint32_t r[32];
+        dev::tmem_ld_32x32b_x32(tmem_base + ((q * 32) << 16) + acc * BN + j * 32, r);
+        dev::tmem_ld_wait();
+        adamw_chunk(p, stage, row0, col0, min(32, p.N - col0), r, lane);
+      }
+      dev::tc_fence_before();
+      if (lane == 0) dev::mbar_arrive_cluster(tempty_leader + acc * 8);
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
       }
     }
   } else if (kOpt && warp >= 4) {
@@ -883,7 +921,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(p_threads<EPI>(), 1)
     }
   }
 
-  if constexpr (kOpt) {
+  if constexpr (kOpt && !SW_ADAMW_DIRECT) {
     if (warp >= 4 && lane == 0) dev::bulk_wait_all();
   }
   dev::tc_fence_before();

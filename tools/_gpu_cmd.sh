@@ -1,6 +1,7 @@
-timeout 600 python -m pytest tests -m gpu -q -x > gpurun_out/t.log 2>&1; echo EXIT $? >> gpurun_out/t.log
-for i in 1 2; do for lib in variants/libsw_tanhf.so paper_2310_16355_b200/libshardweave_b200.so; do
-rm -f gpurun_out/prof.csv; SW_LIB_PATH=$lib SW_PROFILE_LOG=gpurun_out/prof.csv timeout 400 python bench.py --no-cpu-baseline --steps 5 > gpurun_out/bench2.log 2>&1
-echo "== $lib $(python3 -c "import json; d=json.loads(open('gpurun_out/bench2.log').read().strip().splitlines()[-1]); print(round(d['value']), round(d['ms_per_step'],1), d['clocks']['sm_mhz'])")"
-python tools/gemm_shape_report.py gpurun_out/prof.csv 2 | grep "epi2\|epi4" | cut -c1-130
-done; done > gpurun_out/pf_ab.log 2>&1
+SW_LIB_PATH=variants/libsw_direct.so timeout 600 python -m pytest tests/test_model_gpu.py tests/test_kernels_gpu.py tests/test_gemm_gpu.py -q -x -k "adamw or fused" > gpurun_out/t.log 2>&1; echo EXIT $? >> gpurun_out/t.log
+for i in 1 2; do for lib in paper_2310_16355_b200/libshardweave_b200.so variants/libsw_direct.so; do
+  echo "$lib"; SW_LIB_PATH=$lib python -c "
+import sys, json; sys.path.insert(0,'.')
+from tools.gemm_bench import bench_adamw
+for sh in [(12288,4096,8192),(4096,11008,8192),(4096,4096,8192)]: print(json.dumps(bench_adamw(*sh)))"
+done; done > gpurun_out/d_ab.log 2>&1
