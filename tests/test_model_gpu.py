@@ -340,3 +340,28 @@ def test_replicated_param_grads_are_deterministic():
         runs.append({n: model.get_grad(n).view(np.uint32).copy() for n in names})
     for n in names:
         assert np.array_equal(runs[0][n], runs[1][n]), n
+
+
+@pytest.mark.parametrize("spec_name", ["llama7b_vocab_parallel.spec", "llama7b_swiglu.spec"])
+def test_llama7b_width_tp8_matches_tp1(spec_name):
+    """The shapes the 8-GPU scaling run hits (LLaMA-7B width at mp = 8: 4 heads, d/t = 512,
+    d_ff/t = 1376 (GEMM N and K tails), vocab shard 4000), depth 2 and 512 tokens, on the
+    emulated mesh: the mp = 8 step equals the unsharded one."""
+    text = open(os.path.join(SPECS, spec_name)).read().replace("n_layers = 32", "n_layers = 2")
+    spec = rules.parse_model_spec(text)
+    rng = np.random.default_rng(3)
+    tokens = rng.integers(0, spec.vocab_size, (2, 256), dtype=np.int32)
+    targets = rng.integers(0, spec.vocab_size, (2, 256), dtype=np.int32)
+    res = {}
+    for mp in (1, 8):
+        model, mesh, plan = make(spec, 1, mp, 2, 256)
+        model.init_params(42, "model-init")
+        model.stage_batch(tokens, targets, None)
+        model.forward_backward()
+        res[mp] = (model.loss(), {n: model.get_grad(n) for n in ("block_0/attn/q/kernel", "block_1/mlp/fc2/kernel",
+                                                                 "block_1/attn/o/kernel", "lm_head/kernel")})
+        model.close()
+        mesh.close()
+    assert abs(res[8][0] - res[1][0]) / res[1][0] < 2e-4, (res[8][0], res[1][0])
+    for n in res[1][1]:
+        assert rel_l2(res[8][1][n].astype(np.float64), res[1][1][n].astype(np.float64)) < 1e-2, n

@@ -55,6 +55,12 @@ def main(B=4, T=2048, Hl=32, hd=128, iters=10):
     sd = lambda: torch.nn.functional.scaled_dot_product_attention(q, k, v, is_causal=True)  # noqa: E731
     ms = timeit(sd)
     res["torch_sdpa_fwd_tflops"] = flops_fwd / ms / 1e9
+    qg, kg, vg = (t.detach().requires_grad_(True) for t in (q, k, v))
+    og = torch.nn.functional.scaled_dot_product_attention(qg, kg, vg, is_causal=True)
+    go = torch.randn_like(og)
+    sdb = lambda: torch.autograd.grad(og, (qg, kg, vg), go, retain_graph=True)  # noqa: E731
+    ms = timeit(sdb)
+    res["torch_sdpa_bwd_tflops"] = 2 * flops_fwd / ms / 1e9
     # correctness on the first (b, h)
     fwd()
     torch.cuda.synchronize()
