@@ -67,8 +67,10 @@ def _merge(x):
     return x.transpose(0, 2, 1, 3).reshape(B, T, H * dk)
 
 
-def attention_fwd(q, k, v, bias=None, causal=False):
-    """q [B,H,Tq,dk], k/v [B,H,Tk,dk]; scores unscaled (T5) + bias [H,Tq,Tk] (+ causal mask)."""
+def attention_fwd(q, k, v, bias=None, causal=False, round_p=False):
+    """q [B,H,Tq,dk], k/v [B,H,Tk,dk]; scores unscaled (T5) + bias [H,Tq,Tk] (+ causal mask).
+    round_p: the tensor-core kernels' arithmetic -- the max-shifted exponentials enter the P.V
+    product as bf16, the row sum stays fp32."""
     s = q @ k.transpose(0, 1, 3, 2)
     if bias is not None:
         s = s + bias[None]
@@ -76,21 +78,27 @@ def attention_fwd(q, k, v, bias=None, causal=False):
         Tq, Tk = s.shape[-2:]
         s = s + np.triu(np.full((Tq, Tk), -1e9), 1)
     P = _softmax(s)
+    if round_p:
+        e = np.exp(s - s.max(-1, keepdims=True))
+        return (bf16_round(e) @ v) / e.sum(-1, keepdims=True), P
     return P @ v, P
 
 
-def attention_bwd(q, k, v, P, dout, o_stored=None):
+def attention_bwd(q, k, v, P, dout, o_stored=None, round_p=False):
     """delta = rowsum(dP * P); with o_stored (bf16_acts) the flash form rowsum(dO * O) over the
-    stored output, as the device computes it (model_ref does the same)."""
+    stored output, as the device computes it (model_ref does the same). round_p: P and dS enter
+    the dV / dK / dQ products as bf16 (tensor-core kernels); the bias gradient uses fp32 dS."""
     dP = dout @ v.transpose(0, 1, 3, 2)
-    dv = P.transpose(0, 1, 3, 2) @ dout
+    Pm = bf16_round(P) if round_p else P
+    dv = Pm.transpose(0, 1, 3, 2) @ dout
     delta = (dP * P).sum(-1, keepdims=True) if o_stored is None else (dout * o_stored).sum(-1, keepdims=True)
     dS = P * (dP - delta)
-    return dS @ k, dS.transpose(0, 1, 3, 2) @ q, dv, dS
+    dSm = bf16_round(dS) if round_p else dS
+    return dSm @ k, dSm.transpose(0, 1, 3, 2) @ q, dv, dSm
 
 
 def forward_backward(params: dict, spec: dict, enc_tokens, dec_tokens, targets, weights, need_grads=True,
-                     bf16_acts=False):
+                     bf16_acts=False, round_p=False):
     """Returns (loss, grads, logits). enc_tokens [B,Te], dec_tokens/targets/weights [B,Td].
     bf16_acts rounds what the device stores in bf16 (GEMM inputs/outputs, attention operands)."""
     R = bf16_round if bf16_acts else (lambda x: x)
@@ -117,7 +125,7 @@ def forward_backward(params: dict, spec: dict, enc_tokens, dec_tokens, targets, 
         q = _heads(R(lin(a, pre + f"{scope}/q/kernel")), H)
         k = _heads(R(lin(src, pre + f"{scope}/k/kernel")), H)
         v = _heads(R(lin(src, pre + f"{scope}/v/kernel")), H)
-        o, P = attention_fwd(q, k, v, bias, causal)
+        o, P = attention_fwd(q, k, v, bias, causal, round_p)
         om = R(_merge(o))
         cache[(pre, scope)] = (a, xh, r, q, k, v, P, om)
         return x_in + lin(om, pre + f"{scope}/o/kernel")
@@ -190,7 +198,7 @@ def forward_backward(params: dict, spec: dict, enc_tokens, dec_tokens, targets, 
         dyf = R(dy.reshape(-1, d))
         grads[pre + f"{scope}/o/kernel"] = dyf.T @ om.reshape(-1, om.shape[-1])
         dom = R(dyf.reshape(dy.shape) @ p[pre + f"{scope}/o/kernel"])
-        dq, dk, dv, dS = attention_bwd(q, k, v, P, _heads(dom, H), _heads(om, H) if bf16_acts else None)
+        dq, dk, dv, dS = attention_bwd(q, k, v, P, _heads(dom, H), _heads(om, H) if bf16_acts else None, round_p)
         if ids is not None:
             scatter_bias(st, ids, dS)
         dqf, dkf, dvf = (R(_merge(t)) for t in (dq, dk, dv))

@@ -18,6 +18,11 @@ bool attention_mma_fwd(const bf16* qkv, bf16* o, float* lse, int B, int T, int H
                        cudaStream_t s);
 bool attention_mma_bwd(const bf16* qkv, const bf16* o, const float* lse, const bf16* dout,
                        bf16* dqkv, float* scratch, int B, int T, int Hl, int hd, cudaStream_t s);
+bool attention_mma_fwd_ex(const bf16* qkv, bf16* o, float* lse, int B, int T, int Hl, int hd, int causal,
+                          const float* lut, float scale, cudaStream_t s);
+bool attention_mma_bwd_ex(const bf16* qkv, const bf16* o, const float* lse, const bf16* dout, bf16* dqkv,
+                          float* scratch, int B, int T, int Hl, int hd, int causal, const float* lut, float* dlut,
+                          float scale, cudaStream_t s);
 
 namespace {
 
@@ -182,6 +187,17 @@ void attention_bwd(const bf16* qkv, const bf16* o, const float* lse, const bf16*
   attn_bwd_generic<<<grid, 128, 0, s>>>(qkv, lse, delta, dout, dqkv, dkv, T, Hl, hd,
                                         static_cast<float>(1.0 / std::sqrt(static_cast<double>(hd))));
   dkv_to_bf16<<<1184, 256, 0, s>>>(dkv, dqkv, M, Dl);
+}
+
+bool attention_fwd_ex(const bf16* qkv, bf16* o, float* lse, int B, int T, int Hl, int hd, int causal,
+                      const float* lut, float scale, cudaStream_t s) {
+  return attention_mma_fwd_ex(qkv, o, lse, B, T, Hl, hd, causal, lut, scale, s);
+}
+
+bool attention_bwd_ex(const bf16* qkv, const bf16* o, const float* lse, const bf16* dout, bf16* dqkv,
+                      float* scratch, int B, int T, int Hl, int hd, int causal, const float* lut, float* dlut,
+                      float scale, cudaStream_t s) {
+  return attention_mma_bwd_ex(qkv, o, lse, dout, dqkv, scratch, B, T, Hl, hd, causal, lut, dlut, scale, s);
 }
 
 }  // namespace k

@@ -390,7 +390,8 @@ struct Fwd2Layout {
 
 __global__ void __launch_bounds__(384, 1)
     attn_fwd_tc2(const __grid_constant__ CUtensorMap tm, bf16* __restrict__ out, float* __restrict__ lse, int T,
-                 int Hl, float scale_log2, float scale, int nbh, int group) {
+                 int Hl, float scale_log2, float scale, int nbh, int group, int causal,
+                 const float* __restrict__ lut) {
   using Lay = Fwd2Layout;
   constexpr int HD = Lay::HD;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -416,8 +417,13 @@ __global__ void __launch_bounds__(384, 1)
   const int row0 = b * T;
   const int qa = 2 * pi;
   const bool hasB = qa + 1 < nqb;
-  const int nkv_t[2] = {qa + 1, hasB ? qa + 2 : 0};
-  const int nkv = hasB ? qa + 2 : qa + 1;
+  // causal: key blocks up to the diagonal; otherwise (T5 encoder / cross) every key block
+  const int nkv_t[2] = {causal ? qa + 1 : nqb, hasB ? (causal ? qa + 2 : nqb) : 0};
+  const int nkv = causal ? (hasB ? qa + 2 : qa + 1) : nqb;
+  // additive relative-position bias (T5): lut[h][key - query + T - 1] in natural units, row
+  // pitch 2T + 128; the scores are then scale * s + bias and the exp2 runs in log2(e) units
+  const float sl_eff = lut ? 1.4426950408889634f : scale_log2;
+  const float sc_eff = lut ? 1.f : scale;
 
   const uint32_t warp = dev::warp_idx_sync();
   const uint32_t lane = threadIdx.x & 31;
@@ -525,11 +531,16 @@ __global__ void __launch_bounds__(384, 1)
         for (int c = 0; c < 4; ++c)
           dev::tmem_ld_32x32b_x32(tS + c * 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32 * c));
         dev::tmem_ld_wait();
-        if (j == nk - 1 || (j + 1) * 128 > T) {
+        if (lut) {
+          const float* lr = lut + static_cast<int64_t>(h) * (2 * T + 128) + (T - 1 - (q < T ? q : T - 1)) + j * 128;
+#pragma unroll
+          for (int i = 0; i < 128; ++i) v[i] = __float_as_uint(fmaf(__uint_as_float(v[i]), scale, __ldg(lr + i)));
+        }
+        if ((causal && j == nk - 1) || (j + 1) * 128 > T) {
 #pragma unroll
           for (int i = 0; i < 128; ++i) {
             const int key = j * 128 + i;
-            if (!(key <= q && key < T)) v[i] = __float_as_uint(-INFINITY);
+            if (!((!causal || key <= q) && key < T)) v[i] = __float_as_uint(-INFINITY);
           }
         }
         float mx = fmaxf(__uint_as_float(v[0]), __uint_as_float(v[127]));
@@ -542,9 +553,9 @@ __global__ void __launch_bounds__(384, 1)
         float factor = 1.f;
         if (j == 0) {
           m_used = mx;
-        } else if ((mx - m_used) * scale_log2 > 8.f) {
+        } else if ((mx - m_used) * sl_eff > 8.f) {
           resc = true;
-          factor = dev::ex2_approx((m_used - mx) * scale_log2);
+          factor = dev::ex2_approx((m_used - mx) * sl_eff);
           m_used = mx;
           l *= factor;
         }
@@ -562,8 +573,8 @@ __global__ void __launch_bounds__(384, 1)
           }
           dev::tmem_st_wait();
         }
-        const float mb = m_used * scale_log2;
-        const float2 sl2 = make_float2(scale_log2, scale_log2), nmb2 = make_float2(-mb, -mb);
+        const float mb = m_used * sl_eff;
+        const float2 sl2 = make_float2(sl_eff, sl_eff), nmb2 = make_float2(-mb, -mb);
         float2 ls2 = make_float2(0.f, 0.f);
 #pragma unroll
         for (int e = 0; e < 64; ++e) {  // P in place: v[e] = bf16x2(p[2e], p[2e+1])
@@ -600,7 +611,7 @@ __global__ void __launch_bounds__(384, 1)
           }
         }
       }
-      if (q < T) lse[static_cast<int64_t>(bh) * T + q] = m_used * scale + logf(l);
+      if (q < T) lse[static_cast<int64_t>(bh) * T + q] = m_used * sc_eff + logf(l);
     }
   }
   dev::tc_fence_before();
@@ -619,7 +630,8 @@ bool fwd2_enabled() {
   return on;
 }
 
-bool launch_fwd2(const bf16* qkv, bf16* o, float* lse, int B, int T, int Hl, cudaStream_t s) {
+bool launch_fwd2(const bf16* qkv, bf16* o, float* lse, int B, int T, int Hl, cudaStream_t s, int causal = 1,
+                 const float* lut = nullptr, float scale_arg = 0.f) {
   static bool configured = false;
   if (!configured) {
     if (cudaFuncSetAttribute(attn_fwd_tc2, cudaFuncAttributeMaxDynamicSharedMemorySize, Fwd2Layout::BYTES) !=
@@ -633,10 +645,11 @@ bool launch_fwd2(const bf16* qkv, bf16* o, float* lse, int B, int T, int Hl, cud
   const CUtensorMap tm = make_tmap_bf16_2d(qkv, 3ull * Dl, static_cast<uint64_t>(B) * T, 3ull * Dl, 64, 128);
   const int nqb = (T + 127) / 128;
   const int npair = (nqb + 1) / 2;
-  const double scale = 1.0 / std::sqrt(static_cast<double>(HD));
+  const double scale = scale_arg > 0.f ? scale_arg : 1.0 / std::sqrt(static_cast<double>(HD));
   attn_fwd_tc2<<<npair * B * Hl, 384, Fwd2Layout::BYTES, s>>>(tm, o, lse, T, Hl,
                                                               static_cast<float>(scale * 1.4426950408889634),
-                                                              static_cast<float>(scale), B * Hl, work_group());
+                                                              static_cast<float>(scale), B * Hl, work_group(), causal,
+                                                              lut);
   return true;
 }
 
@@ -952,7 +965,8 @@ __global__ void __launch_bounds__(512, 1)
     attn_bwd_tc2(const __grid_constant__ CUtensorMap tm_qkv64, const __grid_constant__ CUtensorMap tm_qkv128,
                  const __grid_constant__ CUtensorMap tm_do64, const __grid_constant__ CUtensorMap tm_dq,
                  const float* __restrict__ lse, const float* __restrict__ delta, bf16* __restrict__ dqkv, int T,
-                 int Hl, float scale_log2, float scale, int nbh, int group, int trace_cta, int dq_first, int ts) {
+                 int Hl, float scale_log2, float scale, int nbh, int group, int trace_cta, int dq_first, int ts,
+                 int causal, const float* __restrict__ lut, float* __restrict__ dlut) {
   using Lay = Bwd2Layout;
   constexpr int HD = Lay::HD;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -973,6 +987,7 @@ __global__ void __launch_bounds__(512, 1)
   uint64_t* p_full = bars + 11;
   uint64_t* mma_done = bars + 12;
   uint64_t* dq_full = bars + 13;   // [2]  dQ^T_n is in S^T buffer n & 1
+  uint64_t* ds_read = bars + 15;   // the dQ warpgroup has read dS^T_n for the bias gradient
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
 
   const int nb = (T + 127) / 128;
@@ -982,7 +997,13 @@ __global__ void __launch_bounds__(512, 1)
   const int Dl = Hl * HD;
   const int key0 = kb * 128;
   const int row0 = b * T;
-  const int nq = (T - key0 + BQ2 - 1) / BQ2;  // 64-query blocks starting at the diagonal
+  // causal: 64-query blocks from the diagonal on; otherwise (T5 encoder / cross) all of them
+  const int qbase = causal ? key0 : 0;
+  const int nq = (T - qbase + BQ2 - 1) / BQ2;
+  // T5 relative bias: lut / dlut [Hl][2T + 128], index key - query + T - 1 (requires ts: the
+  // bias-gradient accumulator takes the otherwise unused P^T tile)
+  const float* lut_h = lut ? lut + static_cast<int64_t>(h) * (2 * T + 128) : nullptr;
+  float* sAcc = reinterpret_cast<float*>(smem + Lay::OFF_PT);  // [T + 128] when dlut
 
   const uint32_t warp = dev::warp_idx_sync();
   const uint32_t lane = threadIdx.x & 31;
@@ -1006,6 +1027,7 @@ __global__ void __launch_bounds__(512, 1)
       dev::mbar_init(&dq_full[i], 1);
     }
     dev::mbar_init(p_full, 256);
+    dev::mbar_init(ds_read, 128);
     dev::mbar_init(mma_done, 1);
     dev::fence_barrier_init();
   }
@@ -1026,7 +1048,7 @@ __global__ void __launch_bounds__(512, 1)
       }
       for (int n = 0; n < nq; ++n) {
         const int st = n % QST;
-        const int qs = key0 + n * BQ2;
+        const int qs = qbase + n * BQ2;
         dev::mbar_wait(&qdo_empty[st], ((n / QST) & 1) ^ 1);
         dev::mbar_arrive_expect_tx(&qdo_full[st], 2 * Lay::QT);
 #pragma unroll
@@ -1143,13 +1165,13 @@ __global__ void __launch_bounds__(512, 1)
     const float stat_mul = tid < BQ2 ? -log2e : -scale;
     const float* stat_src = (tid < BQ2 ? lse : delta) + static_cast<int64_t>(bh) * T;
     auto load_stat = [&](int n) -> float {
-      const int qq = key0 + n * BQ2 + (tid & (BQ2 - 1));
+      const int qq = qbase + n * BQ2 + (tid & (BQ2 - 1));
       return (n < nq && tid < 2 * BQ2 && qq < T) ? __ldg(stat_src + qq) : 0.f;
     };
     float stat_next = load_stat(0);
     for (int n = 0; n < nq; ++n) {
       const int st = n & 1;
-      const int qs = key0 + n * BQ2;
+      const int qs = qbase + n * BQ2;
       float* st_lse = sStat + st * 2 * BQ2;
       float* st_del = st_lse + BQ2;
       if (tid < 2 * BQ2) st_lse[tid] = stat_next * stat_mul;  // [lse | delta] are contiguous
@@ -1164,7 +1186,7 @@ __global__ void __launch_bounds__(512, 1)
       dev::tmem_ld_32x32b_x32(t_dp + lane_base + st * BQ2 + wg * 32, pv);
       dev::tmem_ld_wait();
       // masks only where the block touches the diagonal or the sequence end (block-uniform)
-      const bool masked = qs < key0 + 128 || qs + BQ2 > T || key0 + 128 > T;
+      const bool masked = (causal && qs < key0 + 128) || qs + BQ2 > T || key0 + 128 > T;
       const float4* nl4 = reinterpret_cast<const float4*>(st_lse + wg * 32);
       const float4* nd4 = reinterpret_cast<const float4*>(st_del + wg * 32);
       const float2 sl2 = make_float2(scale_log2, scale_log2), sc2 = make_float2(scale, scale);
@@ -1175,13 +1197,19 @@ __global__ void __launch_bounds__(512, 1)
 #pragma unroll
         for (int hh = 0; hh < 2; ++hh) {
           const int e = 2 * g4 + hh;
-          const float2 a = dev::ffma2(make_float2(__uint_as_float(sv[2 * e]), __uint_as_float(sv[2 * e + 1])), sl2,
-                                      hh ? make_float2(nl.z, nl.w) : make_float2(nl.x, nl.y));
+          float2 a = dev::ffma2(make_float2(__uint_as_float(sv[2 * e]), __uint_as_float(sv[2 * e + 1])), sl2,
+                                hh ? make_float2(nl.z, nl.w) : make_float2(nl.x, nl.y));
+          if (lut_h) {  // + bias(key - query) in log2 units
+            // clamped: entries past the sequence end (masked below) must still load in bounds
+            const int bi = max(key + T - 1 - (qs + wg * 32 + 2 * e), 1);
+            const float b0 = key < T ? __ldg(lut_h + bi) : 0.f, b1 = key < T ? __ldg(lut_h + bi - 1) : 0.f;
+            a = dev::ffma2(make_float2(b0, b1), make_float2(1.4426950408889634f, 1.4426950408889634f), a);
+          }
           float p0 = dev::ex2_approx(a.x), p1 = dev::ex2_approx(a.y);
           if (masked) {
             const int qq = qs + wg * 32 + 2 * e;
-            p0 = (qq < T && key < T && qq >= key) ? p0 : 0.f;
-            p1 = (qq + 1 < T && key < T && qq + 1 >= key) ? p1 : 0.f;
+            p0 = (qq < T && key < T && (!causal || qq >= key)) ? p0 : 0.f;
+            p1 = (qq + 1 < T && key < T && (!causal || qq + 1 >= key)) ? p1 : 0.f;
           }
           const float2 t = dev::ffma2(make_float2(__uint_as_float(pv[2 * e]), __uint_as_float(pv[2 * e + 1])), sc2,
                                       hh ? make_float2(nd.z, nd.w) : make_float2(nd.x, nd.y));
@@ -1193,6 +1221,7 @@ __global__ void __launch_bounds__(512, 1)
       // sPt / sDSt were last read by block n-1's dV / dK / dQ MMAs
       if (lane == 0 && (warp == 4 || warp == 8) && n < 64) ATTN_TR(n * 16 + 5 + (warp == 8) * 5);
       if (n >= 1) dev::mbar_wait(mma_done, (n - 1) & 1);
+      if (dlut && n >= 1) dev::mbar_wait(ds_read, (n - 1) & 1);  // bias-gradient reads of dS^T_{n-1}
       if (lane == 0 && (warp == 4 || warp == 8) && n < 64) ATTN_TR(n * 16 + 6 + (warp == 8) * 5);
       if (ts) {
         // S^T_n / dP^T_n are in registers already: their first 32 columns take P^T / dS^T
@@ -1254,9 +1283,13 @@ __global__ void __launch_bounds__(512, 1)
     const int wd = d & 31;
     uint8_t* bx = sDQ + (d >> 5) * (BQ2 * 128);
     const bool leader = (warp == 12 && lane == 0);
+    const int tq = static_cast<int>(threadIdx.x) - 384;  // 0..127: owner of bias-gradient slots == tq mod 128
+    if (dlut) {
+      for (int i = tq; i < T + 128; i += 128) sAcc[i] = 0.f;
+    }
     for (int n = 0; n < nq; ++n) {
       const int st = n & 1;
-      const int qs = key0 + n * BQ2;
+      const int qs = qbase + n * BQ2;
       dev::mbar_wait(&dq_full[st], (n >> 1) & 1);
       dev::tc_fence_after();
       if (leader && n < 64) ATTN_TR(n * 16 + 13);
@@ -1266,6 +1299,27 @@ __global__ void __launch_bounds__(512, 1)
       dev::tmem_ld_wait();
       dev::tc_fence_before();
       dev::mbar_arrive(&s_free[st]);
+      if (dlut) {
+        // bias gradient: sums of dS^T_n (bf16 tile, [128 keys][64 queries], SW128) along the
+        // diagonals key - query = const; slot key - query + T - 1 - key0 = dl + c is owned by
+        // thread (dl + c) mod 128, so no two threads ever add to the same slot
+        const int c = T - 1 - qs;
+        const int dl0 = (((tq - c) % 128) + 128) % 128;
+#pragma unroll 1
+        for (int pass = 0; pass < 2; ++pass) {
+          const int dl = pass == 0 ? dl0 : dl0 - 128;
+          if (pass == 1 && dl < -(BQ2 - 1)) break;
+          const int e0 = dl < 0 ? -dl : 0, e1 = 127 - dl < BQ2 - 1 ? 127 - dl : BQ2 - 1;
+          float acc = 0.f;
+          for (int e = e0; e <= e1; ++e) {
+            const int tk = e + dl;
+            const uint8_t* pe = sDSt + tk * 128 + ((((e >> 3) ^ (tk & 7))) << 4) + (e & 7) * 2;
+            acc += __bfloat162float(*reinterpret_cast<const bf16*>(pe));
+          }
+          sAcc[dl + c] += acc;
+        }
+        dev::mbar_arrive(ds_read);
+      }
       if (leader && n < 64) ATTN_TR(n * 16 + 14);
       // the previous block's reduce-adds must have read the staging tile
       if (leader) dev::bulk_wait_read();
@@ -1284,6 +1338,12 @@ __global__ void __launch_bounds__(512, 1)
       }
     }
     if (leader) dev::bulk_wait_all();
+    if (dlut) {
+      float* dl_h = dlut + static_cast<int64_t>(h) * (2 * T + 128) + key0;
+      for (int i = tq; i < T + 128; i += 128) {
+        if (sAcc[i] != 0.f) atomicAdd(dl_h + i, sAcc[i]);
+      }
+    }
   }
   dev::tc_fence_before();
   __syncthreads();
@@ -1379,7 +1439,8 @@ bool bwd2_enabled() {
 }
 
 bool launch_bwd2(const bf16* qkv, const bf16* o, const float* lse, const bf16* dout, bf16* dqkv, float* scratch,
-                 int B, int T, int Hl, cudaStream_t s) {
+                 int B, int T, int Hl, cudaStream_t s, int causal = 1, const float* lut = nullptr,
+                 float* dlut = nullptr, float scale_arg = 0.f) {
   constexpr int HD = 128;
   static bool configured = false;
   if (!configured) {
@@ -1402,10 +1463,11 @@ bool launch_bwd2(const bf16* qkv, const bf16* o, const float* lse, const bf16* d
   const CUtensorMap tm_dq = make_tmap_f32_2d(dq, static_cast<uint64_t>(Dl), static_cast<uint64_t>(M),
                                              static_cast<uint64_t>(Dl), 32, BQ2);
   const int nb = (T + 127) / 128;
-  const double scale = 1.0 / std::sqrt(static_cast<double>(HD));
+  const double scale = scale_arg > 0.f ? scale_arg : 1.0 / std::sqrt(static_cast<double>(HD));
   attn_bwd_tc2<<<nb * B * Hl, 512, Bwd2Layout::BYTES, s>>>(tm_qkv64, tm_qkv128, tm_do64, tm_dq, lse, delta, dqkv,
                                                           T, Hl, static_cast<float>(scale * 1.4426950408889634),
-                                                          static_cast<float>(scale), B * Hl, work_group(), trace_cta(), bwd_dq_first(), bwd_ts());
+                                                          static_cast<float>(scale), B * Hl, work_group(), trace_cta(), bwd_dq_first(),
+                                                          (lut || dlut) ? 1 : bwd_ts(), causal, lut, dlut);
   dq_to_bf16<<<1184, 256, 0, s>>>(dq, dqkv, M, Dl);
   return true;
 }
@@ -1449,11 +1511,25 @@ void attention_trace_read(unsigned long long* out) {
   cudaMemcpyFromSymbol(out, g_attn_trace, sizeof(unsigned long long) * 4096);
 }
 
+bool attention_mma_fwd_ex(const bf16* qkv, bf16* o, float* lse, int B, int T, int Hl, int hd, int causal,
+                          const float* lut, float scale, cudaStream_t s) {
+  if (hd != 128 || ((3 * Hl * hd) % 8) != 0) return false;
+  return launch_fwd2(qkv, o, lse, B, T, Hl, s, causal, lut, scale);
+}
+
 bool attention_mma_fwd(const bf16* qkv, bf16* o, float* lse, int B, int T, int Hl, int hd, cudaStream_t s) {
   if (((3 * Hl * hd) % 8) != 0) return false;
   if (hd == 128) return fwd2_enabled() ? launch_fwd2(qkv, o, lse, B, T, Hl, s) : launch_fwd<128>(qkv, o, lse, B, T, Hl, s);
   if (hd == 64) return launch_fwd<64>(qkv, o, lse, B, T, Hl, s);
   return false;
+}
+
+bool attention_mma_bwd_ex(const bf16* qkv, const bf16* o, const float* lse, const bf16* dout, bf16* dqkv,
+                          float* scratch, int B, int T, int Hl, int hd, int causal, const float* lut, float* dlut,
+                          float scale, cudaStream_t s) {
+  if (hd != 128 || ((Hl * hd) % 8) != 0 || ((lut || dlut) && T + 128 > Bwd2Layout::PT / 4) || !bwd2_enabled())
+    return false;
+  return launch_bwd2(qkv, o, lse, dout, dqkv, scratch, B, T, Hl, s, causal, lut, dlut, scale);
 }
 
 bool attention_mma_bwd(const bf16* qkv, const bf16* o, const float* lse, const bf16* dout, bf16* dqkv,

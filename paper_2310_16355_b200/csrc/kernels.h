@@ -135,6 +135,20 @@ void t5_bias_build(const float* table, const int32_t* ids, int H, int h0, int Hl
 // table_grad[bucket, h0 + h] += sum over positions with that bucket of dbias[h]
 void t5_bias_grad(const float* dbias, const int32_t* ids, int H, int h0, int Hl, int64_t TT, int nb,
                   float* table_grad, cudaStream_t s);
+// tcgen05 attention over fused q|k|v activations in the general form the T5 extension needs:
+// causal or not, optional relative-position bias lut [Hl][2T + 128] (index key - query + T - 1,
+// natural units), score scale; the backward adds the bias gradient into dlut. Returns false
+// (nothing launched) when the shape is not covered (head dim != 128, T + 128 > 4096 with a lut).
+bool attention_fwd_ex(const bf16* qkv, bf16* o, float* lse, int B, int T, int Hl, int hd, int causal,
+                      const float* lut, float scale, cudaStream_t s);
+bool attention_bwd_ex(const bf16* qkv, const bf16* o, const float* lse, const bf16* dout, bf16* dqkv,
+                      float* scratch, int B, int T, int Hl, int hd, int causal, const float* lut, float* dlut,
+                      float scale, cudaStream_t s);
+// lut[h][d + T - 1] = table[bucket[d + T - 1], h0 + h] for d in (-T, T); zero padding to 2T + 128
+void t5_lut_build(const float* table, const int32_t* bucket, int H, int h0, int Hl, int T, float* lut, cudaStream_t s);
+// table_grad[bucket[i], h0 + h] += dlut[h][i] for i < 2T - 1
+void t5_lut_grad(const float* dlut, const int32_t* bucket, int H, int h0, int Hl, int T, float* table_grad,
+                 cudaStream_t s);
 void relu_bf16(bf16* x, int64_t n, cudaStream_t s);
 void relu_bwd_bf16(bf16* g, const bf16* act, int64_t n, cudaStream_t s);  // g *= (act > 0)
 

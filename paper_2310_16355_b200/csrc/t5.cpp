@@ -2,6 +2,7 @@
 #include "t5.h"
 
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 #include "gemm.h"
@@ -65,6 +66,11 @@ T5Model::T5Model(const ModelSpec& spec, const Plan& plan, Mesh* mesh, int batch,
   nb_ = spec.rel_buckets;
   maxd_ = spec.rel_max_distance;
   if (dk_ > 256) fail(SW_ERR_CONFIG, "sw_t5_create: d_kv > 256 is not supported by the attention kernels");
+  fused_x_ = Te_ == Td_;
+  {
+    const char* e = std::getenv("SW_T5_TC");
+    tc_ = fused_x_ && dk_ == 128 && Te_ + 128 <= 4096 && !(e != nullptr && e[0] == '0');
+  }
   cuda_check(cudaSetDevice(mesh->cuda_device), "cudaSetDevice");
   cuda_check(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "cudaStreamCreate");
   build_layout();
@@ -208,6 +214,8 @@ void T5Model::build_layout() {
 
 void T5Model::allocate() {
   const int64_t Me = Me_, Md = Md_, Mx = Me > Md ? Me : Md;
+  ld_cq_ = fused_x_ ? 3LL * il_ : il_;
+  ld_ckv_ = fused_x_ ? 3LL * il_ : 2LL * il_;
   std::vector<int32_t> ids_e(static_cast<size_t>(Te_) * Te_), ids_d(static_cast<size_t>(Td_) * Td_);
   for (int i = 0; i < Te_; ++i)
     for (int j = 0; j < Te_; ++j) ids_e[static_cast<size_t>(i) * Te_ + j] = t5_rel_bucket(j - i, true, nb_, maxd_);
@@ -250,8 +258,14 @@ void T5Model::allocate() {
       R.o_d.push_back(alloc<bf16>(Md * il_));
       R.lse_d.push_back(alloc<float>(Md * hl_));
       R.ax_d.push_back(alloc<bf16>(Md * d_));
-      R.cq_d.push_back(alloc<bf16>(Md * il_));
-      R.ckv_d.push_back(alloc<bf16>(Me * 2 * il_));
+      if (fused_x_) {
+        bf16* x = alloc<bf16>(Md * 3 * il_);
+        R.cq_d.push_back(x);
+        R.ckv_d.push_back(x + il_);
+      } else {
+        R.cq_d.push_back(alloc<bf16>(Md * il_));
+        R.ckv_d.push_back(alloc<bf16>(Me * 2 * il_));
+      }
       R.co_d.push_back(alloc<bf16>(Md * il_));
       R.clse_d.push_back(alloc<float>(Md * hl_));
       R.a2_d.push_back(alloc<bf16>(Md * d_));
@@ -264,10 +278,24 @@ void T5Model::allocate() {
     R.ids_d = alloc<int32_t>(static_cast<int64_t>(Td_) * Td_);
     cuda_check(cudaMemcpyAsync(R.ids_e, ids_e.data(), ids_e.size() * 4, cudaMemcpyHostToDevice, stream_), "H2D");
     cuda_check(cudaMemcpyAsync(R.ids_d, ids_d.data(), ids_d.size() * 4, cudaMemcpyHostToDevice, stream_), "H2D");
-    R.bias_e = alloc<float>(static_cast<int64_t>(hl_) * Te_ * Te_);
-    R.dbias_e = alloc<float>(static_cast<int64_t>(hl_) * Te_ * Te_);
-    R.bias_d = alloc<float>(static_cast<int64_t>(hl_) * Td_ * Td_);
-    R.dbias_d = alloc<float>(static_cast<int64_t>(hl_) * Td_ * Td_);
+    if (tc_) {
+      std::vector<int32_t> be(2 * static_cast<size_t>(Te_) - 1), bd(2 * static_cast<size_t>(Td_) - 1);
+      for (int i = 0; i < 2 * Te_ - 1; ++i) be[i] = t5_rel_bucket(i - (Te_ - 1), true, nb_, maxd_);
+      for (int i = 0; i < 2 * Td_ - 1; ++i) bd[i] = t5_rel_bucket(i - (Td_ - 1), false, nb_, maxd_);
+      R.bd_e = alloc<int32_t>(static_cast<int64_t>(be.size()));
+      R.bd_d = alloc<int32_t>(static_cast<int64_t>(bd.size()));
+      cuda_check(cudaMemcpyAsync(R.bd_e, be.data(), be.size() * 4, cudaMemcpyHostToDevice, stream_), "H2D");
+      cuda_check(cudaMemcpyAsync(R.bd_d, bd.data(), bd.size() * 4, cudaMemcpyHostToDevice, stream_), "H2D");
+      R.lut_e = alloc<float>(static_cast<int64_t>(hl_) * (2 * Te_ + 128));
+      R.dlut_e = alloc<float>(static_cast<int64_t>(hl_) * (2 * Te_ + 128));
+      R.lut_d = alloc<float>(static_cast<int64_t>(hl_) * (2 * Td_ + 128));
+      R.dlut_d = alloc<float>(static_cast<int64_t>(hl_) * (2 * Td_ + 128));
+    } else {
+      R.bias_e = alloc<float>(static_cast<int64_t>(hl_) * Te_ * Te_);
+      R.dbias_e = alloc<float>(static_cast<int64_t>(hl_) * Te_ * Te_);
+      R.bias_d = alloc<float>(static_cast<int64_t>(hl_) * Td_ * Td_);
+      R.dbias_d = alloc<float>(static_cast<int64_t>(hl_) * Td_ * Td_);
+    }
     R.enc_tok = alloc<int32_t>(Me);
     R.dec_tok = alloc<int32_t>(Md);
     R.targets = alloc<int32_t>(Md);
@@ -524,7 +552,12 @@ void T5Model::attn_fwd(T5Rank& R, int Tq, int Tk, const bf16* q, int64_t ldq, co
   a.scale = 1.0f;  // T5: no 1/sqrt(d_kv)
   (void)R;
   tic();
-  k::t5_attention_fwd(a, B_, stream_);
+  // tcgen05 path: fused q|k|v rows (ld 3*inner/t, k and v at +inner/t, +2*inner/t), Tq == Tk
+  const bool tc = tc_ && Tq == Tk && ldq == 3LL * il_ && ldkv == 3LL * il_ && kp == q + il_ && vp == q + 2 * il_;
+  if (!(tc && k::attention_fwd_ex(q, o, lse, B_, Tq, hl_, dk_, causal, bias, 1.0f, stream_))) {
+    if (tc_ && bias != nullptr) fail(SW_ERR_INTERNAL, "T5: the tcgen05 attention forward declined a biased self-attention");
+    k::t5_attention_fwd(a, B_, stream_);
+  }
   toc(kProfAttnFwd, 4.0 * B_ * hl_ * static_cast<double>(Tq) * Tk * dk_ * (causal ? 0.5 : 1.0));
   ++launches_;
 }
@@ -554,8 +587,13 @@ void T5Model::forward(bool need_grad) {
   const int d = d_, il = il_, fl = fl_;
   for (T5Rank& R : ranks_) {
     const int h0 = R.mpi * hl_;
-    k::t5_bias_build(P(R, rb_e_), R.ids_e, H_, h0, hl_, static_cast<int64_t>(Te_) * Te_, R.bias_e, stream_);
-    k::t5_bias_build(P(R, rb_d_), R.ids_d, H_, h0, hl_, static_cast<int64_t>(Td_) * Td_, R.bias_d, stream_);
+    if (tc_) {
+      k::t5_lut_build(P(R, rb_e_), R.bd_e, H_, h0, hl_, Te_, R.lut_e, stream_);
+      k::t5_lut_build(P(R, rb_d_), R.bd_d, H_, h0, hl_, Td_, R.lut_d, stream_);
+    } else {
+      k::t5_bias_build(P(R, rb_e_), R.ids_e, H_, h0, hl_, static_cast<int64_t>(Te_) * Te_, R.bias_e, stream_);
+      k::t5_bias_build(P(R, rb_d_), R.ids_d, H_, h0, hl_, static_cast<int64_t>(Td_) * Td_, R.bias_d, stream_);
+    }
     k::embed_fwd(R.enc_tok, P(R, tok_), nullptr, R.hs_e[0], Me, Te_, d, stream_);
     k::embed_fwd(R.dec_tok, P(R, tok_), nullptr, R.hs_d[0], Md, Td_, d, stream_);
     launches_ += 4;
@@ -568,7 +606,7 @@ void T5Model::forward(bool need_grad) {
       gemm(static_cast<int>(Me), 3 * il, d, R.a1_e[l], d, 0, W(R, L.q), d, 0, static_cast<int>(Epi::kStoreBf16),
            R.qkv_e[l], 3 * il);
       attn_fwd(R, Te_, Te_, R.qkv_e[l], 3 * il, R.qkv_e[l] + il, R.qkv_e[l] + 2 * il, 3 * il, R.o_e[l], R.lse_e[l],
-               R.bias_e, 0);
+               tc_ ? R.lut_e : R.bias_e, 0);
     }
     row_parallel(Me, il, [&](T5Rank& R) -> const bf16* { return R.o_e[l]; }, L.o,
                  [&](T5Rank& R) -> const float* { return R.hs_e[l]; }, [&](T5Rank& R) { return R.hm_e[l]; });
@@ -591,17 +629,18 @@ void T5Model::forward(bool need_grad) {
       gemm(static_cast<int>(Md), 3 * il, d, R.a1_d[l], d, 0, W(R, L.q), d, 0, static_cast<int>(Epi::kStoreBf16),
            R.qkv_d[l], 3 * il);
       attn_fwd(R, Td_, Td_, R.qkv_d[l], 3 * il, R.qkv_d[l] + il, R.qkv_d[l] + 2 * il, 3 * il, R.o_d[l], R.lse_d[l],
-               R.bias_d, 1);
+               tc_ ? R.lut_d : R.bias_d, 1);
     }
     row_parallel(Md, il, [&](T5Rank& R) -> const bf16* { return R.o_d[l]; }, L.o,
                  [&](T5Rank& R) -> const float* { return R.hs_d[l]; }, [&](T5Rank& R) { return R.hm_d[l]; });
     for (T5Rank& R : ranks_) {
       rms_fwd(R.hm_d[l], L.lnx, R, R.ax_d[l], R.stx_d[l], Md);
       gemm(static_cast<int>(Md), il, d, R.ax_d[l], d, 0, W(R, L.cq), d, 0, static_cast<int>(Epi::kStoreBf16),
-           R.cq_d[l], il);
+           R.cq_d[l], ld_cq_);
       gemm(static_cast<int>(Me), 2 * il, d, R.eo, d, 0, W(R, L.ck), d, 0, static_cast<int>(Epi::kStoreBf16),
-           R.ckv_d[l], 2 * il);
-      attn_fwd(R, Td_, Te_, R.cq_d[l], il, R.ckv_d[l], R.ckv_d[l] + il, 2 * il, R.co_d[l], R.clse_d[l], nullptr, 0);
+           R.ckv_d[l], ld_ckv_);
+      attn_fwd(R, Td_, Te_, R.cq_d[l], ld_cq_, R.ckv_d[l], R.ckv_d[l] + il, ld_ckv_, R.co_d[l], R.clse_d[l], nullptr,
+               0);
     }
     row_parallel(Md, il, [&](T5Rank& R) -> const bf16* { return R.co_d[l]; }, L.co,
                  [&](T5Rank& R) -> const float* { return R.hm_d[l]; }, [&](T5Rank& R) { return R.hx_d[l]; });
@@ -636,8 +675,13 @@ void T5Model::backward() {
   const int F32 = static_cast<int>(Epi::kStoreF32), BF = static_cast<int>(Epi::kStoreBf16);
   for (T5Rank& R : ranks_) {
     cuda_check(cudaMemsetAsync(R.g, 0, flat_n_ * 4, stream_), "memset");
-    cuda_check(cudaMemsetAsync(R.dbias_e, 0, sizeof(float) * hl_ * Te_ * Te_, stream_), "memset");
-    cuda_check(cudaMemsetAsync(R.dbias_d, 0, sizeof(float) * hl_ * Td_ * Td_, stream_), "memset");
+    if (tc_) {
+      cuda_check(cudaMemsetAsync(R.dlut_e, 0, sizeof(float) * hl_ * (2 * Te_ + 128), stream_), "memset");
+      cuda_check(cudaMemsetAsync(R.dlut_d, 0, sizeof(float) * hl_ * (2 * Td_ + 128), stream_), "memset");
+    } else {
+      cuda_check(cudaMemsetAsync(R.dbias_e, 0, sizeof(float) * hl_ * Te_ * Te_, stream_), "memset");
+      cuda_check(cudaMemsetAsync(R.dbias_d, 0, sizeof(float) * hl_ * Td_ * Td_, stream_), "memset");
+    }
     cuda_check(cudaMemsetAsync(R.d_eout, 0, sizeof(float) * Me * d, stream_), "memset");
     // d(final) = dlogits . W_head; dW_head = dlogits^T . f (replicated head: no collective)
     gemm(static_cast<int>(Md), d, V_, R.logits, V_, 0, W(R, head_), d, 1, F32, R.dx, d);
@@ -665,7 +709,13 @@ void T5Model::backward() {
     a.causal = causal;
     a.scale = 1.0f;
     tic();
-    k::t5_attention_bwd(a, B_, R.dout, il, dq, lddq, dkp, lddkv, dvp, lddkv, R.attn_scratch, dbias, stream_);
+    const bool tc = tc_ && Tq == Tk && ldq == 3LL * il && ldkv == 3LL * il && kp == q + il && vp == q + 2 * il &&
+                    lddq == 3LL * il && lddkv == 3LL * il && dkp == dq + il && dvp == dq + 2 * il;
+    if (!(tc && k::attention_bwd_ex(q, o, lse, R.dout, dq, R.attn_scratch, B_, Tq, hl_, dk_, causal, bias, dbias, 1.0f,
+                                    stream_))) {
+      if (tc_ && bias != nullptr) fail(SW_ERR_INTERNAL, "T5: the tcgen05 attention backward declined (SW_ATTN_BWD_V1?)");
+      k::t5_attention_bwd(a, B_, R.dout, il, dq, lddq, dkp, lddkv, dvp, lddkv, R.attn_scratch, dbias, stream_);
+    }
     toc(kProfAttnBwd, 8.0 * B_ * hl_ * static_cast<double>(Tq) * Tk * dk_ * (causal ? 0.5 : 1.0));
     launches_ += 3;
   };
@@ -687,13 +737,16 @@ void T5Model::backward() {
     for (T5Rank& R : ranks_) {
       gemm(static_cast<int>(Md), il, d, R.gb, d, 0, W(R, L.co), il, 1, BF, R.dout, il);
       gemm(d, il, static_cast<int>(Md), R.gb, d, 1, R.co_d[l], il, 1, F32, G(R, L.co), il);
-      attn_bwd(R, Td_, Te_, R.cq_d[l], il, R.ckv_d[l], R.ckv_d[l] + il, 2 * il, R.co_d[l], R.clse_d[l], nullptr, 0,
-               R.dcq, il, R.dckv, R.dckv + il, 2 * il, nullptr);
-      gemm(static_cast<int>(Md), d, il, R.dcq, il, 0, W(R, L.cq), d, 1, F32, R.dx, d);
-      gemm(il, d, static_cast<int>(Md), R.dcq, il, 1, R.ax_d[l], d, 1, F32, G(R, L.cq), d);
+      // fused layout: dq | dk | dv land in one [M, 3*inner/t] buffer like the forward's
+      bf16* dcq = fused_x_ ? R.dqkv : R.dcq;
+      bf16* dckv = fused_x_ ? R.dqkv + il : R.dckv;
+      attn_bwd(R, Td_, Te_, R.cq_d[l], ld_cq_, R.ckv_d[l], R.ckv_d[l] + il, ld_ckv_, R.co_d[l], R.clse_d[l], nullptr, 0,
+               dcq, ld_cq_, dckv, dckv + il, ld_ckv_, nullptr);
+      gemm(static_cast<int>(Md), d, il, dcq, ld_cq_, 0, W(R, L.cq), d, 1, F32, R.dx, d);
+      gemm(il, d, static_cast<int>(Md), dcq, ld_cq_, 1, R.ax_d[l], d, 1, F32, G(R, L.cq), d);
       // encoder-output gradient: partial over the mp group, summed over layers, reduced once
-      gemm(static_cast<int>(Me), d, 2 * il, R.dckv, 2 * il, 0, W(R, L.ck), d, 1, F32, R.d_eout, d, nullptr, 0, 1);
-      gemm(2 * il, d, static_cast<int>(Me), R.dckv, 2 * il, 1, R.eo, d, 1, F32, G(R, L.ck), d);
+      gemm(static_cast<int>(Me), d, 2 * il, dckv, ld_ckv_, 0, W(R, L.ck), d, 1, F32, R.d_eout, d, nullptr, 0, 1);
+      gemm(2 * il, d, static_cast<int>(Me), dckv, ld_ckv_, 1, R.eo, d, 1, F32, G(R, L.ck), d);
     }
     ar([](T5Rank& R) { return R.dx; }, Md * d);
     for (T5Rank& R : ranks_) rms_bwd(R.hm_d[l], R.stx_d[l], L.lnx, R, R.dx, R.gres_d, Md, 1);
@@ -702,7 +755,8 @@ void T5Model::backward() {
       gemm(static_cast<int>(Md), il, d, R.gb, d, 0, W(R, L.o), il, 1, BF, R.dout, il);
       gemm(d, il, static_cast<int>(Md), R.gb, d, 1, R.o_d[l], il, 1, F32, G(R, L.o), il);
       attn_bwd(R, Td_, Td_, R.qkv_d[l], 3 * il, R.qkv_d[l] + il, R.qkv_d[l] + 2 * il, 3 * il, R.o_d[l], R.lse_d[l],
-               R.bias_d, 1, R.dqkv, 3 * il, R.dqkv + il, R.dqkv + 2 * il, 3 * il, R.dbias_d);
+               tc_ ? R.lut_d : R.bias_d, 1, R.dqkv, 3 * il, R.dqkv + il, R.dqkv + 2 * il, 3 * il,
+               tc_ ? R.dlut_d : R.dbias_d);
       gemm(static_cast<int>(Md), d, 3 * il, R.dqkv, 3 * il, 0, W(R, L.q), d, 1, F32, R.dx, d);
       gemm(3 * il, d, static_cast<int>(Md), R.dqkv, 3 * il, 1, R.a1_d[l], d, 1, F32, G(R, L.q), d);
     }
@@ -711,8 +765,11 @@ void T5Model::backward() {
   }
   for (T5Rank& R : ranks_) {
     k::embed_bwd_tok(R.dec_tok, R.gres_d, G(R, tok_), Md, d, V_, R.tok_keys, stream_);
-    k::t5_bias_grad(R.dbias_d, R.ids_d, H_, R.mpi * hl_, hl_, static_cast<int64_t>(Td_) * Td_, nb_, G(R, rb_d_),
-                    stream_);
+    if (tc_)
+      k::t5_lut_grad(R.dlut_d, R.bd_d, H_, R.mpi * hl_, hl_, Td_, G(R, rb_d_), stream_);
+    else
+      k::t5_bias_grad(R.dbias_d, R.ids_d, H_, R.mpi * hl_, hl_, static_cast<int64_t>(Td_) * Td_, nb_, G(R, rb_d_),
+                      stream_);
     launches_ += 2;
   }
   ar([this](T5Rank& R) { return G(R, rb_d_); }, static_cast<int64_t>(nb_) * H_);
@@ -735,7 +792,8 @@ void T5Model::backward() {
       gemm(static_cast<int>(Me), il, d, R.gb, d, 0, W(R, L.o), il, 1, BF, R.dout, il);
       gemm(d, il, static_cast<int>(Me), R.gb, d, 1, R.o_e[l], il, 1, F32, G(R, L.o), il);
       attn_bwd(R, Te_, Te_, R.qkv_e[l], 3 * il, R.qkv_e[l] + il, R.qkv_e[l] + 2 * il, 3 * il, R.o_e[l], R.lse_e[l],
-               R.bias_e, 0, R.dqkv, 3 * il, R.dqkv + il, R.dqkv + 2 * il, 3 * il, R.dbias_e);
+               tc_ ? R.lut_e : R.bias_e, 0, R.dqkv, 3 * il, R.dqkv + il, R.dqkv + 2 * il, 3 * il,
+               tc_ ? R.dlut_e : R.dbias_e);
       gemm(static_cast<int>(Me), d, 3 * il, R.dqkv, 3 * il, 0, W(R, L.q), d, 1, F32, R.dx, d);
       gemm(3 * il, d, static_cast<int>(Me), R.dqkv, 3 * il, 1, R.a1_e[l], d, 1, F32, G(R, L.q), d);
     }
@@ -744,8 +802,11 @@ void T5Model::backward() {
   }
   for (T5Rank& R : ranks_) {
     k::embed_bwd_tok(R.enc_tok, R.gres_e, G(R, tok_), Me, d, V_, R.tok_keys, stream_);
-    k::t5_bias_grad(R.dbias_e, R.ids_e, H_, R.mpi * hl_, hl_, static_cast<int64_t>(Te_) * Te_, nb_, G(R, rb_e_),
-                    stream_);
+    if (tc_)
+      k::t5_lut_grad(R.dlut_e, R.bd_e, H_, R.mpi * hl_, hl_, Te_, G(R, rb_e_), stream_);
+    else
+      k::t5_bias_grad(R.dbias_e, R.ids_e, H_, R.mpi * hl_, hl_, static_cast<int64_t>(Te_) * Te_, nb_, G(R, rb_e_),
+                      stream_);
     launches_ += 2;
   }
   ar([this](T5Rank& R) { return G(R, rb_e_); }, static_cast<int64_t>(nb_) * H_);

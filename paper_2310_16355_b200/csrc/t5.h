@@ -50,6 +50,9 @@ struct T5Rank {
   // relative-position bias (this rank's heads) and its gradient
   int32_t *ids_e = nullptr, *ids_d = nullptr;
   float *bias_e = nullptr, *bias_d = nullptr, *dbias_e = nullptr, *dbias_d = nullptr;
+  // tcgen05 path: the bias as a per-head LUT over key - query ([Hl][2T + 128]) and its gradient
+  int32_t *bd_e = nullptr, *bd_d = nullptr;  // bucket of each offset key - query + T - 1
+  float *lut_e = nullptr, *lut_d = nullptr, *dlut_e = nullptr, *dlut_d = nullptr;
   // inputs
   int32_t *enc_tok = nullptr, *dec_tok = nullptr, *targets = nullptr;
   float *weights = nullptr, *wloss = nullptr, *wsum = nullptr;
@@ -116,6 +119,12 @@ class T5Model {
   int64_t Me_, Md_;
   int Le_, Ld_, d_, H_, dk_, inner_, dff_, V_, nb_, maxd_;
   int t_ = 1, hl_ = 0, il_ = 0, fl_ = 0;
+  // Te == Td: cross-attention q | k | v share one [B*T, 3*inner/t] buffer (the q GEMM writes
+  // columns [0, inner/t), the k|v GEMM over the encoder output the rest), which is the fused
+  // layout the tcgen05 attention reads; tc_: head dim 128 and Te == Td (SW_T5_TC=0 forces the
+  // CUDA-core kernels)
+  bool fused_x_ = false, tc_ = false;
+  int64_t ld_cq_ = 0, ld_ckv_ = 0;
   std::vector<Slot> slots_;
   std::unordered_map<std::string, int> slot_of_;
   std::vector<T5Layer> enc_, dec_;

@@ -207,6 +207,26 @@ __global__ void relu_bwd_bf16_kernel(bf16* __restrict__ g, const bf16* __restric
   }
 }
 
+__global__ void t5_lut_build_kernel(const float* __restrict__ table, const int32_t* __restrict__ bucket, int H,
+                                    int h0, int Hl, int T, float* __restrict__ lut) {
+  const int64_t W = 2LL * T + 128, n = static_cast<int64_t>(Hl) * W;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t h = e / W, i = e - h * W;
+    lut[e] = i < 2LL * T - 1 ? table[static_cast<int64_t>(bucket[i]) * H + h0 + h] : 0.f;
+  }
+}
+
+__global__ void t5_lut_grad_kernel(const float* __restrict__ dlut, const int32_t* __restrict__ bucket, int H,
+                                   int h0, int T, float* __restrict__ table_grad) {
+  const int h = blockIdx.y;
+  const float* src = dlut + static_cast<int64_t>(h) * (2LL * T + 128);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < 2 * T - 1; i += gridDim.x * blockDim.x) {
+    const float g = src[i];
+    if (g != 0.f) atomicAdd(table_grad + static_cast<int64_t>(bucket[i]) * H + h0 + h, g);
+  }
+}
+
 unsigned blocks_for(int64_t n) {
   const int64_t b = (n + 255) / 256;
   return static_cast<unsigned>(b < 148 * 16 ? (b > 0 ? b : 1) : 148 * 16);
@@ -246,6 +266,17 @@ void t5_bias_grad(const float* dbias, const int32_t* ids, int H, int h0, int Hl,
   const int64_t per = 256 * 16;
   dim3 grid(static_cast<unsigned>((TT + per - 1) / per), Hl);
   t5_bias_grad_kernel<<<grid, 256, nb * sizeof(float), s>>>(dbias, ids, H, h0, TT, nb, table_grad);
+}
+
+void t5_lut_build(const float* table, const int32_t* bucket, int H, int h0, int Hl, int T, float* lut, cudaStream_t s) {
+  t5_lut_build_kernel<<<blocks_for(static_cast<int64_t>(Hl) * (2LL * T + 128)), 256, 0, s>>>(table, bucket, H, h0, Hl, T,
+                                                                                          lut);
+}
+
+void t5_lut_grad(const float* dlut, const int32_t* bucket, int H, int h0, int Hl, int T, float* table_grad,
+                 cudaStream_t s) {
+  dim3 grid(static_cast<unsigned>((2 * T + 255) / 256), Hl);
+  t5_lut_grad_kernel<<<grid, 256, 0, s>>>(dlut, bucket, H, h0, T, table_grad);
 }
 
 void relu_bf16(bf16* x, int64_t n, cudaStream_t s) { relu_bf16_kernel<<<blocks_for(n), 256, 0, s>>>(x, n); }
