@@ -30,6 +30,12 @@ constexpr int B_STAGE = BN * BK * 2;  // 32 KiB
 constexpr int STAGE_BYTES = A_STAGE + B_STAGE;
 constexpr int TMEM_COLS = 512;
 constexpr int NUM_THREADS = 256;
+#ifndef SW_EXP_NO_STATE_STORE
+#define SW_EXP_NO_STATE_STORE 0
+#endif
+#ifndef SW_EXP_NO_SHADOW_STORE
+#define SW_EXP_NO_SHADOW_STORE 0
+#endif
 #ifndef SW_EPI_PF
 #define SW_EPI_PF 0  // epilogue: 0 = load-wait-process per chunk (measured best), 2 = next chunk TMEM load in flight
 #endif
@@ -539,7 +545,7 @@ __device__ __forceinline__ void adamw_chunk_smem(const GemmParams& p, float* sbo
       }
     }
   }
-  if (row < p.M) {
+  if (row < p.M && !SW_EXP_NO_SHADOW_STORE) {  // (the macro: timing experiment only)
     __nv_bfloat16* w = reinterpret_cast<__nv_bfloat16*>(p.adam_w) + static_cast<int64_t>(row) * p.ldc + col0;
 #pragma unroll
     for (int c = 0; c < OC / 4; c += 2) {
@@ -806,9 +812,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(p_threads<EPI>(), 1)
         __syncwarp();
         if (lane == 0) {
           const int rw = row - static_cast<int>(lane);
+#if !SW_EXP_NO_STATE_STORE  // timing experiment only (results invalid when set)
           dev::tma_store_2d(&om.p, sbox, col0, rw);
           dev::tma_store_2d(&om.m, sbox + OPT_ARR / 4, col0, rw);
           dev::tma_store_2d(&om.v, sbox + OPT_ARR / 2, col0, rw);
+#endif
           dev::bulk_commit();
           dev::bulk_wait_read();  // the stores have left shared memory: hand the buffer back
           dev::mbar_arrive(&oempty[wg]);
