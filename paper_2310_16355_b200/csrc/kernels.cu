@@ -457,24 +457,36 @@ __global__ void __launch_bounds__(THREADS, 2) ln_bwd2_kernel(
 
 // dscale[c] += sum_b partials[b][0][c], dbias[c] += sum_b partials[b][1][c]: four interleaved
 // accumulators (b mod 4) combined in a fixed order -- deterministic, and four loads in flight.
-__global__ void ln_param_reduce_kernel(const float* __restrict__ partials, int nblk, int d, float* __restrict__ dscale,
-                                       float* __restrict__ dbias) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= 2 * d) return;
-  const int which = c / d, col = c - which * d;
-  const float* src = partials + which * d + col;
-  const int64_t stride = 2LL * d;
-  float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
-  int b = 0;
-  for (; b + 3 < nblk; b += 4) {
-    s0 += src[(b + 0) * stride];
-    s1 += src[(b + 1) * stride];
-    s2 += src[(b + 2) * stride];
-    s3 += src[(b + 3) * stride];
+// Sum of the per-CTA LayerNorm parameter partials [nblk][2][d] in a fixed order (bit-identical
+// on every replica): a CTA owns 32 columns; its 8 warps take interleaved row groups (coalesced
+// 128-byte rows, 8x the loads in flight of one thread per column) and combine in warp order.
+__global__ void __launch_bounds__(256) ln_param_reduce_kernel(const float* __restrict__ partials, int nblk, int d,
+                                                              float* __restrict__ dscale, float* __restrict__ dbias) {
+  __shared__ float red[8][33];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int c = blockIdx.x * 32 + lane;  // in [0, 2d)
+  float s0 = 0.f, s1 = 0.f;
+  if (c < 2 * d) {
+    const int which = c / d, col = c - which * d;
+    const float* src = partials + which * d + col;
+    const int64_t stride = 2LL * d;
+    int b = w;
+    for (; b + 8 < nblk; b += 16) {
+      s0 += src[b * stride];
+      s1 += src[(b + 8) * stride];
+    }
+    for (; b < nblk; b += 8) s0 += src[b * stride];
   }
-  for (; b < nblk; ++b) s0 += src[b * stride];
-  float* o = which == 0 ? dscale : dbias;
-  if (o != nullptr) o[col] += (s0 + s1) + (s2 + s3);
+  red[w][lane] = s0 + s1;
+  __syncthreads();
+  if (w == 0 && c < 2 * d) {
+    float t = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) t += red[i][lane];
+    const int which = c / d, col = c - which * d;
+    float* o = which == 0 ? dscale : dbias;
+    if (o != nullptr) o[col] += t;
+  }
 }
 
 template <typename DY>
@@ -1016,8 +1028,8 @@ static void layernorm_bwd_t(const float* x, const float* mean, const float* rstd
     return;
   }
   if (partials != nullptr) {
-    ln_param_reduce_kernel<<<static_cast<unsigned>((2 * d + 63) / 64), 64, 0, s>>>(partials, static_cast<int>(nblk), d,
-                                                                                  dscale, dbias);
+    ln_param_reduce_kernel<<<static_cast<unsigned>((2 * d + 31) / 32), 256, 0, s>>>(partials, static_cast<int>(nblk), d,
+                                                                                   dscale, dbias);
   }
 }
 
