@@ -229,11 +229,20 @@ __device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int row, int
     const __nv_bfloat16* pre = reinterpret_cast<const __nv_bfloat16*>(p.aux) + static_cast<int64_t>(row) * p.ld_aux;
     __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(p.C) + static_cast<int64_t>(row) * p.ldc;
     const int half = p.swiglu_half;
+    // every pre-activation load ahead of the stores (C and aux are not declared disjoint, so a
+    // load after a store would wait for it)
+    uint4 rgs[4], rus[4];
 #pragma unroll
     for (int c = 0; c < 32; c += 8) {
       if (c < ncols) {
-        const uint4 rg = *reinterpret_cast<const uint4*>(pre + col0 + c);
-        const uint4 ru = *reinterpret_cast<const uint4*>(pre + half + col0 + c);
+        rgs[c / 8] = *reinterpret_cast<const uint4*>(pre + col0 + c);
+        rus[c / 8] = *reinterpret_cast<const uint4*>(pre + half + col0 + c);
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < 32; c += 8) {
+      if (c < ncols) {
+        const uint4 rg = rgs[c / 8], ru = rus[c / 8];
         const uint32_t wg[4] = {rg.x, rg.y, rg.z, rg.w}, wu[4] = {ru.x, ru.y, ru.z, ru.w};
         uint32_t og[4], ou[4];
 #pragma unroll

@@ -28,7 +28,13 @@ def main(kind, M=12288, N=4096, K=8192):
     A2 = torch.randn(M, K, device="cuda").bfloat16()
     B2 = torch.randn(N, K, device="cuda").bfloat16()
     for _ in range(3):
-        if kind == "resid":  # forward residual epilogue (kResidF32): K-major operands
+        if kind == "swiglu":  # fused gate|up forward: N = h columns, B = [gate; up] [2N, K]
+            Wgu = torch.randn(2 * N, K, device="cuda").bfloat16()
+            Hh = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+            PRE = torch.empty(M, 2 * N, device="cuda", dtype=torch.bfloat16)
+            _lib.check(L.sw_k_gemm_bf16_swiglu(M, N, K, A2.data_ptr(), K, Wgu.data_ptr(), K, Hh.data_ptr(), N,
+                                               PRE.data_ptr(), 2 * N, s))
+        elif kind == "resid":  # forward residual epilogue (kResidF32): K-major operands
             _lib.check(L.sw_k_gemm_bf16(M, N, K, A2.data_ptr(), K, 0, B2.data_ptr(), K, 0, 3, outf.data_ptr(), N,
                                         None, 0, None, aux.data_ptr(), N, 1.0, 0, s))
         elif kind == "fused":
