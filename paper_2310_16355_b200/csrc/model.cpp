@@ -711,7 +711,8 @@ void Model::gemm(Rank& R, int M, int N, int K, const void* A, int64_t lda, int a
   p.accumulate = accumulate;
   tic();
   cuda_check(gemm_bf16(p, stream_), "gemm launch");
-  toc(kProfGemm, 2.0 * M * N * static_cast<double>(K));
+  // kSwiGLU multiplies by the fused [gate; up] weight: 2N output columns of MMA work
+  toc(kProfGemm, 2.0 * M * (epi == static_cast<int>(Epi::kSwiGLU) ? 2.0 * N : N) * static_cast<double>(K));
   if (prof_) {
     prof_tag_.resize(prof_rec_.size());
     prof_tag_.back() = "gemm," + std::to_string(M) + "," + std::to_string(N) + "," + std::to_string(K) + ",epi" +
