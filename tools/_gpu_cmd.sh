@@ -1,6 +1,4 @@
-for i in 1 2; do for lib in paper_2310_16355_b200/libshardweave_b200.so variants/libsw_nostate.so variants/libsw_noshadow.so; do
-  echo "$lib"; SW_LIB_PATH=$lib python -c "
-import sys, json; sys.path.insert(0,'.')
-from tools.gemm_bench import bench_adamw
-for sh in [(12288,4096,8192)]: print(json.dumps(bench_adamw(*sh)))"
-done; done > gpurun_out/x_ab.log 2>&1
+timeout 600 python -m pytest tests -m gpu -q > gpurun_out/t.log 2>&1; echo EXIT $? >> gpurun_out/t.log
+timeout 600 python bench.py > gpurun_out/r1c_bench.log 2>&1
+rm -f gpurun_out/prof.csv; SW_PROFILE_LOG=gpurun_out/prof.csv timeout 400 python bench.py --spec oracle/specs/llama7b_swiglu.spec --no-cpu-baseline > gpurun_out/r1c_bench_swiglu.log 2>&1
+python tools/gemm_shape_report.py gpurun_out/prof.csv 2 > gpurun_out/r1c_swiglu_shapes.log
