@@ -342,11 +342,14 @@ def test_replicated_param_grads_are_deterministic():
         assert np.array_equal(runs[0][n], runs[1][n]), n
 
 
-@pytest.mark.parametrize("spec_name", ["llama7b_vocab_parallel.spec", "llama7b_swiglu.spec"])
-def test_llama7b_width_tp8_matches_tp1(spec_name):
+@pytest.mark.parametrize("spec_name,ar_bf16", [("llama7b_vocab_parallel.spec", "0"), ("llama7b_swiglu.spec", "0"),
+                                               ("llama7b_vocab_parallel.spec", "1")])
+def test_llama7b_width_tp8_matches_tp1(spec_name, ar_bf16, monkeypatch):
     """The shapes the 8-GPU scaling run hits (LLaMA-7B width at mp = 8: 4 heads, d/t = 512,
     d_ff/t = 1376 (GEMM N and K tails), vocab shard 4000), depth 2 and 512 tokens, on the
-    emulated mesh: the mp = 8 step equals the unsharded one."""
+    emulated mesh: the mp = 8 step equals the unsharded one, with fp32 or bf16 (what bench.py uses
+    at N > 1) all-reduce payloads."""
+    monkeypatch.setenv("SW_AR_BF16", ar_bf16)
     text = open(os.path.join(SPECS, spec_name)).read().replace("n_layers = 32", "n_layers = 2")
     spec = rules.parse_model_spec(text)
     rng = np.random.default_rng(3)
