@@ -4,6 +4,7 @@
 // parameter init. All are HBM-bound; they use 16-byte vector accesses where the row pitch
 // allows and grid-stride loops sized to the SM count.
 #include <cmath>
+#include <stdexcept>
 #include <cstdint>
 
 #include "kernels.h"
@@ -334,7 +335,9 @@ __device__ __forceinline__ float4 block_sum4(float4 v, float* red) {
 // are in flight together, their four row sums share one block reduction, and the residual
 // gradient of both rows is prefetched into L1 before that reduction so its latency hides behind
 // it. x / dy are kept in registers between the passes (no re-read).
-template <int THREADS, int V4, typename DY>
+// WG: also the column sums of the written residual gradient g_io (the bias gradient of the
+// row-parallel projection whose output feeds this LayerNorm), as a third partial row.
+template <int THREADS, int V4, typename DY, bool WG>
 __global__ void __launch_bounds__(THREADS, 2) ln_bwd2_kernel(
     const float* __restrict__ x, const float* __restrict__ mean, const float* __restrict__ rstd,
     const float* __restrict__ scale, const DY* __restrict__ dy, float* __restrict__ g_io,
@@ -342,6 +345,13 @@ __global__ void __launch_bounds__(THREADS, 2) ln_bwd2_kernel(
     int d, int accumulate, float* __restrict__ partials, int rms) {
   __shared__ __align__(16) float red[4 * (THREADS / 32)];
   float4 ds[V4], db[V4];
+  // column sums of g_io live in shared memory ([j][thread] float4, conflict-free), not in
+  // registers: the two-row kernel is at its register budget
+  __shared__ float4 gsm[WG ? V4 * THREADS : 1];
+  if constexpr (WG) {
+#pragma unroll
+    for (int j = 0; j < V4; ++j) gsm[j * THREADS + threadIdx.x] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
 #pragma unroll
   for (int j = 0; j < V4; ++j) ds[j] = db[j] = make_float4(0, 0, 0, 0);
   const int64_t pairs = (M + 1) / 2;
@@ -412,6 +422,8 @@ __global__ void __launch_bounds__(THREADS, 2) ln_bwd2_kernel(
           o.x += g.x; o.y += g.y; o.z += g.z; o.w += g.w;
         }
         *reinterpret_cast<float4*>(g_io + r0 * d + c) = o;
+        float4 gacc;
+        if constexpr (WG) gacc = o;
         uint2 w;
         w.x = dev::pack_bf16x2(o.x, o.y);
         w.y = dev::pack_bf16x2(o.z, o.w);
@@ -426,9 +438,17 @@ __global__ void __launch_bounds__(THREADS, 2) ln_bwd2_kernel(
             o.x += g.x; o.y += g.y; o.z += g.z; o.w += g.w;
           }
           *reinterpret_cast<float4*>(g_io + r1 * d + c) = o;
+          if constexpr (WG) {
+            gacc.x += o.x; gacc.y += o.y; gacc.z += o.z; gacc.w += o.w;
+          }
           w.x = dev::pack_bf16x2(o.x, o.y);
           w.y = dev::pack_bf16x2(o.z, o.w);
           *reinterpret_cast<uint2*>(g_bf16 + r1 * d + c) = w;
+        }
+        if constexpr (WG) {
+          float4 t = gsm[j * THREADS + threadIdx.x];
+          t.x += gacc.x; t.y += gacc.y; t.z += gacc.z; t.w += gacc.w;
+          gsm[j * THREADS + threadIdx.x] = t;
         }
       }
     }
@@ -438,9 +458,10 @@ __global__ void __launch_bounds__(THREADS, 2) ln_bwd2_kernel(
     const int c = (threadIdx.x + j * THREADS) * 4;
     if (c < d) {
       if (partials != nullptr) {  // deterministic: per-CTA partials, summed in CTA order later
-        float* pp = partials + static_cast<int64_t>(blockIdx.x) * 2 * d;
+        float* pp = partials + static_cast<int64_t>(blockIdx.x) * (WG ? 3 : 2) * d;
         *reinterpret_cast<float4*>(pp + c) = ds[j];
         *reinterpret_cast<float4*>(pp + d + c) = db[j];
+        if constexpr (WG) *reinterpret_cast<float4*>(pp + 2 * d + c) = gsm[j * THREADS + threadIdx.x];
       } else {
         atomicAdd(dscale + c, ds[j].x); atomicAdd(dscale + c + 1, ds[j].y);
         atomicAdd(dscale + c + 2, ds[j].z); atomicAdd(dscale + c + 3, ds[j].w);
@@ -461,15 +482,16 @@ __global__ void __launch_bounds__(THREADS, 2) ln_bwd2_kernel(
 // on every replica): a CTA owns 32 columns; its 8 warps take interleaved row groups (coalesced
 // 128-byte rows, 8x the loads in flight of one thread per column) and combine in warp order.
 __global__ void __launch_bounds__(256) ln_param_reduce_kernel(const float* __restrict__ partials, int nblk, int d,
-                                                              float* __restrict__ dscale, float* __restrict__ dbias) {
+                                                              float* __restrict__ dscale, float* __restrict__ dbias,
+                                                              int nsec, float* __restrict__ gsum) {
   __shared__ float red[8][33];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int c = blockIdx.x * 32 + lane;  // in [0, 2d)
+  const int c = blockIdx.x * 32 + lane;  // in [0, nsec * d)
   float s0 = 0.f, s1 = 0.f;
-  if (c < 2 * d) {
+  if (c < nsec * d) {
     const int which = c / d, col = c - which * d;
     const float* src = partials + which * d + col;
-    const int64_t stride = 2LL * d;
+    const int64_t stride = static_cast<int64_t>(nsec) * d;
     int b = w;
     for (; b + 8 < nblk; b += 16) {
       s0 += src[b * stride];
@@ -479,12 +501,12 @@ __global__ void __launch_bounds__(256) ln_param_reduce_kernel(const float* __res
   }
   red[w][lane] = s0 + s1;
   __syncthreads();
-  if (w == 0 && c < 2 * d) {
+  if (w == 0 && c < nsec * d) {
     float t = 0.f;
 #pragma unroll
     for (int i = 0; i < 8; ++i) t += red[i][lane];
     const int which = c / d, col = c - which * d;
-    float* o = which == 0 ? dscale : dbias;
+    float* o = which == 0 ? dscale : which == 1 ? dbias : gsum;
     if (o != nullptr) o[col] += t;
   }
 }
@@ -1004,7 +1026,8 @@ int64_t layernorm_bwd_partials(int d) { return static_cast<int64_t>(4 * kSMs) * 
 template <typename DY>
 static void layernorm_bwd_t(const float* x, const float* mean, const float* rstd, const float* scale, const DY* dy,
                             float* g_io, bf16* g_bf16, float* dscale, float* dbias, int64_t M, int d, int accumulate,
-                            cudaStream_t s, float* partials, int rms) {
+                            cudaStream_t s, float* partials, int rms, float* gsum) {
+  bool gsum_fused = false;
   const unsigned g = static_cast<unsigned>(M < 4 * kSMs ? M : 4 * kSMs);
   unsigned nblk = g;
   if (d % 4 == 0 && d <= 512) {
@@ -1016,8 +1039,14 @@ static void layernorm_bwd_t(const float* x, const float* mean, const float* rstd
   } else if (d % 4 == 0 && d <= 4096) {
     const unsigned g2 = static_cast<unsigned>((M + 1) / 2 < 2 * kSMs ? (M + 1) / 2 : 2 * kSMs);
     nblk = g2;
-    ln_bwd2_kernel<256, 4, DY><<<g2, 256, 0, s>>>(x, mean, rstd, scale, dy, g_io, g_bf16, dscale, dbias, M, d,
-                                              accumulate, partials, rms);
+    if (gsum != nullptr && partials != nullptr) {
+      gsum_fused = true;
+      ln_bwd2_kernel<256, 4, DY, true><<<g2, 256, 0, s>>>(x, mean, rstd, scale, dy, g_io, g_bf16, dscale, dbias, M, d,
+                                                          accumulate, partials, rms);
+    } else {
+      ln_bwd2_kernel<256, 4, DY, false><<<g2, 256, 0, s>>>(x, mean, rstd, scale, dy, g_io, g_bf16, dscale, dbias, M, d,
+                                                           accumulate, partials, rms);
+    }
   } else if (d % 4 == 0 && d <= 12288) {
     ln_bwd_kernel<512, 6, DY><<<g, 512, 0, s>>>(x, mean, rstd, scale, dy, g_io, g_bf16, dscale, dbias, M, d, accumulate,
                                             partials, rms);
@@ -1028,21 +1057,26 @@ static void layernorm_bwd_t(const float* x, const float* mean, const float* rstd
     return;
   }
   if (partials != nullptr) {
-    ln_param_reduce_kernel<<<static_cast<unsigned>((2 * d + 31) / 32), 256, 0, s>>>(partials, static_cast<int>(nblk), d,
-                                                                                   dscale, dbias);
+    const int nsec = gsum_fused ? 3 : 2;
+    ln_param_reduce_kernel<<<static_cast<unsigned>((nsec * d + 31) / 32), 256, 0, s>>>(
+        partials, static_cast<int>(nblk), d, dscale, dbias, nsec, gsum_fused ? gsum : nullptr);
+  }
+  if (gsum != nullptr && !gsum_fused) {
+    if (partials == nullptr) throw std::runtime_error("layernorm_bwd: column sums need the partials scratch");
+    colsum_f32(g_io, d, M, d, gsum, 1, partials, s);
   }
 }
 
 void layernorm_bwd(const float* x, const float* mean, const float* rstd, const float* scale, const float* dy,
                    float* g_io, bf16* g_bf16, float* dscale, float* dbias, int64_t M, int d, int accumulate,
-                   cudaStream_t s, float* partials, int rms) {
-  layernorm_bwd_t(x, mean, rstd, scale, dy, g_io, g_bf16, dscale, dbias, M, d, accumulate, s, partials, rms);
+                   cudaStream_t s, float* partials, int rms, float* gsum) {
+  layernorm_bwd_t(x, mean, rstd, scale, dy, g_io, g_bf16, dscale, dbias, M, d, accumulate, s, partials, rms, gsum);
 }
 
 void layernorm_bwd(const float* x, const float* mean, const float* rstd, const float* scale, const bf16* dy,
                    float* g_io, bf16* g_bf16, float* dscale, float* dbias, int64_t M, int d, int accumulate,
-                   cudaStream_t s, float* partials, int rms) {
-  layernorm_bwd_t(x, mean, rstd, scale, dy, g_io, g_bf16, dscale, dbias, M, d, accumulate, s, partials, rms);
+                   cudaStream_t s, float* partials, int rms, float* gsum) {
+  layernorm_bwd_t(x, mean, rstd, scale, dy, g_io, g_bf16, dscale, dbias, M, d, accumulate, s, partials, rms, gsum);
 }
 
 void colsum_bf16(const bf16* X, int64_t ld, int64_t M, int N, int seg, float* out0, float* out1,

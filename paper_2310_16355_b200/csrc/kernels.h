@@ -38,11 +38,13 @@ void layernorm_fwd(const float* x, const float* scale, const float* bias, bf16* 
 // column partials and one fixed-order pass adds them (deterministic); partials == nullptr: atomics.
 void layernorm_bwd(const float* x, const float* mean, const float* rstd, const float* scale,
                    const float* dy, float* g_io, bf16* g_bf16, float* dscale, float* dbias,
-                   int64_t M, int d, int accumulate, cudaStream_t s, float* partials = nullptr, int rms = 0);
+                   int64_t M, int d, int accumulate, cudaStream_t s, float* partials = nullptr, int rms = 0,
+                   float* gsum = nullptr);  // gsum: += column sums of the written g_io
 // Same, with the residual-stream gradient dy in bf16 (after a bf16 all-reduce).
 void layernorm_bwd(const float* x, const float* mean, const float* rstd, const float* scale,
                    const bf16* dy, float* g_io, bf16* g_bf16, float* dscale, float* dbias,
-                   int64_t M, int d, int accumulate, cudaStream_t s, float* partials = nullptr, int rms = 0);
+                   int64_t M, int d, int accumulate, cudaStream_t s, float* partials = nullptr, int rms = 0,
+                   float* gsum = nullptr);  // gsum: += column sums of the written g_io
 int64_t layernorm_bwd_partials(int d);
 
 // Column sums of X [M, N] (bf16 or f32, row pitch ld) written (accumulate=0) or added into

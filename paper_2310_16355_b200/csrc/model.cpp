@@ -910,6 +910,8 @@ void Model::backward_replica(std::vector<Rank*>& grp, bool accumulate) {
         zero(ls.ln1_b);
         zero(ls.ln2_s);
         zero(ls.ln2_b);
+        zero(ls.o_b);    // o / fc2 bias gradients: column sums fused into the LayerNorm backward
+        zero(ls.fc2_b);  // that consumes the same residual gradient (added per row chunk)
       }
       zero(lnf_s_);
       zero(lnf_b_);
@@ -933,7 +935,7 @@ void Model::backward_replica(std::vector<Rank*>& grp, bool accumulate) {
       tic();
       k::layernorm_bwd(R.hs[L_] + r0 * d, R.statsf + r0, R.statsf + M + r0, P(R, lnf_s_), R.dx + r0 * d,
                        R.gres + r0 * d, R.gb + r0 * d, G(R, lnf_s_), Gn(R, lnf_b_), rows, d, 0, stream_, R.ln_partials,
-                       spec_.rmsnorm);
+                       spec_.rmsnorm, Gn(R, layers_[L_ - 1].fc2_b));
       toc(kProfNorm, 18.0 * rows * d);
       ++launches_;
     };
@@ -944,11 +946,11 @@ void Model::backward_replica(std::vector<Rank*>& grp, bool accumulate) {
                if (b16 != nullptr)
                  k::layernorm_bwd(R.hs[L_] + r0 * d, R.statsf + r0, R.statsf + M + r0, P(R, lnf_s_), b16,
                                   R.gres + r0 * d, R.gb + r0 * d, G(R, lnf_s_), Gn(R, lnf_b_), rows, d, 0, stream_,
-                                  R.ln_partials, spec_.rmsnorm);
+                                  R.ln_partials, spec_.rmsnorm, Gn(R, layers_[L_ - 1].fc2_b));
                else
                  k::layernorm_bwd(R.hs[L_] + r0 * d, R.statsf + r0, R.statsf + M + r0, P(R, lnf_s_), f32,
                                   R.gres + r0 * d, R.gb + r0 * d, G(R, lnf_s_), Gn(R, lnf_b_), rows, d, 0, stream_,
-                                  R.ln_partials, spec_.rmsnorm);
+                                  R.ln_partials, spec_.rmsnorm, Gn(R, layers_[L_ - 1].fc2_b));
                toc(kProfNorm, 18.0 * rows * d);
                ++launches_;
              });
@@ -968,10 +970,6 @@ void Model::backward_replica(std::vector<Rank*>& grp, bool accumulate) {
     const int fw = spec_.swiglu ? 2 * fl : fl;
     const int fk = spec_.swiglu ? ls.gate_k : ls.fc1_k;
     for (Rank* R : grp) {
-      if (ls.fc2_b >= 0) {
-        k::colsum_f32(R->gres, d, M, d, G(*R, ls.fc2_b), acc, R->col_scratch, stream_);
-        launches_ += 2;
-      }
       if (spec_.swiglu) {
         gemm(*R, static_cast<int>(M), fl, d, R->gb, d, 0, W(*R, ls.fc2_k), fl, 1,
              static_cast<int>(Epi::kSwiGLUBwd), R->dpre, 2 * fl, nullptr, 0, nullptr, R->pre[l], 2 * fl, 0, 0, 0,
@@ -996,7 +994,7 @@ void Model::backward_replica(std::vector<Rank*>& grp, bool accumulate) {
         tic();
         k::layernorm_bwd(R.hmid[l] + r0 * d, R.stats2[l] + r0, R.stats2[l] + M + r0, P(R, ls.ln2_s), R.dx + r0 * d,
                          R.gres + r0 * d, R.gb + r0 * d, G(R, ls.ln2_s), Gn(R, ls.ln2_b), rows, d, 1, stream_,
-                         R.ln_partials, spec_.rmsnorm);
+                         R.ln_partials, spec_.rmsnorm, G(R, ls.o_b));
         toc(kProfNorm, 18.0 * rows * d);
         ++launches_;
       };
@@ -1007,11 +1005,11 @@ void Model::backward_replica(std::vector<Rank*>& grp, bool accumulate) {
                  if (b16 != nullptr)
                    k::layernorm_bwd(R.hmid[l] + r0 * d, R.stats2[l] + r0, R.stats2[l] + M + r0, P(R, ls.ln2_s), b16,
                                     R.gres + r0 * d, R.gb + r0 * d, G(R, ls.ln2_s), Gn(R, ls.ln2_b), rows, d, 1,
-                                    stream_, R.ln_partials, spec_.rmsnorm);
+                                    stream_, R.ln_partials, spec_.rmsnorm, G(R, ls.o_b));
                  else
                    k::layernorm_bwd(R.hmid[l] + r0 * d, R.stats2[l] + r0, R.stats2[l] + M + r0, P(R, ls.ln2_s), f32,
                                     R.gres + r0 * d, R.gb + r0 * d, G(R, ls.ln2_s), Gn(R, ls.ln2_b), rows, d, 1,
-                                    stream_, R.ln_partials, spec_.rmsnorm);
+                                    stream_, R.ln_partials, spec_.rmsnorm, G(R, ls.o_b));
                  toc(kProfNorm, 18.0 * rows * d);
                  ++launches_;
                });
@@ -1023,8 +1021,6 @@ void Model::backward_replica(std::vector<Rank*>& grp, bool accumulate) {
     for (Rank* R : grp) wgrad(*R, fk, fw, d, static_cast<int>(M), R->dpre, fw, R->a2[l], d, acc);
     // ---- attention ----
     for (Rank* R : grp) {
-      k::colsum_f32(R->gres, d, M, d, G(*R, ls.o_b), acc, R->col_scratch, stream_);
-      launches_ += 2;
       gemm(*R, static_cast<int>(M), dl, d, R->gb, d, 0, W(*R, ls.o_k), dl, 1,
            static_cast<int>(Epi::kStoreBf16), R->dout, dl);
       wgrad(*R, ls.o_k, d, dl, static_cast<int>(M), R->gb, d, R->o[l], dl, acc);
@@ -1046,7 +1042,7 @@ void Model::backward_replica(std::vector<Rank*>& grp, bool accumulate) {
         tic();
         k::layernorm_bwd(R.hs[l] + r0 * d, R.stats1[l] + r0, R.stats1[l] + M + r0, P(R, ls.ln1_s), R.dx + r0 * d,
                          R.gres + r0 * d, R.gb + r0 * d, G(R, ls.ln1_s), Gn(R, ls.ln1_b), rows, d, 1, stream_,
-                         R.ln_partials, spec_.rmsnorm);
+                         R.ln_partials, spec_.rmsnorm, (l > 0 ? Gn(R, layers_[l - 1].fc2_b) : nullptr));
         toc(kProfNorm, 18.0 * rows * d);
         ++launches_;
       };
@@ -1057,11 +1053,11 @@ void Model::backward_replica(std::vector<Rank*>& grp, bool accumulate) {
                  if (b16 != nullptr)
                    k::layernorm_bwd(R.hs[l] + r0 * d, R.stats1[l] + r0, R.stats1[l] + M + r0, P(R, ls.ln1_s), b16,
                                     R.gres + r0 * d, R.gb + r0 * d, G(R, ls.ln1_s), Gn(R, ls.ln1_b), rows, d, 1,
-                                    stream_, R.ln_partials, spec_.rmsnorm);
+                                    stream_, R.ln_partials, spec_.rmsnorm, (l > 0 ? Gn(R, layers_[l - 1].fc2_b) : nullptr));
                  else
                    k::layernorm_bwd(R.hs[l] + r0 * d, R.stats1[l] + r0, R.stats1[l] + M + r0, P(R, ls.ln1_s), f32,
                                     R.gres + r0 * d, R.gb + r0 * d, G(R, ls.ln1_s), Gn(R, ls.ln1_b), rows, d, 1,
-                                    stream_, R.ln_partials, spec_.rmsnorm);
+                                    stream_, R.ln_partials, spec_.rmsnorm, (l > 0 ? Gn(R, layers_[l - 1].fc2_b) : nullptr));
                  toc(kProfNorm, 18.0 * rows * d);
                  ++launches_;
                });
