@@ -368,3 +368,35 @@ def test_llama7b_width_tp8_matches_tp1(spec_name, ar_bf16, monkeypatch):
     assert abs(res[8][0] - res[1][0]) / res[1][0] < 2e-4, (res[8][0], res[1][0])
     for n in res[1][1]:
         assert rel_l2(res[8][1][n].astype(np.float64), res[1][1][n].astype(np.float64)) < 1e-2, n
+
+
+def test_gptj_width_dp2_tp4_matches_single_device():
+    """BASELINE cfg3's mesh (2-way data x 4-way tensor) at GPT-J-6B width (head dim 256: the
+    CUDA-core attention path), depth 2 and 4 x 128 tokens, emulated: the dp x mp step with its
+    dp gradient all-reduce and sharded AdamW equals the single-device step."""
+    text = open(os.path.join(SPECS, "gptj6b.spec")).read()
+    text = "\n".join("n_layers = 2" if ln.startswith("n_layers") else ln for ln in text.splitlines()) + "\n"
+    spec = rules.parse_model_spec(text)
+    rng = np.random.default_rng(5)
+    tokens = rng.integers(0, spec.vocab_size, (4, 128), dtype=np.int32)
+    targets = rng.integers(0, spec.vocab_size, (4, 128), dtype=np.int32)
+    names = ("block_0/attn/q/kernel", "block_1/mlp/fc2/kernel", "block_0/attn/o/bias", "lm_head/kernel")
+    res = {}
+    cfg = engine.AdamWConfig(lr=1e-3, weight_decay=0.01)
+    for dp, mp in ((1, 1), (2, 4)):
+        model, mesh, plan = make(spec, dp, mp, 4 // dp, 128)
+        model.init_params(42, "model-init")
+        model.stage_batch(tokens, targets, None)
+        model.forward_backward()
+        model.dp_sync()
+        grads = {n: model.get_grad(n) for n in names}
+        model.adamw_step(cfg)
+        res[(dp, mp)] = (model.loss(), grads, {n: model.get_param(n) for n in names})
+        model.close()
+        mesh.close()
+    a, b = res[(1, 1)], res[(2, 4)]
+    assert abs(b[0] - a[0]) / a[0] < 2e-4, (b[0], a[0])
+    for n in names:
+        assert rel_l2(b[1][n].astype(np.float64), a[1][n].astype(np.float64)) < 1e-2, n
+        # one AdamW step (~lr * sign(g)) from identical weights
+        assert np.max(np.abs(b[2][n] - a[2][n])) <= 2.5e-3, n
