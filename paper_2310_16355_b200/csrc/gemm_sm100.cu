@@ -36,6 +36,9 @@ constexpr int NUM_THREADS = 256;
 #ifndef SW_EXP_NO_SHADOW_STORE
 #define SW_EXP_NO_SHADOW_STORE 0
 #endif
+#ifndef SW_EPI_WG2
+#define SW_EPI_WG2 0
+#endif
 #ifndef SW_EPI_PF
 #define SW_EPI_PF 0  // epilogue: 0 = load-wait-process per chunk (measured best), 2 = next chunk TMEM load in flight
 #endif
@@ -144,6 +147,38 @@ __device__ __forceinline__ void adamw_chunk(const GemmParams& p, float4* stage, 
     }
   }
   if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(p.adam_flag, 1);
+}
+
+// alpha * acc + bias for one 32-column chunk (the TMA-store epilogue's values)
+__device__ __forceinline__ void epilogue_values(const GemmParams& p, int col0, int ncols, const uint32_t (&r)[32],
+                                                float (&v)[32]) {
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]) * p.alpha;
+  if (p.bias != nullptr) {
+    if (p.bias_seg == 0) {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        if (i < ncols) v[i] += __ldg(p.bias + col0 + i);
+      }
+    } else {
+      const int sg = col0 / p.bias_seg;
+      const int in_seg = col0 - sg * p.bias_seg;
+      if (in_seg + 32 <= p.bias_seg) {  // the chunk lies in one segment: one division per chunk
+        const float* bp = p.bias + sg * p.bias_seg_stride + in_seg;
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          if (i < ncols) v[i] += __ldg(bp + i);
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const int c = col0 + i;
+          const int s2 = c / p.bias_seg;
+          if (i < ncols) v[i] += __ldg(p.bias + s2 * p.bias_seg_stride + (c - s2 * p.bias_seg));
+        }
+      }
+    }
+  }
 }
 
 template <Epi EPI>
@@ -478,9 +513,23 @@ constexpr int OPT_WBOX = 32 * OC * 4;     // one warp's 32-row box of one array
 #endif
 constexpr int OPT_SMEM = SW_ADAMW_DIRECT ? 8 * 32 * 32 * 4 : OPT_NBUF * OPT_BUF;
 // The AdamW epilogue runs two epilogue warpgroups (warps 4-7 and 8-11) on alternate chunks.
+// SW_EPI_TMA: plain-store epilogues (kStoreF32 without accumulate, kStoreBf16) stage each warp's
+// 32x32 chunk in shared memory (double-buffered, row-swizzled) and write it with one TMA store
+// instead of 8 (4) per-lane 16-byte stores that each touch 32 rows.
+#ifndef SW_EPI_TMA
+#define SW_EPI_TMA 1
+#endif
+template <Epi EPI>
+constexpr bool tma_epi() {
+  return SW_EPI_TMA && (EPI == Epi::kStoreF32 || EPI == Epi::kStoreBf16);
+}
+constexpr int EPI_TMA_BUF = 32 * 32 * 4;  // one warp's chunk (fp32 size; bf16 uses half)
 template <Epi EPI>
 constexpr int p_threads() {
-  return EPI == Epi::kAdamW ? 384 : NUM_THREADS;
+  // SW_EPI_WG2: two epilogue warpgroups (warps 4-7 and 8-11) on alternate 32-column chunks for
+  // every epilogue -- twice the warps hiding the TMEM-load / global-store latency of
+  // epilogue-bound (short-K) tiles
+  return EPI == Epi::kAdamW || SW_EPI_WG2 ? 384 : NUM_THREADS;
 }
 template <Epi EPI>
 constexpr int p_stages() {
@@ -491,13 +540,17 @@ constexpr int p_stages() {
 }
 template <Epi EPI>
 constexpr int p_smem_bytes() {
-  return p_stages<EPI>() * P_STAGE_BYTES + (EPI == Epi::kAdamW ? OPT_SMEM : 0) + 1024 + 256;
+  return p_stages<EPI>() * P_STAGE_BYTES + (EPI == Epi::kAdamW ? OPT_SMEM : 0) +
+         (tma_epi<EPI>() ? 4 * 2 * EPI_TMA_BUF : 0) + 1024 + 256;
 }
 
 // fp32 tensor maps over p, m, v ([M, ldc], box OC columns x 32 rows, swizzle span = one row).
 struct OptMaps {
   CUtensorMap p, m, v;
+  CUtensorMap c;  // the output, for the TMA-store epilogue (kStoreF32 / kStoreBf16)
 };
+
+
 
 // AdamW on one warp's 32 rows x OC columns with p/m/v resident in shared memory (TMA swizzled
 // rows: 16-byte chunk c of row r sits at chunk c ^ (r & 7) for 128-byte rows, c ^ ((r >> 1) & 3)
@@ -589,7 +642,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(p_threads<EPI>(), 1)
   uint8_t* sA = smem;
   uint8_t* sB = smem + P_STAGES * P_A_STAGE;
   uint8_t* sOpt = sB + P_STAGES * P_B_STAGE;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sOpt + (kOpt ? OPT_SMEM : 0));
+  uint64_t* full = reinterpret_cast<uint64_t*>(sOpt + (kOpt ? OPT_SMEM : 0) + (tma_epi<EPI>() ? 4 * 2 * EPI_TMA_BUF : 0));
   uint64_t* empty = full + P_STAGES;
   uint64_t* tfull = empty + P_STAGES;
   uint64_t* tempty = tfull + 2;
@@ -618,7 +671,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(p_threads<EPI>(), 1)
     }
     for (int a = 0; a < 2; ++a) {
       dev::mbar_init(&tfull[a], 1);
-      dev::mbar_init(&tempty[a], kOpt ? 16 : 8);  // epilogue warps of both CTAs
+      dev::mbar_init(&tempty[a], kOpt || SW_EPI_WG2 ? 16 : 8);  // epilogue warps of both CTAs
     }
     for (int a = 0; a < OPT_NBUF; ++a) {
       dev::mbar_init(&ofull[a], 1);
@@ -844,6 +897,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(p_threads<EPI>(), 1)
     }
   } else if (warp >= 4) {
     const uint32_t q = warp & 3;
+    // chunk stride and first chunk of this warp's warpgroup (one warpgroup: every chunk)
+    const int cstep = SW_EPI_WG2 ? 2 : 1, cfirst = SW_EPI_WG2 ? (static_cast<int>(warp) - 4) >> 2 : 0;
     const uint32_t tempty_leader = dev::mapa_shared(dev::smem_u32(&tempty[0]), 0);
     int acc = 0;
     uint32_t acc_phase = 0;
@@ -861,7 +916,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(p_threads<EPI>(), 1)
         // accumulator columns [0,128) = gate, [128,256) = up for h columns nb*128 + [0,128)
         const int h_left = p.N - nb * 128;
 #pragma unroll 1
-        for (int j = 0; j < 4; ++j) {
+        for (int j = cfirst; j < 4; j += cstep) {
           const int ncols = min(32, h_left - j * 32);
           if (ncols <= 0) break;
           uint32_t rg[32], ru[32];
@@ -897,14 +952,63 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(p_threads<EPI>(), 1)
       }
 #pragma unroll 1
 #if SW_EPI_PF == 0
+      if constexpr (tma_epi<EPI>()) {
+        if (!p.accumulate) {
+          // stage in shared memory (lane = row of the warp's 32, swizzled 16-byte units), one TMA
+          // store per chunk; a buffer is rewritten only after its previous store read it
+          uint8_t* stg = sOpt + (static_cast<int>(warp) - 4) * 2 * EPI_TMA_BUF;
+          constexpr bool f32 = EPI == Epi::kStoreF32;
 #pragma unroll 1
-      for (int j = 0; j < (kGlu ? 0 : BN / 32); ++j) {
+          for (int j = 0; j < BN / 32; ++j) {
+            if (j * 32 >= n_left) break;
+            uint32_t r[32];
+            dev::tmem_ld_32x32b_x32(tmem_base + ((q * 32) << 16) + acc * BN + j * 32, r);
+            dev::tmem_ld_wait();
+            float v[32];
+            epilogue_values(p, nb * BN + j * 32, min(32, n_left - j * 32), r, v);
+            if (lane == 0) dev::bulk_wait_read_1();  // buffer (j & 1) was read by the store two chunks back
+            __syncwarp();
+            uint8_t* buf = stg + (j & 1) * EPI_TMA_BUF + lane * (f32 ? 128 : 64);
+            if constexpr (f32) {
+#pragma unroll
+              for (int u = 0; u < 8; ++u)
+                *reinterpret_cast<float4*>(buf + ((u ^ (lane & 7)) << 4)) =
+                    make_float4(v[4 * u], v[4 * u + 1], v[4 * u + 2], v[4 * u + 3]);
+            } else {
+#pragma unroll
+              for (int u = 0; u < 4; ++u)
+                *reinterpret_cast<uint4*>(buf + ((u ^ ((lane >> 1) & 3)) << 4)) =
+                    make_uint4(dev::pack_bf16x2(v[8 * u], v[8 * u + 1]), dev::pack_bf16x2(v[8 * u + 2], v[8 * u + 3]),
+                               dev::pack_bf16x2(v[8 * u + 4], v[8 * u + 5]), dev::pack_bf16x2(v[8 * u + 6], v[8 * u + 7]));
+            }
+            dev::fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              dev::tma_store_2d(&om.c, stg + (j & 1) * EPI_TMA_BUF, nb * BN + j * 32, row - static_cast<int>(lane));
+              dev::bulk_commit();
+            }
+          }
+        } else {
+#pragma unroll 1
+          for (int j = 0; j < BN / 32; ++j) {
+            const int ncols = min(32, n_left - j * 32);
+            if (ncols <= 0) break;
+            uint32_t r[32];
+            dev::tmem_ld_32x32b_x32(tmem_base + ((q * 32) << 16) + acc * BN + j * 32, r);
+            dev::tmem_ld_wait();
+            if (row < p.M) epilogue_chunk<EPI>(p, row, nb * BN + j * 32, ncols, r);
+          }
+        }
+      } else {
+#pragma unroll 1
+      for (int j = cfirst; j < (kGlu ? 0 : BN / 32); j += cstep) {
         const int ncols = min(32, n_left - j * 32);
         if (ncols <= 0) break;
         uint32_t r[32];
         dev::tmem_ld_32x32b_x32(tmem_base + ((q * 32) << 16) + acc * BN + j * 32, r);
         dev::tmem_ld_wait();
         if (row < p.M) epilogue_chunk<EPI>(p, row, nb * BN + j * 32, ncols, r);
+      }
       }
 #else
       if constexpr (!kGlu) {
@@ -938,7 +1042,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(p_threads<EPI>(), 1)
     }
   }
 
-  if constexpr (kOpt && !SW_ADAMW_DIRECT) {
+  if constexpr ((kOpt && !SW_ADAMW_DIRECT) || tma_epi<EPI>()) {
     if (warp >= 4 && lane == 0) dev::bulk_wait_all();
   }
   dev::tc_fence_before();
@@ -968,6 +1072,12 @@ cudaError_t launch_2sm(const GemmParams& p, cudaStream_t stream) {
   const int sms = (p.num_sms > 0 ? p.num_sms : device_sm_count()) & ~1;
   const int grid = 2 * num_tiles < sms ? 2 * num_tiles : sms;
   OptMaps om{};
+  if constexpr (tma_epi<EPI>()) {
+    if (!p.accumulate) {
+      om.c = EPI == Epi::kStoreF32 ? make_tmap_f32_2d(p.C, p.N, p.M, p.ldc, 32, 32)
+                                   : make_tmap_bf16_2d_rowswz(p.C, p.N, p.M, p.ldc, 32, 32);
+    }
+  }
   if constexpr (EPI == Epi::kAdamW) {
     om.p = make_tmap_f32_2d(p.adam_p, p.N, p.M, p.ldc, OC, 32);
     om.m = make_tmap_f32_2d(p.adam_m, p.N, p.M, p.ldc, OC, 32);

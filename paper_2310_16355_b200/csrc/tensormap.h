@@ -22,6 +22,10 @@ CUtensorMap make_tmap_bf16_3d(const void* ptr, uint64_t inner, uint64_t mid, uin
 CUtensorMap make_tmap_f32_2d(const void* ptr, uint64_t inner, uint64_t outer, uint64_t ld, uint32_t box_inner,
                              uint32_t box_outer);
 
+// 2-D bf16 tensor map whose swizzle span equals the box row (box_inner * 2 = 128 / 64 / 32 B).
+CUtensorMap make_tmap_bf16_2d_rowswz(const void* ptr, uint64_t inner, uint64_t outer, uint64_t ld,
+                                     uint32_t box_inner, uint32_t box_outer);
+
 int device_sm_count();
 
 }  // namespace sw

@@ -1,8 +1,4 @@
-timeout 900 python -m pytest tests -m gpu -q > gpurun_out/t.log 2>&1; echo EXIT $? >> gpurun_out/t.log
-timeout 600 python bench.py > gpurun_out/r1d_bench.log 2>&1
-timeout 300 python bench.py --impl reference > gpurun_out/r1d_bench_ref.log 2>&1
-rm -f gpurun_out/prof.csv; SW_PROFILE_LOG=gpurun_out/prof.csv timeout 400 python bench.py --no-cpu-baseline --steps 5 > gpurun_out/r1d_run.log 2>&1
-python tools/gemm_shape_report.py gpurun_out/prof.csv 2 > gpurun_out/r1d_gemm_shapes.log
-python tools/profile_step.py > gpurun_out/plain.log 2>&1 && \
-ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r1d_launches.csv python tools/profile_step.py > gpurun_out/ncu1.log 2>&1
-echo done
+for i in 1 2; do for lib in paper_2310_16355_b200/libshardweave_b200.so variants/libsw_tma.so; do
+SW_LIB_PATH=$lib timeout 400 python bench.py --no-cpu-baseline --steps 8 > gpurun_out/b.log 2>&1
+echo "$lib $(python3 -c "import json; d=json.loads(open('gpurun_out/b.log').read().strip().splitlines()[-1]); print(round(d['value']), round(d['ms_per_step'],2), d['clocks']['sm_mhz'], d['breakdown_ms_per_step']['gemm'])")"
+done; done > gpurun_out/tma_ab.log 2>&1
