@@ -521,7 +521,7 @@ constexpr int OPT_SMEM = SW_ADAMW_DIRECT ? 8 * 32 * 32 * 4 : OPT_NBUF * OPT_BUF;
 #endif
 template <Epi EPI>
 constexpr bool tma_epi() {
-  return SW_EPI_TMA && (EPI == Epi::kStoreF32 || EPI == Epi::kStoreBf16);
+  return SW_EPI_TMA && (EPI == Epi::kStoreF32 || EPI == Epi::kStoreBf16 || EPI == Epi::kResidF32);
 }
 constexpr int EPI_TMA_BUF = 32 * 32 * 4;  // one warp's chunk (fp32 size; bf16 uses half)
 template <Epi EPI>
@@ -547,7 +547,8 @@ constexpr int p_smem_bytes() {
 // fp32 tensor maps over p, m, v ([M, ldc], box OC columns x 32 rows, swizzle span = one row).
 struct OptMaps {
   CUtensorMap p, m, v;
-  CUtensorMap c;  // the output, for the TMA-store epilogue (kStoreF32 / kStoreBf16)
+  CUtensorMap c;  // the output, for the TMA-store epilogue (kStoreF32 / kStoreBf16 / kResidF32)
+  CUtensorMap a;  // kResidF32: the residual addend (TMA-loaded into the staging buffer)
 };
 
 
@@ -648,7 +649,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(p_threads<EPI>(), 1)
   uint64_t* tempty = tfull + 2;
   uint64_t* ofull = tempty + 2;
   uint64_t* oempty = ofull + 3;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(oempty + 3);
+  uint64_t* eload = oempty + 3;  // [4 warps][2 buffers] residual-chunk loads (TMA epilogue)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(eload + 8);
 
   const uint32_t warp = dev::warp_idx_sync();
   const uint32_t lane = threadIdx.x & 31;
@@ -673,6 +675,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(p_threads<EPI>(), 1)
       dev::mbar_init(&tfull[a], 1);
       dev::mbar_init(&tempty[a], kOpt || SW_EPI_WG2 ? 16 : 8);  // epilogue warps of both CTAs
     }
+    for (int a = 0; a < 8; ++a) dev::mbar_init(&eload[a], 1);
     for (int a = 0; a < OPT_NBUF; ++a) {
       dev::mbar_init(&ofull[a], 1);
       dev::mbar_init(&oempty[a], 4);
@@ -899,6 +902,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(p_threads<EPI>(), 1)
     const uint32_t q = warp & 3;
     // chunk stride and first chunk of this warp's warpgroup (one warpgroup: every chunk)
     const int cstep = SW_EPI_WG2 ? 2 : 1, cfirst = SW_EPI_WG2 ? (static_cast<int>(warp) - 4) >> 2 : 0;
+    uint32_t rphase[2] = {0u, 0u};  // TMA residual-load barrier phases of the two staging buffers
+    (void)rphase;
     const uint32_t tempty_leader = dev::mapa_shared(dev::smem_u32(&tempty[0]), 0);
     int acc = 0;
     uint32_t acc_phase = 0;
@@ -957,19 +962,36 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(p_threads<EPI>(), 1)
           // stage in shared memory (lane = row of the warp's 32, swizzled 16-byte units), one TMA
           // store per chunk; a buffer is rewritten only after its previous store read it
           uint8_t* stg = sOpt + (static_cast<int>(warp) - 4) * 2 * EPI_TMA_BUF;
-          constexpr bool f32 = EPI == Epi::kStoreF32;
+          constexpr bool f32 = EPI != Epi::kStoreBf16;
+          constexpr bool resid = EPI == Epi::kResidF32;
 #pragma unroll 1
           for (int j = 0; j < BN / 32; ++j) {
             if (j * 32 >= n_left) break;
+            uint64_t* ebar = &eload[(static_cast<int>(warp) - 4) * 2 + (j & 1)];
+            if (lane == 0) {
+              dev::bulk_wait_read_1();  // buffer (j & 1) was read by the store two chunks back
+              if constexpr (resid) {    // the residual chunk lands while the accumulator is read
+                dev::mbar_arrive_expect_tx(ebar, EPI_TMA_BUF);
+                dev::tma_load_2d(stg + (j & 1) * EPI_TMA_BUF, &om.a, ebar, nb * BN + j * 32, row - static_cast<int>(lane));
+              }
+            }
             uint32_t r[32];
             dev::tmem_ld_32x32b_x32(tmem_base + ((q * 32) << 16) + acc * BN + j * 32, r);
             dev::tmem_ld_wait();
             float v[32];
             epilogue_values(p, nb * BN + j * 32, min(32, n_left - j * 32), r, v);
-            if (lane == 0) dev::bulk_wait_read_1();  // buffer (j & 1) was read by the store two chunks back
             __syncwarp();
             uint8_t* buf = stg + (j & 1) * EPI_TMA_BUF + lane * (f32 ? 128 : 64);
-            if constexpr (f32) {
+            if constexpr (resid) {
+              dev::mbar_wait(ebar, rphase[j & 1]);
+              rphase[j & 1] ^= 1u;
+#pragma unroll
+              for (int u = 0; u < 8; ++u) {
+                float4* pa = reinterpret_cast<float4*>(buf + ((u ^ (lane & 7)) << 4));
+                const float4 a = *pa;
+                *pa = make_float4(v[4 * u] + a.x, v[4 * u + 1] + a.y, v[4 * u + 2] + a.z, v[4 * u + 3] + a.w);
+              }
+            } else if constexpr (f32) {
 #pragma unroll
               for (int u = 0; u < 8; ++u)
                 *reinterpret_cast<float4*>(buf + ((u ^ (lane & 7)) << 4)) =
@@ -1074,8 +1096,9 @@ cudaError_t launch_2sm(const GemmParams& p, cudaStream_t stream) {
   OptMaps om{};
   if constexpr (tma_epi<EPI>()) {
     if (!p.accumulate) {
-      om.c = EPI == Epi::kStoreF32 ? make_tmap_f32_2d(p.C, p.N, p.M, p.ldc, 32, 32)
-                                   : make_tmap_bf16_2d_rowswz(p.C, p.N, p.M, p.ldc, 32, 32);
+      om.c = EPI != Epi::kStoreBf16 ? make_tmap_f32_2d(p.C, p.N, p.M, p.ldc, 32, 32)
+                                    : make_tmap_bf16_2d_rowswz(p.C, p.N, p.M, p.ldc, 32, 32);
+      if constexpr (EPI == Epi::kResidF32) om.a = make_tmap_f32_2d(p.aux, p.N, p.M, p.ld_aux, 32, 32);
     }
   }
   if constexpr (EPI == Epi::kAdamW) {
