@@ -28,7 +28,19 @@ def main(kind, M=12288, N=4096, K=8192):
     A2 = torch.randn(M, K, device="cuda").bfloat16()
     B2 = torch.randn(N, K, device="cuda").bfloat16()
     for _ in range(3):
-        if kind == "swiglu":  # fused gate|up forward: N = h columns, B = [gate; up] [2N, K]
+        if kind in ("gelu", "gelubwd"):  # fc1 forward (pre + act) / fc2 dgrad with the GeLU derivative
+            Cb = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+            C2 = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+            pre = torch.randn(M, N, device="cuda").bfloat16()
+            bias = torch.randn(N, device="cuda")
+            if kind == "gelu":
+                _lib.check(L.sw_k_gemm_bf16(M, N, K, A2.data_ptr(), K, 0, B2.data_ptr(), K, 0, 2, Cb.data_ptr(), N,
+                                            C2.data_ptr(), N, bias.data_ptr(), None, 0, 1.0, 0, s))
+            else:
+                B3 = torch.randn(K, N, device="cuda").bfloat16()
+                _lib.check(L.sw_k_gemm_bf16(M, N, K, A2.data_ptr(), K, 0, B3.data_ptr(), N, 1, 4, Cb.data_ptr(), N,
+                                            None, 0, None, pre.data_ptr(), N, 1.0, 0, s))
+        elif kind == "swiglu":  # fused gate|up forward: N = h columns, B = [gate; up] [2N, K]
             Wgu = torch.randn(2 * N, K, device="cuda").bfloat16()
             Hh = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
             PRE = torch.empty(M, 2 * N, device="cuda", dtype=torch.bfloat16)
