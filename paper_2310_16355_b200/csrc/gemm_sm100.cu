@@ -521,7 +521,8 @@ constexpr int OPT_SMEM = SW_ADAMW_DIRECT ? 8 * 32 * 32 * 4 : OPT_NBUF * OPT_BUF;
 #endif
 template <Epi EPI>
 constexpr bool tma_epi() {
-  return SW_EPI_TMA && (EPI == Epi::kStoreF32 || EPI == Epi::kStoreBf16 || EPI == Epi::kResidF32);
+  return SW_EPI_TMA && (EPI == Epi::kStoreF32 || EPI == Epi::kStoreBf16 || EPI == Epi::kResidF32 ||
+                        EPI == Epi::kBiasGelu || EPI == Epi::kGeluBwd);
 }
 constexpr int EPI_TMA_BUF = 32 * 32 * 4;  // one warp's chunk (fp32 size; bf16 uses half)
 template <Epi EPI>
@@ -548,7 +549,8 @@ constexpr int p_smem_bytes() {
 struct OptMaps {
   CUtensorMap p, m, v;
   CUtensorMap c;  // the output, for the TMA-store epilogue (kStoreF32 / kStoreBf16 / kResidF32)
-  CUtensorMap a;  // kResidF32: the residual addend (TMA-loaded into the staging buffer)
+  CUtensorMap a;   // kResidF32: the residual addend; kGeluBwd: the bf16 pre-activations
+  CUtensorMap c2;  // kBiasGelu: the activation output
 };
 
 
@@ -962,16 +964,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(p_threads<EPI>(), 1)
           // stage in shared memory (lane = row of the warp's 32, swizzled 16-byte units), one TMA
           // store per chunk; a buffer is rewritten only after its previous store read it
           uint8_t* stg = sOpt + (static_cast<int>(warp) - 4) * 2 * EPI_TMA_BUF;
-          constexpr bool f32 = EPI != Epi::kStoreBf16;
-          constexpr bool resid = EPI == Epi::kResidF32;
+          constexpr bool f32 = EPI == Epi::kStoreF32 || EPI == Epi::kResidF32;
+          constexpr bool resid = EPI == Epi::kResidF32, gbwd = EPI == Epi::kGeluBwd, gfwd = EPI == Epi::kBiasGelu;
+          constexpr int chunk_bytes = f32 ? 4096 : 2048;
 #pragma unroll 1
           for (int j = 0; j < BN / 32; ++j) {
             if (j * 32 >= n_left) break;
             uint64_t* ebar = &eload[(static_cast<int>(warp) - 4) * 2 + (j & 1)];
             if (lane == 0) {
               dev::bulk_wait_read_1();  // buffer (j & 1) was read by the store two chunks back
-              if constexpr (resid) {    // the residual chunk lands while the accumulator is read
-                dev::mbar_arrive_expect_tx(ebar, EPI_TMA_BUF);
+              if constexpr (resid || gbwd) {  // the addend / pre-activation chunk lands while the accumulator is read
+                dev::mbar_arrive_expect_tx(ebar, chunk_bytes);
                 dev::tma_load_2d(stg + (j & 1) * EPI_TMA_BUF, &om.a, ebar, nb * BN + j * 32, row - static_cast<int>(lane));
               }
             }
@@ -991,6 +994,36 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(p_threads<EPI>(), 1)
                 const float4 a = *pa;
                 *pa = make_float4(v[4 * u] + a.x, v[4 * u + 1] + a.y, v[4 * u + 2] + a.z, v[4 * u + 3] + a.w);
               }
+            } else if constexpr (gbwd) {  // dpre = acc * gelu'(pre), in place over the loaded pre chunk
+              dev::mbar_wait(ebar, rphase[j & 1]);
+              rphase[j & 1] ^= 1u;
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                uint4* pa = reinterpret_cast<uint4*>(buf + ((u ^ ((lane >> 1) & 3)) << 4));
+                const uint4 raw = *pa;
+                const uint32_t w[4] = {raw.x, raw.y, raw.z, raw.w};
+                uint32_t o[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                  const float2 x = dev::unpack_bf16x2(w[e]);
+                  o[e] = dev::pack_bf16x2(v[8 * u + 2 * e] * dev::gelu_tanh_grad(x.x),
+                                          v[8 * u + 2 * e + 1] * dev::gelu_tanh_grad(x.y));
+                }
+                *pa = make_uint4(o[0], o[1], o[2], o[3]);
+              }
+            } else if constexpr (gfwd) {  // pre-activation in the first half, gelu in the second
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                const int sw = (u ^ ((lane >> 1) & 3)) << 4;
+                *reinterpret_cast<uint4*>(buf + sw) =
+                    make_uint4(dev::pack_bf16x2(v[8 * u], v[8 * u + 1]), dev::pack_bf16x2(v[8 * u + 2], v[8 * u + 3]),
+                               dev::pack_bf16x2(v[8 * u + 4], v[8 * u + 5]), dev::pack_bf16x2(v[8 * u + 6], v[8 * u + 7]));
+                *reinterpret_cast<uint4*>(buf + 2048 + sw) =
+                    make_uint4(dev::pack_bf16x2(dev::gelu_tanh(v[8 * u]), dev::gelu_tanh(v[8 * u + 1])),
+                               dev::pack_bf16x2(dev::gelu_tanh(v[8 * u + 2]), dev::gelu_tanh(v[8 * u + 3])),
+                               dev::pack_bf16x2(dev::gelu_tanh(v[8 * u + 4]), dev::gelu_tanh(v[8 * u + 5])),
+                               dev::pack_bf16x2(dev::gelu_tanh(v[8 * u + 6]), dev::gelu_tanh(v[8 * u + 7])));
+              }
             } else if constexpr (f32) {
 #pragma unroll
               for (int u = 0; u < 8; ++u)
@@ -1007,6 +1040,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(p_threads<EPI>(), 1)
             __syncwarp();
             if (lane == 0) {
               dev::tma_store_2d(&om.c, stg + (j & 1) * EPI_TMA_BUF, nb * BN + j * 32, row - static_cast<int>(lane));
+              if constexpr (gfwd)
+                dev::tma_store_2d(&om.c2, stg + (j & 1) * EPI_TMA_BUF + 2048, nb * BN + j * 32,
+                                  row - static_cast<int>(lane));
               dev::bulk_commit();
             }
           }
@@ -1096,9 +1132,12 @@ cudaError_t launch_2sm(const GemmParams& p, cudaStream_t stream) {
   OptMaps om{};
   if constexpr (tma_epi<EPI>()) {
     if (!p.accumulate) {
-      om.c = EPI != Epi::kStoreBf16 ? make_tmap_f32_2d(p.C, p.N, p.M, p.ldc, 32, 32)
-                                    : make_tmap_bf16_2d_rowswz(p.C, p.N, p.M, p.ldc, 32, 32);
+      constexpr bool f32 = EPI == Epi::kStoreF32 || EPI == Epi::kResidF32;
+      om.c = f32 ? make_tmap_f32_2d(p.C, p.N, p.M, p.ldc, 32, 32)
+                 : make_tmap_bf16_2d_rowswz(p.C, p.N, p.M, p.ldc, 32, 32);
       if constexpr (EPI == Epi::kResidF32) om.a = make_tmap_f32_2d(p.aux, p.N, p.M, p.ld_aux, 32, 32);
+      if constexpr (EPI == Epi::kGeluBwd) om.a = make_tmap_bf16_2d_rowswz(p.aux, p.N, p.M, p.ld_aux, 32, 32);
+      if constexpr (EPI == Epi::kBiasGelu) om.c2 = make_tmap_bf16_2d_rowswz(p.C2, p.N, p.M, p.ldc2, 32, 32);
     }
   }
   if constexpr (EPI == Epi::kAdamW) {
