@@ -302,7 +302,10 @@ SW_API void sw_checkpoint_free(sw_checkpoint* ck);
 
 /* C[M,N] = sum_k A[m,k] B[n,k] — bf16 in, fp32 accumulate (tcgen05). a_mn_major / b_mn_major
  * select the operand layouts; epi: 0 bf16, 1 f32 (+accumulate), 2 bias+gelu (C=pre, C2=act),
- * 3 residual f32 (C = aux + acc + bias), 4 gelu-backward (C = acc * gelu'(aux)). */
+ * 3 residual f32 (C = aux + acc + bias), 4 gelu-backward (C = acc * gelu'(aux)), 8 attention
+ * output gradient with the backward's row statistic: C = bf16(acc) and, with C2 = fp32 delta
+ * [M / ldc2][N / 128][ldc2] and ldc2 = sequence length, delta[b][h][t] = sum over the 128 columns
+ * of head h of C[b*ldc2 + t, c] * aux[b*ldc2 + t, c] (aux = bf16 attention output O). */
 SW_API sw_status sw_k_gemm_bf16(int M, int N, int K, const void* A, int64_t lda, int a_mn_major,
                          const void* B, int64_t ldb, int b_mn_major, int epi, void* C, int64_t ldc,
                          void* C2, int64_t ldc2, const float* bias, const void* aux,

@@ -17,7 +17,8 @@ namespace k {
 bool attention_mma_fwd(const bf16* qkv, bf16* o, float* lse, int B, int T, int Hl, int hd,
                        cudaStream_t s);
 bool attention_mma_bwd(const bf16* qkv, const bf16* o, const float* lse, const bf16* dout,
-                       bf16* dqkv, float* scratch, int B, int T, int Hl, int hd, cudaStream_t s);
+                       bf16* dqkv, float* scratch, int B, int T, int Hl, int hd, cudaStream_t s,
+                       bool delta_ready);
 bool attention_mma_fwd_ex(const bf16* qkv, bf16* o, float* lse, int B, int T, int Hl, int hd, int causal,
                           const float* lut, float scale, cudaStream_t s);
 bool attention_mma_bwd_ex(const bf16* qkv, const bf16* o, const float* lse, const bf16* dout, bf16* dqkv,
@@ -175,8 +176,8 @@ void attention_fwd(const bf16* qkv, bf16* o, float* lse, int B, int T, int Hl, i
 }
 
 void attention_bwd(const bf16* qkv, const bf16* o, const float* lse, const bf16* dout, bf16* dqkv,
-                   float* scratch, int B, int T, int Hl, int hd, cudaStream_t s) {
-  if (attention_mma_bwd(qkv, o, lse, dout, dqkv, scratch, B, T, Hl, hd, s)) return;
+                   float* scratch, int B, int T, int Hl, int hd, cudaStream_t s, bool delta_ready) {
+  if (attention_mma_bwd(qkv, o, lse, dout, dqkv, scratch, B, T, Hl, hd, s, delta_ready)) return;
   const int64_t M = static_cast<int64_t>(B) * T;
   const int Dl = Hl * hd;
   float* delta = scratch;

@@ -1440,7 +1440,7 @@ bool bwd2_enabled() {
 
 bool launch_bwd2(const bf16* qkv, const bf16* o, const float* lse, const bf16* dout, bf16* dqkv, float* scratch,
                  int B, int T, int Hl, cudaStream_t s, int causal = 1, const float* lut = nullptr,
-                 float* dlut = nullptr, float scale_arg = 0.f) {
+                 float* dlut = nullptr, float scale_arg = 0.f, bool delta_ready = false) {
   constexpr int HD = 128;
   static bool configured = false;
   if (!configured) {
@@ -1455,7 +1455,7 @@ bool launch_bwd2(const bf16* qkv, const bf16* o, const float* lse, const bf16* d
   float* delta = scratch;
   float* dq = scratch + ((M * Hl + 63) / 64) * 64;
   cudaMemsetAsync(dq, 0, sizeof(float) * M * Dl, s);
-  launch_delta(o, dout, delta, T, Hl, HD, M, s);
+  if (!delta_ready) launch_delta(o, dout, delta, T, Hl, HD, M, s);
   const CUtensorMap tm_qkv64 = make_tmap_bf16_2d(qkv, 3ull * Dl, static_cast<uint64_t>(M), 3ull * Dl, 64, BQ2);
   const CUtensorMap tm_qkv128 = make_tmap_bf16_2d(qkv, 3ull * Dl, static_cast<uint64_t>(M), 3ull * Dl, 64, 128);
   const CUtensorMap tm_do64 = make_tmap_bf16_2d(dout, static_cast<uint64_t>(Dl), static_cast<uint64_t>(M),
@@ -1474,8 +1474,9 @@ bool launch_bwd2(const bf16* qkv, const bf16* o, const float* lse, const bf16* d
 
 template <int HD>
 bool launch_bwd(const bf16* qkv, const bf16* o, const float* lse, const bf16* dout, bf16* dqkv, float* scratch,
-                int B, int T, int Hl, cudaStream_t s) {
-  if (HD == 128 && bwd2_enabled()) return launch_bwd2(qkv, o, lse, dout, dqkv, scratch, B, T, Hl, s);
+                int B, int T, int Hl, cudaStream_t s, bool delta_ready) {
+  if (HD == 128 && bwd2_enabled())
+    return launch_bwd2(qkv, o, lse, dout, dqkv, scratch, B, T, Hl, s, 1, nullptr, nullptr, 0.f, delta_ready);
   using Lay = BwdLayout<HD>;
   static bool configured = false;
   if (!configured) {
@@ -1490,7 +1491,7 @@ bool launch_bwd(const bf16* qkv, const bf16* o, const float* lse, const bf16* do
   float* delta = scratch;
   float* dq = scratch + ((M * Hl + 63) / 64) * 64;
   cudaMemsetAsync(dq, 0, sizeof(float) * M * Dl, s);
-  launch_delta(o, dout, delta, T, Hl, HD, M, s);
+  if (!delta_ready) launch_delta(o, dout, delta, T, Hl, HD, M, s);
   const CUtensorMap tm_qkv = make_tmap_bf16_2d(qkv, 3ull * Dl, static_cast<uint64_t>(M), 3ull * Dl, 64, 128);
   const CUtensorMap tm_do = make_tmap_bf16_2d(dout, static_cast<uint64_t>(Dl), static_cast<uint64_t>(M),
                                               static_cast<uint64_t>(Dl), 64, 128);
@@ -1533,10 +1534,10 @@ bool attention_mma_bwd_ex(const bf16* qkv, const bf16* o, const float* lse, cons
 }
 
 bool attention_mma_bwd(const bf16* qkv, const bf16* o, const float* lse, const bf16* dout, bf16* dqkv,
-                       float* scratch, int B, int T, int Hl, int hd, cudaStream_t s) {
+                       float* scratch, int B, int T, int Hl, int hd, cudaStream_t s, bool delta_ready) {
   if (((Hl * hd) % 8) != 0) return false;
-  if (hd == 128) return launch_bwd<128>(qkv, o, lse, dout, dqkv, scratch, B, T, Hl, s);
-  if (hd == 64) return launch_bwd<64>(qkv, o, lse, dout, dqkv, scratch, B, T, Hl, s);
+  if (hd == 128) return launch_bwd<128>(qkv, o, lse, dout, dqkv, scratch, B, T, Hl, s, delta_ready);
+  if (hd == 64) return launch_bwd<64>(qkv, o, lse, dout, dqkv, scratch, B, T, Hl, s, delta_ready);
   return false;
 }
 

@@ -29,7 +29,7 @@ sw_status sw_k_gemm_bf16(int M, int N, int K, const void* A, int64_t lda, int a_
                          void* C2, int64_t ldc2, const float* bias, const void* aux,
                          int64_t ld_aux, float alpha, int accumulate, void* stream) {
   return sw::guarded([&] {
-    if (epi < 0 || epi > 4) sw::fail(SW_ERR_CONFIG, "sw_k_gemm_bf16: unknown epilogue");
+    if ((epi < 0 || epi > 4) && epi != 8) sw::fail(SW_ERR_CONFIG, "sw_k_gemm_bf16: unknown epilogue");
     sw::GemmParams p;
     p.M = M;
     p.N = N;
@@ -50,6 +50,13 @@ sw_status sw_k_gemm_bf16(int M, int N, int K, const void* A, int64_t lda, int a_
     p.ld_aux = ld_aux;
     p.alpha = alpha;
     p.accumulate = accumulate;
+    if (p.epi == sw::Epi::kBf16Delta) {  // C2 carries the fp32 delta output, ldc2 the sequence length
+      p.delta = static_cast<float*>(C2);
+      p.delta_T = static_cast<int>(ldc2);
+      p.C2 = nullptr;
+      p.ldc2 = 0;
+      if (!sw::gemm_delta_ok(p)) sw::fail(SW_ERR_CONFIG, "sw_k_gemm_bf16: fused delta not available for this shape");
+    }
     sw::cuda_check(sw::gemm_bf16(p, static_cast<cudaStream_t>(stream)), "gemm_bf16 launch");
   });
 }

@@ -31,6 +31,11 @@ enum class Epi : int {
   // kSwiGLUBwd: acc = dh [M, N]; aux = g | u [M, 2N]; C [M, 2N] = dh*u*silu'(g) | dh*silu(g).
   kSwiGLU = 6,
   kSwiGLUBwd = 7,
+  // kBf16Delta: the attention-output gradient GEMM with the flash-attention backward's row
+  // statistic fused in: C(bf16) = alpha*acc and, per row r = b*delta_T + t and 128-column head h,
+  // delta[(b*(N/128) + h)*delta_T + t] = sum_c bf16(C[r, c]) * aux(bf16)[r, c] (aux = the forward
+  // attention output O). CTA-pair TMA-store path only (gemm_delta_ok).
+  kBf16Delta = 8,
 };
 
 struct GemmParams {
@@ -66,10 +71,16 @@ struct GemmParams {
   int adam_fast = 0;  // set by gemm_bf16: bias corrections in [2^-14, 1] admit the branch-free path
   int num_sms = 0;  // 0 = all
   int trace_cta = -1;  // profiling: CTA whose per-tile phases are stamped (SW_GEMM_TRACE_CTA)
+  float* delta = nullptr;  // kBf16Delta output [M / delta_T][N / 128][delta_T]
+  int delta_T = 0;
 };
 
 // Returns cudaSuccess or the launch error. Throws std::runtime_error on invalid shapes.
 cudaError_t gemm_bf16(const GemmParams& p, cudaStream_t stream);
+
+// Whether gemm_bf16 can run p with epi = kBf16Delta (CTA-pair kernel with the TMA-store epilogue,
+// 128-column heads, no accumulate, M a multiple of delta_T).
+bool gemm_delta_ok(const GemmParams& p);
 
 // Profiling: the 1024 per-tile phase stamps of the CTA named by SW_GEMM_TRACE_CTA.
 void gemm_trace_read(unsigned long long* out);

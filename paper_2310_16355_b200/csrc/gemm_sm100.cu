@@ -214,7 +214,7 @@ __device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int row, int
       }
     }
   }
-  if constexpr (EPI == Epi::kStoreBf16 || EPI == Epi::kBiasGelu || EPI == Epi::kGeluBwd) {
+  if constexpr (EPI == Epi::kStoreBf16 || EPI == Epi::kBiasGelu || EPI == Epi::kGeluBwd || EPI == Epi::kBf16Delta) {
     if constexpr (EPI == Epi::kGeluBwd) {
       const __nv_bfloat16* pre =
           reinterpret_cast<const __nv_bfloat16*>(p.aux) + static_cast<int64_t>(row) * p.ld_aux + col0;
@@ -522,7 +522,7 @@ constexpr int OPT_SMEM = SW_ADAMW_DIRECT ? 8 * 32 * 32 * 4 : OPT_NBUF * OPT_BUF;
 template <Epi EPI>
 constexpr bool tma_epi() {
   return SW_EPI_TMA && (EPI == Epi::kStoreF32 || EPI == Epi::kStoreBf16 || EPI == Epi::kResidF32 ||
-                        EPI == Epi::kBiasGelu || EPI == Epi::kGeluBwd);
+                        EPI == Epi::kBiasGelu || EPI == Epi::kGeluBwd || EPI == Epi::kBf16Delta);
 }
 constexpr int EPI_TMA_BUF = 32 * 32 * 4;  // one warp's chunk (fp32 size; bf16 uses half)
 template <Epi EPI>
@@ -549,7 +549,7 @@ constexpr int p_smem_bytes() {
 struct OptMaps {
   CUtensorMap p, m, v;
   CUtensorMap c;  // the output, for the TMA-store epilogue (kStoreF32 / kStoreBf16 / kResidF32)
-  CUtensorMap a;   // kResidF32: the residual addend; kGeluBwd: the bf16 pre-activations
+  CUtensorMap a;   // kResidF32: the residual addend; kGeluBwd: the bf16 pre-activations; kBf16Delta: O
   CUtensorMap c2;  // kBiasGelu: the activation output
 };
 
@@ -966,6 +966,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(p_threads<EPI>(), 1)
           uint8_t* stg = sOpt + (static_cast<int>(warp) - 4) * 2 * EPI_TMA_BUF;
           constexpr bool f32 = EPI == Epi::kStoreF32 || EPI == Epi::kResidF32;
           constexpr bool resid = EPI == Epi::kResidF32, gbwd = EPI == Epi::kGeluBwd, gfwd = EPI == Epi::kBiasGelu;
+          constexpr bool dlt = EPI == Epi::kBf16Delta;
+          float dsum = 0.f;  // kBf16Delta: this row's dO . O over the current 128-column head
           constexpr int chunk_bytes = f32 ? 4096 : 2048;
 #pragma unroll 1
           for (int j = 0; j < BN / 32; ++j) {
@@ -973,7 +975,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(p_threads<EPI>(), 1)
             uint64_t* ebar = &eload[(static_cast<int>(warp) - 4) * 2 + (j & 1)];
             if (lane == 0) {
               dev::bulk_wait_read_1();  // buffer (j & 1) was read by the store two chunks back
-              if constexpr (resid || gbwd) {  // the addend / pre-activation chunk lands while the accumulator is read
+              if constexpr (resid || gbwd || dlt) {  // the addend / pre-activation chunk lands while the accumulator is read
                 dev::mbar_arrive_expect_tx(ebar, chunk_bytes);
                 dev::tma_load_2d(stg + (j & 1) * EPI_TMA_BUF, &om.a, ebar, nb * BN + j * 32, row - static_cast<int>(lane));
               }
@@ -1010,6 +1012,31 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(p_threads<EPI>(), 1)
                                           v[8 * u + 2 * e + 1] * dev::gelu_tanh_grad(x.y));
                 }
                 *pa = make_uint4(o[0], o[1], o[2], o[3]);
+              }
+            } else if constexpr (dlt) {  // dO (bf16) in place over the loaded O chunk; dO . O into dsum
+              dev::mbar_wait(ebar, rphase[j & 1]);
+              rphase[j & 1] ^= 1u;
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                uint4* pa = reinterpret_cast<uint4*>(buf + ((u ^ ((lane >> 1) & 3)) << 4));
+                const uint4 raw = *pa;
+                const uint32_t w[4] = {raw.x, raw.y, raw.z, raw.w};
+                uint32_t o[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                  o[e] = dev::pack_bf16x2(v[8 * u + 2 * e], v[8 * u + 2 * e + 1]);
+                  const float2 x = dev::unpack_bf16x2(w[e]), y = dev::unpack_bf16x2(o[e]);
+                  dsum = fmaf(x.x, y.x, fmaf(x.y, y.y, dsum));
+                }
+                *pa = make_uint4(o[0], o[1], o[2], o[3]);
+              }
+              if ((j & 3) == 3) {
+                const int col = nb * BN + j * 32;
+                if (row < p.M) {
+                  const int b = row / p.delta_T, t = row - b * p.delta_T;
+                  p.delta[(static_cast<int64_t>(b) * (p.N >> 7) + (col >> 7)) * p.delta_T + t] = dsum;
+                }
+                dsum = 0.f;
               }
             } else if constexpr (gfwd) {  // pre-activation in the first half, gelu in the second
 #pragma unroll
@@ -1136,7 +1163,8 @@ cudaError_t launch_2sm(const GemmParams& p, cudaStream_t stream) {
       om.c = f32 ? make_tmap_f32_2d(p.C, p.N, p.M, p.ldc, 32, 32)
                  : make_tmap_bf16_2d_rowswz(p.C, p.N, p.M, p.ldc, 32, 32);
       if constexpr (EPI == Epi::kResidF32) om.a = make_tmap_f32_2d(p.aux, p.N, p.M, p.ld_aux, 32, 32);
-      if constexpr (EPI == Epi::kGeluBwd) om.a = make_tmap_bf16_2d_rowswz(p.aux, p.N, p.M, p.ld_aux, 32, 32);
+      if constexpr (EPI == Epi::kGeluBwd || EPI == Epi::kBf16Delta)
+        om.a = make_tmap_bf16_2d_rowswz(p.aux, p.N, p.M, p.ld_aux, 32, 32);
       if constexpr (EPI == Epi::kBiasGelu) om.c2 = make_tmap_bf16_2d_rowswz(p.C2, p.N, p.M, p.ldc2, 32, 32);
     }
   }
@@ -1294,6 +1322,11 @@ bool gemv_ok(const GemmParams& p) {
 
 }  // namespace
 
+bool gemm_delta_ok(const GemmParams& p) {
+  return SW_EPI_TMA && use_pairs() && !p.accumulate && p.aux != nullptr && p.delta != nullptr && p.delta_T > 0 &&
+         p.M % p.delta_T == 0 && p.N % 128 == 0 && p.ld_aux % 8 == 0 && p.C2 == nullptr && !gemv_ok(p);
+}
+
 void gemm_trace_read(unsigned long long* out) {
   cudaMemcpyFromSymbol(out, g_gemm_trace, sizeof(unsigned long long) * 1024);
 }
@@ -1331,6 +1364,9 @@ cudaError_t gemm_bf16(const GemmParams& p, cudaStream_t stream) {
         throw std::runtime_error("gemm_bf16: SwiGLU backward needs swiglu_half == N and the pre-activations");
       }
       return launch<Epi::kSwiGLUBwd>(p, stream);
+    case Epi::kBf16Delta:
+      if (!gemm_delta_ok(p)) throw std::runtime_error("gemm_bf16: fused attention delta not available for this call");
+      return launch<Epi::kBf16Delta>(p, stream);
     case Epi::kAdamW: {
       GemmParams q = p;
       const float lo = 1.0f / 16384.0f;

@@ -90,8 +90,10 @@ void attention_trace_read(unsigned long long* out);
 void attention_fwd(const bf16* qkv, bf16* o, float* lse, int B, int T, int Hl, int hd,
                    cudaStream_t s);
 // dqkv [M, 3*Dl]; scratch: fp32 [B*Hl*T] (delta) + fp32 [M, 3*Dl] (dk/dv accumulators).
+// delta_ready: scratch already holds delta = rowsum(dO * O) (written by the dO GEMM's kBf16Delta
+// epilogue), so the tcgen05 path skips its delta pass.
 void attention_bwd(const bf16* qkv, const bf16* o, const float* lse, const bf16* dout, bf16* dqkv,
-                   float* scratch, int B, int T, int Hl, int hd, cudaStream_t s);
+                   float* scratch, int B, int T, int Hl, int hd, cudaStream_t s, bool delta_ready = false);
 
 // y = a + b + bias[col]   (row-parallel output after the all-reduce: residual + partial + bias)
 void add_residual_bias(const float* a, const float* b, const float* bias, float* y, int64_t M,

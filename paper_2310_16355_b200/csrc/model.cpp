@@ -685,9 +685,11 @@ void Model::ag_mp_buf(std::vector<Rank*>& grp, float* Rank::*buf, int64_t chunk)
 void Model::gemm(Rank& R, int M, int N, int K, const void* A, int64_t lda, int a_mn, const void* B,
                  int64_t ldb, int b_mn, int epi, void* C, int64_t ldc, void* C2, int64_t ldc2,
                  const float* bias, const void* aux, int64_t ld_aux, int accumulate, int bias_seg,
-                 int64_t bias_seg_stride, int swiglu_half) {
+                 int64_t bias_seg_stride, int swiglu_half, float* delta, int delta_T) {
   (void)R;
   GemmParams p;
+  p.delta = delta;
+  p.delta_T = delta_T;
   p.swiglu_half = swiglu_half;
   p.M = M;
   p.N = N;
@@ -719,6 +721,33 @@ void Model::gemm(Rank& R, int M, int N, int K, const void* A, int64_t lda, int a
                        std::to_string(epi) + (a_mn ? ",A_mn" : ",A_k") + (b_mn ? ",B_mn" : ",B_k");
   }
   ++launches_;
+}
+
+bool Model::gemm_dout(Rank& R, int l, const bf16* wo) {
+  static const bool fuse = [] {
+    const char* e = std::getenv("SW_FUSE_DELTA");
+    return e == nullptr || std::atoi(e) != 0;
+  }();
+  const int M = static_cast<int>(M_);
+  if (fuse && hd_ == 128) {
+    GemmParams p;
+    p.M = M;
+    p.N = dl_;
+    p.K = d_;
+    p.b_mn_major = 1;
+    p.ldc = dl_;
+    p.aux = R.o[l];
+    p.ld_aux = dl_;
+    p.delta = R.attn_scratch;
+    p.delta_T = T_;
+    if (gemm_delta_ok(p)) {
+      gemm(R, M, dl_, d_, R.gb, d_, 0, wo, dl_, 1, static_cast<int>(Epi::kBf16Delta), R.dout, dl_, nullptr, 0,
+           nullptr, R.o[l], dl_, 0, 0, 0, 0, R.attn_scratch, T_);
+      return true;
+    }
+  }
+  gemm(R, M, dl_, d_, R.gb, d_, 0, wo, dl_, 1, static_cast<int>(Epi::kStoreBf16), R.dout, dl_);
+  return false;
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -1021,14 +1050,13 @@ void Model::backward_replica(std::vector<Rank*>& grp, bool accumulate) {
     for (Rank* R : grp) wgrad(*R, fk, fw, d, static_cast<int>(M), R->dpre, fw, R->a2[l], d, acc);
     // ---- attention ----
     for (Rank* R : grp) {
-      gemm(*R, static_cast<int>(M), dl, d, R->gb, d, 0, W(*R, ls.o_k), dl, 1,
-           static_cast<int>(Epi::kStoreBf16), R->dout, dl);
+      const bool delta_ready = gemm_dout(*R, l, W(*R, ls.o_k));
       wgrad(*R, ls.o_k, d, dl, static_cast<int>(M), R->gb, d, R->o[l], dl, acc);
       tic();
       k::attention_bwd(R->qkv[l], R->o[l], R->lse[l], R->dout, R->dqkv, R->attn_scratch, B_, T_, hl_, hd_,
-                       stream_);
+                       stream_, delta_ready);
       toc(kProfAttnBwd, 4.0 * B_ * hl_ * static_cast<double>(T_) * T_ * hd_);
-      launches_ += 3;
+      launches_ += delta_ready ? 2 : 3;
       k::colsum_bf16(R->dqkv, 3 * dl, M, 3 * dl, dl, G(*R, ls.q_b) + R->mpi * dl, G(*R, ls.k_b) + R->mpi * dl,
                      G(*R, ls.v_b) + R->mpi * dl, acc, R->col_scratch, stream_);
       launches_ += 2;

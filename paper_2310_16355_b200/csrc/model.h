@@ -162,7 +162,10 @@ class Model {
             int64_t ldb, int b_mn, int epi, void* C, int64_t ldc, void* C2 = nullptr,
             int64_t ldc2 = 0, const float* bias = nullptr, const void* aux = nullptr,
             int64_t ld_aux = 0, int accumulate = 0, int bias_seg = 0, int64_t bias_seg_stride = 0,
-            int swiglu_half = 0);
+            int swiglu_half = 0, float* delta = nullptr, int delta_T = 0);
+  // dO = gb x Wo with the attention backward's delta = rowsum(dO * O) fused into the epilogue
+  // (kBf16Delta) when the GEMM path supports it; returns whether delta was written
+  bool gemm_dout(Rank& R, int l, const bf16* wo);
   void wgrad(Rank& R, int slot, int M, int N, int K, const void* A, int64_t lda, const void* B, int64_t ldb,
              int accumulate);
   struct FusedAdam {

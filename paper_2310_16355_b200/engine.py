@@ -150,7 +150,10 @@ class Mesh:
             self._h = None
 
     def __del__(self):
-        self.close()
+        try:
+            self.close()
+        except TypeError:  # interpreter teardown: this module's globals are already cleared
+            pass
 
 
 def build_mesh(dp_size: int, mp_size: int, n_hosts: int = 1) -> Mesh:
@@ -176,7 +179,10 @@ class Model:
             self._h = None
 
     def __del__(self):
-        self.close()
+        try:
+            self.close()
+        except TypeError:  # interpreter teardown: this module's globals are already cleared
+            pass
 
     # ---- params ----
     def init_params(self, seed: int = 42, stream: str = "model-init"):
@@ -331,7 +337,10 @@ class T5Model:
             self._h = None
 
     def __del__(self):
-        self.close()
+        try:
+            self.close()
+        except TypeError:  # interpreter teardown: this module's globals are already cleared
+            pass
 
     def init_params(self, seed: int = 42, stream: str = "model-init"):
         _lib.check(_declare().sw_t5_init_params(self._h, seed, stream.encode()))

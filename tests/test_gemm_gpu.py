@@ -222,3 +222,37 @@ def test_small_m_gemv_path(M, epi):
         _gemm(A, 0, B, 0, M, N, K, 3, C, bias=bias, aux=aux)
         want = aux + ref + bias
     assert _rel(C, want) < (1e-2 if epi == 0 else 1e-5)
+
+
+@pytest.mark.parametrize("Bs,T,H,K", [(2, 320, 4, 384), (1, 2048, 2, 4096)])
+def test_gemm_dout_with_attention_delta(Bs, T, H, K):
+    """epi 8: the attention-output-gradient GEMM (dO = g x Wo, Wo MN-major) also writes the flash
+    backward's delta[b, h, t] = sum_c dO[b*T+t, h*128+c] * O[b*T+t, h*128+c] from the bf16 dO it
+    stores (replaces attn_bwd's separate delta pass)."""
+    M, N = Bs * T, H * 128
+    gen = torch.Generator(device=DEV).manual_seed(T + K)
+    g = torch.randn(M, K, generator=gen, device=DEV).bfloat16()
+    wo = torch.randn(K, N, generator=gen, device=DEV).bfloat16()  # [d, dl]: B operand MN-major
+    O = torch.randn(M, N, generator=gen, device=DEV).bfloat16()
+    dO = torch.empty(M, N, device=DEV, dtype=torch.bfloat16)
+    delta = torch.full((Bs * H * T,), float("nan"), device=DEV)
+    L = _lib.lib()
+    _lib.check(L.sw_k_gemm_bf16(M, N, K, g.data_ptr(), K, 0, wo.data_ptr(), N, 1, 8, dO.data_ptr(), N,
+                                delta.data_ptr(), T, None, O.data_ptr(), N, 1.0, 0, None))
+    torch.cuda.synchronize()
+    want = g.float() @ wo.float()
+    assert _rel(dO, want) < 1e-2
+    ref = (dO.float() * O.float()).view(Bs, T, H, 128).sum(-1).permute(0, 2, 1).reshape(-1)
+    assert torch.isfinite(delta).all()
+    assert torch.allclose(delta, ref, rtol=1e-5, atol=1e-3)
+
+
+def test_gemm_dout_delta_rejects_ragged_heads():
+    L = _lib.lib()
+    x = torch.zeros(256, 200, device=DEV, dtype=torch.bfloat16)
+    w = torch.zeros(64, 200, device=DEV, dtype=torch.bfloat16)
+    d = torch.zeros(256 * 2, device=DEV)
+    st = L.sw_k_gemm_bf16(256, 200, 64, torch.zeros(256, 64, device=DEV, dtype=torch.bfloat16).data_ptr(), 64, 0,
+                          w.data_ptr(), 200, 1, 8, x.data_ptr(), 200, d.data_ptr(), 128, None, x.data_ptr(), 200,
+                          1.0, 0, None)
+    assert st != 0

@@ -10,7 +10,7 @@
 
 using namespace sw;
 
-template <int M, int N, int MODE>  // MODE 0: SS K-major A/B; 1: SS, B MN-major; 2: TS (A in TMEM)
+template <int M, int N, int MODE>  // MODE 0: SS K-major A/B; 1: SS, B MN-major; 2: TS (A in TMEM); 3: SS, A and B MN-major
 __global__ void __launch_bounds__(128, 1) mma_rate(unsigned long long* out, int iters) {
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 200 * 1024);
@@ -26,9 +26,9 @@ __global__ void __launch_bounds__(128, 1) mma_rate(unsigned long long* out, int 
   dev::tc_fence_after();
   const uint32_t tmem = *slot;
   if (warp == 1) {
-    const uint32_t idesc = dev::make_idesc_bf16(M, N, 0, MODE == 1 ? 1 : 0);
-    const uint64_t da = dev::make_sdesc_sw128(dev::smem_u32(smem), 16, 1024);
-    const uint64_t db = dev::make_sdesc_sw128(dev::smem_u32(smem + 64 * 1024), MODE == 1 ? 16384 : 16, 1024);
+    const uint32_t idesc = dev::make_idesc_bf16(M, N, MODE == 3 ? 1 : 0, (MODE == 1 || MODE == 3) ? 1 : 0);
+    const uint64_t da = dev::make_sdesc_sw128(dev::smem_u32(smem), MODE == 3 ? 8192 : 16, 1024);
+    const uint64_t db = dev::make_sdesc_sw128(dev::smem_u32(smem + 64 * 1024), (MODE == 1 || MODE == 3) ? 8192 : 16, 1024);
     long long t0 = clock64();
     for (int it = 0; it < iters; ++it) {
       if (dev::elect_one_sync()) {
@@ -36,6 +36,10 @@ __global__ void __launch_bounds__(128, 1) mma_rate(unsigned long long* out, int 
         for (int kk = 0; kk < 16; ++kk) {
           if (MODE == 2)
             dev::umma_f16_ts(tmem + 256, tmem + (kk & 7) * 8, db + ((kk & 3) * 2), idesc, 1u);
+          else if (MODE == 3)
+            dev::umma_f16_ss(tmem, da + ((kk & 3) * 128), db + ((kk & 3) * 128), idesc, 1u);
+          else if (MODE == 1)
+            dev::umma_f16_ss(tmem, da + ((kk & 3) * 2), db + ((kk & 3) * 128), idesc, 1u);
           else
             dev::umma_f16_ss(tmem, da + ((kk & 3) * 2), db + ((kk & 3) * 2), idesc, 1u);
         }
@@ -78,6 +82,9 @@ int main() {
   run<128, 128, 0>("SS M128 N128 K-major", d_out);
   run<128, 128, 1>("SS M128 N128 B MN-major", d_out);
   run<128, 256, 0>("SS M128 N256 K-major", d_out);
+  run<128, 256, 1>("SS M128 N256 B MN-major", d_out);
+  run<128, 256, 3>("SS M128 N256 A+B MN-major", d_out);
+  run<128, 128, 3>("SS M128 N128 A+B MN-major", d_out);
   run<128, 64, 2>("TS M128 N64", d_out);
   run<128, 128, 2>("TS M128 N128", d_out);
   return 0;
