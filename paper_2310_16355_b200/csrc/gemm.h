@@ -72,6 +72,9 @@ struct GemmParams {
   int num_sms = 0;  // 0 = all
   int trace_cta = -1;  // profiling: CTA whose per-tile phases are stamped (SW_GEMM_TRACE_CTA)
   float* delta = nullptr;  // kBf16Delta output [M / delta_T][N / 128][delta_T]
+  // kGeluBwd: per-32-row partial column sums of the stored bf16 output, [ceil(M / 32)][N] (the
+  // bias gradient of the GeLU layer; reduce with k::colsum_chunks). Requires gemm_colsum_ok.
+  float* colsum = nullptr;
   int delta_T = 0;
 };
 
@@ -81,6 +84,8 @@ cudaError_t gemm_bf16(const GemmParams& p, cudaStream_t stream);
 // Whether gemm_bf16 can run p with epi = kBf16Delta (CTA-pair kernel with the TMA-store epilogue,
 // 128-column heads, no accumulate, M a multiple of delta_T).
 bool gemm_delta_ok(const GemmParams& p);
+// Whether a kGeluBwd call can also write the partial column sums (p.colsum).
+bool gemm_colsum_ok(const GemmParams& p);
 
 // Profiling: the 1024 per-tile phase stamps of the CTA named by SW_GEMM_TRACE_CTA.
 void gemm_trace_read(unsigned long long* out);

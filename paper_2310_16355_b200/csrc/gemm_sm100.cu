@@ -1072,6 +1072,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(p_threads<EPI>(), 1)
                                   row - static_cast<int>(lane));
               dev::bulk_commit();
             }
+            if constexpr (gbwd) {
+              if (p.colsum != nullptr) {
+                // column sums of the stored chunk (the bias gradient): lanes 0-15 take the even rows,
+                // 16-31 the odd ones, lane l % 16 owns columns 2(l % 16) and 2(l % 16) + 1
+                const uint8_t* cb = stg + (j & 1) * EPI_TMA_BUF;
+                const int cl = static_cast<int>(lane & 15), rh = static_cast<int>(lane >> 4);
+                float s0 = 0.f, s1 = 0.f;
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                  const int rr = 2 * i + rh;
+                  const float2 x = dev::unpack_bf16x2(*reinterpret_cast<const uint32_t*>(
+                      cb + rr * 64 + (((cl >> 2) ^ ((rr >> 1) & 3)) << 4) + (cl & 3) * 4));
+                  s0 += x.x;
+                  s1 += x.y;
+                }
+                s0 += __shfl_down_sync(0xffffffffu, s0, 16);
+                s1 += __shfl_down_sync(0xffffffffu, s1, 16);
+                const int col = nb * BN + j * 32 + 2 * cl;
+                const int rb = row - static_cast<int>(lane);
+                if (lane < 16 && rb < p.M && col < p.N)
+                  *reinterpret_cast<float2*>(p.colsum + static_cast<int64_t>(rb >> 5) * p.N + col) =
+                      make_float2(s0, s1);
+              }
+            }
           }
         } else {
 #pragma unroll 1
@@ -1327,6 +1351,10 @@ bool gemm_delta_ok(const GemmParams& p) {
          p.M % p.delta_T == 0 && p.N % 128 == 0 && p.ld_aux % 8 == 0 && p.C2 == nullptr && !gemv_ok(p);
 }
 
+bool gemm_colsum_ok(const GemmParams& p) {
+  return SW_EPI_TMA && use_pairs() && p.epi == Epi::kGeluBwd && !p.accumulate && !gemv_ok(p);
+}
+
 void gemm_trace_read(unsigned long long* out) {
   cudaMemcpyFromSymbol(out, g_gemm_trace, sizeof(unsigned long long) * 1024);
 }
@@ -1353,7 +1381,10 @@ cudaError_t gemm_bf16(const GemmParams& p, cudaStream_t stream) {
     case Epi::kStoreF32: return launch<Epi::kStoreF32>(p, stream);
     case Epi::kBiasGelu: return launch<Epi::kBiasGelu>(p, stream);
     case Epi::kResidF32: return launch<Epi::kResidF32>(p, stream);
-    case Epi::kGeluBwd: return launch<Epi::kGeluBwd>(p, stream);
+    case Epi::kGeluBwd:
+      if (p.colsum != nullptr && !gemm_colsum_ok(p))
+        throw std::runtime_error("gemm_bf16: fused column sums not available for this call");
+      return launch<Epi::kGeluBwd>(p, stream);
     case Epi::kSwiGLU:
       if (p.swiglu_half != p.N || p.b_mn_major) {
         throw std::runtime_error("gemm_bf16: SwiGLU needs swiglu_half == N and a K-major fused weight");

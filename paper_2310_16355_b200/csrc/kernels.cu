@@ -611,6 +611,27 @@ __global__ void __launch_bounds__(256) colsum_partial_kernel(const T* __restrict
   }
 }
 
+// out[n] (+)= sum over chunks of partial[c][n] in a fixed order (per-32-row partials written by
+// the GeLU-backward GEMM epilogue): 32 columns x 8 chunk lanes per CTA, then a fixed-order fold.
+__global__ void __launch_bounds__(256) colsum_chunks_kernel(const float* __restrict__ partial, int chunks, int N,
+                                                            float* out, int accumulate) {
+  __shared__ float sm[8][33];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int n = blockIdx.x * 32 + tx;
+  float s = 0.f;
+  if (n < N) {
+    for (int c = ty; c < chunks; c += 8) s += partial[static_cast<int64_t>(c) * N + n];
+  }
+  sm[ty][tx] = s;
+  __syncthreads();
+  if (ty == 0 && n < N) {
+    float t = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) t += sm[i][tx];
+    out[n] = accumulate ? out[n] + t : t;
+  }
+}
+
 __global__ void colsum_final_kernel(const float* __restrict__ partial, int chunks, int N, int seg,
                                     float* out0, float* out1, float* out2, int accumulate) {
   const int n = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1086,6 +1107,10 @@ void colsum_bf16(const bf16* X, int64_t ld, int64_t M, int N, int seg, float* ou
   colsum_partial_kernel<bf16><<<grid, 256, 0, s>>>(X, ld, M, N, scratch);
   colsum_final_kernel<<<(N + 255) / 256, 256, 0, s>>>(scratch, chunks, N, seg > 0 ? seg : N, out0,
                                                      out1, out2, accumulate);
+}
+
+void colsum_chunks(const float* partial, int chunks, int N, float* out, int accumulate, cudaStream_t s) {
+  colsum_chunks_kernel<<<(N + 31) / 32, 256, 0, s>>>(partial, chunks, N, out, accumulate);
 }
 
 void colsum_f32(const float* X, int64_t ld, int64_t M, int N, float* out, int accumulate,

@@ -51,6 +51,8 @@ int64_t layernorm_bwd_partials(int d);
 // out: column n goes to outs[n / seg][n % seg] (up to 3 segments). scratch: >= 64*N floats.
 void colsum_bf16(const bf16* X, int64_t ld, int64_t M, int N, int seg, float* out0, float* out1,
                  float* out2, int accumulate, float* scratch, cudaStream_t s);
+// out[n] (+)= sum_c partial[c * N + n] over `chunks` rows of partial sums, fixed order.
+void colsum_chunks(const float* partial, int chunks, int N, float* out, int accumulate, cudaStream_t s);
 void colsum_f32(const float* X, int64_t ld, int64_t M, int N, float* out, int accumulate,
                 float* scratch, cudaStream_t s);
 

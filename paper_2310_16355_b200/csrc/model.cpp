@@ -3,6 +3,7 @@
 
 #include <unordered_map>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -74,6 +75,8 @@ Model::Model(const ModelSpec& spec, const Plan& plan, Mesh* mesh, int batch, int
   {
     const char* e = std::getenv("SW_AR_BF16");
     ar_bf16_ = mesh_->mp > 1 && e != nullptr && e[0] == '1';
+    const char* fc = std::getenv("SW_FUSE_COLSUM");
+    fuse_colsum_ = fc == nullptr || fc[0] != '0';
   }
   build_layout();
   allocate();
@@ -326,7 +329,8 @@ void Model::allocate() {
     int64_t widest = d_;
     if (3 * dl_ > widest) widest = 3 * dl_;
     if (fl_ > widest) widest = fl_;
-    R.col_scratch = alloc<float>(chunks * widest);
+    // also holds the GeLU-backward epilogue's per-32-row partial column sums of dpre
+    R.col_scratch = alloc<float>(std::max(chunks * widest, ((M + 31) / 32) * static_cast<int64_t>(fl_)));
     R.ln_partials = alloc<float>(k::layernorm_bwd_partials(d_));
     R.tok_keys = alloc<uint32_t>(k::embed_bwd_keys(M_));
     R.attn_scratch = alloc<float>(M * hl_ + M * 2 * dl_ + 64);
@@ -685,9 +689,10 @@ void Model::ag_mp_buf(std::vector<Rank*>& grp, float* Rank::*buf, int64_t chunk)
 void Model::gemm(Rank& R, int M, int N, int K, const void* A, int64_t lda, int a_mn, const void* B,
                  int64_t ldb, int b_mn, int epi, void* C, int64_t ldc, void* C2, int64_t ldc2,
                  const float* bias, const void* aux, int64_t ld_aux, int accumulate, int bias_seg,
-                 int64_t bias_seg_stride, int swiglu_half, float* delta, int delta_T) {
+                 int64_t bias_seg_stride, int swiglu_half, float* delta, int delta_T, float* colsum) {
   (void)R;
   GemmParams p;
+  p.colsum = colsum;
   p.delta = delta;
   p.delta_T = delta_T;
   p.swiglu_half = swiglu_half;
@@ -999,16 +1004,32 @@ void Model::backward_replica(std::vector<Rank*>& grp, bool accumulate) {
     const int fw = spec_.swiglu ? 2 * fl : fl;
     const int fk = spec_.swiglu ? ls.gate_k : ls.fc1_k;
     for (Rank* R : grp) {
+      bool cs_done = false;
       if (spec_.swiglu) {
         gemm(*R, static_cast<int>(M), fl, d, R->gb, d, 0, W(*R, ls.fc2_k), fl, 1,
              static_cast<int>(Epi::kSwiGLUBwd), R->dpre, 2 * fl, nullptr, 0, nullptr, R->pre[l], 2 * fl, 0, 0, 0,
              fl);
       } else {
+        // the fc1 bias gradient's per-32-row column sums come out of the same epilogue
+        GemmParams q;
+        q.M = static_cast<int>(M);
+        q.N = fl;
+        q.K = d;
+        q.b_mn_major = 1;
+        q.epi = Epi::kGeluBwd;
+        const bool fuse_cs = ls.fc1_b >= 0 && fuse_colsum_ && gemm_colsum_ok(q);
         gemm(*R, static_cast<int>(M), fl, d, R->gb, d, 0, W(*R, ls.fc2_k), fl, 1,
-             static_cast<int>(Epi::kGeluBwd), R->dpre, fl, nullptr, 0, nullptr, R->pre[l], fl);
+             static_cast<int>(Epi::kGeluBwd), R->dpre, fl, nullptr, 0, nullptr, R->pre[l], fl, 0, 0, 0, 0,
+             nullptr, 0, fuse_cs ? R->col_scratch : nullptr);
+        if (fuse_cs) {
+          k::colsum_chunks(R->col_scratch, static_cast<int>((M + 31) / 32), fl, G(*R, ls.fc1_b) + R->mpi * fl, acc,
+                           stream_);
+          ++launches_;
+          cs_done = true;
+        }
       }
       wgrad(*R, ls.fc2_k, d, fl, static_cast<int>(M), R->gb, d, R->act[l], fl, acc);
-      if (ls.fc1_b >= 0) {
+      if (ls.fc1_b >= 0 && !cs_done) {
         k::colsum_bf16(R->dpre, fl, M, fl, 0, G(*R, ls.fc1_b) + R->mpi * fl, nullptr, nullptr, acc,
                        R->col_scratch, stream_);
         launches_ += 2;

@@ -162,7 +162,7 @@ class Model {
             int64_t ldb, int b_mn, int epi, void* C, int64_t ldc, void* C2 = nullptr,
             int64_t ldc2 = 0, const float* bias = nullptr, const void* aux = nullptr,
             int64_t ld_aux = 0, int accumulate = 0, int bias_seg = 0, int64_t bias_seg_stride = 0,
-            int swiglu_half = 0, float* delta = nullptr, int delta_T = 0);
+            int swiglu_half = 0, float* delta = nullptr, int delta_T = 0, float* colsum = nullptr);
   // dO = gb x Wo with the attention backward's delta = rowsum(dO * O) fused into the epilogue
   // (kBf16Delta) when the GEMM path supports it; returns whether delta was written
   bool gemm_dout(Rank& R, int l, const bf16* wo);
@@ -203,6 +203,7 @@ class Model {
   // oracle-parity tolerances of the mini configurations (LayerNorm parameter gradients at 1e-2)
   // do not survive it; TP invariance on tiny.spec does (tests/test_model_gpu.py).
   bool ar_bf16_ = false;
+  bool fuse_colsum_ = true;  // SW_FUSE_COLSUM=0: fc1 bias gradient by the separate column-sum pass
   int* d_flag_ = nullptr;
   int64_t launches_ = 0;
   // profiling
