@@ -18,7 +18,7 @@ bool attention_mma_fwd(const bf16* qkv, bf16* o, float* lse, int B, int T, int H
                        cudaStream_t s);
 bool attention_mma_bwd(const bf16* qkv, const bf16* o, const float* lse, const bf16* dout,
                        bf16* dqkv, float* scratch, int B, int T, int Hl, int hd, cudaStream_t s,
-                       bool delta_ready);
+                       bool delta_ready, float* colsum, bool* colsum_done);
 bool attention_mma_fwd_ex(const bf16* qkv, bf16* o, float* lse, int B, int T, int Hl, int hd, int causal,
                           const float* lut, float scale, cudaStream_t s);
 bool attention_mma_bwd_ex(const bf16* qkv, const bf16* o, const float* lse, const bf16* dout, bf16* dqkv,
@@ -176,8 +176,10 @@ void attention_fwd(const bf16* qkv, bf16* o, float* lse, int B, int T, int Hl, i
 }
 
 void attention_bwd(const bf16* qkv, const bf16* o, const float* lse, const bf16* dout, bf16* dqkv,
-                   float* scratch, int B, int T, int Hl, int hd, cudaStream_t s, bool delta_ready) {
-  if (attention_mma_bwd(qkv, o, lse, dout, dqkv, scratch, B, T, Hl, hd, s, delta_ready)) return;
+                   float* scratch, int B, int T, int Hl, int hd, cudaStream_t s, bool delta_ready, float* colsum,
+                   bool* colsum_done) {
+  if (colsum_done != nullptr) *colsum_done = false;
+  if (attention_mma_bwd(qkv, o, lse, dout, dqkv, scratch, B, T, Hl, hd, s, delta_ready, colsum, colsum_done)) return;
   const int64_t M = static_cast<int64_t>(B) * T;
   const int Dl = Hl * hd;
   float* delta = scratch;

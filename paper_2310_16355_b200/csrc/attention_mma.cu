@@ -961,12 +961,29 @@ struct Bwd2Layout {
   static constexpr int BYTES = OFF_BAR + 256;  // dynamic smem base declared 1024-aligned
 };
 
+// Column sums across a warp: lane i holds row i of a 32x32 tile in x[]; returns the sum of
+// column `lane` (transpose-reduce: 31 shuffles, fixed order).
+__device__ __forceinline__ float warp_colsum32(float (&x)[32], uint32_t lane) {
+#pragma unroll
+  for (int s = 16; s >= 1; s >>= 1) {
+    const bool up = (lane & s) != 0;
+#pragma unroll
+    for (int i = 0; i < s; ++i) {
+      const float send = up ? x[i] : x[i + s];
+      const float keep = up ? x[i + s] : x[i];
+      x[i] = keep + __shfl_xor_sync(0xffffffffu, send, s);
+    }
+  }
+  return x[0];
+}
+
 __global__ void __launch_bounds__(512, 1)
     attn_bwd_tc2(const __grid_constant__ CUtensorMap tm_qkv64, const __grid_constant__ CUtensorMap tm_qkv128,
                  const __grid_constant__ CUtensorMap tm_do64, const __grid_constant__ CUtensorMap tm_dq,
                  const float* __restrict__ lse, const float* __restrict__ delta, bf16* __restrict__ dqkv, int T,
                  int Hl, float scale_log2, float scale, int nbh, int group, int trace_cta, int dq_first, int ts,
-                 int causal, const float* __restrict__ lut, float* __restrict__ dlut) {
+                 int causal, const float* __restrict__ lut, float* __restrict__ dlut,
+                 float* __restrict__ colsum) {
   using Lay = Bwd2Layout;
   constexpr int HD = Lay::HD;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -1274,6 +1291,24 @@ __global__ void __launch_bounds__(512, 1)
           *reinterpret_cast<uint4*>(dv_row + c * 32 + 8 * u) = z;
         }
       }
+      if (colsum != nullptr && key - static_cast<int>(lane) < T) {  // k / v bias gradients of this warp's 32 keys
+        float xk[32], xv[32];
+#pragma unroll
+        for (int i = 0; i < 32; i += 2) {
+          const float2 fk = dev::unpack_bf16x2(dev::pack_bf16x2(__uint_as_float(a[i]), __uint_as_float(a[i + 1])));
+          const float2 fv = dev::unpack_bf16x2(dev::pack_bf16x2(__uint_as_float(v[i]), __uint_as_float(v[i + 1])));
+          const bool in = key < T;
+          xk[i] = in ? fk.x : 0.f;
+          xk[i + 1] = in ? fk.y : 0.f;
+          xv[i] = in ? fv.x : 0.f;
+          xv[i + 1] = in ? fv.y : 0.f;
+        }
+        const float sk = warp_colsum32(xk, lane), sv = warp_colsum32(xv, lane);
+        float* dst = colsum + static_cast<int64_t>((row0 + key - static_cast<int>(lane)) >> 5) * (3LL * Dl) + Dl +
+                     h * HD + c * 32 + lane;
+        dst[0] = sk;
+        dst[Dl] = sv;
+      }
     }
   } else if (warp >= 12) {
     // dQ^T_n: lane = head dim d, 64 query columns -> SW128 staging [4 boxes][64 rows][32 fp32]
@@ -1417,6 +1452,33 @@ void launch_delta(const bf16* o, const bf16* dout, float* delta, int T, int Hl, 
   }
 }
 
+// dQ (fp32 accumulator) -> bf16 q columns of dqkv, plus the q bias gradient's per-32-row column
+// partials colsum[r / 32][c] of the rounded values: CTA = 32 rows x 1024 columns, 4 per thread
+__global__ void __launch_bounds__(256) dq_to_bf16_colsum(const float* __restrict__ acc, bf16* __restrict__ dqkv,
+                                                         int64_t rows, int Dl, float* __restrict__ colsum) {
+  const int c = (blockIdx.y * 256 + threadIdx.x) * 4;
+  const int64_t r0 = static_cast<int64_t>(blockIdx.x) * 32;
+  if (c >= Dl) return;
+  float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+#pragma unroll 8
+  for (int i = 0; i < 32; ++i) {
+    const int64_t r = r0 + i;
+    if (r < rows) {
+      const float4 v = *reinterpret_cast<const float4*>(acc + r * Dl + c);
+      uint2 w;
+      w.x = dev::pack_bf16x2(v.x, v.y);
+      w.y = dev::pack_bf16x2(v.z, v.w);
+      *reinterpret_cast<uint2*>(dqkv + r * 3LL * Dl + c) = w;
+      const float2 a = dev::unpack_bf16x2(w.x), b = dev::unpack_bf16x2(w.y);
+      s0 += a.x;
+      s1 += a.y;
+      s2 += b.x;
+      s3 += b.y;
+    }
+  }
+  *reinterpret_cast<float4*>(colsum + blockIdx.x * 3LL * Dl + c) = make_float4(s0, s1, s2, s3);
+}
+
 __global__ void dq_to_bf16(const float* __restrict__ acc, bf16* __restrict__ dqkv, int64_t rows, int Dl) {
   const int64_t n4 = rows * Dl / 4;
   for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n4;
@@ -1440,7 +1502,8 @@ bool bwd2_enabled() {
 
 bool launch_bwd2(const bf16* qkv, const bf16* o, const float* lse, const bf16* dout, bf16* dqkv, float* scratch,
                  int B, int T, int Hl, cudaStream_t s, int causal = 1, const float* lut = nullptr,
-                 float* dlut = nullptr, float scale_arg = 0.f, bool delta_ready = false) {
+                 float* dlut = nullptr, float scale_arg = 0.f, bool delta_ready = false,
+                 float* colsum = nullptr, bool* colsum_done = nullptr) {
   constexpr int HD = 128;
   static bool configured = false;
   if (!configured) {
@@ -1464,19 +1527,28 @@ bool launch_bwd2(const bf16* qkv, const bf16* o, const float* lse, const bf16* d
                                              static_cast<uint64_t>(Dl), 32, BQ2);
   const int nb = (T + 127) / 128;
   const double scale = scale_arg > 0.f ? scale_arg : 1.0 / std::sqrt(static_cast<double>(HD));
+  // bias-gradient partials need 32-row groups that never straddle two sequences
+  float* cs = (colsum != nullptr && T % 32 == 0) ? colsum : nullptr;
   attn_bwd_tc2<<<nb * B * Hl, 512, Bwd2Layout::BYTES, s>>>(tm_qkv64, tm_qkv128, tm_do64, tm_dq, lse, delta, dqkv,
                                                           T, Hl, static_cast<float>(scale * 1.4426950408889634),
                                                           static_cast<float>(scale), B * Hl, work_group(), trace_cta(), bwd_dq_first(),
-                                                          (lut || dlut) ? 1 : bwd_ts(), causal, lut, dlut);
-  dq_to_bf16<<<1184, 256, 0, s>>>(dq, dqkv, M, Dl);
+                                                          (lut || dlut) ? 1 : bwd_ts(), causal, lut, dlut, cs);
+  if (cs != nullptr) {
+    dq_to_bf16_colsum<<<dim3(static_cast<unsigned>((M + 31) / 32), (Dl + 1023) / 1024), 256, 0, s>>>(dq, dqkv, M, Dl,
+                                                                                                      cs);
+  } else {
+    dq_to_bf16<<<1184, 256, 0, s>>>(dq, dqkv, M, Dl);
+  }
+  if (colsum_done != nullptr) *colsum_done = cs != nullptr;
   return true;
 }
 
 template <int HD>
 bool launch_bwd(const bf16* qkv, const bf16* o, const float* lse, const bf16* dout, bf16* dqkv, float* scratch,
-                int B, int T, int Hl, cudaStream_t s, bool delta_ready) {
+                int B, int T, int Hl, cudaStream_t s, bool delta_ready, float* colsum, bool* colsum_done) {
   if (HD == 128 && bwd2_enabled())
-    return launch_bwd2(qkv, o, lse, dout, dqkv, scratch, B, T, Hl, s, 1, nullptr, nullptr, 0.f, delta_ready);
+    return launch_bwd2(qkv, o, lse, dout, dqkv, scratch, B, T, Hl, s, 1, nullptr, nullptr, 0.f, delta_ready, colsum,
+                       colsum_done);
   using Lay = BwdLayout<HD>;
   static bool configured = false;
   if (!configured) {
@@ -1534,10 +1606,11 @@ bool attention_mma_bwd_ex(const bf16* qkv, const bf16* o, const float* lse, cons
 }
 
 bool attention_mma_bwd(const bf16* qkv, const bf16* o, const float* lse, const bf16* dout, bf16* dqkv,
-                       float* scratch, int B, int T, int Hl, int hd, cudaStream_t s, bool delta_ready) {
+                       float* scratch, int B, int T, int Hl, int hd, cudaStream_t s, bool delta_ready,
+                       float* colsum, bool* colsum_done) {
   if (((Hl * hd) % 8) != 0) return false;
-  if (hd == 128) return launch_bwd<128>(qkv, o, lse, dout, dqkv, scratch, B, T, Hl, s, delta_ready);
-  if (hd == 64) return launch_bwd<64>(qkv, o, lse, dout, dqkv, scratch, B, T, Hl, s, delta_ready);
+  if (hd == 128) return launch_bwd<128>(qkv, o, lse, dout, dqkv, scratch, B, T, Hl, s, delta_ready, colsum, colsum_done);
+  if (hd == 64) return launch_bwd<64>(qkv, o, lse, dout, dqkv, scratch, B, T, Hl, s, delta_ready, colsum, colsum_done);
   return false;
 }
 

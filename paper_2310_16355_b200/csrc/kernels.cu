@@ -614,7 +614,8 @@ __global__ void __launch_bounds__(256) colsum_partial_kernel(const T* __restrict
 // out[n] (+)= sum over chunks of partial[c][n] in a fixed order (per-32-row partials written by
 // the GeLU-backward GEMM epilogue): 32 columns x 8 chunk lanes per CTA, then a fixed-order fold.
 __global__ void __launch_bounds__(256) colsum_chunks_kernel(const float* __restrict__ partial, int chunks, int N,
-                                                            float* out, int accumulate) {
+                                                            int seg, float* out0, float* out1, float* out2,
+                                                            int accumulate) {
   __shared__ float sm[8][33];
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const int n = blockIdx.x * 32 + tx;
@@ -628,7 +629,9 @@ __global__ void __launch_bounds__(256) colsum_chunks_kernel(const float* __restr
     float t = 0.f;
 #pragma unroll
     for (int i = 0; i < 8; ++i) t += sm[i][tx];
-    out[n] = accumulate ? out[n] + t : t;
+    const int si = n / seg;
+    float* o = (si == 0 ? out0 : si == 1 ? out1 : out2) + (n - si * seg);
+    *o = accumulate ? *o + t : t;
   }
 }
 
@@ -1109,8 +1112,10 @@ void colsum_bf16(const bf16* X, int64_t ld, int64_t M, int N, int seg, float* ou
                                                      out1, out2, accumulate);
 }
 
-void colsum_chunks(const float* partial, int chunks, int N, float* out, int accumulate, cudaStream_t s) {
-  colsum_chunks_kernel<<<(N + 31) / 32, 256, 0, s>>>(partial, chunks, N, out, accumulate);
+void colsum_chunks(const float* partial, int chunks, int N, float* out, int accumulate, cudaStream_t s, int seg,
+                   float* out1, float* out2) {
+  colsum_chunks_kernel<<<(N + 31) / 32, 256, 0, s>>>(partial, chunks, N, seg > 0 ? seg : N, out, out1, out2,
+                                                     accumulate);
 }
 
 void colsum_f32(const float* X, int64_t ld, int64_t M, int N, float* out, int accumulate,

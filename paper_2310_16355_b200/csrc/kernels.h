@@ -52,7 +52,9 @@ int64_t layernorm_bwd_partials(int d);
 void colsum_bf16(const bf16* X, int64_t ld, int64_t M, int N, int seg, float* out0, float* out1,
                  float* out2, int accumulate, float* scratch, cudaStream_t s);
 // out[n] (+)= sum_c partial[c * N + n] over `chunks` rows of partial sums, fixed order.
-void colsum_chunks(const float* partial, int chunks, int N, float* out, int accumulate, cudaStream_t s);
+// seg > 0: columns [i*seg, (i+1)*seg) go to out_i (i < 3), like colsum_bf16.
+void colsum_chunks(const float* partial, int chunks, int N, float* out, int accumulate, cudaStream_t s,
+                   int seg = 0, float* out1 = nullptr, float* out2 = nullptr);
 void colsum_f32(const float* X, int64_t ld, int64_t M, int N, float* out, int accumulate,
                 float* scratch, cudaStream_t s);
 
@@ -94,8 +96,11 @@ void attention_fwd(const bf16* qkv, bf16* o, float* lse, int B, int T, int Hl, i
 // dqkv [M, 3*Dl]; scratch: fp32 [B*Hl*T] (delta) + fp32 [M, 3*Dl] (dk/dv accumulators).
 // delta_ready: scratch already holds delta = rowsum(dO * O) (written by the dO GEMM's kBf16Delta
 // epilogue), so the tcgen05 path skips its delta pass.
+// colsum (optional, [M / 32][3*Dl] fp32): the q|k|v bias gradients' per-32-row column partials
+// of dqkv, written when *colsum_done comes back true (reduce with colsum_chunks).
 void attention_bwd(const bf16* qkv, const bf16* o, const float* lse, const bf16* dout, bf16* dqkv,
-                   float* scratch, int B, int T, int Hl, int hd, cudaStream_t s, bool delta_ready = false);
+                   float* scratch, int B, int T, int Hl, int hd, cudaStream_t s, bool delta_ready = false,
+                   float* colsum = nullptr, bool* colsum_done = nullptr);
 
 // y = a + b + bias[col]   (row-parallel output after the all-reduce: residual + partial + bias)
 void add_residual_bias(const float* a, const float* b, const float* bias, float* y, int64_t M,

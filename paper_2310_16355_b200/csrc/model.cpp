@@ -330,7 +330,7 @@ void Model::allocate() {
     if (3 * dl_ > widest) widest = 3 * dl_;
     if (fl_ > widest) widest = fl_;
     // also holds the GeLU-backward epilogue's per-32-row partial column sums of dpre
-    R.col_scratch = alloc<float>(std::max(chunks * widest, ((M + 31) / 32) * static_cast<int64_t>(fl_)));
+    R.col_scratch = alloc<float>(std::max(chunks * widest, ((M + 31) / 32) * std::max<int64_t>(fl_, 3 * dl_)));
     R.ln_partials = alloc<float>(k::layernorm_bwd_partials(d_));
     R.tok_keys = alloc<uint32_t>(k::embed_bwd_keys(M_));
     R.attn_scratch = alloc<float>(M * hl_ + M * 2 * dl_ + 64);
@@ -1074,13 +1074,20 @@ void Model::backward_replica(std::vector<Rank*>& grp, bool accumulate) {
       const bool delta_ready = gemm_dout(*R, l, W(*R, ls.o_k));
       wgrad(*R, ls.o_k, d, dl, static_cast<int>(M), R->gb, d, R->o[l], dl, acc);
       tic();
+      bool cs_done = false;
       k::attention_bwd(R->qkv[l], R->o[l], R->lse[l], R->dout, R->dqkv, R->attn_scratch, B_, T_, hl_, hd_,
-                       stream_, delta_ready);
+                       stream_, delta_ready, fuse_colsum_ ? R->col_scratch : nullptr, &cs_done);
       toc(kProfAttnBwd, 4.0 * B_ * hl_ * static_cast<double>(T_) * T_ * hd_);
       launches_ += delta_ready ? 2 : 3;
-      k::colsum_bf16(R->dqkv, 3 * dl, M, 3 * dl, dl, G(*R, ls.q_b) + R->mpi * dl, G(*R, ls.k_b) + R->mpi * dl,
-                     G(*R, ls.v_b) + R->mpi * dl, acc, R->col_scratch, stream_);
-      launches_ += 2;
+      if (cs_done) {  // the q|k|v bias gradients' partials came out of the attention backward
+        k::colsum_chunks(R->col_scratch, static_cast<int>((M + 31) / 32), 3 * dl, G(*R, ls.q_b) + R->mpi * dl, acc,
+                         stream_, dl, G(*R, ls.k_b) + R->mpi * dl, G(*R, ls.v_b) + R->mpi * dl);
+        ++launches_;
+      } else {
+        k::colsum_bf16(R->dqkv, 3 * dl, M, 3 * dl, dl, G(*R, ls.q_b) + R->mpi * dl, G(*R, ls.k_b) + R->mpi * dl,
+                       G(*R, ls.v_b) + R->mpi * dl, acc, R->col_scratch, stream_);
+        launches_ += 2;
+      }
     }
     {
       auto prod = [&](Rank& R, int64_t r0, int64_t rows) {

@@ -400,3 +400,29 @@ def test_gptj_width_dp2_tp4_matches_single_device():
         assert rel_l2(b[1][n].astype(np.float64), a[1][n].astype(np.float64)) < 1e-2, n
         # one AdamW step (~lr * sign(g)) from identical weights
         assert np.max(np.abs(b[2][n] - a[2][n])) <= 2.5e-3, n
+
+
+@pytest.mark.parametrize("mp", [1, 2])
+def test_fused_bias_colsums_match_separate_pass(mp, monkeypatch):
+    """The fc1 bias gradient summed in the GeLU-backward GEMM epilogue and the q|k|v bias
+    gradients summed in the attention backward / dQ conversion (per-32-row partials, fixed-order
+    reduction) equal the separate column-sum passes over dpre / dqkv (SW_FUSE_COLSUM=0)."""
+    text = open(os.path.join(SPECS, "llama7b_vocab_parallel.spec")).read().replace("n_layers = 32", "n_layers = 1")
+    spec = rules.parse_model_spec(text)
+    rng = np.random.default_rng(11)
+    tokens = rng.integers(0, spec.vocab_size, (2, 256), dtype=np.int32)
+    targets = rng.integers(0, spec.vocab_size, (2, 256), dtype=np.int32)
+    names = ("block_0/attn/q/bias", "block_0/attn/k/bias", "block_0/attn/v/bias", "block_0/mlp/fc1/bias")
+    res = {}
+    for fuse in ("0", "1"):
+        monkeypatch.setenv("SW_FUSE_COLSUM", fuse)
+        model, mesh, plan = make(spec, 1, mp, 2, 256)
+        model.init_params(42, "model-init")
+        model.stage_batch(tokens, targets, None)
+        model.forward_backward()
+        res[fuse] = {n: model.get_grad(n).astype(np.float64) for n in names}
+        model.close()
+        mesh.close()
+    for n in names:
+        assert np.abs(res["0"][n]).max() > 0, n
+        assert rel_l2(res["1"][n], res["0"][n]) < 1e-4, n
