@@ -86,6 +86,12 @@ Model::Model(const ModelSpec& spec, const Plan& plan, Mesh* mesh, int batch, int
     const int c = std::atoi(e);
     if (c >= 1 && M_ % c == 0) ar_chunks_ = c;
   }
+  {
+    const char* e = std::getenv("SW_WGRAD_STREAM");
+    if (e == nullptr || e[0] != '0') {
+      cuda_check(cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking), "cudaStreamCreate");
+    }
+  }
   for (int i = 0; i < ar_chunks_; ++i) {
     cudaEvent_t a, b;
     cuda_check(cudaEventCreateWithFlags(&a, cudaEventDisableTiming), "cudaEventCreate");
@@ -98,6 +104,9 @@ Model::Model(const ModelSpec& spec, const Plan& plan, Mesh* mesh, int batch, int
 Model::~Model() {
   if (stream_) cudaStreamSynchronize(stream_);
   if (comm_stream_) cudaStreamSynchronize(comm_stream_);
+  if (side_) cudaStreamSynchronize(side_);
+  for (cudaEvent_t e : side_ev_) cudaEventDestroy(e);
+  if (side_) cudaStreamDestroy(side_);
   for (cudaEvent_t e : events_) cudaEventDestroy(e);
   for (cudaEvent_t e : ev_prod_) cudaEventDestroy(e);
   for (cudaEvent_t e : ev_ar_) cudaEventDestroy(e);
@@ -927,6 +936,33 @@ void Model::wgrad(Rank& R, int slot, int M, int N, int K, const void* A, int64_t
   ++launches_;
 }
 
+cudaEvent_t Model::on_side(const std::function<void()>& f) {
+  if (side_ == nullptr || prof_) {  // profiling times every launch on stream_
+    f();
+    return nullptr;
+  }
+  // every wait on these events is enqueued within the same backward (it ends joined), so the
+  // pool restarts at 0 each backward without re-recording an event that still has a wait due
+  while (side_ev_.size() < side_next_ + 2) {
+    cudaEvent_t e;
+    cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+    side_ev_.push_back(e);
+  }
+  cudaEvent_t fork = side_ev_[side_next_++];
+  cuda_check(cudaEventRecord(fork, stream_), "cudaEventRecord");
+  cuda_check(cudaStreamWaitEvent(side_, fork, 0), "cudaStreamWaitEvent");
+  std::swap(stream_, side_);
+  f();
+  std::swap(stream_, side_);
+  cudaEvent_t done = side_ev_[side_next_++];
+  cuda_check(cudaEventRecord(done, side_), "cudaEventRecord");
+  return done;
+}
+
+void Model::main_wait(cudaEvent_t e) {
+  if (e != nullptr) cuda_check(cudaStreamWaitEvent(stream_, e, 0), "cudaStreamWaitEvent");
+}
+
 void Model::backward_replica(std::vector<Rank*>& grp, bool accumulate) {
   const int64_t M = M_;
   const int d = d_, dl = dl_, fl = fl_;
@@ -993,16 +1029,23 @@ void Model::backward_replica(std::vector<Rank*>& grp, bool accumulate) {
       for (Rank* R : grp) cons(*R, 0, M);
     }
   }
-  for (Rank* R : grp) {
-    // dW_head (+)= dlogits^T . final_h
-    wgrad(*R, head, vl_, d, static_cast<int>(M), R->logits, ldv_, R->f, d, acc);
-  }
+  // side-stream events: a wgrad's inputs may be overwritten only after its event
+  side_next_ = 0;
+  cudaEvent_t ev_last = on_side([&] {
+    for (Rank* R : grp) {
+      // dW_head (+)= dlogits^T . final_h
+      wgrad(*R, head, vl_, d, static_cast<int>(M), R->logits, ldv_, R->f, d, acc);
+    }
+  });
+  cudaEvent_t ev_fc1 = nullptr, ev_qkv = nullptr;
   for (int l = L_ - 1; l >= 0; --l) {
     const LayerSlots& ls = layers_[l];
+    main_wait(ev_fc1);  // the previous layer's fc1 wgrad has read dpre
     // ---- MLP ----
     // SwiGLU: dpre = d(gate) | d(up) [M, 2*fl] against the fused [gate; up] weight at gate_k
     const int fw = spec_.swiglu ? 2 * fl : fl;
     const int fk = spec_.swiglu ? ls.gate_k : ls.fc1_k;
+    cudaEvent_t ev_fc2 = nullptr, ev_o = nullptr;
     for (Rank* R : grp) {
       bool cs_done = false;
       if (spec_.swiglu) {
@@ -1028,7 +1071,7 @@ void Model::backward_replica(std::vector<Rank*>& grp, bool accumulate) {
           cs_done = true;
         }
       }
-      wgrad(*R, ls.fc2_k, d, fl, static_cast<int>(M), R->gb, d, R->act[l], fl, acc);
+      ev_fc2 = on_side([&] { wgrad(*R, ls.fc2_k, d, fl, static_cast<int>(M), R->gb, d, R->act[l], fl, acc); });
       if (ls.fc1_b >= 0 && !cs_done) {
         k::colsum_bf16(R->dpre, fl, M, fl, 0, G(*R, ls.fc1_b) + R->mpi * fl, nullptr, nullptr, acc,
                        R->col_scratch, stream_);
@@ -1041,6 +1084,7 @@ void Model::backward_replica(std::vector<Rank*>& grp, bool accumulate) {
              static_cast<int>(Epi::kStoreF32), R.dx + r0 * d, d);
       };
       auto cons = [&](Rank& R, int64_t r0, int64_t rows) {
+        main_wait(ev_fc2);  // the fc2 wgrad has read gb
         tic();
         k::layernorm_bwd(R.hmid[l] + r0 * d, R.stats2[l] + r0, R.stats2[l] + M + r0, P(R, ls.ln2_s), R.dx + r0 * d,
                          R.gres + r0 * d, R.gb + r0 * d, G(R, ls.ln2_s), Gn(R, ls.ln2_b), rows, d, 1, stream_,
@@ -1051,6 +1095,7 @@ void Model::backward_replica(std::vector<Rank*>& grp, bool accumulate) {
       if (tm_ > 1) {
         row_ar(grp, &Rank::dx, [&](Rank& R) -> const bf16* { return R.dpre; }, fw, fw, fk, 1,
                [&](Rank& R, int64_t r0, int64_t rows, const float* f32, const bf16* b16) {
+                 main_wait(ev_fc2);
                  tic();
                  if (b16 != nullptr)
                    k::layernorm_bwd(R.hmid[l] + r0 * d, R.stats2[l] + r0, R.stats2[l] + M + r0, P(R, ls.ln2_s), b16,
@@ -1068,11 +1113,14 @@ void Model::backward_replica(std::vector<Rank*>& grp, bool accumulate) {
         for (Rank* R : grp) cons(*R, 0, M);
       }
     }
-    for (Rank* R : grp) wgrad(*R, fk, fw, d, static_cast<int>(M), R->dpre, fw, R->a2[l], d, acc);
+    ev_fc1 = on_side([&] {
+      for (Rank* R : grp) wgrad(*R, fk, fw, d, static_cast<int>(M), R->dpre, fw, R->a2[l], d, acc);
+    });
     // ---- attention ----
     for (Rank* R : grp) {
       const bool delta_ready = gemm_dout(*R, l, W(*R, ls.o_k));
-      wgrad(*R, ls.o_k, d, dl, static_cast<int>(M), R->gb, d, R->o[l], dl, acc);
+      ev_o = on_side([&] { wgrad(*R, ls.o_k, d, dl, static_cast<int>(M), R->gb, d, R->o[l], dl, acc); });
+      main_wait(ev_qkv);  // the previous layer's QKV wgrad has read dqkv
       tic();
       bool cs_done = false;
       k::attention_bwd(R->qkv[l], R->o[l], R->lse[l], R->dout, R->dqkv, R->attn_scratch, B_, T_, hl_, hd_,
@@ -1095,6 +1143,7 @@ void Model::backward_replica(std::vector<Rank*>& grp, bool accumulate) {
              static_cast<int>(Epi::kStoreF32), R.dx + r0 * d, d);
       };
       auto cons = [&](Rank& R, int64_t r0, int64_t rows) {
+        main_wait(ev_o);  // the O-projection wgrad has read gb
         tic();
         k::layernorm_bwd(R.hs[l] + r0 * d, R.stats1[l] + r0, R.stats1[l] + M + r0, P(R, ls.ln1_s), R.dx + r0 * d,
                          R.gres + r0 * d, R.gb + r0 * d, G(R, ls.ln1_s), Gn(R, ls.ln1_b), rows, d, 1, stream_,
@@ -1105,6 +1154,7 @@ void Model::backward_replica(std::vector<Rank*>& grp, bool accumulate) {
       if (ta_ > 1) {
         row_ar(grp, &Rank::dx, [&](Rank& R) -> const bf16* { return R.dqkv; }, 3 * dl, 3 * dl, ls.q_k, 1,
                [&](Rank& R, int64_t r0, int64_t rows, const float* f32, const bf16* b16) {
+                 main_wait(ev_o);
                  tic();
                  if (b16 != nullptr)
                    k::layernorm_bwd(R.hs[l] + r0 * d, R.stats1[l] + r0, R.stats1[l] + M + r0, P(R, ls.ln1_s), b16,
@@ -1122,8 +1172,12 @@ void Model::backward_replica(std::vector<Rank*>& grp, bool accumulate) {
         for (Rank* R : grp) cons(*R, 0, M);
       }
     }
-    for (Rank* R : grp) wgrad(*R, ls.q_k, 3 * dl, d, static_cast<int>(M), R->dqkv, 3 * dl, R->a1[l], d, acc);
+    ev_qkv = on_side([&] {
+      for (Rank* R : grp) wgrad(*R, ls.q_k, 3 * dl, d, static_cast<int>(M), R->dqkv, 3 * dl, R->a1[l], d, acc);
+    });
+    ev_last = ev_qkv;
   }
+  main_wait(ev_last);  // every wgrad (and its fused AdamW) done before anything downstream
   for (Rank* R : grp) {
     k::embed_bwd_pos(R->gres, G(*R, pos_), B_, T_, d, acc, stream_);
     k::embed_bwd_tok(R->tokens, R->gres, G(*R, tok_), M, d, spec_.vocab_size, R->tok_keys, stream_);

@@ -196,6 +196,14 @@ class Model {
   std::vector<void*> allocations_;
   cudaStream_t stream_ = nullptr;
   cudaStream_t comm_stream_ = nullptr;
+  // Weight-gradient GEMMs run on side_ (SW_WGRAD_STREAM=0: on stream_), forked after their
+  // inputs are written and joined before those inputs are overwritten, so a wgrad's last
+  // partial wave of tiles shares the SMs with the next dgrad / attention kernel.
+  cudaStream_t side_ = nullptr;
+  std::vector<cudaEvent_t> side_ev_;  // grows on demand; reused from index 0 every backward
+  size_t side_next_ = 0;
+  cudaEvent_t on_side(const std::function<void()>& f);
+  void main_wait(cudaEvent_t e);
   std::vector<cudaEvent_t> ev_prod_, ev_ar_;
   int ar_chunks_ = 1;
   // Row-parallel all-reduce payloads in bf16 (opt-in, SW_AR_BF16=1): half the NVLink bytes of
