@@ -1,5 +1,2 @@
-timeout 900 python -m pytest tests -m gpu -q -x > gpurun_out/t.log 2>&1; echo EXIT $? >> gpurun_out/t.log
-for i in 1 2 3; do for lib in variants/libsw_prev.so paper_2310_16355_b200/libshardweave_b200.so; do
-SW_LIB_PATH=$lib timeout 400 python bench.py --no-cpu-baseline --steps 8 > gpurun_out/b.log 2>&1
-echo "$lib $(python3 -c "import json; d=json.loads(open('gpurun_out/b.log').read().strip().splitlines()[-1]); print(round(d['value']), round(d['ms_per_step'],2), d['clocks']['sm_mhz'], round(d['e2e']['value']))")"
-done; done > gpurun_out/ab.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:gemm_bf16_2sm_kernel -c 1 -o gpurun_out/gemm_qkv_s3 python tools/one_gemm.py 8192 12288 4096 0 0 0 > gpurun_out/ncu_qkv.log 2>&1
+timeout 900 ncu --set full --clock-control none -k regex:gemm_bf16_2sm_kernel -c 1 -o gpurun_out/gemm_adamw_s3 python tools/one_gemm_adamw.py > gpurun_out/ncu_adamw.log 2>&1
