@@ -33,6 +33,9 @@ constexpr int NUM_THREADS = 256;
 #ifndef SW_EXP_NO_STATE_STORE
 #define SW_EXP_NO_STATE_STORE 0
 #endif
+#ifndef SW_EXP_NO_STATE_LOAD
+#define SW_EXP_NO_STATE_LOAD 0
+#endif
 #ifndef SW_EXP_NO_SHADOW_STORE
 #define SW_EXP_NO_SHADOW_STORE 0
 #endif
@@ -798,6 +801,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(p_threads<EPI>(), 1)
             const int buf = c & 1;
             dev::mbar_wait(&oempty[buf], (uses[buf] & 1) ^ 1);
             ++uses[buf];
+#if SW_EXP_NO_STATE_LOAD  // timing experiment only (results invalid when set)
+            dev::mbar_arrive(&ofull[buf]);
+            continue;
+#endif
             dev::mbar_arrive_expect_tx(&ofull[buf], OPT_BUF);
             uint8_t* dst = sOpt + buf * OPT_BUF;
             const int c0 = nb * BN + c * OC;
