@@ -1,2 +1,3 @@
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:gemm_bf16_2sm_kernel -c 1 -o gpurun_out/gemm_qkv_s3 python tools/one_gemm.py 8192 12288 4096 0 0 0 > gpurun_out/ncu_qkv.log 2>&1
-timeout 900 ncu --set full --clock-control none -k regex:gemm_bf16_2sm_kernel -c 1 -o gpurun_out/gemm_adamw_s3 python tools/one_gemm_adamw.py > gpurun_out/ncu_adamw.log 2>&1
+for i in 1 2; do for lib in paper_2310_16355_b200/libshardweave_b200.so variants/libsw_noload.so variants/libsw_nostore.so variants/libsw_noboth.so; do
+echo "$lib $(SW_LIB_PATH=$lib python -c 'import sys; sys.path.insert(0,"."); from tools.gemm_bench import bench_adamw; print(bench_adamw(12288,4096,8192,iters=10))' 2>&1 | tail -1)"
+done; done > gpurun_out/adamw_exp.log 2>&1
