@@ -1,3 +1,4 @@
-for i in 1 2; do for lib in paper_2310_16355_b200/libshardweave_b200.so variants/libsw_noload.so variants/libsw_nostore.so variants/libsw_noboth.so; do
-echo "$lib $(SW_LIB_PATH=$lib python -c 'import sys; sys.path.insert(0,"."); from tools.gemm_bench import bench_adamw; print(bench_adamw(12288,4096,8192,iters=10))' 2>&1 | tail -1)"
-done; done > gpurun_out/adamw_exp.log 2>&1
+timeout 900 python -m pytest tests -m gpu -q > gpurun_out/t.log 2>&1; echo EXIT $? >> gpurun_out/t.log
+python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_out/smoke.log 2>&1
+python bench.py > gpurun_out/bench_end.json 2> gpurun_out/bench_end.err
+python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref_end.json 2>&1
