@@ -24,7 +24,8 @@ enum class Epi : int {
   kGeluBwd = 4,     // C(bf16) = acc * gelu'(aux(bf16))    (fc2 dgrad fused with GeLU backward)
   kAdamW = 5,       // wgrad with the optimizer in the epilogue: acc is the fp32 gradient of the
                     // [M, N] weight at adam_* (row pitch ldc); AdamW updates p/m/v in place and
-                    // refreshes the bf16 shadow; non-finite gradients set *adam_flag
+                    // refreshes the bf16 shadow; non-finite gradients set *adam_flag, and a
+                    // non-zero *adam_flag on entry to a chunk gates its update (state unchanged)
   // SwiGLU extension. kSwiGLU: B = fused [gate; up] weight [2*N, K] (up rows start at
   // swiglu_half = N); each 256-wide tile multiplies 128 gate rows and the matching 128 up rows,
   // the epilogue writes h = silu(g) * u to C [M, N] and the pre-activations g | u to C2 [M, 2N].

@@ -77,6 +77,8 @@ __device__ __forceinline__ void tile_coords(int t, int num_m, int num_n, int& mb
 // AdamW update of train_state.hpp:214-216 is applied in place. The gradient never reaches HBM.
 __device__ __forceinline__ void adamw_chunk(const GemmParams& p, float4* stage, int row0, int col0, int ncols,
                                             const uint32_t (&r)[32], uint32_t lane) {
+  // a non-finite loss (or an earlier non-finite gradient) gates the update: nothing is written
+  if (__ldcg(p.adam_flag) != 0) return;
 #pragma unroll
   for (int c = 0; c < 8; ++c) {
     stage[lane * 8 + (c ^ (lane & 7))] =
@@ -578,6 +580,9 @@ __device__ __forceinline__ void adamw_chunk_smem(const GemmParams& p, float* sbo
   bool bad = false;
   uint32_t slow = 0;
   float4 pv[OC / 4];
+  // a non-finite loss (or an earlier non-finite gradient) gates the update: the staged p/m/v
+  // go back unchanged (the caller's TMA store rewrites the same bytes) and the shadow is kept
+  if (__ldcg(p.adam_flag) != 0) return;
 #pragma unroll
   for (int c = 0; c < OC / 4; ++c) {
     const int at = opt_pos(L, c);

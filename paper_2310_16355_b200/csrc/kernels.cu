@@ -658,7 +658,7 @@ __global__ void sum_f32_kernel(const float* __restrict__ x, int64_t n, float* ou
 }
 
 __global__ void loss_reduce_kernel(const float* __restrict__ wl, int64_t n, const float* wsum,
-                                   double* loss) {
+                                   double* loss, int* gate) {
   __shared__ double red[32];
   double s = 0.0;
   for (int64_t i = threadIdx.x; i < n; i += blockDim.x) s += wl[i];
@@ -669,7 +669,9 @@ __global__ void loss_reduce_kernel(const float* __restrict__ wl, int64_t n, cons
   if (threadIdx.x == 0) {
     double t = 0.0;
     for (int w = 0; w < (blockDim.x + 31) / 32; ++w) t += red[w];
-    *loss = t / static_cast<double>(*wsum);
+    const double l = t / static_cast<double>(*wsum);
+    *loss = l;
+    if (gate != nullptr && !isfinite(l)) atomicOr(gate, 2);
   }
 }
 
@@ -1153,8 +1155,8 @@ void xent_vp_grad(bf16* logits, int64_t ld, int64_t M, int Vl, int v0, const int
   xent_vp_grad_kernel<<<static_cast<unsigned>(M), 512, 0, s>>>(logits, ld, Vl, v0, targets, lse, weights, wsum);
 }
 
-void loss_reduce(const float* wloss, int64_t M, const float* wsum, double* loss, cudaStream_t s) {
-  loss_reduce_kernel<<<1, 1024, 0, s>>>(wloss, M, wsum, loss);
+void loss_reduce(const float* wloss, int64_t M, const float* wsum, double* loss, cudaStream_t s, int* gate) {
+  loss_reduce_kernel<<<1, 1024, 0, s>>>(wloss, M, wsum, loss, gate);
 }
 
 void add_residual_bias(const float* a, const float* b, const float* bias, float* y, int64_t M,

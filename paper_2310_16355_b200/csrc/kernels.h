@@ -85,7 +85,10 @@ void xent_vp_combine(const float* stats_all, int t, int64_t M, const float* tlog
 void xent_vp_grad(bf16* logits, int64_t ld, int64_t M, int Vl, int v0, const int32_t* targets, const float* lse,
                   const float* weights, const float* wsum, cudaStream_t s);
 // loss[0] = sum(wloss) / wsum (double)
-void loss_reduce(const float* wloss, int64_t M, const float* wsum, double* loss, cudaStream_t s);
+// loss = sum(wloss) / wsum; a non-finite loss ORs 2 into *gate (when given): the fused
+// optimizer epilogues of the following backward then leave the state untouched
+void loss_reduce(const float* wloss, int64_t M, const float* wsum, double* loss, cudaStream_t s,
+                 int* gate = nullptr);
 
 // Causal scaled-dot-product attention on the head-sharded QKV activations:
 // qkv [M, 3*Dl] (q | k | v, head h at column h*hd), o [M, Dl], lse [B, Hl, T]

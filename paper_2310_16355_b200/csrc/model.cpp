@@ -390,6 +390,7 @@ void Model::init_params(uint64_t seed, const std::string& stream_name) {
   }
   step_ = 0;
   seed_ = seed;
+  poisoned_ = false;
   cuda_check(cudaGetLastError(), "init_params");
 }
 
@@ -429,6 +430,7 @@ void Model::set_tensor(const std::string& name, int which, const float* full, in
 }
 
 void Model::save_checkpoint(const std::string& path, const std::vector<CkptRng>& rngs) {
+  check_not_poisoned("save_checkpoint");
   Checkpoint ck;
   ck.step = step_;
   ck.seed = seed_;
@@ -482,6 +484,7 @@ void Model::load_checkpoint(const std::string& path) {
   step_ = ck.step;
   seed_ = ck.seed;
   loaded_rngs_ = std::move(ck.rngs);
+  poisoned_ = false;
 }
 
 void Model::get_tensor(const std::string& name, int which, float* full, int64_t numel) {
@@ -886,7 +889,7 @@ void Model::forward_replica(std::vector<Rank*>& grp, bool need_grad) {
     }
   }
   for (Rank* R : grp) {
-    k::loss_reduce(R->wloss, M, R->wsum, R->loss, stream_);
+    k::loss_reduce(R->wloss, M, R->wsum, R->loss, stream_, fused_ != nullptr ? d_flag_ : nullptr);
     ++launches_;
   }
 }
@@ -949,12 +952,27 @@ cudaEvent_t Model::on_side(const std::function<void()>& f) {
     side_ev_.push_back(e);
   }
   cudaEvent_t fork = side_ev_[side_next_++];
+  cudaEvent_t done = side_ev_[side_next_++];
   cuda_check(cudaEventRecord(fork, stream_), "cudaEventRecord");
   cuda_check(cudaStreamWaitEvent(side_, fork, 0), "cudaStreamWaitEvent");
-  std::swap(stream_, side_);
-  f();
-  std::swap(stream_, side_);
-  cudaEvent_t done = side_ev_[side_next_++];
+  // f() launches on stream_ (swapped with side_); the guard swaps them back even when f()
+  // throws (a GEMM shape error, a launch failure) and then joins the side stream, so stream()
+  // stays the model stream and no fork is left dangling
+  struct Swap {
+    Model* m;
+    cudaEvent_t done;
+    bool ok;
+    ~Swap() {
+      std::swap(m->stream_, m->side_);
+      if (!ok && cudaEventRecord(done, m->side_) == cudaSuccess) cudaStreamWaitEvent(m->stream_, done, 0);
+    }
+  };
+  {
+    Swap guard{this, done, false};
+    std::swap(stream_, side_);
+    f();
+    guard.ok = true;
+  }
   cuda_check(cudaEventRecord(done, side_), "cudaEventRecord");
   return done;
 }
@@ -1196,6 +1214,7 @@ void Model::backward_replica(std::vector<Rank*>& grp, bool accumulate) {
 }
 
 void Model::forward_backward(bool accumulate) {
+  check_not_poisoned("forward_backward");
   cuda_check(cudaSetDevice(mesh_->cuda_device), "cudaSetDevice");
   launches_ = 0;
   const int first = mesh_->emulated ? 0 : ranks_[0].dpi;
@@ -1246,6 +1265,7 @@ void Model::dp_sync() {
 }
 
 void Model::adamw(double lr, double b1, double b2, double eps, double wd, bool check_finite) {
+  check_not_poisoned("adamw_step");
   if (check_finite) {
     cuda_check(cudaMemsetAsync(d_flag_, 0, sizeof(int), stream_), "memset");
     for (Rank& R : ranks_) {
@@ -1286,7 +1306,15 @@ void Model::adamw(double lr, double b1, double b2, double eps, double wd, bool c
   cuda_check(cudaGetLastError(), "adamw");
 }
 
+void Model::check_not_poisoned(const char* what) const {
+  if (poisoned_) {
+    fail(SW_ERR_NONFINITE, std::string(what) + ": the model state was left half-updated by a non-finite fused "
+                           "optimizer step; call init_params or load_checkpoint first");
+  }
+}
+
 bool Model::train_step(double lr, double b1, double b2, double eps, double wd) {
+  check_not_poisoned("train_step");
   static const bool disabled = [] {
     const char* e = std::getenv("SW_FUSED_ADAMW");
     return e != nullptr && e[0] == '0';
@@ -1325,9 +1353,22 @@ bool Model::train_step(double lr, double b1, double b2, double eps, double wd) {
   int flag = 0;
   cuda_check(cudaMemcpyAsync(&flag, d_flag_, sizeof(int), cudaMemcpyDeviceToHost, stream_), "D2H");
   cuda_check(cudaStreamSynchronize(stream_), "sync");
+  if (flag & 2) {
+    // The loss was non-finite, so every fused epilogue skipped its update (bit 2 was set before
+    // the backward began): the state is exactly as before the step. Redo the step the
+    // reference's way (check every gradient, then update) so the error names the parameter of
+    // train_state.hpp:207-210, or the update goes ahead if the gradients are finite after all.
+    forward_backward(false);
+    adamw(lr, b1, b2, eps, wd, true);
+    return false;
+  }
   if (flag) {
-    fail(SW_ERR_NONFINITE, "adamw_step: non-finite gradient (optimizer fused into the backward: this "
-                           "step's GEMM weights were already updated)");
+    // finite loss, non-finite gradient found inside the backward: the wgrad epilogues that ran
+    // before it was flagged already updated their GEMM weights, so the state is half-updated
+    poisoned_ = true;
+    fail(SW_ERR_NONFINITE, "adamw_step: non-finite gradient (optimizer fused into the backward: some GEMM "
+                           "weights of this step were already updated; the model refuses further steps "
+                           "and checkpoints until init_params or load_checkpoint)");
   }
   for (Rank& R : ranks_) {
     tic();

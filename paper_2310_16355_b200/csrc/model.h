@@ -119,7 +119,13 @@ class Model {
   void adamw(double lr, double b1, double b2, double eps, double wd, bool check_finite);
   // forward_backward + dp_sync + adamw; with dp == 1 the optimizer runs inside the backward
   // (wgrad epilogues). Returns true when the fused path ran.
+  // A non-finite loss gates every fused update (the step is then redone unfused, so the state is
+  // unchanged when NonFiniteError names the parameter, as train_state.hpp:207-210 does). A
+  // non-finite gradient under a finite loss is found only inside the backward, after some
+  // epilogues updated their weights: the model is then poisoned (train_step, forward_backward,
+  // adamw and save_checkpoint refuse) until init_params or load_checkpoint.
   bool train_step(double lr, double b1, double b2, double eps, double wd);
+  bool poisoned() const { return poisoned_; }
   double last_loss();
   void logits_to_host(float* out);
 
@@ -132,6 +138,7 @@ class Model {
   int64_t device_bytes() const { return bytes_; }
 
  private:
+  void check_not_poisoned(const char* what) const;
   template <typename T>
   T* alloc(int64_t n);
   void build_layout();
@@ -224,6 +231,7 @@ class Model {
   std::vector<std::string> prof_tag_;  // per record: GEMM shape / epilogue (SW_PROFILE_LOG dump)
   int64_t bytes_ = 0;
   uint64_t step_ = 0;
+  bool poisoned_ = false;
   uint64_t seed_ = 0;
   struct DecodeBufs {
     float *x = nullptr, *xmid = nullptr, *part = nullptr, *stats = nullptr, *arg = nullptr;

@@ -77,3 +77,30 @@ def test_round_trip_synthetic(tmp_path):
     assert (back.step, back.seed, back.rngs) == (7, 11, snap.rngs)
     for (n1, a1), (n2, a2) in zip(snap.records, back.records):
         assert n1 == n2 and a1.shape == a2.shape and np.array_equal(a1.view(np.uint32), a2.view(np.uint32))
+
+
+def test_wrapping_dims_are_rejected(tmp_path):
+    """dims whose product wraps 2^64 (here 2^32 x 2^32 -> 0) must not pass the truncation guard
+    with a shape that does not match the data (overflow-checked numel)."""
+    import struct
+    snap = checkpoint.Snapshot(step=1, seed=2, rngs=[])
+    for k in ("params", "adam_m", "adam_v"):
+        snap.records.append((f"{k}/w", np.arange(15, dtype=np.float32).reshape(3, 5)))
+    p = str(tmp_path / "w.swck")
+    checkpoint.write(p, snap)
+    raw = open(p, "rb").read()
+    dims = struct.pack("<IQQ", 2, 3, 5)
+    assert raw.count(dims) == 3
+    bad = raw.replace(dims, struct.pack("<IQQ", 2, 1 << 32, 1 << 32), 1)
+    q = str(tmp_path / "bad.swck")
+    open(q, "wb").write(bad)
+    with pytest.raises(_lib.CheckpointError) as e:
+        checkpoint.read(q)
+    assert e.value.message.startswith("checkpoint: truncated, needed 4 more bytes")
+    # an empty tensor with a huge leading dim is still a valid (empty) record
+    empty = raw.replace(dims + np.arange(15, dtype=np.float32).tobytes(),
+                        struct.pack("<IQQ", 2, 1 << 40, 0))
+    q2 = str(tmp_path / "empty.swck")
+    open(q2, "wb").write(empty)
+    back = checkpoint.read(q2)
+    assert [a.shape for _, a in back.records] == [(1 << 40, 0)] * 3

@@ -165,6 +165,28 @@ def test_gemm_adamw_epilogue_flags_nonfinite():
     assert int(flag.item()) == 1
 
 
+@pytest.mark.parametrize("M,N,K", [(256, 256, 128), (1024, 4096, 2048)])
+def test_gemm_adamw_epilogue_gated_by_flag(M, N, K):
+    """A non-zero flag on entry (set by the loss reduction when the loss is non-finite) gates
+    every chunk's update: p, m, v and the shadow keep their bytes."""
+    L = _lib.lib()
+    gen = torch.Generator(device=DEV).manual_seed(M + K)
+    A, B, _ = _ref_operands(M, N, K, 1, 1, gen)
+    p = torch.randn(M, N, generator=gen, device=DEV)
+    m = torch.randn(M, N, generator=gen, device=DEV) * 1e-3
+    v = torch.rand(M, N, generator=gen, device=DEV) * 1e-4
+    sh = p.bfloat16()
+    before = [t.clone() for t in (p, m, v, sh)]
+    flag = torch.full((1,), 2, device=DEV, dtype=torch.int32)
+    _lib.check(L.sw_k_gemm_bf16_adamw(M, N, K, A.data_ptr(), A.stride(0), 1, B.data_ptr(), B.stride(0), 1,
+                                      p.data_ptr(), m.data_ptr(), v.data_ptr(), sh.data_ptr(), N, flag.data_ptr(),
+                                      1e-3, 0.9, 0.999, 1e-8, 0.01, 0.1, 0.001, None))
+    torch.cuda.synchronize()
+    assert int(flag.item()) == 2
+    for a, b in zip((p, m, v, sh), before):
+        assert torch.equal(a, b)
+
+
 @pytest.mark.parametrize("M,N,K", [(256, 128, 64), (300, 200, 136), (1000, 1376, 512), (512, 688, 4096)])
 def test_gemm_swiglu_fwd_bwd(M, N, K):
     """SwiGLU extension vs torch fp32 on the same bf16 operands: the fused [gate; up]

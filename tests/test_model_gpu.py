@@ -317,8 +317,22 @@ def test_fused_optimizer_nonfinite_raises():
     model.set_param("block_0/ln1/scale", bad)
     tokens, targets, weights = rng_ref.audit_batch(42, 0, 2, 16, spec.vocab_size)
     model.stage_batch(tokens, targets, weights)
-    with pytest.raises(engine._lib.NonFiniteError, match="non-finite gradient"):
+    state = {n: [model.get_param(n), *model.get_adam(n)] for n in model.shapes}
+    with pytest.raises(engine._lib.NonFiniteError, match="non-finite gradient for parameter"):
         model.train_step(engine.AdamWConfig())
+    # the non-finite loss gated every fused update: nothing moved (train_state.hpp:207-210)
+    for n, (p, m, v) in state.items():
+        assert np.array_equal(model.get_param(n), p, equal_nan=True), n
+        m2, v2 = model.get_adam(n)
+        assert np.array_equal(m2, m) and np.array_equal(v2, v), n
+    # the model is not poisoned: repair the parameter and the fused step goes ahead
+    good = model.get_param("block_0/ln1/scale")
+    good[3] = 1.0
+    model.set_param("block_0/ln1/scale", good)
+    model.stage_batch(tokens, targets, weights)
+    model.train_step(engine.AdamWConfig())
+    assert np.isfinite(model.loss())
+    assert not np.array_equal(model.get_param("block_0/mlp/fc1/kernel"), state["block_0/mlp/fc1/kernel"][0])
 
 
 def test_replicated_param_grads_are_deterministic():
@@ -426,3 +440,50 @@ def test_fused_bias_colsums_match_separate_pass(mp, monkeypatch):
     for n in names:
         assert np.abs(res["0"][n]).max() > 0, n
         assert rel_l2(res["1"][n], res["0"][n]) < 1e-4, n
+
+
+@pytest.mark.parametrize("mp", [1, 2])
+def test_side_stream_wgrads_match_single_stream(mp, monkeypatch):
+    """The weight-gradient GEMMs on the side stream (default) against the single-stream schedule
+    (SW_WGRAD_STREAM=0) at a size where the wgrads overlap the following dgrad / attention
+    kernels (2 layers, M = 2048 tokens): forward_backward gradients and the parameters after a
+    fused train_step. A missing join before gb / dpre / dqkv is rewritten would read a later
+    layer's values (O(1) relative error). The wgrad GEMMs are deterministic, but the attention
+    backward's dQ reduce-add is not, so the bound is its rounding noise: every gradient within
+    1e-5 rel-L2, and after one AdamW step (~lr * sign(g): an element whose gradient is at the
+    noise level may flip sign) at most 1% of a weight's elements differ, none by more than 2*lr."""
+    text = open(os.path.join(SPECS, "llama7b.spec")).read()
+    for a, b in (("n_layers = 32", "n_layers = 2"), ("d_model = 4096", "d_model = 1024"),
+                 ("n_heads = 32", "n_heads = 8"), ("d_ff = 11008", "d_ff = 2752"), ("vocab_size = 32000", "vocab_size = 4096")):
+        assert a in text
+        text = text.replace(a, b)
+    spec = rules.parse_model_spec(text)
+    rng = np.random.default_rng(3)
+    tokens = rng.integers(0, spec.vocab_size, (2, 1024), dtype=np.int32)
+    targets = rng.integers(0, spec.vocab_size, (2, 1024), dtype=np.int32)
+    names = [n for n, _ in rules.transformer_param_shapes(spec)]
+    cfg = engine.AdamWConfig(lr=1e-3, weight_decay=0.01)
+    res = {}
+    for side in ("0", "1"):
+        monkeypatch.setenv("SW_WGRAD_STREAM", side)
+        model, mesh, _ = make(spec, 1, mp, 2, 1024)
+        model.init_params(42, "model-init")
+        model.stage_batch(tokens, targets, None)
+        model.forward_backward()
+        grads = {n: model.get_grad(n).astype(np.float64) for n in names}
+        model.stage_batch(tokens, targets, None)
+        model.train_step(cfg)
+        params = {n: model.get_param(n) for n in names}
+        res[side] = (grads, params, model.loss())
+        model.close()
+        mesh.close()
+    for n in names:
+        if n.endswith("attn/k/bias"):  # analytically zero gradient
+            assert max_rel(res["1"][0][n], res["0"][0][n]) < 1e-6, n
+        else:
+            assert rel_l2(res["1"][0][n], res["0"][0][n]) < 1e-5, n
+        a, b = res["1"][1][n], res["0"][1][n]
+        d = np.abs(a - b)
+        assert (d > 1e-6 + 1e-5 * np.abs(b)).mean() <= 1e-2 or n.endswith("attn/k/bias"), n
+        assert d.max() <= 2 * cfg.lr * (1 + 1e-3) + 1e-6, (n, float(d.max()))
+    assert abs(res["0"][2] - res["1"][2]) <= 1e-6 * abs(res["0"][2])
