@@ -19,6 +19,7 @@
 //   to an fp32 dQ accumulator in HBM with vector reductions.
 // Every smem tile is a [rows x 64-column] SWIZZLE_128B chunk array, usable both as a K-major
 // and as an MN-major UMMA operand, so no tile is ever transposed.
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 
@@ -30,6 +31,10 @@ namespace sw {
 namespace k {
 
 namespace {
+
+#ifndef SW_EXP_POLY
+#define SW_EXP_POLY 0  // forward softmax: pairs (of every 8) whose exp2 runs as an FMA polynomial
+#endif
 
 constexpr int BQ = 128;
 constexpr int BKV = 128;
@@ -388,10 +393,22 @@ struct Fwd2Layout {
   static constexpr int BYTES = OFF_BAR + 256;
 };
 
+// Item order of the persistent kernels: the work list (heaviest first, work_item) is dealt to
+// the P resident CTAs in snake order (round r: CTA c takes position c, or P-1-c on odd rounds),
+// so each CTA's summed work stays close to the mean without a dynamic scheduler.
+__device__ __forceinline__ int snake_item(int round, int c, int P) {
+  return round * P + ((round & 1) ? P - 1 - c : c);
+}
+
+// Persistent: a CTA walks its items (snake_item) and keeps the pipeline full across them -- the
+// K/V ring runs on without a break, the next item's Q_t is loaded as soon as tile t's last
+// S = Q K^T has executed (q_empty), and a softmax warpgroup writes its O while the tensor core
+// already runs the next item's first S. Barrier phases count blocks / items per CTA, not per
+// item. With gridDim.x == the item count every CTA takes one item (the non-persistent launch).
 __global__ void __launch_bounds__(384, 1)
     attn_fwd_tc2(const __grid_constant__ CUtensorMap tm, bf16* __restrict__ out, float* __restrict__ lse, int T,
                  int Hl, float scale_log2, float scale, int nbh, int group, int causal,
-                 const float* __restrict__ lut) {
+                 const float* __restrict__ lut, int trace_cta) {
   using Lay = Fwd2Layout;
   constexpr int HD = Lay::HD;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -399,38 +416,52 @@ __global__ void __launch_bounds__(384, 1)
   uint8_t* sK = smem + Lay::OFF_K;
   uint8_t* sV = smem + Lay::OFF_V;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Lay::OFF_BAR);
-  uint64_t* q_full = bars + 0;
-  uint64_t* kv_full = bars + 1;   // [2]
-  uint64_t* kv_empty = bars + 3;  // [2]
-  uint64_t* s_full = bars + 5;    // [tile]
-  uint64_t* p_full = bars + 7;    // [tile]
-  uint64_t* pv_done = bars + 9;   // [tile]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
+  uint64_t* q_full = bars + 0;    // [tile]
+  uint64_t* q_empty = bars + 2;   // [tile] the tile's last S of the item has executed
+  uint64_t* kv_full = bars + 4;   // [2]
+  uint64_t* kv_empty = bars + 6;  // [2]
+  uint64_t* s_full = bars + 8;    // [tile]
+  uint64_t* p_full = bars + 10;   // [tile]
+  uint64_t* pv_done = bars + 12;  // [tile]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14);
 
   const int nqb = (T + 127) / 128;
   const int npair = (nqb + 1) / 2;
-  int rank_, bh;
-  work_item(static_cast<int>(blockIdx.x), npair, nbh, group, rank_, bh);
-  const int pi = npair - 1 - rank_;  // heaviest pair first
-  const int b = bh / Hl, h = bh % Hl;
+  const int nitems = npair * nbh;
   const int Dl = Hl * HD;
-  const int row0 = b * T;
-  const int qa = 2 * pi;
-  const bool hasB = qa + 1 < nqb;
-  // causal: key blocks up to the diagonal; otherwise (T5 encoder / cross) every key block
-  const int nkv_t[2] = {causal ? qa + 1 : nqb, hasB ? (causal ? qa + 2 : nqb) : 0};
-  const int nkv = causal ? (hasB ? qa + 2 : qa + 1) : nqb;
   // additive relative-position bias (T5): lut[h][key - query + T - 1] in natural units, row
   // pitch 2T + 128; the scores are then scale * s + bias and the exp2 runs in log2(e) units
   const float sl_eff = lut ? 1.4426950408889634f : scale_log2;
   const float sc_eff = lut ? 1.f : scale;
+  // the item's geometry: pair index, (batch, head), and the key blocks of each query tile
+  struct Item {
+    int bh, h, row0, qa, nkv, nkv_t[2];
+    bool hasB;
+  };
+  auto item_of = [&](int idx) {
+    Item it;
+    int rank_;
+    work_item(idx, npair, nbh, group, rank_, it.bh);
+    const int pi = npair - 1 - rank_;  // heaviest pair first
+    it.h = it.bh % Hl;
+    it.row0 = (it.bh / Hl) * T;
+    it.qa = 2 * pi;
+    it.hasB = it.qa + 1 < nqb;
+    // causal: key blocks up to the diagonal; otherwise (T5 encoder / cross) every key block
+    it.nkv_t[0] = causal ? it.qa + 1 : nqb;
+    it.nkv_t[1] = it.hasB ? (causal ? it.qa + 2 : nqb) : 0;
+    it.nkv = causal ? (it.hasB ? it.qa + 2 : it.qa + 1) : nqb;
+    return it;
+  };
+  const int P = static_cast<int>(gridDim.x), cta = static_cast<int>(blockIdx.x);
 
   const uint32_t warp = dev::warp_idx_sync();
   const uint32_t lane = threadIdx.x & 31;
   if (warp == 0 && lane == 0) {
     dev::tma_prefetch_desc(&tm);
-    dev::mbar_init(q_full, 1);
     for (int i = 0; i < 2; ++i) {
+      dev::mbar_init(&q_full[i], 1);
+      dev::mbar_init(&q_empty[i], 1);
       dev::mbar_init(&kv_full[i], 1);
       dev::mbar_init(&kv_empty[i], 1);
       dev::mbar_init(&s_full[i], 1);
@@ -444,23 +475,40 @@ __global__ void __launch_bounds__(384, 1)
   __syncthreads();
   dev::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  if (threadIdx.x == 0 && static_cast<int>(blockIdx.x) == trace_cta) {
+    unsigned long long gt;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+    g_attn_trace[4090] = clock64();
+    g_attn_trace[4091] = gt;
+  }
 
   if (warp == 0) {
     if (lane == 0) {
-      dev::mbar_arrive_expect_tx(q_full, Lay::Q * (hasB ? 2 : 1));
-      for (int t = 0; t < (hasB ? 2 : 1); ++t) {
+      int gj = 0;               // K/V blocks loaded so far (ring slot gj & 1)
+      int cq[2] = {0, 0};       // items loaded per query tile
+      for (int r = 0;; ++r) {
+        const int idx = snake_item(r, cta, P);
+        if (idx >= nitems) break;
+        const Item it = item_of(idx);
+        for (int t = 0; t < (it.hasB ? 2 : 1); ++t) {
+          if (cq[t] > 0) dev::mbar_wait(&q_empty[t], (cq[t] - 1) & 1);
+          dev::mbar_arrive_expect_tx(&q_full[t], Lay::Q);
 #pragma unroll
-        for (int c = 0; c < HD / 64; ++c)
-          dev::tma_load_2d(sQ[t] + c * CHUNK, &tm, q_full, h * HD + c * 64, row0 + (qa + t) * 128);
-      }
-      for (int j = 0; j < nkv; ++j) {
-        const int st = j & 1;
-        dev::mbar_wait(&kv_empty[st], ((j >> 1) & 1) ^ 1);
-        dev::mbar_arrive_expect_tx(&kv_full[st], 2 * Lay::KV);
+          for (int c = 0; c < HD / 64; ++c)
+            dev::tma_load_2d(sQ[t] + c * CHUNK, &tm, &q_full[t], it.h * HD + c * 64, it.row0 + (it.qa + t) * 128);
+          ++cq[t];
+        }
+        for (int j = 0; j < it.nkv; ++j, ++gj) {
+          const int st = gj & 1;
+          dev::mbar_wait(&kv_empty[st], ((gj >> 1) & 1) ^ 1);
+          dev::mbar_arrive_expect_tx(&kv_full[st], 2 * Lay::KV);
 #pragma unroll
-        for (int c = 0; c < HD / 64; ++c) {
-          dev::tma_load_2d(sK + st * Lay::KV + c * CHUNK, &tm, &kv_full[st], Dl + h * HD + c * 64, row0 + j * 128);
-          dev::tma_load_2d(sV + st * Lay::KV + c * CHUNK, &tm, &kv_full[st], 2 * Dl + h * HD + c * 64, row0 + j * 128);
+          for (int c = 0; c < HD / 64; ++c) {
+            dev::tma_load_2d(sK + st * Lay::KV + c * CHUNK, &tm, &kv_full[st], Dl + it.h * HD + c * 64,
+                             it.row0 + j * 128);
+            dev::tma_load_2d(sV + st * Lay::KV + c * CHUNK, &tm, &kv_full[st], 2 * Dl + it.h * HD + c * 64,
+                             it.row0 + j * 128);
+          }
         }
       }
     }
@@ -473,127 +521,195 @@ __global__ void __launch_bounds__(384, 1)
     const uint64_t dk = dev::make_sdesc_sw128(dev::smem_u32(sK), 16, 1024);
     const uint64_t dv = dev::make_sdesc_sw128(dev::smem_u32(sV), CHUNK, 1024);
     auto kstep = [](int kk) { return static_cast<uint64_t>((kk >> 2) * (CHUNK >> 4) + (kk & 3) * 2); };
-    auto issue_s = [&](int t, int j) {
-      const uint64_t bk = dk + static_cast<uint64_t>((j & 1) * (Lay::KV >> 4));
-      if (dev::elect_one_sync()) {
+    int gj = 0;              // K/V blocks consumed before this item
+    int ct[2] = {0, 0};      // blocks of each tile before this item (s_full / p_full / pv_done phases)
+    int cq[2] = {0, 0};
+    for (int r = 0;; ++r) {
+      const int idx = snake_item(r, cta, P);
+      if (idx >= nitems) break;
+      const Item it = item_of(idx);
+      // S_t(j) = Q_t K_j^T; after the tile's last block, Q_t may be replaced (q_empty)
+      auto issue_s = [&](int t, int j) {
+        const uint64_t bk = dk + static_cast<uint64_t>(((gj + j) & 1) * (Lay::KV >> 4));
+        if (dev::elect_one_sync()) {
 #pragma unroll
-        for (int kk = 0; kk < HD / 16; ++kk)
-          dev::umma_f16_ss(tmem + t * 256, dq[t] + kstep(kk), bk + kstep(kk), id_s, kk > 0 ? 1u : 0u);
-        dev::umma_commit(&s_full[t]);
-      }
-      __syncwarp();
-    };
-    auto issue_pv = [&](int t, int j) {
-      dev::mbar_wait(&p_full[t], j & 1);
-      dev::tc_fence_after();
-      const uint64_t bv = dv + static_cast<uint64_t>((j & 1) * (Lay::KV >> 4));
-      if (dev::elect_one_sync()) {
-#pragma unroll
-        for (int kk = 0; kk < 128 / 16; ++kk)  // P (bf16 pairs) sits in the first 64 columns of S
-          dev::umma_f16_ts(tmem + t * 256 + 128, tmem + t * 256 + kk * 8, bv + static_cast<uint64_t>(kk * 128), id_o,
-                           (j > 0 || kk > 0) ? 1u : 0u);
-        dev::umma_commit(&pv_done[t]);
-      }
-      __syncwarp();
-    };
-    dev::mbar_wait(q_full, 0);
-    dev::mbar_wait(&kv_full[0], 0);
-    dev::tc_fence_after();
-    issue_s(0, 0);
-    if (hasB) issue_s(1, 0);
-    for (int j = 0; j < nkv; ++j) {
-      if (j < nkv_t[0]) issue_pv(0, j);
-      if (j + 1 < nkv) {
-        dev::mbar_wait(&kv_full[(j + 1) & 1], ((j + 1) >> 1) & 1);
+          for (int kk = 0; kk < HD / 16; ++kk)
+            dev::umma_f16_ss(tmem + t * 256, dq[t] + kstep(kk), bk + kstep(kk), id_s, kk > 0 ? 1u : 0u);
+          dev::umma_commit(&s_full[t]);
+          if (j == it.nkv_t[t] - 1) dev::umma_commit(&q_empty[t]);
+        }
+        __syncwarp();
+      };
+      auto issue_pv = [&](int t, int j) {
+        const int tb = (ct[t] + j) * 16 + 2 * t;  // trace: blocks of this CTA, per tile
+        if (lane == 0 && tb < 3900) ATTN_TR(tb);
+        dev::mbar_wait(&p_full[t], (ct[t] + j) & 1);
+        if (lane == 0 && tb < 3900) ATTN_TR(tb + 1);
         dev::tc_fence_after();
+        const uint64_t bv = dv + static_cast<uint64_t>(((gj + j) & 1) * (Lay::KV >> 4));
+        if (dev::elect_one_sync()) {
+#pragma unroll
+          for (int kk = 0; kk < 128 / 16; ++kk)  // P (bf16 pairs) sits in the first 64 columns of S
+            dev::umma_f16_ts(tmem + t * 256 + 128, tmem + t * 256 + kk * 8, bv + static_cast<uint64_t>(kk * 128), id_o,
+                             (j > 0 || kk > 0) ? 1u : 0u);
+          dev::umma_commit(&pv_done[t]);
+        }
+        __syncwarp();
+      };
+      if (lane == 0 && cq[0] < 16) ATTN_TR(4000 + 4 * cq[0]);
+      dev::mbar_wait(&q_full[0], cq[0] & 1);
+      if (it.hasB) dev::mbar_wait(&q_full[1], cq[1] & 1);
+      if (lane == 0 && cq[0] < 16) ATTN_TR(4001 + 4 * cq[0]);
+      dev::mbar_wait(&kv_full[gj & 1], (gj >> 1) & 1);
+      if (lane == 0 && cq[0] < 16) ATTN_TR(4002 + 4 * cq[0]);
+      dev::tc_fence_after();
+      issue_s(0, 0);
+      if (it.hasB) issue_s(1, 0);
+      for (int j = 0; j < it.nkv; ++j) {
+        if (j < it.nkv_t[0]) issue_pv(0, j);
+        if (j + 1 < it.nkv) {
+          dev::mbar_wait(&kv_full[(gj + j + 1) & 1], ((gj + j + 1) >> 1) & 1);
+          dev::tc_fence_after();
+        }
+        if (j + 1 < it.nkv_t[0]) issue_s(0, j + 1);
+        if (j < it.nkv_t[1]) issue_pv(1, j);
+        if (j + 1 < it.nkv_t[1]) issue_s(1, j + 1);
+        if (dev::elect_one_sync()) dev::umma_commit(&kv_empty[(gj + j) & 1]);  // K_j / V_j consumed
+        __syncwarp();
       }
-      if (j + 1 < nkv_t[0]) issue_s(0, j + 1);
-      if (j < nkv_t[1]) issue_pv(1, j);
-      if (j + 1 < nkv_t[1]) issue_s(1, j + 1);
-      if (dev::elect_one_sync()) dev::umma_commit(&kv_empty[j & 1]);  // K_j / V_j consumed
-      __syncwarp();
+      gj += it.nkv;
+      ct[0] += it.nkv_t[0];
+      ct[1] += it.nkv_t[1];
+      ++cq[0];
+      if (it.hasB) ++cq[1];
     }
   } else if (warp >= 4) {
     const int t = (static_cast<int>(warp) - 4) >> 2;  // query tile of this warpgroup
-    if (t == 0 || hasB) {
-      const int r = static_cast<int>(warp & 3) * 32 + static_cast<int>(lane);
-      const int q0 = (qa + t) * 128;
-      const int q = q0 + r;
-      const int nk = nkv_t[t];
-      const uint32_t lane_base = static_cast<uint32_t>((warp & 3) * 32) << 16;
-      const uint32_t tS = tmem + lane_base + t * 256, tO = tS + 128;
+    const int r = static_cast<int>(warp & 3) * 32 + static_cast<int>(lane);
+    const uint32_t lane_base = static_cast<uint32_t>((warp & 3) * 32) << 16;
+    const uint32_t tS = tmem + lane_base + t * 256, tO = tS + 128;
+    int ct = 0;  // this tile's blocks before the item
+    for (int rr = 0;; ++rr) {
+      const int idx = snake_item(rr, cta, P);
+      if (idx >= nitems) break;
+      const Item it = item_of(idx);
+      if (t == 1 && !it.hasB) continue;
+      const int h = it.h, bh = it.bh;
+      const int q = (it.qa + t) * 128 + r;
+      const int nk = it.nkv_t[t];
       float m_used = -INFINITY, l = 0.f;
+      const bool trw = lane == 0 && (warp & 3) == 0;
       for (int j = 0; j < nk; ++j) {
-        dev::mbar_wait(&s_full[t], j & 1);
+        const int tb = (ct + j) * 16 + 4 + 4 * t;
+        if (trw && tb < 3900) ATTN_TR(tb);
+        dev::mbar_wait(&s_full[t], (ct + j) & 1);
+        if (trw && tb < 3900) ATTN_TR(tb + 1);
         dev::tc_fence_after();
         uint32_t v[128];
 #pragma unroll
         for (int c = 0; c < 4; ++c)
           dev::tmem_ld_32x32b_x32(tS + c * 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32 * c));
         dev::tmem_ld_wait();
-        if (lut) {
-          const float* lr = lut + static_cast<int64_t>(h) * (2 * T + 128) + (T - 1 - (q < T ? q : T - 1)) + j * 128;
+        auto bias_mask = [&]() {
+          if (lut) {
+            const float* lr = lut + static_cast<int64_t>(h) * (2 * T + 128) + (T - 1 - (q < T ? q : T - 1)) + j * 128;
 #pragma unroll
-          for (int i = 0; i < 128; ++i) v[i] = __float_as_uint(fmaf(__uint_as_float(v[i]), scale, __ldg(lr + i)));
-        }
-        if ((causal && j == nk - 1) || (j + 1) * 128 > T) {
-#pragma unroll
-          for (int i = 0; i < 128; ++i) {
-            const int key = j * 128 + i;
-            if (!((!causal || key <= q) && key < T)) v[i] = __float_as_uint(-INFINITY);
+            for (int i = 0; i < 128; ++i) v[i] = __float_as_uint(fmaf(__uint_as_float(v[i]), scale, __ldg(lr + i)));
           }
-        }
-        float mx = fmaxf(__uint_as_float(v[0]), __uint_as_float(v[127]));
+          if ((causal && j == nk - 1) || (j + 1) * 128 > T) {
 #pragma unroll
-        for (int i = 1; i < 127; i += 2) mx = dev::fmax3(mx, __uint_as_float(v[i]), __uint_as_float(v[i + 1]));
-        // lazy rescale: keep the stale max unless the new one is 2^8 larger in exp2 units; the
-        // O rewrite uses warp-collective TMEM loads/stores, so the whole warp takes it together
-        // (factor 1 for the rows that keep their max)
-        bool resc = false;
-        float factor = 1.f;
+            for (int i = 0; i < 128; ++i) {
+              const int key = j * 128 + i;
+              if (!((!causal || key <= q) && key < T)) v[i] = __float_as_uint(-INFINITY);
+            }
+          }
+        };
+        bias_mask();
+        // Lazy rescale (FA4-style): the running max m_used moves only when a row's block max
+        // exceeds it by more than 2^8 in exp2 units. After block 0 the exps are taken against
+        // m_used straight away while the block max is reduced alongside them (independent
+        // chains, no max -> exp dependency on the critical path); a row whose max did jump
+        // takes the rare slow path: O is rescaled and P is recomputed from S, still in TMEM.
+        // The O rewrite uses warp-collective TMEM loads/stores, so the whole warp takes it
+        // together (factor 1 for the rows that keep their max).
+        const float2 sl2 = make_float2(sl_eff, sl_eff);
+        float l_blk;
+        auto exps = [&](float mref) {  // P in place: v[e] = bf16x2(p[2e], p[2e+1]); returns the row sum
+          const float mb = mref * sl_eff;
+          const float2 nmb2 = make_float2(-mb, -mb);
+          float2 ls[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+#pragma unroll
+          for (int e = 0; e < 64; ++e) {
+            const float2 a = dev::ffma2(make_float2(__uint_as_float(v[2 * e]), __uint_as_float(v[2 * e + 1])), sl2, nmb2);
+            // SW_EXP_POLY of every 8 pairs on the FMA pipe, the rest on MUFU
+            const float2 pp = (e & 7) < SW_EXP_POLY ? dev::ex2_poly2(a)
+                                                    : make_float2(dev::ex2_approx(a.x), dev::ex2_approx(a.y));
+            ls[e & 3] = dev::fadd2(ls[e & 3], pp);
+            v[e] = dev::pack_bf16x2(pp.x, pp.y);
+          }
+          const float2 s01 = dev::fadd2(ls[0], ls[1]), s23 = dev::fadd2(ls[2], ls[3]);
+          return (s01.x + s23.x) + (s01.y + s23.y);
+        };
+        auto rowmax = [&]() {
+          float m4[4] = {__uint_as_float(v[0]), __uint_as_float(v[1]), __uint_as_float(v[2]), __uint_as_float(v[3])};
+#pragma unroll
+          for (int i = 4; i < 128; i += 8) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) m4[u] = dev::fmax3(m4[u], __uint_as_float(v[i + 2 * u]), __uint_as_float(v[i + 2 * u + 1]));
+          }
+          return fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
+        };
         if (j == 0) {
-          m_used = mx;
-        } else if ((mx - m_used) * sl_eff > 8.f) {
-          resc = true;
-          factor = dev::ex2_approx((m_used - mx) * sl_eff);
-          m_used = mx;
-          l *= factor;
-        }
-        if (__any_sync(0xffffffffu, resc)) {
-          dev::mbar_wait(&pv_done[t], (j - 1) & 1);  // every earlier P V has landed in O
-          dev::tc_fence_after();
+          m_used = rowmax();
+          l_blk = exps(m_used);
+        } else {
+          // block max from the raw scores before exps() overwrites them (the reductions and the
+          // exps are independent, so the scheduler interleaves them)
+          const float mx = rowmax();
+          l_blk = exps(m_used);
+          const bool resc = (mx - m_used) * sl_eff > 8.f;
+          if (__any_sync(0xffffffffu, resc)) {
+            const float factor = resc ? dev::ex2_approx((m_used - mx) * sl_eff) : 1.f;
+            if (resc) {
+              m_used = mx;
+              l *= factor;
+            }
+            dev::mbar_wait(&pv_done[t], (ct + j - 1) & 1);  // every earlier P V has landed in O
+            dev::tc_fence_after();
 #pragma unroll 1
-          for (int c = 0; c < HD / 32; ++c) {
-            uint32_t o[32];
-            dev::tmem_ld_32x32b_x32(tO + c * 32, o);
+            for (int c = 0; c < HD / 32; ++c) {
+              uint32_t o[32];
+              dev::tmem_ld_32x32b_x32(tO + c * 32, o);
+              dev::tmem_ld_wait();
+#pragma unroll
+              for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * factor);
+              dev::tmem_st_32x32b_x32(tO + c * 32, o);
+            }
+            dev::tmem_st_wait();
+            // P again against the new max: S_j is still in TMEM (reload, re-bias, re-mask)
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+              dev::tmem_ld_32x32b_x32(tS + c * 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32 * c));
             dev::tmem_ld_wait();
-#pragma unroll
-            for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * factor);
-            dev::tmem_st_32x32b_x32(tO + c * 32, o);
+            bias_mask();
+            l_blk = exps(m_used);
           }
-          dev::tmem_st_wait();
         }
-        const float mb = m_used * sl_eff;
-        const float2 sl2 = make_float2(sl_eff, sl_eff), nmb2 = make_float2(-mb, -mb);
-        float2 ls2 = make_float2(0.f, 0.f);
-#pragma unroll
-        for (int e = 0; e < 64; ++e) {  // P in place: v[e] = bf16x2(p[2e], p[2e+1])
-          const float2 a = dev::ffma2(make_float2(__uint_as_float(v[2 * e]), __uint_as_float(v[2 * e + 1])), sl2, nmb2);
-          const float2 pp = make_float2(dev::ex2_approx(a.x), dev::ex2_approx(a.y));
-          ls2 = dev::fadd2(ls2, pp);
-          v[e] = dev::pack_bf16x2(pp.x, pp.y);
-        }
-        l += ls2.x + ls2.y;
         dev::tmem_st_32x32b_x32(tS, *reinterpret_cast<uint32_t(*)[32]>(v));
         dev::tmem_st_32x32b_x32(tS + 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
+        l += l_blk;
+        if (trw && tb < 3900) ATTN_TR(tb + 2);
         dev::tmem_st_wait();
         dev::tc_fence_before();
         dev::mbar_arrive(&p_full[t]);
+        if (trw && tb < 3900) ATTN_TR(tb + 3);
       }
-      dev::mbar_wait(&pv_done[t], (nk - 1) & 1);
+      // O of this item; the next item's first P V (which overwrites O) waits for this warpgroup's
+      // next p_full, so the TMEM reads below are done before it
+      dev::mbar_wait(&pv_done[t], (ct + nk - 1) & 1);
       dev::tc_fence_after();
       const float inv = 1.f / l;
-      bf16* orow = out + (static_cast<int64_t>(row0) + q) * Dl + h * HD;
+      bf16* orow = out + (static_cast<int64_t>(it.row0) + q) * Dl + h * HD;
 #pragma unroll
       for (int c = 0; c < HD / 32; ++c) {
         uint32_t o[32];
@@ -612,14 +728,36 @@ __global__ void __launch_bounds__(384, 1)
         }
       }
       if (q < T) lse[static_cast<int64_t>(bh) * T + q] = m_used * sc_eff + logf(l);
+      if (trw && t == 0 && rr < 16) ATTN_TR(4003 + 4 * rr);
+      dev::tc_fence_before();
+      ct += nk;
     }
   }
   dev::tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0 && static_cast<int>(blockIdx.x) == trace_cta) {
+    unsigned long long gt;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+    g_attn_trace[4092] = clock64();
+    g_attn_trace[4093] = gt;
+  }
   if (warp == 2) {
     dev::tc_fence_after();
     dev::tmem_dealloc<512>(tmem);
   }
+}
+
+// SW_ATTN_PERSIST=1: one resident CTA per SM walking several items (snake order). Measured
+// on B200 (tools/attn_bench.py, LLaMA-7B heads): equal at T = 2048 (the next item's Q load and
+// the pipeline refill are not hidden by it), 25% slower at T = 8192 (the hardware's in-order
+// block dispatch keeps a head group's K/V reads together in L2, the static deal does not), so
+// the default launches one CTA per item.
+bool attn_persist() {
+  static const bool on = [] {
+    const char* e = std::getenv("SW_ATTN_PERSIST");
+    return e != nullptr && e[0] == '1';
+  }();
+  return on;
 }
 
 bool fwd2_enabled() {
@@ -646,10 +784,12 @@ bool launch_fwd2(const bf16* qkv, bf16* o, float* lse, int B, int T, int Hl, cud
   const int nqb = (T + 127) / 128;
   const int npair = (nqb + 1) / 2;
   const double scale = scale_arg > 0.f ? scale_arg : 1.0 / std::sqrt(static_cast<double>(HD));
-  attn_fwd_tc2<<<npair * B * Hl, 384, Fwd2Layout::BYTES, s>>>(tm, o, lse, T, Hl,
+  const int nitems = npair * B * Hl;
+  const int grid = attn_persist() ? std::min(nitems, device_sm_count()) : nitems;
+  attn_fwd_tc2<<<grid, 384, Fwd2Layout::BYTES, s>>>(tm, o, lse, T, Hl,
                                                               static_cast<float>(scale * 1.4426950408889634),
                                                               static_cast<float>(scale), B * Hl, work_group(), causal,
-                                                              lut);
+                                                              lut, trace_cta());
   return true;
 }
 

@@ -29,7 +29,11 @@ def ref_attention(qkv, B, T, Hl, hd):
 
 @pytest.mark.parametrize("B,T,Hl,hd", [(2, 64, 2, 8), (2, 128, 2, 64), (1, 256, 2, 128), (2, 200, 3, 64),
                                         (2, 200, 2, 128), (1, 1000, 3, 128), (2, 96, 1, 128), (1, 2048, 2, 128),
-                                        (1, 160, 2, 256)])
+                                        (1, 160, 2, 256),
+                                        # more work items than SMs: the persistent kernels walk
+                                        # several items per CTA (T = 640: an odd query-block count,
+                                        # so the last pair has one tile)
+                                        (4, 640, 48, 128), (2, 1024, 40, 128)])
 def test_attention_fwd_bwd(B, T, Hl, hd):
     L = _lib.lib()
     g = torch.Generator(device=DEV).manual_seed(B * 1000 + T + hd)
