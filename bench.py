@@ -56,6 +56,15 @@ def load_peaks():
     return FALLBACK_PEAKS, "fallback"
 
 
+def shape_name(spec_path):
+    """The BASELINE config a spec file stands for (oracle/specs/*.spec)."""
+    base = os.path.basename(spec_path)
+    for key, name in (("gptj", "GPT-J-6B-shape"), ("opt66b", "OPT-66B-shape"), ("llama7b", "LLaMA-7B-shape")):
+        if base.startswith(key):
+            return name
+    return os.path.splitext(base)[0]
+
+
 def read_spec(path):
     out = {"tie_embeddings": False}
     for ln in open(path):
@@ -194,7 +203,7 @@ def run_reference(args):
         "ms_per_step": 1000.0 * args.batch * args.seq / res["value"],
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic",
-        "config": {"workload": f"LLaMA-7B-shape decoder (reference family) fwd+bwd+AdamW, "
+        "config": {"workload": f"{shape_name(args.spec)} decoder (reference family) fwd+bwd+AdamW, "
                                f"seq {args.seq}, batch {args.batch}, CPU reference", "seq_len": args.seq,
                    "global_batch": args.batch, "parallelism": "cpu"},
         "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")},
@@ -324,7 +333,7 @@ def run_ours(args):
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (uniform random token ids, random-init weights from the reference init stream)",
-        "config": {"workload": f"LLaMA-7B-shape decoder ("
+        "config": {"workload": f"{shape_name(args.spec)} decoder ("
                                + ("SwiGLU MLP + RMSNorm extension" if s.get("mlp") == "swiglu"
                                   else "reference model family")
                                + f", {s['n_layers']} layers, "

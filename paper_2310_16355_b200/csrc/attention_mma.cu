@@ -1720,7 +1720,15 @@ bool launch_bwd(const bf16* qkv, const bf16* o, const float* lse, const bf16* do
 
 }  // namespace
 
+void attention_hd256_trace_read(unsigned long long* out);
+
+// SW_ATTN_TRACE_HD256=1: the head_dim-256 backward's trace (attention_hd256.cu) instead
 void attention_trace_read(unsigned long long* out) {
+  const char* e = std::getenv("SW_ATTN_TRACE_HD256");
+  if (e != nullptr && e[0] == '1') {
+    attention_hd256_trace_read(out);
+    return;
+  }
   cudaMemcpyFromSymbol(out, g_attn_trace, sizeof(unsigned long long) * 4096);
 }
 
@@ -1730,8 +1738,22 @@ bool attention_mma_fwd_ex(const bf16* qkv, bf16* o, float* lse, int B, int T, in
   return launch_fwd2(qkv, o, lse, B, T, Hl, s, causal, lut, scale);
 }
 
+bool attention_hd256_fwd(const bf16* qkv, bf16* o, float* lse, int B, int T, int Hl, cudaStream_t s);
+bool attention_hd256_bwd(const bf16* qkv, const bf16* o, const float* lse, const bf16* dout, bf16* dqkv,
+                         float* scratch, int B, int T, int Hl, cudaStream_t s, bool delta_ready);
+
+// shared with attention_hd256.cu: delta = rowsum(dO * O) per (bh, q), and the fp32 dQ accumulator
+// -> bf16 q columns of dqkv
+void attn_delta(const bf16* o, const bf16* dout, float* delta, int T, int Hl, int hd, int64_t M, cudaStream_t s) {
+  launch_delta(o, dout, delta, T, Hl, hd, M, s);
+}
+void attn_dq_to_bf16(const float* dq, bf16* dqkv, int64_t M, int Dl, cudaStream_t s) {
+  dq_to_bf16<<<1184, 256, 0, s>>>(dq, dqkv, M, Dl);
+}
+
 bool attention_mma_fwd(const bf16* qkv, bf16* o, float* lse, int B, int T, int Hl, int hd, cudaStream_t s) {
   if (((3 * Hl * hd) % 8) != 0) return false;
+  if (hd == 256) return attention_hd256_fwd(qkv, o, lse, B, T, Hl, s);
   if (hd == 128) return fwd2_enabled() ? launch_fwd2(qkv, o, lse, B, T, Hl, s) : launch_fwd<128>(qkv, o, lse, B, T, Hl, s);
   if (hd == 64) return launch_fwd<64>(qkv, o, lse, B, T, Hl, s);
   return false;
@@ -1749,6 +1771,10 @@ bool attention_mma_bwd(const bf16* qkv, const bf16* o, const float* lse, const b
                        float* scratch, int B, int T, int Hl, int hd, cudaStream_t s, bool delta_ready,
                        float* colsum, bool* colsum_done) {
   if (((Hl * hd) % 8) != 0) return false;
+  if (hd == 256) {
+    if (colsum_done != nullptr) *colsum_done = false;
+    return attention_hd256_bwd(qkv, o, lse, dout, dqkv, scratch, B, T, Hl, s, delta_ready);
+  }
   if (hd == 128) return launch_bwd<128>(qkv, o, lse, dout, dqkv, scratch, B, T, Hl, s, delta_ready, colsum, colsum_done);
   if (hd == 64) return launch_bwd<64>(qkv, o, lse, dout, dqkv, scratch, B, T, Hl, s, delta_ready, colsum, colsum_done);
   return false;

@@ -33,7 +33,9 @@ def ref_attention(qkv, B, T, Hl, hd):
                                         # more work items than SMs: the persistent kernels walk
                                         # several items per CTA (T = 640: an odd query-block count,
                                         # so the last pair has one tile)
-                                        (4, 640, 48, 128), (2, 1024, 40, 128)])
+                                        (4, 640, 48, 128), (2, 1024, 40, 128),
+                                        # head_dim 256 (GPT-J): tcgen05 forward, 64-key blocks
+                                        (2, 1000, 4, 256), (1, 2048, 3, 256)])
 def test_attention_fwd_bwd(B, T, Hl, hd):
     L = _lib.lib()
     g = torch.Generator(device=DEV).manual_seed(B * 1000 + T + hd)
