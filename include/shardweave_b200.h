@@ -313,6 +313,14 @@ SW_API sw_status sw_k_gemm_bf16(int M, int N, int K, const void* A, int64_t lda,
 
 /* Causal attention over head-sharded activations (graph.hpp:650-661 + model.hpp:100-106):
  * qkv [B*T, 3*Hl*hd] bf16 (q | k | v), o [B*T, Hl*hd] bf16, lse [B, Hl, T] fp32. */
+/* One cached decode step of attention (the Predictor's KV-cached next token):
+ * qkv_new [B, 3*Hl*hd] bf16 is the step's q | k | v row per sequence; cache [B*T, 3*Hl*hd] bf16
+ * holds keys/values 0..p-1 (the layer's qkv activations); out [B, Hl*hd] bf16. split != 0: the
+ * split-key kernel, which also writes the new k | v into cache row p (part: B*Hl*16*(hd+2)
+ * floats, ticket: B*Hl zero-initialised uints); split == 0: kv scatter + the one-CTA-per-head
+ * kernel. */
+SW_API sw_status sw_k_decode_attention(const void* qkv_new, void* cache, void* out, int B, int T, int p, int Hl,
+                                       int hd, int split, float* part, unsigned int* ticket, void* stream);
 SW_API sw_status sw_k_attention_fwd(const void* qkv, void* o, float* lse, int B, int T, int Hl,
                                     int hd, void* stream);
 /* dqkv [B*T, 3*Hl*hd] bf16; scratch fp32 of B*T*Hl + B*T*2*Hl*hd elements. */

@@ -101,6 +101,8 @@ def _declare(L: C.CDLL) -> None:
                                  C.c_int, vp, i64, vp, i64, vp, vp, i64, f32, C.c_int, vp]
     L.sw_k_gemm_bf16.restype = C.c_int
     L.sw_k_attention_fwd.argtypes = [vp, vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, vp]
+    L.sw_k_decode_attention.argtypes = [vp, vp, vp] + [C.c_int] * 6 + [vp, vp, vp]
+    L.sw_k_decode_attention.restype = C.c_int
     L.sw_k_attention_bwd.argtypes = [vp, vp, vp, vp, vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, vp]
     L.sw_k_layernorm_fwd.argtypes = [vp, vp, vp, vp, vp, vp, i64, C.c_int, f32, vp]
     L.sw_k_layernorm_bwd.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, vp, i64, C.c_int, C.c_int, vp]

@@ -140,6 +140,21 @@ sw_status sw_k_gemm_bf16_adamw(int M, int N, int K, const void* A, int64_t lda, 
   });
 }
 
+sw_status sw_k_decode_attention(const void* qkv_new, void* cache, void* out, int B, int T, int p, int Hl, int hd,
+                                int split, float* part, unsigned int* ticket, void* stream) {
+  return sw::guarded([&] {
+    const auto* q = static_cast<const sw::k::bf16*>(qkv_new);
+    auto* c = static_cast<sw::k::bf16*>(cache);
+    auto* o = static_cast<sw::k::bf16*>(out);
+    const auto st = static_cast<cudaStream_t>(stream);
+    if (!(split && sw::k::decode_attention_split(q, c, o, B, T, p, Hl, hd, st, nullptr, part, ticket))) {
+      sw::k::kv_scatter(q, c, B, T, p, Hl * hd, st);
+      sw::k::decode_attention(q, c, o, B, T, p, Hl, hd, st);
+    }
+    sw::cuda_check(cudaGetLastError(), "decode_attention");
+  });
+}
+
 sw_status sw_k_attention_fwd(const void* qkv, void* o, float* lse, int B, int T, int Hl, int hd,
                              void* stream) {
   return sw::guarded([&] {

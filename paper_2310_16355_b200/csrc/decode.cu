@@ -1,6 +1,7 @@
 // Greedy-decode kernels (the Predictor's next-token loop, cli.cpp:425-447,
 // with a KV cache instead of re-running the window): one new position per sequence per step.
 // HBM-bound (every step reads the weights and the cached keys/values once).
+#include <algorithm>
 #include <cfloat>
 #include <stdexcept>
 
@@ -14,14 +15,18 @@ namespace {
 
 // x[b] = tok[ids[b]] + pos[p]   (model.hpp:92 embedding + learned position)
 __global__ void embed_rows_kernel(const int32_t* __restrict__ ids, const float* __restrict__ tok,
-                                  const float* __restrict__ pos, int p, float* __restrict__ x, int d) {
+                                  const float* __restrict__ pos, int p, const int* __restrict__ pd,
+                                  float* __restrict__ x, int d) {
+  if (pd != nullptr) p = *pd;  // position kept on the device (CUDA-graph decode steps)
   const int b = blockIdx.x;
   const int64_t id = ids[b];
   for (int c = threadIdx.x; c < d; c += blockDim.x) x[static_cast<int64_t>(b) * d + c] = tok[id * d + c] + pos[static_cast<int64_t>(p) * d + c];
 }
 
 // k | v of the new row b go to cache row b*T + p of the layer's qkv activations
-__global__ void kv_scatter_kernel(const bf16* __restrict__ src, bf16* __restrict__ cache, int T, int p, int dl) {
+__global__ void kv_scatter_kernel(const bf16* __restrict__ src, bf16* __restrict__ cache, int T, int p,
+                                  const int* __restrict__ pd, int dl) {
+  if (pd != nullptr) p = *pd;
   const int b = blockIdx.x;
   const bf16* s = src + static_cast<int64_t>(b) * 3 * dl + dl;
   bf16* t = cache + (static_cast<int64_t>(b) * T + p) * 3 * dl + dl;
@@ -36,8 +41,10 @@ __global__ void kv_scatter_kernel(const bf16* __restrict__ src, bf16* __restrict
 template <int HD>
 __global__ void __launch_bounds__(256) decode_attention_kernel(const bf16* __restrict__ qnew,
                                                                const bf16* __restrict__ cache,
-                                                               bf16* __restrict__ out, int T, int p, int Hl,
+                                                               bf16* __restrict__ out, int T, int p,
+                                                               const int* __restrict__ pd, int Hl,
                                                                float scale_log2) {
+  if (pd != nullptr) p = *pd;
   constexpr int G = HD / 8;          // lanes per key
   constexpr int KPW = 32 / G;        // keys per warp step
   constexpr int NG = 8 * KPW;        // groups per CTA
@@ -112,12 +119,154 @@ __global__ void __launch_bounds__(256) decode_attention_kernel(const bf16* __res
   }
 }
 
+// Split-key decode attention (flash-decoding): grid (B * Hl, DSPLIT). Split s of a head takes
+// keys [s c, min(p + 1, (s + 1) c)), c = ceil((p + 1) / DSPLIT); lanes work in groups of
+// G = hd / 8 (16-byte loads) and every warp keeps UNR keys' K / V loads in flight before
+// consuming them. The split holding key p reads the new k / v from the step's qkv row and writes
+// them into the cache (the fused kv_scatter). Each split leaves an unnormalised (m, l, o) partial;
+// the split that takes the last ticket of its head's counter merges them (the counter is never
+// reset: tickets are counted modulo DSPLIT).
+constexpr int DSPLIT = 16;
+constexpr int DUNR = 4;
+
+template <int HD>
+__global__ void __launch_bounds__(256) decode_attention_split_kernel(const bf16* __restrict__ qnew,
+                                                                     bf16* __restrict__ cache,
+                                                                     bf16* __restrict__ out, int T, int p,
+                                                                     const int* __restrict__ pd, int Hl,
+                                                                     float scale_log2, float* __restrict__ part,
+                                                                     unsigned int* __restrict__ ticket) {
+  if (pd != nullptr) p = *pd;
+  constexpr int G = HD / 8;
+  constexpr int KPW = 32 / G;
+  constexpr int NG = 8 * KPW;
+  __shared__ float sm_m[NG], sm_l[NG];
+  __shared__ float sm_o[NG][HD];
+  __shared__ bool last;
+  const int bh = blockIdx.x, b = bh / Hl, h = bh % Hl, sp = blockIdx.y;
+  const int dl = Hl * HD;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int grp = lane / G, gl = lane % G;
+  const int gid = warp * KPW + grp;
+  const int nk = p + 1;
+  const int chunk = (nk + DSPLIT - 1) / DSPLIT;
+  const int k0 = sp * chunk, k1 = min(nk, k0 + chunk);
+  const bf16* qrow = qnew + static_cast<int64_t>(b) * 3 * dl;
+  float q[8];
+  {
+    const uint4 qv = *reinterpret_cast<const uint4*>(qrow + h * HD + gl * 8);
+    const uint32_t qq[4] = {qv.x, qv.y, qv.z, qv.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float2 f = dev::unpack_bf16x2(qq[e]);
+      q[2 * e] = f.x * scale_log2;
+      q[2 * e + 1] = f.y * scale_log2;
+    }
+  }
+  float m = -INFINITY, l = 0.f, o[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) o[i] = 0.f;
+  for (int jb = k0 + warp * KPW; jb < k1; jb += NG * DUNR) {
+    uint4 kv[DUNR], vv[DUNR];
+#pragma unroll
+    for (int u = 0; u < DUNR; ++u) {  // all of this warp's loads first
+      const int j = jb + u * NG + grp;
+      const int jj = j < k1 ? j : k0;
+      const bf16* kr = jj == p ? qrow + dl + h * HD + gl * 8
+                               : cache + (static_cast<int64_t>(b) * T + jj) * 3 * dl + dl + h * HD + gl * 8;
+      kv[u] = *reinterpret_cast<const uint4*>(kr);
+      vv[u] = *reinterpret_cast<const uint4*>(kr + dl);
+      if (jj == p && j == p) {  // the new row joins the cache (fused kv_scatter); j past this split's
+                                // range (jj = k0) must not write, even when it equals p
+        bf16* cr = cache + (static_cast<int64_t>(b) * T + p) * 3 * dl + dl + h * HD + gl * 8;
+        *reinterpret_cast<uint4*>(cr) = kv[u];
+        *reinterpret_cast<uint4*>(cr + dl) = vv[u];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < DUNR; ++u) {
+      const int j = jb + u * NG + grp;
+      const uint32_t kk[4] = {kv[u].x, kv[u].y, kv[u].z, kv[u].w}, vw[4] = {vv[u].x, vv[u].y, vv[u].z, vv[u].w};
+      float sc = 0.f;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 f = dev::unpack_bf16x2(kk[e]);
+        sc = fmaf(q[2 * e], f.x, fmaf(q[2 * e + 1], f.y, sc));
+      }
+#pragma unroll
+      for (int x = G / 2; x > 0; x >>= 1) sc += __shfl_xor_sync(0xffffffffu, sc, x);
+      if (j < k1) {
+        const float mn = fmaxf(m, sc);
+        const float corr = dev::ex2_approx(m - mn), e1 = dev::ex2_approx(sc - mn);
+        l = l * corr + e1;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float2 f = dev::unpack_bf16x2(vw[e]);
+          o[2 * e] = o[2 * e] * corr + e1 * f.x;
+          o[2 * e + 1] = o[2 * e + 1] * corr + e1 * f.y;
+        }
+        m = mn;
+      }
+    }
+  }
+  if (gl == 0) {
+    sm_m[gid] = m;
+    sm_l[gid] = l;
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) sm_o[gid][gl * 8 + i] = o[i];
+  __syncthreads();
+  float* mine = part + (static_cast<int64_t>(bh) * DSPLIT + sp) * (HD + 2);
+  if (threadIdx.x < HD) {  // this split's partial: (M, L, unnormalised O) over its groups
+    const int c = threadIdx.x;
+    float M = -INFINITY;
+    for (int g = 0; g < NG; ++g) M = fmaxf(M, sm_m[g]);
+    float L = 0.f, acc = 0.f;
+    if (M != -INFINITY) {
+      for (int g = 0; g < NG; ++g) {
+        if (sm_m[g] == -INFINITY) continue;
+        const float f = dev::ex2_approx(sm_m[g] - M);
+        L += sm_l[g] * f;
+        acc += sm_o[g][c] * f;
+      }
+    }
+    mine[2 + c] = acc;
+    if (c == 0) {
+      mine[0] = M;
+      mine[1] = L;
+    }
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = (atomicAdd(ticket + bh, 1u) % DSPLIT) == DSPLIT - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (threadIdx.x < HD) {
+    const int c = threadIdx.x;
+    const float* ph = part + static_cast<int64_t>(bh) * DSPLIT * (HD + 2);
+    float M = -INFINITY;
+    for (int s2 = 0; s2 < DSPLIT; ++s2) M = fmaxf(M, __ldcg(ph + s2 * (HD + 2)));
+    float L = 0.f, acc = 0.f;
+    for (int s2 = 0; s2 < DSPLIT; ++s2) {
+      const float ms = __ldcg(ph + s2 * (HD + 2));
+      if (ms == -INFINITY) continue;
+      const float f = dev::ex2_approx(ms - M);
+      L += __ldcg(ph + s2 * (HD + 2) + 1) * f;
+      acc += __ldcg(ph + s2 * (HD + 2) + 2 + c) * f;
+    }
+    out[static_cast<int64_t>(b) * dl + h * HD + c] = __float2bfloat16(acc / L);
+  }
+}
+
 // Any head dim <= 256 (scalar loads): lane i holds head-dim elements i, i+32, ...
 template <int HDV>
 __global__ void __launch_bounds__(256) decode_attention_any_kernel(const bf16* __restrict__ qnew,
                                                                    const bf16* __restrict__ cache,
-                                                                   bf16* __restrict__ out, int T, int p, int Hl,
+                                                                   bf16* __restrict__ out, int T, int p,
+                                                                   const int* __restrict__ pd, int Hl,
                                                                    int hd, float scale_log2) {
+  if (pd != nullptr) p = *pd;
   constexpr int WARPS = 8;
   __shared__ float sm_m[WARPS], sm_l[WARPS];
   __shared__ float sm_o[WARPS][32 * HDV];
@@ -186,13 +335,17 @@ __global__ void __launch_bounds__(256) decode_attention_any_kernel(const bf16* _
 
 // First maximum of each row (kernels.hpp:515-527 semantics: strict > keeps the lowest index).
 // Writes (value, global index) as floats so ranks can combine shards.
+// argmax of row b over columns [blockIdx.y * chunk, ...) -> out[(b * gridDim.y + blockIdx.y) * 2 + {0, 1}]
+// (value, index_base + column); ties to the smaller index
 __global__ void argmax_rows_kernel(const bf16* __restrict__ x, int64_t row_stride, int n, int index_base,
                                    float* __restrict__ out) {
   const int b = blockIdx.x;
+  const int chunk = (n + gridDim.y - 1) / gridDim.y;
+  const int i0 = blockIdx.y * chunk, i1 = min(n, i0 + chunk);
   const bf16* xr = x + static_cast<int64_t>(b) * row_stride;
   float best = -INFINITY;
   int bi = 0x7fffffff;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+  for (int i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
     const float v = __bfloat162float(xr[i]);
     if (v > best || (v == best && i < bi)) {
       best = v;
@@ -223,9 +376,27 @@ __global__ void argmax_rows_kernel(const bf16* __restrict__ x, int64_t row_strid
         bi = si[k];
       }
     }
-    out[2 * b] = best;
-    out[2 * b + 1] = static_cast<float>(index_base + bi);
+    const int64_t o = (static_cast<int64_t>(b) * gridDim.y + blockIdx.y) * 2;
+    out[o] = best;
+    out[o + 1] = bi == 0x7fffffff ? -1.f : static_cast<float>(index_base + bi);
   }
+}
+
+// parts [B][C][2] -> out [B][2], first maximum (smallest index among equal values)
+__global__ void argmax_chunks_kernel(const float* __restrict__ parts, int C, int B, float* __restrict__ out) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  float best = -INFINITY, bi = -1.f;
+  for (int c = 0; c < C; ++c) {
+    const float v = parts[(static_cast<int64_t>(b) * C + c) * 2], i = parts[(static_cast<int64_t>(b) * C + c) * 2 + 1];
+    if (i < 0.f) continue;
+    if (bi < 0.f || v > best || (v == best && i < bi)) {
+      best = v;
+      bi = i;
+    }
+  }
+  out[2 * b] = best;
+  out[2 * b + 1] = bi;
 }
 
 // parts[r][b] = (value, index) of shard r; token[b] = index of the first maximum over shards
@@ -247,35 +418,70 @@ __global__ void argmax_combine_kernel(const float* __restrict__ parts, int shard
 
 }  // namespace
 
-void embed_rows(const int32_t* ids, const float* tok, const float* pos, int p, float* x, int B, int d, cudaStream_t s) {
-  embed_rows_kernel<<<B, 256, 0, s>>>(ids, tok, pos, p, x, d);
+void embed_rows(const int32_t* ids, const float* tok, const float* pos, int p, float* x, int B, int d, cudaStream_t s,
+                const int* p_dev) {
+  embed_rows_kernel<<<B, 256, 0, s>>>(ids, tok, pos, p, p_dev, x, d);
 }
 
-void kv_scatter(const bf16* qkv_new, bf16* cache, int B, int T, int p, int dl, cudaStream_t s) {
-  kv_scatter_kernel<<<B, 128, 0, s>>>(qkv_new, cache, T, p, dl);
+void kv_scatter(const bf16* qkv_new, bf16* cache, int B, int T, int p, int dl, cudaStream_t s, const int* p_dev) {
+  kv_scatter_kernel<<<B, 128, 0, s>>>(qkv_new, cache, T, p, p_dev, dl);
 }
 
 void decode_attention(const bf16* qkv_new, const bf16* cache, bf16* out, int B, int T, int p, int Hl, int hd,
-                      cudaStream_t s) {
+                      cudaStream_t s, const int* p_dev) {
   const float scale_log2 = static_cast<float>(1.4426950408889634 / sqrt(static_cast<double>(hd)));
   switch (hd) {
-    case 64: decode_attention_kernel<64><<<B * Hl, 256, 0, s>>>(qkv_new, cache, out, T, p, Hl, scale_log2); break;
-    case 128: decode_attention_kernel<128><<<B * Hl, 256, 0, s>>>(qkv_new, cache, out, T, p, Hl, scale_log2); break;
-    case 256: decode_attention_kernel<256><<<B * Hl, 256, 0, s>>>(qkv_new, cache, out, T, p, Hl, scale_log2); break;
+    case 64: decode_attention_kernel<64><<<B * Hl, 256, 0, s>>>(qkv_new, cache, out, T, p, p_dev, Hl, scale_log2); break;
+    case 128: decode_attention_kernel<128><<<B * Hl, 256, 0, s>>>(qkv_new, cache, out, T, p, p_dev, Hl, scale_log2); break;
+    case 256: decode_attention_kernel<256><<<B * Hl, 256, 0, s>>>(qkv_new, cache, out, T, p, p_dev, Hl, scale_log2); break;
     default:
       if (hd > 256) throw std::runtime_error("decode_attention: head_dim must be <= 256");
       if (hd <= 64) {
-        decode_attention_any_kernel<2><<<B * Hl, 256, 0, s>>>(qkv_new, cache, out, T, p, Hl, hd, scale_log2);
+        decode_attention_any_kernel<2><<<B * Hl, 256, 0, s>>>(qkv_new, cache, out, T, p, p_dev, Hl, hd, scale_log2);
       } else if (hd <= 128) {
-        decode_attention_any_kernel<4><<<B * Hl, 256, 0, s>>>(qkv_new, cache, out, T, p, Hl, hd, scale_log2);
+        decode_attention_any_kernel<4><<<B * Hl, 256, 0, s>>>(qkv_new, cache, out, T, p, p_dev, Hl, hd, scale_log2);
       } else {
-        decode_attention_any_kernel<8><<<B * Hl, 256, 0, s>>>(qkv_new, cache, out, T, p, Hl, hd, scale_log2);
+        decode_attention_any_kernel<8><<<B * Hl, 256, 0, s>>>(qkv_new, cache, out, T, p, p_dev, Hl, hd, scale_log2);
       }
   }
 }
 
-void argmax_rows(const bf16* x, int64_t row_stride, int B, int n, int index_base, float* out, cudaStream_t s) {
-  argmax_rows_kernel<<<B, 256, 0, s>>>(x, row_stride, n, index_base, out);
+__global__ void bump_kernel(int* x) { *x += 1; }
+
+void bump_i32(int* x, cudaStream_t s) { bump_kernel<<<1, 1, 0, s>>>(x); }
+
+bool decode_attention_split(const bf16* qkv_new, bf16* cache, bf16* out, int B, int T, int p, int Hl, int hd,
+                            cudaStream_t s, const int* p_dev, float* part, unsigned int* ticket) {
+  const float scale_log2 = static_cast<float>(1.4426950408889634 / sqrt(static_cast<double>(hd)));
+  const dim3 grid(B * Hl, DSPLIT);
+  switch (hd) {
+    case 64:
+      decode_attention_split_kernel<64><<<grid, 256, 0, s>>>(qkv_new, cache, out, T, p, p_dev, Hl, scale_log2, part, ticket);
+      return true;
+    case 128:
+      decode_attention_split_kernel<128><<<grid, 256, 0, s>>>(qkv_new, cache, out, T, p, p_dev, Hl, scale_log2, part, ticket);
+      return true;
+    case 256:
+      decode_attention_split_kernel<256><<<grid, 256, 0, s>>>(qkv_new, cache, out, T, p, p_dev, Hl, scale_log2, part, ticket);
+      return true;
+    default:
+      return false;
+  }
+}
+
+int decode_split_count() { return DSPLIT; }
+
+void argmax_rows(const bf16* x, int64_t row_stride, int B, int n, int index_base, float* out, cudaStream_t s,
+                 float* scratch) {
+  // one CTA per row is a single SM streaming the whole vocabulary row: with scratch, the row is
+  // cut into up to 64 chunks of >= 1024 columns and the chunk winners are combined
+  const int C = scratch != nullptr ? std::max(1, std::min(kArgmaxChunks, n / 1024)) : 1;
+  if (C == 1) {
+    argmax_rows_kernel<<<dim3(B, 1), 256, 0, s>>>(x, row_stride, n, index_base, out);
+    return;
+  }
+  argmax_rows_kernel<<<dim3(B, C), 256, 0, s>>>(x, row_stride, n, index_base, scratch);
+  argmax_chunks_kernel<<<(B + 127) / 128, 128, 0, s>>>(scratch, C, B, out);
 }
 
 void argmax_combine(const float* parts, int shards, int B, int32_t* tok, cudaStream_t s) {

@@ -60,11 +60,24 @@ void colsum_f32(const float* X, int64_t ld, int64_t M, int N, float* out, int ac
 
 // sum of weights -> wsum[0]
 // Greedy decode (decode.cu): one new position per sequence.
-void embed_rows(const int32_t* ids, const float* tok, const float* pos, int p, float* x, int B, int d, cudaStream_t s);
-void kv_scatter(const bf16* qkv_new, bf16* cache, int B, int T, int p, int dl, cudaStream_t s);
+// p_dev (optional): read the position from the device instead of p (CUDA-graph decode steps)
+void embed_rows(const int32_t* ids, const float* tok, const float* pos, int p, float* x, int B, int d, cudaStream_t s,
+                const int* p_dev = nullptr);
+void kv_scatter(const bf16* qkv_new, bf16* cache, int B, int T, int p, int dl, cudaStream_t s,
+                const int* p_dev = nullptr);
+void bump_i32(int* x, cudaStream_t s);  // *x += 1 on the device
 void decode_attention(const bf16* qkv_new, const bf16* cache, bf16* out, int B, int T, int p, int Hl, int hd,
-                      cudaStream_t s);
-void argmax_rows(const bf16* x, int64_t row_stride, int B, int n, int index_base, float* out, cudaStream_t s);
+                      cudaStream_t s, const int* p_dev = nullptr);
+// Split-key decode attention for head_dim 64 / 128 / 256 with the kv_scatter of the new row
+// fused in (returns false for other head dims): part holds B*Hl*decode_split_count()*(hd+2)
+// floats, ticket B*Hl zero-initialised counters (never reset)
+bool decode_attention_split(const bf16* qkv_new, bf16* cache, bf16* out, int B, int T, int p, int Hl, int hd,
+                            cudaStream_t s, const int* p_dev, float* part, unsigned int* ticket);
+int decode_split_count();
+// scratch (optional, B * kArgmaxChunks * 2 floats): split each row over up to kArgmaxChunks CTAs
+constexpr int kArgmaxChunks = 64;
+void argmax_rows(const bf16* x, int64_t row_stride, int B, int n, int index_base, float* out, cudaStream_t s,
+                 float* scratch = nullptr);
 void argmax_combine(const float* parts, int shards, int B, int32_t* tok, cudaStream_t s);
 
 void sum_f32(const float* x, int64_t n, float* out, cudaStream_t s);

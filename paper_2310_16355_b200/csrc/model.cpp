@@ -111,6 +111,8 @@ Model::~Model() {
   for (cudaEvent_t e : ev_prod_) cudaEventDestroy(e);
   for (cudaEvent_t e : ev_ar_) cudaEventDestroy(e);
   if (comm_stream_) cudaStreamDestroy(comm_stream_);
+  if (dec_graph_) cudaGraphExecDestroy(dec_graph_);
+  if (dec_out_) cudaFree(dec_out_);
   for (void* p : allocations_) cudaFree(p);
   if (stream_) cudaStreamDestroy(stream_);
 }
@@ -1392,8 +1394,9 @@ void Model::pick_tokens(std::vector<Rank*>& grp, const std::vector<const bf16*>&
     DecodeBufs& D = dec_[static_cast<size_t>(&R - ranks_.data())];
     const int shard = th_ > 1 ? R.mpi : 0;
     if (th_ > 1) cuda_check(cudaMemsetAsync(D.arg, 0, sizeof(float) * 2 * B * th_, stream_), "memset");
-    k::argmax_rows(rows[i], stride, B, vl_, shard * vl_, D.arg + static_cast<int64_t>(shard) * 2 * B, stream_);
-    ++launches_;
+    k::argmax_rows(rows[i], stride, B, vl_, shard * vl_, D.arg + static_cast<int64_t>(shard) * 2 * B, stream_,
+                   D.argpart);
+    launches_ += 2;
   }
   if (th_ > 1) {
     std::vector<float*> ptrs;
@@ -1429,9 +1432,11 @@ void Model::window_forward(std::vector<Rank*>& grp, const std::vector<std::vecto
 
 void Model::decode_step(std::vector<Rank*>& grp, int p) {
   const int B = B_, d = d_, dl = dl_, fl = fl_;
+  const bool dev_pos = p < 0;
+  auto pd = [&](Rank& R) -> const int* { return dev_pos ? dec_[static_cast<size_t>(&R - ranks_.data())].pos : nullptr; };
   for (Rank* R : grp) {
     DecodeBufs& D = dec_[static_cast<size_t>(R - ranks_.data())];
-    k::embed_rows(D.tok, P(*R, tok_), P(*R, pos_), p, D.x, B, d, stream_);
+    k::embed_rows(D.tok, P(*R, tok_), P(*R, pos_), p, D.x, B, d, stream_, pd(*R));
     ++launches_;
   }
   auto each = [&](auto&& fn) {
@@ -1450,9 +1455,14 @@ void Model::decode_step(std::vector<Rank*>& grp, int p) {
       ++launches_;
       gemm(R, B, 3 * dl, d, D.a, d, 0, W(R, ls.q_k), d, 0, static_cast<int>(Epi::kStoreBf16), D.qkv, 3 * dl, nullptr,
            0, P(R, ls.q_b) + R.mpi * dl, nullptr, 0, 0, dl, d);
-      k::kv_scatter(D.qkv, R.qkv[l], B, T_, p, dl, stream_);
-      k::decode_attention(D.qkv, R.qkv[l], D.o, B, T_, p, hl_, hd_, stream_);
-      launches_ += 2;
+      if (k::decode_attention_split(D.qkv, R.qkv[l], D.o, B, T_, p, hl_, hd_, stream_, pd(R), D.attn_part,
+                                    D.attn_ticket)) {
+        ++launches_;
+      } else {
+        k::kv_scatter(D.qkv, R.qkv[l], B, T_, p, dl, stream_, pd(R));
+        k::decode_attention(D.qkv, R.qkv[l], D.o, B, T_, p, hl_, hd_, stream_, pd(R));
+        launches_ += 2;
+      }
       if (ta_ == 1) {
         gemm(R, B, d, dl, D.o, dl, 0, W(R, ls.o_k), dl, 0, static_cast<int>(Epi::kResidF32), D.xmid, d, nullptr, 0,
              P(R, ls.o_b), D.x, d);
@@ -1503,6 +1513,12 @@ void Model::decode_step(std::vector<Rank*>& grp, int p) {
     rows.push_back(D.logits);
   });
   pick_tokens(grp, rows, ldv_);
+  if (dev_pos) {
+    each([&](Rank&, DecodeBufs& D) {
+      k::bump_i32(D.pos, stream_);
+      ++launches_;
+    });
+  }
 }
 
 void Model::generate(const int32_t* prompts, int P, int n_new, int32_t* out) {
@@ -1529,6 +1545,11 @@ void Model::generate(const int32_t* prompts, int P, int n_new, int32_t* out) {
       D.f = alloc<bf16>(B * d_);
       D.logits = alloc<bf16>(B * ldv_);
       D.tok = alloc<int32_t>(B);
+      D.pos = alloc<int>(1);
+      D.attn_part = alloc<float>(B * hl_ * k::decode_split_count() * (hd_ + 2));
+      D.attn_ticket = alloc<unsigned int>(B * hl_);
+      D.argpart = alloc<float>(B * k::kArgmaxChunks * 2);
+      cuda_check(cudaMemset(D.attn_ticket, 0, sizeof(unsigned int) * B * hl_), "memset");
       dec_.push_back(D);
     }
   }
@@ -1536,21 +1557,86 @@ void Model::generate(const int32_t* prompts, int P, int n_new, int32_t* out) {
   DecodeBufs& D0 = dec_[static_cast<size_t>(grp[0] - ranks_.data())];
   std::vector<std::vector<int32_t>> ctx(static_cast<size_t>(B_));
   for (int b = 0; b < B_; ++b) ctx[static_cast<size_t>(b)].assign(prompts + static_cast<int64_t>(b) * P, prompts + static_cast<int64_t>(b + 1) * P);
-  std::vector<int32_t> tok(static_cast<size_t>(B_));
-  for (int i = 0; i < n_new; ++i) {
-    const int len = static_cast<int>(ctx[0].size());  // context before this step's token
-    if (i == 0 || len > T_) {
-      window_forward(grp, ctx, len < T_ ? len : T_);  // prefill, or the sliding window
-    } else {
-      decode_step(grp, len - 1);  // the newest token sits at position len - 1
-    }
-    cuda_check(cudaMemcpyAsync(tok.data(), D0.tok, B_ * 4, cudaMemcpyDeviceToHost, stream_), "D2H");
-    cuda_check(cudaStreamSynchronize(stream_), "generate");
-    for (int b = 0; b < B_; ++b) {
-      out[static_cast<int64_t>(b) * n_new + i] = tok[static_cast<size_t>(b)];
-      ctx[static_cast<size_t>(b)].push_back(tok[static_cast<size_t>(b)]);
-    }
+  // Cached steps are data-independent of the host (the new token stays on the device, the
+  // position is known), so they run back to back: each one is a single CUDA-graph launch (the
+  // emulated mesh; NCCL ranks launch eagerly) whose tokens are copied into dec_out_ and read back
+  // once, before the window slides or at the end. SW_DECODE_GRAPH=0: eager launches.
+  static const bool graph_on = [] {
+    const char* e = std::getenv("SW_DECODE_GRAPH");
+    return !(e != nullptr && e[0] == '0');
+  }();
+  const bool use_graph = graph_on && mesh_->emulated && !prof_;
+  if (dec_out_cap_ < static_cast<int64_t>(n_new) * B_) {
+    if (dec_out_ != nullptr) cudaFree(dec_out_);
+    dec_out_ = nullptr;
+    cuda_check(cudaMalloc(&dec_out_, sizeof(int32_t) * n_new * B_), "cudaMalloc");
+    dec_out_cap_ = static_cast<int64_t>(n_new) * B_;
   }
+  std::vector<int32_t> tok(static_cast<size_t>(B_));
+  int pending = 0;  // cached steps whose tokens are still only on the device
+  auto flush = [&](int upto) {  // read back steps [upto - pending, upto)
+    if (pending == 0) return;
+    std::vector<int32_t> buf(static_cast<size_t>(pending) * B_);
+    cuda_check(cudaMemcpyAsync(buf.data(), dec_out_, buf.size() * 4, cudaMemcpyDeviceToHost, stream_), "D2H");
+    cuda_check(cudaStreamSynchronize(stream_), "generate");
+    for (int j = 0; j < pending; ++j) {
+      const int i = upto - pending + j;
+      for (int b = 0; b < B_; ++b) {
+        const int32_t t = buf[static_cast<size_t>(j) * B_ + b];
+        out[static_cast<int64_t>(b) * n_new + i] = t;
+        ctx[static_cast<size_t>(b)].push_back(t);
+      }
+    }
+    pending = 0;
+  };
+  int len = P;  // context length before step i's token
+  for (int i = 0; i < n_new; ++i, ++len) {
+    if (i == 0 || len > T_) {
+      flush(i);
+      window_forward(grp, ctx, len < T_ ? len : T_);  // prefill, or the sliding window
+      cuda_check(cudaMemcpyAsync(tok.data(), D0.tok, B_ * 4, cudaMemcpyDeviceToHost, stream_), "D2H");
+      cuda_check(cudaStreamSynchronize(stream_), "generate");
+      for (int b = 0; b < B_; ++b) {
+        out[static_cast<int64_t>(b) * n_new + i] = tok[static_cast<size_t>(b)];
+        ctx[static_cast<size_t>(b)].push_back(tok[static_cast<size_t>(b)]);
+      }
+      continue;
+    }
+    // the newest token sits at position len - 1
+    if (pending == 0) {
+      for (Rank* R : grp) {
+        const int p0 = len - 1;
+        cuda_check(cudaMemcpyAsync(dec_[static_cast<size_t>(R - ranks_.data())].pos, &p0, sizeof(int),
+                                   cudaMemcpyHostToDevice, stream_),
+                   "H2D");
+        cuda_check(cudaStreamSynchronize(stream_), "generate");  // p0 is a stack value
+      }
+    }
+    if (use_graph) {
+      if (dec_graph_ == nullptr) {
+        cudaGraph_t g = nullptr;
+        cuda_check(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal), "capture");
+        try {
+          decode_step(grp, -1);
+        } catch (...) {
+          cudaStreamEndCapture(stream_, &g);
+          if (g != nullptr) cudaGraphDestroy(g);
+          throw;
+        }
+        cuda_check(cudaStreamEndCapture(stream_, &g), "capture");
+        cuda_check(cudaGraphInstantiate(&dec_graph_, g, 0), "cudaGraphInstantiate");
+        cudaGraphDestroy(g);
+      }
+      cuda_check(cudaGraphLaunch(dec_graph_, stream_), "cudaGraphLaunch");
+    } else {
+      decode_step(grp, -1);
+    }
+    cuda_check(cudaMemcpyAsync(dec_out_ + static_cast<int64_t>(pending) * B_, D0.tok, B_ * 4, cudaMemcpyDeviceToDevice,
+                               stream_),
+               "D2D");
+    ++pending;
+  }
+  flush(n_new);
 }
 
 double Model::last_loss() {

@@ -237,8 +237,16 @@ class Model {
     float *x = nullptr, *xmid = nullptr, *part = nullptr, *stats = nullptr, *arg = nullptr;
     bf16 *a = nullptr, *qkv = nullptr, *o = nullptr, *pre = nullptr, *h = nullptr, *f = nullptr, *logits = nullptr;
     int32_t* tok = nullptr;
+    int* pos = nullptr;  // device position of the cached step (read by the CUDA-graph step)
+    float* attn_part = nullptr;       // split-key decode attention partials
+    unsigned int* attn_ticket = nullptr;
+    float* argpart = nullptr;  // per-chunk argmax winners
   };
   std::vector<DecodeBufs> dec_;  // per local rank, allocated on the first generate()
+  int32_t* dec_out_ = nullptr;   // [n_cap, B] tokens of cached steps, read back in batches
+  int64_t dec_out_cap_ = 0;
+  cudaGraphExec_t dec_graph_ = nullptr;  // one cached decode step, position on the device
+  // p >= 0: position p (host value); p < 0: every rank's dec_[].pos, advanced at the step's end
   void decode_step(std::vector<Rank*>& grp, int p);
   void window_forward(std::vector<Rank*>& grp, const std::vector<std::vector<int32_t>>& ctx, int take);
   // argmax of one logits row per sequence (per-rank base pointer, row stride in elements) into

@@ -48,6 +48,27 @@ CUtensorMap make_tmap_bf16_2d(const void* ptr, uint64_t inner, uint64_t outer, u
   return map;
 }
 
+CUtensorMap make_tmap_bf16_2d_plain(const void* ptr, uint64_t inner, uint64_t outer, uint64_t ld,
+                                    uint32_t box_inner, uint32_t box_outer) {
+  if ((reinterpret_cast<uintptr_t>(ptr) & 15u) != 0 || (ld * 2) % 16 != 0) {
+    throw std::runtime_error("tensor map: base must be 16-byte aligned and pitch a multiple of 8 "
+                             "bf16 elements (ld=" + std::to_string(ld) + ")");
+  }
+  CUtensorMap map;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {ld * 2};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode_fn()(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims,
+                           strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    throw std::runtime_error("cuTensorMapEncodeTiled(2d plain) failed with code " + std::to_string(r));
+  }
+  return map;
+}
+
 CUtensorMap make_tmap_f32_2d(const void* ptr, uint64_t inner, uint64_t outer, uint64_t ld, uint32_t box_inner,
                              uint32_t box_outer) {
   if ((reinterpret_cast<uintptr_t>(ptr) & 15u) != 0 || (ld * 4) % 16 != 0) {

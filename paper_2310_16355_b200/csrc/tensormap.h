@@ -26,6 +26,11 @@ CUtensorMap make_tmap_f32_2d(const void* ptr, uint64_t inner, uint64_t outer, ui
 CUtensorMap make_tmap_bf16_2d_rowswz(const void* ptr, uint64_t inner, uint64_t outer, uint64_t ld,
                                      uint32_t box_inner, uint32_t box_outer);
 
+// 2-D bf16 tensor map without swizzle (box_inner * 2 bytes a multiple of 16, box_inner <= 256):
+// plain row-major boxes for streaming kernels
+CUtensorMap make_tmap_bf16_2d_plain(const void* ptr, uint64_t inner, uint64_t outer, uint64_t ld,
+                                    uint32_t box_inner, uint32_t box_outer);
+
 int device_sm_count();
 
 }  // namespace sw

@@ -224,9 +224,10 @@ def test_gemm_swiglu_fwd_bwd(M, N, K):
 
 @pytest.mark.parametrize("M", [1, 3, 8])
 @pytest.mark.parametrize("epi", [0, 1, 3])
-def test_small_m_gemv_path(M, epi):
-    """M <= 8 forward GEMMs (the decode step) take the weight-streaming path; same epilogues."""
-    N, K = 200, 136
+@pytest.mark.parametrize("N,K", [(200, 136), (4096, 1376), (12288, 4096)])
+def test_small_m_gemv_path(M, epi, N, K):
+    """M <= 8 forward GEMMs (the decode step) take the TMA-streamed weight path (8-row groups,
+    256-column boxes: K = 1376 ends in a partial box, N = 200 in a partial group); same epilogues."""
     gen = torch.Generator(device=DEV).manual_seed(M * 10 + epi)
     A, B, ref = _ref_operands(M, N, K, 0, 0, gen)
     bias = torch.randn(N, generator=gen, device=DEV)

@@ -210,3 +210,34 @@ def test_attention_lazy_rescale_path(hd):
     want_o, want_lse = ref_attention(qkv, B, T, Hl, hd)
     assert rel(o, want_o) < 1e-2
     assert ((lse - want_lse).abs() / want_lse.abs().clamp_min(1)).max().item() < 1e-3
+
+
+@pytest.mark.parametrize("hd", [64, 128, 256])
+@pytest.mark.parametrize("p", [0, 5, 17, 200, 1023])
+@pytest.mark.parametrize("split", [0, 1])
+def test_decode_attention_step(hd, p, split):
+    """One KV-cached decode step against torch fp32 attention of the new query over keys 0..p,
+    where key / value p are the step's own (written into cache row p by the kernel)."""
+    L = _lib.lib()
+    B, T, Hl = 3, 1024, 4
+    Dl = Hl * hd
+    g = torch.Generator(device=DEV).manual_seed(hd * 7 + p)
+    cache = torch.randn(B * T, 3 * Dl, generator=g, device=DEV).bfloat16()
+    new = torch.randn(B, 3 * Dl, generator=g, device=DEV).bfloat16()
+    out = torch.empty(B, Dl, device=DEV, dtype=torch.bfloat16)
+    part = torch.empty(B * Hl * 16 * (hd + 2), device=DEV)
+    ticket = torch.zeros(B * Hl, device=DEV, dtype=torch.int32)
+    want_cache = cache.clone().view(B, T, 3 * Dl)
+    want_cache[:, p, Dl:] = new[:, Dl:]
+    for rep in range(2):  # the second launch exercises the never-reset split tickets
+        c = cache.clone()
+        _lib.check(L.sw_k_decode_attention(new.data_ptr(), c.data_ptr(), out.data_ptr(), B, T, p, Hl, hd, split,
+                                           part.data_ptr(), ticket.data_ptr(), None))
+        torch.cuda.synchronize()
+        assert torch.equal(c.view(B, T, 3 * Dl)[:, p, Dl:], new[:, Dl:])
+        kv = want_cache[:, : p + 1].float()
+        q = new[:, :Dl].float().view(B, Hl, 1, hd)
+        k = kv[..., Dl:2 * Dl].view(B, p + 1, Hl, hd).transpose(1, 2)
+        v = kv[..., 2 * Dl:].view(B, p + 1, Hl, hd).transpose(1, 2)
+        ref = torch.softmax(q @ k.transpose(-1, -2) / math.sqrt(hd), -1) @ v
+        assert rel(out, ref.view(B, Dl)) < 1e-2, (rep, rel(out, ref.view(B, Dl)))
