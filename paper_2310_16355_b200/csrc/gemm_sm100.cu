@@ -50,6 +50,15 @@ constexpr int NUM_THREADS = 256;
 #define SW_GROUP_M 8
 #endif
 constexpr int GROUP_M = SW_GROUP_M;  // tile rows per raster group (operand reuse in L2)
+// CTA-pair kernel cluster size: 2 (one pair) or 4 (two pairs on adjacent n-blocks sharing their
+// A rows through TMA multicast: a quarter less operand traffic from L2). 4 passes the GEMM tests
+// but measured ~35% slower on B200 for every shape (tools/gemm_bench.py: 1000 vs 1510-1570 TF/s
+// plain, 760-780 vs 1130-1180 fused-AdamW): four-CTA clusters leave SMs of every GPC idle and
+// lock two pairs' pipelines together, so the default stays 2.
+#ifndef SW_GEMM_CL
+#define SW_GEMM_CL 2
+#endif
+constexpr int GEMM_CL = SW_GEMM_CL;
 constexpr int EPI_STAGE_BYTES = 4 * 32 * 32 * 4;  // per-warp 32x32 fp32 transpose buffers (kAdamW)
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256 + EPI_STAGE_BYTES;
 
@@ -643,7 +652,7 @@ __device__ __forceinline__ void adamw_chunk_smem(const GemmParams& p, float* sbo
 __device__ unsigned long long g_gemm_trace[1024];
 
 template <Epi EPI>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(p_threads<EPI>(), 1)
+__global__ void __cluster_dims__(GEMM_CL, 1, 1) __launch_bounds__(p_threads<EPI>(), 1)
     gemm_bf16_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                          const __grid_constant__ OptMaps om, const GemmParams p) {
   constexpr int P_STAGES = p_stages<EPI>();
@@ -665,22 +674,38 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(p_threads<EPI>(), 1)
 
   const uint32_t warp = dev::warp_idx_sync();
   const uint32_t lane = threadIdx.x & 31;
-  const uint32_t rank = dev::cluster_ctarank();
+  // cluster = GEMM_CL / 2 CTA pairs on one tile row: pair pidx of the cluster takes n-block
+  // 2 nbp + pidx of cluster tile (mb, nbp), and with GEMM_CL == 4 the two CTAs holding the same
+  // A rows (ranks prank and prank + 2) each fetch half of them and multicast it to both
+  const uint32_t crank = dev::cluster_ctarank();
+  const uint32_t rank = crank & 1u;   // rank inside the CTA pair
+  const int pidx = static_cast<int>(crank >> 1);
 
   const int num_m = (p.M + 2 * BM - 1) / (2 * BM);  // pair tiles along M (256 rows)
   constexpr bool kGlu = EPI == Epi::kSwiGLU;
   const int num_n = kGlu ? (p.N + 127) / 128 : (p.N + BN - 1) / BN;  // SwiGLU: 128 h columns per tile
   const int num_tiles = num_m * num_n;
   const int num_kb = (p.K + BK - 1) / BK;
-  const int pair = static_cast<int>(blockIdx.x) >> 1;
-  const int npairs = static_cast<int>(gridDim.x) >> 1;
+  const int pair = static_cast<int>(blockIdx.x) / GEMM_CL;     // cluster index
+  const int npairs = static_cast<int>(gridDim.x) / GEMM_CL;
+  const int num_nc = GEMM_CL == 4 ? (num_n + 1) / 2 : num_n;   // n-block units per cluster tile
+  const int num_units = num_m * num_nc;
+  auto pair_tile = [&](int t, int& mb, int& nb) {
+    if constexpr (GEMM_CL == 4) {
+      int nbp;
+      tile_coords(t, num_m, num_nc, mb, nbp);
+      nb = 2 * nbp + pidx;  // past num_n on an odd tail: B reads zeros, the epilogue stores nothing
+    } else {
+      tile_coords(t, num_m, num_n, mb, nb);
+    }
+  };
 
   if (warp == 0 && lane == 0) {
     dev::tma_prefetch_desc(&tmA);
     dev::tma_prefetch_desc(&tmB);
     for (int s = 0; s < P_STAGES; ++s) {
       dev::mbar_init(&full[s], 1);
-      dev::mbar_init(&empty[s], 1);
+      dev::mbar_init(&empty[s], GEMM_CL / 2);  // one MMA commit per pair of the cluster
     }
     for (int a = 0; a < 2; ++a) {
       dev::mbar_init(&tfull[a], 1);
@@ -703,9 +728,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(p_threads<EPI>(), 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = pair; t < num_tiles; t += npairs) {
+      for (int t = pair; t < num_units; t += npairs) {
         int mb, nb;
-        tile_coords(t, num_m, num_n, mb, nb);
+        pair_tile(t, mb, nb);
         const int m0 = mb * 2 * BM + static_cast<int>(rank) * BM;
         // SwiGLU: CTA 0 stages the tile's 128 gate rows, CTA 1 the matching 128 up rows
         const int n0 = kGlu ? (rank == 0 ? nb * 128 : p.swiglu_half + nb * 128)
@@ -716,7 +741,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(p_threads<EPI>(), 1)
           const int k0 = kb * BK;
           uint8_t* a_dst = sA + stage * P_A_STAGE;
           uint8_t* b_dst = sB + stage * P_B_STAGE;
-          if (!p.a_mn_major) {
+          if constexpr (GEMM_CL == 4) {
+            // 64 of the 128 A rows (K-major: one [64 k x 64 rows] box; MN-major: one of the two
+            // [64 rows x 64 k] boxes), landing in both CTAs that hold these rows
+            const uint16_t mc = static_cast<uint16_t>((1u << rank) | (1u << (rank + 2)));
+            if (!p.a_mn_major) {
+              dev::tma_load_2d_2sm_mc(a_dst + pidx * 8192, &tmA, &full[stage], k0, m0 + 64 * pidx, mc);
+            } else {
+              dev::tma_load_2d_2sm_mc(a_dst + pidx * 8192, &tmA, &full[stage], m0 + 64 * pidx, k0, mc);
+            }
+          } else if (!p.a_mn_major) {
             dev::tma_load_2d_2sm(a_dst, &tmA, &full[stage], k0, m0);
           } else {
             dev::tma_load_2d_2sm(a_dst, &tmA, &full[stage], m0, k0);
@@ -752,7 +786,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(p_threads<EPI>(), 1)
       uint32_t acc_phase = 0;
       const bool tr = static_cast<int>(blockIdx.x) == p.trace_cta;
       int ti = 0;
-      for (int t = pair; t < num_tiles; t += npairs, ++ti) {
+      for (int t = pair; t < num_units; t += npairs, ++ti) {
         dev::mbar_wait(&tempty[acc], acc_phase ^ 1);
         dev::tc_fence_after();
         if (tr && lane == 0 && ti < 64) g_gemm_trace[8 * ti] = clock64();
@@ -769,7 +803,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(p_threads<EPI>(), 1)
 #pragma unroll
             for (int k = 0; k < BK / 16; ++k)
               dev::umma_f16_ss_2sm(d_tmem, as + k * a_step, bs + k * b_step, idesc, (kb | k) != 0 ? 1u : 0u);
-            dev::umma_commit_2sm(&empty[stage], 0x3);
+            // the stage is free once every pair that reads or multicasts into it is done
+            dev::umma_commit_2sm(&empty[stage], GEMM_CL == 4 ? 0xF : 0x3);
           }
           __syncwarp();
           if (++stage == P_STAGES) {
@@ -777,7 +812,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(p_threads<EPI>(), 1)
             phase ^= 1;
           }
         }
-        if (dev::elect_one_sync()) dev::umma_commit_2sm(&tfull[acc], 0x3);
+        if (dev::elect_one_sync()) dev::umma_commit_2sm(&tfull[acc], static_cast<uint16_t>(0x3u << (2 * pidx)));
         __syncwarp();
         if (tr && lane == 0 && ti < 64) {
           g_gemm_trace[8 * ti + 1] = clock64();
@@ -797,9 +832,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(p_threads<EPI>(), 1)
         dev::tma_prefetch_desc(&om.m);
         dev::tma_prefetch_desc(&om.v);
         uint32_t uses[OPT_NBUF] = {0, 0};
-        for (int t = pair; t < num_tiles; t += npairs) {
+        for (int t = pair; t < num_units; t += npairs) {
           int mb, nb;
-          tile_coords(t, num_m, num_n, mb, nb);
+          pair_tile(t, mb, nb);
           const int r0 = mb * 2 * BM + static_cast<int>(rank) * BM;
           const int n_left = p.N - nb * BN;
           // chunk c of the tile goes to buffer c & 1, i.e. to epilogue warpgroup c & 1
@@ -829,12 +864,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(p_threads<EPI>(), 1)
     const uint32_t q = warp & 3;
     const int wg = (static_cast<int>(warp) - 4) >> 2;
     float4* stage = reinterpret_cast<float4*>(sOpt) + (static_cast<int>(warp) - 4) * 256;
-    const uint32_t tempty_leader = dev::mapa_shared(dev::smem_u32(&tempty[0]), 0);
+    const uint32_t tempty_leader = dev::mapa_shared(dev::smem_u32(&tempty[0]), crank & ~1u);
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int t = pair; t < num_tiles; t += npairs) {
+    for (int t = pair; t < num_units; t += npairs) {
       int mb, nb;
-      tile_coords(t, num_m, num_n, mb, nb);
+      pair_tile(t, mb, nb);
       const int row0 = mb * 2 * BM + static_cast<int>(rank) * BM + static_cast<int>(q) * 32;
       dev::mbar_wait(&tfull[acc], acc_phase);
       dev::tc_fence_after();
@@ -861,15 +896,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(p_threads<EPI>(), 1)
     // one overlaps the other's loads, math and TMA stores.
     const uint32_t q = warp & 3;
     const int wg = (static_cast<int>(warp) - 4) >> 2;
-    const uint32_t tempty_leader = dev::mapa_shared(dev::smem_u32(&tempty[0]), 0);
+    const uint32_t tempty_leader = dev::mapa_shared(dev::smem_u32(&tempty[0]), crank & ~1u);
     int acc = 0;
     uint32_t acc_phase = 0;
     uint32_t uses = 0;
     const bool tr = static_cast<int>(blockIdx.x) == p.trace_cta && lane == 0;
     int ti = 0;
-    for (int t = pair; t < num_tiles; t += npairs, ++ti) {
+    for (int t = pair; t < num_units; t += npairs, ++ti) {
       int mb, nb;
-      tile_coords(t, num_m, num_n, mb, nb);
+      pair_tile(t, mb, nb);
       const int row = mb * 2 * BM + static_cast<int>(rank) * BM + static_cast<int>(q) * 32 + static_cast<int>(lane);
       dev::mbar_wait(&tfull[acc], acc_phase);
       dev::tc_fence_after();
@@ -919,14 +954,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(p_threads<EPI>(), 1)
     const int cstep = SW_EPI_WG2 ? 2 : 1, cfirst = SW_EPI_WG2 ? (static_cast<int>(warp) - 4) >> 2 : 0;
     uint32_t rphase[2] = {0u, 0u};  // TMA residual-load barrier phases of the two staging buffers
     (void)rphase;
-    const uint32_t tempty_leader = dev::mapa_shared(dev::smem_u32(&tempty[0]), 0);
+    const uint32_t tempty_leader = dev::mapa_shared(dev::smem_u32(&tempty[0]), crank & ~1u);
     int acc = 0;
     uint32_t acc_phase = 0;
     const bool tr = static_cast<int>(blockIdx.x) == p.trace_cta && lane == 0 && warp == 4;
     int ti = 0;
-    for (int t = pair; t < num_tiles; t += npairs, ++ti) {
+    for (int t = pair; t < num_units; t += npairs, ++ti) {
       int mb, nb;
-      tile_coords(t, num_m, num_n, mb, nb);
+      pair_tile(t, mb, nb);
       const int row = mb * 2 * BM + static_cast<int>(rank) * BM + static_cast<int>(q) * 32 + static_cast<int>(lane);
       dev::mbar_wait(&tfull[acc], acc_phase);
       dev::tc_fence_after();
@@ -1184,15 +1219,16 @@ cudaError_t launch_2sm(const GemmParams& p, cudaStream_t stream) {
     if (e != cudaSuccess) return e;
     configured = true;
   }
+  // K-major A: one [64 k x 128 rows] box per stage, or half of it per multicasting CTA
   CUtensorMap ta = p.a_mn_major ? make_tmap_bf16_2d(p.A, p.M, p.K, p.lda, 64, 64)
-                                : make_tmap_bf16_2d(p.A, p.K, p.M, p.lda, 64, BM);
+                                : make_tmap_bf16_2d(p.A, p.K, p.M, p.lda, 64, GEMM_CL == 4 ? 64 : BM);
   const uint64_t b_rows = EPI == Epi::kSwiGLU ? 2ull * p.swiglu_half : static_cast<uint64_t>(p.N);
   CUtensorMap tb = p.b_mn_major ? make_tmap_bf16_2d(p.B, p.N, p.K, p.ldb, 64, 64)
                                 : make_tmap_bf16_2d(p.B, p.K, b_rows, p.ldb, 64, 128);
   const int num_n = EPI == Epi::kSwiGLU ? (p.N + 127) / 128 : (p.N + BN - 1) / BN;
-  const int num_tiles = ((p.M + 2 * BM - 1) / (2 * BM)) * num_n;
-  const int sms = (p.num_sms > 0 ? p.num_sms : device_sm_count()) & ~1;
-  const int grid = 2 * num_tiles < sms ? 2 * num_tiles : sms;
+  const int num_units = ((p.M + 2 * BM - 1) / (2 * BM)) * (GEMM_CL == 4 ? (num_n + 1) / 2 : num_n);
+  const int sms = (p.num_sms > 0 ? p.num_sms : device_sm_count()) & ~(GEMM_CL - 1);
+  const int grid = GEMM_CL * num_units < sms ? GEMM_CL * num_units : sms;
   OptMaps om{};
   if constexpr (tma_epi<EPI>()) {
     if (!p.accumulate) {
