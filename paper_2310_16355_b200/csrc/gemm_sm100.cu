@@ -11,6 +11,7 @@
 // branches of SpmdInterpreter::linear_onto (spmd.hpp:274-340) and for the linear VJP
 // matmuls emitted by autodiff (autodiff.hpp:124-139).
 #include <algorithm>
+#include <type_traits>
 #include <cstdlib>
 #include <stdexcept>
 #include <string>
@@ -1297,10 +1298,10 @@ constexpr int GEMV_COLS = SW_GEMV_COLS;  // output columns per CTA (enough CTAs 
 #endif
 // KSPLIT warp octets split K (more loads in flight per CTA: the narrow N = d_model GEMVs have
 // fewer CTAs than the HBM latency needs); UNROLL k-steps of weight loads in flight per warp.
-template <Epi EPI, int GEMV_KSPLIT, int GEMV_UNROLL>
+template <Epi EPI, int GEMV_KSPLIT, int GEMV_UNROLL, int MX>
 __global__ void __launch_bounds__(256 * GEMV_KSPLIT) gemv_bf16_kernel(const GemmParams p) {
   __shared__ float sout[GEMV_MAX_M][2 * GEMV_COLS];
-  __shared__ float spart[GEMV_KSPLIT > 1 ? GEMV_KSPLIT - 1 : 1][2 * GEMV_COLS][GEMV_MAX_M];
+  __shared__ float spart[GEMV_KSPLIT > 1 ? GEMV_KSPLIT - 1 : 1][2 * GEMV_COLS][MX];
   constexpr bool kGlu = EPI == Epi::kSwiGLU;
   constexpr int ROWS = kGlu ? 2 * GEMV_COLS : GEMV_COLS;  // SwiGLU: the gate rows and the matching up rows
   constexpr int RPW = ROWS / 8 > 0 ? ROWS / 8 : 1;         // weight rows per warp, streamed together
@@ -1329,11 +1330,11 @@ __global__ void __launch_bounds__(256 * GEMV_KSPLIT) gemv_bf16_kernel(const Gemm
                             static_cast<uint32_t>(K) * 2u);
     }
   }
-  float acc[RPW][GEMV_MAX_M];
+  float acc[RPW][MX];  // MX = the activation rows this instance handles (registers)
 #pragma unroll
   for (int j = 0; j < RPW; ++j)
 #pragma unroll
-    for (int m = 0; m < GEMV_MAX_M; ++m) acc[j][m] = 0.f;
+    for (int m = 0; m < MX; ++m) acc[j][m] = 0.f;
   const __nv_bfloat16* A = reinterpret_cast<const __nv_bfloat16*>(p.A);
 #pragma unroll GEMV_UNROLL
   for (int k = lane * 8 + ks * 256; k < K; k += 256 * GEMV_KSPLIT) {
@@ -1341,7 +1342,7 @@ __global__ void __launch_bounds__(256 * GEMV_KSPLIT) gemv_bf16_kernel(const Gemm
 #pragma unroll
     for (int j = 0; j < RPW; ++j) wv[j] = __ldcs(reinterpret_cast<const uint4*>(w[j] + k));  // streamed once
 #pragma unroll
-    for (int m = 0; m < GEMV_MAX_M; ++m) {
+    for (int m = 0; m < MX; ++m) {
       if (m < M) {
         const uint4 av = __ldg(reinterpret_cast<const uint4*>(A + static_cast<int64_t>(m) * p.lda + k));  // L1-resident
         const uint32_t aa[4] = {av.x, av.y, av.z, av.w};
@@ -1360,7 +1361,7 @@ __global__ void __launch_bounds__(256 * GEMV_KSPLIT) gemv_bf16_kernel(const Gemm
 #pragma unroll
   for (int j = 0; j < RPW; ++j) {
 #pragma unroll
-    for (int m = 0; m < GEMV_MAX_M; ++m) {
+    for (int m = 0; m < MX; ++m) {
 #pragma unroll
       for (int x = 16; x > 0; x >>= 1) acc[j][m] += __shfl_xor_sync(0xffffffffu, acc[j][m], x);
     }
@@ -1409,10 +1410,25 @@ __global__ void __launch_bounds__(256 * GEMV_KSPLIT) gemv_bf16_kernel(const Gemm
 template <Epi EPI>
 cudaError_t launch_gemv(const GemmParams& p, cudaStream_t stream) {
   const int grid = (p.N + GEMV_COLS - 1) / GEMV_COLS;
-  if (p.N <= 8192) {
-    gemv_bf16_kernel<EPI, 2, 4><<<grid, 512, 0, stream>>>(p);
+  // accumulators sized for the actual M: at M = 1 the kernel needs far fewer registers, so more
+  // CTAs (and their weight loads) are resident per SM (ncu: 80 registers capped the M <= 8
+  // instance at 3 CTAs / 37.5% warps per SM)
+  auto go = [&](auto mx) {
+    constexpr int MX = decltype(mx)::value;
+    if (p.N <= 8192) {
+      gemv_bf16_kernel<EPI, 2, 4, MX><<<grid, 512, 0, stream>>>(p);
+    } else {
+      gemv_bf16_kernel<EPI, 1, 2, MX><<<grid, 256, 0, stream>>>(p);
+    }
+  };
+  if (p.M == 1) {
+    go(std::integral_constant<int, 1>{});
+  } else if (p.M == 2) {
+    go(std::integral_constant<int, 2>{});
+  } else if (p.M <= 4) {
+    go(std::integral_constant<int, 4>{});
   } else {
-    gemv_bf16_kernel<EPI, 1, 2><<<grid, 256, 0, stream>>>(p);
+    go(std::integral_constant<int, GEMV_MAX_M>{});
   }
   return cudaGetLastError();
 }
