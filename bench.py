@@ -41,7 +41,10 @@ def parse_args():
     ap.add_argument("--spec", default=os.path.join(ROOT, "oracle", "specs", "llama7b_vocab_parallel.spec"),
                     help="model spec; the default carries `role lm_head/kernel = fully_connected` "
                          "(vocab-parallel head, SURVEY D1) - identical to llama7b.spec at TP=1")
-    ap.add_argument("--batch", type=int, default=4, help="sequences per replica per step")
+    ap.add_argument("--batch", type=int, default=8,
+                    help="sequences per replica per step (8 x 2048 tokens: 165 GB of the 180 GB at TP=1; the "
+                         "per-tile optimizer traffic of the fused wgrads is amortised over twice the tokens "
+                         "of batch 4: +3%% tokens/s at a lower clock, profiles/r2_bench_batch8_vs_4.txt)")
     ap.add_argument("--seq", type=int, default=2048)
     ap.add_argument("--profile-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
