@@ -362,7 +362,8 @@ constexpr int DV_NST = 3;
 struct DvLay {
   static constexpr int OFF_Q = 0;                     // [DV_NST]
   static constexpr int OFF_DO = OFF_Q + DV_NST * QB;  // [DV_NST]
-  static constexpr int OFF_BAR = OFF_DO + DV_NST * QB;
+  static constexpr int OFF_STAT = OFF_DO + DV_NST * QB;  // [2][64] -lse log2e of the block
+  static constexpr int OFF_BAR = OFF_STAT + 2 * BQB * 4;
   static constexpr int BYTES = OFF_BAR + 256;
 };
 constexpr uint32_t D_ACC = 0, D_K = 256, D_S = 384;  // S^T buffer b at D_S + 64 b
@@ -370,11 +371,12 @@ constexpr uint32_t D_ACC = 0, D_K = 256, D_S = 384;  // S^T buffer b at D_S + 64
 __global__ void __launch_bounds__(256, 1)
     attn_bwd_hd256_dv(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_do,
                       const bf16* __restrict__ qkv, const float* __restrict__ lse, bf16* __restrict__ dqkv, int T,
-                      int Hl, float scale_log2, int nbh) {
+                      int Hl, float scale_log2, int nbh, int trace_cta) {
   using Lay = DvLay;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sQ = smem + Lay::OFF_Q;
   uint8_t* sDO = smem + Lay::OFF_DO;
+  float* sStat = reinterpret_cast<float*>(smem + Lay::OFF_STAT);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Lay::OFF_BAR);
   uint64_t* qd_full = bars;                 // [DV_NST]
   uint64_t* qd_empty = bars + DV_NST;       // [DV_NST]
@@ -453,10 +455,13 @@ __global__ void __launch_bounds__(256, 1)
       }
       __syncwarp();
     };
+    if (lane == 0) T256(2000);
     issue_s(0);
     for (int n = 0; n < nq; ++n) {
       if (n + 1 < nq) issue_s(n + 1);  // into the buffer of P^T_{n-1}, whose dV MMA precedes it
+      if (lane == 0) T256(16 * n);
       dev::mbar_wait(&p_full[n & 1], (n >> 1) & 1);
+      if (lane == 0) T256(16 * n + 1);
       dev::tc_fence_after();
       const uint64_t bdo = ddo + (n % DV_NST) * QB16;
       if (dev::elect_one_sync()) {
@@ -482,7 +487,15 @@ __global__ void __launch_bounds__(256, 1)
     const float2 sl2 = make_float2(scale_log2, scale_log2);
     for (int n = 0; n < nq; ++n) {
       const int qs = key0 + n * BQB;
+      const bool tw = warp == 4 && lane == 0;
+      // the block's -lse log2e through shared memory (double-buffered: one barrier per block),
+      // loaded before the wait for S^T so the global load latency is hidden
+      float* st = sStat + (n & 1) * BQB;
+      if (t < BQB) st[t] = qs + t < T ? -__ldg(lse_bh + qs + t) * log2e : 0.f;
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (tw) T256(16 * n + 4);
       dev::mbar_wait(&s_full[n & 1], (n >> 1) & 1);
+      if (tw) T256(16 * n + 5);
       dev::tc_fence_after();
       const uint32_t tS = tmem + lb + D_S + (n & 1) * 64;
       uint32_t v[64];
@@ -490,12 +503,11 @@ __global__ void __launch_bounds__(256, 1)
       dev::tmem_ld_32x32b_x32(tS + 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
       dev::tmem_ld_wait();
       const bool masked = qs < key0 + 128 || qs + BQB > T || key0 + 128 > T;
+      const float2* nl2 = reinterpret_cast<const float2*>(st);
 #pragma unroll
       for (int e = 0; e < BQB / 2; ++e) {  // P^T = 2^(s * sl - lse * log2e)
         const int qq = qs + 2 * e;
-        const float l0 = qq < T ? __ldg(lse_bh + qq) : 0.f, l1 = qq + 1 < T ? __ldg(lse_bh + qq + 1) : 0.f;
-        const float2 a = dev::ffma2(make_float2(__uint_as_float(v[2 * e]), __uint_as_float(v[2 * e + 1])), sl2,
-                                    make_float2(-l0 * log2e, -l1 * log2e));
+        const float2 a = dev::ffma2(make_float2(__uint_as_float(v[2 * e]), __uint_as_float(v[2 * e + 1])), sl2, nl2[e]);
         float p0 = dev::ex2_approx(a.x), p1 = dev::ex2_approx(a.y);
         if (masked) {
           p0 = (qq < T && key < T && qq >= key) ? p0 : 0.f;
@@ -507,7 +519,9 @@ __global__ void __launch_bounds__(256, 1)
       dev::tmem_st_wait();
       dev::tc_fence_before();
       dev::mbar_arrive(&p_full[n & 1]);
+      if (tw) T256(16 * n + 6);
     }
+    if (warp == 4 && lane == 0) T256(2001);
     dev::mbar_wait(acc_done, 0);
     dev::tc_fence_after();
     acc_row_out(tmem + lb + D_ACC, dqkv + (static_cast<int64_t>(row0) + key) * ld + 2 * Dl + h * HD, key < T);
@@ -836,11 +850,19 @@ bool attention_hd256_bwd(const bf16* qkv, const bf16* o, const float* lse, const
   const int nkb = (T + 127) / 128;
   const double scale = 1.0 / std::sqrt(static_cast<double>(HD));
   const float sl = static_cast<float>(scale * 1.4426950408889634);
-  attn_bwd_hd256_dv<<<nkb * B * Hl, 256, DvLay::BYTES, s>>>(tm_q, tm_do, qkv, lse, dqkv, T, Hl, sl, B * Hl);
-  static const int trace_cta = [] {
+  // phase traces (SW_ATTN_TRACE_HD256=1 reads them): the dK/dQ pass, or with SW_ATTN_TRACE_DV=1
+  // the dV pass (tools/attn256_trace.py, tools/attn256_dv_trace.py)
+  static const int trace_cta0 = [] {
     const char* e = std::getenv("SW_ATTN_TRACE_CTA");
     return e != nullptr ? std::atoi(e) : -1;
   }();
+  static const bool trace_dv = [] {
+    const char* e = std::getenv("SW_ATTN_TRACE_DV");
+    return e != nullptr && e[0] == '1';
+  }();
+  attn_bwd_hd256_dv<<<nkb * B * Hl, 256, DvLay::BYTES, s>>>(tm_q, tm_do, qkv, lse, dqkv, T, Hl, sl, B * Hl,
+                                                           trace_dv ? trace_cta0 : -1);
+  const int trace_cta = trace_dv ? -1 : trace_cta0;
   const CUtensorMap tm_dq = make_tmap_f32_2d(dq, static_cast<uint64_t>(Dl), static_cast<uint64_t>(M),
                                              static_cast<uint64_t>(Dl), 32, BQB);
   attn_bwd_hd256_dkq<<<nkb * B * Hl, 384, DkLay::BYTES, s>>>(tm_k, tm_q, tm_do, tm_dq, qkv, lse, delta, dqkv, dq, T, Hl, sl,
