@@ -24,6 +24,11 @@ bool attention_mma_fwd_ex(const bf16* qkv, bf16* o, float* lse, int B, int T, in
 bool attention_mma_bwd_ex(const bf16* qkv, const bf16* o, const float* lse, const bf16* dout, bf16* dqkv,
                           float* scratch, int B, int T, int Hl, int hd, int causal, const float* lut, float* dlut,
                           float scale, cudaStream_t s);
+bool attention_mma_fwd_cross(const bf16* q, int64_t ldq, const bf16* kv, int64_t ldkv, int voff, bf16* o, float* lse,
+                             int B, int Tq, int Tk, int Hl, int hd, float scale, cudaStream_t s);
+bool attention_mma_bwd_cross(const bf16* q, int64_t ldq, const bf16* kv, int64_t ldkv, int voff, const bf16* o,
+                             const float* lse, const bf16* dout, bf16* dq, int64_t ld_dq, bf16* dkv, int64_t ld_dkv,
+                             float* scratch, int B, int Tq, int Tk, int Hl, int hd, float scale, cudaStream_t s);
 
 namespace {
 
@@ -201,6 +206,18 @@ bool attention_bwd_ex(const bf16* qkv, const bf16* o, const float* lse, const bf
                       float* scratch, int B, int T, int Hl, int hd, int causal, const float* lut, float* dlut,
                       float scale, cudaStream_t s) {
   return attention_mma_bwd_ex(qkv, o, lse, dout, dqkv, scratch, B, T, Hl, hd, causal, lut, dlut, scale, s);
+}
+
+bool attention_fwd_cross(const bf16* q, int64_t ldq, const bf16* kv, int64_t ldkv, int voff, bf16* o, float* lse,
+                         int B, int Tq, int Tk, int Hl, int hd, float scale, cudaStream_t s) {
+  return attention_mma_fwd_cross(q, ldq, kv, ldkv, voff, o, lse, B, Tq, Tk, Hl, hd, scale, s);
+}
+
+bool attention_bwd_cross(const bf16* q, int64_t ldq, const bf16* kv, int64_t ldkv, int voff, const bf16* o,
+                         const float* lse, const bf16* dout, bf16* dq, int64_t ld_dq, bf16* dkv, int64_t ld_dkv,
+                         float* scratch, int B, int Tq, int Tk, int Hl, int hd, float scale, cudaStream_t s) {
+  return attention_mma_bwd_cross(q, ldq, kv, ldkv, voff, o, lse, dout, dq, ld_dq, dkv, ld_dkv, scratch, B, Tq, Tk, Hl,
+                                 hd, scale, s);
 }
 
 }  // namespace k

@@ -406,9 +406,13 @@ __device__ __forceinline__ int snake_item(int round, int c, int P) {
 // already runs the next item's first S. Barrier phases count blocks / items per CTA, not per
 // item. With gridDim.x == the item count every CTA takes one item (the non-persistent launch).
 __global__ void __launch_bounds__(384, 1)
-    attn_fwd_tc2(const __grid_constant__ CUtensorMap tm, bf16* __restrict__ out, float* __restrict__ lse, int T,
-                 int Hl, float scale_log2, float scale, int nbh, int group, int causal,
-                 const float* __restrict__ lut, int trace_cta) {
+    attn_fwd_tc2(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CUtensorMap tm_kv,
+                 bf16* __restrict__ out, float* __restrict__ lse, int T, int Tk, int kcol, int vcol, int Hl,
+                 float scale_log2, float scale, int nbh, int group, int causal, const float* __restrict__ lut,
+                 int trace_cta) {
+  // T queries per sequence from tm (q at column h*HD); Tk keys from tm_kv (k at kcol + h*HD,
+  // v at vcol + h*HD). Self-attention: tm_kv == tm, Tk == T, kcol = Dl, vcol = 2 Dl (fused
+  // q|k|v); cross-attention (T5): separate encoder K/V, Tk != T allowed (non-causal, no bias).
   using Lay = Fwd2Layout;
   constexpr int HD = Lay::HD;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -435,7 +439,7 @@ __global__ void __launch_bounds__(384, 1)
   const float sc_eff = lut ? 1.f : scale;
   // the item's geometry: pair index, (batch, head), and the key blocks of each query tile
   struct Item {
-    int bh, h, row0, qa, nkv, nkv_t[2];
+    int bh, h, row0, row0k, qa, nkv, nkv_t[2];
     bool hasB;
   };
   auto item_of = [&](int idx) {
@@ -445,12 +449,14 @@ __global__ void __launch_bounds__(384, 1)
     const int pi = npair - 1 - rank_;  // heaviest pair first
     it.h = it.bh % Hl;
     it.row0 = (it.bh / Hl) * T;
+    it.row0k = (it.bh / Hl) * Tk;
     it.qa = 2 * pi;
     it.hasB = it.qa + 1 < nqb;
     // causal: key blocks up to the diagonal; otherwise (T5 encoder / cross) every key block
-    it.nkv_t[0] = causal ? it.qa + 1 : nqb;
-    it.nkv_t[1] = it.hasB ? (causal ? it.qa + 2 : nqb) : 0;
-    it.nkv = causal ? (it.hasB ? it.qa + 2 : it.qa + 1) : nqb;
+    const int nkb = (Tk + 127) / 128;
+    it.nkv_t[0] = causal ? it.qa + 1 : nkb;
+    it.nkv_t[1] = it.hasB ? (causal ? it.qa + 2 : nkb) : 0;
+    it.nkv = causal ? (it.hasB ? it.qa + 2 : it.qa + 1) : nkb;
     return it;
   };
   const int P = static_cast<int>(gridDim.x), cta = static_cast<int>(blockIdx.x);
@@ -459,6 +465,7 @@ __global__ void __launch_bounds__(384, 1)
   const uint32_t lane = threadIdx.x & 31;
   if (warp == 0 && lane == 0) {
     dev::tma_prefetch_desc(&tm);
+    dev::tma_prefetch_desc(&tm_kv);
     for (int i = 0; i < 2; ++i) {
       dev::mbar_init(&q_full[i], 1);
       dev::mbar_init(&q_empty[i], 1);
@@ -504,10 +511,10 @@ __global__ void __launch_bounds__(384, 1)
           dev::mbar_arrive_expect_tx(&kv_full[st], 2 * Lay::KV);
 #pragma unroll
           for (int c = 0; c < HD / 64; ++c) {
-            dev::tma_load_2d(sK + st * Lay::KV + c * CHUNK, &tm, &kv_full[st], Dl + it.h * HD + c * 64,
-                             it.row0 + j * 128);
-            dev::tma_load_2d(sV + st * Lay::KV + c * CHUNK, &tm, &kv_full[st], 2 * Dl + it.h * HD + c * 64,
-                             it.row0 + j * 128);
+            dev::tma_load_2d(sK + st * Lay::KV + c * CHUNK, &tm_kv, &kv_full[st], kcol + it.h * HD + c * 64,
+                             it.row0k + j * 128);
+            dev::tma_load_2d(sV + st * Lay::KV + c * CHUNK, &tm_kv, &kv_full[st], vcol + it.h * HD + c * 64,
+                             it.row0k + j * 128);
           }
         }
       }
@@ -616,11 +623,11 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll
             for (int i = 0; i < 128; ++i) v[i] = __float_as_uint(fmaf(__uint_as_float(v[i]), scale, __ldg(lr + i)));
           }
-          if ((causal && j == nk - 1) || (j + 1) * 128 > T) {
+          if ((causal && j == nk - 1) || (j + 1) * 128 > Tk) {
 #pragma unroll
             for (int i = 0; i < 128; ++i) {
               const int key = j * 128 + i;
-              if (!((!causal || key <= q) && key < T)) v[i] = __float_as_uint(-INFINITY);
+              if (!((!causal || key <= q) && key < Tk)) v[i] = __float_as_uint(-INFINITY);
             }
           }
         };
@@ -768,8 +775,11 @@ bool fwd2_enabled() {
   return on;
 }
 
+// kv == nullptr: self-attention over the fused q|k|v rows of qkv; otherwise cross-attention: q
+// rows [B*T, ldq] (column h*128), k / v rows [B*Tk, ldkv] with k at kv + h*128, v at kv + voff
 bool launch_fwd2(const bf16* qkv, bf16* o, float* lse, int B, int T, int Hl, cudaStream_t s, int causal = 1,
-                 const float* lut = nullptr, float scale_arg = 0.f) {
+                 const float* lut = nullptr, float scale_arg = 0.f, const bf16* kv = nullptr, int Tk = 0,
+                 int64_t ldq = 0, int64_t ldkv = 0, int voff = 0) {
   static bool configured = false;
   if (!configured) {
     if (cudaFuncSetAttribute(attn_fwd_tc2, cudaFuncAttributeMaxDynamicSharedMemorySize, Fwd2Layout::BYTES) !=
@@ -780,13 +790,20 @@ bool launch_fwd2(const bf16* qkv, bf16* o, float* lse, int B, int T, int Hl, cud
   }
   constexpr int HD = 128;
   const int Dl = Hl * HD;
-  const CUtensorMap tm = make_tmap_bf16_2d(qkv, 3ull * Dl, static_cast<uint64_t>(B) * T, 3ull * Dl, 64, 128);
+  const bool cross = kv != nullptr;
+  const uint64_t lq = cross ? static_cast<uint64_t>(ldq) : 3ull * Dl;
+  const CUtensorMap tm = make_tmap_bf16_2d(qkv, cross ? static_cast<uint64_t>(Dl) : 3ull * Dl,
+                                           static_cast<uint64_t>(B) * T, lq, 64, 128);
+  const CUtensorMap tm_kv = cross ? make_tmap_bf16_2d(kv, static_cast<uint64_t>(voff + Dl), static_cast<uint64_t>(B) * Tk,
+                                                      static_cast<uint64_t>(ldkv), 64, 128)
+                                  : tm;
   const int nqb = (T + 127) / 128;
   const int npair = (nqb + 1) / 2;
   const double scale = scale_arg > 0.f ? scale_arg : 1.0 / std::sqrt(static_cast<double>(HD));
   const int nitems = npair * B * Hl;
   const int grid = attn_persist() ? std::min(nitems, device_sm_count()) : nitems;
-  attn_fwd_tc2<<<grid, 384, Fwd2Layout::BYTES, s>>>(tm, o, lse, T, Hl,
+  attn_fwd_tc2<<<grid, 384, Fwd2Layout::BYTES, s>>>(tm, tm_kv, o, lse, T, cross ? Tk : T, cross ? 0 : Dl,
+                                                    cross ? voff : 2 * Dl, Hl,
                                                               static_cast<float>(scale * 1.4426950408889634),
                                                               static_cast<float>(scale), B * Hl, work_group(), causal,
                                                               lut, trace_cta());
@@ -1123,7 +1140,11 @@ __global__ void __launch_bounds__(512, 1)
                  const float* __restrict__ lse, const float* __restrict__ delta, bf16* __restrict__ dqkv, int T,
                  int Hl, float scale_log2, float scale, int nbh, int group, int trace_cta, int dq_first, int ts,
                  int causal, const float* __restrict__ lut, float* __restrict__ dlut,
-                 float* __restrict__ colsum) {
+                 float* __restrict__ colsum, int Tk, int kcol, int vcol, bf16* __restrict__ dkv, int64_t ld_dkv,
+                 int dvoff) {
+  // T queries (tm_qkv64 / tm_do64 / tm_dq rows b*T), Tk keys (tm_qkv128 rows b*Tk, k at kcol,
+  // v at vcol); dK / dV rows go to dkv (row pitch ld_dkv, dV at +dvoff). Self-attention: Tk == T,
+  // kcol = Dl, vcol = 2 Dl, dkv = dqkv + Dl, ld_dkv = 3 Dl, dvoff = Dl.
   using Lay = Bwd2Layout;
   constexpr int HD = Lay::HD;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -1147,13 +1168,14 @@ __global__ void __launch_bounds__(512, 1)
   uint64_t* ds_read = bars + 15;   // the dQ warpgroup has read dS^T_n for the bias gradient
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
 
-  const int nb = (T + 127) / 128;
+  const int nb = (Tk + 127) / 128;
   int kb, bh;
   work_item(static_cast<int>(blockIdx.x), nb, nbh, group, kb, bh);  // kb 0 = most query blocks
   const int b = bh / Hl, h = bh % Hl;
   const int Dl = Hl * HD;
   const int key0 = kb * 128;
   const int row0 = b * T;
+  const int row0k = b * Tk;
   // causal: 64-query blocks from the diagonal on; otherwise (T5 encoder / cross) all of them
   const int qbase = causal ? key0 : 0;
   const int nq = (T - qbase + BQ2 - 1) / BQ2;
@@ -1200,8 +1222,8 @@ __global__ void __launch_bounds__(512, 1)
       dev::mbar_arrive_expect_tx(kv_full, 2 * Lay::KV);
 #pragma unroll
       for (int c = 0; c < HD / 64; ++c) {
-        dev::tma_load_2d(sK + c * CHUNK, &tm_qkv128, kv_full, Dl + h * HD + c * 64, row0 + key0);
-        dev::tma_load_2d(sV + c * CHUNK, &tm_qkv128, kv_full, 2 * Dl + h * HD + c * 64, row0 + key0);
+        dev::tma_load_2d(sK + c * CHUNK, &tm_qkv128, kv_full, kcol + h * HD + c * 64, row0k + key0);
+        dev::tma_load_2d(sV + c * CHUNK, &tm_qkv128, kv_full, vcol + h * HD + c * 64, row0k + key0);
       }
       for (int n = 0; n < nq; ++n) {
         const int st = n % QST;
@@ -1343,7 +1365,7 @@ __global__ void __launch_bounds__(512, 1)
       dev::tmem_ld_32x32b_x32(t_dp + lane_base + st * BQ2 + wg * 32, pv);
       dev::tmem_ld_wait();
       // masks only where the block touches the diagonal or the sequence end (block-uniform)
-      const bool masked = (causal && qs < key0 + 128) || qs + BQ2 > T || key0 + 128 > T;
+      const bool masked = (causal && qs < key0 + 128) || qs + BQ2 > T || key0 + 128 > Tk;
       const float4* nl4 = reinterpret_cast<const float4*>(st_lse + wg * 32);
       const float4* nd4 = reinterpret_cast<const float4*>(st_del + wg * 32);
       const float2 sl2 = make_float2(scale_log2, scale_log2), sc2 = make_float2(scale, scale);
@@ -1365,8 +1387,8 @@ __global__ void __launch_bounds__(512, 1)
           float p0 = dev::ex2_approx(a.x), p1 = dev::ex2_approx(a.y);
           if (masked) {
             const int qq = qs + wg * 32 + 2 * e;
-            p0 = (qq < T && key < T && (!causal || qq >= key)) ? p0 : 0.f;
-            p1 = (qq + 1 < T && key < T && (!causal || qq + 1 >= key)) ? p1 : 0.f;
+            p0 = (qq < T && key < Tk && (!causal || qq >= key)) ? p0 : 0.f;
+            p1 = (qq + 1 < T && key < Tk && (!causal || qq + 1 >= key)) ? p1 : 0.f;
           }
           const float2 t = dev::ffma2(make_float2(__uint_as_float(pv[2 * e]), __uint_as_float(pv[2 * e + 1])), sc2,
                                       hh ? make_float2(nd.z, nd.w) : make_float2(nd.x, nd.y));
@@ -1406,16 +1428,15 @@ __global__ void __launch_bounds__(512, 1)
     dev::mbar_wait(mma_done, (nq - 1) & 1);
     dev::tc_fence_after();
     if (lane == 0 && warp == 4) ATTN_TR(4003);
-    const int64_t ld = 3LL * Dl;
-    bf16* dk_row = dqkv + (static_cast<int64_t>(row0) + key) * ld + Dl + h * HD;
-    bf16* dv_row = dk_row + Dl;
+    bf16* dk_row = dkv + (static_cast<int64_t>(row0k) + key) * ld_dkv + h * HD;
+    bf16* dv_row = dk_row + dvoff;
 #pragma unroll 1
     for (int c = wg * (HD / 64); c < (wg + 1) * (HD / 64); ++c) {
       uint32_t a[32], v[32];
       dev::tmem_ld_32x32b_x32(t_dk + lane_base + c * 32, a);
       dev::tmem_ld_32x32b_x32(t_dv + lane_base + c * 32, v);
       dev::tmem_ld_wait();
-      if (key < T) {
+      if (key < Tk) {
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           uint4 w, z;
@@ -1619,7 +1640,9 @@ __global__ void __launch_bounds__(256) dq_to_bf16_colsum(const float* __restrict
   *reinterpret_cast<float4*>(colsum + blockIdx.x * 3LL * Dl + c) = make_float4(s0, s1, s2, s3);
 }
 
-__global__ void dq_to_bf16(const float* __restrict__ acc, bf16* __restrict__ dqkv, int64_t rows, int Dl) {
+__global__ void dq_to_bf16(const float* __restrict__ acc, bf16* __restrict__ dqkv, int64_t rows, int Dl,
+                           int64_t ld_out = 0) {
+  const int64_t ld = ld_out > 0 ? ld_out : 3LL * Dl;  // default: the q columns of fused dq|dk|dv rows
   const int64_t n4 = rows * Dl / 4;
   for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n4;
        e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -1628,7 +1651,7 @@ __global__ void dq_to_bf16(const float* __restrict__ acc, bf16* __restrict__ dqk
     uint2 w;
     w.x = dev::pack_bf16x2(v.x, v.y);
     w.y = dev::pack_bf16x2(v.z, v.w);
-    *reinterpret_cast<uint2*>(dqkv + r * 3LL * Dl + c) = w;
+    *reinterpret_cast<uint2*>(dqkv + r * ld + c) = w;
   }
 }
 
@@ -1640,10 +1663,15 @@ bool bwd2_enabled() {
   return on;
 }
 
+// kv == nullptr: self-attention over fused q|k|v rows (gradients into the fused dqkv rows);
+// otherwise cross-attention: q [B*T, ldq], k|v [B*Tk, ldkv] (v at +voff), dq [B*T, ld_dq],
+// dk|dv [B*Tk, ld_dkv] (dv at +voff)
 bool launch_bwd2(const bf16* qkv, const bf16* o, const float* lse, const bf16* dout, bf16* dqkv, float* scratch,
                  int B, int T, int Hl, cudaStream_t s, int causal = 1, const float* lut = nullptr,
                  float* dlut = nullptr, float scale_arg = 0.f, bool delta_ready = false,
-                 float* colsum = nullptr, bool* colsum_done = nullptr) {
+                 float* colsum = nullptr, bool* colsum_done = nullptr, const bf16* kv = nullptr, int Tk = 0,
+                 int64_t ldq = 0, int64_t ldkv = 0, int voff = 0, bf16* dkv = nullptr, int64_t ld_dq = 0,
+                 int64_t ld_dkv = 0) {
   constexpr int HD = 128;
   static bool configured = false;
   if (!configured) {
@@ -1659,25 +1687,33 @@ bool launch_bwd2(const bf16* qkv, const bf16* o, const float* lse, const bf16* d
   float* dq = scratch + ((M * Hl + 63) / 64) * 64;
   cudaMemsetAsync(dq, 0, sizeof(float) * M * Dl, s);
   if (!delta_ready) launch_delta(o, dout, delta, T, Hl, HD, M, s);
-  const CUtensorMap tm_qkv64 = make_tmap_bf16_2d(qkv, 3ull * Dl, static_cast<uint64_t>(M), 3ull * Dl, 64, BQ2);
-  const CUtensorMap tm_qkv128 = make_tmap_bf16_2d(qkv, 3ull * Dl, static_cast<uint64_t>(M), 3ull * Dl, 64, 128);
+  const bool cross = kv != nullptr;
+  const CUtensorMap tm_qkv64 =
+      cross ? make_tmap_bf16_2d(qkv, static_cast<uint64_t>(Dl), static_cast<uint64_t>(M), static_cast<uint64_t>(ldq), 64,
+                                BQ2)
+            : make_tmap_bf16_2d(qkv, 3ull * Dl, static_cast<uint64_t>(M), 3ull * Dl, 64, BQ2);
+  const CUtensorMap tm_qkv128 =
+      cross ? make_tmap_bf16_2d(kv, static_cast<uint64_t>(voff + Dl), static_cast<uint64_t>(B) * Tk,
+                                static_cast<uint64_t>(ldkv), 64, 128)
+            : make_tmap_bf16_2d(qkv, 3ull * Dl, static_cast<uint64_t>(M), 3ull * Dl, 64, 128);
   const CUtensorMap tm_do64 = make_tmap_bf16_2d(dout, static_cast<uint64_t>(Dl), static_cast<uint64_t>(M),
                                                 static_cast<uint64_t>(Dl), 64, BQ2);
   const CUtensorMap tm_dq = make_tmap_f32_2d(dq, static_cast<uint64_t>(Dl), static_cast<uint64_t>(M),
                                              static_cast<uint64_t>(Dl), 32, BQ2);
-  const int nb = (T + 127) / 128;
+  const int nb = ((cross ? Tk : T) + 127) / 128;
   const double scale = scale_arg > 0.f ? scale_arg : 1.0 / std::sqrt(static_cast<double>(HD));
   // bias-gradient partials need 32-row groups that never straddle two sequences
-  float* cs = (colsum != nullptr && T % 32 == 0) ? colsum : nullptr;
-  attn_bwd_tc2<<<nb * B * Hl, 512, Bwd2Layout::BYTES, s>>>(tm_qkv64, tm_qkv128, tm_do64, tm_dq, lse, delta, dqkv,
-                                                          T, Hl, static_cast<float>(scale * 1.4426950408889634),
-                                                          static_cast<float>(scale), B * Hl, work_group(), trace_cta(), bwd_dq_first(),
-                                                          (lut || dlut) ? 1 : bwd_ts(), causal, lut, dlut, cs);
+  float* cs = (colsum != nullptr && T % 32 == 0 && !cross) ? colsum : nullptr;
+  attn_bwd_tc2<<<nb * B * Hl, 512, Bwd2Layout::BYTES, s>>>(
+      tm_qkv64, tm_qkv128, tm_do64, tm_dq, lse, delta, dqkv, T, Hl, static_cast<float>(scale * 1.4426950408889634),
+      static_cast<float>(scale), B * Hl, work_group(), trace_cta(), bwd_dq_first(), (lut || dlut) ? 1 : bwd_ts(),
+      causal, lut, dlut, cs, cross ? Tk : T, cross ? 0 : Dl, cross ? voff : 2 * Dl, cross ? dkv : dqkv + Dl,
+      cross ? ld_dkv : 3LL * Dl, cross ? voff : Dl);
   if (cs != nullptr) {
     dq_to_bf16_colsum<<<dim3(static_cast<unsigned>((M + 31) / 32), (Dl + 1023) / 1024), 256, 0, s>>>(dq, dqkv, M, Dl,
                                                                                                       cs);
   } else {
-    dq_to_bf16<<<1184, 256, 0, s>>>(dq, dqkv, M, Dl);
+    dq_to_bf16<<<1184, 256, 0, s>>>(dq, dqkv, M, Dl, cross ? ld_dq : 0);
   }
   if (colsum_done != nullptr) *colsum_done = cs != nullptr;
   return true;
@@ -1757,6 +1793,22 @@ bool attention_mma_fwd(const bf16* qkv, bf16* o, float* lse, int B, int T, int H
   if (hd == 128) return fwd2_enabled() ? launch_fwd2(qkv, o, lse, B, T, Hl, s) : launch_fwd<128>(qkv, o, lse, B, T, Hl, s);
   if (hd == 64) return launch_fwd<64>(qkv, o, lse, B, T, Hl, s);
   return false;
+}
+
+// Cross-attention (T5, non-causal, no bias) for head_dim 128 on the tensor cores: queries [B*Tq]
+// of q (row pitch ldq), keys / values [B*Tk] of kv (k at column h*128, v at voff + h*128).
+bool attention_mma_fwd_cross(const bf16* q, int64_t ldq, const bf16* kv, int64_t ldkv, int voff, bf16* o, float* lse,
+                             int B, int Tq, int Tk, int Hl, int hd, float scale, cudaStream_t s) {
+  if (hd != 128 || ldq % 8 != 0 || ldkv % 8 != 0 || voff % 8 != 0) return false;
+  return launch_fwd2(q, o, lse, B, Tq, Hl, s, 0, nullptr, scale, kv, Tk, ldq, ldkv, voff);
+}
+
+bool attention_mma_bwd_cross(const bf16* q, int64_t ldq, const bf16* kv, int64_t ldkv, int voff, const bf16* o,
+                             const float* lse, const bf16* dout, bf16* dq, int64_t ld_dq, bf16* dkv, int64_t ld_dkv,
+                             float* scratch, int B, int Tq, int Tk, int Hl, int hd, float scale, cudaStream_t s) {
+  if (hd != 128 || ldq % 8 != 0 || ldkv % 8 != 0 || voff % 8 != 0 || ld_dq % 4 != 0 || !bwd2_enabled()) return false;
+  return launch_bwd2(q, o, lse, dout, dq, scratch, B, Tq, Hl, s, 0, nullptr, nullptr, scale, false, nullptr, nullptr,
+                     kv, Tk, ldq, ldkv, voff, dkv, ld_dq, ld_dkv);
 }
 
 bool attention_mma_bwd_ex(const bf16* qkv, const bf16* o, const float* lse, const bf16* dout, bf16* dqkv,

@@ -171,6 +171,14 @@ bool attention_fwd_ex(const bf16* qkv, bf16* o, float* lse, int B, int T, int Hl
 bool attention_bwd_ex(const bf16* qkv, const bf16* o, const float* lse, const bf16* dout, bf16* dqkv,
                       float* scratch, int B, int T, int Hl, int hd, int causal, const float* lut, float* dlut,
                       float scale, cudaStream_t s);
+// Cross-attention on the tensor cores (head_dim 128, non-causal, no bias): q [B*Tq] rows of
+// pitch ldq, k | v [B*Tk] rows of pitch ldkv with v at +voff; backward writes dq (pitch ld_dq)
+// and dk | dv (pitch ld_dkv, dv at +voff). false = not handled (use the CUDA-core kernels).
+bool attention_fwd_cross(const bf16* q, int64_t ldq, const bf16* kv, int64_t ldkv, int voff, bf16* o, float* lse,
+                         int B, int Tq, int Tk, int Hl, int hd, float scale, cudaStream_t s);
+bool attention_bwd_cross(const bf16* q, int64_t ldq, const bf16* kv, int64_t ldkv, int voff, const bf16* o,
+                         const float* lse, const bf16* dout, bf16* dq, int64_t ld_dq, bf16* dkv, int64_t ld_dkv,
+                         float* scratch, int B, int Tq, int Tk, int Hl, int hd, float scale, cudaStream_t s);
 // lut[h][d + T - 1] = table[bucket[d + T - 1], h0 + h] for d in (-T, T); zero padding to 2T + 128
 void t5_lut_build(const float* table, const int32_t* bucket, int H, int h0, int Hl, int T, float* lut, cudaStream_t s);
 // table_grad[bucket[i], h0 + h] += dlut[h][i] for i < 2T - 1

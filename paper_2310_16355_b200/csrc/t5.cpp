@@ -69,7 +69,9 @@ T5Model::T5Model(const ModelSpec& spec, const Plan& plan, Mesh* mesh, int batch,
   fused_x_ = Te_ == Td_;
   {
     const char* e = std::getenv("SW_T5_TC");
-    tc_ = fused_x_ && dk_ == 128 && Te_ + 128 <= 4096 && !(e != nullptr && e[0] == '0');
+    // tcgen05 attention for d_kv = 128: self-attention over the fused q|k|v rows (relative bias
+    // as a LUT of 2T + 128 entries per head), cross-attention over separate q and encoder k|v
+    tc_ = dk_ == 128 && (Te_ > Td_ ? Te_ : Td_) + 128 <= 4096 && !(e != nullptr && e[0] == '0');
   }
   cuda_check(cudaSetDevice(mesh->cuda_device), "cudaSetDevice");
   cuda_check(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "cudaStreamCreate");
@@ -554,7 +556,10 @@ void T5Model::attn_fwd(T5Rank& R, int Tq, int Tk, const bf16* q, int64_t ldq, co
   tic();
   // tcgen05 path: fused q|k|v rows (ld 3*inner/t, k and v at +inner/t, +2*inner/t), Tq == Tk
   const bool tc = tc_ && Tq == Tk && ldq == 3LL * il_ && ldkv == 3LL * il_ && kp == q + il_ && vp == q + 2 * il_;
-  if (!(tc && k::attention_fwd_ex(q, o, lse, B_, Tq, hl_, dk_, causal, bias, 1.0f, stream_))) {
+  const bool tc_cross = tc_ && !tc && bias == nullptr && !causal;  // separate q and encoder k|v rows
+  if (!(tc && k::attention_fwd_ex(q, o, lse, B_, Tq, hl_, dk_, causal, bias, 1.0f, stream_)) &&
+      !(tc_cross && k::attention_fwd_cross(q, ldq, kp, ldkv, static_cast<int>(vp - kp), o, lse, B_, Tq, Tk, hl_, dk_,
+                                           1.0f, stream_))) {
     if (tc_ && bias != nullptr) fail(SW_ERR_INTERNAL, "T5: the tcgen05 attention forward declined a biased self-attention");
     k::t5_attention_fwd(a, B_, stream_);
   }
@@ -711,8 +716,11 @@ void T5Model::backward() {
     tic();
     const bool tc = tc_ && Tq == Tk && ldq == 3LL * il && ldkv == 3LL * il && kp == q + il && vp == q + 2 * il &&
                     lddq == 3LL * il && lddkv == 3LL * il && dkp == dq + il && dvp == dq + 2 * il;
+    const bool tc_cross = tc_ && !tc && bias == nullptr && !causal && vp - kp == dvp - dkp;
     if (!(tc && k::attention_bwd_ex(q, o, lse, R.dout, dq, R.attn_scratch, B_, Tq, hl_, dk_, causal, bias, dbias, 1.0f,
-                                    stream_))) {
+                                    stream_)) &&
+        !(tc_cross && k::attention_bwd_cross(q, ldq, kp, ldkv, static_cast<int>(vp - kp), o, lse, R.dout, dq, lddq, dkp,
+                                             lddkv, R.attn_scratch, B_, Tq, Tk, hl_, dk_, 1.0f, stream_))) {
       if (tc_ && bias != nullptr) fail(SW_ERR_INTERNAL, "T5: the tcgen05 attention backward declined (SW_ATTN_BWD_V1?)");
       k::t5_attention_bwd(a, B_, R.dout, il, dq, lddq, dkp, lddkv, dvp, lddkv, R.attn_scratch, dbias, stream_);
     }

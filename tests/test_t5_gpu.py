@@ -117,11 +117,12 @@ def test_t5_tensor_parallel_invariance_and_training():
 
 
 @pytest.mark.parametrize("tc", ["1", "0"])
-@pytest.mark.parametrize("mp,T", [(1, 160), (2, 128)])
-def test_t5_head_dim_128_attention_paths(tc, mp, T, monkeypatch):
-    """d_kv = 128 with enc_len == dec_len runs the tcgen05 attention (relative bias as a per-head
-    LUT over key - query, non-causal encoder and cross-attention over fused q|k|v, the bias
-    gradient summed along diagonals of dS); SW_T5_TC=0 forces the CUDA-core kernels. Both match
+@pytest.mark.parametrize("mp,T,Td", [(1, 160, 160), (2, 128, 128), (1, 192, 128), (2, 128, 200)])
+def test_t5_head_dim_128_attention_paths(tc, mp, T, Td, monkeypatch):
+    """d_kv = 128 runs the tcgen05 attention (relative bias as a per-head LUT over key - query,
+    non-causal encoder, the bias gradient summed along diagonals of dS; cross-attention over fused
+    q|k|v when enc_len == dec_len, over separate decoder q and encoder k|v rows otherwise -- the
+    last two cases); SW_T5_TC=0 forces the CUDA-core kernels. Both match
     the oracle (which models the tensor-core kernels' bf16 P / dS operands); T = 160 exercises the
     sequence tails. Tolerance 3e-2 (score path 4e-2): in this d_model = 64 / inner = 256 shape the
     bf16 forward noise flips ReLU masks below the last MLP, so both attention paths sit at 1-2.5%
@@ -131,10 +132,10 @@ def test_t5_head_dim_128_attention_paths(tc, mp, T, monkeypatch):
     shapes = rules.transformer_param_shapes(spec)
     plan = rules.derive_plan(shapes, mp, spec.overrides)
     mesh = engine.Mesh(1, mp)
-    model = engine.T5Model(spec, plan, mesh, 2, T, T)
+    model = engine.T5Model(spec, plan, mesh, 2, T, Td)
     model.init_params(11, "model-init")
     t5_init_scaling(model, spec)
-    enc, dec, tgt, w = t5_ref.t5_batch(11, 0, 2, T, T, spec.vocab_size)
+    enc, dec, tgt, w = t5_ref.t5_batch(11, 0, 2, T, Td, spec.vocab_size)
     model.stage_batch(enc, dec, tgt, w)
     model.forward_backward()
     loss = model.loss()
