@@ -1405,10 +1405,106 @@ __global__ void __launch_bounds__(256 * GEMV_KSPLIT) gemv_bf16_kernel(const Gemm
   }
 }
 
+// Small-M path on the tensor cores (M <= 8, K % 32 == 0, all epilogues but SwiGLU): out^T [16 rows x 8] = W [16 x K] .
+// A^T [K x 8] with mma.sync m16n8k16 (bf16 in, fp32 accumulate), the activations as the
+// 8-column B operand (columns >= M zero). Each lane streams 16 bytes of two weight rows (g, g+8)
+// and 16 bytes of activation row g per 32-deep k step; the contraction order inside a step is
+// permuted identically for both operands (lane t's 8 consecutive k feed the fragment slots 2t,
+// 2t+1, 2t+8, 2t+9 of two MMAs), so fragments load straight from global memory with 16-byte
+// loads. One activation load now serves 16 weight rows (the register kernel re-reads all M
+// activation slices from L1 for every pair of rows, which made M = 8 L1-bound at 1.4 TB/s).
+// CTA = 16 output columns, 8 warps interleaved along K; partial tiles reduced through shared
+// memory, then the common epilogue.
+__device__ __forceinline__ void mma_bf16_16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                               uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
+      "{%0, %1, %2, %3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+template <Epi EPI>
+__global__ void __launch_bounds__(256) gemv_mma_kernel(const GemmParams p) {
+  __shared__ float sred[8][16][8];
+  __shared__ float sout[GEMV_MAX_M][2 * GEMV_COLS];
+  const int K = p.K, M = p.M;
+  const int c0 = blockIdx.x * 16;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int r_lo = min(c0 + g, p.N - 1), r_hi = min(c0 + g + 8, p.N - 1);
+  const __nv_bfloat16* wlo_p = reinterpret_cast<const __nv_bfloat16*>(p.B) + static_cast<int64_t>(r_lo) * p.ldb + 8 * t;
+  const __nv_bfloat16* whi_p = reinterpret_cast<const __nv_bfloat16*>(p.B) + static_cast<int64_t>(r_hi) * p.ldb + 8 * t;
+  const bool act_row = g < M;
+  const __nv_bfloat16* a_p = reinterpret_cast<const __nv_bfloat16*>(p.A) + static_cast<int64_t>(act_row ? g : 0) * p.lda + 8 * t;
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  constexpr int U = 4;  // 32-deep k steps per warp with their loads in flight together
+  for (int k = warp * 32; k < K; k += 256 * U) {
+    uint4 wl[U], wh[U], av[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int kk = k + u * 256;
+      if (kk < K) {
+        wl[u] = __ldcs(reinterpret_cast<const uint4*>(wlo_p + kk));
+        wh[u] = __ldcs(reinterpret_cast<const uint4*>(whi_p + kk));
+        av[u] = act_row ? __ldg(reinterpret_cast<const uint4*>(a_p + kk)) : make_uint4(0, 0, 0, 0);
+      } else {
+        wl[u] = wh[u] = av[u] = make_uint4(0, 0, 0, 0);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      mma_bf16_16816(acc, wl[u].x, wh[u].x, wl[u].y, wh[u].y, av[u].x, av[u].y);
+      mma_bf16_16816(acc, wl[u].z, wh[u].z, wl[u].w, wh[u].w, av[u].z, av[u].w);
+    }
+  }
+  // d0, d1: (row g, activation rows 2t, 2t+1); d2, d3: (row g+8, same)
+  sred[warp][g][2 * t] = acc[0];
+  sred[warp][g][2 * t + 1] = acc[1];
+  sred[warp][g + 8][2 * t] = acc[2];
+  sred[warp][g + 8][2 * t + 1] = acc[3];
+  __syncthreads();
+  if (threadIdx.x < 16 * GEMV_MAX_M) {
+    const int r = threadIdx.x & 15, m = threadIdx.x >> 4;
+    float v = 0.f;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) v += sred[w][r][m];
+    sout[m][r] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < M) {
+    const int row = threadIdx.x;
+    uint32_t rr[32];
+#pragma unroll
+    for (int c = 0; c < 32; ++c) rr[c] = __float_as_uint(c < 16 ? sout[row][c] : 0.f);
+    epilogue_chunk<EPI>(p, row, c0, min(16, p.N - c0), rr);
+  }
+}
+
+// SW_GEMV_MMA=0: the register-streamed kernel for every M
+bool gemv_mma_on() {
+  static const bool on = [] {
+    const char* e = std::getenv("SW_GEMV_MMA");
+    return !(e != nullptr && e[0] == '0');
+  }();
+  return on;
+}
+
 // Measured on B200 (tools/gemv_bench.py, M = 1): KSPLIT 2 / UNROLL 4 streams N = 4096 weights at
 // 2.7-3.9 TB/s (was 2.3-2.6), KSPLIT 1 / UNROLL 2 is best from N = 11008 up (3.1-4.0 TB/s)
 template <Epi EPI>
 cudaError_t launch_gemv(const GemmParams& p, cudaStream_t stream) {
+  if constexpr (EPI != Epi::kSwiGLU) {
+    static const int mma_min_m = [] {
+      // measured: at M = 1 as well the tensor-core kernel streams as fast or faster (4.3-6.1 TB/s)
+      const char* e = std::getenv("SW_GEMV_MMA_MIN_M");
+      return e != nullptr ? std::atoi(e) : 1;
+    }();
+    if (p.M >= mma_min_m && p.K % 32 == 0 && gemv_mma_on()) {
+      gemv_mma_kernel<EPI><<<(p.N + 15) / 16, 256, 0, stream>>>(p);
+      return cudaGetLastError();
+    }
+  }
   const int grid = (p.N + GEMV_COLS - 1) / GEMV_COLS;
   // accumulators sized for the actual M: at M = 1 the kernel needs far fewer registers, so more
   // CTAs (and their weight loads) are resident per SM (ncu: 80 registers capped the M <= 8
