@@ -1405,7 +1405,7 @@ __global__ void __launch_bounds__(256 * GEMV_KSPLIT) gemv_bf16_kernel(const Gemm
   }
 }
 
-// Small-M path on the tensor cores (M <= 8, K % 32 == 0, all epilogues but SwiGLU): out^T [16 rows x 8] = W [16 x K] .
+// Small-M path on the tensor cores (M <= 8, K % 32 == 0; SwiGLU: gate and up tiles side by side): out^T [16 rows x 8] = W [16 x K] .
 // A^T [K x 8] with mma.sync m16n8k16 (bf16 in, fp32 accumulate), the activations as the
 // 8-column B operand (columns >= M zero). Each lane streams 16 bytes of two weight rows (g, g+8)
 // and 16 bytes of activation row g per 32-deep k step; the contraction order inside a step is
@@ -1426,58 +1426,96 @@ __device__ __forceinline__ void mma_bf16_16816(float (&d)[4], uint32_t a0, uint3
 
 template <Epi EPI>
 __global__ void __launch_bounds__(256) gemv_mma_kernel(const GemmParams p) {
-  __shared__ float sred[8][16][8];
+  constexpr bool kGlu = EPI == Epi::kSwiGLU;  // SwiGLU: gate rows c0.. and up rows swiglu_half + c0..
+  constexpr int NT = kGlu ? 2 : 1;
+  __shared__ float sred[NT][8][16][8];
   __shared__ float sout[GEMV_MAX_M][2 * GEMV_COLS];
   const int K = p.K, M = p.M;
   const int c0 = blockIdx.x * 16;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
   const int r_lo = min(c0 + g, p.N - 1), r_hi = min(c0 + g + 8, p.N - 1);
-  const __nv_bfloat16* wlo_p = reinterpret_cast<const __nv_bfloat16*>(p.B) + static_cast<int64_t>(r_lo) * p.ldb + 8 * t;
-  const __nv_bfloat16* whi_p = reinterpret_cast<const __nv_bfloat16*>(p.B) + static_cast<int64_t>(r_hi) * p.ldb + 8 * t;
+  const __nv_bfloat16* wb = reinterpret_cast<const __nv_bfloat16*>(p.B);
+  const __nv_bfloat16* wlo_p[NT];
+  const __nv_bfloat16* whi_p[NT];
+#pragma unroll
+  for (int q = 0; q < NT; ++q) {
+    const int off = q ? p.swiglu_half : 0;
+    wlo_p[q] = wb + static_cast<int64_t>(off + r_lo) * p.ldb + 8 * t;
+    whi_p[q] = wb + static_cast<int64_t>(off + r_hi) * p.ldb + 8 * t;
+  }
   const bool act_row = g < M;
   const __nv_bfloat16* a_p = reinterpret_cast<const __nv_bfloat16*>(p.A) + static_cast<int64_t>(act_row ? g : 0) * p.lda + 8 * t;
-  float acc[4] = {0.f, 0.f, 0.f, 0.f};
-  constexpr int U = 4;  // 32-deep k steps per warp with their loads in flight together
+  float acc[NT][4];
+#pragma unroll
+  for (int q = 0; q < NT; ++q) acc[q][0] = acc[q][1] = acc[q][2] = acc[q][3] = 0.f;
+  constexpr int U = kGlu ? 2 : 4;  // 32-deep k steps per warp with their loads in flight together
   for (int k = warp * 32; k < K; k += 256 * U) {
-    uint4 wl[U], wh[U], av[U];
+    uint4 wl[U][NT], wh[U][NT], av[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int kk = k + u * 256;
       if (kk < K) {
-        wl[u] = __ldcs(reinterpret_cast<const uint4*>(wlo_p + kk));
-        wh[u] = __ldcs(reinterpret_cast<const uint4*>(whi_p + kk));
+#pragma unroll
+        for (int q = 0; q < NT; ++q) {
+          wl[u][q] = __ldcs(reinterpret_cast<const uint4*>(wlo_p[q] + kk));
+          wh[u][q] = __ldcs(reinterpret_cast<const uint4*>(whi_p[q] + kk));
+        }
         av[u] = act_row ? __ldg(reinterpret_cast<const uint4*>(a_p + kk)) : make_uint4(0, 0, 0, 0);
       } else {
-        wl[u] = wh[u] = av[u] = make_uint4(0, 0, 0, 0);
+#pragma unroll
+        for (int q = 0; q < NT; ++q) wl[u][q] = wh[u][q] = make_uint4(0, 0, 0, 0);
+        av[u] = make_uint4(0, 0, 0, 0);
       }
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      mma_bf16_16816(acc, wl[u].x, wh[u].x, wl[u].y, wh[u].y, av[u].x, av[u].y);
-      mma_bf16_16816(acc, wl[u].z, wh[u].z, wl[u].w, wh[u].w, av[u].z, av[u].w);
+#pragma unroll
+      for (int q = 0; q < NT; ++q) {
+        mma_bf16_16816(acc[q], wl[u][q].x, wh[u][q].x, wl[u][q].y, wh[u][q].y, av[u].x, av[u].y);
+        mma_bf16_16816(acc[q], wl[u][q].z, wh[u][q].z, wl[u][q].w, wh[u][q].w, av[u].z, av[u].w);
+      }
     }
   }
   // d0, d1: (row g, activation rows 2t, 2t+1); d2, d3: (row g+8, same)
-  sred[warp][g][2 * t] = acc[0];
-  sred[warp][g][2 * t + 1] = acc[1];
-  sred[warp][g + 8][2 * t] = acc[2];
-  sred[warp][g + 8][2 * t + 1] = acc[3];
+#pragma unroll
+  for (int q = 0; q < NT; ++q) {
+    sred[q][warp][g][2 * t] = acc[q][0];
+    sred[q][warp][g][2 * t + 1] = acc[q][1];
+    sred[q][warp][g + 8][2 * t] = acc[q][2];
+    sred[q][warp][g + 8][2 * t + 1] = acc[q][3];
+  }
   __syncthreads();
   if (threadIdx.x < 16 * GEMV_MAX_M) {
     const int r = threadIdx.x & 15, m = threadIdx.x >> 4;
-    float v = 0.f;
 #pragma unroll
-    for (int w = 0; w < 8; ++w) v += sred[w][r][m];
-    sout[m][r] = v;
+    for (int q = 0; q < NT; ++q) {
+      float v = 0.f;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) v += sred[q][w][r][m];
+      sout[m][q * GEMV_COLS + r] = v;
+    }
   }
   __syncthreads();
   if (threadIdx.x < M) {
     const int row = threadIdx.x;
-    uint32_t rr[32];
+    const int ncols = min(16, p.N - c0);
+    if constexpr (kGlu) {  // the register kernel's SwiGLU epilogue: h = silu(g) * u, pre = g | u (bf16)
+      __nv_bfloat16* hrow = reinterpret_cast<__nv_bfloat16*>(p.C) + static_cast<int64_t>(row) * p.ldc + c0;
+      __nv_bfloat16* prow = reinterpret_cast<__nv_bfloat16*>(p.C2) + static_cast<int64_t>(row) * p.ldc2 + c0;
+      for (int c = 0; c < ncols; ++c) {
+        const float gv = __bfloat162float(__float2bfloat16(sout[row][c]));
+        const float uv = __bfloat162float(__float2bfloat16(sout[row][GEMV_COLS + c]));
+        prow[c] = __float2bfloat16(gv);
+        prow[p.swiglu_half + c] = __float2bfloat16(uv);
+        hrow[c] = __float2bfloat16(dev::silu(gv) * uv);
+      }
+    } else {
+      uint32_t rr[32];
 #pragma unroll
-    for (int c = 0; c < 32; ++c) rr[c] = __float_as_uint(c < 16 ? sout[row][c] : 0.f);
-    epilogue_chunk<EPI>(p, row, c0, min(16, p.N - c0), rr);
+      for (int c = 0; c < 32; ++c) rr[c] = __float_as_uint(c < 16 ? sout[row][c] : 0.f);
+      epilogue_chunk<EPI>(p, row, c0, ncols, rr);
+    }
   }
 }
 
@@ -1494,7 +1532,7 @@ bool gemv_mma_on() {
 // 2.7-3.9 TB/s (was 2.3-2.6), KSPLIT 1 / UNROLL 2 is best from N = 11008 up (3.1-4.0 TB/s)
 template <Epi EPI>
 cudaError_t launch_gemv(const GemmParams& p, cudaStream_t stream) {
-  if constexpr (EPI != Epi::kSwiGLU) {
+  {
     static const int mma_min_m = [] {
       // measured: at M = 1 as well the tensor-core kernel streams as fast or faster (4.3-6.1 TB/s)
       const char* e = std::getenv("SW_GEMV_MMA_MIN_M");

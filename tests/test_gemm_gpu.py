@@ -187,7 +187,10 @@ def test_gemm_adamw_epilogue_gated_by_flag(M, N, K):
         assert torch.equal(a, b)
 
 
-@pytest.mark.parametrize("M,N,K", [(256, 128, 64), (300, 200, 136), (1000, 1376, 512), (512, 688, 4096)])
+@pytest.mark.parametrize("M,N,K", [(256, 128, 64), (300, 200, 136), (1000, 1376, 512), (512, 688, 4096),
+                                   # decode sizes: the small-M kernels (tensor-core GEMV; K = 136 the
+                                   # register-streamed one)
+                                   (1, 1376, 4096), (3, 200, 136), (8, 688, 512)])
 def test_gemm_swiglu_fwd_bwd(M, N, K):
     """SwiGLU extension vs torch fp32 on the same bf16 operands: the fused [gate; up]
     GEMM writes h = silu(g)*u and the bf16 pre-activations; the down-projection dgrad epilogue
