@@ -754,6 +754,312 @@ __global__ void __launch_bounds__(384, 1)
   }
 }
 
+// ---------------------------------------------------------------------------------------------
+// forward v3 (head_dim 128, causal self-attention): two query tiles per CTA as in v2, but 64-key
+// blocks with each tile's S double-buffered, so a tile's S_{j+1} = Q K_{j+1}^T executes while its
+// softmax warpgroup works on S_j (v2's single S buffer per tile serialised softmax -> P V -> S
+// per tile). TMEM per tile: O (128 columns) | S0 (64) | S1 (64); P_j (bf16) over S_j's first 32.
+//   warp 0  TMA: Q_A, Q_B once; K_j / V_j ([64 keys x 128] each) into a 4-stage ring
+//   warp 1  MMA: per key block j: S_A(j), S_B(j), then P_A(j-1) V_{j-1}, P_B(j-1) V_{j-1}
+//   warps 4-7 / 8-11  softmax of tile A / B (thread = query row), lazy running max
+// ---------------------------------------------------------------------------------------------
+constexpr int F3_BK = 64;
+constexpr int F3_NST = 4;
+constexpr int F3_CH = F3_BK * 128;  // [64 rows x 64 bf16] SW128 chunk: 8 KiB
+struct Fwd3Layout {
+  static constexpr int HD = 128;
+  static constexpr int Q = 128 * HD * 2;     // 32 KiB
+  static constexpr int KV = F3_BK * HD * 2;  // 16 KiB
+  static constexpr int OFF_QA = 0;
+  static constexpr int OFF_QB = OFF_QA + Q;
+  static constexpr int OFF_K = OFF_QB + Q;           // [F3_NST]
+  static constexpr int OFF_V = OFF_K + F3_NST * KV;  // [F3_NST]
+  static constexpr int OFF_BAR = OFF_V + F3_NST * KV;
+  static constexpr int BYTES = OFF_BAR + 256;
+};
+
+__global__ void __launch_bounds__(384, 1)
+    attn_fwd_tc3(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_kv,
+                 bf16* __restrict__ out, float* __restrict__ lse, int T, int Hl, float scale_log2, float scale,
+                 int nbh, int group) {
+  using Lay = Fwd3Layout;
+  constexpr int HD = Lay::HD;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t* sQ[2] = {smem + Lay::OFF_QA, smem + Lay::OFF_QB};
+  uint8_t* sK = smem + Lay::OFF_K;
+  uint8_t* sV = smem + Lay::OFF_V;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Lay::OFF_BAR);
+  uint64_t* q_full = bars;                   // 1
+  uint64_t* kv_full = bars + 1;              // [F3_NST]
+  uint64_t* kv_empty = kv_full + F3_NST;     // [F3_NST]
+  uint64_t* s_full = kv_empty + F3_NST;      // [tile][2]
+  uint64_t* p_full = s_full + 4;             // [tile][2]
+  uint64_t* pv_done = p_full + 4;            // [tile][2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pv_done + 4);
+
+  const int nqb = (T + 127) / 128;
+  const int npair = (nqb + 1) / 2;
+  int rank_, bh;
+  work_item(static_cast<int>(blockIdx.x), npair, nbh, group, rank_, bh);
+  const int pi = npair - 1 - rank_;  // heaviest pair first
+  const int h = bh % Hl;
+  const int row0 = (bh / Hl) * T;
+  const int qa = 2 * pi;
+  const bool hasB = qa + 1 < nqb;
+  const int nkt = (T + F3_BK - 1) / F3_BK;
+  // causal: 64-key blocks through each tile's diagonal
+  const int nk_t[2] = {min(2 * (qa + 1), nkt), hasB ? min(2 * (qa + 2), nkt) : 0};
+  const int nkv = hasB ? nk_t[1] : nk_t[0];
+  const int Dl = Hl * HD;
+
+  const uint32_t warp = dev::warp_idx_sync();
+  const uint32_t lane = threadIdx.x & 31;
+  if (warp == 0 && lane == 0) {
+    dev::tma_prefetch_desc(&tm_q);
+    dev::tma_prefetch_desc(&tm_kv);
+    dev::mbar_init(q_full, 1);
+    for (int i = 0; i < F3_NST; ++i) {
+      dev::mbar_init(&kv_full[i], 1);
+      dev::mbar_init(&kv_empty[i], 1);
+    }
+    for (int i = 0; i < 4; ++i) {
+      dev::mbar_init(&s_full[i], 1);
+      dev::mbar_init(&p_full[i], 128);
+      dev::mbar_init(&pv_done[i], 1);
+    }
+    dev::fence_barrier_init();
+  }
+  if (warp == 2) dev::tmem_alloc<512>(tmem_slot);
+  dev::tc_fence_before();
+  __syncthreads();
+  dev::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      dev::mbar_arrive_expect_tx(q_full, Lay::Q * (hasB ? 2 : 1));
+      for (int t = 0; t < (hasB ? 2 : 1); ++t) {
+#pragma unroll
+        for (int c = 0; c < HD / 64; ++c)
+          dev::tma_load_2d(sQ[t] + c * CHUNK, &tm_q, q_full, h * HD + c * 64, row0 + (qa + t) * 128);
+      }
+      for (int j = 0; j < nkv; ++j) {
+        const int st = j % F3_NST;
+        dev::mbar_wait(&kv_empty[st], ((j / F3_NST) & 1) ^ 1);
+        dev::mbar_arrive_expect_tx(&kv_full[st], 2 * Lay::KV);
+#pragma unroll
+        for (int c = 0; c < HD / 64; ++c) {
+          dev::tma_load_2d(sK + st * Lay::KV + c * F3_CH, &tm_kv, &kv_full[st], Dl + h * HD + c * 64, row0 + j * F3_BK);
+          dev::tma_load_2d(sV + st * Lay::KV + c * F3_CH, &tm_kv, &kv_full[st], 2 * Dl + h * HD + c * 64,
+                           row0 + j * F3_BK);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    const uint32_t id_s = dev::make_idesc_bf16(128, F3_BK, 0, 0);
+    const uint32_t id_o = dev::make_idesc_bf16(128, HD, 0, 1);
+    const uint64_t dq[2] = {dev::make_sdesc_sw128(dev::smem_u32(sQ[0]), 16, 1024),
+                            dev::make_sdesc_sw128(dev::smem_u32(sQ[1]), 16, 1024)};
+    const uint64_t dk = dev::make_sdesc_sw128(dev::smem_u32(sK), 16, 1024);
+    const uint64_t dv = dev::make_sdesc_sw128(dev::smem_u32(sV), F3_CH, 1024);
+    constexpr uint64_t KV16 = Lay::KV >> 4;
+    auto kq = [](int kk) { return static_cast<uint64_t>((kk >> 2) * (CHUNK >> 4) + (kk & 3) * 2); };   // Q: 128-row chunks
+    auto kk64 = [](int kk) { return static_cast<uint64_t>((kk >> 2) * (F3_CH >> 4) + (kk & 3) * 2); }; // K: 64-row chunks
+    auto tS = [&](int t, int j) { return tmem + t * 256 + 128 + (j & 1) * 64; };
+    auto issue_pv = [&](int t, int j) {
+      dev::mbar_wait(&p_full[2 * t + (j & 1)], (j >> 1) & 1);
+      dev::tc_fence_after();
+      const uint64_t bv = dv + (j % F3_NST) * KV16;
+      if (dev::elect_one_sync()) {
+#pragma unroll
+        for (int kk = 0; kk < F3_BK / 16; ++kk)  // P (bf16 pairs) in the first 32 columns of S_t(j)
+          dev::umma_f16_ts(tmem + t * 256, tS(t, j) + kk * 8, bv + static_cast<uint64_t>(kk * 128), id_o,
+                           (j > 0 || kk > 0) ? 1u : 0u);
+        dev::umma_commit(&pv_done[2 * t + (j & 1)]);
+      }
+      __syncwarp();
+    };
+    dev::mbar_wait(q_full, 0);
+    for (int j = 0; j < nkv; ++j) {
+      const int st = j % F3_NST;
+      dev::mbar_wait(&kv_full[st], (j / F3_NST) & 1);
+      dev::tc_fence_after();
+      const uint64_t bk = dk + st * KV16;
+      if (dev::elect_one_sync()) {
+        // S_t(j) goes into the buffer of P_t(j-2), whose P V was issued (and so executes) before it
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+          if (j < nk_t[t]) {
+#pragma unroll
+            for (int kk = 0; kk < HD / 16; ++kk)
+              dev::umma_f16_ss(tS(t, j), dq[t] + kq(kk), bk + kk64(kk), id_s, kk > 0 ? 1u : 0u);
+            dev::umma_commit(&s_full[2 * t + (j & 1)]);
+          }
+        }
+      }
+      __syncwarp();
+      if (j >= 1) {
+        if (j - 1 < nk_t[0]) issue_pv(0, j - 1);
+        if (j - 1 < nk_t[1]) issue_pv(1, j - 1);
+        if (dev::elect_one_sync()) dev::umma_commit(&kv_empty[(j - 1) % F3_NST]);  // K/V_{j-1} consumed
+        __syncwarp();
+      }
+    }
+    if (nk_t[0] == nkv) issue_pv(0, nkv - 1);
+    if (nk_t[1] == nkv) issue_pv(1, nkv - 1);
+    if (dev::elect_one_sync()) dev::umma_commit(&kv_empty[(nkv - 1) % F3_NST]);
+    __syncwarp();
+  } else if (warp >= 4) {
+    const int t = (static_cast<int>(warp) - 4) >> 2;
+    if (t == 0 || hasB) {
+      const int r = static_cast<int>(warp & 3) * 32 + static_cast<int>(lane);
+      const int q = (qa + t) * 128 + r;
+      const int nk = nk_t[t];
+      const uint32_t lb = static_cast<uint32_t>((warp & 3) * 32) << 16;
+      const uint32_t tO = tmem + lb + t * 256;
+      const float2 sl2 = make_float2(scale_log2, scale_log2);
+      float m_used = -INFINITY, l = 0.f;
+      for (int j = 0; j < nk; ++j) {
+        dev::mbar_wait(&s_full[2 * t + (j & 1)], (j >> 1) & 1);
+        dev::tc_fence_after();
+        const uint32_t tSj = tmem + lb + t * 256 + 128 + (j & 1) * 64;
+        uint32_t v[64];
+        auto load_s = [&]() {
+          dev::tmem_ld_32x32b_x32(tSj, *reinterpret_cast<uint32_t(*)[32]>(v));
+          dev::tmem_ld_32x32b_x32(tSj + 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
+          dev::tmem_ld_wait();
+          if ((j + 1) * F3_BK > (qa + t) * 128 || (j + 1) * F3_BK > T) {
+#pragma unroll
+            for (int i = 0; i < F3_BK; ++i) {
+              const int key = j * F3_BK + i;
+              if (key > q || key >= T) v[i] = __float_as_uint(-INFINITY);
+            }
+          }
+        };
+        auto rowmax = [&]() {
+          float m4[4] = {__uint_as_float(v[0]), __uint_as_float(v[1]), __uint_as_float(v[2]), __uint_as_float(v[3])};
+#pragma unroll
+          for (int i = 4; i < F3_BK; i += 8) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              m4[u] = dev::fmax3(m4[u], __uint_as_float(v[i + 2 * u]), __uint_as_float(v[i + 2 * u + 1]));
+          }
+          return fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
+        };
+        auto exps = [&](float mref) {  // P in place: v[e] = bf16x2(p[2e], p[2e+1]); returns the row sum
+          const float mb = mref * scale_log2;
+          const float2 nmb2 = make_float2(-mb, -mb);
+          float2 ls[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+#pragma unroll
+          for (int e = 0; e < F3_BK / 2; ++e) {
+            const float2 a = dev::ffma2(make_float2(__uint_as_float(v[2 * e]), __uint_as_float(v[2 * e + 1])), sl2, nmb2);
+            const float2 pp = make_float2(dev::ex2_approx(a.x), dev::ex2_approx(a.y));
+            ls[e & 3] = dev::fadd2(ls[e & 3], pp);
+            v[e] = dev::pack_bf16x2(pp.x, pp.y);
+          }
+          const float2 s01 = dev::fadd2(ls[0], ls[1]), s23 = dev::fadd2(ls[2], ls[3]);
+          return (s01.x + s23.x) + (s01.y + s23.y);
+        };
+        load_s();
+        float l_blk;
+        if (j == 0) {
+          m_used = rowmax();
+          l_blk = exps(m_used);
+        } else {
+          const float mx = rowmax();
+          l_blk = exps(m_used);
+          const bool resc = (mx - m_used) * scale_log2 > 8.f;
+          if (__any_sync(0xffffffffu, resc)) {
+            const float factor = resc ? dev::ex2_approx((m_used - mx) * scale_log2) : 1.f;
+            if (resc) {
+              m_used = mx;
+              l *= factor;
+            }
+            dev::mbar_wait(&pv_done[2 * t + ((j - 1) & 1)], ((j - 1) >> 1) & 1);  // every earlier P V is in O
+            dev::tc_fence_after();
+#pragma unroll 1
+            for (int c = 0; c < HD / 32; ++c) {
+              uint32_t o[32];
+              dev::tmem_ld_32x32b_x32(tO + c * 32, o);
+              dev::tmem_ld_wait();
+#pragma unroll
+              for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * factor);
+              dev::tmem_st_32x32b_x32(tO + c * 32, o);
+            }
+            dev::tmem_st_wait();
+            load_s();  // S_j is still in TMEM: P again against the new max
+            l_blk = exps(m_used);
+          }
+        }
+        l += l_blk;
+        dev::tmem_st_32x32b_x32(tSj, *reinterpret_cast<uint32_t(*)[32]>(v));
+        dev::tmem_st_wait();
+        dev::tc_fence_before();
+        dev::mbar_arrive(&p_full[2 * t + (j & 1)]);
+      }
+      dev::mbar_wait(&pv_done[2 * t + ((nk - 1) & 1)], ((nk - 1) >> 1) & 1);
+      dev::tc_fence_after();
+      const float inv = 1.f / l;
+      bf16* orow = out + (static_cast<int64_t>(row0) + q) * Dl + h * HD;
+#pragma unroll 1
+      for (int c = 0; c < HD / 32; ++c) {
+        uint32_t o[32];
+        dev::tmem_ld_32x32b_x32(tO + c * 32, o);
+        dev::tmem_ld_wait();
+        if (q < T) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            uint4 w;
+            w.x = dev::pack_bf16x2(__uint_as_float(o[8 * u + 0]) * inv, __uint_as_float(o[8 * u + 1]) * inv);
+            w.y = dev::pack_bf16x2(__uint_as_float(o[8 * u + 2]) * inv, __uint_as_float(o[8 * u + 3]) * inv);
+            w.z = dev::pack_bf16x2(__uint_as_float(o[8 * u + 4]) * inv, __uint_as_float(o[8 * u + 5]) * inv);
+            w.w = dev::pack_bf16x2(__uint_as_float(o[8 * u + 6]) * inv, __uint_as_float(o[8 * u + 7]) * inv);
+            *reinterpret_cast<uint4*>(orow + c * 32 + 8 * u) = w;
+          }
+        }
+      }
+      if (q < T) lse[static_cast<int64_t>(bh) * T + q] = m_used * scale + logf(l);
+    }
+  }
+  dev::tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    dev::tc_fence_after();
+    dev::tmem_dealloc<512>(tmem);
+  }
+}
+
+// SW_ATTN_FWD3=0: the v2 forward (128-key blocks, one S buffer per tile) for causal self-attention
+bool fwd3_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("SW_ATTN_FWD3");
+    return !(e != nullptr && e[0] == '0');
+  }();
+  return on;
+}
+
+bool launch_fwd3(const bf16* qkv, bf16* o, float* lse, int B, int T, int Hl, cudaStream_t s) {
+  static bool configured = false;
+  if (!configured) {
+    if (cudaFuncSetAttribute(attn_fwd_tc3, cudaFuncAttributeMaxDynamicSharedMemorySize, Fwd3Layout::BYTES) !=
+        cudaSuccess) {
+      return false;
+    }
+    configured = true;
+  }
+  constexpr int HD = 128;
+  const int Dl = Hl * HD;
+  const CUtensorMap tm_q = make_tmap_bf16_2d(qkv, 3ull * Dl, static_cast<uint64_t>(B) * T, 3ull * Dl, 64, 128);
+  const CUtensorMap tm_kv = make_tmap_bf16_2d(qkv, 3ull * Dl, static_cast<uint64_t>(B) * T, 3ull * Dl, 64, F3_BK);
+  const int nqb = (T + 127) / 128;
+  const int npair = (nqb + 1) / 2;
+  const double scale = 1.0 / std::sqrt(static_cast<double>(HD));
+  attn_fwd_tc3<<<npair * B * Hl, 384, Fwd3Layout::BYTES, s>>>(tm_q, tm_kv, o, lse, T, Hl,
+                                                              static_cast<float>(scale * 1.4426950408889634),
+                                                              static_cast<float>(scale), B * Hl, work_group());
+  return true;
+}
+
 // SW_ATTN_PERSIST=1: one resident CTA per SM walking several items (snake order). Measured
 // on B200 (tools/attn_bench.py, LLaMA-7B heads): equal at T = 2048 (the next item's Q load and
 // the pipeline refill are not hidden by it), 25% slower at T = 8192 (the hardware's in-order
@@ -1790,7 +2096,10 @@ void attn_dq_to_bf16(const float* dq, bf16* dqkv, int64_t M, int Dl, cudaStream_
 bool attention_mma_fwd(const bf16* qkv, bf16* o, float* lse, int B, int T, int Hl, int hd, cudaStream_t s) {
   if (((3 * Hl * hd) % 8) != 0) return false;
   if (hd == 256) return attention_hd256_fwd(qkv, o, lse, B, T, Hl, s);
-  if (hd == 128) return fwd2_enabled() ? launch_fwd2(qkv, o, lse, B, T, Hl, s) : launch_fwd<128>(qkv, o, lse, B, T, Hl, s);
+  if (hd == 128) {
+    if (fwd2_enabled() && fwd3_enabled()) return launch_fwd3(qkv, o, lse, B, T, Hl, s);
+    return fwd2_enabled() ? launch_fwd2(qkv, o, lse, B, T, Hl, s) : launch_fwd<128>(qkv, o, lse, B, T, Hl, s);
+  }
   if (hd == 64) return launch_fwd<64>(qkv, o, lse, B, T, Hl, s);
   return false;
 }
