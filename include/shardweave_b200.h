@@ -166,6 +166,13 @@ typedef struct sw_adamw_cfg {
  * `batch` is the per-replica batch (rows of each dp slice, spmd.hpp:751-769). */
 SW_API sw_status sw_model_create(const sw_model_spec* spec, const sw_plan* plan, sw_mesh* mesh,
                           int batch, int seq_len, sw_model** out);
+/* The same program for the Predictor path only (cli.cpp:425-447, pipeline.hpp:189-246:
+ * predict / generate on restored parameters): bf16 GEMM weight shards, fp32 small parameters
+ * and the K/V cache; no gradients, AdamW moments or fp32 master copies of the GEMM weights.
+ * forward_logits / last_loss / generate / set_param / get_tensor(which 0) / load_checkpoint
+ * (parameters only) work; the training entry points return SW_ERR_CONFIG. */
+SW_API sw_status sw_model_create_inference(const sw_model_spec* spec, const sw_plan* plan, sw_mesh* mesh,
+                                           int batch, int seq_len, sw_model** out);
 SW_API void sw_model_free(sw_model* model);
 
 /* init_transformer_params(spec, RngStream(seed, stream_name)) (model.hpp:49-70), generated

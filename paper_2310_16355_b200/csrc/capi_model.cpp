@@ -90,6 +90,17 @@ sw_status sw_model_create(const sw_model_spec* spec, const sw_plan* plan, sw_mes
   });
 }
 
+sw_status sw_model_create_inference(const sw_model_spec* spec, const sw_plan* plan, sw_mesh* mesh, int batch,
+                                    int seq_len, sw_model** out) {
+  return sw::guarded([&] {
+    require(spec, "spec");
+    require(plan, "plan");
+    require(mesh, "mesh");
+    require(out, "out");
+    *out = new sw_model{new sw::Model(spec->spec, plan->plan, mesh->mesh, batch, seq_len, true)};
+  });
+}
+
 void sw_model_free(sw_model* model) {
   if (model != nullptr) {
     delete model->model;

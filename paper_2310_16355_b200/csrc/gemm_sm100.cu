@@ -1424,14 +1424,20 @@ __device__ __forceinline__ void mma_bf16_16816(float (&d)[4], uint32_t a0, uint3
       : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
 
-template <Epi EPI>
+// NB: 8-row activation groups per warp (the weight fragments of a k step feed NB mmas);
+// gridDim.x: groups of 8 * NB activation rows, adjacent CTAs, so the re-reads of a weight tile
+// by the CTAs of the other groups hit L2 (M up to GEMV_MMA_MAX_M).
+template <Epi EPI, int NB>
 __global__ void __launch_bounds__(256) gemv_mma_kernel(const GemmParams p) {
   constexpr bool kGlu = EPI == Epi::kSwiGLU;  // SwiGLU: gate rows c0.. and up rows swiglu_half + c0..
   constexpr int NT = kGlu ? 2 : 1;
-  __shared__ float sred[NT][8][16][8];
-  __shared__ float sout[GEMV_MAX_M][2 * GEMV_COLS];
-  const int K = p.K, M = p.M;
-  const int c0 = blockIdx.x * 16;
+  constexpr int MR = 8 * NB;  // activation rows per CTA
+  __shared__ float sred[NT][8][16][MR];
+  __shared__ float sout[MR][2 * GEMV_COLS];
+  const int K = p.K;
+  const int m0 = blockIdx.x * MR;
+  const int M = min(MR, p.M - m0);
+  const int c0 = blockIdx.y * 16;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
   const int r_lo = min(c0 + g, p.N - 1), r_hi = min(c0 + g + 8, p.N - 1);
@@ -1444,14 +1450,22 @@ __global__ void __launch_bounds__(256) gemv_mma_kernel(const GemmParams p) {
     wlo_p[q] = wb + static_cast<int64_t>(off + r_lo) * p.ldb + 8 * t;
     whi_p[q] = wb + static_cast<int64_t>(off + r_hi) * p.ldb + 8 * t;
   }
-  const bool act_row = g < M;
-  const __nv_bfloat16* a_p = reinterpret_cast<const __nv_bfloat16*>(p.A) + static_cast<int64_t>(act_row ? g : 0) * p.lda + 8 * t;
-  float acc[NT][4];
+  const __nv_bfloat16* a_p[NB];
+  bool act_row[NB];
 #pragma unroll
-  for (int q = 0; q < NT; ++q) acc[q][0] = acc[q][1] = acc[q][2] = acc[q][3] = 0.f;
-  constexpr int U = kGlu ? 2 : 4;  // 32-deep k steps per warp with their loads in flight together
+  for (int j = 0; j < NB; ++j) {
+    act_row[j] = 8 * j + g < M;
+    a_p[j] = reinterpret_cast<const __nv_bfloat16*>(p.A) + static_cast<int64_t>(m0 + (act_row[j] ? 8 * j + g : 0)) * p.lda + 8 * t;
+  }
+  float acc[NT][NB][4];
+#pragma unroll
+  for (int q = 0; q < NT; ++q)
+#pragma unroll
+    for (int j = 0; j < NB; ++j) acc[q][j][0] = acc[q][j][1] = acc[q][j][2] = acc[q][j][3] = 0.f;
+  // 32-deep k steps per warp with their loads in flight together
+  constexpr int U = NB >= 4 ? 2 : kGlu ? 2 : 4;
   for (int k = warp * 32; k < K; k += 256 * U) {
-    uint4 wl[U][NT], wh[U][NT], av[U];
+    uint4 wl[U][NT], wh[U][NT], av[U][NB];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int kk = k + u * 256;
@@ -1461,33 +1475,42 @@ __global__ void __launch_bounds__(256) gemv_mma_kernel(const GemmParams p) {
           wl[u][q] = __ldcs(reinterpret_cast<const uint4*>(wlo_p[q] + kk));
           wh[u][q] = __ldcs(reinterpret_cast<const uint4*>(whi_p[q] + kk));
         }
-        av[u] = act_row ? __ldg(reinterpret_cast<const uint4*>(a_p + kk)) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+        for (int j = 0; j < NB; ++j)
+          av[u][j] = act_row[j] ? __ldg(reinterpret_cast<const uint4*>(a_p[j] + kk)) : make_uint4(0, 0, 0, 0);
       } else {
 #pragma unroll
         for (int q = 0; q < NT; ++q) wl[u][q] = wh[u][q] = make_uint4(0, 0, 0, 0);
-        av[u] = make_uint4(0, 0, 0, 0);
+#pragma unroll
+        for (int j = 0; j < NB; ++j) av[u][j] = make_uint4(0, 0, 0, 0);
       }
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
 #pragma unroll
       for (int q = 0; q < NT; ++q) {
-        mma_bf16_16816(acc[q], wl[u][q].x, wh[u][q].x, wl[u][q].y, wh[u][q].y, av[u].x, av[u].y);
-        mma_bf16_16816(acc[q], wl[u][q].z, wh[u][q].z, wl[u][q].w, wh[u][q].w, av[u].z, av[u].w);
+#pragma unroll
+        for (int j = 0; j < NB; ++j) {
+          mma_bf16_16816(acc[q][j], wl[u][q].x, wh[u][q].x, wl[u][q].y, wh[u][q].y, av[u][j].x, av[u][j].y);
+          mma_bf16_16816(acc[q][j], wl[u][q].z, wh[u][q].z, wl[u][q].w, wh[u][q].w, av[u][j].z, av[u][j].w);
+        }
       }
     }
   }
-  // d0, d1: (row g, activation rows 2t, 2t+1); d2, d3: (row g+8, same)
+  // d0, d1: (row g, activation rows 8j + 2t, 8j + 2t + 1); d2, d3: (row g + 8, same)
 #pragma unroll
   for (int q = 0; q < NT; ++q) {
-    sred[q][warp][g][2 * t] = acc[q][0];
-    sred[q][warp][g][2 * t + 1] = acc[q][1];
-    sred[q][warp][g + 8][2 * t] = acc[q][2];
-    sred[q][warp][g + 8][2 * t + 1] = acc[q][3];
+#pragma unroll
+    for (int j = 0; j < NB; ++j) {
+      sred[q][warp][g][8 * j + 2 * t] = acc[q][j][0];
+      sred[q][warp][g][8 * j + 2 * t + 1] = acc[q][j][1];
+      sred[q][warp][g + 8][8 * j + 2 * t] = acc[q][j][2];
+      sred[q][warp][g + 8][8 * j + 2 * t + 1] = acc[q][j][3];
+    }
   }
   __syncthreads();
-  if (threadIdx.x < 16 * GEMV_MAX_M) {
-    const int r = threadIdx.x & 15, m = threadIdx.x >> 4;
+  for (int i = threadIdx.x; i < 16 * M; i += 256) {
+    const int r = i & 15, m = i >> 4;
 #pragma unroll
     for (int q = 0; q < NT; ++q) {
       float v = 0.f;
@@ -1498,14 +1521,14 @@ __global__ void __launch_bounds__(256) gemv_mma_kernel(const GemmParams p) {
   }
   __syncthreads();
   if (threadIdx.x < M) {
-    const int row = threadIdx.x;
+    const int lrow = threadIdx.x, row = m0 + lrow;
     const int ncols = min(16, p.N - c0);
     if constexpr (kGlu) {  // the register kernel's SwiGLU epilogue: h = silu(g) * u, pre = g | u (bf16)
       __nv_bfloat16* hrow = reinterpret_cast<__nv_bfloat16*>(p.C) + static_cast<int64_t>(row) * p.ldc + c0;
       __nv_bfloat16* prow = reinterpret_cast<__nv_bfloat16*>(p.C2) + static_cast<int64_t>(row) * p.ldc2 + c0;
       for (int c = 0; c < ncols; ++c) {
-        const float gv = __bfloat162float(__float2bfloat16(sout[row][c]));
-        const float uv = __bfloat162float(__float2bfloat16(sout[row][GEMV_COLS + c]));
+        const float gv = __bfloat162float(__float2bfloat16(sout[lrow][c]));
+        const float uv = __bfloat162float(__float2bfloat16(sout[lrow][GEMV_COLS + c]));
         prow[c] = __float2bfloat16(gv);
         prow[p.swiglu_half + c] = __float2bfloat16(uv);
         hrow[c] = __float2bfloat16(dev::silu(gv) * uv);
@@ -1513,7 +1536,7 @@ __global__ void __launch_bounds__(256) gemv_mma_kernel(const GemmParams p) {
     } else {
       uint32_t rr[32];
 #pragma unroll
-      for (int c = 0; c < 32; ++c) rr[c] = __float_as_uint(c < 16 ? sout[row][c] : 0.f);
+      for (int c = 0; c < 32; ++c) rr[c] = __float_as_uint(c < 16 ? sout[lrow][c] : 0.f);
       epilogue_chunk<EPI>(p, row, c0, ncols, rr);
     }
   }
@@ -1528,6 +1551,16 @@ bool gemv_mma_on() {
   return on;
 }
 
+// Largest M the tensor-core weight-streaming kernel takes (SW_GEMV_MMA_MAX_M); above it the
+// tcgen05 GEMM, whose 128-row tiles leave most SMs idle at decode batch sizes (N / 256 CTAs).
+int gemv_mma_max_m() {
+  static const int v = [] {
+    const char* e = std::getenv("SW_GEMV_MMA_MAX_M");
+    return e != nullptr ? std::atoi(e) : 64;
+  }();
+  return v;
+}
+
 // Measured on B200 (tools/gemv_bench.py, M = 1): KSPLIT 2 / UNROLL 4 streams N = 4096 weights at
 // 2.7-3.9 TB/s (was 2.3-2.6), KSPLIT 1 / UNROLL 2 is best from N = 11008 up (3.1-4.0 TB/s)
 template <Epi EPI>
@@ -1538,8 +1571,15 @@ cudaError_t launch_gemv(const GemmParams& p, cudaStream_t stream) {
       const char* e = std::getenv("SW_GEMV_MMA_MIN_M");
       return e != nullptr ? std::atoi(e) : 1;
     }();
-    if (p.M >= mma_min_m && p.K % 32 == 0 && gemv_mma_on()) {
-      gemv_mma_kernel<EPI><<<(p.N + 15) / 16, 256, 0, stream>>>(p);
+    if ((p.M >= mma_min_m || p.M > GEMV_MAX_M) && p.K % 32 == 0 && gemv_mma_on()) {
+      const unsigned nt = static_cast<unsigned>((p.N + 15) / 16);
+      if (p.M <= 8) {
+        gemv_mma_kernel<EPI, 1><<<dim3(1, nt), 256, 0, stream>>>(p);
+      } else if (p.M <= 16) {
+        gemv_mma_kernel<EPI, 2><<<dim3(1, nt), 256, 0, stream>>>(p);
+      } else {
+        gemv_mma_kernel<EPI, 4><<<dim3((p.M + 31) / 32, nt), 256, 0, stream>>>(p);
+      }
       return cudaGetLastError();
     }
   }
@@ -1718,7 +1758,7 @@ bool gemv_tma_on() {
 
 // The small-M path applies to forward-layout GEMMs whose activations fit in shared memory.
 bool gemv_ok(const GemmParams& p) {
-  return p.M <= GEMV_MAX_M && !p.a_mn_major && !p.b_mn_major && p.K % 8 == 0 && p.lda % 8 == 0 &&
+  return (p.M <= GEMV_MAX_M || (p.M <= gemv_mma_max_m() && p.K % 32 == 0 && gemv_mma_on())) && !p.a_mn_major && !p.b_mn_major && p.K % 8 == 0 && p.lda % 8 == 0 &&
          p.ldb % 8 == 0 &&
          (p.epi == Epi::kStoreBf16 || p.epi == Epi::kStoreF32 || p.epi == Epi::kBiasGelu ||
           p.epi == Epi::kResidF32 || p.epi == Epi::kSwiGLU) &&
@@ -1747,7 +1787,7 @@ cudaError_t gemm_bf16(const GemmParams& p, cudaStream_t stream) {
   }
   if (p.N % 8 != 0) throw std::runtime_error("gemm_bf16: N must be a multiple of 8");
   if (p.ldc % 8 != 0) throw std::runtime_error("gemm_bf16: ldc must be a multiple of 8");
-  if (gemv_ok(p) && p.epi != Epi::kSwiGLU && gemv_tma_on()) {
+  if (gemv_ok(p) && p.M <= GEMV_MAX_M && p.epi != Epi::kSwiGLU && gemv_tma_on()) {
     switch (p.epi) {
       case Epi::kStoreBf16: return launch_gemv_tma<Epi::kStoreBf16>(p, stream);
       case Epi::kStoreF32: return launch_gemv_tma<Epi::kStoreF32>(p, stream);

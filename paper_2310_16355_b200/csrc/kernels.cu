@@ -926,6 +926,13 @@ __global__ void cast_kernel(const float* __restrict__ x, bf16* __restrict__ y, i
   }
 }
 
+__global__ void widen_kernel(const bf16* __restrict__ x, float* __restrict__ y, int64_t n) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    y[i] = __bfloat162float(x[i]);
+  }
+}
+
 __global__ void fill_kernel(float* x, int64_t n, float v) {
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -1186,6 +1193,10 @@ void scale_f32(float* x, int64_t n, float a, cudaStream_t s) {
 
 void cast_f32_bf16(const float* x, bf16* y, int64_t n, cudaStream_t s) {
   cast_kernel<<<grid_for(n, 256, 4), 256, 0, s>>>(x, y, n);
+}
+
+void cast_bf16_f32(const bf16* x, float* y, int64_t n, cudaStream_t s) {
+  widen_kernel<<<grid_for(n, 256, 4), 256, 0, s>>>(x, y, n);
 }
 
 void fill_f32(float* out, int64_t n, float v, cudaStream_t s) {

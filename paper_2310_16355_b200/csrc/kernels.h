@@ -132,6 +132,7 @@ void adamw(float* p, float* m, float* v, const float* g, bf16* shadow, int64_t n
 void nonfinite_check(const float* x, int64_t n, int* flag, cudaStream_t s);
 void scale_f32(float* x, int64_t n, float a, cudaStream_t s);
 void cast_f32_bf16(const float* x, bf16* y, int64_t n, cudaStream_t s);
+void cast_bf16_f32(const bf16* x, float* y, int64_t n, cudaStream_t s);
 
 // ---- T5 encoder-decoder extension (t5_kernels.cu) ----
 // q / k / v / o: bf16 rows of B*T tokens (row pitch ld*), head h at column h*dk; lse [B, Hl, Tq];

@@ -47,8 +47,8 @@ constexpr int64_t kAlign = 64;  // elements; keeps every slot 256-B aligned in f
 // ---------------------------------------------------------------------------------------------
 // construction: plan -> per-rank layout
 // ---------------------------------------------------------------------------------------------
-Model::Model(const ModelSpec& spec, const Plan& plan, Mesh* mesh, int batch, int seq_len)
-    : spec_(spec), plan_(plan), mesh_(mesh), B_(batch), T_(seq_len) {
+Model::Model(const ModelSpec& spec, const Plan& plan, Mesh* mesh, int batch, int seq_len, bool inference)
+    : spec_(spec), plan_(plan), mesh_(mesh), B_(batch), T_(seq_len), inference_(inference) {
   if (mesh == nullptr) fail(SW_ERR_CONFIG, "sw_model_create: mesh is NULL");
   if (batch < 1 || seq_len < 1) {
     fail(SW_ERR_CONFIG, "transformer_logits: batch and seq_len must be positive");
@@ -291,29 +291,54 @@ void Model::build_layout() {
 
 void Model::allocate() {
   const int64_t M = M_;
+  // Inference-only models (sw_model_create_inference) hold the bf16 GEMM weights, the fp32
+  // small parameters (region 2) and, per layer, only the K/V cache (the qkv activations): no
+  // fp32 master copies of the GEMM weights, no gradients or AdamW moments, and the other
+  // activations alternate between two buffers because nothing reads them back.
+  const int64_t n_small = flat_n_ - weights_end_;
+  const int keep = inference_ ? std::min(L_, 2) : L_;  // distinct per-layer activation buffers
   for (int dev : mesh_->local_devices()) {
     Rank R;
     R.device = dev;
     R.dpi = mesh_->dp_index(dev);
     R.mpi = mesh_->mp_index(dev);
-    R.p = alloc<float>(flat_n_);
-    R.g = alloc<float>(flat_n_);
-    R.m = alloc<float>(flat_n_);
-    R.v = alloc<float>(flat_n_);
     R.w = alloc<bf16>(flat_n_);
-    cuda_check(cudaMemsetAsync(R.p, 0, flat_n_ * 4, stream_), "memset");
-    cuda_check(cudaMemsetAsync(R.g, 0, flat_n_ * 4, stream_), "memset");
-    cuda_check(cudaMemsetAsync(R.m, 0, flat_n_ * 4, stream_), "memset");
-    cuda_check(cudaMemsetAsync(R.v, 0, flat_n_ * 4, stream_), "memset");
     cuda_check(cudaMemsetAsync(R.w, 0, flat_n_ * 2, stream_), "memset");
-    for (int l = 0; l <= L_; ++l) R.hs.push_back(alloc<float>(M * d_));
+    if (inference_) {
+      float* small = alloc<float>(n_small);
+      cuda_check(cudaMemsetAsync(small, 0, n_small * 4, stream_), "memset");
+      R.p = small - weights_end_;  // only offsets >= weights_end_ are dereferenced
+    } else {
+      R.p = alloc<float>(flat_n_);
+      R.g = alloc<float>(flat_n_);
+      R.m = alloc<float>(flat_n_);
+      R.v = alloc<float>(flat_n_);
+      cuda_check(cudaMemsetAsync(R.p, 0, flat_n_ * 4, stream_), "memset");
+      cuda_check(cudaMemsetAsync(R.g, 0, flat_n_ * 4, stream_), "memset");
+      cuda_check(cudaMemsetAsync(R.m, 0, flat_n_ * 4, stream_), "memset");
+      cuda_check(cudaMemsetAsync(R.v, 0, flat_n_ * 4, stream_), "memset");
+    }
+    for (int l = 0; l <= L_; ++l) R.hs.push_back(l <= keep ? alloc<float>(M * d_) : R.hs[l % 2]);
     for (int l = 0; l < L_; ++l) {
+      R.qkv.push_back(alloc<bf16>(M * 3 * dl_));
+      if (l >= keep) {
+        const int j = l % 2;
+        R.hmid.push_back(R.hmid[j]);
+        R.stats1.push_back(R.stats1[j]);
+        R.stats2.push_back(R.stats2[j]);
+        R.a1.push_back(R.a1[j]);
+        R.a2.push_back(R.a2[j]);
+        R.o.push_back(R.o[j]);
+        R.lse.push_back(R.lse[j]);
+        R.pre.push_back(R.pre[j]);
+        R.act.push_back(R.act[j]);
+        continue;
+      }
       R.hmid.push_back(alloc<float>(M * d_));
       R.stats1.push_back(alloc<float>(2 * M));
       R.stats2.push_back(alloc<float>(2 * M));
       R.a1.push_back(alloc<bf16>(M * d_));
       R.a2.push_back(alloc<bf16>(M * d_));
-      R.qkv.push_back(alloc<bf16>(M * 3 * dl_));
       R.o.push_back(alloc<bf16>(M * dl_));
       R.lse.push_back(alloc<float>(M * hl_));
       R.pre.push_back(alloc<bf16>(M * fl_ * (spec_.swiglu ? 2 : 1)));  // SwiGLU: gate | up
@@ -329,25 +354,27 @@ void Model::allocate() {
     R.wsum = alloc<float>(1);
     R.loss = alloc<double>(1);
     R.part = alloc<float>(M * d_);
-    R.dx = alloc<float>(M * d_);
     if (ar_bf16_) R.arb = alloc<bf16>(M * d_);
-    R.gres = alloc<float>(M * d_);
-    R.gb = alloc<bf16>(M * d_);
-    R.dpre = alloc<bf16>(M * fl_ * (spec_.swiglu ? 2 : 1));
-    R.dout = alloc<bf16>(M * dl_);
-    R.dqkv = alloc<bf16>(M * 3 * dl_);
-    const int64_t chunks = (M + 255) / 256;
-    int64_t widest = d_;
-    if (3 * dl_ > widest) widest = 3 * dl_;
-    if (fl_ > widest) widest = fl_;
-    // also holds the GeLU-backward epilogue's per-32-row partial column sums of dpre
-    R.col_scratch = alloc<float>(std::max(chunks * widest, ((M + 31) / 32) * std::max<int64_t>(fl_, 3 * dl_)));
-    R.ln_partials = alloc<float>(k::layernorm_bwd_partials(d_));
-    R.tok_keys = alloc<uint32_t>(k::embed_bwd_keys(M_));
-    R.attn_scratch = alloc<float>(M * hl_ + M * 2 * dl_ + 64);
     R.xstats = alloc<float>(static_cast<int64_t>(mesh_->mp) * M * 2);
     R.xt = alloc<float>(M);
     R.xlse = alloc<float>(M);
+    if (!inference_) {  // backward-only buffers
+      R.dx = alloc<float>(M * d_);
+      R.gres = alloc<float>(M * d_);
+      R.gb = alloc<bf16>(M * d_);
+      R.dpre = alloc<bf16>(M * fl_ * (spec_.swiglu ? 2 : 1));
+      R.dout = alloc<bf16>(M * dl_);
+      R.dqkv = alloc<bf16>(M * 3 * dl_);
+      const int64_t chunks = (M + 255) / 256;
+      int64_t widest = d_;
+      if (3 * dl_ > widest) widest = 3 * dl_;
+      if (fl_ > widest) widest = fl_;
+      // also holds the GeLU-backward epilogue's per-32-row partial column sums of dpre
+      R.col_scratch = alloc<float>(std::max(chunks * widest, ((M + 31) / 32) * std::max<int64_t>(fl_, 3 * dl_)));
+      R.ln_partials = alloc<float>(k::layernorm_bwd_partials(d_));
+      R.tok_keys = alloc<uint32_t>(k::embed_bwd_keys(M_));
+      R.attn_scratch = alloc<float>(M * hl_ + M * 2 * dl_ + 64);
+    }
     ranks_.push_back(R);
   }
   d_flag_ = alloc<int>(1);
@@ -367,9 +394,18 @@ std::vector<Rank*> Model::replica(int dpi) {
 // ---------------------------------------------------------------------------------------------
 void Model::init_params(uint64_t seed, const std::string& stream_name) {
   const uint64_t key = mix64(seed ^ mix64(fnv1a(stream_name)));
+  // inference-only: a GEMM weight is drawn in fp32 into a scratch slot and rounded into w
+  float* scratch = nullptr;
+  if (inference_) {
+    int64_t widest = 0;
+    for (const Slot& s : slots_)
+      if (s.offset < weights_end_) widest = std::max(widest, s.numel);
+    if (widest > 0) cuda_check(cudaMalloc(&scratch, widest * 4), "cudaMalloc");
+  }
   for (Rank& R : ranks_) {
     for (const Slot& s : slots_) {
-      float* dst = R.p + s.offset;
+      const bool via_scratch = inference_ && s.offset < weights_end_;
+      float* dst = via_scratch ? scratch : R.p + s.offset;
       if (s.init == 0) {
         cuda_check(cudaMemsetAsync(dst, 0, s.numel * 4, stream_), "memset");
       } else if (s.init == 1) {
@@ -384,11 +420,23 @@ void Model::init_params(uint64_t seed, const std::string& stream_name) {
                        s.init_scale, stream_);
         ++launches_;
       }
+      if (via_scratch) {
+        k::cast_f32_bf16(scratch, W(R, static_cast<int>(&s - slots_.data())), s.numel, stream_);
+        ++launches_;
+      }
     }
-    cuda_check(cudaMemsetAsync(R.m, 0, flat_n_ * 4, stream_), "memset");
-    cuda_check(cudaMemsetAsync(R.v, 0, flat_n_ * 4, stream_), "memset");
-    k::cast_f32_bf16(R.p, R.w, flat_n_, stream_);
+    if (inference_) {
+      k::cast_f32_bf16(R.p + weights_end_, R.w + weights_end_, flat_n_ - weights_end_, stream_);
+    } else {
+      cuda_check(cudaMemsetAsync(R.m, 0, flat_n_ * 4, stream_), "memset");
+      cuda_check(cudaMemsetAsync(R.v, 0, flat_n_ * 4, stream_), "memset");
+      k::cast_f32_bf16(R.p, R.w, flat_n_, stream_);
+    }
     ++launches_;
+  }
+  if (scratch != nullptr) {
+    cuda_check(cudaStreamSynchronize(stream_), "init_params");
+    cudaFree(scratch);
   }
   step_ = 0;
   seed_ = seed;
@@ -409,8 +457,12 @@ void Model::set_tensor(const std::string& name, int which, const float* full, in
                            " elements, got " + std::to_string(numel));
   }
   if (which != 0 && which != 2 && which != 3) fail(SW_ERR_CONFIG, "set_tensor: `which` must be 0, 2 or 3");
+  if (which != 0) check_trainable("set_tensor (AdamW moments)");
+  const bool via_scratch = inference_ && s.offset < weights_end_;
+  float* scratch = nullptr;
+  if (via_scratch) cuda_check(cudaMalloc(&scratch, s.numel * 4), "cudaMalloc");
   for (Rank& R : ranks_) {
-    float* dst = (which == 0 ? R.p : which == 2 ? R.m : R.v) + s.offset;
+    float* dst = via_scratch ? scratch : (which == 0 ? R.p : which == 2 ? R.m : R.v) + s.offset;
     if (s.layout.kind != Layout::kSplit) {
       cuda_check(cudaMemcpyAsync(dst, full, numel * 4, cudaMemcpyHostToDevice, stream_), "H2D");
     } else {
@@ -427,11 +479,14 @@ void Model::set_tensor(const std::string& name, int which, const float* full, in
       }
     }
     if (which == 0) k::cast_f32_bf16(dst, R.w + s.offset, s.numel, stream_);
+    if (via_scratch) cuda_check(cudaStreamSynchronize(stream_), "set_param");  // scratch reused per rank
   }
   cuda_check(cudaStreamSynchronize(stream_), "set_param");
+  if (scratch != nullptr) cudaFree(scratch);
 }
 
 void Model::save_checkpoint(const std::string& path, const std::vector<CkptRng>& rngs) {
+  check_trainable("save_checkpoint");
   check_not_poisoned("save_checkpoint");
   Checkpoint ck;
   ck.step = step_;
@@ -480,6 +535,7 @@ void Model::load_checkpoint(const std::string& path) {
     const std::string name = ck.records[r].name.substr(7);
     const int64_t n = static_cast<int64_t>(ck.records[r].data.size());
     set_tensor(name, 0, ck.records[r].data.data(), n);
+    if (inference_) continue;  // the Predictor's load: parameters only
     set_tensor(name, 2, ck.records[r + 1].data.data(), n);
     set_tensor(name, 3, ck.records[r + 2].data.data(), n);
   }
@@ -497,30 +553,41 @@ void Model::get_tensor(const std::string& name, int which, float* full, int64_t 
     fail(SW_ERR_SHAPE, "get_tensor: '" + name + "' has " + std::to_string(numel_of(s.global)) +
                            " elements, got a buffer of " + std::to_string(numel));
   }
-  auto base = [&](Rank& R) -> float* {
-    switch (which) {
-      case 0: return R.p;
-      case 1: return R.g;
-      case 2: return R.m;
-      case 3: return R.v;
+  if (which < 0 || which > 3) fail(SW_ERR_CONFIG, "get_tensor: `which` must be 0..3");
+  if (which != 0) check_trainable("get_tensor (gradients / AdamW moments)");
+  // an inference-only model keeps GEMM weights in bf16 only: they are widened into scratch
+  struct Scratch {
+    float* p = nullptr;
+    ~Scratch() {
+      if (p != nullptr) cudaFree(p);
     }
-    fail(SW_ERR_CONFIG, "get_tensor: `which` must be 0..3");
+  } scratch;
+  const bool widen = inference_ && s.offset < weights_end_;
+  if (widen) cuda_check(cudaMalloc(&scratch.p, s.numel * 4), "cudaMalloc");
+  auto src = [&](Rank& R) -> const float* {
+    if (widen) {
+      k::cast_bf16_f32(R.w + s.offset, scratch.p, s.numel, stream_);
+      cuda_check(cudaStreamSynchronize(stream_), "get_tensor");
+      return scratch.p;
+    }
+    float* base = which == 0 ? R.p : which == 1 ? R.g : which == 2 ? R.m : R.v;
+    return base + s.offset;
   };
   cuda_check(cudaStreamSynchronize(stream_), "sync");
   if (s.layout.kind != Layout::kSplit) {
     Rank& R = *replica(mesh_->emulated ? 0 : ranks_[0].dpi)[0];
-    cuda_check(cudaMemcpy(full, base(R) + s.offset, numel * 4, cudaMemcpyDeviceToHost), "D2H");
+    cuda_check(cudaMemcpy(full, src(R), numel * 4, cudaMemcpyDeviceToHost), "D2H");
     return;
   }
   const int64_t rows = s.global[0], cols = s.global[1];
   if (mesh_->emulated) {
     for (Rank* R : replica(0)) {
-      const float* src = base(*R) + s.offset;
+      const float* from = src(*R);
       if (s.layout.dim == 0) {
-        cuda_check(cudaMemcpy(full + R->mpi * s.local[0] * cols, src, s.numel * 4, cudaMemcpyDeviceToHost), "D2H");
+        cuda_check(cudaMemcpy(full + R->mpi * s.local[0] * cols, from, s.numel * 4, cudaMemcpyDeviceToHost), "D2H");
       } else {
         const int64_t lc = s.local[1];
-        cuda_check(cudaMemcpy2D(full + R->mpi * lc, cols * 4, src, lc * 4, lc * 4, rows, cudaMemcpyDeviceToHost),
+        cuda_check(cudaMemcpy2D(full + R->mpi * lc, cols * 4, from, lc * 4, lc * 4, rows, cudaMemcpyDeviceToHost),
                    "D2H 2D");
       }
     }
@@ -530,7 +597,7 @@ void Model::get_tensor(const std::string& name, int which, float* full, int64_t 
   Rank& R = ranks_[0];
   float* tmp = nullptr;
   cuda_check(cudaMalloc(&tmp, numel * 4), "cudaMalloc");
-  nccl_check(ncclAllGather(base(R) + s.offset, tmp, s.numel, ncclFloat, mesh_->mp_comm, stream_), "AllGather");
+  nccl_check(ncclAllGather(src(R), tmp, s.numel, ncclFloat, mesh_->mp_comm, stream_), "AllGather");
   std::vector<float> host(numel);
   cuda_check(cudaMemcpyAsync(host.data(), tmp, numel * 4, cudaMemcpyDeviceToHost, stream_), "D2H");
   cuda_check(cudaStreamSynchronize(stream_), "sync");
@@ -1216,6 +1283,7 @@ void Model::backward_replica(std::vector<Rank*>& grp, bool accumulate) {
 }
 
 void Model::forward_backward(bool accumulate) {
+  check_trainable("forward_backward");
   check_not_poisoned("forward_backward");
   cuda_check(cudaSetDevice(mesh_->cuda_device), "cudaSetDevice");
   launches_ = 0;
@@ -1241,6 +1309,7 @@ void Model::forward_only() {
 }
 
 void Model::scale_grads(double factor) {
+  check_trainable("scale_grads");
   for (Rank& R : ranks_) {
     k::scale_f32(R.g, flat_n_, static_cast<float>(factor), stream_);
     ++launches_;
@@ -1248,6 +1317,7 @@ void Model::scale_grads(double factor) {
 }
 
 void Model::dp_sync() {
+  check_trainable("dp_sync_grads");
   if (mesh_->dp == 1) return;
   const float inv = 1.0f / static_cast<float>(mesh_->dp);
   for (int j = 0; j < mesh_->mp; ++j) {
@@ -1267,6 +1337,7 @@ void Model::dp_sync() {
 }
 
 void Model::adamw(double lr, double b1, double b2, double eps, double wd, bool check_finite) {
+  check_trainable("adamw_step");
   check_not_poisoned("adamw_step");
   if (check_finite) {
     cuda_check(cudaMemsetAsync(d_flag_, 0, sizeof(int), stream_), "memset");
@@ -1308,6 +1379,10 @@ void Model::adamw(double lr, double b1, double b2, double eps, double wd, bool c
   cuda_check(cudaGetLastError(), "adamw");
 }
 
+void Model::check_trainable(const char* what) const {
+  if (inference_) fail(SW_ERR_CONFIG, std::string(what) + ": this is an inference-only model (no gradients or optimizer state)");
+}
+
 void Model::check_not_poisoned(const char* what) const {
   if (poisoned_) {
     fail(SW_ERR_NONFINITE, std::string(what) + ": the model state was left half-updated by a non-finite fused "
@@ -1316,6 +1391,7 @@ void Model::check_not_poisoned(const char* what) const {
 }
 
 bool Model::train_step(double lr, double b1, double b2, double eps, double wd) {
+  check_trainable("train_step");
   check_not_poisoned("train_step");
   static const bool disabled = [] {
     const char* e = std::getenv("SW_FUSED_ADAMW");
@@ -1410,6 +1486,40 @@ void Model::pick_tokens(std::vector<Rank*>& grp, const std::vector<const bf16*>&
   }
 }
 
+void Model::shift_rows(std::vector<Rank*>& grp, int64_t rows) {
+  const int64_t d = d_, mp = mesh_->mp;
+  auto mv = [rows](auto& ptr, int64_t per_row) {
+    if (ptr != nullptr) ptr += rows * per_row;
+  };
+  for (Rank* R : grp) {
+    for (int l = 0; l <= L_; ++l) mv(R->hs[l], d);
+    for (int l = 0; l < L_; ++l) {
+      mv(R->hmid[l], d);
+      mv(R->stats1[l], 1);
+      mv(R->stats2[l], 1);
+      mv(R->a1[l], d);
+      mv(R->a2[l], d);
+      mv(R->qkv[l], 3 * dl_);
+      mv(R->o[l], dl_);
+      mv(R->lse[l], hl_);
+      mv(R->pre[l], fl_ * (spec_.swiglu ? 2 : 1));
+      mv(R->act[l], fl_);
+    }
+    mv(R->statsf, 1);
+    mv(R->f, d);
+    mv(R->logits, ldv_);
+    mv(R->tokens, 1);
+    mv(R->targets, 1);
+    mv(R->weights, 1);
+    mv(R->wloss, 1);
+    mv(R->part, d);
+    mv(R->arb, d);
+    mv(R->xstats, 2 * mp);
+    mv(R->xt, 1);
+    mv(R->xlse, 1);
+  }
+}
+
 void Model::window_forward(std::vector<Rank*>& grp, const std::vector<std::vector<int32_t>>& ctx, int take) {
   // the reference's window (cli.cpp:435-440): the last `take` context tokens at positions
   // 0..take-1, zeros after; the causal mask keeps the padding out of position take-1
@@ -1424,7 +1534,46 @@ void Model::window_forward(std::vector<Rank*>& grp, const std::vector<std::vecto
     k::fill_f32(R->weights, M_, 1.0f, stream_);
     ++launches_;
   }
-  forward_replica(grp, false);
+  // Causality makes rows >= take irrelevant to the logits of row take-1 and to the K/V cache
+  // rows a later cached step reads (< take; it writes row p itself before attending to it), so
+  // a short prompt's prefill runs only the first Tp = take rounded up to 128 rows of each
+  // sequence, one sequence at a time (SW_PREFILL_TRIM=0: the whole window, as the reference).
+  static const bool trim_on = [] {
+    const char* e = std::getenv("SW_PREFILL_TRIM");
+    return !(e != nullptr && e[0] == '0');
+  }();
+  const int Tp = (take + 127) / 128 * 128;
+  if (trim_on && Tp < T_) {
+    const int B = B_, T = T_, chunks = ar_chunks_;
+    const int64_t M = M_;
+    B_ = 1;
+    T_ = Tp;
+    M_ = Tp;
+    if (Tp % ar_chunks_ != 0) ar_chunks_ = 1;
+    int shifted = 0;
+    auto restore = [&] {
+      shift_rows(grp, -static_cast<int64_t>(shifted) * T);
+      B_ = B;
+      T_ = T;
+      M_ = M;
+      ar_chunks_ = chunks;
+    };
+    try {
+      for (int b = 0; b < B; ++b) {
+        forward_replica(grp, false);
+        if (b + 1 < B) {
+          shift_rows(grp, T);
+          ++shifted;
+        }
+      }
+    } catch (...) {
+      restore();
+      throw;
+    }
+    restore();
+  } else {
+    forward_replica(grp, false);
+  }
   std::vector<const bf16*> rows;
   for (Rank* R : grp) rows.push_back(R->logits + static_cast<int64_t>(take - 1) * ldv_);
   pick_tokens(grp, rows, static_cast<int64_t>(T_) * ldv_);

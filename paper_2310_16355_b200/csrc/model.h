@@ -49,6 +49,7 @@ struct LayerSlots {
 
 struct Rank {
   int device = 0, dpi = 0, mpi = 0;
+  // inference-only model: g, m, v null; p valid at region-2 offsets only (>= weights_end_)
   float *p = nullptr, *g = nullptr, *m = nullptr, *v = nullptr;
   bf16* w = nullptr;
   // activations saved for the backward, per layer
@@ -90,7 +91,10 @@ enum ProfCat : int {
 
 class Model {
  public:
-  Model(const ModelSpec& spec, const Plan& plan, Mesh* mesh, int batch, int seq_len);
+  // inference = true: an inference-only model (generate / forward_only / logits; see allocate):
+  // bf16 GEMM weights + fp32 small parameters + the K/V cache, about a ninth of the training
+  // footprint, so an OPT-66B-shape model fits one B200 (cfg5).
+  Model(const ModelSpec& spec, const Plan& plan, Mesh* mesh, int batch, int seq_len, bool inference = false);
   ~Model();
 
   void init_params(uint64_t seed, const std::string& stream_name);
@@ -126,6 +130,7 @@ class Model {
   // adamw and save_checkpoint refuse) until init_params or load_checkpoint.
   bool train_step(double lr, double b1, double b2, double eps, double wd);
   bool poisoned() const { return poisoned_; }
+  bool inference() const { return inference_; }
   double last_loss();
   void logits_to_host(float* out);
 
@@ -139,6 +144,7 @@ class Model {
 
  private:
   void check_not_poisoned(const char* what) const;
+  void check_trainable(const char* what) const;  // refuses on an inference-only model
   template <typename T>
   T* alloc(int64_t n);
   void build_layout();
@@ -232,6 +238,7 @@ class Model {
   int64_t bytes_ = 0;
   uint64_t step_ = 0;
   bool poisoned_ = false;
+  bool inference_ = false;
   uint64_t seed_ = 0;
   struct DecodeBufs {
     float *x = nullptr, *xmid = nullptr, *part = nullptr, *stats = nullptr, *arg = nullptr;
@@ -249,6 +256,9 @@ class Model {
   // p >= 0: position p (host value); p < 0: every rank's dec_[].pos, advanced at the step's end
   void decode_step(std::vector<Rank*>& grp, int p);
   void window_forward(std::vector<Rank*>& grp, const std::vector<std::vector<int32_t>>& ctx, int take);
+  // moves every per-token activation pointer of the group by `rows` token rows (the prefill runs
+  // one sequence at a time over the first rows of its window, see window_forward)
+  void shift_rows(std::vector<Rank*>& grp, int64_t rows);
   // argmax of one logits row per sequence (per-rank base pointer, row stride in elements) into
   // every rank's dec_[].tok, combining vocab shards when the head is split
   void pick_tokens(std::vector<Rank*>& grp, const std::vector<const bf16*>& rows, int64_t stride);

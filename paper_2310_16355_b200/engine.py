@@ -33,6 +33,7 @@ def _declare():
     L.sw_mesh_free.argtypes = [vp]
     L.sw_mesh_free.restype = None
     L.sw_model_create.argtypes = [vp, vp, vp, C.c_int, C.c_int, C.POINTER(vp)]
+    L.sw_model_create_inference.argtypes = [vp, vp, vp, C.c_int, C.c_int, C.POINTER(vp)]
     L.sw_model_free.argtypes = [vp]
     L.sw_model_free.restype = None
     L.sw_model_init_params.argtypes = [vp, C.c_uint64, C.c_char_p]
@@ -81,7 +82,7 @@ def _declare():
                "sw_t5_launch_count", "sw_t5_device_bytes"):
         getattr(L, fn).restype = C.c_int
     for fn in ("sw_nccl_unique_id", "sw_mesh_create", "sw_mesh_comm_report",
-               "sw_mesh_reset_comm_report", "sw_model_create", "sw_model_init_params",
+               "sw_mesh_reset_comm_report", "sw_model_create", "sw_model_create_inference", "sw_model_init_params",
                "sw_model_set_param", "sw_model_get_tensor", "sw_model_stage_batch",
                "sw_model_forward_backward", "sw_model_scale_grads", "sw_model_dp_sync",
                "sw_model_adamw_step", "sw_model_train_step", "sw_model_last_loss",
@@ -162,15 +163,21 @@ def build_mesh(dp_size: int, mp_size: int, n_hosts: int = 1) -> Mesh:
 
 class Model:
     """The traced transformer_loss program lowered onto a mesh with a sharding plan, plus its
-    sharded train state (params, grads, AdamW moments) in HBM."""
+    sharded train state (params, grads, AdamW moments) in HBM.
 
-    def __init__(self, spec: rules.ModelSpec, plan: rules.Plan, mesh: Mesh, batch: int, seq_len: int):
+    inference=True builds the Predictor-only variant (sw_model_create_inference): bf16 weight
+    shards + K/V cache, no gradients or optimizer state; the training methods raise ConfigError."""
+
+    def __init__(self, spec: rules.ModelSpec, plan: rules.Plan, mesh: Mesh, batch: int, seq_len: int,
+                 inference: bool = False):
         L = _declare()
         self.spec, self.plan, self.mesh = spec, plan, mesh
         self.batch, self.seq_len = batch, seq_len
+        self.inference = inference
         self.shapes = dict(rules.transformer_param_shapes(spec))
         h = C.c_void_p()
-        _lib.check(L.sw_model_create(spec.handle, plan.handle, mesh.handle, batch, seq_len, C.byref(h)))
+        create = L.sw_model_create_inference if inference else L.sw_model_create
+        _lib.check(create(spec.handle, plan.handle, mesh.handle, batch, seq_len, C.byref(h)))
         self._h = h
 
     def close(self):

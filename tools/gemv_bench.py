@@ -30,6 +30,11 @@ def run(M, N, K, iters=50):
 
 
 if __name__ == "__main__":
+    if len(sys.argv) > 1:  # M list: the decode projections of LLaMA-7B at each M
+        for M in (int(x) for x in sys.argv[1].split(",")):
+            for N, K in ((12288, 4096), (4096, 4096), (22016, 4096), (4096, 11008)):
+                print(json.dumps(run(M, N, K)))
+        sys.exit(0)
     for sh in [(1, 12288, 4096), (1, 4096, 4096), (1, 11008, 4096), (1, 4096, 11008), (1, 32000, 4096),
                (4, 12288, 4096), (8, 4096, 11008)]:
         print(json.dumps(run(*sh)))
