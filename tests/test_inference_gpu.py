@@ -95,3 +95,39 @@ def test_inference_footprint():
     # training: 4 fp32 + 1 bf16 copies of the state; inference: bf16 + the small fp32 region
     assert train.device_bytes() >= 18 * n
     assert infer.device_bytes() < train.device_bytes() / 2
+
+
+def test_opt66b_width_tp8_generation_matches_tp1(tmp_path):
+    """cfg5 at OPT-66B width (2 of 64 layers, tied 50272 x 9216 embedding, 72 heads of 128): the
+    TP=8 plan's KV-cached greedy generation (inference-only model, the 8 ranks emulated on one
+    GPU) picks the tokens of the unsharded model's teacher-forced full-window forward except at
+    near-ties; the per-rank footprint is the TP=8 shard of the bf16 weights + K/V cache."""
+    path = tmp_path / "opt66b_2l.spec"
+    path.write_text("vocab_size = 50272\nn_layers = 2\nd_model = 9216\nn_heads = 72\nd_ff = 36864\n"
+                    "max_seq_len = 256\ntie_embeddings = true\n")
+    spec = rules.read_model_spec(str(path))
+    shapes = rules.transformer_param_shapes(spec)
+    batch, P, n_new = 2, 24, 40
+    prompts = rng_ref.RngStream(4, "prompts").below(batch * P, spec.vocab_size).reshape(batch, P)
+    got = {}
+    for mp in (8, 1):
+        plan = rules.derive_plan(shapes, mp, spec.overrides)
+        model = engine.Model(spec, plan, engine.Mesh(1, mp), batch, 256, inference=True)
+        model.init_params(3, "model-init")
+        model.set_param("embed/tok/kernel", model.get_param("embed/tok/kernel") * 24.0)
+        got[mp] = model.generate(prompts, n_new)
+        if mp == 8:
+            per_rank = model.device_bytes() / 8
+            continue
+        ctx = np.concatenate([prompts, got[8]], 1)
+        win = np.zeros((batch, 256), np.int32)
+        win[:, :P + n_new - 1] = ctx[:, :P + n_new - 1]
+        model.stage_batch(win, win)
+        logits = model.forward_logits()[:, P - 1:P + n_new - 1]
+    srt = np.sort(logits, -1)
+    margin = (srt[..., -1] - srt[..., -2]) / np.maximum(np.abs(srt[..., -1]), 1.0)
+    decisive = margin >= 0.02
+    assert np.array_equal(logits.argmax(-1)[decisive], got[8][decisive])
+    assert decisive.mean() > 0.5
+    n_params = sum(int(np.prod(d)) for _, d in shapes)
+    assert per_rank < 2 * n_params / 8 + 4 * (50272 + 256) * 9216 + 1.5e9
