@@ -88,20 +88,23 @@ def test_generate_rejects_bad_prompts():
         model.generate(np.zeros((2, 17), np.int32), 3)
 
 
-@pytest.mark.parametrize("hd,mp,batch", [(64, 2, 2), (128, 1, 3)])
-def test_trimmed_prefill_matches_full_window(tmp_path, hd, mp, batch):
+@pytest.mark.parametrize("hd,mp,batch,extra", [(64, 2, 2, ""), (128, 1, 3, ""),
+                                             (64, 2, 2, "role lm_head/kernel = fully_connected\n"),
+                                             (128, 2, 2, "mlp = swiglu\nnorm = rmsnorm\n")])
+def test_trimmed_prefill_matches_full_window(tmp_path, hd, mp, batch, extra):
     """A prompt much shorter than seq_len is prefilled over its first 128-row tile only, one
     sequence at a time (window_forward); the cached steps then cross that tile. Every generated
     token must be the argmax of the untrimmed full-window forward over the same context
     (teacher-forced, one device forward) except at near-ties."""
     path = tmp_path / "long.spec"
     path.write_text(f"vocab_size = 96\nn_layers = 2\nd_model = {2 * hd}\nn_heads = 2\nd_ff = {4 * hd}\n"
-                    "max_seq_len = 384\n")
+                    "max_seq_len = 384\n" + extra)
     spec = rules.read_model_spec(str(path))
     plan = rules.derive_plan(rules.transformer_param_shapes(spec), mp, spec.overrides)
     model = engine.Model(spec, plan, engine.Mesh(1, mp), batch, 384, inference=True)
     model.init_params(5, "model-init")
-    model.set_param("embed/tok/kernel", model.get_param("embed/tok/kernel") * 24.0)
+    head = "embed/tok/kernel" if spec.tie_embeddings else "lm_head/kernel"
+    model.set_param(head, model.get_param(head) * 24.0)
     P, n_new = 40, 100
     prompts = rng_ref.RngStream(9, "prompts").below(batch * P, spec.vocab_size).reshape(batch, P)
     got = model.generate(prompts, n_new)
