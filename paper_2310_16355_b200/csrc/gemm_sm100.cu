@@ -1542,6 +1542,170 @@ __global__ void __launch_bounds__(256) gemv_mma_kernel(const GemmParams p) {
   }
 }
 
+// ---------------------------------------------------------------------------------------------
+// Decode-size GEMMs on tcgen05 (9 <= M <= 128 activation rows): swap-AB, C^T[N, M] = W[N, K] .
+// A[M, K]^T, so the weight rows fill the 128-lane MMA M dimension and the few activation rows
+// are the MMA N (MP = M rounded up to 16; the mma.sync kernel above tops out near 90 TF/s, which
+// caps it from M ~ 24 on). One CTA per (128 weight rows, K slice): a TMA ring streams [128 x 64]
+// weight boxes, one pass over the weights for the whole job, against [MP x 64] activation boxes
+// (L2-resident). The S K-slices of a row block form one thread-block cluster: their fp32
+// partials are summed in rank order through distributed shared memory (deterministic, no global
+// workspace or counters, graph- and stream-safe), then the rank-0 CTA runs the epilogue shared
+// with the other GEMM kernels. Two CTAs per SM (~100 KB of shared memory each).
+// ---------------------------------------------------------------------------------------------
+template <Epi EPI, int MP>
+struct Gtc {
+  static constexpr int NT = EPI == Epi::kSwiGLU ? 2 : 1;  // SwiGLU: gate and up tiles
+  static constexpr int W_BYTES = 128 * 64 * 2;
+  static constexpr int A_BYTES = MP * 64 * 2;
+  static constexpr int STAGE = NT * W_BYTES + A_BYTES;
+  static constexpr int RAW = (100 * 1024) / STAGE;
+  static constexpr int STAGES = RAW < 3 ? 3 : (RAW > 8 ? 8 : RAW);
+  static constexpr int ROWP = 129;  // padded row (floats) of the transposed accumulator
+  static constexpr int RED = NT * MP * ROWP * 4;
+  static constexpr int BODY = STAGES * STAGE > RED ? STAGES * STAGE : RED;
+  static constexpr int SMEM = BODY + 256 + 1024;  // + barriers + alignment slack
+  static constexpr uint32_t TCOLS = NT * MP <= 32 ? 32 : NT * MP <= 64 ? 64 : NT * MP <= 128 ? 128 : 256;
+};
+
+template <Epi EPI, int MP>
+__global__ void __launch_bounds__(128, 1) gemv_tc_kernel(const __grid_constant__ CUtensorMap tw,
+                                                         const __grid_constant__ CUtensorMap ta, const GemmParams p,
+                                                         int S) {
+  using G = Gtc<EPI, MP>;
+  extern __shared__ uint8_t gtc_raw[];
+  uint8_t* sm = gtc_raw + ((1024 - (dev::smem_u32(gtc_raw) & 1023)) & 1023);
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + G::BODY);
+  uint64_t* empty = full + G::STAGES;
+  uint64_t* done = empty + G::STAGES;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(done + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
+  const int rb = blockIdx.x / S, s = blockIdx.x - rb * S;  // the cluster: the S slices of row block rb
+  const int n0 = rb * 128;
+  const int nkb = (p.K + 63) / 64;
+  const int kb0 = s * nkb / S, kb1 = (s + 1) * nkb / S;
+  if (tid == 0) {
+    dev::tma_prefetch_desc(&tw);
+    dev::tma_prefetch_desc(&ta);
+    for (int i = 0; i < G::STAGES; ++i) {
+      dev::mbar_init(&full[i], 1);
+      dev::mbar_init(&empty[i], 1);
+    }
+    dev::mbar_init(done, 1);
+    dev::fence_barrier_init();
+  }
+  if (warp == 2) dev::tmem_alloc<G::TCOLS>(tslot);
+  dev::tc_fence_before();
+  __syncthreads();
+  dev::tc_fence_after();
+  const uint32_t tmem = *tslot;
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int kb = kb0, i = 0; kb < kb1; ++kb, ++i) {
+        const int st = i % G::STAGES;
+        dev::mbar_wait(&empty[st], ((i / G::STAGES) & 1) ^ 1);
+        uint8_t* b = sm + st * G::STAGE;
+        dev::mbar_arrive_expect_tx(&full[st], G::STAGE);
+        dev::tma_load_2d(b, &tw, &full[st], kb * 64, n0);
+        if constexpr (G::NT == 2) dev::tma_load_2d(b + G::W_BYTES, &tw, &full[st], kb * 64, p.swiglu_half + n0);
+        dev::tma_load_2d(b + G::NT * G::W_BYTES, &ta, &full[st], kb * 64, 0);
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t idesc = dev::make_idesc_bf16(128, MP, 0, 0);
+    for (int kb = kb0, i = 0; kb < kb1; ++kb, ++i) {
+      const int st = i % G::STAGES;
+      dev::mbar_wait(&full[st], (i / G::STAGES) & 1);
+      dev::tc_fence_after();
+      const uint32_t b = dev::smem_u32(sm + st * G::STAGE);
+      if (dev::elect_one_sync()) {
+        const uint64_t da = dev::make_sdesc_sw128(b + G::NT * G::W_BYTES, 16, 1024);
+#pragma unroll
+        for (int q = 0; q < G::NT; ++q) {
+          const uint64_t dw = dev::make_sdesc_sw128(b + q * G::W_BYTES, 16, 1024);
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)
+            dev::umma_f16_ss(tmem + q * MP, dw + kk * 2, da + kk * 2, idesc, (i > 0 || kk > 0) ? 1u : 0u);
+        }
+        dev::umma_commit(&empty[st]);
+      }
+      __syncwarp();
+    }
+    if (dev::elect_one_sync()) dev::umma_commit(done);
+    __syncwarp();
+  }
+  // accumulator (lane = weight row n0 + tid, column = activation row) -> transposed in shared
+  // memory (the ring is idle: every MMA, hence every TMA load, has completed)
+  dev::mbar_wait(done, 0);
+  dev::tc_fence_after();
+  float* sT = reinterpret_cast<float*>(sm);
+  const uint32_t lb = static_cast<uint32_t>(warp * 32) << 16;
+#pragma unroll 1
+  for (int c = 0; c < G::NT * MP; c += 16) {
+    uint32_t r[16];
+    dev::tmem_ld_32x32b_x16(tmem + lb + c, r);
+    dev::tmem_ld_wait();
+#pragma unroll
+    for (int j = 0; j < 16; ++j) sT[(c + j) * G::ROWP + tid] = __uint_as_float(r[j]);
+  }
+  dev::tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    dev::tc_fence_after();
+    dev::tmem_dealloc<G::TCOLS>(tmem);
+  }
+  const int M = p.M;
+  // Activation rows m with m % S == s are summed over the S slices (in rank order: the same bits
+  // whichever CTA adds them) and written out by this CTA. Only the owner of a row reads the
+  // peers' copies of it, so the sum goes back into the owner's own copy in place.
+  if (S > 1) {
+    dev::cluster_sync();  // every slice's partial is in its shared memory
+    const uint32_t base = dev::smem_u32(sT);
+#pragma unroll 1
+    for (int m = s; m < M; m += S) {
+#pragma unroll
+      for (int q = 0; q < G::NT; ++q) {
+        const int e = (q * MP + m) * G::ROWP + tid;
+        float part[8];
+#pragma unroll
+        for (int r = 0; r < 8; ++r)
+          part[r] = r < S ? (r == s ? sT[e] : dev::ld_shared_cluster_f32(dev::mapa_shared(base + e * 4, r))) : 0.f;
+        float v = part[0];
+#pragma unroll
+        for (int r = 1; r < 8; ++r)
+          if (r < S) v += part[r];
+        sT[e] = v;
+      }
+    }
+    dev::cluster_sync();  // the peers have read this CTA's partials
+  }
+  __syncthreads();
+  const int mine = S > 1 ? (M - s + S - 1) / S : M;  // rows s, s + S, ...
+  for (int it = tid; it < mine * 4; it += 128) {
+    const int m = s + (it >> 2) * S, cc = it & 3;
+    const int col0 = n0 + cc * 32;
+    const int ncols = min(32, p.N - col0);
+    if (ncols <= 0) continue;
+    const float* row = sT + m * G::ROWP + cc * 32;
+    if constexpr (EPI == Epi::kSwiGLU) {  // h = silu(g) * u, pre = g | u (bf16), as the other kernels
+      __nv_bfloat16* hrow = reinterpret_cast<__nv_bfloat16*>(p.C) + static_cast<int64_t>(m) * p.ldc + col0;
+      __nv_bfloat16* prow = reinterpret_cast<__nv_bfloat16*>(p.C2) + static_cast<int64_t>(m) * p.ldc2 + col0;
+      for (int c = 0; c < ncols; ++c) {
+        const float gv = __bfloat162float(__float2bfloat16(row[c]));
+        const float uv = __bfloat162float(__float2bfloat16(row[MP * G::ROWP + c]));
+        prow[c] = __float2bfloat16(gv);
+        prow[p.swiglu_half + c] = __float2bfloat16(uv);
+        hrow[c] = __float2bfloat16(dev::silu(gv) * uv);
+      }
+    } else {
+      uint32_t r[32];
+#pragma unroll
+      for (int c = 0; c < 32; ++c) r[c] = __float_as_uint(row[c]);
+      epilogue_chunk<EPI>(p, m, col0, ncols, r);
+    }
+  }
+}
+
 // SW_GEMV_MMA=0: the register-streamed kernel for every M
 bool gemv_mma_on() {
   static const bool on = [] {
@@ -1605,6 +1769,63 @@ cudaError_t launch_gemv(const GemmParams& p, cudaStream_t stream) {
     go(std::integral_constant<int, GEMV_MAX_M>{});
   }
   return cudaGetLastError();
+}
+
+// SW_GEMV_TC=0: no tcgen05 decode GEMM; SW_GEMV_TC_MIN_M: smallest M it takes (default 9)
+bool gemv_tc_on() {
+  static const bool on = [] {
+    const char* e = std::getenv("SW_GEMV_TC");
+    return !(e != nullptr && e[0] == '0');
+  }();
+  return on;
+}
+
+int gemv_tc_min_m() {
+  static const int v = [] {
+    const char* e = std::getenv("SW_GEMV_TC_MIN_M");
+    return e != nullptr ? std::atoi(e) : 9;
+  }();
+  return v;
+}
+
+template <Epi EPI, int MP>
+cudaError_t launch_gemv_tc_mp(const GemmParams& p, cudaStream_t stream) {
+  using G = Gtc<EPI, MP>;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(gemv_tc_kernel<EPI, MP>, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  const uint64_t w_rows = EPI == Epi::kSwiGLU ? 2ull * p.swiglu_half : static_cast<uint64_t>(p.N);
+  const CUtensorMap tw = make_tmap_bf16_2d(p.B, p.K, w_rows, p.ldb, 64, 128);
+  const CUtensorMap ta = make_tmap_bf16_2d(p.A, p.K, p.M, p.lda, 64, MP);
+  const int nrb = (p.N + 127) / 128, nkb = (p.K + 63) / 64;
+  // K slices per row block: enough CTAs for two per SM, each slice at least two 64-deep blocks
+  const int target = 2 * device_sm_count();
+  int S = 1;
+  while (S < 8 && nrb * S * 2 <= target && nkb / (S * 2) >= 2) S *= 2;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(nrb * S));
+  cfg.blockDim = dim3(128);
+  cfg.dynamicSmemBytes = G::SMEM;
+  cfg.stream = stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = static_cast<unsigned>(S);
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, gemv_tc_kernel<EPI, MP>, tw, ta, p, S);
+}
+
+template <Epi EPI>
+cudaError_t launch_gemv_tc(const GemmParams& p, cudaStream_t stream) {
+  if (p.M <= 16) return launch_gemv_tc_mp<EPI, 16>(p, stream);
+  if (p.M <= 32) return launch_gemv_tc_mp<EPI, 32>(p, stream);
+  if (p.M <= 64) return launch_gemv_tc_mp<EPI, 64>(p, stream);
+  return launch_gemv_tc_mp<EPI, 128>(p, stream);
 }
 
 // Small-M path, TMA-streamed (every epilogue but SwiGLU): the weight [N, K] is read as boxes of
@@ -1757,6 +1978,14 @@ bool gemv_tma_on() {
 }
 
 // The small-M path applies to forward-layout GEMMs whose activations fit in shared memory.
+bool gemv_tc_ok(const GemmParams& p) {
+  return gemv_tc_on() && p.M >= gemv_tc_min_m() && p.M <= 128 && !p.a_mn_major && !p.b_mn_major && p.K % 8 == 0 &&
+         p.lda % 8 == 0 && p.ldb % 8 == 0 &&
+         (p.epi == Epi::kStoreBf16 || p.epi == Epi::kStoreF32 || p.epi == Epi::kBiasGelu ||
+          p.epi == Epi::kResidF32 || p.epi == Epi::kSwiGLU) &&
+         !(p.epi == Epi::kStoreF32 && p.accumulate);
+}
+
 bool gemv_ok(const GemmParams& p) {
   return (p.M <= GEMV_MAX_M || (p.M <= gemv_mma_max_m() && p.K % 32 == 0 && gemv_mma_on())) && !p.a_mn_major && !p.b_mn_major && p.K % 8 == 0 && p.lda % 8 == 0 &&
          p.ldb % 8 == 0 &&
@@ -1787,6 +2016,16 @@ cudaError_t gemm_bf16(const GemmParams& p, cudaStream_t stream) {
   }
   if (p.N % 8 != 0) throw std::runtime_error("gemm_bf16: N must be a multiple of 8");
   if (p.ldc % 8 != 0) throw std::runtime_error("gemm_bf16: ldc must be a multiple of 8");
+  if (gemv_tc_ok(p)) {
+    switch (p.epi) {
+      case Epi::kStoreBf16: return launch_gemv_tc<Epi::kStoreBf16>(p, stream);
+      case Epi::kStoreF32: return launch_gemv_tc<Epi::kStoreF32>(p, stream);
+      case Epi::kBiasGelu: return launch_gemv_tc<Epi::kBiasGelu>(p, stream);
+      case Epi::kResidF32: return launch_gemv_tc<Epi::kResidF32>(p, stream);
+      case Epi::kSwiGLU: return launch_gemv_tc<Epi::kSwiGLU>(p, stream);
+      default: break;
+    }
+  }
   if (gemv_ok(p) && p.M <= GEMV_MAX_M && p.epi != Epi::kSwiGLU && gemv_tma_on()) {
     switch (p.epi) {
       case Epi::kStoreBf16: return launch_gemv_tma<Epi::kStoreBf16>(p, stream);

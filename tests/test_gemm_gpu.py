@@ -192,7 +192,7 @@ def test_gemm_adamw_epilogue_gated_by_flag(M, N, K):
                                    # register-streamed one)
                                    (1, 1376, 4096), (3, 200, 136), (8, 688, 512),
                                    # batched decode: 2 / 4 activation groups per warp, 2 CTA groups
-                                   (16, 688, 512), (29, 1376, 4096), (64, 200, 1376)])
+                                   (16, 688, 512), (29, 1376, 4096), (64, 200, 1376), (128, 1376, 4096)])
 def test_gemm_swiglu_fwd_bwd(M, N, K):
     """SwiGLU extension vs torch fp32 on the same bf16 operands: the fused [gate; up]
     GEMM writes h = silu(g)*u and the bf16 pre-activations; the down-projection dgrad epilogue
@@ -227,14 +227,14 @@ def test_gemm_swiglu_fwd_bwd(M, N, K):
     assert _rel(dpre[:, :N], want_g) < 1e-2 and _rel(dpre[:, N:], want_u) < 1e-2
 
 
-@pytest.mark.parametrize("M", [1, 3, 8, 12, 16, 29, 32, 47, 64])
+@pytest.mark.parametrize("M", [1, 3, 8, 12, 16, 29, 32, 47, 64, 65, 100, 128])
 @pytest.mark.parametrize("epi", [0, 1, 3])
 @pytest.mark.parametrize("N,K", [(200, 136), (4096, 1376), (12288, 4096)])
 def test_small_m_gemv_path(M, epi, N, K):
-    """Decode-size forward GEMMs (M <= 64) take the weight-streaming kernels: the tensor-core one
-    (mma.sync, 1 / 2 / 4 activation groups of 8 rows per warp, CTA groups of 32 rows past M = 32;
-    ragged M and N = 200 in a partial 16-row tile) when K % 32 == 0, else the register-streamed
-    one (M <= 8) or the tcgen05 GEMM; same epilogues."""
+    """Decode-size forward GEMMs take the weight-streaming kernels: M <= 8 the mma.sync one (the
+    register-streamed one when K % 32 != 0), 9 <= M <= 128 the tcgen05 swap-AB kernel (weight rows
+    as the MMA M, K slices reduced across a cluster through distributed shared memory; ragged M,
+    N = 200 in a partial 128-row block, K = 136 / 1376 in partial 64-deep boxes); same epilogues."""
     gen = torch.Generator(device=DEV).manual_seed(M * 10 + epi)
     A, B, ref = _ref_operands(M, N, K, 0, 0, gen)
     bias = torch.randn(N, generator=gen, device=DEV)

@@ -11,11 +11,18 @@ from paper_2310_16355_b200 import _lib  # noqa: E402
 def run(M, N, K, iters=50):
     L = _lib.lib()
     A = torch.randn(M, K, device="cuda").bfloat16()
-    W = torch.randn(N, K, device="cuda").bfloat16()
+    # enough weight copies to exceed L2 (126 MB) several times over: every launch streams from HBM
+    n_w = max(2, -(-512 * 2**20 // (N * K * 2)))
+    Ws = [torch.randn(N, K, device="cuda").bfloat16() for _ in range(n_w)]
     C = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
     s = torch.cuda.current_stream().cuda_stream
-    f = lambda: _lib.check(L.sw_k_gemm_bf16(M, N, K, A.data_ptr(), K, 0, W.data_ptr(), K, 0, 0, C.data_ptr(), N,  # noqa: E731
-                                            None, 0, None, None, 0, 1.0, 0, s))
+    it = [0]
+
+    def f():
+        W = Ws[it[0] % n_w]
+        it[0] += 1
+        _lib.check(L.sw_k_gemm_bf16(M, N, K, A.data_ptr(), K, 0, W.data_ptr(), K, 0, 0, C.data_ptr(), N,
+                                    None, 0, None, None, 0, 1.0, 0, s))
     for _ in range(5):
         f()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
