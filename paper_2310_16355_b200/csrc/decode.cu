@@ -3,6 +3,7 @@
 // HBM-bound (every step reads the weights and the cached keys/values once).
 #include <algorithm>
 #include <cfloat>
+#include <cstdlib>
 #include <stdexcept>
 
 #include "kernels.h"
@@ -119,15 +120,46 @@ __global__ void __launch_bounds__(256) decode_attention_kernel(const bf16* __res
   }
 }
 
-// Split-key decode attention (flash-decoding): grid (B * Hl, DSPLIT). Split s of a head takes
-// keys [s c, min(p + 1, (s + 1) c)), c = ceil((p + 1) / DSPLIT); lanes work in groups of
-// G = hd / 8 (16-byte loads) and every warp keeps UNR keys' K / V loads in flight before
-// consuming them. The split holding key p reads the new k / v from the step's qkv row and writes
-// them into the cache (the fused kv_scatter). Each split leaves an unnormalised (m, l, o) partial;
-// the split that takes the last ticket of its head's counter merges them (the counter is never
-// reset: tickets are counted modulo DSPLIT).
-constexpr int DSPLIT = 16;
-constexpr int DUNR = 4;
+// Split-key decode attention (flash-decoding): grid (B * Hl, S), S = the CTA budget of a launch
+// (SW_DECODE_CTAS, 640) over the B * Hl heads, at most DSPLIT. The position is known on the device
+// only (CUDA-graph step), so the splits actually used are chosen there: n = min(S, ceil((p + 1) /
+// kps)), kps = SW_DECODE_KPS (64), and the CTAs of splits >= n exit at once. Split s of a head
+// takes keys [s c, min(p + 1, (s + 1) c)), c = ceil((p + 1) / n); lanes work in groups of G =
+// hd / 8 (16-byte loads) and every warp keeps UNR keys' K / V loads in flight before consuming
+// them. The split holding key p reads the new k / v from the step's qkv row and writes them into
+// the cache (the fused kv_scatter). Each split leaves an unnormalised (m, l, o) partial; the
+// split that takes the last ticket of its head's counter merges them and resets the counter.
+// Measured: tools/decode_attn_bench.py (graph-timed kernel: 16 fixed splits 12.8 / 16.5 us at
+// p = 512 with 32 / 72 heads, ~8.5 / 9.5 with ~4 splits) and tools/ab_decode.sh (LLaMA-7B step,
+// same box: batch 1 2.98 -> 2.80 ms/token, batch 8 3.87 -> 3.36).
+#ifndef SW_DSPLIT
+#define SW_DSPLIT 16
+#endif
+#ifndef SW_DUNR
+#define SW_DUNR 2
+#endif
+#ifndef SW_DKPS
+#define SW_DKPS 64
+#endif
+#ifndef SW_DCTAS
+#define SW_DCTAS 640
+#endif
+// fewest keys per split (SW_DECODE_KPS) and the CTA budget of one launch (SW_DECODE_CTAS)
+int env_or(const char* name, int dflt) {
+  const char* e = std::getenv(name);
+  return e != nullptr && std::atoi(e) > 0 ? std::atoi(e) : dflt;
+}
+int decode_kps() {
+  static const int v = env_or("SW_DECODE_KPS", SW_DKPS);
+  return v;
+}
+int decode_ctas() {
+  static const int v = env_or("SW_DECODE_CTAS", SW_DCTAS);
+  return v;
+}
+constexpr int DSPLIT = SW_DSPLIT;  // most splits (partial buffer rows per head)
+constexpr int DUNR = SW_DUNR;
+
 
 template <int HD>
 __global__ void __launch_bounds__(256) decode_attention_split_kernel(const bf16* __restrict__ qnew,
@@ -135,7 +167,8 @@ __global__ void __launch_bounds__(256) decode_attention_split_kernel(const bf16*
                                                                      bf16* __restrict__ out, int T, int p,
                                                                      const int* __restrict__ pd, int Hl,
                                                                      float scale_log2, float* __restrict__ part,
-                                                                     unsigned int* __restrict__ ticket) {
+                                                                     unsigned int* __restrict__ ticket, int kps,
+                                                                     int max_split) {
   if (pd != nullptr) p = *pd;
   constexpr int G = HD / 8;
   constexpr int KPW = 32 / G;
@@ -149,7 +182,9 @@ __global__ void __launch_bounds__(256) decode_attention_split_kernel(const bf16*
   const int grp = lane / G, gl = lane % G;
   const int gid = warp * KPW + grp;
   const int nk = p + 1;
-  const int chunk = (nk + DSPLIT - 1) / DSPLIT;
+  const int nsplit = max(1, min(max_split, (nk + kps - 1) / kps));
+  if (sp >= nsplit) return;
+  const int chunk = (nk + nsplit - 1) / nsplit;
   const int k0 = sp * chunk, k1 = min(nk, k0 + chunk);
   const bf16* qrow = qnew + static_cast<int64_t>(b) * 3 * dl;
   float q[8];
@@ -238,7 +273,10 @@ __global__ void __launch_bounds__(256) decode_attention_split_kernel(const bf16*
   }
   __threadfence();
   __syncthreads();
-  if (threadIdx.x == 0) last = (atomicAdd(ticket + bh, 1u) % DSPLIT) == DSPLIT - 1;
+  if (threadIdx.x == 0) {
+    last = atomicAdd(ticket + bh, 1u) == static_cast<unsigned>(nsplit - 1);
+    if (last) ticket[bh] = 0;  // every split of this head has arrived
+  }
   __syncthreads();
   if (!last) return;
   __threadfence();
@@ -246,9 +284,9 @@ __global__ void __launch_bounds__(256) decode_attention_split_kernel(const bf16*
     const int c = threadIdx.x;
     const float* ph = part + static_cast<int64_t>(bh) * DSPLIT * (HD + 2);
     float M = -INFINITY;
-    for (int s2 = 0; s2 < DSPLIT; ++s2) M = fmaxf(M, __ldcg(ph + s2 * (HD + 2)));
+    for (int s2 = 0; s2 < nsplit; ++s2) M = fmaxf(M, __ldcg(ph + s2 * (HD + 2)));
     float L = 0.f, acc = 0.f;
-    for (int s2 = 0; s2 < DSPLIT; ++s2) {
+    for (int s2 = 0; s2 < nsplit; ++s2) {
       const float ms = __ldcg(ph + s2 * (HD + 2));
       if (ms == -INFINITY) continue;
       const float f = dev::ex2_approx(ms - M);
@@ -453,16 +491,21 @@ void bump_i32(int* x, cudaStream_t s) { bump_kernel<<<1, 1, 0, s>>>(x); }
 bool decode_attention_split(const bf16* qkv_new, bf16* cache, bf16* out, int B, int T, int p, int Hl, int hd,
                             cudaStream_t s, const int* p_dev, float* part, unsigned int* ticket) {
   const float scale_log2 = static_cast<float>(1.4426950408889634 / sqrt(static_cast<double>(hd)));
-  const dim3 grid(B * Hl, DSPLIT);
+  // splits per head: keys / kps, at most the CTA budget spread over the B * Hl heads
+  const int max_split = std::max(1, std::min(DSPLIT, decode_ctas() / (B * Hl)));
+  const dim3 grid(B * Hl, max_split);
   switch (hd) {
     case 64:
-      decode_attention_split_kernel<64><<<grid, 256, 0, s>>>(qkv_new, cache, out, T, p, p_dev, Hl, scale_log2, part, ticket);
+      decode_attention_split_kernel<64><<<grid, 256, 0, s>>>(qkv_new, cache, out, T, p, p_dev, Hl, scale_log2, part, ticket,
+                                                                decode_kps(), max_split);
       return true;
     case 128:
-      decode_attention_split_kernel<128><<<grid, 256, 0, s>>>(qkv_new, cache, out, T, p, p_dev, Hl, scale_log2, part, ticket);
+      decode_attention_split_kernel<128><<<grid, 256, 0, s>>>(qkv_new, cache, out, T, p, p_dev, Hl, scale_log2, part, ticket,
+                                                                decode_kps(), max_split);
       return true;
     case 256:
-      decode_attention_split_kernel<256><<<grid, 256, 0, s>>>(qkv_new, cache, out, T, p, p_dev, Hl, scale_log2, part, ticket);
+      decode_attention_split_kernel<256><<<grid, 256, 0, s>>>(qkv_new, cache, out, T, p, p_dev, Hl, scale_log2, part, ticket,
+                                                                decode_kps(), max_split);
       return true;
     default:
       return false;
