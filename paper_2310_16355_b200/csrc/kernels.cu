@@ -1031,6 +1031,72 @@ void embed_bwd_pos(const float* g, float* dpos, int B, int T, int d, int accumul
   embed_bwd_pos_kernel<<<T, 256, 0, s>>>(g, dpos, B, T, d, accumulate);
 }
 
+// Decode-size rows (M <= 8, one CTA of 1024 threads per row): the statistics in one pass (sum and
+// sum of squares reduced together, var = E[x^2] - mean^2), so the row costs one block reduction
+// instead of two -- the kernel is latency-bound at this size. SW_DECODE_LN1P=0 keeps ln_fwd.
+template <int V4>
+__global__ void __launch_bounds__(1024) ln_fwd_1pass_kernel(const float* __restrict__ x, const float* __restrict__ scale,
+                                                            const float* __restrict__ bias, bf16* __restrict__ y,
+                                                            float* __restrict__ mean_out, float* __restrict__ rstd_out,
+                                                            int d, float eps, int rms) {
+  __shared__ float2 red[32];
+  const int64_t row = blockIdx.x;
+  const float* xr = x + row * d;
+  float4 v[V4];
+  float s = 0.f, q = 0.f;
+#pragma unroll
+  for (int j = 0; j < V4; ++j) {
+    const int c = (threadIdx.x + j * 1024) * 4;
+    v[j] = c < d ? *reinterpret_cast<const float4*>(xr + c) : make_float4(0, 0, 0, 0);
+    s += v[j].x + v[j].y + v[j].z + v[j].w;
+    q += v[j].x * v[j].x + v[j].y * v[j].y + v[j].z * v[j].z + v[j].w * v[j].w;
+  }
+  s = warp_sum(s);
+  q = warp_sum(q);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane == 0) red[w] = make_float2(s, q);
+  __syncthreads();
+  float2 t = red[lane];
+  t.x = warp_sum(t.x);
+  t.y = warp_sum(t.y);
+  const float mean = rms ? 0.f : t.x / d;
+  const float var = fmaxf(t.y / d - mean * mean, 0.f);
+  const float rstd = 1.0f / sqrtf(var + eps);
+  bf16* yr = y + row * d;
+#pragma unroll
+  for (int j = 0; j < V4; ++j) {
+    const int c = (threadIdx.x + j * 1024) * 4;
+    if (c < d) {
+      const float4 sc = *reinterpret_cast<const float4*>(scale + c);
+      const float4 bi = rms ? make_float4(0.f, 0.f, 0.f, 0.f) : *reinterpret_cast<const float4*>(bias + c);
+      uint2 o;
+      o.x = dev::pack_bf16x2((v[j].x - mean) * rstd * sc.x + bi.x, (v[j].y - mean) * rstd * sc.y + bi.y);
+      o.y = dev::pack_bf16x2((v[j].z - mean) * rstd * sc.z + bi.z, (v[j].w - mean) * rstd * sc.w + bi.w);
+      *reinterpret_cast<uint2*>(yr + c) = o;
+    }
+  }
+  if (threadIdx.x == 0) {
+    if (mean_out != nullptr) mean_out[row] = mean;
+    rstd_out[row] = rstd;
+  }
+}
+
+void layernorm_fwd_small(const float* x, const float* scale, const float* bias, bf16* y, float* mean, float* rstd,
+                         int64_t M, int d, float eps, cudaStream_t s, int rms) {
+  static const bool on = [] {
+    const char* e = std::getenv("SW_DECODE_LN1P");
+    return !(e != nullptr && e[0] == '0');
+  }();
+  const unsigned g = static_cast<unsigned>(M);
+  if (on && M <= 8 && d % 4 == 0 && d <= 4096) {
+    ln_fwd_1pass_kernel<1><<<g, 1024, 0, s>>>(x, scale, bias, y, mean, rstd, d, eps, rms);
+  } else if (on && M <= 8 && d % 4 == 0 && d <= 12288) {
+    ln_fwd_1pass_kernel<3><<<g, 1024, 0, s>>>(x, scale, bias, y, mean, rstd, d, eps, rms);
+  } else {
+    layernorm_fwd(x, scale, bias, y, mean, rstd, M, d, eps, s, rms);
+  }
+}
+
 void layernorm_fwd(const float* x, const float* scale, const float* bias, bf16* y, float* mean,
                    float* rstd, int64_t M, int d, float eps, cudaStream_t s, int rms) {
   const unsigned g = static_cast<unsigned>(M);

@@ -31,6 +31,10 @@ void embed_bwd_pos(const float* g, float* dpos, int B, int T, int d, int accumul
 // rms = 1: RMSNorm (extension): no centring, no bias (bias may be null), mean = 0.
 void layernorm_fwd(const float* x, const float* scale, const float* bias, bf16* y, float* mean,
                    float* rstd, int64_t M, int d, float eps, cudaStream_t s, int rms = 0);
+// Decode-step variant (M <= 8): one-pass statistics, one CTA of 1024 threads per row; other
+// sizes fall through to layernorm_fwd.
+void layernorm_fwd_small(const float* x, const float* scale, const float* bias, bf16* y, float* mean, float* rstd,
+                         int64_t M, int d, float eps, cudaStream_t s, int rms);
 // dx = rstd*(g - mean(g) - xhat*mean(g*xhat)), g = dy*scale (kernels.hpp:232-271).
 // g_io: residual-stream gradient; g_io = (accumulate ? g_io : 0) + dx; g_bf16 = bf16(g_io).
 // dscale += sum_rows dy*xhat, dbias += sum_rows dy (atomics; caller zeroes when needed).

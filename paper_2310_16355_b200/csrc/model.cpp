@@ -1603,7 +1603,7 @@ void Model::decode_step(std::vector<Rank*>& grp, int p) {
   for (int l = 0; l < L_; ++l) {
     const LayerSlots& ls = layers_[l];
     each([&](Rank& R, DecodeBufs& D) {
-      k::layernorm_fwd(D.x, P(R, ls.ln1_s), Pn(R, ls.ln1_b), D.a, D.stats, D.stats + B, B, d, 1e-5f, stream_,
+      k::layernorm_fwd_small(D.x, P(R, ls.ln1_s), Pn(R, ls.ln1_b), D.a, D.stats, D.stats + B, B, d, 1e-5f, stream_,
                        spec_.rmsnorm);
       ++launches_;
       gemm(R, B, 3 * dl, d, D.a, d, 0, W(R, ls.q_k), d, 0, static_cast<int>(Epi::kStoreBf16), D.qkv, 3 * dl, nullptr,
@@ -1631,7 +1631,7 @@ void Model::decode_step(std::vector<Rank*>& grp, int p) {
       });
     }
     each([&](Rank& R, DecodeBufs& D) {
-      k::layernorm_fwd(D.xmid, P(R, ls.ln2_s), Pn(R, ls.ln2_b), D.a, D.stats, D.stats + B, B, d, 1e-5f, stream_,
+      k::layernorm_fwd_small(D.xmid, P(R, ls.ln2_s), Pn(R, ls.ln2_b), D.a, D.stats, D.stats + B, B, d, 1e-5f, stream_,
                        spec_.rmsnorm);
       ++launches_;
       if (spec_.swiglu) {
@@ -1659,7 +1659,7 @@ void Model::decode_step(std::vector<Rank*>& grp, int p) {
   const int head = head_ >= 0 ? head_ : tok_;
   std::vector<const bf16*> rows;
   each([&](Rank& R, DecodeBufs& D) {
-    k::layernorm_fwd(D.x, P(R, lnf_s_), Pn(R, lnf_b_), D.f, D.stats, D.stats + B, B, d, 1e-5f, stream_,
+    k::layernorm_fwd_small(D.x, P(R, lnf_s_), Pn(R, lnf_b_), D.f, D.stats, D.stats + B, B, d, 1e-5f, stream_,
                      spec_.rmsnorm);
     ++launches_;
     gemm(R, B, vl_, d, D.f, d, 0, W(R, head), d, 0, static_cast<int>(Epi::kStoreBf16), D.logits, ldv_);
