@@ -311,7 +311,7 @@ void Model::allocate() {
     if (inference_) {
       float* small = alloc<float>(n_small);
       cuda_check(cudaMemsetAsync(small, 0, n_small * 4, stream_), "memset");
-      R.p = small - weights_end_;  // only offsets >= weights_end_ are dereferenced
+      R.p_small = small;
     } else {
       R.p = alloc<float>(flat_n_);
       R.g = alloc<float>(flat_n_);
@@ -409,7 +409,7 @@ void Model::init_params(uint64_t seed, const std::string& stream_name) {
   for (Rank& R : ranks_) {
     for (const Slot& s : slots_) {
       const bool via_scratch = inference_ && s.offset < weights_end_;
-      float* dst = via_scratch ? scratch : R.p + s.offset;
+      float* dst = via_scratch ? scratch : pval(R, s.offset);
       if (s.init == 0) {
         cuda_check(cudaMemsetAsync(dst, 0, s.numel * 4, stream_), "memset");
       } else if (s.init == 1) {
@@ -430,7 +430,7 @@ void Model::init_params(uint64_t seed, const std::string& stream_name) {
       }
     }
     if (inference_) {
-      k::cast_f32_bf16(R.p + weights_end_, R.w + weights_end_, flat_n_ - weights_end_, stream_);
+      k::cast_f32_bf16(R.p_small, R.w + weights_end_, flat_n_ - weights_end_, stream_);
     } else {
       cuda_check(cudaMemsetAsync(R.m, 0, flat_n_ * 4, stream_), "memset");
       cuda_check(cudaMemsetAsync(R.v, 0, flat_n_ * 4, stream_), "memset");
@@ -466,7 +466,7 @@ void Model::set_tensor(const std::string& name, int which, const float* full, in
   float* scratch = nullptr;
   if (via_scratch) cuda_check(cudaMalloc(&scratch, s.numel * 4), "cudaMalloc");
   for (Rank& R : ranks_) {
-    float* dst = via_scratch ? scratch : (which == 0 ? R.p : which == 2 ? R.m : R.v) + s.offset;
+    float* dst = via_scratch ? scratch : which == 0 ? pval(R, s.offset) : (which == 2 ? R.m : R.v) + s.offset;
     if (s.layout.kind != Layout::kSplit) {
       cuda_check(cudaMemcpyAsync(dst, full, numel * 4, cudaMemcpyHostToDevice, stream_), "H2D");
     } else {
@@ -574,8 +574,8 @@ void Model::get_tensor(const std::string& name, int which, float* full, int64_t 
       cuda_check(cudaStreamSynchronize(stream_), "get_tensor");
       return scratch.p;
     }
-    float* base = which == 0 ? R.p : which == 1 ? R.g : which == 2 ? R.m : R.v;
-    return base + s.offset;
+    if (which == 0) return pval(R, s.offset);
+    return (which == 1 ? R.g : which == 2 ? R.m : R.v) + s.offset;
   };
   cuda_check(cudaStreamSynchronize(stream_), "sync");
   if (s.layout.kind != Layout::kSplit) {
@@ -1381,6 +1381,10 @@ void Model::adamw(double lr, double b1, double b2, double eps, double wd, bool c
   }
   ++step_;
   cuda_check(cudaGetLastError(), "adamw");
+}
+
+void Model::fail_no_fp32_weight() {
+  fail(SW_ERR_CONFIG, "inference-only model: GEMM weights are held in bf16 only");
 }
 
 void Model::check_trainable(const char* what) const {

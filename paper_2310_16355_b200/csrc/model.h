@@ -49,8 +49,10 @@ struct LayerSlots {
 
 struct Rank {
   int device = 0, dpi = 0, mpi = 0;
-  // inference-only model: g, m, v null; p valid at region-2 offsets only (>= weights_end_)
+  // inference-only model: p, g, m, v null; p_small holds the region-2 parameters (flat offsets
+  // >= weights_end_), the GEMM weights live in w only
   float *p = nullptr, *g = nullptr, *m = nullptr, *v = nullptr;
+  float* p_small = nullptr;
   bf16* w = nullptr;
   // activations saved for the backward, per layer
   std::vector<float*> hs, hmid, stats1, stats2;  // stats: mean[M] | rstd[M]
@@ -185,7 +187,14 @@ class Model {
     float lr, b1, b2, eps, wd, c1, c2;
   };
   const FusedAdam* fused_ = nullptr;
-  float* P(Rank& R, int slot) { return R.p + slots_[slot].offset; }
+  // fp32 parameter at a flat offset (an inference-only model keeps region 2 only)
+  float* pval(Rank& R, int64_t offset) {
+    if (R.p != nullptr) return R.p + offset;
+    if (offset < weights_end_) fail_no_fp32_weight();
+    return R.p_small + (offset - weights_end_);
+  }
+  [[noreturn]] static void fail_no_fp32_weight();
+  float* P(Rank& R, int slot) { return pval(R, slots_[slot].offset); }
   float* Pn(Rank& R, int slot) { return slot < 0 ? nullptr : P(R, slot); }  // absent slot -> null
   float* Gn(Rank& R, int slot) { return slot < 0 ? nullptr : G(R, slot); }
   float* G(Rank& R, int slot) { return R.g + slots_[slot].offset; }
