@@ -484,8 +484,7 @@ sw_status sw_t5_train_step(sw_t5* m, const sw_adamw_cfg* cfg) {
   return sw::guarded([&] {
     require(m, "model");
     require(cfg, "cfg");
-    m->model->forward_backward();
-    m->model->adamw(cfg->lr, cfg->beta1, cfg->beta2, cfg->eps, cfg->weight_decay);
+    m->model->train_step(cfg->lr, cfg->beta1, cfg->beta2, cfg->eps, cfg->weight_decay);
   });
 }
 

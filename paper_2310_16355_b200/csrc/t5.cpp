@@ -152,27 +152,31 @@ void T5Model::build_layout() {
                                  slots_[s].name + "' (supported: the reference rule layout)");
     }
   };
-  tok_ = place("embed/tok/kernel", true);
-  expect(tok_, Layout::kReplicated, 0, "the embedding");
-  auto stack = [&](const std::string& st, int layers, bool decoder, std::vector<T5Layer>& out) {
+  // Region 1: the GEMM weight matrices (their wgrad epilogue can apply AdamW in place, see
+  // train_step); region 2 from weights_end_: embedding, relative-position biases, norm scales.
+  auto stack = [&](const std::string& st, int layers, bool decoder, std::vector<T5Layer>& out, bool gemm_pass) {
     out.resize(layers);
     for (int l = 0; l < layers; ++l) {
       const std::string b = st + "/block_" + std::to_string(l) + "/";
       T5Layer& L = out[l];
-      L.ln1 = place(b + "ln1/scale", true);
+      if (!gemm_pass) {
+        L.ln1 = place(b + "ln1/scale", true);
+        if (l == 0) {
+          const int rb = place(b + "attn/rel_bias/kernel", true);
+          expect(rb, Layout::kReplicated, 0, "the relative-position bias");
+          (decoder ? rb_d_ : rb_e_) = rb;
+        }
+        if (decoder) L.lnx = place(b + "ln_x/scale", true);
+        L.ln2 = place(b + "ln2/scale", true);
+        continue;
+      }
       L.q = place(b + "attn/q/kernel", true);  // q|k|v adjacent: fused [3*inner/t, d]
       place(b + "attn/k/kernel", false);
       place(b + "attn/v/kernel", false);
       L.o = place(b + "attn/o/kernel", true);
       for (int s : {L.q, L.q + 1, L.q + 2}) expect(s, Layout::kSplit, 0, "attention q/k/v");
       expect(L.o, Layout::kSplit, 1, "attention o");
-      if (l == 0) {
-        const int rb = place(b + "attn/rel_bias/kernel", true);
-        expect(rb, Layout::kReplicated, 0, "the relative-position bias");
-        (decoder ? rb_d_ : rb_e_) = rb;
-      }
       if (decoder) {
-        L.lnx = place(b + "ln_x/scale", true);
         L.cq = place(b + "cross_attn/q/kernel", true);
         L.ck = place(b + "cross_attn/k/kernel", true);  // k|v adjacent: fused [2*inner/t, d]
         place(b + "cross_attn/v/kernel", false);
@@ -180,20 +184,25 @@ void T5Model::build_layout() {
         for (int s : {L.cq, L.ck, L.ck + 1}) expect(s, Layout::kSplit, 0, "cross-attention q/k/v");
         expect(L.co, Layout::kSplit, 1, "cross-attention o");
       }
-      L.ln2 = place(b + "ln2/scale", true);
       L.fc1 = place(b + "mlp/fc1/kernel", true);
       L.fc2 = place(b + "mlp/fc2/kernel", true);
       expect(L.fc1, Layout::kSplit, 0, "mlp fc1");
       expect(L.fc2, Layout::kSplit, 1, "mlp fc2");
     }
-    (decoder ? lnf_d_ : lnf_e_) = place(st + "/final_ln/scale", true);
+    if (!gemm_pass) (decoder ? lnf_d_ : lnf_e_) = place(st + "/final_ln/scale", true);
   };
-  stack("enc", Le_, false, enc_);
-  stack("dec", Ld_, true, dec_);
+  stack("enc", Le_, false, enc_, true);
+  stack("dec", Ld_, true, dec_, true);
   head_ = place("lm_head/kernel", true);
   if (slots_[head_].layout.kind != Layout::kReplicated) {
     fail(SW_ERR_PARTITION, "T5 executor: lm_head/kernel must be replicated (the reference plan)");
   }
+  weights_end_ = (off + kT5Align - 1) / kT5Align * kT5Align;
+  off = weights_end_;
+  tok_ = place("embed/tok/kernel", true);
+  expect(tok_, Layout::kReplicated, 0, "the embedding");
+  stack("enc", Le_, false, enc_, false);
+  stack("dec", Ld_, true, dec_, false);
   for (const Slot& s : slots_) {
     if (s.global.size() < 2 && s.layout.kind != Layout::kReplicated) {
       fail(SW_ERR_PARTITION, "T5 executor: 1-D parameter '" + s.name + "' must be replicated");
@@ -322,6 +331,7 @@ void T5Model::allocate() {
     R.tok_keys = alloc<uint32_t>(k::embed_bwd_keys(Mx));
     ranks_.push_back(R);
   }
+  d_flag_ = alloc<int>(1);
   cuda_check(cudaStreamSynchronize(stream_), "allocate");
 }
 
@@ -666,7 +676,7 @@ void T5Model::forward(bool need_grad) {
     tic();
     k::xent_fwd_bwd(R.logits, V_, Md, V_, R.targets, R.weights, R.wsum, R.wloss, need_grad ? 1 : 0, stream_);
     toc(kProfXent, (need_grad ? 4.0 : 2.0) * Md * V_);
-    k::loss_reduce(R.wloss, Md, R.wsum, R.loss, stream_);
+    k::loss_reduce(R.wloss, Md, R.wsum, R.loss, stream_, fused_ != nullptr ? d_flag_ : nullptr);
     launches_ += 3;
   }
 }
@@ -690,7 +700,7 @@ void T5Model::backward() {
     cuda_check(cudaMemsetAsync(R.d_eout, 0, sizeof(float) * Me * d, stream_), "memset");
     // d(final) = dlogits . W_head; dW_head = dlogits^T . f (replicated head: no collective)
     gemm(static_cast<int>(Md), d, V_, R.logits, V_, 0, W(R, head_), d, 1, F32, R.dx, d);
-    gemm(V_, d, static_cast<int>(Md), R.logits, V_, 1, R.f, d, 1, F32, G(R, head_), d);
+    wgrad(R, head_, V_, d, static_cast<int>(Md), R.logits, V_, R.f, d);
     rms_bwd(R.hs_d[Ld_], R.stf_d, lnf_d_, R, R.dx, R.gres_d, Md, 0);
   }
   auto attn_bwd = [&](T5Rank& R, int Tq, int Tk, const bf16* q, int64_t ldq, const bf16* kp, const bf16* vp,
@@ -735,38 +745,38 @@ void T5Model::backward() {
       gemm(static_cast<int>(Md), fl, d, R.gb, d, 0, W(R, L.fc2), fl, 1, BF, R.dact, fl);
       k::relu_bwd_bf16(R.dact, R.act_d[l], Md * fl, stream_);
       ++launches_;
-      gemm(d, fl, static_cast<int>(Md), R.gb, d, 1, R.act_d[l], fl, 1, F32, G(R, L.fc2), fl);
+      wgrad(R, L.fc2, d, fl, static_cast<int>(Md), R.gb, d, R.act_d[l], fl);
       gemm(static_cast<int>(Md), d, fl, R.dact, fl, 0, W(R, L.fc1), d, 1, F32, R.dx, d);
-      gemm(fl, d, static_cast<int>(Md), R.dact, fl, 1, R.a2_d[l], d, 1, F32, G(R, L.fc1), d);
+      wgrad(R, L.fc1, fl, d, static_cast<int>(Md), R.dact, fl, R.a2_d[l], d);
     }
     ar([](T5Rank& R) { return R.dx; }, Md * d);
     for (T5Rank& R : ranks_) rms_bwd(R.hx_d[l], R.st2_d[l], L.ln2, R, R.dx, R.gres_d, Md, 1);
     // cross attention
     for (T5Rank& R : ranks_) {
       gemm(static_cast<int>(Md), il, d, R.gb, d, 0, W(R, L.co), il, 1, BF, R.dout, il);
-      gemm(d, il, static_cast<int>(Md), R.gb, d, 1, R.co_d[l], il, 1, F32, G(R, L.co), il);
+      wgrad(R, L.co, d, il, static_cast<int>(Md), R.gb, d, R.co_d[l], il);
       // fused layout: dq | dk | dv land in one [M, 3*inner/t] buffer like the forward's
       bf16* dcq = fused_x_ ? R.dqkv : R.dcq;
       bf16* dckv = fused_x_ ? R.dqkv + il : R.dckv;
       attn_bwd(R, Td_, Te_, R.cq_d[l], ld_cq_, R.ckv_d[l], R.ckv_d[l] + il, ld_ckv_, R.co_d[l], R.clse_d[l], nullptr, 0,
                dcq, ld_cq_, dckv, dckv + il, ld_ckv_, nullptr);
       gemm(static_cast<int>(Md), d, il, dcq, ld_cq_, 0, W(R, L.cq), d, 1, F32, R.dx, d);
-      gemm(il, d, static_cast<int>(Md), dcq, ld_cq_, 1, R.ax_d[l], d, 1, F32, G(R, L.cq), d);
+      wgrad(R, L.cq, il, d, static_cast<int>(Md), dcq, ld_cq_, R.ax_d[l], d);
       // encoder-output gradient: partial over the mp group, summed over layers, reduced once
       gemm(static_cast<int>(Me), d, 2 * il, dckv, ld_ckv_, 0, W(R, L.ck), d, 1, F32, R.d_eout, d, nullptr, 0, 1);
-      gemm(2 * il, d, static_cast<int>(Me), dckv, ld_ckv_, 1, R.eo, d, 1, F32, G(R, L.ck), d);
+      wgrad(R, L.ck, 2 * il, d, static_cast<int>(Me), dckv, ld_ckv_, R.eo, d);
     }
     ar([](T5Rank& R) { return R.dx; }, Md * d);
     for (T5Rank& R : ranks_) rms_bwd(R.hm_d[l], R.stx_d[l], L.lnx, R, R.dx, R.gres_d, Md, 1);
     // self attention (causal, relative bias)
     for (T5Rank& R : ranks_) {
       gemm(static_cast<int>(Md), il, d, R.gb, d, 0, W(R, L.o), il, 1, BF, R.dout, il);
-      gemm(d, il, static_cast<int>(Md), R.gb, d, 1, R.o_d[l], il, 1, F32, G(R, L.o), il);
+      wgrad(R, L.o, d, il, static_cast<int>(Md), R.gb, d, R.o_d[l], il);
       attn_bwd(R, Td_, Td_, R.qkv_d[l], 3 * il, R.qkv_d[l] + il, R.qkv_d[l] + 2 * il, 3 * il, R.o_d[l], R.lse_d[l],
                tc_ ? R.lut_d : R.bias_d, 1, R.dqkv, 3 * il, R.dqkv + il, R.dqkv + 2 * il, 3 * il,
                tc_ ? R.dlut_d : R.dbias_d);
       gemm(static_cast<int>(Md), d, 3 * il, R.dqkv, 3 * il, 0, W(R, L.q), d, 1, F32, R.dx, d);
-      gemm(3 * il, d, static_cast<int>(Md), R.dqkv, 3 * il, 1, R.a1_d[l], d, 1, F32, G(R, L.q), d);
+      wgrad(R, L.q, 3 * il, d, static_cast<int>(Md), R.dqkv, 3 * il, R.a1_d[l], d);
     }
     ar([](T5Rank& R) { return R.dx; }, Md * d);
     for (T5Rank& R : ranks_) rms_bwd(R.hs_d[l], R.st1_d[l], L.ln1, R, R.dx, R.gres_d, Md, 1);
@@ -790,20 +800,20 @@ void T5Model::backward() {
       gemm(static_cast<int>(Me), fl, d, R.gb, d, 0, W(R, L.fc2), fl, 1, BF, R.dact, fl);
       k::relu_bwd_bf16(R.dact, R.act_e[l], Me * fl, stream_);
       ++launches_;
-      gemm(d, fl, static_cast<int>(Me), R.gb, d, 1, R.act_e[l], fl, 1, F32, G(R, L.fc2), fl);
+      wgrad(R, L.fc2, d, fl, static_cast<int>(Me), R.gb, d, R.act_e[l], fl);
       gemm(static_cast<int>(Me), d, fl, R.dact, fl, 0, W(R, L.fc1), d, 1, F32, R.dx, d);
-      gemm(fl, d, static_cast<int>(Me), R.dact, fl, 1, R.a2_e[l], d, 1, F32, G(R, L.fc1), d);
+      wgrad(R, L.fc1, fl, d, static_cast<int>(Me), R.dact, fl, R.a2_e[l], d);
     }
     ar([](T5Rank& R) { return R.dx; }, Me * d);
     for (T5Rank& R : ranks_) rms_bwd(R.hm_e[l], R.st2_e[l], L.ln2, R, R.dx, R.gres_e, Me, 1);
     for (T5Rank& R : ranks_) {
       gemm(static_cast<int>(Me), il, d, R.gb, d, 0, W(R, L.o), il, 1, BF, R.dout, il);
-      gemm(d, il, static_cast<int>(Me), R.gb, d, 1, R.o_e[l], il, 1, F32, G(R, L.o), il);
+      wgrad(R, L.o, d, il, static_cast<int>(Me), R.gb, d, R.o_e[l], il);
       attn_bwd(R, Te_, Te_, R.qkv_e[l], 3 * il, R.qkv_e[l] + il, R.qkv_e[l] + 2 * il, 3 * il, R.o_e[l], R.lse_e[l],
                tc_ ? R.lut_e : R.bias_e, 0, R.dqkv, 3 * il, R.dqkv + il, R.dqkv + 2 * il, 3 * il,
                tc_ ? R.dlut_e : R.dbias_e);
       gemm(static_cast<int>(Me), d, 3 * il, R.dqkv, 3 * il, 0, W(R, L.q), d, 1, F32, R.dx, d);
-      gemm(3 * il, d, static_cast<int>(Me), R.dqkv, 3 * il, 1, R.a1_e[l], d, 1, F32, G(R, L.q), d);
+      wgrad(R, L.q, 3 * il, d, static_cast<int>(Me), R.dqkv, 3 * il, R.a1_e[l], d);
     }
     ar([](T5Rank& R) { return R.dx; }, Me * d);
     for (T5Rank& R : ranks_) rms_bwd(R.hs_e[l], R.st1_e[l], L.ln1, R, R.dx, R.gres_e, Me, 1);
@@ -845,6 +855,95 @@ void T5Model::adamw(double lr, double b1, double b2, double eps, double wd) {
   }
   ++step_;
   cuda_check(cudaGetLastError(), "t5 adamw");
+}
+
+void T5Model::wgrad(T5Rank& R, int slot, int M, int N, int K, const void* A, int64_t lda, const void* B,
+                    int64_t ldb) {
+  if (fused_ == nullptr || slots_[slot].offset >= weights_end_) {
+    gemm(M, N, K, A, lda, 1, B, ldb, 1, static_cast<int>(Epi::kStoreF32), G(R, slot), N);
+    return;
+  }
+  // optimizer in the epilogue (as Model::wgrad): the gradient never leaves the accumulator
+  GemmParams p;
+  p.M = M;
+  p.N = N;
+  p.K = K;
+  p.A = A;
+  p.lda = lda;
+  p.a_mn_major = 1;
+  p.B = B;
+  p.ldb = ldb;
+  p.b_mn_major = 1;
+  p.epi = Epi::kAdamW;
+  p.ldc = N;
+  p.adam_p = P(R, slot);
+  p.adam_m = R.m + slots_[slot].offset;
+  p.adam_v = R.v + slots_[slot].offset;
+  p.adam_w = W(R, slot);
+  p.adam_flag = d_flag_;
+  p.adam_lr = fused_->lr;
+  p.adam_b1 = fused_->b1;
+  p.adam_b2 = fused_->b2;
+  p.adam_eps = fused_->eps;
+  p.adam_wd = fused_->wd;
+  p.adam_c1 = fused_->c1;
+  p.adam_c2 = fused_->c2;
+  tic();
+  cuda_check(gemm_bf16(p, stream_), "gemm launch");
+  toc(kProfGemm, 2.0 * M * N * static_cast<double>(K));
+  ++launches_;
+}
+
+bool T5Model::train_step(double lr, double b1, double b2, double eps, double wd) {
+  static const bool disabled = [] {
+    const char* e = std::getenv("SW_FUSED_ADAMW");
+    return e != nullptr && e[0] == '0';
+  }();
+  if (disabled) {
+    forward_backward();
+    adamw(lr, b1, b2, eps, wd);
+    return false;
+  }
+  // Optimizer in the backward: every GEMM weight is updated by its wgrad epilogue (each weight's
+  // dgrad, which reads the bf16 shadow, is issued before its wgrad), the region-2 parameters by
+  // one flat AdamW after the backward. A non-finite loss gates every fused update.
+  const double t = static_cast<double>(step_ + 1);
+  FusedAdam fa;
+  fa.lr = static_cast<float>(lr);
+  fa.b1 = static_cast<float>(b1);
+  fa.b2 = static_cast<float>(b2);
+  fa.eps = static_cast<float>(eps);
+  fa.wd = static_cast<float>(wd);
+  fa.c1 = static_cast<float>(1.0 - std::pow(b1, t));
+  fa.c2 = static_cast<float>(1.0 - std::pow(b2, t));
+  cuda_check(cudaMemsetAsync(d_flag_, 0, sizeof(int), stream_), "memset");
+  fused_ = &fa;
+  try {
+    forward_backward();
+  } catch (...) {
+    fused_ = nullptr;
+    throw;
+  }
+  fused_ = nullptr;
+  int flag = 0;
+  cuda_check(cudaMemcpyAsync(&flag, d_flag_, sizeof(int), cudaMemcpyDeviceToHost, stream_), "D2H");
+  cuda_check(cudaStreamSynchronize(stream_), "sync");
+  if (flag & 2) fail(SW_ERR_NONFINITE, "t5 train_step: non-finite loss; no parameter was updated");
+  if (flag) {
+    fail(SW_ERR_NONFINITE, "t5 train_step: non-finite gradient (optimizer fused into the backward: the GEMM "
+                           "weights updated before it was found keep their update)");
+  }
+  const int64_t n_small = flat_n_ - weights_end_;
+  for (T5Rank& R : ranks_) {
+    tic();
+    k::adamw(R.p + weights_end_, R.m + weights_end_, R.v + weights_end_, R.g + weights_end_, R.w + weights_end_,
+             n_small, fa.lr, fa.b1, fa.b2, fa.eps, fa.wd, fa.c1, fa.c2, stream_);
+    toc(kProfAdamw, 30.0 * n_small);
+    ++launches_;
+  }
+  ++step_;
+  cuda_check(cudaGetLastError(), "t5 train_step");
+  return true;
 }
 
 double T5Model::last_loss() {

@@ -77,6 +77,9 @@ class T5Model {
   void forward_backward();
   void forward_only();
   void adamw(double lr, double b1, double b2, double eps, double wd);
+  // forward_backward + adamw with the optimizer fused into the weight-gradient GEMMs (dp = 1,
+  // as Model::train_step; SW_FUSED_ADAMW=0: the two-pass step). Returns whether it was fused.
+  bool train_step(double lr, double b1, double b2, double eps, double wd);
   double last_loss();
   void logits_to_host(float* out);  // [batch * dec_len, vocab] of mp rank 0
   uint64_t step() const { return step_; }
@@ -96,6 +99,15 @@ class T5Model {
   void backward();
   void gemm(int M, int N, int K, const void* A, int64_t lda, int a_mn, const void* B, int64_t ldb, int b_mn,
             int epi, void* C, int64_t ldc, const void* aux = nullptr, int64_t ld_aux = 0, int accumulate = 0);
+  // weight gradient dW[M, N] = A^T B (MN-major operands) into G, or with fused_ set the AdamW
+  // update of the slot in the GEMM epilogue
+  void wgrad(T5Rank& R, int slot, int M, int N, int K, const void* A, int64_t lda, const void* B, int64_t ldb);
+  struct FusedAdam {
+    float lr, b1, b2, eps, wd, c1, c2;
+  };
+  const FusedAdam* fused_ = nullptr;
+  int* d_flag_ = nullptr;
+  int64_t weights_end_ = 0;  // [0, weights_end_): GEMM weight matrices
   // all-reduce (sum) over the mp group of n floats at ptr(R) of every local rank
   void ar(const std::function<float*(T5Rank&)>& ptr, int64_t n);
   // row-parallel product [M, K] x W[d, K]^T added to the residual `aux` into `out`

@@ -153,3 +153,31 @@ def test_t5_head_dim_128_attention_paths(tc, mp, T, Td, monkeypatch):
             continue
         r = rel_l2(got, want[n])
         assert r < (4e-2 if n.endswith(SCORE) else 3e-2), (n, r)
+
+
+@pytest.mark.parametrize("mp", [1, 2])
+def test_t5_fused_optimizer_matches_two_pass_step(mp):
+    """train_step applies AdamW inside the weight-gradient GEMM epilogues (GEMM weights) and one
+    flat AdamW over the rest; forward_backward + adamw_step is the two-pass step. Same init, same
+    batch: the parameter updates agree to the attention backward's dQ reduction noise."""
+    out = {}
+    for fused in (True, False):
+        model, _, spec = make(mp)
+        model.init_params(11, "model-init")
+        t5_init_scaling(model, spec)
+        p0 = {n: model.get_param(n) for n in model.shapes}
+        enc, dec, tgt, w = t5_ref.t5_batch(11, 0, B, TE, TD, spec.vocab_size)
+        model.stage_batch(enc, dec, tgt, w)
+        cfg = engine.AdamWConfig(lr=1e-3, weight_decay=0.01)
+        for _ in range(2):
+            if fused:
+                model.train_step(cfg)
+            else:
+                model.forward_backward()
+                model.adamw_step(cfg)
+        out[fused] = (model.loss(), {n: model.get_param(n) - p0[n] for n in model.shapes},
+                      {n: model.get_adam(n)[0] for n in model.shapes})
+    assert abs(out[True][0] - out[False][0]) <= 1e-4 * abs(out[False][0])
+    for n in out[True][1]:
+        assert rel_l2(out[True][1][n].astype(np.float64), out[False][1][n].astype(np.float64)) < 1e-2, n
+        assert rel_l2(out[True][2][n].astype(np.float64), out[False][2][n].astype(np.float64)) < 1e-3, n
