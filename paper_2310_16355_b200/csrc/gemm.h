@@ -77,6 +77,9 @@ struct GemmParams {
   // bias gradient of the GeLU layer; reduce with k::colsum_chunks). Requires gemm_colsum_ok.
   float* colsum = nullptr;
   int delta_T = 0;
+  // ReLU instead of GeLU (T5 MLP): kStoreBf16 stores relu(acc + bias); kGeluBwd multiplies by
+  // relu'(aux) = (aux > 0) with aux = the stored ReLU output
+  int relu = 0;
 };
 
 // Returns cudaSuccess or the launch error. Throws std::runtime_error on invalid shapes.

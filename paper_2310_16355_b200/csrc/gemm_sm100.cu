@@ -166,6 +166,11 @@ __device__ __forceinline__ void adamw_chunk(const GemmParams& p, float4* stage, 
 }
 
 // alpha * acc + bias for one 32-column chunk (the TMA-store epilogue's values)
+// derivative of the MLP activation at the stored bf16 value x (GeLU pre-activation, or ReLU output)
+__device__ __forceinline__ float act_grad(const GemmParams& p, float x) {
+  return p.relu ? (x > 0.f ? 1.f : 0.f) : dev::gelu_tanh_grad(x);
+}
+
 __device__ __forceinline__ void epilogue_values(const GemmParams& p, int col0, int ncols, const uint32_t (&r)[32],
                                                 float (&v)[32]) {
 #pragma unroll
@@ -242,10 +247,16 @@ __device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int row, int
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
             float2 x = dev::unpack_bf16x2(w[j]);
-            v[c + 2 * j] *= dev::gelu_tanh_grad(x.x);
-            v[c + 2 * j + 1] *= dev::gelu_tanh_grad(x.y);
+            v[c + 2 * j] *= act_grad(p, x.x);
+            v[c + 2 * j + 1] *= act_grad(p, x.y);
           }
         }
+      }
+    }
+    if constexpr (EPI == Epi::kStoreBf16) {
+      if (p.relu) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i], 0.f);
       }
     }
     __nv_bfloat16* out =
@@ -1034,6 +1045,12 @@ __global__ void __cluster_dims__(GEMM_CL, 1, 1) __launch_bounds__(p_threads<EPI>
             dev::tmem_ld_wait();
             float v[32];
             epilogue_values(p, nb * BN + j * 32, min(32, n_left - j * 32), r, v);
+            if constexpr (EPI == Epi::kStoreBf16) {
+              if (p.relu) {
+#pragma unroll
+                for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i], 0.f);
+              }
+            }
             __syncwarp();
             uint8_t* buf = stg + (j & 1) * EPI_TMA_BUF + lane * (f32 ? 128 : 64);
             if constexpr (resid) {
@@ -1057,8 +1074,8 @@ __global__ void __cluster_dims__(GEMM_CL, 1, 1) __launch_bounds__(p_threads<EPI>
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
                   const float2 x = dev::unpack_bf16x2(w[e]);
-                  o[e] = dev::pack_bf16x2(v[8 * u + 2 * e] * dev::gelu_tanh_grad(x.x),
-                                          v[8 * u + 2 * e + 1] * dev::gelu_tanh_grad(x.y));
+                  o[e] = dev::pack_bf16x2(v[8 * u + 2 * e] * act_grad(p, x.x),
+                                          v[8 * u + 2 * e + 1] * act_grad(p, x.y));
                 }
                 *pa = make_uint4(o[0], o[1], o[2], o[3]);
               }

@@ -189,8 +189,6 @@ void t5_lut_build(const float* table, const int32_t* bucket, int H, int h0, int 
 // table_grad[bucket[i], h0 + h] += dlut[h][i] for i < 2T - 1
 void t5_lut_grad(const float* dlut, const int32_t* bucket, int H, int h0, int Hl, int T, float* table_grad,
                  cudaStream_t s);
-void relu_bf16(bf16* x, int64_t n, cudaStream_t s);
-void relu_bwd_bf16(bf16* g, const bf16* act, int64_t n, cudaStream_t s);  // g *= (act > 0)
 
 // Emulated collective: every bufs[r][0..n) <- sum_{r ascending} bufs[r] (collectives.hpp:27-52).
 void sum_ranks_f32(float* const* bufs, int nranks, int64_t n, float scale, cudaStream_t s);

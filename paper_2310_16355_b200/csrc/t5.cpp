@@ -484,8 +484,9 @@ void T5Model::read_profile(double* ms, double* work, int64_t* count) {
 }
 
 void T5Model::gemm(int M, int N, int K, const void* A, int64_t lda, int a_mn, const void* B, int64_t ldb, int b_mn,
-                   int epi, void* C, int64_t ldc, const void* aux, int64_t ld_aux, int accumulate) {
+                   int epi, void* C, int64_t ldc, const void* aux, int64_t ld_aux, int accumulate, int relu) {
   GemmParams p;
+  p.relu = relu;
   p.M = M;
   p.N = N;
   p.K = K;
@@ -628,9 +629,7 @@ void T5Model::forward(bool need_grad) {
     for (T5Rank& R : ranks_) {
       rms_fwd(R.hm_e[l], L.ln2, R, R.a2_e[l], R.st2_e[l], Me);
       gemm(static_cast<int>(Me), fl, d, R.a2_e[l], d, 0, W(R, L.fc1), d, 0, static_cast<int>(Epi::kStoreBf16),
-           R.act_e[l], fl);
-      k::relu_bf16(R.act_e[l], Me * fl, stream_);
-      ++launches_;
+           R.act_e[l], fl, nullptr, 0, 0, /*relu=*/1);
     }
     row_parallel(Me, fl, [&](T5Rank& R) -> const bf16* { return R.act_e[l]; }, L.fc2,
                  [&](T5Rank& R) -> const float* { return R.hm_e[l]; }, [&](T5Rank& R) { return R.hs_e[l + 1]; });
@@ -662,9 +661,7 @@ void T5Model::forward(bool need_grad) {
     for (T5Rank& R : ranks_) {
       rms_fwd(R.hx_d[l], L.ln2, R, R.a2_d[l], R.st2_d[l], Md);
       gemm(static_cast<int>(Md), fl, d, R.a2_d[l], d, 0, W(R, L.fc1), d, 0, static_cast<int>(Epi::kStoreBf16),
-           R.act_d[l], fl);
-      k::relu_bf16(R.act_d[l], Md * fl, stream_);
-      ++launches_;
+           R.act_d[l], fl, nullptr, 0, 0, /*relu=*/1);
     }
     row_parallel(Md, fl, [&](T5Rank& R) -> const bf16* { return R.act_d[l]; }, L.fc2,
                  [&](T5Rank& R) -> const float* { return R.hx_d[l]; }, [&](T5Rank& R) { return R.hs_d[l + 1]; });
@@ -742,9 +739,8 @@ void T5Model::backward() {
     const T5Layer& L = dec_[l];
     // MLP
     for (T5Rank& R : ranks_) {
-      gemm(static_cast<int>(Md), fl, d, R.gb, d, 0, W(R, L.fc2), fl, 1, BF, R.dact, fl);
-      k::relu_bwd_bf16(R.dact, R.act_d[l], Md * fl, stream_);
-      ++launches_;
+      gemm(static_cast<int>(Md), fl, d, R.gb, d, 0, W(R, L.fc2), fl, 1, static_cast<int>(Epi::kGeluBwd), R.dact, fl,
+           R.act_d[l], fl, 0, /*relu=*/1);
       wgrad(R, L.fc2, d, fl, static_cast<int>(Md), R.gb, d, R.act_d[l], fl);
       gemm(static_cast<int>(Md), d, fl, R.dact, fl, 0, W(R, L.fc1), d, 1, F32, R.dx, d);
       wgrad(R, L.fc1, fl, d, static_cast<int>(Md), R.dact, fl, R.a2_d[l], d);
@@ -797,9 +793,9 @@ void T5Model::backward() {
   for (int l = Le_ - 1; l >= 0; --l) {
     const T5Layer& L = enc_[l];
     for (T5Rank& R : ranks_) {
-      gemm(static_cast<int>(Me), fl, d, R.gb, d, 0, W(R, L.fc2), fl, 1, BF, R.dact, fl);
-      k::relu_bwd_bf16(R.dact, R.act_e[l], Me * fl, stream_);
-      ++launches_;
+      // dact = (gb . W_fc2) * relu'(act), the ReLU derivative from the stored activation
+      gemm(static_cast<int>(Me), fl, d, R.gb, d, 0, W(R, L.fc2), fl, 1, static_cast<int>(Epi::kGeluBwd), R.dact, fl,
+           R.act_e[l], fl, 0, /*relu=*/1);
       wgrad(R, L.fc2, d, fl, static_cast<int>(Me), R.gb, d, R.act_e[l], fl);
       gemm(static_cast<int>(Me), d, fl, R.dact, fl, 0, W(R, L.fc1), d, 1, F32, R.dx, d);
       wgrad(R, L.fc1, fl, d, static_cast<int>(Me), R.dact, fl, R.a2_e[l], d);

@@ -97,8 +97,10 @@ class T5Model {
   void allocate();
   void forward(bool need_grad);
   void backward();
+  // relu: the MLP's ReLU in the epilogue (kStoreBf16 / kGeluBwd with GemmParams::relu)
   void gemm(int M, int N, int K, const void* A, int64_t lda, int a_mn, const void* B, int64_t ldb, int b_mn,
-            int epi, void* C, int64_t ldc, const void* aux = nullptr, int64_t ld_aux = 0, int accumulate = 0);
+            int epi, void* C, int64_t ldc, const void* aux = nullptr, int64_t ld_aux = 0, int accumulate = 0,
+            int relu = 0);
   // weight gradient dW[M, N] = A^T B (MN-major operands) into G, or with fused_ set the AdamW
   // update of the slot in the GEMM epilogue
   void wgrad(T5Rank& R, int slot, int M, int N, int K, const void* A, int64_t lda, const void* B, int64_t ldb);

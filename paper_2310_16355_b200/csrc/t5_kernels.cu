@@ -192,21 +192,6 @@ __global__ void t5_bias_grad_kernel(const float* __restrict__ dbias, const int32
   for (int t = threadIdx.x; t < nb; t += blockDim.x) atomicAdd(table_grad + static_cast<int64_t>(t) * H + h0 + h, acc[t]);
 }
 
-__global__ void relu_bf16_kernel(bf16* __restrict__ x, int64_t n) {
-  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n;
-       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const float v = __bfloat162float(x[e]);
-    x[e] = __float2bfloat16(v > 0.f ? v : 0.f);
-  }
-}
-
-__global__ void relu_bwd_bf16_kernel(bf16* __restrict__ g, const bf16* __restrict__ act, int64_t n) {
-  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n;
-       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    if (!(__bfloat162float(act[e]) > 0.f)) g[e] = __float2bfloat16(0.f);
-  }
-}
-
 __global__ void t5_lut_build_kernel(const float* __restrict__ table, const int32_t* __restrict__ bucket, int H,
                                     int h0, int Hl, int T, float* __restrict__ lut) {
   const int64_t W = 2LL * T + 128, n = static_cast<int64_t>(Hl) * W;
@@ -279,11 +264,6 @@ void t5_lut_grad(const float* dlut, const int32_t* bucket, int H, int h0, int Hl
   t5_lut_grad_kernel<<<grid, 256, 0, s>>>(dlut, bucket, H, h0, T, table_grad);
 }
 
-void relu_bf16(bf16* x, int64_t n, cudaStream_t s) { relu_bf16_kernel<<<blocks_for(n), 256, 0, s>>>(x, n); }
-
-void relu_bwd_bf16(bf16* g, const bf16* act, int64_t n, cudaStream_t s) {
-  relu_bwd_bf16_kernel<<<blocks_for(n), 256, 0, s>>>(g, act, n);
-}
 
 }  // namespace k
 }  // namespace sw
