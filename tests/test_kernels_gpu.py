@@ -215,11 +215,12 @@ def test_attention_lazy_rescale_path(hd):
 @pytest.mark.parametrize("hd", [64, 128, 256])
 @pytest.mark.parametrize("p", [0, 5, 17, 200, 1023])
 @pytest.mark.parametrize("split", [0, 1])
-def test_decode_attention_step(hd, p, split):
+def test_decode_attention_step(hd, p, split, Hl=4):
     """One KV-cached decode step against torch fp32 attention of the new query over keys 0..p,
-    where key / value p are the step's own (written into cache row p by the kernel)."""
+    where key / value p are the step's own (written into cache row p by the kernel). With 12
+    heads the split kernel uses ceil((p + 1) / 64) splits up to 16 (1, 4 and 16 here)."""
     L = _lib.lib()
-    B, T, Hl = 3, 1024, 4
+    B, T = 3, 1024
     Dl = Hl * hd
     g = torch.Generator(device=DEV).manual_seed(hd * 7 + p)
     cache = torch.randn(B * T, 3 * Dl, generator=g, device=DEV).bfloat16()
@@ -241,3 +242,10 @@ def test_decode_attention_step(hd, p, split):
         v = kv[..., 2 * Dl:].view(B, p + 1, Hl, hd).transpose(1, 2)
         ref = torch.softmax(q @ k.transpose(-1, -2) / math.sqrt(hd), -1) @ v
         assert rel(out, ref.view(B, Dl)) < 1e-2, (rep, rel(out, ref.view(B, Dl)))
+
+
+@pytest.mark.parametrize("p", [150, 1023])
+def test_decode_attention_split_budget(p):
+    """192 heads: the launch's CTA budget caps the split count at 3, so a split covers up to 342
+    keys (several 2-key unrolled passes per warp); same check as the one-step test."""
+    test_decode_attention_step(128, p, 1, Hl=64)
