@@ -1480,7 +1480,10 @@ __global__ void __launch_bounds__(256) gemv_mma_kernel(const GemmParams p) {
 #pragma unroll
     for (int j = 0; j < NB; ++j) acc[q][j][0] = acc[q][j][1] = acc[q][j][2] = acc[q][j][3] = 0.f;
   // 32-deep k steps per warp with their loads in flight together
-  constexpr int U = NB >= 4 ? 2 : kGlu ? 2 : 4;
+#ifndef SW_GEMV_U
+#define SW_GEMV_U 4
+#endif
+  constexpr int U = NB >= 4 ? 2 : kGlu ? (SW_GEMV_U >= 4 ? SW_GEMV_U / 2 : 2) : SW_GEMV_U;
   for (int k = warp * 32; k < K; k += 256 * U) {
     uint4 wl[U][NT], wh[U][NT], av[U][NB];
 #pragma unroll
