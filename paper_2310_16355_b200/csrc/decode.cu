@@ -5,6 +5,7 @@
 #include <cfloat>
 #include <cstdlib>
 #include <stdexcept>
+#include <string>
 
 #include "kernels.h"
 #include "sm100.cuh"
@@ -161,7 +162,10 @@ constexpr int DSPLIT = SW_DSPLIT;  // most splits (partial buffer rows per head)
 constexpr int DUNR = SW_DUNR;
 
 
-template <int HD>
+// CL: the splits of a head form one thread-block cluster (grid.y = cluster size <= 8) and their
+// partials meet in distributed shared memory: split 0 merges them after a cluster barrier, so
+// there is no global partial round trip, fence or ticket (SW_DECODE_CLUSTER=0: the global path).
+template <int HD, bool CL>
 __global__ void __launch_bounds__(256) decode_attention_split_kernel(const bf16* __restrict__ qnew,
                                                                      bf16* __restrict__ cache,
                                                                      bf16* __restrict__ out, int T, int p,
@@ -176,6 +180,7 @@ __global__ void __launch_bounds__(256) decode_attention_split_kernel(const bf16*
   __shared__ float sm_m[NG], sm_l[NG];
   __shared__ float sm_o[NG][HD];
   __shared__ bool last;
+  __shared__ float sm_part[HD + 2];  // CL: this split's (M, L, unnormalised O)
   const int bh = blockIdx.x, b = bh / Hl, h = bh % Hl, sp = blockIdx.y;
   const int dl = Hl * HD;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -183,9 +188,9 @@ __global__ void __launch_bounds__(256) decode_attention_split_kernel(const bf16*
   const int gid = warp * KPW + grp;
   const int nk = p + 1;
   const int nsplit = max(1, min(max_split, (nk + kps - 1) / kps));
-  if (sp >= nsplit) return;
+  if (!CL && sp >= nsplit) return;  // a cluster's idle splits still meet its barriers (empty range)
   const int chunk = (nk + nsplit - 1) / nsplit;
-  const int k0 = sp * chunk, k1 = min(nk, k0 + chunk);
+  const int k0 = sp < nsplit ? sp * chunk : nk, k1 = sp < nsplit ? min(nk, k0 + chunk) : nk;
   const bf16* qrow = qnew + static_cast<int64_t>(b) * 3 * dl;
   float q[8];
   {
@@ -251,7 +256,7 @@ __global__ void __launch_bounds__(256) decode_attention_split_kernel(const bf16*
 #pragma unroll
   for (int i = 0; i < 8; ++i) sm_o[gid][gl * 8 + i] = o[i];
   __syncthreads();
-  float* mine = part + (static_cast<int64_t>(bh) * DSPLIT + sp) * (HD + 2);
+  float* mine = CL ? sm_part : part + (static_cast<int64_t>(bh) * DSPLIT + sp) * (HD + 2);
   if (threadIdx.x < HD) {  // this split's partial: (M, L, unnormalised O) over its groups
     const int c = threadIdx.x;
     float M = -INFINITY;
@@ -270,6 +275,30 @@ __global__ void __launch_bounds__(256) decode_attention_split_kernel(const bf16*
       mine[0] = M;
       mine[1] = L;
     }
+  }
+  if constexpr (CL) {
+    dev::cluster_sync();  // every split's partial is in its shared memory
+    if (sp == 0 && threadIdx.x < HD) {
+      const int c = threadIdx.x;
+      const uint32_t base = dev::smem_u32(sm_part);
+      float Ms[8];
+#pragma unroll
+      for (int r = 0; r < 8; ++r) Ms[r] = r < nsplit ? dev::ld_shared_cluster_f32(dev::mapa_shared(base, r)) : -INFINITY;
+      float M = -INFINITY;
+#pragma unroll
+      for (int r = 0; r < 8; ++r) M = fmaxf(M, Ms[r]);
+      float L = 0.f, acc = 0.f;
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        if (r >= nsplit || Ms[r] == -INFINITY) continue;
+        const float f = dev::ex2_approx(Ms[r] - M);
+        L += dev::ld_shared_cluster_f32(dev::mapa_shared(base + 4, r)) * f;
+        acc += dev::ld_shared_cluster_f32(dev::mapa_shared(base + 4 * (2 + c), r)) * f;
+      }
+      out[static_cast<int64_t>(b) * dl + h * HD + c] = __float2bfloat16(acc / L);
+    }
+    dev::cluster_sync();  // the partials have been read
+    return;
   }
   __threadfence();
   __syncthreads();
@@ -488,24 +517,56 @@ __global__ void bump_kernel(int* x) { *x += 1; }
 
 void bump_i32(int* x, cudaStream_t s) { bump_kernel<<<1, 1, 0, s>>>(x); }
 
+bool decode_cluster_on() {
+  static const bool on = [] {
+    const char* e = std::getenv("SW_DECODE_CLUSTER");
+    return !(e != nullptr && e[0] == '0');
+  }();
+  return on;
+}
+
+template <int HD>
+void launch_decode_split(const bf16* qkv_new, bf16* cache, bf16* out, int B, int T, int p, int Hl, float scale_log2,
+                         cudaStream_t s, const int* p_dev, float* part, unsigned int* ticket) {
+  const int kps = decode_kps();
+  if (decode_cluster_on()) {
+    // splits per head: keys / kps, at most the CTA budget over the B * Hl heads and the portable
+    // cluster size
+    const int max_split = std::max(1, std::min(8, decode_ctas() / (B * Hl)));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>(B * Hl), static_cast<unsigned>(max_split));
+    cfg.blockDim = dim3(256);
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 1;
+    at[0].val.clusterDim.y = static_cast<unsigned>(max_split);
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, decode_attention_split_kernel<HD, true>, qkv_new, cache, out, T,
+                                             p, p_dev, Hl, scale_log2, part, ticket, kps, max_split);
+    if (e != cudaSuccess) throw std::runtime_error(std::string("decode attention launch: ") + cudaGetErrorString(e));
+    return;
+  }
+  const int max_split = std::max(1, std::min(DSPLIT, decode_ctas() / (B * Hl)));
+  const dim3 grid(B * Hl, max_split);
+  decode_attention_split_kernel<HD, false><<<grid, 256, 0, s>>>(qkv_new, cache, out, T, p, p_dev, Hl, scale_log2,
+                                                                part, ticket, kps, max_split);
+}
+
 bool decode_attention_split(const bf16* qkv_new, bf16* cache, bf16* out, int B, int T, int p, int Hl, int hd,
                             cudaStream_t s, const int* p_dev, float* part, unsigned int* ticket) {
   const float scale_log2 = static_cast<float>(1.4426950408889634 / sqrt(static_cast<double>(hd)));
-  // splits per head: keys / kps, at most the CTA budget spread over the B * Hl heads
-  const int max_split = std::max(1, std::min(DSPLIT, decode_ctas() / (B * Hl)));
-  const dim3 grid(B * Hl, max_split);
   switch (hd) {
     case 64:
-      decode_attention_split_kernel<64><<<grid, 256, 0, s>>>(qkv_new, cache, out, T, p, p_dev, Hl, scale_log2, part, ticket,
-                                                                decode_kps(), max_split);
+      launch_decode_split<64>(qkv_new, cache, out, B, T, p, Hl, scale_log2, s, p_dev, part, ticket);
       return true;
     case 128:
-      decode_attention_split_kernel<128><<<grid, 256, 0, s>>>(qkv_new, cache, out, T, p, p_dev, Hl, scale_log2, part, ticket,
-                                                                decode_kps(), max_split);
+      launch_decode_split<128>(qkv_new, cache, out, B, T, p, Hl, scale_log2, s, p_dev, part, ticket);
       return true;
     case 256:
-      decode_attention_split_kernel<256><<<grid, 256, 0, s>>>(qkv_new, cache, out, T, p, p_dev, Hl, scale_log2, part, ticket,
-                                                                decode_kps(), max_split);
+      launch_decode_split<256>(qkv_new, cache, out, B, T, p, Hl, scale_log2, s, p_dev, part, ticket);
       return true;
     default:
       return false;
