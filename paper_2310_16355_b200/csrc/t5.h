@@ -8,9 +8,12 @@
 // shadow); q|k|v of a self-attention block are adjacent (one fused QKV GEMM) and k|v of a
 // cross-attention block are adjacent (one fused KV GEMM over the encoder output).
 //
-// Scope of this round: dp = 1 (tensor parallel over the mesh's mp axis, emulated or NCCL),
-// replicated lm_head, flat AdamW after the backward. Attention runs on the CUDA-core kernels of
-// t5_kernels.cu (bias, cross and non-causal forms); the GEMMs are the tcgen05 family.
+// Scope: dp = 1 (tensor parallel over the mesh's mp axis, emulated or NCCL), replicated lm_head.
+// The GEMMs are the tcgen05 family (the MLP's ReLU and its derivative in their epilogues);
+// train_step applies AdamW inside the weight-gradient GEMM epilogues (GEMM weights, region 1 of
+// the flat layout) and one flat AdamW over the rest. Attention: the tcgen05 kernels of
+// attention_mma.cu for d_kv = 128 (relative bias as a per-head LUT, cross-attention over the
+// encoder K/V), the CUDA-core kernels of t5_kernels.cu otherwise.
 #pragma once
 
 #include <cuda_runtime.h>
