@@ -339,6 +339,7 @@ void T5Model::allocate() {
 // parameters (the same materialiser rules as Model: contiguous even chunks, sharded_tensor.hpp)
 // ---------------------------------------------------------------------------------------------
 void T5Model::init_params(uint64_t seed, const std::string& stream_name) {
+  poisoned_ = false;
   const uint64_t key = t5_mix64(seed ^ t5_mix64(t5_fnv1a(stream_name)));
   for (T5Rank& R : ranks_) {
     for (const Slot& s : slots_) {
@@ -827,6 +828,7 @@ void T5Model::backward() {
 }
 
 void T5Model::forward_backward() {
+  check_not_poisoned("t5 forward_backward");
   launches_ = 0;
   forward(true);
   backward();
@@ -839,6 +841,7 @@ void T5Model::forward_only() {
 }
 
 void T5Model::adamw(double lr, double b1, double b2, double eps, double wd) {
+  check_not_poisoned("t5 adamw_step");
   const double t = static_cast<double>(step_ + 1);
   const float c1 = static_cast<float>(1.0 - std::pow(b1, t));
   const float c2 = static_cast<float>(1.0 - std::pow(b2, t));
@@ -890,7 +893,15 @@ void T5Model::wgrad(T5Rank& R, int slot, int M, int N, int K, const void* A, int
   ++launches_;
 }
 
+void T5Model::check_not_poisoned(const char* what) const {
+  if (poisoned_) {
+    fail(SW_ERR_NONFINITE, std::string(what) + ": a fused step found a non-finite gradient after updating some "
+                                               "weights; re-initialise the model (init_params)");
+  }
+}
+
 bool T5Model::train_step(double lr, double b1, double b2, double eps, double wd) {
+  check_not_poisoned("t5 train_step");
   static const bool disabled = [] {
     const char* e = std::getenv("SW_FUSED_ADAMW");
     return e != nullptr && e[0] == '0';
@@ -926,8 +937,10 @@ bool T5Model::train_step(double lr, double b1, double b2, double eps, double wd)
   cuda_check(cudaStreamSynchronize(stream_), "sync");
   if (flag & 2) fail(SW_ERR_NONFINITE, "t5 train_step: non-finite loss; no parameter was updated");
   if (flag) {
+    poisoned_ = true;
     fail(SW_ERR_NONFINITE, "t5 train_step: non-finite gradient (optimizer fused into the backward: the GEMM "
-                           "weights updated before it was found keep their update)");
+                           "weights updated before it was found keep their update; the model refuses further "
+                           "steps until init_params)");
   }
   const int64_t n_small = flat_n_ - weights_end_;
   for (T5Rank& R : ranks_) {

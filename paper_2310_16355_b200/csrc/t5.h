@@ -113,6 +113,8 @@ class T5Model {
   const FusedAdam* fused_ = nullptr;
   int* d_flag_ = nullptr;
   int64_t weights_end_ = 0;  // [0, weights_end_): GEMM weight matrices
+  bool poisoned_ = false;  // a fused step updated some weights before finding a non-finite gradient
+  void check_not_poisoned(const char* what) const;
   // all-reduce (sum) over the mp group of n floats at ptr(R) of every local rank
   void ar(const std::function<float*(T5Rank&)>& ptr, int64_t n);
   // row-parallel product [M, K] x W[d, K]^T added to the residual `aux` into `out`

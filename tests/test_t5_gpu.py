@@ -191,3 +191,25 @@ def test_t5_fused_optimizer_matches_two_pass_step(mp):
         assert diff.max() <= 2 * lr * steps + 1e-6, n
         # the attention-score kernels carry the noisiest gradients (~1% of their elements flip)
         assert (diff > 1e-4).sum() <= max(2, 0.05 * diff.size), (n, int((diff > 1e-4).sum()))
+
+
+def test_t5_fused_step_nonfinite_loss_leaves_state_unchanged():
+    """A non-finite loss gates every fused AdamW epilogue: train_step raises NonFiniteError and
+    every parameter and moment is exactly as before the step (the model stays usable)."""
+    model, _, spec = make(1)
+    model.init_params(5, "model-init")
+    enc, dec, tgt, w = t5_ref.t5_batch(5, 0, B, TE, TD, spec.vocab_size)
+    tok = model.get_param("embed/tok/kernel")
+    bad = tok.copy()
+    bad[int(dec[0, 0])] = np.inf  # a decoder input row: the logits, hence the loss, go non-finite
+    model.set_param("embed/tok/kernel", bad)
+    model.stage_batch(enc, dec, tgt, w)
+    before = {n: (model.get_param(n), *model.get_adam(n)) for n in model.shapes}
+    with pytest.raises(engine._lib.NonFiniteError, match="non-finite loss"):
+        model.train_step(engine.AdamWConfig(lr=1e-3))
+    for n, (p, m, v) in before.items():
+        p2, m2, v2 = model.get_param(n), *model.get_adam(n)
+        assert np.array_equal(p, p2, equal_nan=True) and np.array_equal(m, m2) and np.array_equal(v, v2), n
+    model.set_param("embed/tok/kernel", tok)
+    model.train_step(engine.AdamWConfig(lr=1e-3))
+    assert np.isfinite(model.loss())
