@@ -115,6 +115,11 @@ Model::~Model() {
   for (cudaEvent_t e : ev_prod_) cudaEventDestroy(e);
   for (cudaEvent_t e : ev_ar_) cudaEventDestroy(e);
   if (comm_stream_) cudaStreamDestroy(comm_stream_);
+  if (dp_stream_) {
+    cudaStreamSynchronize(dp_stream_);
+    cudaStreamDestroy(dp_stream_);
+  }
+  for (cudaEvent_t e : dp_ev_) cudaEventDestroy(e);
   if (dec_graph_) cudaGraphExecDestroy(dec_graph_);
   if (dec_out_) cudaFree(dec_out_);
   for (void* p : allocations_) cudaFree(p);
@@ -209,6 +214,7 @@ void Model::build_layout() {
     }
     ls.fc2_k = place(b + "mlp/fc2/kernel", true);
   }
+  layers_end_ = off;
   if (!spec_.tie_embeddings) head_ = place("lm_head/kernel", true);
   weights_end_ = (off + kAlign - 1) / kAlign * kAlign;
   tok_ = place("embed/tok/kernel", true);
@@ -1267,6 +1273,7 @@ void Model::backward_replica(std::vector<Rank*>& grp, bool accumulate) {
       for (Rank* R : grp) wgrad(*R, ls.q_k, 3 * dl, d, static_cast<int>(M), R->dqkv, 3 * dl, R->a1[l], d, acc);
     });
     ev_last = ev_qkv;
+    if (dp_overlap_) dp_bucket(grp, l, ev_qkv);
   }
   main_wait(ev_last);  // every wgrad (and its fused AdamW) done before anything downstream
   for (Rank* R : grp) {
@@ -1320,24 +1327,62 @@ void Model::scale_grads(double factor) {
   }
 }
 
-void Model::dp_sync() {
-  check_trainable("dp_sync_grads");
-  if (mesh_->dp == 1) return;
+void Model::dp_reduce_range(int64_t off, int64_t n, cudaStream_t s) {
   const float inv = 1.0f / static_cast<float>(mesh_->dp);
   for (int j = 0; j < mesh_->mp; ++j) {
     if (mesh_->emulated) {
       std::vector<float*> ptrs;
-      for (int id : mesh_->dp_group(j)) ptrs.push_back(ranks_[id].g);
-      k::sum_ranks_f32(ptrs.data(), static_cast<int>(ptrs.size()), flat_n_, inv, stream_);
+      for (int id : mesh_->dp_group(j)) ptrs.push_back(ranks_[id].g + off);
+      k::sum_ranks_f32(ptrs.data(), static_cast<int>(ptrs.size()), n, inv, s);
       ++launches_;
     } else if (ranks_[0].mpi == j) {
-      nccl_check(ncclAllReduce(ranks_[0].g, ranks_[0].g, flat_n_, ncclFloat, ncclSum, mesh_->dp_comm, stream_),
+      nccl_check(ncclAllReduce(ranks_[0].g + off, ranks_[0].g + off, n, ncclFloat, ncclSum, mesh_->dp_comm, s),
                  "AllReduce(dp)");
-      k::scale_f32(ranks_[0].g, flat_n_, inv, stream_);
+      k::scale_f32(ranks_[0].g + off, n, inv, s);
       ++launches_;
     }
-    mesh_->record(CollKind::kAllReduce, mesh_->dp_group(j), static_cast<uint64_t>(flat_n_) * 4);
   }
+}
+
+void Model::dp_bucket(std::vector<Rank*>& grp, int l, cudaEvent_t ready) {
+  // emulated mesh: the replicas run one after another, so a layer's gradients are final once
+  // the last replica's backward has produced them
+  if (mesh_->emulated && grp[0]->dpi != mesh_->dp - 1) return;
+  if (dp_stream_ == nullptr) {
+    cuda_check(cudaStreamCreateWithFlags(&dp_stream_, cudaStreamNonBlocking), "cudaStreamCreate");
+  }
+  while (static_cast<int>(dp_ev_.size()) < L_ + 1) {
+    cudaEvent_t e;
+    cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+    dp_ev_.push_back(e);
+  }
+  if (ready == nullptr) {  // the wgrads ran on stream_
+    ready = dp_ev_[static_cast<size_t>(l)];
+    cuda_check(cudaEventRecord(ready, stream_), "cudaEventRecord");
+  }
+  cuda_check(cudaStreamWaitEvent(dp_stream_, ready, 0), "cudaStreamWaitEvent");
+  const LayerSlots& ls = layers_[l];
+  const int64_t off = slots_[ls.q_k].offset;
+  const int64_t end = slots_[ls.fc2_k].offset + slots_[ls.fc2_k].numel;
+  dp_reduce_range(off, end - off, dp_stream_);
+  dp_buckets_issued_ = true;
+}
+
+void Model::dp_sync() {
+  check_trainable("dp_sync_grads");
+  if (mesh_->dp == 1) return;
+  if (dp_buckets_issued_) {
+    // the layers' GEMM-weight gradients were reduced during the backward: join, then the rest
+    cudaEvent_t e = dp_ev_[static_cast<size_t>(L_)];
+    cuda_check(cudaEventRecord(e, dp_stream_), "cudaEventRecord");
+    cuda_check(cudaStreamWaitEvent(stream_, e, 0), "cudaStreamWaitEvent");
+    dp_reduce_range(layers_end_, flat_n_ - layers_end_, stream_);
+    dp_buckets_issued_ = false;
+  } else {
+    dp_reduce_range(0, flat_n_, stream_);
+  }
+  for (int j = 0; j < mesh_->mp; ++j)
+    mesh_->record(CollKind::kAllReduce, mesh_->dp_group(j), static_cast<uint64_t>(flat_n_) * 4);
 }
 
 void Model::adamw(double lr, double b1, double b2, double eps, double wd, bool check_finite) {
@@ -1406,7 +1451,18 @@ bool Model::train_step(double lr, double b1, double b2, double eps, double wd) {
     return e != nullptr && e[0] == '0';
   }();
   if (disabled || mesh_->dp != 1) {
-    forward_backward(false);
+    static const bool overlap = [] {
+      const char* e = std::getenv("SW_DP_OVERLAP");
+      return !(e != nullptr && e[0] == '0');
+    }();
+    dp_overlap_ = overlap && mesh_->dp > 1;
+    try {
+      forward_backward(false);
+    } catch (...) {
+      dp_overlap_ = false;
+      throw;
+    }
+    dp_overlap_ = false;
     dp_sync();
     adamw(lr, b1, b2, eps, wd, true);
     return false;

@@ -226,6 +226,16 @@ class Model {
   size_t side_next_ = 0;
   cudaEvent_t on_side(const std::function<void()>& f);
   void main_wait(cudaEvent_t e);
+  // dp gradient all-reduce overlapped with the backward (train_step with dp > 1): layer l's
+  // GEMM-weight gradients (a contiguous range of region 1) are all-reduced on dp_stream_ as soon
+  // as its last weight-gradient GEMM is done; dp_sync then reduces only the rest
+  bool dp_overlap_ = false;
+  bool dp_buckets_issued_ = false;
+  cudaStream_t dp_stream_ = nullptr;
+  std::vector<cudaEvent_t> dp_ev_;
+  int64_t layers_end_ = 0;  // end of the last layer's GEMM weights in the flat layout
+  void dp_reduce_range(int64_t off, int64_t n, cudaStream_t s);
+  void dp_bucket(std::vector<Rank*>& grp, int l, cudaEvent_t ready);
   std::vector<cudaEvent_t> ev_prod_, ev_ar_;
   int ar_chunks_ = 1;
   // Row-parallel all-reduce payloads in bf16 (opt-in, SW_AR_BF16=1): half the NVLink bytes of

@@ -489,3 +489,34 @@ def test_side_stream_wgrads_match_single_stream(mp, monkeypatch):
         assert (d > 1e-6 + 1e-5 * np.abs(b)).mean() <= 1e-2 or n.endswith("attn/k/bias"), n
         assert d.max() <= 2 * cfg.lr * (1 + 1e-3) + 1e-6, (n, float(d.max()))
     assert abs(res["0"][2] - res["1"][2]) <= 1e-6 * abs(res["0"][2])
+
+
+@pytest.mark.parametrize("spec_name,mp", [("mini.spec", 2), ("mini_swiglu.spec", 1)])
+def test_dp_allreduce_overlapped_with_backward(spec_name, mp):
+    """train_step with dp = 2 all-reduces each layer's GEMM-weight gradients on a side stream as
+    soon as the layer's weight-gradient GEMMs are done (emulated mesh: after the last replica's),
+    then the rest in dp_sync; forward_backward + dp_sync + adamw_step reduces the whole flat
+    buffer after the backward. Same update, up to the atomics-order noise every backward has."""
+    spec = spec_of(spec_name)
+    seq = 16
+    cfg = engine.AdamWConfig(lr=1e-2, weight_decay=0.01)
+    out = {}
+    for overlapped in (True, False):
+        model, _, _ = make(spec, 2, mp, 2, seq)
+        model.init_params(42, "model-init")
+        for step in range(3):
+            tokens, targets, weights = rng_ref.audit_batch(42, step, 4, seq, spec.vocab_size)
+            model.stage_batch(tokens, targets, weights)
+            if overlapped:
+                model.train_step(cfg)
+            else:
+                model.forward_backward()
+                model.dp_sync()
+                model.adamw_step(cfg)
+        out[overlapped] = (model.loss(), {n: model.get_param(n) for n in model.shapes})
+    assert abs(out[True][0] - out[False][0]) <= 1e-4 * abs(out[False][0])
+    for n in out[True][1]:
+        d = np.abs(out[True][1][n] - out[False][1][n])
+        off = d > 1e-6 + 1e-5 * np.abs(out[False][1][n])
+        assert off.sum() <= max(2, 2e-3 * off.size) or n.endswith("attn/k/bias"), (n, int(off.sum()))
+        assert d.max() <= 3 * 2 * cfg.lr + 1e-6, n
