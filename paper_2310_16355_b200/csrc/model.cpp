@@ -1298,6 +1298,12 @@ void Model::forward_backward(bool accumulate) {
   check_not_poisoned("forward_backward");
   cuda_check(cudaSetDevice(mesh_->cuda_device), "cudaSetDevice");
   launches_ = 0;
+  if (dp_buckets_issued_) {  // a previous overlapped backward that never reached dp_sync
+    cudaEvent_t e = dp_ev_[static_cast<size_t>(L_)];
+    cuda_check(cudaEventRecord(e, dp_stream_), "cudaEventRecord");
+    cuda_check(cudaStreamWaitEvent(stream_, e, 0), "cudaStreamWaitEvent");
+    dp_buckets_issued_ = false;
+  }
   const int first = mesh_->emulated ? 0 : ranks_[0].dpi;
   const int last = mesh_->emulated ? mesh_->dp - 1 : ranks_[0].dpi;
   for (int r = first; r <= last; ++r) {
