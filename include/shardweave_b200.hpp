@@ -250,8 +250,12 @@ struct AdamWConfig {  // train_state.hpp:172-178
 // transformer_loss program on the mesh + its sharded TrainState in HBM.
 class Model {
  public:
-  Model(const ModelSpec& spec, const ShardingPlan& plan, Mesh& mesh, int batch, int seq_len) {
-    check(sw_model_create(spec.get(), plan.get(), mesh.get(), batch, seq_len, &h_));
+  /// inference = true: the Predictor-only model (sw_model_create_inference): bf16 weight shards
+  /// and the K/V cache, no gradients or optimizer state.
+  Model(const ModelSpec& spec, const ShardingPlan& plan, Mesh& mesh, int batch, int seq_len, bool inference = false) {
+    check(inference ? sw_model_create_inference(spec.get(), plan.get(), mesh.get(), batch, seq_len, &h_)
+                    : sw_model_create(spec.get(), plan.get(), mesh.get(), batch, seq_len, &h_));
+    batch_ = batch;
   }
   ~Model() { sw_model_free(h_); }
   Model(const Model&) = delete;
@@ -312,6 +316,15 @@ class Model {
     }
     return out;
   }
+  /// The Predictor's greedy next-token loop (cli.cpp:425-447): prompts [batch * P] -> [batch * n_new].
+  std::vector<int32_t> generate(const std::vector<int32_t>& prompts, int P, int n_new) {
+    if (P < 1 || n_new < 1 || prompts.size() != static_cast<size_t>(batch_) * static_cast<size_t>(P)) {
+      throw std::invalid_argument("generate: prompts must hold batch * P tokens, P and n_new positive");
+    }
+    std::vector<int32_t> out(static_cast<size_t>(batch_) * static_cast<size_t>(n_new));
+    check(sw_model_generate(h_, prompts.data(), P, n_new, out.data()));
+    return out;
+  }
   uint64_t step() {
     uint64_t st = 0, sd = 0;
     check(sw_model_state_info(h_, &st, &sd));
@@ -325,6 +338,7 @@ class Model {
     return out;
   }
   sw_model* h_ = nullptr;
+  int batch_ = 0;
 };
 
 }  // namespace b200
