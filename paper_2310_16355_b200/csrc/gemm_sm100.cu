@@ -1310,9 +1310,6 @@ constexpr int GEMV_MAX_M = 8;
 #endif
 constexpr int GEMV_COLS = SW_GEMV_COLS;  // output columns per CTA (enough CTAs to cover the SMs at N = d_model)
 
-#ifndef SW_GEMV_L2PF
-#define SW_GEMV_L2PF 0
-#endif
 // KSPLIT warp octets split K (more loads in flight per CTA: the narrow N = d_model GEMVs have
 // fewer CTAs than the HBM latency needs); UNROLL k-steps of weight loads in flight per warp.
 template <Epi EPI, int GEMV_KSPLIT, int GEMV_UNROLL, int MX>
@@ -1335,17 +1332,6 @@ __global__ void __launch_bounds__(256 * GEMV_KSPLIT) gemv_bf16_kernel(const Gemm
     ok[j] = col < p.N;
     const int wrow = kGlu ? (rr < GEMV_COLS ? col : p.swiglu_half + col) : col;
     w[j] = reinterpret_cast<const __nv_bfloat16*>(p.B) + static_cast<int64_t>(ok[j] ? wrow : 0) * p.ldb;
-  }
-  // SW_GEMV_L2PF=1: every weight row of this CTA is requested from HBM at once (bulk L2
-  // prefetch, one row per lane of warp 0). Off: +15% in tools/gemv_bench.py, where the same
-  // weights come back every launch, but a 13% slower LLaMA-7B decode step (tools/decode_bench.py)
-  if (SW_GEMV_L2PF && ks == 0 && warp == 0 && lane < ROWS) {
-    const int col = c0 + (lane % GEMV_COLS);
-    if (col < p.N) {
-      const int wrow = kGlu ? (lane < GEMV_COLS ? col : p.swiglu_half + col) : col;
-      dev::bulk_prefetch_l2(reinterpret_cast<const __nv_bfloat16*>(p.B) + static_cast<int64_t>(wrow) * p.ldb,
-                            static_cast<uint32_t>(K) * 2u);
-    }
   }
   float acc[RPW][MX];  // MX = the activation rows this instance handles (registers)
 #pragma unroll
@@ -1848,154 +1834,6 @@ cudaError_t launch_gemv_tc(const GemmParams& p, cudaStream_t stream) {
   return launch_gemv_tc_mp<EPI, 128>(p, stream);
 }
 
-// Small-M path, TMA-streamed (every epilogue but SwiGLU): the weight [N, K] is read as boxes of
-// 8 rows x 256 columns (4 KiB) through a 16-stage shared-memory ring per CTA (two CTAs per SM:
-// ~128 KiB of weight in flight per SM, enough to cover HBM latency at full bandwidth for any N,
-// where the register-streamed kernel above keeps 16 KiB per CTA in flight and falls to
-// 2.3 TB/s at N = 4096). Each CTA owns a contiguous range of 8-row groups. Warp w takes columns
-// [32 w, 32 w + 32) of a box, lane l row l / 4 and 8 columns of those: its M activation slices
-// (16-byte L1 broadcasts) are shared by the warp's 8 rows. Per group the 8 x M dot products are
-// reduced over the 4 lanes of a row and the 8 warps, then the same epilogue as the tensor-core
-// kernel writes 8 output columns per activation row.
-#ifndef SW_GV_NST
-#define SW_GV_NST 16
-#endif
-#ifndef SW_GV_CTAS
-#define SW_GV_CTAS 2
-#endif
-constexpr int GV_BOXK = 256, GV_ROWS = 8, GV_NST = SW_GV_NST;
-constexpr int GV_BOX = GV_BOXK * GV_ROWS * 2;
-
-template <Epi EPI>
-__global__ void __launch_bounds__(288) gemv_tma_kernel(const __grid_constant__ CUtensorMap tw, const GemmParams p) {
-  extern __shared__ __align__(128) uint8_t gsm[];
-  uint8_t* ring = gsm;
-  float* red = reinterpret_cast<float*>(gsm + GV_NST * GV_BOX);       // [8 warps][8 rows][M]
-  uint64_t* full = reinterpret_cast<uint64_t*>(red + 8 * GV_ROWS * GEMV_MAX_M);
-  uint64_t* empty = full + GV_NST;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int ng = (p.N + GV_ROWS - 1) / GV_ROWS;
-  const int g0 = static_cast<int>((static_cast<int64_t>(blockIdx.x) * ng) / gridDim.x);
-  const int g1 = static_cast<int>((static_cast<int64_t>(blockIdx.x + 1) * ng) / gridDim.x);
-  const int nkc = (p.K + GV_BOXK - 1) / GV_BOXK;
-  if (threadIdx.x == 0) {
-    dev::tma_prefetch_desc(&tw);
-    for (int i = 0; i < GV_NST; ++i) {
-      dev::mbar_init(&full[i], 1);
-      dev::mbar_init(&empty[i], 8);
-    }
-    dev::fence_barrier_init();
-  }
-  __syncthreads();
-  if (warp == 8) {  // producer
-    if (lane == 0) {
-      int it = 0;
-      for (int g = g0; g < g1; ++g) {
-        for (int kc = 0; kc < nkc; ++kc, ++it) {
-          const int st = it % GV_NST;
-          dev::mbar_wait(&empty[st], ((it / GV_NST) & 1) ^ 1);
-          dev::mbar_arrive_expect_tx(&full[st], GV_BOX);
-          dev::tma_load_2d(ring + st * GV_BOX, &tw, &full[st], kc * GV_BOXK, g * GV_ROWS);
-        }
-      }
-    }
-    return;
-  }
-  const int M = p.M;
-  const int row = lane >> 2, kq = lane & 3;
-  const __nv_bfloat16* A = reinterpret_cast<const __nv_bfloat16*>(p.A);
-  int it = 0;
-  for (int g = g0; g < g1; ++g) {
-    float acc[GEMV_MAX_M];
-#pragma unroll
-    for (int m = 0; m < GEMV_MAX_M; ++m) acc[m] = 0.f;
-    for (int kc = 0; kc < nkc; ++kc, ++it) {
-      const int st = it % GV_NST;
-      const int k = kc * GV_BOXK + 32 * warp + 8 * kq;
-      // activation slices first (independent of the barrier)
-      uint4 av[GEMV_MAX_M];
-#pragma unroll
-      for (int m = 0; m < GEMV_MAX_M; ++m)
-        av[m] = (m < M && k < p.K) ? __ldg(reinterpret_cast<const uint4*>(A + static_cast<int64_t>(m) * p.lda + k))
-                                   : make_uint4(0, 0, 0, 0);
-      dev::mbar_wait(&full[st], (it / GV_NST) & 1);
-#if SW_GV_NOREAD
-      const uint4 wv = make_uint4(0, 0, 0, 0);
-#else
-      const uint4 wv = *reinterpret_cast<const uint4*>(ring + st * GV_BOX + row * (GV_BOXK * 2) + (32 * warp + 8 * kq) * 2);
-#endif
-      __syncwarp();
-      if (lane == 0) dev::mbar_arrive(&empty[st]);
-      const uint32_t ww[4] = {wv.x, wv.y, wv.z, wv.w};
-#pragma unroll
-      for (int m = 0; m < GEMV_MAX_M; ++m) {
-        if (m < M) {
-          const uint32_t aa[4] = {av[m].x, av[m].y, av[m].z, av[m].w};
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const float2 a2 = dev::unpack_bf16x2(aa[e]), w2 = dev::unpack_bf16x2(ww[e]);
-            acc[m] = fmaf(a2.x, w2.x, fmaf(a2.y, w2.y, acc[m]));
-          }
-        }
-      }
-    }
-    // reduce: the 4 lanes of a row, then the 8 warps through shared memory
-#pragma unroll
-    for (int m = 0; m < GEMV_MAX_M; ++m) {
-      acc[m] += __shfl_xor_sync(0xffffffffu, acc[m], 1);
-      acc[m] += __shfl_xor_sync(0xffffffffu, acc[m], 2);
-    }
-    if (kq == 0) {
-#pragma unroll
-      for (int m = 0; m < GEMV_MAX_M; ++m)
-        if (m < M) red[(warp * GV_ROWS + row) * GEMV_MAX_M + m] = acc[m];
-    }
-    asm volatile("bar.sync 1, 256;" ::: "memory");
-    if (threadIdx.x < M) {
-      const int m = threadIdx.x;
-      uint32_t r[32];
-#pragma unroll
-      for (int c = 0; c < 32; ++c) {
-        float v = 0.f;
-        if (c < GV_ROWS) {
-#pragma unroll
-          for (int w = 0; w < 8; ++w) v += red[(w * GV_ROWS + c) * GEMV_MAX_M + m];
-        }
-        r[c] = __float_as_uint(v);
-      }
-      epilogue_chunk<EPI>(p, m, g * GV_ROWS, min(GV_ROWS, p.N - g * GV_ROWS), r);
-    }
-    asm volatile("bar.sync 1, 256;" ::: "memory");  // red is rewritten by the next group
-  }
-}
-
-constexpr int GV_SMEM = GV_NST * GV_BOX + 8 * GV_ROWS * GEMV_MAX_M * 4 + 2 * GV_NST * 8;
-
-template <Epi EPI>
-cudaError_t launch_gemv_tma(const GemmParams& p, cudaStream_t stream) {
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(gemv_tma_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, GV_SMEM);
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
-  const CUtensorMap tw = make_tmap_bf16_2d_plain(p.B, p.K, p.N, p.ldb, GV_BOXK, GV_ROWS);
-  const int ng = (p.N + GV_ROWS - 1) / GV_ROWS;
-  const int grid = std::min(ng, SW_GV_CTAS * device_sm_count());
-  gemv_tma_kernel<EPI><<<grid, 288, GV_SMEM, stream>>>(tw, p);
-  return cudaGetLastError();
-}
-
-// SW_GEMV_TMA=1 selects the TMA-streamed kernel. Measured slower on B200 (1.5-1.9 TB/s against
-// 2.7-4.0 for the register-streamed kernel; 1.95 TB/s even with the consumers' shared-memory
-// reads removed: the 4 KiB boxes' issue/barrier round trip limits it), so it is off by default.
-bool gemv_tma_on() {
-  static const bool on = [] {
-    const char* e = std::getenv("SW_GEMV_TMA");
-    return e != nullptr && e[0] == '1';
-  }();
-  return on;
-}
 
 // The small-M path applies to forward-layout GEMMs whose activations fit in shared memory.
 bool gemv_tc_ok(const GemmParams& p) {
@@ -2043,15 +1881,6 @@ cudaError_t gemm_bf16(const GemmParams& p, cudaStream_t stream) {
       case Epi::kBiasGelu: return launch_gemv_tc<Epi::kBiasGelu>(p, stream);
       case Epi::kResidF32: return launch_gemv_tc<Epi::kResidF32>(p, stream);
       case Epi::kSwiGLU: return launch_gemv_tc<Epi::kSwiGLU>(p, stream);
-      default: break;
-    }
-  }
-  if (gemv_ok(p) && p.M <= GEMV_MAX_M && p.epi != Epi::kSwiGLU && gemv_tma_on()) {
-    switch (p.epi) {
-      case Epi::kStoreBf16: return launch_gemv_tma<Epi::kStoreBf16>(p, stream);
-      case Epi::kStoreF32: return launch_gemv_tma<Epi::kStoreF32>(p, stream);
-      case Epi::kBiasGelu: return launch_gemv_tma<Epi::kBiasGelu>(p, stream);
-      case Epi::kResidF32: return launch_gemv_tma<Epi::kResidF32>(p, stream);
       default: break;
     }
   }
