@@ -122,7 +122,8 @@ __global__ void __launch_bounds__(256) decode_attention_kernel(const bf16* __res
 }
 
 // Split-key decode attention (flash-decoding): grid (B * Hl, S), S = the CTA budget of a launch
-// (SW_DECODE_CTAS, 640) over the B * Hl heads, at most DSPLIT. The position is known on the device
+// (SW_DECODE_CTAS, 320) over the B * Hl heads, at least 2 and at most 8 (one cluster) -- the
+// global-merge variant (SW_DECODE_CLUSTER=0) allows DSPLIT with a budget floor of 1. The position is known on the device
 // only (CUDA-graph step), so the splits actually used are chosen there: n = min(S, ceil((p + 1) /
 // kps)), kps = SW_DECODE_KPS (64), and the CTAs of splits >= n exit at once. Split s of a head
 // takes keys [s c, min(p + 1, (s + 1) c)), c = ceil((p + 1) / n); lanes work in groups of G =
@@ -143,7 +144,7 @@ __global__ void __launch_bounds__(256) decode_attention_kernel(const bf16* __res
 #define SW_DKPS 64
 #endif
 #ifndef SW_DCTAS
-#define SW_DCTAS 640
+#define SW_DCTAS 320
 #endif
 // fewest keys per split (SW_DECODE_KPS) and the CTA budget of one launch (SW_DECODE_CTAS)
 int env_or(const char* name, int dflt) {
@@ -532,7 +533,8 @@ void launch_decode_split(const bf16* qkv_new, bf16* cache, bf16* out, int B, int
   if (decode_cluster_on()) {
     // splits per head: keys / kps, at most the CTA budget over the B * Hl heads and the portable
     // cluster size
-    const int max_split = std::max(1, std::min(8, decode_ctas() / (B * Hl)));
+    // (at least two: with many heads one split per head leaves each CTA the whole context)
+    const int max_split = std::max(2, std::min(8, decode_ctas() / (B * Hl)));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(static_cast<unsigned>(B * Hl), static_cast<unsigned>(max_split));
     cfg.blockDim = dim3(256);
