@@ -174,6 +174,7 @@ __global__ void __launch_bounds__(256) decode_attention_split_kernel(const bf16*
                                                                      float scale_log2, float* __restrict__ part,
                                                                      unsigned int* __restrict__ ticket, int kps,
                                                                      int max_split) {
+  asm volatile("griddepcontrol.launch_dependents;");  // the output projection may start streaming
   if (pd != nullptr) p = *pd;
   constexpr int G = HD / 8;
   constexpr int KPW = 32 / G;

@@ -80,6 +80,9 @@ struct GemmParams {
   // ReLU instead of GeLU (T5 MLP): kStoreBf16 stores relu(acc + bias); kGeluBwd multiplies by
   // relu'(aux) = (aux > 0) with aux = the stored ReLU output
   int relu = 0;
+  // Decode: launch the weight-streaming kernel as a programmatic dependent of the previous kernel
+  // in the stream (its first weight lines are requested before griddepcontrol.wait)
+  int pdl = 0;
 };
 
 // Returns cudaSuccess or the launch error. Throws std::runtime_error on invalid shapes.

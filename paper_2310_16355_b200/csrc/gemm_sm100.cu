@@ -1470,6 +1470,26 @@ __global__ void __launch_bounds__(256) gemv_mma_kernel(const GemmParams p) {
 #define SW_GEMV_U 4
 #endif
   constexpr int U = NB >= 4 ? 2 : kGlu ? (SW_GEMV_U >= 4 ? SW_GEMV_U / 2 : 2) : SW_GEMV_U;
+  // programmatic dependent launch (decode): the weights do not depend on the previous kernel, so
+  // the first steps' lines are requested into L2 before waiting for it (a no-op without PDL)
+  if (p.pdl) {
+    // prefetch depth: measured faster for weight matrices that fit L2 (LLaMA-7B width, 2.64 ->
+    // 2.56 ms/token), slower for larger ones (OPT-66B width), where only the early launch is kept
+    const bool fits_l2 = static_cast<int64_t>(p.N) * p.K * 2 * NT <= (128ll << 20);
+    const int pf_steps = (p.pdl >= 3 && fits_l2) ? 2 * U : (p.pdl == 2 ? U : 0);
+#pragma unroll
+    for (int u = 0; u < 2 * U; ++u) {
+      const int kk = warp * 32 + u * 256;
+      if (kk < K && u < pf_steps) {
+#pragma unroll
+        for (int q = 0; q < NT; ++q) {
+          dev::prefetch_l2(wlo_p[q] + kk);
+          dev::prefetch_l2(whi_p[q] + kk);
+        }
+      }
+    }
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+  }
   for (int k = warp * 32; k < K; k += 256 * U) {
     uint4 wl[U][NT], wh[U][NT], av[U][NB];
 #pragma unroll
@@ -1503,6 +1523,7 @@ __global__ void __launch_bounds__(256) gemv_mma_kernel(const GemmParams p) {
       }
     }
   }
+  if (p.pdl) asm volatile("griddepcontrol.launch_dependents;");
   // d0, d1: (row g, activation rows 8j + 2t, 8j + 2t + 1); d2, d3: (row g + 8, same)
 #pragma unroll
   for (int q = 0; q < NT; ++q) {
@@ -1743,7 +1764,18 @@ cudaError_t launch_gemv(const GemmParams& p, cudaStream_t stream) {
     }();
     if ((p.M >= mma_min_m || p.M > GEMV_MAX_M) && p.K % 32 == 0 && gemv_mma_on()) {
       const unsigned nt = static_cast<unsigned>((p.N + 15) / 16);
-      if (p.M <= 8) {
+      if (p.M <= 8 && p.pdl) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(1, nt);
+        cfg.blockDim = dim3(256);
+        cfg.stream = stream;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        return cudaLaunchKernelEx(&cfg, gemv_mma_kernel<EPI, 1>, p);
+      } else if (p.M <= 8) {
         gemv_mma_kernel<EPI, 1><<<dim3(1, nt), 256, 0, stream>>>(p);
       } else if (p.M <= 16) {
         gemv_mma_kernel<EPI, 2><<<dim3(1, nt), 256, 0, stream>>>(p);

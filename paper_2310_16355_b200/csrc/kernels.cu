@@ -1039,6 +1039,7 @@ __global__ void __launch_bounds__(1024) ln_fwd_1pass_kernel(const float* __restr
                                                             const float* __restrict__ bias, bf16* __restrict__ y,
                                                             float* __restrict__ mean_out, float* __restrict__ rstd_out,
                                                             int d, float eps, int rms) {
+  asm volatile("griddepcontrol.launch_dependents;");  // the next weight-streaming GEMM may start
   __shared__ float2 red[32];
   const int64_t row = blockIdx.x;
   const float* xr = x + row * d;

@@ -807,6 +807,7 @@ void Model::gemm(Rank& R, int M, int N, int K, const void* A, int64_t lda, int a
   p.aux = aux;
   p.ld_aux = ld_aux;
   p.accumulate = accumulate;
+  p.pdl = prof_ ? 0 : pdl_;
   tic();
   cuda_check(gemm_bf16(p, stream_), "gemm launch");
   // kSwiGLU multiplies by the fused [gate; up] weight: 2N output columns of MMA work
@@ -1651,6 +1652,15 @@ void Model::window_forward(std::vector<Rank*>& grp, const std::vector<std::vecto
 
 void Model::decode_step(std::vector<Rank*>& grp, int p) {
   const int B = B_, d = d_, dl = dl_, fl = fl_;
+  static const int pdl_on = [] {
+    const char* e = std::getenv("SW_DECODE_PDL");
+    return e != nullptr ? std::atoi(e) : 3;
+  }();
+  struct PdlScope {
+    int& f;
+    PdlScope(int& flag, int v) : f(flag) { f = v; }
+    ~PdlScope() { f = 0; }
+  } pdl_scope(pdl_, pdl_on);
   const bool dev_pos = p < 0;
   auto pd = [&](Rank& R) -> const int* { return dev_pos ? dec_[static_cast<size_t>(&R - ranks_.data())].pos : nullptr; };
   for (Rank* R : grp) {

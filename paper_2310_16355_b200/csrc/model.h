@@ -272,6 +272,9 @@ class Model {
   int32_t* dec_out_ = nullptr;   // [n_cap, B] tokens of cached steps, read back in batches
   int64_t dec_out_cap_ = 0;
   cudaGraphExec_t dec_graph_ = nullptr;  // one cached decode step, position on the device
+  // decode_step: small-M GEMMs launched as programmatic dependents (0 off; 1 + n: n x U weight
+  // steps requested into L2 before griddepcontrol.wait)
+  int pdl_ = 0;
   // p >= 0: position p (host value); p < 0: every rank's dec_[].pos, advanced at the step's end
   void decode_step(std::vector<Rank*>& grp, int p);
   void window_forward(std::vector<Rank*>& grp, const std::vector<std::vector<int32_t>>& ctx, int take);
