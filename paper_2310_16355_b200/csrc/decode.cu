@@ -193,6 +193,18 @@ __global__ void __launch_bounds__(256) decode_attention_split_kernel(const bf16*
   if (!CL && sp >= nsplit) return;  // a cluster's idle splits still meet its barriers (empty range)
   const int chunk = (nk + nsplit - 1) / nsplit;
   const int k0 = sp < nsplit ? sp * chunk : nk, k1 = sp < nsplit ? min(nk, k0 + chunk) : nk;
+  if constexpr (CL) {
+    // launched as a programmatic dependent of the QKV GEMM: the cached keys / values (every row
+    // but p, which that GEMM is producing) are requested into L2 before waiting for it
+    for (int i = threadIdx.x; i < 2 * (k1 - k0) * (HD / 64); i += blockDim.x) {
+      const int j = k0 + i / (2 * (HD / 64));
+      const int part = i % (2 * (HD / 64));  // K or V, 128-byte line of the head's row
+      if (j != p)
+        dev::prefetch_l2(cache + (static_cast<int64_t>(b) * T + j) * 3 * dl + dl + (part / (HD / 64)) * dl + h * HD +
+                         (part % (HD / 64)) * 64);
+    }
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+  }
   const bf16* qrow = qnew + static_cast<int64_t>(b) * 3 * dl;
   float q[8];
   {
@@ -519,6 +531,15 @@ __global__ void bump_kernel(int* x) { *x += 1; }
 
 void bump_i32(int* x, cudaStream_t s) { bump_kernel<<<1, 1, 0, s>>>(x); }
 
+// SW_DECODE_PDL=0: the decode attention / LayerNorm kernels wait for their predecessor to finish
+bool decode_pdl_on() {
+  static const bool on = [] {
+    const char* e = std::getenv("SW_DECODE_PDL");
+    return !(e != nullptr && e[0] == '0');
+  }();
+  return on;
+}
+
 bool decode_cluster_on() {
   static const bool on = [] {
     const char* e = std::getenv("SW_DECODE_CLUSTER");
@@ -540,13 +561,15 @@ void launch_decode_split(const bf16* qkv_new, bf16* cache, bf16* out, int B, int
     cfg.gridDim = dim3(static_cast<unsigned>(B * Hl), static_cast<unsigned>(max_split));
     cfg.blockDim = dim3(256);
     cfg.stream = s;
-    cudaLaunchAttribute at[1];
+    cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = 1;
     at[0].val.clusterDim.y = static_cast<unsigned>(max_split);
     at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = decode_pdl_on() ? 1 : 0;
     cfg.attrs = at;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 2;
     const cudaError_t e = cudaLaunchKernelEx(&cfg, decode_attention_split_kernel<HD, true>, qkv_new, cache, out, T,
                                              p, p_dev, Hl, scale_log2, part, ticket, kps, max_split);
     if (e != cudaSuccess) throw std::runtime_error(std::string("decode attention launch: ") + cudaGetErrorString(e));

@@ -1040,6 +1040,8 @@ __global__ void __launch_bounds__(1024) ln_fwd_1pass_kernel(const float* __restr
                                                             float* __restrict__ mean_out, float* __restrict__ rstd_out,
                                                             int d, float eps, int rms) {
   asm volatile("griddepcontrol.launch_dependents;");  // the next weight-streaming GEMM may start
+  // launched as a programmatic dependent (decode): x comes from the kernel before
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   __shared__ float2 red[32];
   const int64_t row = blockIdx.x;
   const float* xr = x + row * d;
@@ -1089,10 +1091,25 @@ void layernorm_fwd_small(const float* x, const float* scale, const float* bias, 
     return !(e != nullptr && e[0] == '0');
   }();
   const unsigned g = static_cast<unsigned>(M);
-  if (on && M <= 8 && d % 4 == 0 && d <= 4096) {
-    ln_fwd_1pass_kernel<1><<<g, 1024, 0, s>>>(x, scale, bias, y, mean, rstd, d, eps, rms);
-  } else if (on && M <= 8 && d % 4 == 0 && d <= 12288) {
-    ln_fwd_1pass_kernel<3><<<g, 1024, 0, s>>>(x, scale, bias, y, mean, rstd, d, eps, rms);
+  static const bool pdl = [] {
+    const char* e = std::getenv("SW_DECODE_PDL");
+    return !(e != nullptr && e[0] == '0');
+  }();
+  if (on && M <= 8 && d % 4 == 0 && d <= 12288) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(g);
+    cfg.blockDim = dim3(1024);
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    if (d <= 4096) {
+      cudaLaunchKernelEx(&cfg, ln_fwd_1pass_kernel<1>, x, scale, bias, y, mean, rstd, d, eps, rms);
+    } else {
+      cudaLaunchKernelEx(&cfg, ln_fwd_1pass_kernel<3>, x, scale, bias, y, mean, rstd, d, eps, rms);
+    }
   } else {
     layernorm_fwd(x, scale, bias, y, mean, rstd, M, d, eps, s, rms);
   }
