@@ -1622,6 +1622,20 @@ __global__ void __launch_bounds__(128, 1) gemv_tc_kernel(const __grid_constant__
     dev::fence_barrier_init();
   }
   if (warp == 2) dev::tmem_alloc<G::TCOLS>(tslot);
+  if (p.pdl) {
+    // programmatic dependent launch (decode): the first stages' weight rows are requested into L2
+    // before waiting for the kernel that produces the activations
+    const int nb = min(kb1 - kb0, G::STAGES);
+    for (int i = tid; i < 128 * G::NT * nb * 2; i += 128) {
+      const int half = i & 1, kb = kb0 + (i >> 1) / (128 * G::NT), rr = ((i >> 1) % (128 * G::NT));
+      const int row = (rr < 128 ? n0 + rr : p.swiglu_half + n0 + rr - 128);
+      const int64_t rows_total = G::NT == 2 ? 2LL * p.swiglu_half : p.N;
+      if (row < rows_total && kb * 64 + half * 32 < p.K)
+        dev::prefetch_l2(reinterpret_cast<const __nv_bfloat16*>(p.B) + static_cast<int64_t>(row) * p.ldb + kb * 64 +
+                         half * 32);
+    }
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+  }
   dev::tc_fence_before();
   __syncthreads();
   dev::tc_fence_after();
@@ -1664,6 +1678,7 @@ __global__ void __launch_bounds__(128, 1) gemv_tc_kernel(const __grid_constant__
   // accumulator (lane = weight row n0 + tid, column = activation row) -> transposed in shared
   // memory (the ring is idle: every MMA, hence every TMA load, has completed)
   dev::mbar_wait(done, 0);
+  if (p.pdl) asm volatile("griddepcontrol.launch_dependents;");
   dev::tc_fence_after();
   float* sT = reinterpret_cast<float*>(sm);
   const uint32_t lb = static_cast<uint32_t>(warp * 32) << 16;
@@ -1848,13 +1863,15 @@ cudaError_t launch_gemv_tc_mp(const GemmParams& p, cudaStream_t stream) {
   cfg.blockDim = dim3(128);
   cfg.dynamicSmemBytes = G::SMEM;
   cfg.stream = stream;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = static_cast<unsigned>(S);
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = p.pdl ? 1 : 0;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   return cudaLaunchKernelEx(&cfg, gemv_tc_kernel<EPI, MP>, tw, ta, p, S);
 }
 
