@@ -1430,7 +1430,12 @@ __device__ __forceinline__ void mma_bf16_16816(float (&d)[4], uint32_t a0, uint3
 // NB: 8-row activation groups per warp (the weight fragments of a k step feed NB mmas);
 // gridDim.x: groups of 8 * NB activation rows, adjacent CTAs, so the re-reads of a weight tile
 // by the CTAs of the other groups hit L2 (M up to GEMV_MMA_MAX_M).
-template <Epi EPI, int NB>
+#ifndef SW_GEMV_U
+#define SW_GEMV_U 4
+#endif
+// UX: 32-deep k steps per warp in flight (4; 8 for matrices larger than L2, measured: OPT-66B
+// decode 23.3 -> 22.9 ms/token, while the LLaMA-7B-width matrices prefer 4)
+template <Epi EPI, int NB, int UX = SW_GEMV_U>
 __global__ void __launch_bounds__(256) gemv_mma_kernel(const GemmParams p) {
   constexpr bool kGlu = EPI == Epi::kSwiGLU;  // SwiGLU: gate rows c0.. and up rows swiglu_half + c0..
   constexpr int NT = kGlu ? 2 : 1;
@@ -1466,10 +1471,7 @@ __global__ void __launch_bounds__(256) gemv_mma_kernel(const GemmParams p) {
 #pragma unroll
     for (int j = 0; j < NB; ++j) acc[q][j][0] = acc[q][j][1] = acc[q][j][2] = acc[q][j][3] = 0.f;
   // 32-deep k steps per warp with their loads in flight together
-#ifndef SW_GEMV_U
-#define SW_GEMV_U 4
-#endif
-  constexpr int U = NB >= 4 ? 2 : kGlu ? (SW_GEMV_U >= 4 ? SW_GEMV_U / 2 : 2) : SW_GEMV_U;
+  constexpr int U = NB >= 4 ? 2 : kGlu ? (UX >= 4 ? UX / 2 : 2) : UX;
   // programmatic dependent launch (decode): the weights do not depend on the previous kernel, so
   // the first steps' lines are requested into L2 before waiting for it (a no-op without PDL)
   if (p.pdl) {
@@ -1779,6 +1781,7 @@ cudaError_t launch_gemv(const GemmParams& p, cudaStream_t stream) {
     }();
     if ((p.M >= mma_min_m || p.M > GEMV_MAX_M) && p.K % 32 == 0 && gemv_mma_on()) {
       const unsigned nt = static_cast<unsigned>((p.N + 15) / 16);
+      const bool big = static_cast<int64_t>(p.N) * p.K * 2 * (EPI == Epi::kSwiGLU ? 2 : 1) > (128ll << 20);
       if (p.M <= 8 && p.pdl) {
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(1, nt);
@@ -1789,9 +1792,14 @@ cudaError_t launch_gemv(const GemmParams& p, cudaStream_t stream) {
         at[0].val.programmaticStreamSerializationAllowed = 1;
         cfg.attrs = at;
         cfg.numAttrs = 1;
-        return cudaLaunchKernelEx(&cfg, gemv_mma_kernel<EPI, 1>, p);
+        return big ? cudaLaunchKernelEx(&cfg, gemv_mma_kernel<EPI, 1, 8>, p)
+                   : cudaLaunchKernelEx(&cfg, gemv_mma_kernel<EPI, 1>, p);
       } else if (p.M <= 8) {
-        gemv_mma_kernel<EPI, 1><<<dim3(1, nt), 256, 0, stream>>>(p);
+        if (big) {
+          gemv_mma_kernel<EPI, 1, 8><<<dim3(1, nt), 256, 0, stream>>>(p);
+        } else {
+          gemv_mma_kernel<EPI, 1><<<dim3(1, nt), 256, 0, stream>>>(p);
+        }
       } else if (p.M <= 16) {
         gemv_mma_kernel<EPI, 2><<<dim3(1, nt), 256, 0, stream>>>(p);
       } else {
