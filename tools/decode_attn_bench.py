@@ -43,6 +43,12 @@ def run(Hl, p, B=1, T=2048, hd=128, iters=200):
 
 
 if __name__ == "__main__":
+    if len(sys.argv) > 1:  # batched: python tools/decode_attn_bench.py B [Hl p]
+        B = int(sys.argv[1])
+        Hl = int(sys.argv[2]) if len(sys.argv) > 2 else 32
+        for p in ([int(sys.argv[3])] if len(sys.argv) > 3 else (512, 1024)):
+            print(json.dumps(run(Hl, p, B=B, iters=50)))
+        sys.exit(0)
     for Hl in (32, 72):
         for p in (128, 512, 1024, 2000):
             print(json.dumps(run(Hl, p)))
