@@ -1614,6 +1614,53 @@ void Model::window_forward(std::vector<Rank*>& grp, const std::vector<std::vecto
     return !(e != nullptr && e[0] == '0');
   }();
   const int Tp = (take + 127) / 128 * 128;
+  if (trim_on && Tp < T_ && B_ > 1 && T_ >= 2 * Tp) {
+    // Several sequences: their first Tp rows side by side ([B, Tp] rows) in one forward (GEMMs
+    // of B * Tp rows instead of B launches of Tp), then each sequence's K/V rows move to its
+    // [B, T] cache rows. Sequence b's packed rows [b Tp, b Tp + Tp) lie below every later
+    // sequence's destination and T >= 2 Tp keeps a destination off its own source, so moving
+    // b = B-1 down to 1 never overwrites a row that is still to be read.
+    const int B = B_, T = T_, chunks = ar_chunks_;
+    const int64_t M = M_;
+    std::vector<int32_t> packed(static_cast<size_t>(B) * Tp, 0);
+    for (int b = 0; b < B; ++b)
+      std::copy(win.begin() + static_cast<int64_t>(b) * T, win.begin() + static_cast<int64_t>(b) * T + Tp,
+                packed.begin() + static_cast<int64_t>(b) * Tp);
+    for (Rank* R : grp) {
+      cuda_check(cudaMemcpyAsync(R->tokens, packed.data(), packed.size() * 4, cudaMemcpyHostToDevice, stream_),
+                 "H2D");
+    }
+    cuda_check(cudaStreamSynchronize(stream_), "prefill");  // `packed` is a host temporary
+    T_ = Tp;
+    M_ = static_cast<int64_t>(B) * Tp;
+    if (M_ % ar_chunks_ != 0) ar_chunks_ = 1;
+    try {
+      forward_replica(grp, false);
+    } catch (...) {
+      T_ = T;
+      M_ = M;
+      ar_chunks_ = chunks;
+      throw;
+    }
+    T_ = T;
+    M_ = M;
+    ar_chunks_ = chunks;
+    const int64_t row = 3LL * dl_;
+    for (Rank* R : grp) {
+      for (int l = 0; l < L_; ++l) {
+        for (int b = B - 1; b >= 1; --b) {
+          cuda_check(cudaMemcpyAsync(R->qkv[l] + static_cast<int64_t>(b) * T * row,
+                                     R->qkv[l] + static_cast<int64_t>(b) * Tp * row, static_cast<size_t>(Tp) * row * 2,
+                                     cudaMemcpyDeviceToDevice, stream_),
+                     "D2D");
+        }
+      }
+    }
+    std::vector<const bf16*> rows;
+    for (Rank* R : grp) rows.push_back(R->logits + static_cast<int64_t>(take - 1) * ldv_);
+    pick_tokens(grp, rows, static_cast<int64_t>(Tp) * ldv_);
+    return;
+  }
   if (trim_on && Tp < T_) {
     const int B = B_, T = T_, chunks = ar_chunks_;
     const int64_t M = M_;
