@@ -926,6 +926,43 @@ void Model::forward_replica(std::vector<Rank*>& grp, bool need_grad) {
     }
   }
   const int head = head_ >= 0 ? head_ : tok_;
+  static const bool head_row_on = [] {
+    const char* e = std::getenv("SW_PREFILL_HEAD_ROW");
+    return !(e != nullptr && e[0] == '0');
+  }();
+  if (head_row_ >= 0 && !head_row_on) {  // all rows through the head, then the rows picked
+    for (Rank* R : grp) {
+      DecodeBufs& D = dec_[static_cast<size_t>(R - ranks_.data())];
+      k::layernorm_fwd(R->hs[L_], P(*R, lnf_s_), Pn(*R, lnf_b_), R->f, R->statsf, R->statsf + M, M, d, 1e-5f,
+                       stream_, spec_.rmsnorm);
+      gemm(*R, static_cast<int>(M), vl_, d, R->f, d, 0, W(*R, head), d, 0, static_cast<int>(Epi::kStoreBf16),
+           R->logits, ldv_);
+      cuda_check(cudaMemcpy2DAsync(D.logits + static_cast<int64_t>(head_seq_) * ldv_, static_cast<size_t>(ldv_) * 2,
+                                   R->logits + static_cast<int64_t>(head_row_) * ldv_,
+                                   static_cast<size_t>(T_) * ldv_ * 2, static_cast<size_t>(ldv_) * 2, B_,
+                                   cudaMemcpyDeviceToDevice, stream_),
+                 "D2D 2D");
+    }
+    return;
+  }
+  if (head_row_ >= 0) {
+    // prefill: only row head_row_ of every sequence needs logits (the next token); its final
+    // hidden row goes through the head as a small-M GEMM into the decode buffers, no loss
+    for (Rank* R : grp) {
+      DecodeBufs& D = dec_[static_cast<size_t>(R - ranks_.data())];
+      k::layernorm_fwd(R->hs[L_], P(*R, lnf_s_), Pn(*R, lnf_b_), R->f, R->statsf, R->statsf + M, M, d, 1e-5f,
+                       stream_, spec_.rmsnorm);
+      ++launches_;
+      bf16* f = D.f + static_cast<int64_t>(head_seq_) * d;
+      cuda_check(cudaMemcpy2DAsync(f, static_cast<size_t>(d) * 2, R->f + static_cast<int64_t>(head_row_) * d,
+                                   static_cast<size_t>(T_) * d * 2, static_cast<size_t>(d) * 2, B_,
+                                   cudaMemcpyDeviceToDevice, stream_),
+                 "D2D 2D");
+      gemm(*R, B_, vl_, d, f, d, 0, W(*R, head), d, 0, static_cast<int>(Epi::kStoreBf16),
+           D.logits + static_cast<int64_t>(head_seq_) * ldv_, ldv_);
+    }
+    return;
+  }
   for (Rank* R : grp) {
     tic();
     k::layernorm_fwd(R->hs[L_], P(*R, lnf_s_), Pn(*R, lnf_b_), R->f, R->statsf, R->statsf + M, M, d, 1e-5f,
@@ -1634,17 +1671,20 @@ void Model::window_forward(std::vector<Rank*>& grp, const std::vector<std::vecto
     T_ = Tp;
     M_ = static_cast<int64_t>(B) * Tp;
     if (M_ % ar_chunks_ != 0) ar_chunks_ = 1;
+    head_row_ = take - 1;
     try {
       forward_replica(grp, false);
     } catch (...) {
       T_ = T;
       M_ = M;
       ar_chunks_ = chunks;
+      head_row_ = -1;
       throw;
     }
     T_ = T;
     M_ = M;
     ar_chunks_ = chunks;
+    head_row_ = -1;
     const int64_t row = 3LL * dl_;
     for (Rank* R : grp) {
       for (int l = 0; l < L_; ++l) {
@@ -1657,8 +1697,8 @@ void Model::window_forward(std::vector<Rank*>& grp, const std::vector<std::vecto
       }
     }
     std::vector<const bf16*> rows;
-    for (Rank* R : grp) rows.push_back(R->logits + static_cast<int64_t>(take - 1) * ldv_);
-    pick_tokens(grp, rows, static_cast<int64_t>(Tp) * ldv_);
+    for (Rank* R : grp) rows.push_back(dec_[static_cast<size_t>(R - ranks_.data())].logits);
+    pick_tokens(grp, rows, ldv_);
     return;
   }
   if (trim_on && Tp < T_) {
@@ -1676,8 +1716,10 @@ void Model::window_forward(std::vector<Rank*>& grp, const std::vector<std::vecto
       M_ = M;
       ar_chunks_ = chunks;
     };
+    head_row_ = take - 1;
     try {
       for (int b = 0; b < B; ++b) {
+        head_seq_ = b;
         forward_replica(grp, false);
         if (b + 1 < B) {
           shift_rows(grp, T);
@@ -1686,15 +1728,26 @@ void Model::window_forward(std::vector<Rank*>& grp, const std::vector<std::vecto
       }
     } catch (...) {
       restore();
+      head_row_ = -1;
+      head_seq_ = 0;
       throw;
     }
     restore();
+    head_row_ = -1;
+    head_seq_ = 0;
   } else {
-    forward_replica(grp, false);
+    head_row_ = take - 1;
+    try {
+      forward_replica(grp, false);
+    } catch (...) {
+      head_row_ = -1;
+      throw;
+    }
+    head_row_ = -1;
   }
   std::vector<const bf16*> rows;
-  for (Rank* R : grp) rows.push_back(R->logits + static_cast<int64_t>(take - 1) * ldv_);
-  pick_tokens(grp, rows, static_cast<int64_t>(T_) * ldv_);
+  for (Rank* R : grp) rows.push_back(dec_[static_cast<size_t>(R - ranks_.data())].logits);
+  pick_tokens(grp, rows, ldv_);
 }
 
 void Model::decode_step(std::vector<Rank*>& grp, int p) {

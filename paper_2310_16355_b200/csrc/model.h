@@ -272,6 +272,10 @@ class Model {
   int32_t* dec_out_ = nullptr;   // [n_cap, B] tokens of cached steps, read back in batches
   int64_t dec_out_cap_ = 0;
   cudaGraphExec_t dec_graph_ = nullptr;  // one cached decode step, position on the device
+  // prefill (window_forward): >= 0 makes forward_replica compute the logits of only this row of
+  // every sequence, into the decode buffers, and skip the loss
+  int head_row_ = -1;
+  int head_seq_ = 0;  // the decode-buffer row its logits go to (one-sequence-at-a-time prefill)
   // decode_step: small-M GEMMs launched as programmatic dependents (0 off; 1 + n: n x U weight
   // steps requested into L2 before griddepcontrol.wait)
   int pdl_ = 0;
