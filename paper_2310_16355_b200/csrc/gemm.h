@@ -83,6 +83,10 @@ struct GemmParams {
   // Decode: launch the weight-streaming kernel as a programmatic dependent of the previous kernel
   // in the stream (its first weight lines are requested before griddepcontrol.wait)
   int pdl = 0;
+  // kStoreF32 only: K split into this many slices whose fp32 partial tiles are reduce-added into C
+  // by TMA (0 = chosen by gemm_bf16 for GEMMs with too few tiles to fill the GPU; C is zeroed
+  // first unless accumulate). Summation order differs from the unsplit GEMM (fp32 rounding).
+  int split_k = 0;
 };
 
 // Returns cudaSuccess or the launch error. Throws std::runtime_error on invalid shapes.
@@ -93,6 +97,9 @@ cudaError_t gemm_bf16(const GemmParams& p, cudaStream_t stream);
 bool gemm_delta_ok(const GemmParams& p);
 // Whether a kGeluBwd call can also write the partial column sums (p.colsum).
 bool gemm_colsum_ok(const GemmParams& p);
+
+// The split-K slice count gemm_bf16 would use for p run as an fp32-store GEMM (1 = no split).
+int gemm_split_k(const GemmParams& p);
 
 // Profiling: the 1024 per-tile phase stamps of the CTA named by SW_GEMM_TRACE_CTA.
 void gemm_trace_read(unsigned long long* out);

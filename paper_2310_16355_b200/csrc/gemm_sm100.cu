@@ -701,8 +701,12 @@ __global__ void __cluster_dims__(GEMM_CL, 1, 1) __launch_bounds__(p_threads<EPI>
   const int pair = static_cast<int>(blockIdx.x) / GEMM_CL;     // cluster index
   const int npairs = static_cast<int>(gridDim.x) / GEMM_CL;
   const int num_nc = GEMM_CL == 4 ? (num_n + 1) / 2 : num_n;   // n-block units per cluster tile
-  const int num_units = num_m * num_nc;
-  auto pair_tile = [&](int t, int& mb, int& nb) {
+  // split-K (kStoreF32): unit u is K slice u % nsplit of tile u / nsplit, so a tile's slices run
+  // side by side and meet in C through TMA reduce-adds
+  const int nsplit = p.split_k > 1 ? p.split_k : 1;
+  const int num_units = num_m * num_nc * nsplit;
+  auto pair_tile = [&](int u, int& mb, int& nb) {
+    const int t = u / nsplit;
     if constexpr (GEMM_CL == 4) {
       int nbp;
       tile_coords(t, num_m, num_nc, mb, nbp);
@@ -711,6 +715,8 @@ __global__ void __cluster_dims__(GEMM_CL, 1, 1) __launch_bounds__(p_threads<EPI>
       tile_coords(t, num_m, num_n, mb, nb);
     }
   };
+  auto kb_lo = [&](int u) { return (u % nsplit) * num_kb / nsplit; };
+  auto kb_hi = [&](int u) { return (u % nsplit + 1) * num_kb / nsplit; };
 
   if (warp == 0 && lane == 0) {
     dev::tma_prefetch_desc(&tmA);
@@ -747,7 +753,7 @@ __global__ void __cluster_dims__(GEMM_CL, 1, 1) __launch_bounds__(p_threads<EPI>
         // SwiGLU: CTA 0 stages the tile's 128 gate rows, CTA 1 the matching 128 up rows
         const int n0 = kGlu ? (rank == 0 ? nb * 128 : p.swiglu_half + nb * 128)
                             : nb * BN + static_cast<int>(rank) * 128;
-        for (int kb = 0; kb < num_kb; ++kb) {
+        for (int kb = kb_lo(t), kb_end = kb_hi(t); kb < kb_end; ++kb) {
           dev::mbar_wait(&empty[stage], phase ^ 1);
           if (rank == 0) dev::mbar_arrive_expect_tx(&full[stage], 2 * P_STAGE_BYTES);
           const int k0 = kb * BK;
@@ -804,7 +810,8 @@ __global__ void __cluster_dims__(GEMM_CL, 1, 1) __launch_bounds__(p_threads<EPI>
         if (tr && lane == 0 && ti < 64) g_gemm_trace[8 * ti] = clock64();
         long long waited = 0;
         const uint32_t d_tmem = tmem_base + acc * BN;
-        for (int kb = 0; kb < num_kb; ++kb) {
+        const int kb0 = kb_lo(t);
+        for (int kb = kb0, kb_end = kb_hi(t); kb < kb_end; ++kb) {
           const long long w0 = tr ? clock64() : 0;
           dev::mbar_wait(&full[stage], phase);
           dev::tc_fence_after();
@@ -814,7 +821,7 @@ __global__ void __cluster_dims__(GEMM_CL, 1, 1) __launch_bounds__(p_threads<EPI>
           if (dev::elect_one_sync()) {
 #pragma unroll
             for (int k = 0; k < BK / 16; ++k)
-              dev::umma_f16_ss_2sm(d_tmem, as + k * a_step, bs + k * b_step, idesc, (kb | k) != 0 ? 1u : 0u);
+              dev::umma_f16_ss_2sm(d_tmem, as + k * a_step, bs + k * b_step, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
             // the stage is free once every pair that reads or multicasts into it is done
             dev::umma_commit_2sm(&empty[stage], GEMM_CL == 4 ? 0xF : 0x3);
           }
@@ -1020,9 +1027,10 @@ __global__ void __cluster_dims__(GEMM_CL, 1, 1) __launch_bounds__(p_threads<EPI>
 #pragma unroll 1
 #if SW_EPI_PF == 0
       if constexpr (tma_epi<EPI>()) {
-        if (!p.accumulate) {
+        if (!p.accumulate || nsplit > 1) {
           // stage in shared memory (lane = row of the warp's 32, swizzled 16-byte units), one TMA
-          // store per chunk; a buffer is rewritten only after its previous store read it
+          // store per chunk (a reduce-add under split-K); a buffer is rewritten only after its
+          // previous store read it
           uint8_t* stg = sOpt + (static_cast<int>(warp) - 4) * 2 * EPI_TMA_BUF;
           constexpr bool f32 = EPI == Epi::kStoreF32 || EPI == Epi::kResidF32;
           constexpr bool resid = EPI == Epi::kResidF32, gbwd = EPI == Epi::kGeluBwd, gfwd = EPI == Epi::kBiasGelu;
@@ -1132,7 +1140,11 @@ __global__ void __cluster_dims__(GEMM_CL, 1, 1) __launch_bounds__(p_threads<EPI>
             dev::fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) {
-              dev::tma_store_2d(&om.c, stg + (j & 1) * EPI_TMA_BUF, nb * BN + j * 32, row - static_cast<int>(lane));
+              if (nsplit > 1) {
+                dev::tma_reduce_add_2d(&om.c, stg + (j & 1) * EPI_TMA_BUF, nb * BN + j * 32, row - static_cast<int>(lane));
+              } else {
+                dev::tma_store_2d(&om.c, stg + (j & 1) * EPI_TMA_BUF, nb * BN + j * 32, row - static_cast<int>(lane));
+              }
               if constexpr (gfwd)
                 dev::tma_store_2d(&om.c2, stg + (j & 1) * EPI_TMA_BUF + 2048, nb * BN + j * 32,
                                   row - static_cast<int>(lane));
@@ -1244,12 +1256,13 @@ cudaError_t launch_2sm(const GemmParams& p, cudaStream_t stream) {
   CUtensorMap tb = p.b_mn_major ? make_tmap_bf16_2d(p.B, p.N, p.K, p.ldb, 64, 64)
                                 : make_tmap_bf16_2d(p.B, p.K, b_rows, p.ldb, 64, 128);
   const int num_n = EPI == Epi::kSwiGLU ? (p.N + 127) / 128 : (p.N + BN - 1) / BN;
-  const int num_units = ((p.M + 2 * BM - 1) / (2 * BM)) * (GEMM_CL == 4 ? (num_n + 1) / 2 : num_n);
+  const int num_units = ((p.M + 2 * BM - 1) / (2 * BM)) * (GEMM_CL == 4 ? (num_n + 1) / 2 : num_n) *
+                        (p.split_k > 1 ? p.split_k : 1);
   const int sms = (p.num_sms > 0 ? p.num_sms : device_sm_count()) & ~(GEMM_CL - 1);
   const int grid = GEMM_CL * num_units < sms ? GEMM_CL * num_units : sms;
   OptMaps om{};
   if constexpr (tma_epi<EPI>()) {
-    if (!p.accumulate) {
+    if (!p.accumulate || p.split_k > 1) {
       constexpr bool f32 = EPI == Epi::kStoreF32 || EPI == Epi::kResidF32;
       om.c = f32 ? make_tmap_f32_2d(p.C, p.N, p.M, p.ldc, 32, 32)
                  : make_tmap_bf16_2d_rowswz(p.C, p.N, p.M, p.ldc, 32, 32);
@@ -1911,6 +1924,45 @@ bool gemv_ok(const GemmParams& p) {
 
 }  // namespace
 
+// Split-K for fp32-store weight-gradient GEMMs with too few 256 x 256 tiles for the CTA pairs
+// (the shards of tensor-parallel layers: 4096 x 512 at TP = 8 is 32 tiles for 74 pairs): the
+// slice count 1..8 whose units fill the pairs' waves best, with at least 8 k-blocks per slice.
+// SW_GEMM_SPLITK=0 disables; p.split_k > 0 forces.
+int choose_split_k(const GemmParams& p) {
+  if (p.split_k > 0) return p.split_k;
+  static const bool on = [] {
+    const char* e = std::getenv("SW_GEMM_SPLITK");
+    return !(e != nullptr && e[0] == '0');
+  }();
+  // weight-gradient layout only (both operands MN-major): the reduce-adds make the sum's order
+  // run-dependent, which the activation-gradient path (amplified through the attention
+  // backward) should not be
+  if (!on || !p.a_mn_major || !p.b_mn_major || p.bias != nullptr || p.alpha != 1.0f || gemv_ok(p) ||
+      gemv_tc_ok(p))
+    return 1;
+  const int tiles = ((p.M + 2 * BM - 1) / (2 * BM)) * ((p.N + BN - 1) / BN);
+  const int pairs = device_sm_count() / 2;
+  const int num_kb = (p.K + BK - 1) / BK;
+  if (tiles >= 2 * pairs) return 1;
+  int best = 1;
+  double best_eff = static_cast<double>(tiles) / (((tiles + pairs - 1) / pairs) * pairs);
+  for (int s = 2; s <= 8 && num_kb / s >= 8; ++s) {
+    const int units = tiles * s;
+    const double eff = static_cast<double>(units) / (((units + pairs - 1) / pairs) * pairs);
+    if (eff > best_eff + 0.05) {
+      best = s;
+      best_eff = eff;
+    }
+  }
+  return best;
+}
+
+int gemm_split_k(const GemmParams& p) {
+  GemmParams q = p;
+  q.epi = Epi::kStoreF32;
+  return use_pairs() && SW_EPI_TMA ? choose_split_k(q) : 1;
+}
+
 bool gemm_delta_ok(const GemmParams& p) {
   return SW_EPI_TMA && use_pairs() && !p.accumulate && p.aux != nullptr && p.delta != nullptr && p.delta_T > 0 &&
          p.M % p.delta_T == 0 && p.N % 128 == 0 && p.ld_aux % 8 == 0 && p.C2 == nullptr && !gemv_ok(p);
@@ -1949,6 +2001,18 @@ cudaError_t gemm_bf16(const GemmParams& p, cudaStream_t stream) {
       case Epi::kResidF32: return launch_gemv<Epi::kResidF32>(p, stream);
       case Epi::kSwiGLU: return launch_gemv<Epi::kSwiGLU>(p, stream);
       default: break;
+    }
+  }
+  if (p.epi == Epi::kStoreF32 && use_pairs() && SW_EPI_TMA) {
+    GemmParams q = p;
+    q.split_k = choose_split_k(p);
+    if (q.split_k > 1) {
+      if (!p.accumulate) {
+        const cudaError_t e = cudaMemset2DAsync(p.C, static_cast<size_t>(p.ldc) * 4, 0, static_cast<size_t>(p.N) * 4,
+                                                static_cast<size_t>(p.M), stream);
+        if (e != cudaSuccess) return e;
+      }
+      return launch<Epi::kStoreF32>(q, stream);
     }
   }
   switch (p.epi) {

@@ -877,7 +877,9 @@ __device__ __forceinline__ void adamw_one(float& p, float& m, float& v, float g,
 
 __global__ void adamw_kernel(float* __restrict__ p, float* __restrict__ m, float* __restrict__ v,
                              const float* __restrict__ g, bf16* __restrict__ shadow, int64_t n,
-                             float lr, float b1, float b2, float eps, float wd, float c1, float c2) {
+                             float lr, float b1, float b2, float eps, float wd, float c1, float c2,
+                             const int* __restrict__ gate) {
+  if (gate != nullptr && *gate != 0) return;  // a non-finite loss or gradient: state unchanged
   const int64_t n4 = n / 4;
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n4; i += stride) {
@@ -1263,8 +1265,8 @@ void add_residual_bias(const float* a, const bf16* b, const float* bias, float* 
 }
 
 void adamw(float* p, float* m, float* v, const float* g, bf16* shadow, int64_t n, float lr,
-           float b1, float b2, float eps, float wd, float c1, float c2, cudaStream_t s) {
-  adamw_kernel<<<grid_for(n / 4 + 1, 256), 256, 0, s>>>(p, m, v, g, shadow, n, lr, b1, b2, eps, wd, c1, c2);
+           float b1, float b2, float eps, float wd, float c1, float c2, cudaStream_t s, const int* gate) {
+  adamw_kernel<<<grid_for(n / 4 + 1, 256), 256, 0, s>>>(p, m, v, g, shadow, n, lr, b1, b2, eps, wd, c1, c2, gate);
 }
 
 void nonfinite_check(const float* x, int64_t n, int* flag, cudaStream_t s) {

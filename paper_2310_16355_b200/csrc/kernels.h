@@ -130,8 +130,10 @@ void add_residual_bias(const float* a, const bf16* b, const float* bias, float* 
 
 // AdamW over a flat shard (train_state.hpp:183-220, Scalar = float); also refreshes the bf16
 // shadow copy used by the GEMMs.
+// gate (optional): skip the update when *gate != 0 (read on the device)
 void adamw(float* p, float* m, float* v, const float* g, bf16* shadow, int64_t n, float lr,
-           float b1, float b2, float eps, float wd, float c1, float c2, cudaStream_t s);
+           float b1, float b2, float eps, float wd, float c1, float c2, cudaStream_t s,
+           const int* gate = nullptr);
 // flag[0] |= any non-finite among x[0..n)
 void nonfinite_check(const float* x, int64_t n, int* flag, cudaStream_t s);
 void scale_f32(float* x, int64_t n, float a, cudaStream_t s);

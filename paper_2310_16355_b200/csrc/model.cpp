@@ -1021,6 +1021,35 @@ void Model::wgrad(Rank& R, int slot, int M, int N, int K, const void* A, int64_t
          nullptr, 0, accumulate);
     return;
   }
+  {
+    // A weight with too few output tiles to fill the GPU (the shards of tensor-parallel layers):
+    // its gradient is split-K-reduced into G, checked, and the slot updated by the flat AdamW
+    // kernel, gated like the fused epilogue (same arithmetic, the flag read on the device)
+    GemmParams q;
+    q.M = M;
+    q.N = N;
+    q.K = K;
+    q.a_mn_major = 1;
+    q.b_mn_major = 1;
+    q.lda = lda;
+    q.ldb = ldb;
+    q.ldc = N;
+    static const bool split_on = [] {
+      const char* e = std::getenv("SW_WGRAD_SPLITK");
+      return !(e != nullptr && e[0] == '0');
+    }();
+    if (split_on && gemm_split_k(q) > 1) {
+      // the [M, N] gradient can span adjacent slots (the fused q|k|v or gate|up weights)
+      const Slot& s = slots_[slot];
+      const int64_t n = static_cast<int64_t>(M) * N;
+      gemm(R, M, N, K, A, lda, 1, B, ldb, 1, static_cast<int>(Epi::kStoreF32), G(R, slot), N);
+      k::nonfinite_check(G(R, slot), n, d_flag_, stream_);
+      k::adamw(P(R, slot), R.m + s.offset, R.v + s.offset, G(R, slot), W(R, slot), n, fused_->lr, fused_->b1,
+               fused_->b2, fused_->eps, fused_->wd, fused_->c1, fused_->c2, stream_, d_flag_);
+      launches_ += 2;
+      return;
+    }
+  }
   // optimizer in the epilogue: the gradient never leaves the accumulator
   GemmParams p;
   p.M = M;
