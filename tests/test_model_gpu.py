@@ -451,9 +451,9 @@ def test_side_stream_wgrads_match_single_stream(mp, monkeypatch):
     (SW_WGRAD_STREAM=0) at a size where the wgrads overlap the following dgrad / attention
     kernels (2 layers, M = 2048 tokens): forward_backward gradients and the parameters after a
     fused train_step. A missing join before gb / dpre / dqkv is rewritten would read a later
-    layer's values (O(1) relative error). The wgrad GEMMs are deterministic, but the attention
-    backward's dQ reduce-add is not, so the bound is its rounding noise: every gradient within
-    1e-5 rel-L2, and after one AdamW step (~lr * sign(g): an element whose gradient is at the
+    layer's values (O(1) relative error). The attention backward's dQ reduce-add (and split-K
+    weight gradients' slice order) are not deterministic, so the bound is their rounding noise:
+    every gradient within 1e-3 rel-L2, and after one AdamW step (~lr * sign(g): an element whose gradient is at the
     noise level may flip sign) at most 1% of a weight's elements differ, none by more than 2*lr."""
     text = open(os.path.join(SPECS, "llama7b.spec")).read()
     for a, b in (("n_layers = 32", "n_layers = 2"), ("d_model = 4096", "d_model = 1024"),
@@ -484,7 +484,9 @@ def test_side_stream_wgrads_match_single_stream(mp, monkeypatch):
         if n.endswith("attn/k/bias"):  # analytically zero gradient
             assert max_rel(res["1"][0][n], res["0"][0][n]) < 1e-6, n
         else:
-            assert rel_l2(res["1"][0][n], res["0"][0][n]) < 1e-5, n
+            # the dQ reduce-add noise reaches the embedding through every layer's residual
+            # gradient (seen up to 2.6e-4 once in ~20 runs); a missed join is O(1)
+            assert rel_l2(res["1"][0][n], res["0"][0][n]) < 1e-3, n
         a, b = res["1"][1][n], res["0"][1][n]
         d = np.abs(a - b)
         assert (d > 1e-6 + 1e-5 * np.abs(b)).mean() <= 1e-2 or n.endswith("attn/k/bias"), n
