@@ -1943,13 +1943,21 @@ int choose_split_k(const GemmParams& p) {
   const int tiles = ((p.M + 2 * BM - 1) / (2 * BM)) * ((p.N + BN - 1) / BN);
   const int pairs = device_sm_count() / 2;
   const int num_kb = (p.K + BK - 1) / BK;
-  if (tiles >= 2 * pairs) return 1;
+  static const int max_waves = [] {
+    const char* e = std::getenv("SW_GEMM_SPLITK_WAVES");
+    return e != nullptr ? std::atoi(e) : 2;
+  }();
+  static const double min_gain = [] {
+    const char* e = std::getenv("SW_GEMM_SPLITK_GAIN");
+    return e != nullptr ? std::atof(e) : 0.05;
+  }();
+  if (tiles >= max_waves * pairs) return 1;
   int best = 1;
   double best_eff = static_cast<double>(tiles) / (((tiles + pairs - 1) / pairs) * pairs);
   for (int s = 2; s <= 8 && num_kb / s >= 8; ++s) {
     const int units = tiles * s;
     const double eff = static_cast<double>(units) / (((units + pairs - 1) / pairs) * pairs);
-    if (eff > best_eff + 0.05) {
+    if (eff > best_eff + min_gain) {
       best = s;
       best_eff = eff;
     }
