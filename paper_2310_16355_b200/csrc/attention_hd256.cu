@@ -27,6 +27,7 @@
 //             fp32 dQ accumulator.                        TMEM: dK 256 | V 128 | S^T 64 | dP^T 64
 // The S^T / dP^T recompute of the second pass is the price of the budget (6 of the 5 + 1 tile
 // products); the dQ accumulator is converted to bf16 once per launch (attention_mma.cu).
+#include <type_traits>
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
@@ -504,17 +505,21 @@ __global__ void __launch_bounds__(256, 1)
       dev::tmem_ld_wait();
       const bool masked = qs < key0 + 128 || qs + BQB > T || key0 + 128 > T;
       const float2* nl2 = reinterpret_cast<const float2*>(st);
+      // masked / unmasked as separate straight-line loops (a branch per pair serialises the exps)
+      auto pmath = [&](auto kMask) {
 #pragma unroll
-      for (int e = 0; e < BQB / 2; ++e) {  // P^T = 2^(s * sl - lse * log2e)
-        const int qq = qs + 2 * e;
-        const float2 a = dev::ffma2(make_float2(__uint_as_float(v[2 * e]), __uint_as_float(v[2 * e + 1])), sl2, nl2[e]);
-        float p0 = dev::ex2_approx(a.x), p1 = dev::ex2_approx(a.y);
-        if (masked) {
-          p0 = (qq < T && key < T && qq >= key) ? p0 : 0.f;
-          p1 = (qq + 1 < T && key < T && qq + 1 >= key) ? p1 : 0.f;
+        for (int e = 0; e < BQB / 2; ++e) {  // P^T = 2^(s * sl - lse * log2e)
+          const int qq = qs + 2 * e;
+          const float2 a = dev::ffma2(make_float2(__uint_as_float(v[2 * e]), __uint_as_float(v[2 * e + 1])), sl2, nl2[e]);
+          float p0 = dev::ex2_approx(a.x), p1 = dev::ex2_approx(a.y);
+          if constexpr (decltype(kMask)::value) {
+            p0 = (qq < T && key < T && qq >= key) ? p0 : 0.f;
+            p1 = (qq + 1 < T && key < T && qq + 1 >= key) ? p1 : 0.f;
+          }
+          v[e] = dev::pack_bf16x2(p0, p1);
         }
-        v[e] = dev::pack_bf16x2(p0, p1);
-      }
+      };
+      if (masked) pmath(std::true_type{}); else pmath(std::false_type{});
       dev::tmem_st_32x32b_x32(tS, *reinterpret_cast<uint32_t(*)[32]>(v));
       dev::tmem_st_wait();
       dev::tc_fence_before();
@@ -724,19 +729,22 @@ __global__ void __launch_bounds__(384, 1)
       const bool masked = qs < key0 + 128 || qs + BQB > T || key0 + 128 > T;
       const float2* nl2 = reinterpret_cast<const float2*>(sStat);
       const float2* nd2 = reinterpret_cast<const float2*>(sStat + BQB);
+      auto dsmath = [&](auto kMask) {
 #pragma unroll
-      for (int e = 0; e < BQB / 2; ++e) {  // P = 2^(s sl - lse log2e), dS = P (dP - delta) scale
-        const int qq = qs + 2 * e;
-        const float2 a = dev::ffma2(make_float2(__uint_as_float(sv[2 * e]), __uint_as_float(sv[2 * e + 1])), sl2, nl2[e]);
-        float p0 = dev::ex2_approx(a.x), p1 = dev::ex2_approx(a.y);
-        if (masked) {
-          p0 = (qq < T && key < T && qq >= key) ? p0 : 0.f;
-          p1 = (qq + 1 < T && key < T && qq + 1 >= key) ? p1 : 0.f;
+        for (int e = 0; e < BQB / 2; ++e) {  // P = 2^(s sl - lse log2e), dS = P (dP - delta) scale
+          const int qq = qs + 2 * e;
+          const float2 a = dev::ffma2(make_float2(__uint_as_float(sv[2 * e]), __uint_as_float(sv[2 * e + 1])), sl2, nl2[e]);
+          float p0 = dev::ex2_approx(a.x), p1 = dev::ex2_approx(a.y);
+          if constexpr (decltype(kMask)::value) {
+            p0 = (qq < T && key < T && qq >= key) ? p0 : 0.f;
+            p1 = (qq + 1 < T && key < T && qq + 1 >= key) ? p1 : 0.f;
+          }
+          const float2 g = dev::ffma2(make_float2(__uint_as_float(pv[2 * e]), __uint_as_float(pv[2 * e + 1])), sc2, nd2[e]);
+          const float2 ds = dev::fmul2(make_float2(p0, p1), g);
+          sv[e] = dev::pack_bf16x2(ds.x, ds.y);
         }
-        const float2 g = dev::ffma2(make_float2(__uint_as_float(pv[2 * e]), __uint_as_float(pv[2 * e + 1])), sc2, nd2[e]);
-        const float2 ds = dev::fmul2(make_float2(p0, p1), g);
-        sv[e] = dev::pack_bf16x2(ds.x, ds.y);
-      }
+      };
+      if (masked) dsmath(std::true_type{}); else dsmath(std::false_type{});
       // dS^T_n: TMEM (A of dK, over the dP^T columns just read) and shared memory (B of dQ^T).
       // The shared tile was last read by dQ^T_{n-1} (complete before s_full of block n) and then
       // served as dQ_{n-1}'s staging: wait until TMA has read that

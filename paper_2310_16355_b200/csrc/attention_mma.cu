@@ -22,6 +22,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <type_traits>
 
 #include "kernels.h"
 #include "sm100.cuh"
@@ -1494,7 +1495,10 @@ __global__ void __launch_bounds__(512, 1)
   const uint32_t lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     ATTN_TR(4000);
-    if (static_cast<int>(blockIdx.x) == trace_cta) g_attn_trace[4001] = static_cast<unsigned long long>(nq);
+    if (static_cast<int>(blockIdx.x) == trace_cta) {
+      g_attn_trace[4001] = static_cast<unsigned long long>(nq);
+      for (int i = 0; i < 64; ++i) g_attn_trace[i * 16 + 15] = 0;
+    }
   }
   if (warp == 0 && lane == 0) {
     dev::tma_prefetch_desc(&tm_qkv64);
@@ -1676,32 +1680,41 @@ __global__ void __launch_bounds__(512, 1)
       const float4* nd4 = reinterpret_cast<const float4*>(st_del + wg * 32);
       const float2 sl2 = make_float2(scale_log2, scale_log2), sc2 = make_float2(scale, scale);
       uint32_t pk[16], dk[16];
+      // the bias and mask variants are separate straight-line copies of the loop: a branch per
+      // pair would split it into basic blocks and serialise each pair's exp2 latency
+      auto math = [&](auto kLut, auto kMask) {
 #pragma unroll
-      for (int g4 = 0; g4 < 8; ++g4) {  // 4 query columns per step: P = 2^(s*sl - lse), dS = P*(dP*sc - sc*delta)
-        const float4 nl = nl4[g4], nd = nd4[g4];
+        for (int g4 = 0; g4 < 8; ++g4) {  // 4 query columns per step: P = 2^(s*sl - lse), dS = P*(dP*sc - sc*delta)
+          const float4 nl = nl4[g4], nd = nd4[g4];
 #pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {
-          const int e = 2 * g4 + hh;
-          float2 a = dev::ffma2(make_float2(__uint_as_float(sv[2 * e]), __uint_as_float(sv[2 * e + 1])), sl2,
-                                hh ? make_float2(nl.z, nl.w) : make_float2(nl.x, nl.y));
-          if (lut_h) {  // + bias(key - query) in log2 units
-            // clamped: entries past the sequence end (masked below) must still load in bounds
-            const int bi = max(key + T - 1 - (qs + wg * 32 + 2 * e), 1);
-            const float b0 = key < T ? __ldg(lut_h + bi) : 0.f, b1 = key < T ? __ldg(lut_h + bi - 1) : 0.f;
-            a = dev::ffma2(make_float2(b0, b1), make_float2(1.4426950408889634f, 1.4426950408889634f), a);
+          for (int hh = 0; hh < 2; ++hh) {
+            const int e = 2 * g4 + hh;
+            float2 a = dev::ffma2(make_float2(__uint_as_float(sv[2 * e]), __uint_as_float(sv[2 * e + 1])), sl2,
+                                  hh ? make_float2(nl.z, nl.w) : make_float2(nl.x, nl.y));
+            if (decltype(kLut)::value && lut_h != nullptr) {  // + bias(key - query) in log2 units
+              // clamped: entries past the sequence end (masked below) must still load in bounds
+              const int bi = max(key + T - 1 - (qs + wg * 32 + 2 * e), 1);
+              const float b0 = key < T ? __ldg(lut_h + bi) : 0.f, b1 = key < T ? __ldg(lut_h + bi - 1) : 0.f;
+              a = dev::ffma2(make_float2(b0, b1), make_float2(1.4426950408889634f, 1.4426950408889634f), a);
+            }
+            float p0 = dev::ex2_approx(a.x), p1 = dev::ex2_approx(a.y);
+            if (decltype(kMask)::value && masked) {
+              const int qq = qs + wg * 32 + 2 * e;
+              p0 = (qq < T && key < Tk && (!causal || qq >= key)) ? p0 : 0.f;
+              p1 = (qq + 1 < T && key < Tk && (!causal || qq + 1 >= key)) ? p1 : 0.f;
+            }
+            const float2 t = dev::ffma2(make_float2(__uint_as_float(pv[2 * e]), __uint_as_float(pv[2 * e + 1])), sc2,
+                                        hh ? make_float2(nd.z, nd.w) : make_float2(nd.x, nd.y));
+            const float2 d = dev::fmul2(make_float2(p0, p1), t);
+            pk[e] = dev::pack_bf16x2(p0, p1);
+            dk[e] = dev::pack_bf16x2(d.x, d.y);
           }
-          float p0 = dev::ex2_approx(a.x), p1 = dev::ex2_approx(a.y);
-          if (masked) {
-            const int qq = qs + wg * 32 + 2 * e;
-            p0 = (qq < T && key < Tk && (!causal || qq >= key)) ? p0 : 0.f;
-            p1 = (qq + 1 < T && key < Tk && (!causal || qq + 1 >= key)) ? p1 : 0.f;
-          }
-          const float2 t = dev::ffma2(make_float2(__uint_as_float(pv[2 * e]), __uint_as_float(pv[2 * e + 1])), sc2,
-                                      hh ? make_float2(nd.z, nd.w) : make_float2(nd.x, nd.y));
-          const float2 d = dev::fmul2(make_float2(p0, p1), t);
-          pk[e] = dev::pack_bf16x2(p0, p1);
-          dk[e] = dev::pack_bf16x2(d.x, d.y);
         }
+      };
+      if (lut_h == nullptr && !masked) {
+        math(std::false_type{}, std::false_type{});
+      } else {
+        math(std::true_type{}, std::true_type{});  // both guards are exact no-ops when off
       }
       // sPt / sDSt were last read by block n-1's dV / dK / dQ MMAs
       if (lane == 0 && (warp == 4 || warp == 8) && n < 64) ATTN_TR(n * 16 + 5 + (warp == 8) * 5);
@@ -1729,6 +1742,8 @@ __global__ void __launch_bounds__(512, 1)
       dev::tc_fence_before();
       dev::mbar_arrive(p_full);
       if (lane == 0 && (warp == 4 || warp == 8) && n < 64) ATTN_TR(n * 16 + 7 + (warp == 8) * 5);
+      if (lane == 0 && n < 64 && static_cast<int>(blockIdx.x) == trace_cta)  // the last softmax warp's arrival
+        atomicMax(&g_attn_trace[n * 16 + 15], static_cast<unsigned long long>(clock64()));
     }
     // dK, dV (lane = key row) -> bf16 rows of dqkv; each warpgroup writes HD/2 columns
     dev::mbar_wait(mma_done, (nq - 1) & 1);

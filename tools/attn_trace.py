@@ -42,7 +42,7 @@ def main(B=4, T=2048, Hl=32, hd=128):
            "kv_full": rel(buf[4002]), "epilogue": rel(buf[4003]), "end": rel(buf[4004]), "blocks": []}
     for n in range(min(nq, 64)):
         b = [rel(buf[n * 16 + i]) for i in range(16)]
-        out["blocks"].append({"mma": [b[0], b[1], b[2]], "sm0": b[3:8], "sm1": b[8:13], "dq": [b[13], b[14]]})
+        out["blocks"].append({"mma": [b[0], b[1], b[2]], "sm0": b[3:8], "sm1": b[8:13], "dq": [b[13], b[14]], "p_full_last": b[15]})
     print(json.dumps(out))
 
 
