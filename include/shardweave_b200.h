@@ -330,10 +330,13 @@ SW_API sw_status sw_k_decode_attention(const void* qkv_new, void* cache, void* o
                                        int hd, int split, float* part, unsigned int* ticket, void* stream);
 SW_API sw_status sw_k_attention_fwd(const void* qkv, void* o, float* lse, int B, int T, int Hl,
                                     int hd, void* stream);
-/* dqkv [B*T, 3*Hl*hd] bf16; scratch fp32 of B*T*Hl + B*T*2*Hl*hd elements. */
+/* dqkv [B*T, 3*Hl*hd] bf16; scratch fp32 of sw_k_attention_bwd_scratch(B, T, Hl, hd) elements. */
 SW_API sw_status sw_k_attention_bwd(const void* qkv, const void* o, const float* lse,
                                     const void* dout, void* dqkv, float* scratch, int B, int T,
                                     int Hl, int hd, void* stream);
+/* fp32 elements of sw_k_attention_bwd's scratch (delta, and the fp32 dQ accumulator or, for
+ * head_dim 128 with T % 128 == 0, the dS^T tiles of the query-block dQ kernel). */
+SW_API long long sw_k_attention_bwd_scratch(int B, int T, int Hl, int hd);
 /* Debug/profiling only: 4096 clock64 stamps of the attention-backward CTA named by the
  * SW_ATTN_TRACE_CTA environment variable (slot map in tools/attn_trace.py). */
 SW_API sw_status sw_k_attention_trace(unsigned long long* out);

@@ -104,6 +104,8 @@ def _declare(L: C.CDLL) -> None:
     L.sw_k_decode_attention.argtypes = [vp, vp, vp] + [C.c_int] * 6 + [vp, vp, vp]
     L.sw_k_decode_attention.restype = C.c_int
     L.sw_k_attention_bwd.argtypes = [vp, vp, vp, vp, vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, vp]
+    L.sw_k_attention_bwd_scratch.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int]
+    L.sw_k_attention_bwd_scratch.restype = C.c_longlong
     L.sw_k_layernorm_fwd.argtypes = [vp, vp, vp, vp, vp, vp, i64, C.c_int, f32, vp]
     L.sw_k_layernorm_bwd.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, vp, i64, C.c_int, C.c_int, vp]
     L.sw_k_gemm_bf16_swiglu.argtypes = [C.c_int, C.c_int, C.c_int, vp, i64, vp, i64, vp, i64, vp, i64, vp]

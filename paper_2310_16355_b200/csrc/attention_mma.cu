@@ -82,6 +82,26 @@ int bwd_ts() {
   return v;
 }
 
+// SW_ATTN_DQ_EXT=0: dQ accumulated inside the key-block kernel (dQ^T = K^T dS^T per block, fp32
+// TMA reduce-adds into HBM) instead of the dS^T tiles written out for the query-block dQ kernel
+int bwd_dq_ext() {
+  static const int v = [] {
+    const char* e = std::getenv("SW_ATTN_DQ_EXT");
+    return e != nullptr ? std::atoi(e) : 1;
+  }();
+  return v;
+}
+
+// dS^T tiles of the causal backward for the dQ kernel: per (batch*head), key block kb holds the
+// 64-query chunks n = 0 .. (T - 128 kb) / 64 - 1 (queries 128 kb + 64 n ..), each a [128 keys x
+// 64 queries] bf16 SW128 image (16 KiB, the shared-memory layout the MMA reads). Chunk index:
+__host__ __device__ __forceinline__ int64_t ds_chunks_before(int kb, int T) {
+  return static_cast<int64_t>(kb) * (T / 64) - static_cast<int64_t>(kb) * (kb - 1);
+}
+__host__ __device__ __forceinline__ int64_t ds_chunk(int bh, int kb, int n, int T) {
+  return static_cast<int64_t>(bh) * ds_chunks_before(T / 128, T) + ds_chunks_before(kb, T) + n;
+}
+
 int bwd_dq_first() {
   static const int v = [] {
     const char* e = std::getenv("SW_ATTN_BWD_DQ_FIRST");
@@ -1448,7 +1468,11 @@ __global__ void __launch_bounds__(512, 1)
                  int Hl, float scale_log2, float scale, int nbh, int group, int trace_cta, int dq_first, int ts,
                  int causal, const float* __restrict__ lut, float* __restrict__ dlut,
                  float* __restrict__ colsum, int Tk, int kcol, int vcol, bf16* __restrict__ dkv, int64_t ld_dkv,
-                 int dvoff) {
+                 int dvoff, uint8_t* __restrict__ ds_out) {
+  // ds_out != nullptr (causal self-attention, ts, T % 128 == 0): dQ is not formed here; the dQ
+  // warpgroup copies each block's dS^T (bf16, from the dP^T columns of tensor memory) to its
+  // ds_chunk() tile for attn_bwd_dq, so the dQ^T MMA, the dS^T shared-memory tile and the fp32
+  // dQ staging leave this kernel
   // T queries (tm_qkv64 / tm_do64 / tm_dq rows b*T), Tk keys (tm_qkv128 rows b*Tk, k at kcol,
   // v at vcol); dK / dV rows go to dkv (row pitch ld_dkv, dV at +dvoff). Self-attention: Tk == T,
   // kcol = Dl, vcol = 2 Dl, dkv = dqkv + Dl, ld_dkv = 3 Dl, dvoff = Dl.
@@ -1609,10 +1633,12 @@ __global__ void __launch_bounds__(512, 1)
 #pragma unroll
             for (int kk = 0; kk < BQ2 / 16; ++kk)
               dev::umma_f16_ts(t_dk, t_dp + st * BQ2 + kk * 8, q_mn + mn(kk), id_kv, (n > 0 || kk > 0) ? 1u : 0u);
+            if (ds_out == nullptr) {
 #pragma unroll
-            for (int kk = 0; kk < 128 / 16; ++kk)
-              dev::umma_f16_ss(t_s + st * BQ2, dK_mn + mn(kk), dDSt_mn + mn(kk), id_dq, kk > 0 ? 1u : 0u);
-            dev::umma_commit(&dq_full[st]);
+              for (int kk = 0; kk < 128 / 16; ++kk)
+                dev::umma_f16_ss(t_s + st * BQ2, dK_mn + mn(kk), dDSt_mn + mn(kk), id_dq, kk > 0 ? 1u : 0u);
+            }
+            dev::umma_commit(&dq_full[st]);  // ds_out: dV / dK have read P^T / dS^T
           } else {
           // dQ^T first (default): its TMEM drain (dQ warpgroup) then overlaps dV / dK, so the S
           // buffer it occupies is free again by the time S_{n+2} is issued
@@ -1727,9 +1753,11 @@ __global__ void __launch_bounds__(512, 1)
         // memory as the B operand of dQ^T
         dev::tmem_st_32x32b_x16(t_s + lane_base + st * BQ2 + wg * 16, pk);
         dev::tmem_st_32x32b_x16(t_dp + lane_base + st * BQ2 + wg * 16, dk);
+        if (ds_out == nullptr) {
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
-          dev::st_sw128(sDSt, 128, t, 0, wg * 4 + u, make_uint4(dk[4 * u], dk[4 * u + 1], dk[4 * u + 2], dk[4 * u + 3]));
+          for (int u = 0; u < 4; ++u)
+            dev::st_sw128(sDSt, 128, t, 0, wg * 4 + u, make_uint4(dk[4 * u], dk[4 * u + 1], dk[4 * u + 2], dk[4 * u + 3]));
+        }
         dev::tmem_st_wait();
       } else {
 #pragma unroll
@@ -1804,7 +1832,34 @@ __global__ void __launch_bounds__(512, 1)
     if (dlut) {
       for (int i = tq; i < T + 128; i += 128) sAcc[i] = 0.f;
     }
-    for (int n = 0; n < nq; ++n) {
+    if (ds_out != nullptr) {
+      // dS^T_n (bf16 pairs in the first 32 columns of dP^T_n, lane = key row) -> SW128 image in
+      // the (otherwise unused) dQ staging buffer, 2 x 16 KiB -> one bulk store per block
+      const int tk = static_cast<int>(warp & 3) * 32 + static_cast<int>(lane);
+      for (int n = 0; n < nq; ++n) {
+        const int st = n & 1;
+        dev::mbar_wait(&dq_full[st], (n >> 1) & 1);
+        dev::tc_fence_after();
+        uint32_t r[32];
+        dev::tmem_ld_32x32b_x32(t_dp + lane_base + st * BQ2, r);
+        dev::tmem_ld_wait();
+        dev::tc_fence_before();
+        dev::mbar_arrive(&s_free[st]);
+        uint8_t* stg = sDQ + st * (BQ2 * 256);
+        if (leader && n >= 2) dev::bulk_wait_read_1();  // block n-2's store has read this buffer
+        asm volatile("bar.sync 2, 128;" ::: "memory");
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          dev::st_sw128(stg, 128, tk, 0, u, make_uint4(r[4 * u], r[4 * u + 1], r[4 * u + 2], r[4 * u + 3]));
+        dev::fence_proxy_async_smem();
+        asm volatile("bar.sync 2, 128;" ::: "memory");
+        if (leader) {
+          dev::bulk_store(ds_out + ds_chunk(bh, kb, n, T) * (BQ2 * 256), stg, BQ2 * 256);
+          dev::bulk_commit();
+        }
+      }
+    }
+    for (int n = 0; n < (ds_out != nullptr ? 0 : nq); ++n) {
       const int st = n & 1;
       const int qs = qbase + n * BQ2;
       dev::mbar_wait(&dq_full[st], (n >> 1) & 1);
@@ -1868,6 +1923,127 @@ __global__ void __launch_bounds__(512, 1)
   if (warp == 2) {
     dev::tc_fence_after();
     dev::tmem_dealloc<512>(tmem);
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// dQ of the causal backward (head_dim 128), one CTA per (128-query tile, batch*head), heaviest
+// tiles first: dQ = sum over key blocks kb <= qi of dS_(qi,kb) K_kb, accumulated in tensor memory
+// (fp32, lane = query) in key order, so dQ is deterministic and never round-trips HBM in fp32.
+//   warp 0      loads 64-key steps into a 3-stage ring: the two [64 keys x 64 queries] halves of
+//               the dS^T tile (bulk copies of attn_bwd_tc2's SW128 images) and K [64 keys x 128]
+//               (TMA, two 64-column boxes)
+//   warp 1      MMA: D[128 q x 128 d] += dS (A, MN-major) K (B, MN-major), 4 k steps per stage
+//   warps 2-5   epilogue: bf16 q columns of dqkv + the q bias gradient's per-32-row partials
+// ---------------------------------------------------------------------------------------------
+constexpr int DQ_STAGES = 3;
+constexpr int DQ_STAGE = 32768;
+constexpr int DQ_SMEM = DQ_STAGES * DQ_STAGE + 1024 + 128;
+
+__global__ void __launch_bounds__(192, 2)
+    attn_bwd_dq(const __grid_constant__ CUtensorMap tm_qkv64, const uint8_t* __restrict__ ds, bf16* __restrict__ dqkv,
+                float* __restrict__ colsum, int T, int Hl, int nbh, int group) {
+  constexpr int HD = 128;
+  extern __shared__ uint8_t dq_smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(dq_smem_raw) + 1023) &
+                                           ~static_cast<uintptr_t>(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + DQ_STAGES * DQ_STAGE);
+  uint64_t* empty = full + DQ_STAGES;
+  uint64_t* tfull = empty + DQ_STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
+  const int nb = T / 128;
+  int unit, bh;
+  work_item(static_cast<int>(blockIdx.x), nb, nbh, group, unit, bh);
+  const int qi = nb - 1 - unit;  // unit 0 = the last query tile (most key blocks)
+  const int b = bh / Hl, h = bh % Hl;
+  const int Dl = Hl * HD;
+  const int row0 = b * T;
+  const int nsteps = 2 * (qi + 1);
+  const uint32_t warp = dev::warp_idx_sync();
+  const uint32_t lane = threadIdx.x & 31;
+  if (warp == 0 && lane == 0) {
+    dev::tma_prefetch_desc(&tm_qkv64);
+    for (int i = 0; i < DQ_STAGES; ++i) {
+      dev::mbar_init(&full[i], 1);
+      dev::mbar_init(&empty[i], 1);
+    }
+    dev::mbar_init(tfull, 1);
+    dev::fence_barrier_init();
+  }
+  if (warp == 2) dev::tmem_alloc<128>(tmem_slot);
+  dev::tc_fence_before();
+  __syncthreads();
+  dev::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int s = 0; s < nsteps; ++s) {
+        const int st = s % DQ_STAGES, kb = s >> 1, half = s & 1;
+        dev::mbar_wait(&empty[st], ((s / DQ_STAGES) & 1) ^ 1);
+        dev::mbar_arrive_expect_tx(&full[st], DQ_STAGE);
+        uint8_t* dst = sm + st * DQ_STAGE;
+        // queries of tile qi = chunks 2 (qi - kb) and 2 (qi - kb) + 1 of key block kb
+        const uint8_t* src = ds + ds_chunk(bh, kb, 2 * (qi - kb), T) * 16384 + half * 8192;
+        dev::bulk_load(dst, src, 8192, &full[st]);
+        dev::bulk_load(dst + 8192, src + 16384, 8192, &full[st]);
+        const int krow = row0 + kb * 128 + half * 64;
+        dev::tma_load_2d(dst + 16384, &tm_qkv64, &full[st], Dl + h * HD, krow);
+        dev::tma_load_2d(dst + 24576, &tm_qkv64, &full[st], Dl + h * HD + 64, krow);
+      }
+    }
+  } else if (warp == 1) {
+    const uint32_t idesc = dev::make_idesc_bf16(128, HD, 1, 1);
+    for (int s = 0; s < nsteps; ++s) {
+      const int st = s % DQ_STAGES;
+      dev::mbar_wait(&full[st], (s / DQ_STAGES) & 1);
+      dev::tc_fence_after();
+      const uint32_t a = dev::smem_u32(sm + st * DQ_STAGE);
+      if (dev::elect_one_sync()) {
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          dev::umma_f16_ss(tmem, dev::make_sdesc_sw128(a + kk * 2048, 8192, 1024),
+                           dev::make_sdesc_sw128(a + 16384 + kk * 2048, 8192, 1024), idesc,
+                           (s > 0 || kk > 0) ? 1u : 0u);
+        dev::umma_commit(&empty[st]);
+        if (s == nsteps - 1) dev::umma_commit(tfull);
+      }
+      __syncwarp();
+    }
+  } else {
+    const uint32_t q = warp & 3;  // TMEM lane quarter of this warp
+    const int r32 = qi * 128 + static_cast<int>(q) * 32;  // first query of the warp's 32 rows
+    dev::mbar_wait(tfull, 0);
+    dev::tc_fence_after();
+    bf16* out = dqkv + static_cast<int64_t>(row0 + r32 + static_cast<int>(lane)) * 3 * Dl + h * HD;
+#pragma unroll 1
+    for (int c = 0; c < HD / 32; ++c) {
+      uint32_t v[32];
+      dev::tmem_ld_32x32b_x32(tmem + ((q * 32) << 16) + c * 32, v);
+      dev::tmem_ld_wait();
+      uint32_t w[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) w[i] = dev::pack_bf16x2(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1]));
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        *reinterpret_cast<uint4*>(out + c * 32 + 8 * u) = make_uint4(w[4 * u], w[4 * u + 1], w[4 * u + 2], w[4 * u + 3]);
+      if (colsum != nullptr) {  // q bias gradient: column sums of the rounded values over the 32 rows
+        float x[32];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const float2 f = dev::unpack_bf16x2(w[i]);
+          x[2 * i] = f.x;
+          x[2 * i + 1] = f.y;
+        }
+        const float sum = warp_colsum32(x, lane);
+        colsum[static_cast<int64_t>((row0 + r32) >> 5) * (3LL * Dl) + h * HD + c * 32 + lane] = sum;
+      }
+    }
+  }
+  dev::tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    dev::tc_fence_after();
+    dev::tmem_dealloc<128>(tmem);
   }
 }
 
@@ -1992,12 +2168,13 @@ bool launch_bwd2(const bf16* qkv, const bf16* o, const float* lse, const bf16* d
                  float* dlut = nullptr, float scale_arg = 0.f, bool delta_ready = false,
                  float* colsum = nullptr, bool* colsum_done = nullptr, const bf16* kv = nullptr, int Tk = 0,
                  int64_t ldq = 0, int64_t ldkv = 0, int voff = 0, bf16* dkv = nullptr, int64_t ld_dq = 0,
-                 int64_t ld_dkv = 0) {
+                 int64_t ld_dkv = 0, bool allow_ds = false) {
   constexpr int HD = 128;
   static bool configured = false;
   if (!configured) {
     if (cudaFuncSetAttribute(attn_bwd_tc2, cudaFuncAttributeMaxDynamicSharedMemorySize, Bwd2Layout::BYTES) !=
-        cudaSuccess) {
+            cudaSuccess ||
+        cudaFuncSetAttribute(attn_bwd_dq, cudaFuncAttributeMaxDynamicSharedMemorySize, DQ_SMEM) != cudaSuccess) {
       return false;
     }
     configured = true;
@@ -2006,7 +2183,12 @@ bool launch_bwd2(const bf16* qkv, const bf16* o, const float* lse, const bf16* d
   const int64_t M = static_cast<int64_t>(B) * T;
   float* delta = scratch;
   float* dq = scratch + ((M * Hl + 63) / 64) * 64;
-  cudaMemsetAsync(dq, 0, sizeof(float) * M * Dl, s);
+  // the decoder's causal self-attention: dS^T tiles out, dQ from attn_bwd_dq (scratch sized by
+  // attention_bwd_scratch_floats)
+  const bool ext = allow_ds && kv == nullptr && causal && lut == nullptr && dlut == nullptr && T % 128 == 0 &&
+                   bwd_ts() && bwd_dq_ext();
+  uint8_t* ds = ext ? reinterpret_cast<uint8_t*>(dq) : nullptr;
+  if (!ext) cudaMemsetAsync(dq, 0, sizeof(float) * M * Dl, s);
   if (!delta_ready) launch_delta(o, dout, delta, T, Hl, HD, M, s);
   const bool cross = kv != nullptr;
   const CUtensorMap tm_qkv64 =
@@ -2029,8 +2211,10 @@ bool launch_bwd2(const bf16* qkv, const bf16* o, const float* lse, const bf16* d
       tm_qkv64, tm_qkv128, tm_do64, tm_dq, lse, delta, dqkv, T, Hl, static_cast<float>(scale * 1.4426950408889634),
       static_cast<float>(scale), B * Hl, work_group(), trace_cta(), bwd_dq_first(), (lut || dlut) ? 1 : bwd_ts(),
       causal, lut, dlut, cs, cross ? Tk : T, cross ? 0 : Dl, cross ? voff : 2 * Dl, cross ? dkv : dqkv + Dl,
-      cross ? ld_dkv : 3LL * Dl, cross ? voff : Dl);
-  if (cs != nullptr) {
+      cross ? ld_dkv : 3LL * Dl, cross ? voff : Dl, ds);
+  if (ext) {
+    attn_bwd_dq<<<nb * B * Hl, 192, DQ_SMEM, s>>>(tm_qkv64, ds, dqkv, cs, T, Hl, B * Hl, work_group());
+  } else if (cs != nullptr) {
     dq_to_bf16_colsum<<<dim3(static_cast<unsigned>((M + 31) / 32), (Dl + 1023) / 1024), 256, 0, s>>>(dq, dqkv, M, Dl,
                                                                                                       cs);
   } else {
@@ -2045,7 +2229,7 @@ bool launch_bwd(const bf16* qkv, const bf16* o, const float* lse, const bf16* do
                 int B, int T, int Hl, cudaStream_t s, bool delta_ready, float* colsum, bool* colsum_done) {
   if (HD == 128 && bwd2_enabled())
     return launch_bwd2(qkv, o, lse, dout, dqkv, scratch, B, T, Hl, s, 1, nullptr, nullptr, 0.f, delta_ready, colsum,
-                       colsum_done);
+                       colsum_done, nullptr, 0, 0, 0, 0, nullptr, 0, 0, true);
   using Lay = BwdLayout<HD>;
   static bool configured = false;
   if (!configured) {
@@ -2141,6 +2325,16 @@ bool attention_mma_bwd_ex(const bf16* qkv, const bf16* o, const float* lse, cons
   if (hd != 128 || ((Hl * hd) % 8) != 0 || ((lut || dlut) && T + 128 > Bwd2Layout::PT / 4) || !bwd2_enabled())
     return false;
   return launch_bwd2(qkv, o, lse, dout, dqkv, scratch, B, T, Hl, s, causal, lut, dlut, scale);
+}
+
+int64_t attention_bwd_scratch_floats(int B, int T, int Hl, int hd) {
+  const int64_t M = static_cast<int64_t>(B) * T;
+  int64_t n = M * Hl + 2 * M * Hl * hd + 64;
+  if (hd == 128 && T % 128 == 0) {  // delta + the dS^T tiles of attn_bwd_dq
+    const int64_t ds = static_cast<int64_t>(B) * Hl * ds_chunks_before(T / 128, T) * (16384 / 4);
+    n = std::max(n, (M * Hl + 63) / 64 * 64 + ds);
+  }
+  return n;
 }
 
 bool attention_mma_bwd(const bf16* qkv, const bf16* o, const float* lse, const bf16* dout, bf16* dqkv,

@@ -174,6 +174,10 @@ sw_status sw_k_attention_bwd(const void* qkv, const void* o, const float* lse, c
   });
 }
 
+long long sw_k_attention_bwd_scratch(int B, int T, int Hl, int hd) {
+  return static_cast<long long>(sw::k::attention_bwd_scratch_floats(B, T, Hl, hd));
+}
+
 sw_status sw_k_gemm_trace(unsigned long long* out) {
   return sw::guarded([&] { sw::gemm_trace_read(out); });
 }

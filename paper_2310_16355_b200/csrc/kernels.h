@@ -113,11 +113,13 @@ void loss_reduce(const float* wloss, int64_t M, const float* wsum, double* loss,
 void attention_trace_read(unsigned long long* out);
 void attention_fwd(const bf16* qkv, bf16* o, float* lse, int B, int T, int Hl, int hd,
                    cudaStream_t s);
-// dqkv [M, 3*Dl]; scratch: fp32 [B*Hl*T] (delta) + fp32 [M, 3*Dl] (dk/dv accumulators).
+// dqkv [M, 3*Dl]; scratch: attention_bwd_scratch_floats(B, T, Hl, hd) fp32 elements (delta, and
+// the fp32 dQ accumulator or, for head_dim 128 with T % 128 == 0, the dS^T tiles of the dQ kernel).
 // delta_ready: scratch already holds delta = rowsum(dO * O) (written by the dO GEMM's kBf16Delta
 // epilogue), so the tcgen05 path skips its delta pass.
 // colsum (optional, [M / 32][3*Dl] fp32): the q|k|v bias gradients' per-32-row column partials
 // of dqkv, written when *colsum_done comes back true (reduce with colsum_chunks).
+int64_t attention_bwd_scratch_floats(int B, int T, int Hl, int hd);
 void attention_bwd(const bf16* qkv, const bf16* o, const float* lse, const bf16* dout, bf16* dqkv,
                    float* scratch, int B, int T, int Hl, int hd, cudaStream_t s, bool delta_ready = false,
                    float* colsum = nullptr, bool* colsum_done = nullptr);

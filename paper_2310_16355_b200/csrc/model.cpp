@@ -383,7 +383,8 @@ void Model::allocate() {
       R.col_scratch = alloc<float>(std::max(chunks * widest, ((M + 31) / 32) * std::max<int64_t>(fl_, 3 * dl_)));
       R.ln_partials = alloc<float>(k::layernorm_bwd_partials(d_));
       R.tok_keys = alloc<uint32_t>(k::embed_bwd_keys(M_));
-      R.attn_scratch = alloc<float>(M * hl_ + M * 2 * dl_ + 64);
+      R.attn_scratch = alloc<float>(std::max<int64_t>(M * hl_ + M * 2 * dl_ + 64,
+                                                      k::attention_bwd_scratch_floats(B_, T_, hl_, hd_)));
     }
     ranks_.push_back(R);
   }

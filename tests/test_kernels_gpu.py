@@ -52,7 +52,7 @@ def test_attention_fwd_bwd(B, T, Hl, hd):
     # backward vs autograd through the fp32 reference on the same bf16 inputs
     dout = torch.randn(B * T, Dl, generator=g, device=DEV).bfloat16()
     dqkv = torch.empty_like(qkv)
-    scratch = torch.empty(B * T * Hl + B * T * 2 * Dl, device=DEV)
+    scratch = torch.empty(L.sw_k_attention_bwd_scratch(B, T, Hl, hd), device=DEV)
     _lib.check(L.sw_k_attention_bwd(qkv.data_ptr(), o.data_ptr(), lse.data_ptr(), dout.data_ptr(),
                                     dqkv.data_ptr(), scratch.data_ptr(), B, T, Hl, hd, None))
     torch.cuda.synchronize()

@@ -24,7 +24,7 @@ def main(B=4, T=2048, Hl=32, hd=128):
     lse = torch.empty(B, Hl, T, device="cuda")
     dout = torch.randn(B * T, Dl, generator=g, device="cuda").bfloat16()
     dqkv = torch.empty_like(qkv)
-    scratch = torch.empty(B * T * Hl + B * T * 2 * Dl + B * T * Dl, device="cuda")
+    scratch = torch.empty(L.sw_k_attention_bwd_scratch(B, T, Hl, hd), device="cuda")
     s = torch.cuda.current_stream().cuda_stream
     _lib.check(L.sw_k_attention_fwd(qkv.data_ptr(), o.data_ptr(), lse.data_ptr(), B, T, Hl, hd, s))
     for _ in range(3):
