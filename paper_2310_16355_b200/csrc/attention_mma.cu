@@ -1498,6 +1498,7 @@ __global__ void __launch_bounds__(512, 1)
   uint64_t* dq_full = bars + 13;   // [2]  dQ^T_n is in S^T buffer n & 1
   uint64_t* ds_read = bars + 15;   // the dQ warpgroup has read dS^T_n for the bias gradient
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
+  uint64_t* acc_done = bars + 17;  // every MMA of the CTA complete: dV / dK final
 
   const int nb = (Tk + 127) / 128;
   int kb, bh;
@@ -1542,6 +1543,7 @@ __global__ void __launch_bounds__(512, 1)
     dev::mbar_init(p_full, 256);
     dev::mbar_init(ds_read, 128);
     dev::mbar_init(mma_done, 1);
+    dev::mbar_init(acc_done, 1);
     dev::fence_barrier_init();
   }
   if (warp == 2) dev::tmem_alloc<512>(tmem_slot);
@@ -1663,6 +1665,7 @@ __global__ void __launch_bounds__(512, 1)
           }
           dev::umma_commit(mma_done);
           dev::umma_commit(&qdo_empty[qst]);
+          if (n == nq - 1) dev::umma_commit(acc_done);
         }
         __syncwarp();
       }
@@ -1744,7 +1747,9 @@ __global__ void __launch_bounds__(512, 1)
       }
       // sPt / sDSt were last read by block n-1's dV / dK / dQ MMAs
       if (lane == 0 && (warp == 4 || warp == 8) && n < 64) ATTN_TR(n * 16 + 5 + (warp == 8) * 5);
-      if (n >= 1) dev::mbar_wait(mma_done, (n - 1) & 1);
+      // (ts with ds_out writes no shared-memory tile here: P^T / dS^T go to this block's own TMEM
+      // columns, so nothing waits for block n-1's MMAs)
+      if (n >= 1 && !(ts && ds_out != nullptr)) dev::mbar_wait(mma_done, (n - 1) & 1);
       if (dlut && n >= 1) dev::mbar_wait(ds_read, (n - 1) & 1);  // bias-gradient reads of dS^T_{n-1}
       if (lane == 0 && (warp == 4 || warp == 8) && n < 64) ATTN_TR(n * 16 + 6 + (warp == 8) * 5);
       if (ts) {
@@ -1774,7 +1779,7 @@ __global__ void __launch_bounds__(512, 1)
         atomicMax(&g_attn_trace[n * 16 + 15], static_cast<unsigned long long>(clock64()));
     }
     // dK, dV (lane = key row) -> bf16 rows of dqkv; each warpgroup writes HD/2 columns
-    dev::mbar_wait(mma_done, (nq - 1) & 1);
+    dev::mbar_wait(acc_done, 0);
     dev::tc_fence_after();
     if (lane == 0 && warp == 4) ATTN_TR(4003);
     bf16* dk_row = dkv + (static_cast<int64_t>(row0k) + key) * ld_dkv + h * HD;
