@@ -1926,8 +1926,11 @@ bool gemv_ok(const GemmParams& p) {
 
 // Split-K for fp32-store weight-gradient GEMMs with too few 256 x 256 tiles for the CTA pairs
 // (the shards of tensor-parallel layers: 4096 x 512 at TP = 8 is 32 tiles for 74 pairs): the
-// slice count 1..8 whose units fill the pairs' waves best, with at least 8 k-blocks per slice.
-// SW_GEMM_SPLITK=0 disables; p.split_k > 0 forces.
+// slice count whose units fill the pairs' waves best, with at least 8 k-blocks per slice. At
+// most 2 slices by default (SW_GEMM_SPLITK_MAX): two reduce-adds onto the zeroed output commute
+// (0 + a + b == 0 + b + a), so the result stays bitwise deterministic; 3+ slices measured only
+// 0-2.5% faster on the TP = 8 shapes. Not when accumulating into C (C + a + b would depend on the
+// order). SW_GEMM_SPLITK=0 disables; p.split_k > 0 forces.
 int choose_split_k(const GemmParams& p) {
   if (p.split_k > 0) return p.split_k;
   static const bool on = [] {
@@ -1937,7 +1940,7 @@ int choose_split_k(const GemmParams& p) {
   // weight-gradient layout only (both operands MN-major): the reduce-adds make the sum's order
   // run-dependent, which the activation-gradient path (amplified through the attention
   // backward) should not be
-  if (!on || !p.a_mn_major || !p.b_mn_major || p.bias != nullptr || p.alpha != 1.0f || gemv_ok(p) ||
+  if (!on || p.accumulate || !p.a_mn_major || !p.b_mn_major || p.bias != nullptr || p.alpha != 1.0f || gemv_ok(p) ||
       gemv_tc_ok(p))
     return 1;
   const int tiles = ((p.M + 2 * BM - 1) / (2 * BM)) * ((p.N + BN - 1) / BN);
@@ -1951,10 +1954,14 @@ int choose_split_k(const GemmParams& p) {
     const char* e = std::getenv("SW_GEMM_SPLITK_GAIN");
     return e != nullptr ? std::atof(e) : 0.05;
   }();
+  static const int max_split = [] {
+    const char* e = std::getenv("SW_GEMM_SPLITK_MAX");
+    return e != nullptr ? std::max(1, std::min(8, std::atoi(e))) : 2;
+  }();
   if (tiles >= max_waves * pairs) return 1;
   int best = 1;
   double best_eff = static_cast<double>(tiles) / (((tiles + pairs - 1) / pairs) * pairs);
-  for (int s = 2; s <= 8 && num_kb / s >= 8; ++s) {
+  for (int s = 2; s <= max_split && num_kb / s >= 8; ++s) {
     const int units = tiles * s;
     const double eff = static_cast<double>(units) / (((units + pairs - 1) / pairs) * pairs);
     if (eff > best_eff + min_gain) {

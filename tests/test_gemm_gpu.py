@@ -57,14 +57,15 @@ def test_gemm_layouts_f32(M, N, K, a_mn, b_mn):
 def test_gemm_split_k_f32(M, N, K, a_mn, b_mn, acc):
     """fp32-store weight-gradient GEMMs with too few 256 x 256 tiles for the GPU (the TP = 8
     shards) run split-K: K slices reduce-added into C by TMA (C zeroed first, or accumulated
-    into)."""
+    into; accumulating GEMMs stay unsplit). The bound is fp32 summation noise over K = 16384
+    (an unsplit 16384-deep accumulation measured 1.9e-5); a lost or doubled slice is O(1)."""
     gen = torch.Generator(device=DEV).manual_seed(M + N + K + acc)
     A, B, ref = _ref_operands(M, N, K, a_mn, b_mn, gen)
     C0 = torch.randn(M, N, generator=gen, device=DEV) if acc else torch.full((M, N), float("nan"), device=DEV)
     C = C0.clone()
     _gemm(A, a_mn, B, b_mn, M, N, K, 1, C, acc=acc)
     want = ref + (C0 if acc else 0)
-    assert _rel(C, want) < 1e-5
+    assert _rel(C, want) < 5e-5
 
 
 @pytest.mark.parametrize("M,N,K", [(384, 768, 512), (4096, 4096, 4096)])

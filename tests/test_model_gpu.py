@@ -446,6 +446,47 @@ def test_fused_bias_colsums_match_separate_pass(mp, monkeypatch):
 
 
 @pytest.mark.parametrize("mp", [1, 2])
+def test_step_bitwise_reproducible(mp, monkeypatch):
+    """With head_dim 128 causal attention (dQ summed in key order by the query-block kernel),
+    GEMMs that split K into at most two slices (two adds onto zero commute), and fixed-order
+    bias / LayerNorm / embedding reductions, the training step is bitwise reproducible: two
+    runs of forward_backward + a fused train_step from the same state, with the weight
+    gradients on the side stream or on the main stream, give identical gradients, parameters
+    and losses (2 layers at d = 1024, 2 x 1024 tokens: the q|k|v weight gradient splits K)."""
+    text = open(os.path.join(SPECS, "llama7b.spec")).read()
+    for a, b in (("n_layers = 32", "n_layers = 2"), ("d_model = 4096", "d_model = 1024"),
+                 ("n_heads = 32", "n_heads = 8"), ("d_ff = 11008", "d_ff = 2752"), ("vocab_size = 32000", "vocab_size = 4096")):
+        text = text.replace(a, b)
+    spec = rules.parse_model_spec(text)
+    rng = np.random.default_rng(5)
+    tokens = rng.integers(0, spec.vocab_size, (2, 1024), dtype=np.int32)
+    targets = rng.integers(0, spec.vocab_size, (2, 1024), dtype=np.int32)
+    names = [n for n, _ in rules.transformer_param_shapes(spec)]
+    cfg = engine.AdamWConfig(lr=1e-3, weight_decay=0.01)
+    runs = []
+    for side in ("1", "1", "0"):
+        monkeypatch.setenv("SW_WGRAD_STREAM", side)
+        model, mesh, _ = make(spec, 1, mp, 2, 1024)
+        model.init_params(42, "model-init")
+        model.stage_batch(tokens, targets, None)
+        model.forward_backward()
+        grads = {n: model.get_grad(n) for n in names}
+        loss0 = model.loss()
+        model.stage_batch(tokens, targets, None)
+        model.train_step(cfg)
+        model.stage_batch(tokens, targets, None)
+        model.train_step(cfg)
+        runs.append((grads, {n: model.get_param(n) for n in names}, loss0, model.loss()))
+        model.close()
+        mesh.close()
+    for other in runs[1:]:
+        assert other[2] == runs[0][2] and other[3] == runs[0][3]
+        for n in names:
+            assert np.array_equal(other[0][n], runs[0][0][n]), n
+            assert np.array_equal(other[1][n], runs[0][1][n]), n
+
+
+@pytest.mark.parametrize("mp", [1, 2])
 def test_side_stream_wgrads_match_single_stream(mp, monkeypatch):
     """The weight-gradient GEMMs on the side stream (default) against the single-stream schedule
     (SW_WGRAD_STREAM=0) at a size where the wgrads overlap the following dgrad / attention
