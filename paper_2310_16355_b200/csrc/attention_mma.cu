@@ -1742,6 +1742,8 @@ __global__ void __launch_bounds__(512, 1)
       };
       if (lut_h == nullptr && !masked) {
         math(std::false_type{}, std::false_type{});
+      } else if (!masked) {  // T5: the relative-position bias on every block, the mask on few
+        math(std::true_type{}, std::false_type{});
       } else {
         math(std::true_type{}, std::true_type{});  // both guards are exact no-ops when off
       }
